@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the sliced fast kernel summation hot path (Alg. 1) on B200.
+
+Metric (BASELINE.json): slice-points/s = (N+M)*P / t and ms per kernel sum.  A "step" is one full
+kernel sum (all Sec. 8a rows: projection, sort/Fourier 1D engines, slice mean, and for N>1 GPUs the
+NCCL all-reduce of the M-length partial sums) over one batch of seeded synthetic inputs already
+resident in HBM.  Default workload: BASELINE.json configs[1] ("cfg2", negative distance, d=50,
+N=M=1e5, P=256).  Slices are partitioned over ranks ([rP/G, (r+1)P/G)), scaling is strong.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfgX] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on the launch stream,
+L2 flushed (256 MiB write) before every step outside the events; barrier + synchronize around the
+timed region; max over ranks.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2401_08260_b200 import inputs as I  # noqa: E402
+
+METRIC = "slice-points/s ((N+M)·P) and ms per kernel sum at 1/2/4/8 B200"
+UNIT = "slice-points/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(I.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+# ------------------------------------------------------------------ algorithmic bytes per launch
+def algorithmic_bytes(slot, cfg, np_local, plan):
+    """Compulsory HBM bytes of one launch of each kernel slot (inputs read once, outputs written once);
+    the per-unit figures and their derivation are in DESIGN.md "Roofline model"."""
+    N, M, d, P = cfg.N, cfg.M, cfg.d, np_local
+    L = N + M
+    n = plan.get("n_grid", 0) or 0
+    nb = plan.get("n_buckets", 0) or 0
+    if slot == "project":
+        return 4 * L * d + 4 * L * P + 4 * P * d
+    if slot == "bucket":
+        return 4 * N * P + 8 * N * P + 28 * (nb + 1) * P + 4 * N
+    if slot == "spread":
+        return 4 * N * P + 4 * N + 4 * n * P
+    if slot == "fft_filter":
+        return 4 * n * P + 4 * (n // 2 + 1) * P + 4 * n * P
+    if slot == "plan_D":
+        return 4 * (n // 2 + 1) * P
+    if slot == "eval":
+        b = 4 * M * P + 16 * M
+        if nb:
+            b += 8 * N * P + 28 * (nb + 1) * P
+        if n:
+            b += 4 * n * P
+        return b
+    return 0
+
+
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, dev_index):
+        self.dev = dev_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"sks_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = [r.split(", ") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        rows = [r for r in rows if len(r) == len(self.FIELDS)]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ oracle (CPU) timing
+def oracle_sample(cfg, param, x, y, w, target_seconds):
+    """time oracle (b) on a bounded sample of the workload; returns (slice-points/s extrapolated, cores, desc)."""
+    import oracle as O
+    kind_param = param if cfg.kind != "negdist" else 0.0
+    P = cfg.P
+    p_sub = P if cfg.N * cfg.d < 5e7 else max(1, P // 32)
+    m = 4
+    t = 0.0
+    while True:
+        tgt = I.target_subset(cfg.M, m, seed=777)
+        t0 = time.perf_counter()
+        O.sliced_sum(cfg.kind, kind_param, x, y, w, P, cfg.dir_seed, targets=tgt, p0=0, p1=p_sub, matern_p=cfg.matern_p)
+        t = time.perf_counter() - t0
+        if t >= target_seconds / 3 or m >= cfg.M:
+            break
+        m = min(cfg.M, max(m * 2, int(m * target_seconds / max(t, 1e-3) / 2)))
+    frac = (len(tgt) / cfg.M) * (p_sub / P)
+    value = (cfg.N + cfg.M) * P / (t / frac)
+    desc = (f"oracle (b) on {len(tgt)} of {cfg.M} targets x {p_sub} of {P} slices x all {cfg.N} sources "
+            f"({t:.2f} s); time extrapolated linearly in targets and slices")
+    return value, O.num_threads(), desc, t
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    O.build()
+    x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
+    param = I.kernel_param(cfg)
+    kind_param = param if cfg.kind != "negdist" else 0.0
+    P = cfg.P
+    p_sub = P if cfg.N * cfg.d < 5e7 else max(1, P // 32)
+    n_tgt = 8
+    tgt = I.target_subset(cfg.M, n_tgt, seed=778)
+    for _ in range(args.warmup):
+        O.sliced_sum(cfg.kind, kind_param, x, y, w, P, cfg.dir_seed, targets=tgt[:2], p0=0, p1=1)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.sliced_sum(cfg.kind, kind_param, x, y, w, P, cfg.dir_seed, targets=tgt, p0=0, p1=p_sub,
+                     matern_p=cfg.matern_p)
+        ts.append(time.perf_counter() - t0)
+    frac = (len(tgt) / cfg.M) * (p_sub / P)
+    t_full = statistics.mean(ts) / frac
+    value = (cfg.N + cfg.M) * P / t_full
+    sample = (f"oracle (b) on {len(tgt)} of {cfg.M} targets x {p_sub} of {P} slices x all {cfg.N} sources per step; "
+              f"time extrapolated linearly in targets and slices")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(cfg, param, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, param, G):
+    return {"workload": cfg.name, "kernel": cfg.kind, "kernel_param": param, "d": cfg.d, "N": cfg.N, "M": cfg.M,
+            "P": cfg.P, "slices_per_gpu": cfg.P // G, "parallelism": f"slices{G}",
+            "l2": "flushed before every step (256 MiB write, outside the timed events)"}
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    cfg = I.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_08260_b200 as S
+    from paper_2401_08260_b200 import build as B
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    G = world
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    if rank == 0:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    S._lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
+    param = I.kernel_param(cfg)
+    scale = param if cfg.kind != "negdist" else 1.0
+    p0, p1 = rank * cfg.P // G, (rank + 1) * cfg.P // G
+    xd, yd, wd = (torch.from_numpy(a).to(dev) for a in (x, y, w))
+    ws = torch.empty(S.sks_workspace_size(cfg.N, cfg.M, cfg.d, cfg.kind, scale, cfg.P, p0, p1, cfg.matern_p),
+                     dtype=torch.uint8, device=dev)
+    s = torch.empty(cfg.M, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        S.sks_sum(xd, yd, wd, cfg.kind, scale, cfg.P, cfg.dir_seed, p0, p1, cfg.matern_p, out=s, workspace=ws)
+        if G > 1:
+            dist.all_reduce(s)
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    plan = S.sks_last_plan()
+    S.sks_profile_enable(True)
+    S.sks_profile_read()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if G > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for a, b in evs:
+        flush.zero_()
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    prof = S.sks_profile_read()
+    S.sks_profile_enable(False)
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if G > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = (cfg.N + cfg.M) * cfg.P / (ms * 1e-3)
+
+    # ---- end to end through the public host-buffer API (H2D inputs + D2H result inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        xh, yh, wh = (torch.from_numpy(a).pin_memory() for a in (x, y, w))
+        sh = torch.empty(cfg.M, dtype=torch.float32).pin_memory()
+        wsh = torch.empty(S.sks_workspace_size_host(cfg.N, cfg.M, cfg.d, cfg.kind, scale, cfg.P, p0, p1, cfg.matern_p),
+                          dtype=torch.uint8, device=dev)
+        del ws
+        def e2e_step():
+            S.sks_sum_host(xh.numpy(), yh.numpy(), wh.numpy(), cfg.kind, scale, cfg.P, cfg.dir_seed, p0, p1,
+                           cfg.matern_p, out=sh.numpy(), workspace=wsh)
+            if G > 1:
+                sd = sh.to(dev, non_blocking=True)
+                dist.all_reduce(sd)
+                sh.copy_(sd)
+        for _ in range(2):
+            e2e_step()
+        ke = max(3, min(args.steps, 10))
+        evs2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ke)]
+        if G > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for a, b in evs2:
+            flush.zero_()
+            a.record(stream)
+            e2e_step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        me = sum(a.elapsed_time(b) for a, b in evs2) / ke
+        te = torch.tensor([me], dtype=torch.float64, device=dev)
+        if G > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        me = float(te.item())
+        e2e = {"value": (cfg.N + cfg.M) * cfg.P / (me * 1e-3), "unit": UNIT, "ms_per_step": me,
+               "h2d_bytes_per_step": 4 * (cfg.N * cfg.d + cfg.M * cfg.d + cfg.N),
+               "d2h_bytes_per_step": 4 * cfg.M, "api": "sks_sum_host (pinned host buffers)"}
+
+    if rank != 0:
+        if G > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (live CUDA-event durations over the timed region)
+    pk = peaks()
+    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps} for k, v in prof.items()
+               if v[1] > 0}
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    n_launch = prof[dom][1]
+    per_launch_ms = prof[dom][0] / max(1, n_launch)
+    np_local = p1 - p0
+    alg = algorithmic_bytes(dom, cfg, np_local if plan.get("slice_batch", 0) in (0, np_local) else plan["slice_batch"],
+                            plan)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    if dom == "project":
+        flops = 2.0 * (cfg.N + cfg.M) * cfg.d * np_local
+        fp32_peak = 148 * 128 * 2 * (pk.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
+        roof = {"kernel": dom, "bound": "alu", "achieved": flops / (per_launch_ms * 1e-3) / 1e12,
+                "peak": fp32_peak, "unit": "TFLOP/s",
+                "peak_source": "148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (MEASURED_PEAKS.json)",
+                "traffic": traffic}
+    else:
+        roof = {"kernel": dom, "bound": "hbm", "achieved": alg / (per_launch_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else ""),
+                "algorithmic_bytes_per_launch": alg, "traffic": traffic}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["share_of_step"] = kernels[dom]["ms_per_step"] / ms
+
+    cpu = None
+    if not args.no_cpu_baseline and G == 1:
+        v, cores, desc, _ = oracle_sample(cfg, param, x, y, w, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config_dict(cfg, param, G), "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": int(sum(v[1] for v in prof.values())), "clocks": clk,
+            "kernels": kernels, "plan": plan}
+    print(json.dumps(line), flush=True)
+    if G > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

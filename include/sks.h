@@ -1,0 +1,163 @@
+/*
+ * sks.h -- sliced fast kernel summation on B200 (sm_100a), C ABI.
+ *
+ * Computes, for radial kernels K(x,y) = F(||x-y||), the kernel sums
+ *     s_m = sum_{n=1}^{N} w_n F(||x_n - y_m||),  m = 1..M
+ * by the paper's slicing method (Alg. 1):
+ *     s_m ~= (1/P) sum_{p=1}^{P} t_{m,p},   t_{m,p} = sum_n w_n f(|<xi_p,x_n> - <xi_p,y_m>|)
+ * with f the 1D counterpart of F (Table 1; App. C), xi_p iid uniform
+ * directions on S^{d-1} drawn from `seed` (R1), and each 1D sum evaluated by
+ *   - NEGDIST:   the exact sorting algorithm of Sec. 3.2 (Alg. 2), realised as a
+ *                one-pass MSD (counting) sort + fp64 prefix sums;
+ *   - GAUSSIAN / MATERN: fast Fourier summation on the torus (Sec. 3.1) with the
+ *                NFFT (Remark P:519-525): spread -> FFT -> x D_k -> iFFT -> interpolate;
+ *   - LAPLACIAN: the decomposition of Sec. 3.3: sorting part + Fourier part.
+ *
+ * Every compute step runs in this library's CUDA kernels (sm_100a).  There is no CPU fallback:
+ * without a usable CUDA device every compute entry point returns SKS_ERR_CUDA.
+ *
+ * Conventions for all entry points
+ *   - Point sets are row-major fp32: x is N x d (x[n*d + j]), y is M x d.  w is N fp32.
+ *   - "DEVICE" pointers must be CUDA device (or managed) memory owned by the caller; the library
+ *     never frees or retains them.  "HOST" pointers are ordinary host memory (pinned memory is
+ *     faster for the _host variant).
+ *   - The library allocates no memory on the hot path.  It keeps a small immutable per-process cache
+ *     of device copies of the directions, keyed by (seed, P, d, p_begin, p_end), created on first use.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All work is enqueued
+ *     on `stream`; the call returns after the stream has executed it (v0 synchronises twice: the Fourier
+ *     planner reads back the per-slice projection ranges once per slice batch, and every call reads back
+ *     the non-finite flag at its end so that SKS_ERR_NONFINITE is reported by the call itself).
+ *   - Return value: SKS_OK or an error status; sks_last_error() then returns a thread-local message.
+ *     On error the contents of output buffers are unspecified.
+ *   - Thread safety: calls on different streams / threads may run concurrently; the direction cache
+ *     is internally locked.
+ */
+#ifndef SKS_H_
+#define SKS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SKS_OK = 0,
+  SKS_ERR_INVALID = 1,      /* bad argument: sizes <= 0, NULL pointer, scale <= 0, bad slice range      */
+  SKS_ERR_UNSUPPORTED = 2,  /* kernel kind not in sks_kind, Matern p outside [0, 8], or a plan that
+                               exceeds the built limits (grid n > 16384)                                 */
+  SKS_ERR_CUDA = 3,         /* CUDA runtime error (incl. no device / missing sm_100a support)            */
+  SKS_ERR_WORKSPACE = 4,    /* workspace NULL or smaller than sks_workspace_size()                       */
+  SKS_ERR_NONFINITE = 5     /* a projection was NaN/Inf (checked by the planner / at the end of the call) */
+} sks_status;
+
+typedef enum {
+  SKS_GAUSSIAN = 0,   /* F(r) = exp(-r^2/(2 scale^2))                  Table 1                */
+  SKS_NEGDIST = 1,    /* F(r) = -r                      (scale unused) Table 1                */
+  SKS_LAPLACIAN = 2,  /* F(r) = exp(-r/scale): scale is a LENGTH, the paper's rate alpha = 1/scale
+                         (R8)                                                    */
+  SKS_MATERN = 3      /* Matern nu = matern_p + 1/2, length beta = scale (closed form P:1163)  */
+} sks_kind;
+
+typedef struct {
+  int32_t kind;       /* sks_kind                                                   */
+  int32_t matern_p;   /* SKS_MATERN only: nu = matern_p + 1/2, 0 <= matern_p <= 8   */
+  double scale;       /* sigma | unused | ell | beta  (must be > 0 unless NEGDIST)  */
+} sks_kernel;
+
+/* Optional tuning knobs.  Pass NULL for the defaults (given in brackets). */
+typedef struct {
+  double eps;            /* [1e-6] absolute tail mass (f(0)-relative) of dropped Fourier coefficients and aliasing level
+                            of the torus scaling (readings R3/R5 of P:339-349)             */
+  int32_t window_w;      /* [6]  NFFT window width in grid cells (taps per point), 2..12              */
+  int32_t oversample;    /* [2]  NFFT oversampling factor n >= oversample * 2 * (k_max + 1)           */
+  int32_t slice_batch;   /* [0 = auto] slices processed per batch (memory bound, Remark P:973-979)   */
+  int32_t reserved;      /* must be 0                                                                 */
+} sks_options;
+
+/* Diagnostic description of the last plan built on this thread (for reports and tests). */
+typedef struct {
+  int32_t path;          /* 0 = Fourier only, 1 = sort only, 2 = sort + Fourier                        */
+  int32_t n_grid;        /* NFFT grid length n (power of two), 0 if no Fourier part                     */
+  int32_t k_max;         /* largest |k| kept over the slices                                            */
+  int32_t band_lo_min;   /* smallest lower band edge over the slices (Gaussian bands exclude 0..lo-1)   */
+  int32_t window_w;      /* taps per point                                                              */
+  int32_t spread_cells;  /* widest per-slice grid footprint W (cells)                                   */
+  int32_t n_buckets;     /* buckets of the counting sort (sort part), 0 if none                         */
+  int32_t slice_batch;   /* slices per batch                                                            */
+  int32_t n_batches;     /* batches in the call                                                         */
+  int32_t launches;      /* CUDA kernels launched by the call                                           */
+  double tau_min, tau_max;   /* torus scaling range over slices                                         */
+} sks_plan_info;
+
+/* Bytes of DEVICE workspace sks_sum needs for this problem (slice range [p_begin, p_end) of P).
+ * Returns SKS_OK and writes *bytes, or an error for invalid arguments. */
+sks_status sks_workspace_size(int64_t N, int64_t M, int32_t d, sks_kernel kernel, int32_t P,
+                              int32_t p_begin, int32_t p_end, const sks_options* opt, size_t* bytes);
+
+/* The hot path (Alg. 1) over slices p in [p_begin, p_end) of a P-direction estimate.
+ *   x: DEVICE N x d fp32;  y: DEVICE M x d fp32;  w: DEVICE N fp32;
+ *   s: DEVICE M fp32 out:  s_m = (1/P) sum_{p in [p_begin,p_end)} t_{m,p}.
+ * With p_begin = 0, p_end = P this is the full estimate; partial ranges on several GPUs add up
+ * (one all-reduce SUM of s) to the same estimate, because direction p depends only on (seed, p).
+ * workspace: DEVICE, >= sks_workspace_size() bytes, 256-byte aligned. */
+sks_status sks_sum(const float* x, int64_t N, const float* y, int64_t M, int32_t d, const float* w,
+                   sks_kernel kernel, int32_t P, uint64_t seed, int32_t p_begin, int32_t p_end, float* s,
+                   void* workspace, size_t workspace_bytes, const sks_options* opt, void* stream);
+
+/* Same computation from HOST buffers x, y, w (copied in) to HOST s (copied out); blocks until s is
+ * written.  workspace: DEVICE, >= sks_workspace_size_host() bytes. */
+sks_status sks_workspace_size_host(int64_t N, int64_t M, int32_t d, sks_kernel kernel, int32_t P,
+                                   int32_t p_begin, int32_t p_end, const sks_options* opt, size_t* bytes);
+sks_status sks_sum_host(const float* x, int64_t N, const float* y, int64_t M, int32_t d, const float* w,
+                        sks_kernel kernel, int32_t P, uint64_t seed, int32_t p_begin, int32_t p_end, float* s,
+                        void* workspace, size_t workspace_bytes, const sks_options* opt, void* stream);
+
+/* Directions of DESIGN.md R1 (host only, no GPU needed): for p in [p_begin, p_end),
+ *   g_out[(p-p_begin)*d + j] = g_p[j]  (HOST, unnormalised N(0,1) draw rounded to bf16, exact in fp32)
+ *   inv_norm_out[p-p_begin]   = 1/||g_p|| in fp64 (HOST);  xi_p = g_p * inv_norm_p. */
+sks_status sks_directions(int32_t P, int32_t d, uint64_t seed, int32_t p_begin, int32_t p_end, float* g_out,
+                          double* inv_norm_out);
+
+/* Row a1 alone: z[(p-p_begin)*n + i] = <xi_p, pts_i>, pts DEVICE n x d fp32, z DEVICE fp32. */
+sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64_t seed, int32_t p_begin,
+                       int32_t p_end, float* z, void* stream);
+
+/* Rows a2-a7 alone: per-slice 1D sums t[q*M + m] = sum_n w_n f(|zx[q*N+n] - zy[q*M+m]|) for q < n_slices
+ * on given DEVICE projections zx (n_slices x N), zy (n_slices x M), DEVICE w (N); t DEVICE fp32 out.
+ * f is the 1D counterpart of `kernel` in dimension d.  workspace: >= sks_workspace_size_1d(). */
+sks_status sks_workspace_size_1d(int64_t N, int64_t M, int32_t d, sks_kernel kernel, int32_t n_slices,
+                                 const sks_options* opt, size_t* bytes);
+sks_status sks_sum_1d(const float* zx, const float* zy, const float* w, int64_t N, int64_t M, int32_t n_slices,
+                      int32_t d, sks_kernel kernel, float* t, void* workspace, size_t workspace_bytes,
+                      const sks_options* opt, void* stream);
+
+/* Torus Fourier coefficients used by the planner (host only): out[k-k0] = c_k for k in [k0, k1] of the
+ * periodised 1D counterpart on the torus of period 1/tau (Lemma 2.5 P:304-338 for GAUSSIAN; DESIGN.md
+ * R7 / R7b closed forms for LAPLACIAN (smooth part of the Sec. 3.3 decomposition) and MATERN). */
+sks_status sks_fourier_coeffs(sks_kernel kernel, int32_t d, double tau, int32_t k0, int32_t k1, double* out);
+
+/* Plan of the last sks_sum / sks_sum_1d call on this thread. */
+sks_status sks_last_plan(sks_plan_info* info);
+
+/* Opt-in measurement support (bench.py): while enabled, every kernel launch of sks_sum / sks_sum_1d is
+ * bracketed by CUDA events recorded on the launch stream (negligible overhead, no synchronisation). */
+sks_status sks_profile_enable(int32_t enable);
+/* Accumulated device time (ms) and launch count per kernel slot since the last read; waits for the
+ * recorded events, then resets.  n_slots >= SKS_PROFILE_SLOTS; slot names: sks_profile_names(). */
+#define SKS_PROFILE_SLOTS 8
+sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots);
+/* Comma-separated slot names: "project,minmax,bucket,plan_D,spread,fft_filter,eval,aux". */
+const char* sks_profile_names(void);
+
+/* Thread-local message for the last non-OK status ("" if none). */
+const char* sks_last_error(void);
+
+/* Library version string. */
+const char* sks_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKS_H_ */

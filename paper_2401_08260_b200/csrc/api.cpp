@@ -1,0 +1,620 @@
+// api.cpp -- the C ABI of libsks (include/sks.h): validation, workspace carving, direction cache,
+// slice batching and the per-batch kernel sequence of Alg. 1.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/sks.h"
+#include "host.h"
+#include "kernels.h"
+
+namespace {
+
+// ---- opt-in kernel timing (sks_profile_*): event pairs per slot, resolved on read
+enum Slot { PS_PROJECT = 0, PS_MINMAX, PS_BUCKET, PS_PLAN, PS_SPREAD, PS_FFT, PS_EVAL, PS_AUX, PS_N };
+struct Prof {
+  std::mutex mu;
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;
+  double ms[PS_N] = {};
+  int64_t cnt[PS_N] = {};
+} g_prof;
+
+cudaEvent_t prof_event() {
+  if (!g_prof.pool.empty()) {
+    cudaEvent_t e = g_prof.pool.back();
+    g_prof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {   // brackets one launch with events on its stream when profiling is on
+  int slot;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(int s, cudaStream_t stream) : slot(s), st(stream) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (!g_prof.on) return;
+    a = prof_event();
+    cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, st);
+    g_prof.pending.emplace_back(slot, a, b);
+  }
+};
+#define PROF(slot) ProfScope prof_scope_##__LINE__(slot, st)
+
+thread_local std::string g_err;
+thread_local sks_plan_info g_plan{};
+
+sks_status fail(sks_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define SKS_CUDA(call)                                                                                  \
+  do {                                                                                                  \
+    cudaError_t e_ = (call);                                                                            \
+    if (e_ != cudaSuccess) return fail(SKS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct Opts {
+  double eps = 1e-6;
+  int w = 6;
+  int os = 2;
+  int batch = 0;
+};
+
+sks_status resolve_opts(const sks_options* o, Opts* r) {
+  Opts d;
+  if (o) {
+    if (o->eps > 0) d.eps = o->eps;
+    if (o->window_w) d.w = o->window_w;
+    if (o->oversample) d.os = o->oversample;
+    d.batch = o->slice_batch;
+    if (d.w < 2 || d.w > 12) return fail(SKS_ERR_INVALID, "window_w must be in [2, 12]");
+    if (d.os < 2 || d.os > 16) return fail(SKS_ERR_INVALID, "oversample must be in [2, 16]");
+    if (d.batch < 0) return fail(SKS_ERR_INVALID, "slice_batch must be >= 0");
+    if (o->reserved != 0) return fail(SKS_ERR_INVALID, "reserved option field must be 0");
+  }
+  *r = d;
+  return SKS_OK;
+}
+
+sks_status check_kernel(const sks_kernel& k) {
+  if (k.kind < 0 || k.kind > 3) return fail(SKS_ERR_UNSUPPORTED, "unsupported kernel kind " + std::to_string(k.kind));
+  if (k.kind != SKS_NEGDIST && !(k.scale > 0.0 && std::isfinite(k.scale)))
+    return fail(SKS_ERR_INVALID, "kernel scale must be finite and > 0");
+  if (k.kind == SKS_MATERN && (k.matern_p < 0 || k.matern_p > 8))
+    return fail(SKS_ERR_UNSUPPORTED, "Matern p must be in [0, 8]");
+  return SKS_OK;
+}
+
+struct Path {
+  bool sort, fourier, moment;
+};
+Path path_of(int kind) {
+  return Path{kind == SKS_NEGDIST || kind == SKS_LAPLACIAN, kind != SKS_NEGDIST, kind == SKS_LAPLACIAN};
+}
+
+int buckets_for(int64_t N) {
+  int64_t nb = 1024;
+  while (nb < N / 4 && nb < 16384) nb <<= 1;
+  return static_cast<int>(nb);
+}
+
+constexpr int kNmax = 16384;   // largest NFFT grid the kernels are built for
+constexpr size_t kAlign = 256;
+inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
+
+// workspace layout of one slice batch (offsets in bytes)
+struct Layout {
+  size_t Z = 0, mm = 0, xs = 0, off = 0, tab = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
+         flag = 0, total = 0;
+};
+
+Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb) {
+  Layout L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += al(bytes);
+    return at;
+  };
+  L.flag = take(16);
+  L.s64 = take(sizeof(double) * M);
+  L.mm = take(sizeof(unsigned) * 4 * nbat);
+  if (with_Z) L.Z = take(sizeof(float) * (N + M) * nbat);
+  if (pt.sort || pt.moment) {
+    L.xs = take(sizeof(float2) * N * nbat);
+    L.off = take(sizeof(int) * (nb + 1) * static_cast<size_t>(nbat));
+    L.tab = take(sizeof(double) * 3 * (nb + 1) * static_cast<size_t>(nbat));
+    L.bpar = take(sizeof(float) * 2 * nbat);
+  }
+  if (pt.fourier) {
+    L.grid = take(sizeof(float) * kNmax * static_cast<size_t>(nbat));
+    L.h = take(sizeof(float) * kNmax * static_cast<size_t>(nbat));
+    L.D = take(sizeof(float) * (kNmax / 2 + 1) * static_cast<size_t>(nbat));
+    L.fpar = take(sizeof(sks::FPar) * nbat);
+    L.phi = take(sizeof(float) * (kNmax / 2 + 1));
+  }
+  L.total = o;
+  return L;
+}
+
+int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int nb, int req) {
+  if (req > 0) return std::min(req, np);
+  // auto: all local slices unless the batch working set would exceed 64 GiB of HBM
+  const size_t budget = size_t(64) << 30;
+  int b = np;
+  while (b > 1 && make_layout(N, M, pt, b, with_Z, nb).total > budget) b = (b + 1) / 2;
+  return b;
+}
+
+// ---- direction cache (device copies; immutable once created)
+struct DirEntry {
+  float* g = nullptr;      // np x d
+  float* inv = nullptr;    // np
+};
+std::mutex g_dir_mu;
+std::map<std::tuple<int, uint64_t, int, int, int, int>, DirEntry> g_dirs;
+
+sks_status get_dirs(int P, int d, uint64_t seed, int p0, int p1, DirEntry* out) {
+  int dev = 0;
+  SKS_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(dev, seed, P, d, p0, p1);
+  std::lock_guard<std::mutex> lk(g_dir_mu);
+  auto it = g_dirs.find(key);
+  if (it != g_dirs.end()) {
+    *out = it->second;
+    return SKS_OK;
+  }
+  const int np = p1 - p0;
+  std::vector<float> g(static_cast<size_t>(np) * d);
+  std::vector<double> inv(np);
+  sks::make_directions(P, d, seed, p0, p1, g.data(), inv.data());
+  std::vector<float> invf(np);
+  for (int i = 0; i < np; ++i) invf[i] = static_cast<float>(inv[i]);
+  DirEntry e;
+  SKS_CUDA(cudaMalloc(&e.g, sizeof(float) * g.size()));
+  SKS_CUDA(cudaMalloc(&e.inv, sizeof(float) * np));
+  SKS_CUDA(cudaMemcpy(e.g, g.data(), sizeof(float) * g.size(), cudaMemcpyHostToDevice));
+  SKS_CUDA(cudaMemcpy(e.inv, invf.data(), sizeof(float) * np, cudaMemcpyHostToDevice));
+  g_dirs[key] = e;
+  *out = e;
+  return SKS_OK;
+}
+
+// ---- pinned host staging (per thread, grows)
+struct Staging {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~Staging() {
+    if (p) cudaFreeHost(p);
+  }
+};
+thread_local Staging g_stage;
+
+sks_status stage(size_t bytes, void** out) {
+  if (g_stage.cap < bytes) {
+    if (g_stage.p) cudaFreeHost(g_stage.p);
+    g_stage.p = nullptr;
+    g_stage.cap = 0;
+    SKS_CUDA(cudaHostAlloc(&g_stage.p, bytes, cudaHostAllocDefault));
+    g_stage.cap = bytes;
+  }
+  *out = g_stage.p;
+  return SKS_OK;
+}
+
+sks::CoeffConst coeff_const(const sks_kernel& k, int d) {
+  sks::CoeffConst c{};
+  c.kind = k.kind;
+  c.d = d;
+  c.scale = k.scale;
+  const double PI = 3.14159265358979323846;
+  if (k.kind == SKS_GAUSSIAN) c.logpref = std::log(d * PI / std::sqrt(2.0)) - std::lgamma(0.5 * d + 1.0);
+  if (k.kind == SKS_LAPLACIAN) {
+    c.logpref = std::log(2.0 * sks::cd(d));
+    c.lap_A = sks::cd(d) / k.scale;
+  }
+  if (k.kind == SKS_MATERN) {
+    const double nu = k.matern_p + 0.5;
+    c.nu = nu;
+    c.logpref = 0.5 * d * std::log(PI) - std::lgamma(0.5 * d) + d * std::log(2.0) + 0.5 * d * std::log(PI) +
+                std::lgamma(nu + 0.5 * d) + nu * std::log(2.0 * nu) - std::lgamma(nu);
+  }
+  return c;
+}
+
+// Fourier part of one batch: planner (one readback of the ranges), device D_k, spread, FFT filter.
+sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView zv, const float* w, int nbat,
+                         char* ws, const Layout& L, cudaStream_t st, sks::FourierPlan* plan, int* launches) {
+  void* hbuf = nullptr;
+  sks_status s = stage(sizeof(unsigned) * 4 * nbat + 16 + sizeof(sks::FPar) * nbat + sizeof(float) * (kNmax / 2 + 1), &hbuf);
+  if (s != SKS_OK) return s;
+  unsigned* hmm = static_cast<unsigned*>(hbuf);
+  int* hflag = reinterpret_cast<int*>(hmm + 4 * nbat);
+  SKS_CUDA(cudaMemcpyAsync(hmm, ws + L.mm, sizeof(unsigned) * 4 * nbat, cudaMemcpyDeviceToHost, st));
+  SKS_CUDA(cudaMemcpyAsync(hflag, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SKS_CUDA(cudaStreamSynchronize(st));
+  if (*hflag) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
+  std::vector<float> r(4 * nbat);
+  sks::decode_minmax(hmm, r.data(), 4 * nbat);
+  std::vector<float> xmn(nbat), xmx(nbat), amn(nbat), amx(nbat);
+  for (int p = 0; p < nbat; ++p) {
+    xmn[p] = r[4 * p];
+    xmx[p] = r[4 * p + 1];
+    amn[p] = r[4 * p + 2];
+    amx[p] = r[4 * p + 3];
+    if (zv.N == 0) { xmn[p] = amn[p]; xmx[p] = amx[p]; }
+  }
+  sks::KernelModel km{k.kind, k.matern_p, k.scale, d};
+  std::string err;
+  if (!sks::build_fourier_plan(km, o.eps, o.w, o.os, nbat, xmn.data(), xmx.data(), amn.data(), amx.data(), *plan, &err))
+    return fail(err.rfind("non-finite", 0) == 0 ? SKS_ERR_NONFINITE : SKS_ERR_UNSUPPORTED, err);
+  const int n = plan->n;
+  sks::FPar* hfp = reinterpret_cast<sks::FPar*>(hflag + 4);
+  for (int p = 0; p < nbat; ++p) {
+    const sks::SlicePlan& sp = plan->slices[p];
+    hfp[p] = sks::FPar{sp.tau, sp.cen, sp.lmin, (sp.klo << 16) | sp.khi};
+  }
+  float* hphi = reinterpret_cast<float*>(hfp + nbat);
+  for (int kk = 0; kk <= n / 2; ++kk) hphi[kk] = plan->phi2inv[kk];
+  SKS_CUDA(cudaMemcpyAsync(ws + L.fpar, hfp, sizeof(sks::FPar) * nbat, cudaMemcpyHostToDevice, st));
+  SKS_CUDA(cudaMemcpyAsync(ws + L.phi, hphi, sizeof(float) * (n / 2 + 1), cudaMemcpyHostToDevice, st));
+  const sks::FPar* dfp = reinterpret_cast<const sks::FPar*>(ws + L.fpar);
+  {
+    ProfScope ps(PS_PLAN, st);
+    SKS_CUDA(sks::launch_plan_D(dfp, nbat, coeff_const(k, d), reinterpret_cast<const float*>(ws + L.phi), n,
+                                reinterpret_cast<float*>(ws + L.D), st));
+  }
+  {
+    ProfScope ps(PS_AUX, st);
+    SKS_CUDA(sks::launch_zero(ws + L.grid, al(sizeof(float) * static_cast<size_t>(n) * nbat), st));
+  }
+  {
+    ProfScope ps(PS_SPREAD, st);
+    SKS_CUDA(sks::launch_spread(zv, w, nbat, dfp, n, o.w, plan->beta, plan->W, reinterpret_cast<float*>(ws + L.grid), st));
+  }
+  {
+    ProfScope ps(PS_FFT, st);
+    SKS_CUDA(sks::launch_fft_filter(reinterpret_cast<const float*>(ws + L.grid), reinterpret_cast<const float*>(ws + L.D),
+                                    nbat, n, reinterpret_cast<float*>(ws + L.h), st));
+  }
+  *launches += 4;
+  return SKS_OK;
+}
+
+sks_status validate_common(int64_t N, int64_t M, int32_t d, const sks_kernel& k, int32_t P, int32_t p0, int32_t p1) {
+  if (N <= 0 || M <= 0 || d <= 0) return fail(SKS_ERR_INVALID, "N, M and d must be > 0");
+  if (N > (int64_t(1) << 31) - 1 || M > (int64_t(1) << 40)) return fail(SKS_ERR_INVALID, "N must be < 2^31");
+  if (P <= 0 || p0 < 0 || p1 > P || p0 >= p1) return fail(SKS_ERR_INVALID, "slice range must satisfy 0 <= p_begin < p_end <= P");
+  return check_kernel(k);
+}
+
+// the batched pipeline shared by sks_sum and sks_sum_1d
+struct Problem {
+  int64_t N, M;
+  int d;
+  sks_kernel k;
+  int nslices;
+  bool with_Z;
+};
+
+sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const float* y, const float* w,
+                       const DirEntry* dirs, const float* zx_in, const float* zy_in, float* s_out, float* t_out,
+                       double inv_P, void* workspace, size_t ws_bytes, cudaStream_t st) {
+  const Path pt = path_of(pr.k.kind);
+  const int nb = (pt.sort || pt.moment) ? buckets_for(pr.N) : 0;
+  const int batch = choose_batch(pr.N, pr.M, pt, pr.nslices, pr.with_Z, nb, o.batch);
+  const Layout L = make_layout(pr.N, pr.M, pt, batch, pr.with_Z, nb);
+  if (!workspace || ws_bytes < L.total)
+    return fail(SKS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(SKS_ERR_INVALID, "workspace must be 256-byte aligned");
+  char* ws = static_cast<char*>(workspace);
+  const double cdd = sks::cd(pr.d);
+  int launches = 0, nbatches = 0;
+  sks::FourierPlan plan;
+  sks_plan_info info{};
+  info.tau_min = 1e300;
+  {
+    ProfScope ps(PS_AUX, st);
+    SKS_CUDA(sks::launch_zero(ws + L.flag, al(16), st));
+  }
+  if (s_out) {
+    ProfScope ps(PS_AUX, st);
+    SKS_CUDA(sks::launch_zero(ws + L.s64, al(sizeof(double) * pr.M), st));
+  }
+  launches += s_out ? 2 : 1;
+  for (int b0 = 0; b0 < pr.nslices; b0 += batch) {
+    const int nbat = std::min(batch, pr.nslices - b0);
+    ++nbatches;
+    unsigned* mm = reinterpret_cast<unsigned*>(ws + L.mm);
+    int* flag = reinterpret_cast<int*>(ws + L.flag);
+    {
+      ProfScope ps(PS_AUX, st);
+      SKS_CUDA(sks::launch_init_minmax(mm, nbat, st));
+    }
+    sks::ZView zv;
+    if (pr.with_Z) {
+      float* Z = reinterpret_cast<float*>(ws + L.Z);
+      const int64_t ldz = pr.N + pr.M;
+      ProfScope ps(PS_PROJECT, st);
+      SKS_CUDA(sks::launch_project(x, pr.N, y, pr.M, pr.d, dirs->g + static_cast<int64_t>(b0) * pr.d, dirs->inv + b0,
+                                   nbat, Z, ldz, mm, flag, st));
+      zv = sks::ZView{Z, Z + pr.N, ldz, ldz, pr.N, pr.M};
+    } else {
+      zv = sks::ZView{zx_in + static_cast<int64_t>(b0) * pr.N, zy_in + static_cast<int64_t>(b0) * pr.M, pr.N, pr.M,
+                      pr.N, pr.M};
+      ProfScope ps(PS_MINMAX, st);
+      SKS_CUDA(sks::launch_minmax(zv, nbat, mm, flag, st));
+    }
+    launches += 2;
+    sks::EvalArgs ea{};
+    ea.zv = zv;
+    ea.np = nbat;
+    if (pt.sort || pt.moment) {
+      ProfScope ps(PS_BUCKET, st);
+      SKS_CUDA(sks::launch_bucket_build(zv, w, nbat, nb, mm, reinterpret_cast<float2*>(ws + L.xs),
+                                        reinterpret_cast<int*>(ws + L.off), reinterpret_cast<double*>(ws + L.tab),
+                                        reinterpret_cast<float*>(ws + L.bpar), st));
+      ++launches;
+      ea.nb = nb;
+      ea.xs = reinterpret_cast<const float2*>(ws + L.xs);
+      ea.off = reinterpret_cast<const int*>(ws + L.off);
+      ea.tab = reinterpret_cast<const double*>(ws + L.tab);
+      ea.bpar = reinterpret_cast<const float*>(ws + L.bpar);
+    }
+    if (pt.sort) {
+      ea.sort = true;
+      // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)
+      ea.sort_coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
+    }
+    if (pt.fourier) {
+      sks_status s = fourier_batch(pr.k, pr.d, o, zv, w, nbat, ws, L, st, &plan, &launches);
+      if (s != SKS_OK) return s;
+      ea.fourier = true;
+      ea.fp = reinterpret_cast<const sks::FPar*>(ws + L.fpar);
+      ea.h = reinterpret_cast<const float*>(ws + L.h);
+      ea.n = plan.n;
+      ea.wt = o.w;
+      ea.beta = plan.beta;
+      info.n_grid = plan.n;
+      info.k_max = std::max(info.k_max, plan.k_max);
+      info.band_lo_min = plan.band_lo_min;
+      info.spread_cells = std::max(info.spread_cells, plan.W);
+      info.tau_min = std::min(info.tau_min, plan.tau_min);
+      info.tau_max = std::max(info.tau_max, plan.tau_max);
+    }
+    if (pt.moment) {
+      ea.moment = true;
+      ea.mom_coef = cdd / pr.k.scale;   // + alpha c_d tau sum_n w_n (z_n - z_m)^2   (R7)
+    }
+    ea.s64 = s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr;
+    ea.per_slice_out = t_out ? t_out + static_cast<int64_t>(b0) * pr.M : nullptr;
+    {
+      ProfScope ps(PS_EVAL, st);
+      SKS_CUDA(sks::launch_eval(ea, st));
+    }
+    ++launches;
+  }
+  if (s_out) {
+    ProfScope ps(PS_AUX, st);
+    SKS_CUDA(sks::launch_finalize(reinterpret_cast<const double*>(ws + L.s64), pr.M, inv_P, s_out, st));
+    ++launches;
+  }
+  // fail loudly on non-finite projections (one readback at the end of the call)
+  {
+    void* hb = nullptr;
+    sks_status s = stage(16, &hb);
+    if (s != SKS_OK) return s;
+    SKS_CUDA(cudaMemcpyAsync(hb, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SKS_CUDA(cudaStreamSynchronize(st));
+    if (*static_cast<int*>(hb)) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
+  }
+  info.path = pt.fourier ? (pt.sort ? 2 : 0) : 1;
+  info.window_w = pt.fourier ? o.w : 0;
+  info.n_buckets = nb;
+  info.slice_batch = batch;
+  info.n_batches = nbatches;
+  info.launches = launches;
+  if (!pt.fourier) info.tau_min = 0;
+  g_plan = info;
+  return SKS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sks_version(void) { return "sks 0.1 (sm_100a)"; }
+
+const char* sks_last_error(void) { return g_err.c_str(); }
+
+sks_status sks_profile_enable(int32_t enable) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = enable != 0;
+  return SKS_OK;
+}
+
+sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots) {
+  if (!ms || !launches || n_slots < PS_N) return fail(SKS_ERR_INVALID, "need SKS_PROFILE_SLOTS slots");
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  for (auto& t : g_prof.pending) {
+    const int slot = std::get<0>(t);
+    cudaEvent_t a = std::get<1>(t), b = std::get<2>(t);
+    float e = 0.f;
+    SKS_CUDA(cudaEventSynchronize(b));
+    SKS_CUDA(cudaEventElapsedTime(&e, a, b));
+    g_prof.ms[slot] += e;
+    g_prof.cnt[slot] += 1;
+    g_prof.pool.push_back(a);
+    g_prof.pool.push_back(b);
+  }
+  g_prof.pending.clear();
+  for (int i = 0; i < PS_N; ++i) {
+    ms[i] = g_prof.ms[i];
+    launches[i] = g_prof.cnt[i];
+    g_prof.ms[i] = 0.0;
+    g_prof.cnt[i] = 0;
+  }
+  return SKS_OK;
+}
+
+const char* sks_profile_names(void) { return "project,minmax,bucket,plan_D,spread,fft_filter,eval,aux"; }
+
+sks_status sks_last_plan(sks_plan_info* info) {
+  if (!info) return fail(SKS_ERR_INVALID, "info is NULL");
+  *info = g_plan;
+  return SKS_OK;
+}
+
+sks_status sks_directions(int32_t P, int32_t d, uint64_t seed, int32_t p_begin, int32_t p_end, float* g_out,
+                          double* inv_norm_out) {
+  if (P <= 0 || d <= 0 || p_begin < 0 || p_end > P || p_begin >= p_end) return fail(SKS_ERR_INVALID, "bad P/d/range");
+  if (!g_out || !inv_norm_out) return fail(SKS_ERR_INVALID, "NULL output");
+  sks::make_directions(P, d, seed, p_begin, p_end, g_out, inv_norm_out);
+  return SKS_OK;
+}
+
+sks_status sks_fourier_coeffs(sks_kernel kernel, int32_t d, double tau, int32_t k0, int32_t k1, double* out) {
+  sks_status s = check_kernel(kernel);
+  if (s != SKS_OK) return s;
+  if (kernel.kind == SKS_NEGDIST) return fail(SKS_ERR_UNSUPPORTED, "negdist has no Fourier path (Remark P:527-533)");
+  if (d <= 0 || !(tau > 0) || k1 < k0 || !out) return fail(SKS_ERR_INVALID, "bad d/tau/range/out");
+  sks::KernelModel km{kernel.kind, kernel.matern_p, kernel.scale, d};
+  for (int32_t k = k0; k <= k1; ++k) out[k - k0] = sks::torus_coeff(km, tau, k < 0 ? -int64_t(k) : int64_t(k));
+  return SKS_OK;
+}
+
+sks_status sks_workspace_size(int64_t N, int64_t M, int32_t d, sks_kernel kernel, int32_t P, int32_t p_begin,
+                              int32_t p_end, const sks_options* opt, size_t* bytes) {
+  sks_status s = validate_common(N, M, d, kernel, P, p_begin, p_end);
+  if (s != SKS_OK) return s;
+  Opts o;
+  if ((s = resolve_opts(opt, &o)) != SKS_OK) return s;
+  if (!bytes) return fail(SKS_ERR_INVALID, "bytes is NULL");
+  const Path pt = path_of(kernel.kind);
+  const int nb = (pt.sort || pt.moment) ? buckets_for(N) : 0;
+  const int batch = choose_batch(N, M, pt, p_end - p_begin, true, nb, o.batch);
+  *bytes = make_layout(N, M, pt, batch, true, nb).total;
+  return SKS_OK;
+}
+
+sks_status sks_sum(const float* x, int64_t N, const float* y, int64_t M, int32_t d, const float* w, sks_kernel kernel,
+                   int32_t P, uint64_t seed, int32_t p_begin, int32_t p_end, float* s, void* workspace,
+                   size_t workspace_bytes, const sks_options* opt, void* stream) {
+  sks_status st = validate_common(N, M, d, kernel, P, p_begin, p_end);
+  if (st != SKS_OK) return st;
+  if (!x || !y || !w || !s) return fail(SKS_ERR_INVALID, "NULL x/y/w/s");
+  Opts o;
+  if ((st = resolve_opts(opt, &o)) != SKS_OK) return st;
+  DirEntry dirs;
+  if ((st = get_dirs(P, d, seed, p_begin, p_end, &dirs)) != SKS_OK) return st;
+  Problem pr{N, M, d, kernel, p_end - p_begin, true};
+  return run_batches(pr, o, x, y, w, &dirs, nullptr, nullptr, s, nullptr, 1.0 / P, workspace, workspace_bytes,
+                     static_cast<cudaStream_t>(stream));
+}
+
+sks_status sks_workspace_size_host(int64_t N, int64_t M, int32_t d, sks_kernel kernel, int32_t P, int32_t p_begin,
+                                   int32_t p_end, const sks_options* opt, size_t* bytes) {
+  sks_status s = sks_workspace_size(N, M, d, kernel, P, p_begin, p_end, opt, bytes);
+  if (s != SKS_OK) return s;
+  *bytes += al(sizeof(float) * N * d) + al(sizeof(float) * M * d) + al(sizeof(float) * N) + al(sizeof(float) * M);
+  return SKS_OK;
+}
+
+sks_status sks_sum_host(const float* x, int64_t N, const float* y, int64_t M, int32_t d, const float* w,
+                        sks_kernel kernel, int32_t P, uint64_t seed, int32_t p_begin, int32_t p_end, float* s,
+                        void* workspace, size_t workspace_bytes, const sks_options* opt, void* stream) {
+  size_t need = 0;
+  sks_status st = sks_workspace_size_host(N, M, d, kernel, P, p_begin, p_end, opt, &need);
+  if (st != SKS_OK) return st;
+  if (!x || !y || !w || !s) return fail(SKS_ERR_INVALID, "NULL x/y/w/s");
+  if (!workspace || workspace_bytes < need) return fail(SKS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(SKS_ERR_INVALID, "workspace must be 256-byte aligned");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  float* dx = reinterpret_cast<float*>(ws);
+  float* dy = reinterpret_cast<float*>(ws + al(sizeof(float) * N * d));
+  float* dw = reinterpret_cast<float*>(reinterpret_cast<char*>(dy) + al(sizeof(float) * M * d));
+  float* ds = reinterpret_cast<float*>(reinterpret_cast<char*>(dw) + al(sizeof(float) * N));
+  char* rest = reinterpret_cast<char*>(ds) + al(sizeof(float) * M);
+  const size_t used = static_cast<size_t>(rest - ws);
+  SKS_CUDA(cudaMemcpyAsync(dx, x, sizeof(float) * N * d, cudaMemcpyHostToDevice, cs));
+  SKS_CUDA(cudaMemcpyAsync(dy, y, sizeof(float) * M * d, cudaMemcpyHostToDevice, cs));
+  SKS_CUDA(cudaMemcpyAsync(dw, w, sizeof(float) * N, cudaMemcpyHostToDevice, cs));
+  st = sks_sum(dx, N, dy, M, d, dw, kernel, P, seed, p_begin, p_end, ds, rest, workspace_bytes - used, opt, stream);
+  if (st != SKS_OK) return st;
+  SKS_CUDA(cudaMemcpyAsync(s, ds, sizeof(float) * M, cudaMemcpyDeviceToHost, cs));
+  SKS_CUDA(cudaStreamSynchronize(cs));
+  return SKS_OK;
+}
+
+sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64_t seed, int32_t p_begin,
+                       int32_t p_end, float* z, void* stream) {
+  if (!pts || !z || n <= 0 || d <= 0) return fail(SKS_ERR_INVALID, "bad pts/z/n/d");
+  if (P <= 0 || p_begin < 0 || p_end > P || p_begin >= p_end) return fail(SKS_ERR_INVALID, "bad slice range");
+  DirEntry dirs;
+  sks_status st = get_dirs(P, d, seed, p_begin, p_end, &dirs);
+  if (st != SKS_OK) return st;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  const int np = p_end - p_begin;
+  // ranges / flag are not needed by the caller: use a small scratch in the direction cache's stream order
+  static thread_local unsigned* scratch = nullptr;
+  static thread_local int scratch_np = 0;
+  if (scratch_np < np) {
+    if (scratch) cudaFree(scratch);
+    SKS_CUDA(cudaMalloc(&scratch, sizeof(unsigned) * 4 * np + 16));
+    scratch_np = np;
+  }
+  SKS_CUDA(sks::launch_init_minmax(scratch, np, cs));
+  SKS_CUDA(sks::launch_project(pts, n, pts, 0, d, dirs.g, dirs.inv, np, z, n, scratch,
+                               reinterpret_cast<int*>(scratch + 4 * np), cs));
+  return SKS_OK;
+}
+
+sks_status sks_workspace_size_1d(int64_t N, int64_t M, int32_t d, sks_kernel kernel, int32_t n_slices,
+                                 const sks_options* opt, size_t* bytes) {
+  sks_status s = validate_common(N, M, d, kernel, n_slices, 0, n_slices);
+  if (s != SKS_OK) return s;
+  Opts o;
+  if ((s = resolve_opts(opt, &o)) != SKS_OK) return s;
+  if (!bytes) return fail(SKS_ERR_INVALID, "bytes is NULL");
+  const Path pt = path_of(kernel.kind);
+  const int nb = (pt.sort || pt.moment) ? buckets_for(N) : 0;
+  const int batch = choose_batch(N, M, pt, n_slices, false, nb, o.batch);
+  *bytes = make_layout(N, M, pt, batch, false, nb).total;
+  return SKS_OK;
+}
+
+sks_status sks_sum_1d(const float* zx, const float* zy, const float* w, int64_t N, int64_t M, int32_t n_slices,
+                      int32_t d, sks_kernel kernel, float* t, void* workspace, size_t workspace_bytes,
+                      const sks_options* opt, void* stream) {
+  sks_status st = validate_common(N, M, d, kernel, n_slices, 0, n_slices);
+  if (st != SKS_OK) return st;
+  if (!zx || !zy || !w || !t) return fail(SKS_ERR_INVALID, "NULL zx/zy/w/t");
+  Opts o;
+  if ((st = resolve_opts(opt, &o)) != SKS_OK) return st;
+  Problem pr{N, M, d, kernel, n_slices, false};
+  return run_batches(pr, o, nullptr, nullptr, w, nullptr, zx, zy, nullptr, t, 1.0, workspace, workspace_bytes,
+                     static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

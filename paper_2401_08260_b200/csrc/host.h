@@ -1,0 +1,59 @@
+// host.h -- host-side (C++) pieces of libsks: directions (R1) and the torus planner
+// (Sec. 3.1 P:485-551 with readings R3-R7b).  Shares nothing with oracle/.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace sks {
+
+// ---- directions (R1): one SplitMix64 substream per slice p, Box-Muller in fp64, bf16 RNE
+void make_directions(int P, int d, uint64_t seed, int p0, int p1, float* g, double* inv_norm);
+
+// ---- kernel model: f(x) = f1(x/scale), f1 the unit-scale 1D counterpart (Table 1)
+struct KernelModel {
+  int kind;      // sks_kind
+  int matern_p;  // nu = p + 1/2
+  double scale;  // sigma | - | ell | beta
+  int d;
+};
+
+double cd(int d);  // sqrt(pi) Gamma((d+1)/2)/Gamma(d/2)
+
+// Fourier transform of the unit-scale counterpart: fhat1(rho) = int f1(x) e^{-2 pi i x rho} dx
+//   Gaussian: Lemma 2.5 with sigma = 1; Laplacian / Matern: Fourier-slice identity (R7/R7b)
+double fhat1(const KernelModel& k, double rho);
+
+// torus coefficient c_k of the periodised counterpart on period 1/tau (R4, R7):
+//   Gaussian / Matern: tau * fhat(tau k);  Laplacian smooth part: tau fhat(tau k) + (alpha c_d / tau) hhat_k
+double torus_coeff(const KernelModel& k, double tau, int64_t kk);
+
+// decay radius (in x units) beyond which |f(x)| <= eps  (reading R3): numeric Fourier integral, cached
+double decay_radius(const KernelModel& k, double eps);
+
+// ---- per-call Fourier plan
+struct SlicePlan {
+  float tau, cen;   // u = tau (z - cen) in [-1/2, 1/2)
+  int lmin;         // first grid cell of the x footprint (unwrapped)
+  int klo, khi;     // kept band: klo <= |k| <= khi
+};
+
+struct FourierPlan {
+  int n = 0;            // grid length (power of two)
+  int w = 0;            // window taps
+  float beta = 0.f;     // ES window shape
+  int k_max = 0, band_lo_min = 0;
+  int W = 0;            // widest per-slice footprint (cells)
+  double tau_min = 0, tau_max = 0;
+  std::vector<SlicePlan> slices;
+  std::vector<float> phi2inv;   // [n/2 + 1]  1 / Phi(k/n)^2 (window deconvolution, folded into D_k on device)
+};
+
+// Build the plan for `ns` slices from per-slice projection ranges.
+//   xmin/xmax: range of the x (source) projections, amin/amax: range over x and y.
+// Returns false with a message on failure (unsupported size / non-finite range).
+bool build_fourier_plan(const KernelModel& k, double eps, int w, int oversample, int ns, const float* xmin,
+                        const float* xmax, const float* amin, const float* amax, FourierPlan& out,
+                        std::string* err);
+
+}  // namespace sks

@@ -1,0 +1,617 @@
+// kernels.cu -- sm_100a kernels of libsks (v0: SIMT projection, counting-sort sort path, NFFT path).
+//
+// Row map (SURVEY.md Sec. 8a / DESIGN.md):
+//   a1 projection ............ k_project            (Alg.1)
+//   a2 torus plan (D_k) ....... k_plan_D             (R3-R7b)
+//   a3 sort (counting sort) ... k_bucket_build       (Sec. 3.2, Alg. 2)
+//   a4 scans + evaluate ....... k_bucket_build (fp64 prefix sums) + k_eval (sort part)
+//   a5 spread ................. k_spread_private / k_spread_shared   (NFFT adjoint)
+//   a6 FFT x D iFFT ........... k_fft_filter
+//   a7 interpolate + mean ..... k_eval (Fourier part) + k_finalize   (Alg.1)
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace sks {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ unsigned f2key(float f) {  // order-preserving float -> uint
+  unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ inline float key2f(unsigned k) {
+  unsigned u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(u);
+#else
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+#endif
+}
+
+void decode_minmax(const unsigned* enc, float* dec, int n) {
+  for (int i = 0; i < n; ++i) dec[i] = key2f(enc[i]);
+}
+
+// bucket index: monotone non-decreasing in z (fp32 sub/mul round monotonically), clamped to [0, nb)
+__device__ __forceinline__ int bucket_of(float z, float zmin, float scale, int nb) {
+  float t = __fmul_rn(__fsub_rn(z, zmin), scale);
+  int b = (t >= 0.f) ? static_cast<int>(t) : 0;   // t < 2^31 guaranteed by min()
+  return b < nb ? b : nb - 1;
+}
+
+// ES window phi(t) = exp(beta (sqrt(1 - t^2) - 1)), |t| <= 1   (R6)
+__device__ __forceinline__ float es_window(float t, float beta) {
+  float s = fmaxf(0.f, 1.f - t * t);
+  return __expf(beta * (sqrtf(s) - 1.f));
+}
+
+// grid coordinate: identical fp32 op sequence on host (planner footprint) and device
+__device__ __forceinline__ float grid_coord(float z, float cen, float tau, float nf) {
+  return __fmul_rn(__fmul_rn(__fsub_rn(z, cen), tau), nf);
+}
+
+// ------------------------------------------------------------------ a1: projection (SIMT fp32, v0)
+// Z[p][i] = inv_norm[p] * sum_j g[p][j] * pt_i[j];  tile 64 slices x 128 points, K-step 16
+constexpr int PJ_BM = 64, PJ_BN = 128, PJ_BK = 16;
+
+__global__ void __launch_bounds__(256) k_project(const float* __restrict__ x, int64_t N, const float* __restrict__ y,
+                                                 int64_t M, int d, const float* __restrict__ g,
+                                                 const float* __restrict__ inv_norm, int np, float* __restrict__ Z,
+                                                 int64_t ldz, unsigned* __restrict__ mm, int* __restrict__ flag) {
+  __shared__ float Gs[PJ_BK][PJ_BM + 4];
+  __shared__ float Ps[PJ_BK][PJ_BN + 4];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t L = N + M;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * PJ_BN;
+  const int s0 = blockIdx.y * PJ_BM;
+  float acc[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+
+  for (int k0 = 0; k0 < d; k0 += PJ_BK) {
+    // G tile: 64 x 16, 4 per thread
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = tid + r * 256, row = e >> 4, col = e & 15;
+      const int s = s0 + row, k = k0 + col;
+      Gs[col][row] = (s < np && k < d) ? g[static_cast<int64_t>(s) * d + k] : 0.f;
+    }
+    // point tile: 128 x 16, 8 per thread
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = tid + r * 256, row = e >> 4, col = e & 15;
+      const int64_t i = i0 + row;
+      const int k = k0 + col;
+      float v = 0.f;
+      if (i < L && k < d) v = (i < N) ? x[i * d + k] : y[(i - N) * d + k];
+      Ps[col][row] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < PJ_BK; ++kk) {
+      float a[4], b[8];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = Gs[kk][ty * 4 + r];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) b[c] = Ps[kk][tx + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+  // epilogue: normalise, store, per-slice ranges (x-only and all) + non-finite flag
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int s = s0 + ty * 4 + r;
+    const float sc = (s < np) ? inv_norm[s] : 0.f;
+    float xmn = CUDART_INF_F, xmx = -CUDART_INF_F, amn = CUDART_INF_F, amx = -CUDART_INF_F;
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int64_t i = i0 + tx + 16 * c;
+      const float z = acc[r][c] * sc;
+      if (s < np && i < L) {
+        Z[static_cast<int64_t>(s) * ldz + i] = z;
+        if (!isfinite(z)) bad = true;
+        amn = fminf(amn, z);
+        amx = fmaxf(amx, z);
+        if (i < N) { xmn = fminf(xmn, z); xmx = fmaxf(xmx, z); }
+      }
+    }
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {   // reduce over the 16 lanes sharing this slice row
+      xmn = fminf(xmn, __shfl_xor_sync(0xffffffffu, xmn, o));
+      xmx = fmaxf(xmx, __shfl_xor_sync(0xffffffffu, xmx, o));
+      amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, o));
+      amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+    }
+    if (bad) atomicOr(flag, 1);
+    if (tx == 0 && s < np) {
+      if (xmn <= xmx) { atomicMin(&mm[s * 4 + 0], f2key(xmn)); atomicMax(&mm[s * 4 + 1], f2key(xmx)); }
+      if (amn <= amx) { atomicMin(&mm[s * 4 + 2], f2key(amn)); atomicMax(&mm[s * 4 + 3], f2key(amx)); }
+    }
+  }
+}
+
+__global__ void k_init_minmax(unsigned* mm, int np) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < np) { mm[i * 4 + 0] = 0xffffffffu; mm[i * 4 + 1] = 0u; mm[i * 4 + 2] = 0xffffffffu; mm[i * 4 + 3] = 0u; }
+}
+
+__global__ void k_minmax(ZView zv, unsigned* mm, int* flag) {
+  const int p = blockIdx.y;
+  float xmn = CUDART_INF_F, xmx = -CUDART_INF_F, amn = CUDART_INF_F, amx = -CUDART_INF_F;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < zv.N + zv.M; i += (int64_t)gridDim.x * blockDim.x) {
+    const float z = (i < zv.N) ? zv.zx[p * zv.ldx + i] : zv.zy[p * zv.ldy + (i - zv.N)];
+    if (!isfinite(z)) bad = true;
+    amn = fminf(amn, z);
+    amx = fmaxf(amx, z);
+    if (i < zv.N) { xmn = fminf(xmn, z); xmx = fmaxf(xmx, z); }
+  }
+  for (int o = 16; o >= 1; o >>= 1) {
+    xmn = fminf(xmn, __shfl_xor_sync(0xffffffffu, xmn, o));
+    xmx = fmaxf(xmx, __shfl_xor_sync(0xffffffffu, xmx, o));
+    amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, o));
+    amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+  }
+  if (bad) atomicOr(flag, 1);
+  if ((threadIdx.x & 31) == 0) {
+    if (xmn <= xmx) { atomicMin(&mm[p * 4 + 0], f2key(xmn)); atomicMax(&mm[p * 4 + 1], f2key(xmx)); }
+    if (amn <= amx) { atomicMin(&mm[p * 4 + 2], f2key(amn)); atomicMax(&mm[p * 4 + 3], f2key(amx)); }
+  }
+}
+
+cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st) {
+  k_init_minmax<<<(np + 255) / 256, 256, 0, st>>>(mm, np);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_project(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g,
+                           const float* inv_norm, int np, float* Z, int64_t ldz, unsigned* mm, int* flag,
+                           cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((N + M + PJ_BN - 1) / PJ_BN), (np + PJ_BM - 1) / PJ_BM);
+  k_project<<<grid, 256, 0, st>>>(x, N, y, M, d, g, inv_norm, np, Z, ldz, mm, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_t st) {
+  const int64_t L = zv.N + zv.M;
+  int bx = static_cast<int>((L + 255) / 256);
+  if (bx > 64) bx = 64;
+  k_minmax<<<dim3(bx, np), 256, 0, st>>>(zv, mm, flag);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a3/a4: counting sort + fp64 prefix sums
+// One CTA (1024 threads) per slice.  smem: nb int counters.
+//  1. count x projections per bucket (smem atomics)      2. exclusive scan -> bucket offsets
+//  3. scatter (z, w) into bucket order (smem cursors)    4. fp64 bucket sums (A=sum w, B=sum wz, C=sum wz^2)
+//  5. exclusive fp64 scan over buckets -> tab[p][b] = sums over buckets < b; tab[p][nb] = totals
+constexpr int BK_THREADS = 1024;
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(BK_THREADS) k_bucket_build(ZView zv, const float* __restrict__ w, int nb,
+                                                             const unsigned* __restrict__ mm, float2* __restrict__ xs,
+                                                             int* __restrict__ off, double* __restrict__ tab,
+                                                             float* __restrict__ bpar) {
+  extern __shared__ int cnt[];
+  __shared__ int wsum_i[32];
+  __shared__ double wsum_d[3][32];
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t N = zv.N;
+  const float* zx = zv.zx + p * zv.ldx;
+  const float zmin = key2f(mm[p * 4 + 0]), zmax = key2f(mm[p * 4 + 1]);
+  const float range = zmax - zmin;
+  const float scale = (range > 0.f) ? static_cast<float>(nb) / range : 0.f;
+  if (tid == 0) { bpar[p * 2 + 0] = zmin; bpar[p * 2 + 1] = scale; }
+  for (int b = tid; b < nb; b += BK_THREADS) cnt[b] = 0;
+  __syncthreads();
+  for (int64_t i = tid; i < N; i += BK_THREADS) atomicAdd(&cnt[bucket_of(zx[i], zmin, scale, nb)], 1);
+  __syncthreads();
+  // exclusive scan of cnt (E = nb / 1024 consecutive entries per thread)
+  const int E = nb / BK_THREADS;
+  const int b0 = tid * E;
+  int loc = 0;
+  for (int e = 0; e < E; ++e) loc += cnt[b0 + e];
+  int inc = warp_incl_scan(loc);
+  if (lane == 31) wsum_i[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int v = wsum_i[lane];
+    int vi = warp_incl_scan(v);
+    wsum_i[lane] = vi - v;
+  }
+  __syncthreads();
+  int run = wsum_i[wid] + inc - loc;
+  int* offp = off + static_cast<int64_t>(p) * (nb + 1);
+  for (int e = 0; e < E; ++e) {
+    const int c = cnt[b0 + e];
+    cnt[b0 + e] = run;
+    offp[b0 + e] = run;
+    run += c;
+  }
+  if (tid == BK_THREADS - 1) offp[nb] = run;   // == N
+  __syncthreads();
+  // scatter into bucket order (order inside a bucket is irrelevant: those terms are summed directly)
+  float2* xsp = xs + static_cast<int64_t>(p) * N;
+  for (int64_t i = tid; i < N; i += BK_THREADS) {
+    const float z = zx[i];
+    const int pos = atomicAdd(&cnt[bucket_of(z, zmin, scale, nb)], 1);
+    xsp[pos] = make_float2(z, w[i]);
+  }
+  __syncthreads();
+  // fp64 sums over this thread's buckets
+  double A = 0.0, B = 0.0, C = 0.0;
+  {
+    const int lo = offp[b0], hi = offp[b0 + E];
+    for (int j = lo; j < hi; ++j) {
+      const float2 e = xsp[j];
+      const double wz = static_cast<double>(e.y) * e.x;
+      A += e.y;
+      B += wz;
+      C += wz * e.x;
+    }
+  }
+  double iA = warp_incl_scan(A), iB = warp_incl_scan(B), iC = warp_incl_scan(C);
+  if (lane == 31) { wsum_d[0][wid] = iA; wsum_d[1][wid] = iB; wsum_d[2][wid] = iC; }
+  __syncthreads();
+  if (wid == 0) {
+    double a = wsum_d[0][lane], b = wsum_d[1][lane], c = wsum_d[2][lane];
+    double ia = warp_incl_scan(a), ib = warp_incl_scan(b), ic = warp_incl_scan(c);
+    wsum_d[0][lane] = ia - a;
+    wsum_d[1][lane] = ib - b;
+    wsum_d[2][lane] = ic - c;
+  }
+  __syncthreads();
+  double rA = wsum_d[0][wid] + iA - A, rB = wsum_d[1][wid] + iB - B, rC = wsum_d[2][wid] + iC - C;
+  double* tp = tab + static_cast<int64_t>(p) * (nb + 1) * 3;
+  for (int e = 0; e < E; ++e) {
+    const int b = b0 + e;
+    tp[b * 3 + 0] = rA;
+    tp[b * 3 + 1] = rB;
+    tp[b * 3 + 2] = rC;
+    const int lo = offp[b], hi = offp[b + 1];
+    for (int j = lo; j < hi; ++j) {
+      const float2 q = xsp[j];
+      const double wz = static_cast<double>(q.y) * q.x;
+      rA += q.y;
+      rB += wz;
+      rC += wz * q.x;
+    }
+  }
+  if (tid == BK_THREADS - 1) { tp[nb * 3 + 0] = rA; tp[nb * 3 + 1] = rB; tp[nb * 3 + 2] = rC; }
+}
+
+cudaError_t launch_bucket_build(ZView zv, const float* w, int np, int nb, const unsigned* mm, float2* xs, int* off,
+                                double* tab, float* bpar, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(nb) * sizeof(int);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_bucket_build, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4);
+    attr_set = true;
+  }
+  k_bucket_build<<<np, BK_THREADS, smem, st>>>(zv, w, nb, mm, xs, off, tab, bpar);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a2: device planner D_k = c_k / Phi_k^2
+__device__ double torus_coeff_dev(const CoeffConst& c, double tau, int k) {
+  const double PI = 3.14159265358979323846;
+  const double rho = c.scale * tau * static_cast<double>(k);
+  double fh = 0.0;
+  if (c.kind == 0) {
+    if (rho == 0.0) fh = (c.d == 1) ? sqrt(2.0 * PI) : 0.0;
+    else {
+      const double a = 2.0 * PI * PI * rho * rho;
+      fh = exp(c.logpref - a + 0.5 * (c.d - 1) * log(a));
+    }
+  } else if (c.kind == 2) {
+    const double s = 2.0 * PI * rho;
+    if (s == 0.0) fh = (c.d == 1) ? 2.0 : 0.0;
+    else fh = exp(c.logpref + (c.d - 1) * log(s) - 0.5 * (c.d + 1) * log1p(s * s));
+  } else if (c.kind == 3) {
+    const double lr = (c.d == 1) ? 0.0 : ((rho == 0.0) ? -INFINITY : (c.d - 1) * log(rho));
+    fh = exp(c.logpref + lr - (c.nu + 0.5 * c.d) * log(2.0 * c.nu + 4.0 * PI * PI * rho * rho));
+  }
+  double v = tau * c.scale * fh;
+  if (c.kind == 2) {
+    const double A = c.lap_A / tau;
+    v += (k == 0) ? A / 6.0 : -A / (2.0 * PI * PI * static_cast<double>(k) * static_cast<double>(k));
+  }
+  return v;
+}
+
+__global__ void k_plan_D(const FPar* __restrict__ fp, CoeffConst cc, const float* __restrict__ phi2inv, int n,
+                         float* __restrict__ D) {
+  const int p = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nh = n / 2 + 1;
+  if (k >= nh) return;
+  const FPar f = fp[p];
+  const int klo = f.klo_khi >> 16, khi = f.klo_khi & 0xffff;
+  float v = 0.f;
+  if (k >= klo && k <= khi) v = static_cast<float>(torus_coeff_dev(cc, static_cast<double>(f.tau), k) * phi2inv[k]);
+  D[static_cast<int64_t>(p) * nh + k] = v;
+}
+
+cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* phi2inv, int n, float* D,
+                          cudaStream_t st) {
+  const int nh = n / 2 + 1;
+  k_plan_D<<<dim3((nh + 255) / 256, np), 256, 0, st>>>(fp, cc, phi2inv, n, D);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a5: spreading (adjoint NFFT gridding)
+// Per-lane private sub-grids [warp][cell][lane] (conflict-free RMW, no atomics) over the slice's footprint
+// of W cells; one CTA = (chunk of points, slice).  Fallback for wide footprints: CTA grid + smem atomics.
+constexpr int SP_THREADS = 256, SP_WARPS = SP_THREADS / 32, SP_WMAX_PRIV = 64;
+
+__global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const float* __restrict__ w,
+                                                               const FPar* __restrict__ fp, int n, int wt, float beta,
+                                                               int W, int64_t chunk, float* __restrict__ grid) {
+  extern __shared__ float priv[];   // [SP_WARPS][W][32]
+  const int p = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const FPar f = fp[p];
+  float* mine = priv + static_cast<int64_t>(wid) * W * 32;
+  for (int c = lane; c < W * 32; c += 32) mine[c] = 0.f;
+  __syncwarp();
+  const float nf = static_cast<float>(n), hw = 0.5f * wt, inv_hw = 2.0f / wt;
+  const int64_t i0 = blockIdx.x * chunk, i1 = min(zv.N, i0 + chunk);
+  const float* zx = zv.zx + p * zv.ldx;
+  for (int64_t i = i0 + tid; i < i1; i += SP_THREADS) {
+    const float v = grid_coord(zx[i], f.cen, f.tau, nf);
+    const int l0 = static_cast<int>(floorf(__fsub_rn(v, hw))) + 1;
+    const float wi = w[i];
+    const int loc = l0 - f.lmin;
+    float dist = v - static_cast<float>(l0);
+    for (int j = 0; j < wt; ++j) {
+      mine[(loc + j) * 32 + lane] += wi * es_window(dist * inv_hw, beta);
+      dist -= 1.f;
+    }
+  }
+  __syncthreads();
+  // reduce: cell c -> sum over warps (registers) then lanes (shuffles)
+  for (int c = wid; c < W; c += SP_WARPS) {
+    float s = 0.f;
+#pragma unroll 8
+    for (int q = 0; q < SP_WARPS; ++q) s += priv[(static_cast<int64_t>(q) * W + c) * 32 + lane];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0 && s != 0.f) atomicAdd(&grid[static_cast<int64_t>(p) * n + ((f.lmin + c) & (n - 1))], s);
+  }
+}
+
+__global__ void __launch_bounds__(SP_THREADS) k_spread_shared(ZView zv, const float* __restrict__ w,
+                                                              const FPar* __restrict__ fp, int n, int wt, float beta,
+                                                              int64_t chunk, float* __restrict__ grid) {
+  extern __shared__ float sg[];   // [n]
+  const int p = blockIdx.y, tid = threadIdx.x;
+  const FPar f = fp[p];
+  for (int c = tid; c < n; c += SP_THREADS) sg[c] = 0.f;
+  __syncthreads();
+  const float nf = static_cast<float>(n), hw = 0.5f * wt, inv_hw = 2.0f / wt;
+  const int64_t i0 = blockIdx.x * chunk, i1 = min(zv.N, i0 + chunk);
+  const float* zx = zv.zx + p * zv.ldx;
+  for (int64_t i = i0 + tid; i < i1; i += SP_THREADS) {
+    const float v = grid_coord(zx[i], f.cen, f.tau, nf);
+    const int l0 = static_cast<int>(floorf(__fsub_rn(v, hw))) + 1;
+    const float wi = w[i];
+    float dist = v - static_cast<float>(l0);
+    for (int j = 0; j < wt; ++j) {
+      atomicAdd(&sg[(l0 + j) & (n - 1)], wi * es_window(dist * inv_hw, beta));
+      dist -= 1.f;
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < n; c += SP_THREADS) {
+    const float s = sg[c];
+    if (s != 0.f) atomicAdd(&grid[static_cast<int64_t>(p) * n + c], s);
+  }
+}
+
+cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int n, int wt, float beta, int W,
+                          float* grid, cudaStream_t st) {
+  // chunking: enough CTAs to fill 148 SMs several times, >= 2048 points per CTA to amortise the flush
+  int64_t chunk = 8192;
+  while (chunk > 2048 && ((zv.N + chunk - 1) / chunk) * np < 4 * 148) chunk >>= 1;
+  const unsigned nchunk = static_cast<unsigned>((zv.N + chunk - 1) / chunk);
+  if (nchunk == 0) return cudaSuccess;
+  if (W <= SP_WMAX_PRIV) {
+    const size_t smem = static_cast<size_t>(SP_WARPS) * W * 32 * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_spread_private, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SP_WARPS * SP_WMAX_PRIV * 32 * 4);
+      attr = true;
+    }
+    k_spread_private<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, wt, beta, W, chunk, grid);
+  } else {
+    const size_t smem = static_cast<size_t>(n) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_spread_shared, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4);
+      attr = true;
+    }
+    k_spread_shared<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, wt, beta, chunk, grid);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a6: FFT -> x D -> inverse FFT (one CTA per slice)
+constexpr int FF_THREADS = 512;
+
+__device__ __forceinline__ void fft_stages(float2* buf, const float2* tw, int n, int logn) {
+  for (int s = 1; s <= logn; ++s) {
+    const int half = 1 << (s - 1);
+    const int tstride = n >> s;
+    for (int b = threadIdx.x; b < n / 2; b += FF_THREADS) {
+      const int grp = b >> (s - 1), pos = b & (half - 1);
+      const int i = grp * 2 * half + pos, j = i + half;
+      const float2 t = tw[pos * tstride];
+      const float2 a = buf[i], c = buf[j];
+      const float2 bt = make_float2(c.x * t.x - c.y * t.y, c.x * t.y + c.y * t.x);
+      buf[i] = make_float2(a.x + bt.x, a.y + bt.y);
+      buf[j] = make_float2(a.x - bt.x, a.y - bt.y);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restrict__ grid, const float* __restrict__ D,
+                                                           int n, int logn, float* __restrict__ h) {
+  extern __shared__ float2 sm[];
+  float2* buf = sm;          // [n]
+  float2* tw = sm + n;       // [n/2] forward twiddles e^{-2 pi i j / n}
+  const int p = blockIdx.x;
+  const int nh = n / 2 + 1;
+  for (int j = threadIdx.x; j < n / 2; j += FF_THREADS) {
+    float sv, cv;
+    sincospif(2.0f * static_cast<float>(j) / static_cast<float>(n), &sv, &cv);
+    tw[j] = make_float2(cv, -sv);
+  }
+  const float* gp = grid + static_cast<int64_t>(p) * n;
+  for (int l = threadIdx.x; l < n; l += FF_THREADS) buf[__brev(l) >> (32 - logn)] = make_float2(gp[l], 0.f);
+  __syncthreads();
+  fft_stages(buf, tw, n, logn);                     // G_k = sum_l g_l e^{-2 pi i k l / n}
+  const float* Dp = D + static_cast<int64_t>(p) * nh;
+  for (int k = threadIdx.x; k < n; k += FF_THREADS) {
+    const float dk = Dp[k <= n / 2 ? k : n - k];
+    const float2 v = buf[k];
+    buf[k] = make_float2(v.x * dk, -v.y * dk);      // conj(D_k G_k)
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < n; l += FF_THREADS) {   // bit-reversal permutation in place
+    const int r = __brev(l) >> (32 - logn);
+    if (l < r) { const float2 t = buf[l]; buf[l] = buf[r]; buf[r] = t; }
+  }
+  __syncthreads();
+  fft_stages(buf, tw, n, logn);                     // h_l = conj(FFT(conj X))_l; real part
+  float* hp = h + static_cast<int64_t>(p) * n;
+  for (int l = threadIdx.x; l < n; l += FF_THREADS) hp[l] = buf[l].x;
+}
+
+cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, cudaStream_t st) {
+  int logn = 0;
+  while ((1 << logn) < n) ++logn;
+  const size_t smem = static_cast<size_t>(n) * sizeof(float2) + static_cast<size_t>(n / 2) * sizeof(float2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft_filter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         16384 * 8 + 8192 * 8);
+    attr = true;
+  }
+  k_fft_filter<<<np, FF_THREADS, smem, st>>>(grid, D, n, logn, h);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a4 + a7: evaluation at the targets
+__global__ void __launch_bounds__(256) k_eval(EvalArgs a) {
+  const int64_t M = a.zv.M;
+  const float nf = static_cast<float>(a.n), hw = 0.5f * a.wt, inv_hw = 2.0f / a.wt;
+  for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < M;
+       m += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int p = 0; p < a.np; ++p) {
+      const float z = a.zv.zy[p * a.zv.ldy + m];
+      const double zd = z;
+      double t = 0.0;
+      if (a.sort || a.moment) {
+        const double* tp = a.tab + static_cast<int64_t>(p) * (a.nb + 1) * 3;
+        const double Atot = tp[a.nb * 3 + 0], Btot = tp[a.nb * 3 + 1];
+        if (a.sort) {
+          const int b = bucket_of(z, a.bpar[p * 2 + 0], a.bpar[p * 2 + 1], a.nb);
+          const int* op = a.off + static_cast<int64_t>(p) * (a.nb + 1);
+          const int lo = op[b], hi = op[b + 1];
+          const double Alo = tp[b * 3 + 0], Blo = tp[b * 3 + 1];
+          const double Ahi = Atot - tp[(b + 1) * 3 + 0], Bhi = Btot - tp[(b + 1) * 3 + 1];
+          // sum_n w_n |z_n - z| = [z A_lo - B_lo] + [B_hi - z A_hi] + (same-bucket terms, direct)
+          double same = 0.0;
+          const float2* xp = a.xs + static_cast<int64_t>(p) * a.zv.N;
+          for (int j = lo; j < hi; ++j) {
+            const float2 q = xp[j];
+            same += static_cast<double>(q.y) * fabs(static_cast<double>(q.x) - zd);
+          }
+          t -= a.sort_coef * ((zd * Alo - Blo) + (Bhi - zd * Ahi) + same);
+        }
+        if (a.moment) {
+          const double Ctot = tp[a.nb * 3 + 2];
+          t += a.mom_coef * static_cast<double>(a.fp[p].tau) * (Ctot - 2.0 * zd * Btot + zd * zd * Atot);
+        }
+      }
+      if (a.fourier) {
+        const FPar f = a.fp[p];
+        const float v = grid_coord(z, f.cen, f.tau, nf);
+        const int l0 = static_cast<int>(floorf(__fsub_rn(v, hw))) + 1;
+        const float* hp = a.h + static_cast<int64_t>(p) * a.n;
+        float dist = v - static_cast<float>(l0);
+        float tf = 0.f;
+        for (int j = 0; j < a.wt; ++j) {
+          tf += hp[(l0 + j) & (a.n - 1)] * es_window(dist * inv_hw, a.beta);
+          dist -= 1.f;
+        }
+        t += tf;
+      }
+      if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
+      acc += t;
+    }
+    if (a.s64) a.s64[m] += acc;
+  }
+}
+
+cudaError_t launch_eval(const EvalArgs& a, cudaStream_t st) {
+  int64_t blocks = (a.zv.M + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_eval<<<static_cast<unsigned>(blocks), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+__global__ void k_zero(uint4* p, size_t n16) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n16; i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    p[i] = make_uint4(0, 0, 0, 0);
+}
+
+cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t st) {
+  // bytes is a multiple of 16 (workspace carving aligns every region to 256 B)
+  const size_t n16 = bytes / 16;
+  if (n16 == 0) return cudaSuccess;
+  size_t blocks = (n16 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_zero<<<static_cast<unsigned>(blocks), 256, 0, st>>>(static_cast<uint4*>(p), n16);
+  return cudaGetLastError();
+}
+
+__global__ void k_finalize(const double* __restrict__ s64, int64_t M, double scale, float* __restrict__ s) {
+  for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < M; m += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    s[m] = static_cast<float>(s64[m] * scale);
+}
+
+cudaError_t launch_finalize(const double* s64, int64_t M, double scale, float* s, cudaStream_t st) {
+  int64_t blocks = (M + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  k_finalize<<<static_cast<unsigned>(blocks), 256, 0, st>>>(s64, M, scale, s);
+  return cudaGetLastError();
+}
+
+}  // namespace sks

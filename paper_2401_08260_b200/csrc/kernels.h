@@ -1,0 +1,87 @@
+// kernels.h -- launch wrappers of the sm_100a kernels of libsks (defined in *.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace sks {
+
+// per-slice Fourier parameters (device copy of SlicePlan)
+struct FPar {
+  float tau, cen;
+  int lmin;
+  int klo_khi;  // (klo << 16) | khi
+};
+
+// per-call constants of the closed-form torus coefficients (device planner, row a2)
+struct CoeffConst {
+  int kind, d;
+  double scale;     // sigma | ell | beta
+  double logpref;   // log of the constant prefactor of fhat1 (see host: fhat1)
+  double nu;        // Matern nu
+  double lap_A;     // Laplacian: c_d / scale  (alpha c_d), multiplied by 1/tau per slice
+};
+
+// views of the projected points of a slice batch: x-part zx[p*ldx + i], y-part zy[p*ldy + m]
+struct ZView {
+  const float* zx;
+  const float* zy;
+  int64_t ldx, ldy;
+  int64_t N, M;
+};
+
+// row a1: Z[p][i] = inv_norm[p] * <g_p, pt_i>, i in [0, N+M) (x block then y block); per-slice ranges
+// mm[p*4 + {0,1,2,3}] = encoded {xmin, xmax, allmin, allmax}; nonfinite flag.
+cudaError_t launch_project(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g,
+                           const float* inv_norm, int np, float* Z, int64_t ldz, unsigned* mm, int* flag,
+                           cudaStream_t st);
+// per-slice ranges of given projections (sks_sum_1d)
+cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_t st);
+cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st);
+void decode_minmax(const unsigned* enc, float* dec, int n);
+
+// rows a3 (+ a4 prefix sums): one-pass MSD counting sort of the x projections into nb buckets per
+// slice, fp64 bucket prefix sums (A = sum w, B = sum w z, C = sum w z^2) -> tab[p][b][3], off[p][b]
+cudaError_t launch_bucket_build(ZView zv, const float* w, int np, int nb, const unsigned* mm, float2* xs, int* off,
+                                double* tab, float* bpar, cudaStream_t st);
+
+// row a2: D[p][k] = c_k(tau_p) / Phi_k^2 on the band of slice p, else 0  (k = 0..n/2)
+cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* phi2inv, int n, float* D,
+                          cudaStream_t st);
+// row a5: g[p][l] = sum_n w_n phi_win(v_n - l) over the x projections (ES window, w taps)
+cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int n, int wt, float beta, int W,
+                          float* grid, cudaStream_t st);
+// row a6: h[p] = IFFT_n(D[p] * FFT_n(g[p]))   (unnormalised, one CTA per slice, smem radix-2)
+cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, cudaStream_t st);
+
+// rows a4 + a7 (+ Laplacian moment term) + slice accumulation:
+//   per y_m: acc = sum_p [ sort_coef * S_sort + Fourier interp + mom_coef * tau_p * S_moment ]
+//   s64[m] += acc   (per_slice_out == nullptr)   or   per_slice_out[p*M + m] = t_{m,p}
+struct EvalArgs {
+  ZView zv;
+  int np;
+  // sort part
+  bool sort;
+  int nb;
+  const float2* xs;
+  const int* off;
+  const double* tab;
+  const float* bpar;
+  double sort_coef;   // t += -sort_coef * sum_n w_n |z_n - z_m|
+  // Fourier part
+  bool fourier;
+  const FPar* fp;
+  const float* h;
+  int n, wt;
+  float beta;
+  // Laplacian moment part: t += mom_coef * tau_p * sum_n w_n (z_n - z_m)^2
+  bool moment;
+  double mom_coef;
+  // outputs
+  double* s64;
+  float* per_slice_out;
+};
+cudaError_t launch_eval(const EvalArgs& a, cudaStream_t st);
+cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t st);
+cudaError_t launch_finalize(const double* s64, int64_t M, double scale, float* s, cudaStream_t st);
+
+}  // namespace sks

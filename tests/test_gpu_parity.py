@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU fp64 oracle (-m gpu).
+
+Metric (BASELINE.json north_star): max|s_gpu - s_oracle| / sum|w_n| against oracle (b), the sliced
+estimator on the same seeded directions with direct 1D sums.  Tolerances (north_star, R15):
+1e-5 for the sorting path (negdist), 1e-4 for the Fourier paths (Gaussian, Matern) and the
+combined Laplacian path.  Sizes: small cases the oracle finishes in seconds spanning several tiles
+and ragged tails, plus BASELINE.json's full sizes on sampled targets.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2401_08260_b200 import inputs as I
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2401_08260_b200 as S  # noqa: E402
+
+TOL = {"negdist": 1e-5, "gaussian": 1e-4, "matern": 1e-4, "laplacian": 1e-4}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    from paper_2401_08260_b200 import build
+    build.build()
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def rel_err(got, ref, w):
+    return float(np.max(np.abs(np.asarray(got, np.float64) - ref)) / np.abs(w.astype(np.float64)).sum())
+
+
+# ---------------------------------------------------------------- a1: projection
+@pytest.mark.parametrize("n,d,P", [(1, 3, 1), (300, 3, 64), (1000, 50, 70), (257, 784, 33), (129, 3072, 17)])
+def test_projection_parity(n, d, P):
+    rng = np.random.default_rng(n + d)
+    pts = rng.uniform(-1, 1, (n, d)).astype(np.float32)
+    z = S.sks_project(dev(pts), P, seed=7).cpu().numpy()
+    zo = O.project(pts, O.unit_directions(P, d, 7))
+    scale = np.linalg.norm(pts.astype(np.float64), axis=1).max()
+    assert np.max(np.abs(z - zo)) <= 2e-6 * scale * max(1.0, np.sqrt(d / 50)), np.max(np.abs(z - zo))
+
+
+# ---------------------------------------------------------------- a2-a7: the 1D engines on given projections
+CASES_1D = [
+    # kind, scale, d, N, M, S
+    ("negdist", 0.0, 50, 3001, 1537, 5),
+    ("negdist", 0.0, 3, 1, 1, 2),
+    ("negdist", 0.0, 3, 70000, 333, 2),
+    ("gaussian", 1.0, 3, 2003, 1001, 4),
+    ("gaussian", 11.0, 784, 4097, 515, 3),
+    ("gaussian", 30.0, 100, 5000, 700, 3),
+    ("laplacian", 22.6, 3072, 3001, 517, 3),
+    ("laplacian", 2.0, 50, 2500, 600, 3),
+    ("matern", 1.0, 50, 3000, 600, 3),
+    ("matern", 1.0, 3, 1500, 400, 2),
+]
+
+
+@pytest.mark.parametrize("kind,scale,d,N,M,nsl", CASES_1D)
+def test_sum_1d_parity(kind, scale, d, N, M, nsl):
+    rng = np.random.default_rng(N + M + d)
+    spread = {3: 1.0, 50: 1.0, 100: 2.2, 784: 0.28, 3072: 0.29}[d]
+    zx = (spread * rng.standard_normal((nsl, N))).astype(np.float32)
+    zy = (spread * rng.standard_normal((nsl, M)) + 0.1).astype(np.float32)
+    w = rng.uniform(-1, 1, N).astype(np.float32)
+    t = S.sks_sum_1d(dev(zx), dev(zy), dev(w), d, kind, scale if scale else 1.0).cpu().numpy()
+    for q in range(nsl):
+        ref = O.sum_1d(kind, scale, d, zx[q].astype(np.float64), w.astype(np.float64), zy[q].astype(np.float64))
+        err = rel_err(t[q], ref, w)
+        assert err <= TOL[kind], (q, err)
+
+
+def test_sum_1d_degenerate_identical_points():
+    # all sources at one point (zero range) and targets on top of it / away from it
+    N, M = 1000, 300
+    zx = np.full((2, N), 0.75, np.float32)
+    zy = np.concatenate([np.full((2, 100), 0.75), np.linspace(-2, 3, 200)[None].repeat(2, 0)], 1).astype(np.float32)
+    w = np.random.default_rng(0).random(N).astype(np.float32)
+    for kind, scale, d in [("negdist", 1.0, 5), ("gaussian", 1.0, 5), ("laplacian", 1.0, 5)]:
+        t = S.sks_sum_1d(dev(zx), dev(zy), dev(w), d, kind, scale).cpu().numpy()
+        for q in range(2):
+            ref = O.sum_1d(kind, scale if kind != "negdist" else 0.0, d, zx[q].astype(np.float64),
+                           w.astype(np.float64), zy[q].astype(np.float64))
+            assert rel_err(t[q], ref, w) <= TOL[kind], kind
+
+
+# ---------------------------------------------------------------- end to end (Alg. 1) vs oracle (b)
+def run_cfg(cfg, n_tgt=None, p0=0, p1=None, **opts):
+    x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
+    param = I.kernel_param(cfg)
+    s = S.sks_sum(dev(x), dev(y), dev(w), cfg.kind, param if cfg.kind != "negdist" else 1.0, cfg.P, cfg.dir_seed,
+                  p_begin=p0, p_end=p1, matern_p=cfg.matern_p, **opts).cpu().numpy()
+    tgt = I.target_subset(cfg.M, n_tgt) if n_tgt else np.arange(cfg.M)
+    ref = O.sliced_sum(cfg.kind, param if cfg.kind != "negdist" else 0.0, x, y, w, cfg.P, cfg.dir_seed, targets=tgt,
+                       p0=p0, p1=p1, matern_p=cfg.matern_p)
+    return s, s[tgt], ref, w, (x, y, param, tgt)
+
+
+SMALL = [
+    ("cfg1", {}),                                               # full BASELINE configs[0]
+    ("cfg2", dict(N=20000, M=4000, P=24)),
+    ("cfg3", dict(N=6000, M=1200, P=16)),
+    ("cfg4", dict(N=4000, M=800, P=8)),
+    ("cfg5", dict(N=30000, M=2000, P=16)),
+    ("paper_gauss", dict(N=3000, M=1000, P=32)),
+    ("paper_matern", dict(N=3000, M=1000, P=32)),
+    ("paper_negdist", dict(N=3000, M=1000, P=32)),
+    ("paper_laplace", dict(N=3000, M=1000, P=32)),
+]
+
+
+@pytest.mark.parametrize("name,size", SMALL, ids=[s[0] for s in SMALL])
+def test_end_to_end_small(name, size):
+    cfg = I.scaled(I.CONFIGS[name], **size) if size else I.CONFIGS[name]
+    _, got, ref, w, _ = run_cfg(cfg, n_tgt=min(cfg.M, 400))
+    err = rel_err(got, ref, w)
+    print(f"{name}: max|ds|/sum|w| = {err:.3e}  plan={S.sks_last_plan()}")
+    assert err <= TOL[cfg.kind], err
+
+
+def test_slice_ranges_add_up():
+    # the multi-GPU contract: partial ranges sum (one all-reduce) to the full estimate (north_star)
+    cfg = I.scaled(I.CONFIGS["cfg2"], N=5000, M=1000, P=32)
+    full = run_cfg(cfg, n_tgt=50)[0]
+    a = run_cfg(cfg, n_tgt=50, p0=0, p1=12)[0]
+    b = run_cfg(cfg, n_tgt=50, p0=12, p1=32)[0]
+    w = I.weights(cfg)
+    assert rel_err(a + b, full.astype(np.float64), w) <= 1e-6
+    cfg = I.scaled(I.CONFIGS["cfg3"], N=3000, M=500, P=8)
+    full = run_cfg(cfg, n_tgt=50)[0]
+    parts = sum(run_cfg(cfg, n_tgt=50, p0=q, p1=q + 2)[0].astype(np.float64) for q in range(0, 8, 2))
+    assert rel_err(parts, full.astype(np.float64), I.weights(cfg)) <= 1e-6
+
+
+def test_slice_batching_invariance():
+    cfg = I.scaled(I.CONFIGS["paper_laplace"], N=2000, M=500, P=20)
+    a = run_cfg(cfg, n_tgt=20)[0]
+    b = run_cfg(cfg, n_tgt=20, slice_batch=7)[0]
+    assert rel_err(a, b.astype(np.float64), I.weights(cfg)) <= 1e-6
+
+
+def test_host_entry_point_matches_device():
+    cfg = I.scaled(I.CONFIGS["cfg2"], N=3000, M=700, P=16)
+    x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
+    s_dev = S.sks_sum(dev(x), dev(y), dev(w), "negdist", 1.0, cfg.P, cfg.dir_seed).cpu().numpy()
+    s_host = S.sks_sum_host(x, y, w, "negdist", 1.0, cfg.P, cfg.dir_seed)
+    assert rel_err(s_host, s_dev.astype(np.float64), w) <= 1e-6
+
+
+def test_errors_fail_loudly():
+    x = torch.randn(100, 4, device="cuda")
+    y = torch.randn(30, 4, device="cuda")
+    w = torch.rand(100, device="cuda")
+    x[5, 1] = float("nan")
+    for kind in ("negdist", "gaussian"):
+        with pytest.raises(S.SKSError) as e:
+            S.sks_sum(x, y, w, kind, 1.0, 8, 1)
+        assert e.value.status == 5
+    ws = torch.empty(256, dtype=torch.uint8, device="cuda")
+    with pytest.raises(S.SKSError) as e:
+        S.sks_sum(torch.randn(100, 4, device="cuda"), y, w, "negdist", 1.0, 8, 1, workspace=ws)
+    assert e.value.status == 4
+
+
+# ---------------------------------------------------------------- BASELINE.json full sizes, sampled targets
+FULL = [("cfg2", 48), ("cfg3", 12), ("cfg4", 10)]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,n_tgt", FULL, ids=[f[0] for f in FULL])
+def test_full_size_sampled(name, n_tgt):
+    cfg = I.CONFIGS[name]
+    _, got, ref, w, _ = run_cfg(cfg, n_tgt=n_tgt)
+    err = rel_err(got, ref, w)
+    print(f"{name} FULL: max|ds|/sum|w| = {err:.3e}  plan={S.sks_last_plan()}")
+    assert err <= TOL[cfg.kind], err
+
+
+@pytest.mark.slow
+def test_cfg5_slice_subset_sampled():
+    # cfg5 at full N=M=1e7 on one GPU for a 2-slice sub-range of each of the 8 ranks' ranges
+    cfg = I.CONFIGS["cfg5"]
+    x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
+    param = I.kernel_param(cfg)
+    xd, yd, wd = dev(x), dev(y), dev(w)
+    tgt = I.target_subset(cfg.M, 8)
+    for rank in (0, 7):
+        p0 = rank * cfg.P // 8
+        s = S.sks_sum(xd, yd, wd, "gaussian", param, cfg.P, cfg.dir_seed, p_begin=p0, p_end=p0 + 2).cpu().numpy()
+        ref = O.sliced_sum("gaussian", param, x, y, w, cfg.P, cfg.dir_seed, targets=tgt, p0=p0, p1=p0 + 2)
+        # the 2-slice partial is (1/P) * sum of 2 slices: compare on the per-slice-mean scale
+        err = rel_err(s[tgt] * cfg.P / 2, ref * cfg.P / 2, w)
+        assert err <= TOL["gaussian"], err
