@@ -57,8 +57,9 @@ CASES_1D = [
     ("gaussian", 30.0, 100, 5000, 700, 3),
     ("laplacian", 22.6, 3072, 3001, 517, 3),
     ("laplacian", 2.0, 50, 2500, 600, 3),
-    ("matern", 1.0, 50, 3000, 600, 3),
-    ("matern", 1.0, 3, 1500, 400, 2),
+    ("matern", 8.0, 50, 3000, 600, 3),    # beta large enough that the oracle's 1F2 series stays well
+    ("matern", 3.0, 3, 1500, 400, 2),     # conditioned over the test's |dz| range
+    ("matern", 5.0, 10, 2000, 300, 2),
 ]
 
 
