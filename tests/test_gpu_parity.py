@@ -66,7 +66,7 @@ CASES_1D = [
 @pytest.mark.parametrize("kind,scale,d,N,M,nsl", CASES_1D)
 def test_sum_1d_parity(kind, scale, d, N, M, nsl):
     rng = np.random.default_rng(N + M + d)
-    spread = {3: 1.0, 50: 1.0, 100: 2.2, 784: 0.28, 3072: 0.29}[d]
+    spread = {3: 1.0, 10: 1.0, 50: 1.0, 100: 2.2, 784: 0.28, 3072: 0.29}[d]
     zx = (spread * rng.standard_normal((nsl, N))).astype(np.float32)
     zy = (spread * rng.standard_normal((nsl, M)) + 0.1).astype(np.float32)
     w = rng.uniform(-1, 1, N).astype(np.float32)
