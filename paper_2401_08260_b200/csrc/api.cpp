@@ -124,7 +124,7 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, mm = 0, xs = 0, off = 0, tab = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
+  size_t Z = 0, mm = 0, xs = 0, rec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
          flag = 0, total = 0;
 };
 
@@ -142,8 +142,8 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb)
   if (with_Z) L.Z = take(sizeof(float) * (N + M) * nbat);
   if (pt.sort || pt.moment) {
     L.xs = take(sizeof(float2) * N * nbat);
-    L.off = take(sizeof(int) * (nb + 1) * static_cast<size_t>(nbat));
-    L.tab = take(sizeof(double) * 3 * (nb + 1) * static_cast<size_t>(nbat));
+    L.rec = take(sizeof(sks::BucketRec) * nb * static_cast<size_t>(nbat));
+    L.tot = take(sizeof(sks::SliceTot) * static_cast<size_t>(nbat));
     L.bpar = take(sizeof(float) * 2 * nbat);
   }
   if (pt.fourier) {
@@ -372,13 +372,14 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     if (pt.sort || pt.moment) {
       ProfScope ps(PS_BUCKET, st);
       SKS_CUDA(sks::launch_bucket_build(zv, w, nbat, nb, mm, reinterpret_cast<float2*>(ws + L.xs),
-                                        reinterpret_cast<int*>(ws + L.off), reinterpret_cast<double*>(ws + L.tab),
+                                        reinterpret_cast<sks::BucketRec*>(ws + L.rec),
+                                        reinterpret_cast<sks::SliceTot*>(ws + L.tot),
                                         reinterpret_cast<float*>(ws + L.bpar), st));
       ++launches;
       ea.nb = nb;
       ea.xs = reinterpret_cast<const float2*>(ws + L.xs);
-      ea.off = reinterpret_cast<const int*>(ws + L.off);
-      ea.tab = reinterpret_cast<const double*>(ws + L.tab);
+      ea.rec = reinterpret_cast<const sks::BucketRec*>(ws + L.rec);
+      ea.tot = reinterpret_cast<const sks::SliceTot*>(ws + L.tot);
       ea.bpar = reinterpret_cast<const float*>(ws + L.bpar);
     }
     if (pt.sort) {

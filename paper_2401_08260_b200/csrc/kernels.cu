@@ -193,11 +193,14 @@ cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_
 }
 
 // ------------------------------------------------------------------ a3/a4: counting sort + fp64 prefix sums
-// One CTA (1024 threads) per slice.  smem: nb int counters.
-//  1. count x projections per bucket (smem atomics)      2. exclusive scan -> bucket offsets
-//  3. scatter (z, w) into bucket order (smem cursors)    4. fp64 bucket sums (A=sum w, B=sum wz, C=sum wz^2)
-//  5. exclusive fp64 scan over buckets -> tab[p][b] = sums over buckets < b; tab[p][nb] = totals
-constexpr int BK_THREADS = 1024;
+// One CTA (512 threads, 2 CTAs/SM) per slice; smem: nb int counters/cursors.
+//  P0 zero the bucket sums            P1 count x projections per bucket (smem atomics)
+//  P2 exclusive scan -> cursors       P3 scatter (z, w) into bucket order (smem cursors)
+//  P4 bucket sums over the bucket-ordered array: coalesced, warp-segmented by bucket id, fp64, one
+//     global fp64 atomic per (warp-iteration, bucket) segment; slice totals (A, B, C)
+//  P5 exclusive fp64 scan over buckets -> 32-byte records {A_excl, B_excl, off, cnt, w_b, wz_b}
+constexpr int BK_THREADS = 512;
+constexpr int BK_WARPS = BK_THREADS / 32;
 
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
@@ -210,107 +213,153 @@ __device__ __forceinline__ T warp_incl_scan(T v) {
   return v;
 }
 
-__global__ void __launch_bounds__(BK_THREADS) k_bucket_build(ZView zv, const float* __restrict__ w, int nb,
-                                                             const unsigned* __restrict__ mm, float2* __restrict__ xs,
-                                                             int* __restrict__ off, double* __restrict__ tab,
-                                                             float* __restrict__ bpar) {
-  extern __shared__ int cnt[];
-  __shared__ int wsum_i[32];
-  __shared__ double wsum_d[3][32];
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(BK_THREADS, 2) k_bucket_build(ZView zv, const float* __restrict__ w, int nb,
+                                                                const unsigned* __restrict__ mm,
+                                                                float2* __restrict__ xs, BucketRec* __restrict__ rec,
+                                                                SliceTot* __restrict__ tot, float* __restrict__ bpar) {
+  extern __shared__ int cur[];
+  __shared__ int wsum_i[BK_WARPS];
+  __shared__ double wsum_d[3][BK_WARPS];
   const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t N = zv.N;
   const float* zx = zv.zx + p * zv.ldx;
   const float zmin = key2f(mm[p * 4 + 0]), zmax = key2f(mm[p * 4 + 1]);
   const float range = zmax - zmin;
   const float scale = (range > 0.f) ? static_cast<float>(nb) / range : 0.f;
+  BucketRec* rp = rec + static_cast<int64_t>(p) * nb;
+  float2* xsp = xs + static_cast<int64_t>(p) * N;
   if (tid == 0) { bpar[p * 2 + 0] = zmin; bpar[p * 2 + 1] = scale; }
-  for (int b = tid; b < nb; b += BK_THREADS) cnt[b] = 0;
+  // P0
+  for (int b = tid; b < nb; b += BK_THREADS) {
+    cur[b] = 0;
+    reinterpret_cast<double2*>(rp + b)[0] = make_double2(0.0, 0.0);
+  }
   __syncthreads();
-  for (int64_t i = tid; i < N; i += BK_THREADS) atomicAdd(&cnt[bucket_of(zx[i], zmin, scale, nb)], 1);
+  // P1
+  for (int64_t i = tid; i < N; i += BK_THREADS) atomicAdd(&cur[bucket_of(__ldg(zx + i), zmin, scale, nb)], 1);
   __syncthreads();
-  // exclusive scan of cnt (E = nb / 1024 consecutive entries per thread)
+  // P2: exclusive scan (E consecutive counters per thread)
   const int E = nb / BK_THREADS;
   const int b0 = tid * E;
-  int loc = 0;
-  for (int e = 0; e < E; ++e) loc += cnt[b0 + e];
-  int inc = warp_incl_scan(loc);
-  if (lane == 31) wsum_i[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    int v = wsum_i[lane];
-    int vi = warp_incl_scan(v);
-    wsum_i[lane] = vi - v;
-  }
-  __syncthreads();
-  int run = wsum_i[wid] + inc - loc;
-  int* offp = off + static_cast<int64_t>(p) * (nb + 1);
-  for (int e = 0; e < E; ++e) {
-    const int c = cnt[b0 + e];
-    cnt[b0 + e] = run;
-    offp[b0 + e] = run;
-    run += c;
-  }
-  if (tid == BK_THREADS - 1) offp[nb] = run;   // == N
-  __syncthreads();
-  // scatter into bucket order (order inside a bucket is irrelevant: those terms are summed directly)
-  float2* xsp = xs + static_cast<int64_t>(p) * N;
-  for (int64_t i = tid; i < N; i += BK_THREADS) {
-    const float z = zx[i];
-    const int pos = atomicAdd(&cnt[bucket_of(z, zmin, scale, nb)], 1);
-    xsp[pos] = make_float2(z, w[i]);
-  }
-  __syncthreads();
-  // fp64 sums over this thread's buckets
-  double A = 0.0, B = 0.0, C = 0.0;
   {
-    const int lo = offp[b0], hi = offp[b0 + E];
-    for (int j = lo; j < hi; ++j) {
-      const float2 e = xsp[j];
-      const double wz = static_cast<double>(e.y) * e.x;
-      A += e.y;
-      B += wz;
-      C += wz * e.x;
+    int loc = 0;
+    for (int e = 0; e < E; ++e) loc += cur[b0 + e];
+    const int inc = warp_incl_scan(loc);
+    if (lane == 31) wsum_i[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      const int v = lane < BK_WARPS ? wsum_i[lane] : 0;
+      const int vi = warp_incl_scan(v);
+      if (lane < BK_WARPS) wsum_i[lane] = vi - v;
+    }
+    __syncthreads();
+    int run = wsum_i[wid] + inc - loc;
+    for (int e = 0; e < E; ++e) {
+      const int c = cur[b0 + e];
+      cur[b0 + e] = run;
+      run += c;
     }
   }
-  double iA = warp_incl_scan(A), iB = warp_incl_scan(B), iC = warp_incl_scan(C);
-  if (lane == 31) { wsum_d[0][wid] = iA; wsum_d[1][wid] = iB; wsum_d[2][wid] = iC; }
   __syncthreads();
-  if (wid == 0) {
-    double a = wsum_d[0][lane], b = wsum_d[1][lane], c = wsum_d[2][lane];
-    double ia = warp_incl_scan(a), ib = warp_incl_scan(b), ic = warp_incl_scan(c);
-    wsum_d[0][lane] = ia - a;
-    wsum_d[1][lane] = ib - b;
-    wsum_d[2][lane] = ic - c;
+  // P3: scatter; afterwards cur[b] = end of bucket b = start of bucket b+1
+  for (int64_t i = tid; i < N; i += BK_THREADS) {
+    const float z = __ldg(zx + i);
+    const int pos = atomicAdd(&cur[bucket_of(z, zmin, scale, nb)], 1);
+    xsp[pos] = make_float2(z, __ldg(w + i));
   }
   __syncthreads();
-  double rA = wsum_d[0][wid] + iA - A, rB = wsum_d[1][wid] + iB - B, rC = wsum_d[2][wid] + iC - C;
-  double* tp = tab + static_cast<int64_t>(p) * (nb + 1) * 3;
-  for (int e = 0; e < E; ++e) {
-    const int b = b0 + e;
-    tp[b * 3 + 0] = rA;
-    tp[b * 3 + 1] = rB;
-    tp[b * 3 + 2] = rC;
-    const int lo = offp[b], hi = offp[b + 1];
-    for (int j = lo; j < hi; ++j) {
-      const float2 q = xsp[j];
-      const double wz = static_cast<double>(q.y) * q.x;
-      rA += q.y;
-      rB += wz;
-      rC += wz * q.x;
+  // P4: warp-segmented fp64 bucket sums over xs (bucket ids are non-decreasing along xs)
+  double tA = 0.0, tB = 0.0, tC = 0.0;
+  {
+    const int64_t per = (N + BK_WARPS - 1) / BK_WARPS;
+    const int64_t s0 = min(N, wid * per), s1 = min(N, s0 + per);
+    for (int64_t base = s0; base < s1; base += 32) {
+      const int64_t i = base + lane;
+      const bool valid = i < s1;
+      float2 e = valid ? xsp[i] : make_float2(0.f, 0.f);
+      const int key = valid ? bucket_of(e.x, zmin, scale, nb) : -1 - lane;   // invalid lanes: unique keys
+      double a = e.y, bz = static_cast<double>(e.y) * e.x;
+      tA += a;
+      tB += bz;
+      tC += bz * e.x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double na = __shfl_up_sync(0xffffffffu, a, o), nbz = __shfl_up_sync(0xffffffffu, bz, o);
+        const int nk = __shfl_up_sync(0xffffffffu, key, o);
+        // keys are sorted, so equal key o lanes back means the whole run in between shares it
+        if (lane >= o && nk == key) { a += na; bz += nbz; }
+      }
+      const int next = __shfl_down_sync(0xffffffffu, key, 1);
+      const bool seg_end = valid && (lane == 31 || next != key);
+      if (seg_end) {
+        atomicAdd(&rp[key].A, a);
+        atomicAdd(&rp[key].B, bz);
+      }
     }
   }
-  if (tid == BK_THREADS - 1) { tp[nb * 3 + 0] = rA; tp[nb * 3 + 1] = rB; tp[nb * 3 + 2] = rC; }
+  tA = warp_sum(tA);
+  tB = warp_sum(tB);
+  tC = warp_sum(tC);
+  if (lane == 0) { wsum_d[0][wid] = tA; wsum_d[1][wid] = tB; wsum_d[2][wid] = tC; }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0, b = 0, c = 0;
+    for (int q = 0; q < BK_WARPS; ++q) { a += wsum_d[0][q]; b += wsum_d[1][q]; c += wsum_d[2][q]; }
+    tot[p] = SliceTot{a, b, c, 0.0};
+  }
+  __syncthreads();
+  // P5: exclusive fp64 scan over buckets, write the records
+  {
+    double lA = 0.0, lB = 0.0;
+    for (int e = 0; e < E; ++e) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + b0 + e));
+      lA += v.x;
+      lB += v.y;
+    }
+    const double iA = warp_incl_scan(lA), iB = warp_incl_scan(lB);
+    if (lane == 31) { wsum_d[0][wid] = iA; wsum_d[1][wid] = iB; }
+    __syncthreads();
+    if (wid == 0) {
+      const double a = lane < BK_WARPS ? wsum_d[0][lane] : 0.0, b = lane < BK_WARPS ? wsum_d[1][lane] : 0.0;
+      const double ia = warp_incl_scan(a), ib = warp_incl_scan(b);
+      if (lane < BK_WARPS) { wsum_d[0][lane] = ia - a; wsum_d[1][lane] = ib - b; }
+    }
+    __syncthreads();
+    double rA = wsum_d[0][wid] + iA - lA, rB = wsum_d[1][wid] + iB - lB;
+    for (int e = 0; e < E; ++e) {
+      const int b = b0 + e;
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + b));
+      const int off = (b == 0) ? 0 : cur[b - 1];
+      BucketRec r;
+      r.A = rA;
+      r.B = rB;
+      r.off = off;
+      r.cnt = cur[b] - off;
+      r.w = static_cast<float>(v.x);
+      r.wz = static_cast<float>(v.y);
+      rp[b] = r;
+      rA += v.x;
+      rB += v.y;
+    }
+  }
 }
 
-cudaError_t launch_bucket_build(ZView zv, const float* w, int np, int nb, const unsigned* mm, float2* xs, int* off,
-                                double* tab, float* bpar, cudaStream_t st) {
+cudaError_t launch_bucket_build(ZView zv, const float* w, int np, int nb, const unsigned* mm, float2* xs,
+                                BucketRec* rec, SliceTot* tot, float* bpar, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(nb) * sizeof(int);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_bucket_build, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4);
     attr_set = true;
   }
-  k_bucket_build<<<np, BK_THREADS, smem, st>>>(zv, w, nb, mm, xs, off, tab, bpar);
+  k_bucket_build<<<np, BK_THREADS, smem, st>>>(zv, w, nb, mm, xs, rec, tot, bpar);
   return cudaGetLastError();
 }
 
@@ -525,64 +574,65 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, 
 }
 
 // ------------------------------------------------------------------ a4 + a7: evaluation at the targets
-__global__ void __launch_bounds__(256) k_eval(EvalArgs a) {
+// grid (target blocks, slice groups): each thread handles one target over EV_SG slices, then one fp64
+// atomic into s64 (or per-slice stores for sks_sum_1d).  Target blocks vary fastest, so the CTAs resident
+// at a time work on the same slice group and its bucket records / grids stay in L2.
+constexpr int EV_THREADS = 256, EV_SG = 8;
+
+__global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
   const int64_t M = a.zv.M;
+  const int64_t m = blockIdx.x * static_cast<int64_t>(EV_THREADS) + threadIdx.x;
+  if (m >= M) return;
+  const int p0 = blockIdx.y * EV_SG, p1 = min(a.np, p0 + EV_SG);
   const float nf = static_cast<float>(a.n), hw = 0.5f * a.wt, inv_hw = 2.0f / a.wt;
-  for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < M;
-       m += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double acc = 0.0;
-    for (int p = 0; p < a.np; ++p) {
-      const float z = a.zv.zy[p * a.zv.ldy + m];
-      const double zd = z;
-      double t = 0.0;
-      if (a.sort || a.moment) {
-        const double* tp = a.tab + static_cast<int64_t>(p) * (a.nb + 1) * 3;
-        const double Atot = tp[a.nb * 3 + 0], Btot = tp[a.nb * 3 + 1];
-        if (a.sort) {
-          const int b = bucket_of(z, a.bpar[p * 2 + 0], a.bpar[p * 2 + 1], a.nb);
-          const int* op = a.off + static_cast<int64_t>(p) * (a.nb + 1);
-          const int lo = op[b], hi = op[b + 1];
-          const double Alo = tp[b * 3 + 0], Blo = tp[b * 3 + 1];
-          const double Ahi = Atot - tp[(b + 1) * 3 + 0], Bhi = Btot - tp[(b + 1) * 3 + 1];
-          // sum_n w_n |z_n - z| = [z A_lo - B_lo] + [B_hi - z A_hi] + (same-bucket terms, direct)
-          double same = 0.0;
-          const float2* xp = a.xs + static_cast<int64_t>(p) * a.zv.N;
-          for (int j = lo; j < hi; ++j) {
-            const float2 q = xp[j];
-            same += static_cast<double>(q.y) * fabs(static_cast<double>(q.x) - zd);
-          }
-          t -= a.sort_coef * ((zd * Alo - Blo) + (Bhi - zd * Ahi) + same);
+  double acc = 0.0;
+  for (int p = p0; p < p1; ++p) {
+    const float z = __ldg(a.zv.zy + p * a.zv.ldy + m);
+    const double zd = z;
+    double t = 0.0;
+    if (a.sort || a.moment) {
+      const SliceTot T = a.tot[p];
+      if (a.sort) {
+        const int b = bucket_of(z, a.bpar[p * 2 + 0], a.bpar[p * 2 + 1], a.nb);
+        const BucketRec* rp = a.rec + static_cast<int64_t>(p) * a.nb + b;
+        const double2 AB = __ldg(reinterpret_cast<const double2*>(rp));
+        const int4 oc = __ldg(reinterpret_cast<const int4*>(rp) + 1);
+        const float wb = __int_as_float(oc.z), wzb = __int_as_float(oc.w);
+        const double Ahi = T.A - AB.x - wb, Bhi = T.B - AB.y - wzb;
+        // sum_n w_n |z_n - z| = [z A_lo - B_lo] + [B_hi - z A_hi] + (same-bucket terms, summed directly)
+        double same = 0.0;
+        const float2* xp = a.xs + static_cast<int64_t>(p) * a.zv.N + oc.x;
+        for (int j = 0; j < oc.y; ++j) {
+          const float2 q = __ldg(xp + j);
+          same += static_cast<double>(q.y) * fabs(static_cast<double>(q.x) - zd);
         }
-        if (a.moment) {
-          const double Ctot = tp[a.nb * 3 + 2];
-          t += a.mom_coef * static_cast<double>(a.fp[p].tau) * (Ctot - 2.0 * zd * Btot + zd * zd * Atot);
-        }
+        t -= a.sort_coef * ((zd * AB.x - AB.y) + (Bhi - zd * Ahi) + same);
       }
-      if (a.fourier) {
-        const FPar f = a.fp[p];
-        const float v = grid_coord(z, f.cen, f.tau, nf);
-        const int l0 = static_cast<int>(floorf(__fsub_rn(v, hw))) + 1;
-        const float* hp = a.h + static_cast<int64_t>(p) * a.n;
-        float dist = v - static_cast<float>(l0);
-        float tf = 0.f;
-        for (int j = 0; j < a.wt; ++j) {
-          tf += hp[(l0 + j) & (a.n - 1)] * es_window(dist * inv_hw, a.beta);
-          dist -= 1.f;
-        }
-        t += tf;
-      }
-      if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
-      acc += t;
+      if (a.moment) t += a.mom_coef * static_cast<double>(a.fp[p].tau) * (T.C - 2.0 * zd * T.B + zd * zd * T.A);
     }
-    if (a.s64) a.s64[m] += acc;
+    if (a.fourier) {
+      const FPar f = a.fp[p];
+      const float v = grid_coord(z, f.cen, f.tau, nf);
+      const int l0 = static_cast<int>(floorf(__fsub_rn(v, hw))) + 1;
+      const float* hp = a.h + static_cast<int64_t>(p) * a.n;
+      float dist = v - static_cast<float>(l0);
+      float tf = 0.f;
+      for (int j = 0; j < a.wt; ++j) {
+        tf += __ldg(hp + ((l0 + j) & (a.n - 1))) * es_window(dist * inv_hw, a.beta);
+        dist -= 1.f;
+      }
+      t += tf;
+    }
+    if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
+    acc += t;
   }
+  if (a.s64) atomicAdd(a.s64 + m, acc);
 }
 
 cudaError_t launch_eval(const EvalArgs& a, cudaStream_t st) {
-  int64_t blocks = (a.zv.M + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
-  k_eval<<<static_cast<unsigned>(blocks), 256, 0, st>>>(a);
+  const unsigned bx = static_cast<unsigned>((a.zv.M + EV_THREADS - 1) / EV_THREADS);
+  const unsigned by = static_cast<unsigned>((a.np + EV_SG - 1) / EV_SG);
+  k_eval<<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
   return cudaGetLastError();
 }
 

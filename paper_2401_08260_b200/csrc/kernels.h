@@ -40,9 +40,19 @@ cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st);
 void decode_minmax(const unsigned* enc, float* dec, int n);
 
 // rows a3 (+ a4 prefix sums): one-pass MSD counting sort of the x projections into nb buckets per
-// slice, fp64 bucket prefix sums (A = sum w, B = sum w z, C = sum w z^2) -> tab[p][b][3], off[p][b]
-cudaError_t launch_bucket_build(ZView zv, const float* w, int np, int nb, const unsigned* mm, float2* xs, int* off,
-                                double* tab, float* bpar, cudaStream_t st);
+// slice.  One 32-byte record per bucket: exclusive fp64 prefix sums over the buckets to its left
+// (A = sum w, B = sum w z), its slot range [off, off+cnt) in the bucket-ordered (z, w) array xs, and
+// its own sums rounded to fp32.  Slice totals (A, B, C = sum w z^2) in fp64.
+struct BucketRec {
+  double A, B;
+  int off, cnt;
+  float w, wz;
+};
+struct SliceTot {
+  double A, B, C, pad;
+};
+cudaError_t launch_bucket_build(ZView zv, const float* w, int np, int nb, const unsigned* mm, float2* xs,
+                                BucketRec* rec, SliceTot* tot, float* bpar, cudaStream_t st);
 
 // row a2: D[p][k] = c_k(tau_p) / Phi_k^2 on the band of slice p, else 0  (k = 0..n/2)
 cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* phi2inv, int n, float* D,
@@ -63,8 +73,8 @@ struct EvalArgs {
   bool sort;
   int nb;
   const float2* xs;
-  const int* off;
-  const double* tab;
+  const BucketRec* rec;
+  const SliceTot* tot;
   const float* bpar;
   double sort_coef;   // t += -sort_coef * sum_n w_n |z_n - z_m|
   // Fourier part
