@@ -65,21 +65,16 @@ def algorithmic_bytes(slot, cfg, np_local, plan):
     nb = plan.get("n_buckets", 0) or 0
     if slot == "project":
         return 4 * L * d + 4 * L * P + 4 * P * d
-    if slot == "bucket":
-        return 4 * N * P + 8 * N * P + 28 * (nb + 1) * P + 4 * N
+    if slot == "sortsum":   # fused sort path: its scratch (bucketed x/y, records) stays in L2
+        return 4 * (N + M) * P + 4 * N + 16 * M
     if slot == "spread":
         return 4 * N * P + 4 * N + 4 * n * P
     if slot == "fft_filter":
         return 4 * n * P + 4 * (n // 2 + 1) * P + 4 * n * P
     if slot == "plan_D":
         return 4 * (n // 2 + 1) * P
-    if slot == "eval":
-        b = 4 * M * P + 16 * M
-        if nb:
-            b += 8 * N * P + 28 * (nb + 1) * P
-        if n:
-            b += 4 * n * P
-        return b
+    if slot == "eval":       # Fourier interpolation (+ Laplacian moment term)
+        return 4 * M * P + 16 * M + 4 * n * P
     return 0
 
 

@@ -148,7 +148,7 @@ sks_status sks_profile_enable(int32_t enable);
  * recorded events, then resets.  n_slots >= SKS_PROFILE_SLOTS; slot names: sks_profile_names(). */
 #define SKS_PROFILE_SLOTS 8
 sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots);
-/* Comma-separated slot names: "project,minmax,bucket,plan_D,spread,fft_filter,eval,aux". */
+/* Comma-separated slot names: "project,minmax,sortsum,plan_D,spread,fft_filter,eval,aux". */
 const char* sks_profile_names(void);
 
 /* Thread-local message for the last non-OK status ("" if none). */

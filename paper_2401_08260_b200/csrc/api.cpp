@@ -124,7 +124,7 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, mm = 0, xs = 0, rec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
+  size_t Z = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
          flag = 0, total = 0;
 };
 
@@ -142,6 +142,7 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb)
   if (with_Z) L.Z = take(sizeof(float) * (N + M) * nbat);
   if (pt.sort || pt.moment) {
     L.xs = take(sizeof(float2) * N * nbat);
+    L.ys = take(sizeof(float2) * M * nbat);
     L.rec = take(sizeof(sks::BucketRec) * nb * static_cast<size_t>(nbat));
     L.tot = take(sizeof(sks::SliceTot) * static_cast<size_t>(nbat));
     L.bpar = take(sizeof(float) * 2 * nbat);
@@ -369,23 +370,28 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     sks::EvalArgs ea{};
     ea.zv = zv;
     ea.np = nbat;
-    if (pt.sort || pt.moment) {
-      ProfScope ps(PS_BUCKET, st);
-      SKS_CUDA(sks::launch_bucket_build(zv, w, nbat, nb, mm, reinterpret_cast<float2*>(ws + L.xs),
-                                        reinterpret_cast<sks::BucketRec*>(ws + L.rec),
-                                        reinterpret_cast<sks::SliceTot*>(ws + L.tot),
-                                        reinterpret_cast<float*>(ws + L.bpar), st));
-      ++launches;
-      ea.nb = nb;
-      ea.xs = reinterpret_cast<const float2*>(ws + L.xs);
-      ea.rec = reinterpret_cast<const sks::BucketRec*>(ws + L.rec);
-      ea.tot = reinterpret_cast<const sks::SliceTot*>(ws + L.tot);
-      ea.bpar = reinterpret_cast<const float*>(ws + L.bpar);
-    }
+    double* s64 = s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr;
+    float* tps = t_out ? t_out + static_cast<int64_t>(b0) * pr.M : nullptr;
     if (pt.sort) {
-      ea.sort = true;
       // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)
-      ea.sort_coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
+      sks::SortArgs sa{};
+      sa.zv = zv;
+      sa.w = w;
+      sa.np = nbat;
+      sa.nb = nb;
+      sa.mm = mm;
+      sa.xs = reinterpret_cast<float2*>(ws + L.xs);
+      sa.ys = reinterpret_cast<float2*>(ws + L.ys);
+      sa.rec = reinterpret_cast<sks::BucketRec*>(ws + L.rec);
+      sa.tot = reinterpret_cast<sks::SliceTot*>(ws + L.tot);
+      sa.bpar = reinterpret_cast<float*>(ws + L.bpar);
+      sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
+      sa.s64 = s64;
+      sa.per_slice_out = tps;
+      ProfScope ps(PS_BUCKET, st);
+      SKS_CUDA(sks::launch_sortsum(sa, st));
+      ++launches;
+      ea.tot = sa.tot;
     }
     if (pt.fourier) {
       sks_status s = fourier_batch(pr.k, pr.d, o, zv, w, nbat, ws, L, st, &plan, &launches);
@@ -407,13 +413,14 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ea.moment = true;
       ea.mom_coef = cdd / pr.k.scale;   // + alpha c_d tau sum_n w_n (z_n - z_m)^2   (R7)
     }
-    ea.s64 = s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr;
-    ea.per_slice_out = t_out ? t_out + static_cast<int64_t>(b0) * pr.M : nullptr;
-    {
+    ea.s64 = s64;
+    ea.per_slice_out = tps;
+    ea.accumulate_out = pt.sort;
+    if (pt.fourier || pt.moment) {
       ProfScope ps(PS_EVAL, st);
       SKS_CUDA(sks::launch_eval(ea, st));
+      ++launches;
     }
-    ++launches;
   }
   if (s_out) {
     ProfScope ps(PS_AUX, st);
@@ -478,7 +485,7 @@ sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots) {
   return SKS_OK;
 }
 
-const char* sks_profile_names(void) { return "project,minmax,bucket,plan_D,spread,fft_filter,eval,aux"; }
+const char* sks_profile_names(void) { return "project,minmax,sortsum,plan_D,spread,fft_filter,eval,aux"; }
 
 sks_status sks_last_plan(sks_plan_info* info) {
   if (!info) return fail(SKS_ERR_INVALID, "info is NULL");

@@ -192,15 +192,19 @@ cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ a3/a4: counting sort + fp64 prefix sums
-// One CTA (512 threads, 2 CTAs/SM) per slice; smem: nb int counters/cursors.
-//  P0 zero the bucket sums            P1 count x projections per bucket (smem atomics)
-//  P2 exclusive scan -> cursors       P3 scatter (z, w) into bucket order (smem cursors)
-//  P4 bucket sums over the bucket-ordered array: coalesced, warp-segmented by bucket id, fp64, one
-//     global fp64 atomic per (warp-iteration, bucket) segment; slice totals (A, B, C)
-//  P5 exclusive fp64 scan over buckets -> 32-byte records {A_excl, B_excl, off, cnt, w_b, wz_b}
-constexpr int BK_THREADS = 512;
-constexpr int BK_WARPS = BK_THREADS / 32;
+// ------------------------------------------------------------------ a3/a4: fused sort path (one CTA per slice)
+// Sec. 3.2 / Alg. 2 as a one-pass MSD counting sort of BOTH point sets into nb monotone buckets
+// of the slice's x range, fp64 prefix sums over the x buckets, and a bucket-ordered evaluation of the
+// targets:  sum_n w_n |x_n - z| = [z A_lo - B_lo] + [B_hi - z A_hi] + sum_{x in z's bucket} w |x - z|.
+//  P0 zero counters and bucket sums        P1 count x and y per bucket (smem atomics)
+//  P2 exclusive scans -> cursors           P3 scatter (z,w) -> xs, (z,m) -> ys in bucket order
+//  P4 warp-segmented fp64 bucket sums of x (coalesced; one fp64 atomic per segment) + slice totals
+//  P5 exclusive fp64 scan -> 32-byte records {A_excl, B_excl, off, cnt, w_b, wz_b}
+//  P6 targets in bucket order: lanes of a warp share buckets (broadcast loads of the bucket's x's);
+//     t_{m,p} -> fp64 atomic into s64[m] (or per-slice output)
+// All scratch (xs, ys, records) is written and re-read by the same CTA: it stays in L2.
+constexpr int SS_THREADS = 1024;
+constexpr int SS_WARPS = SS_THREADS / 32;
 
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
@@ -220,87 +224,99 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-__global__ void __launch_bounds__(BK_THREADS, 2) k_bucket_build(ZView zv, const float* __restrict__ w, int nb,
-                                                                const unsigned* __restrict__ mm,
-                                                                float2* __restrict__ xs, BucketRec* __restrict__ rec,
-                                                                SliceTot* __restrict__ tot, float* __restrict__ bpar) {
-  extern __shared__ int cur[];
-  __shared__ int wsum_i[BK_WARPS];
-  __shared__ double wsum_d[3][BK_WARPS];
+// block-wide exclusive scan of E consecutive ints per thread, in place; returns nothing
+__device__ __forceinline__ void block_excl_scan_int(int* a, int E, int* wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int b0 = tid * E;
+  int loc = 0;
+  for (int e = 0; e < E; ++e) loc += a[b0 + e];
+  const int inc = warp_incl_scan(loc);
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const int v = lane < SS_WARPS ? wsum[lane] : 0;
+    const int vi = warp_incl_scan(v);
+    if (lane < SS_WARPS) wsum[lane] = vi - v;
+  }
+  __syncthreads();
+  int run = wsum[wid] + inc - loc;
+  for (int e = 0; e < E; ++e) {
+    const int c = a[b0 + e];
+    a[b0 + e] = run;
+    run += c;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(SS_THREADS, 1) k_sortsum(SortArgs a) {
+  extern __shared__ int smem_i[];
+  int* cx = smem_i;            // [nb] x counters -> cursors -> bucket ends
+  int* cy = smem_i + a.nb;     // [nb] y counters -> cursors -> bucket ends
+  __shared__ int wsum_i[SS_WARPS];
+  __shared__ double wsum_d[3][SS_WARPS];
+  const int nb = a.nb;
   const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t N = zv.N;
-  const float* zx = zv.zx + p * zv.ldx;
-  const float zmin = key2f(mm[p * 4 + 0]), zmax = key2f(mm[p * 4 + 1]);
+  const int64_t N = a.zv.N, M = a.zv.M;
+  const float* zx = a.zv.zx + p * a.zv.ldx;
+  const float* zy = a.zv.zy + p * a.zv.ldy;
+  const float zmin = key2f(a.mm[p * 4 + 0]), zmax = key2f(a.mm[p * 4 + 1]);
   const float range = zmax - zmin;
   const float scale = (range > 0.f) ? static_cast<float>(nb) / range : 0.f;
-  BucketRec* rp = rec + static_cast<int64_t>(p) * nb;
-  float2* xsp = xs + static_cast<int64_t>(p) * N;
-  if (tid == 0) { bpar[p * 2 + 0] = zmin; bpar[p * 2 + 1] = scale; }
+  BucketRec* rp = a.rec + static_cast<int64_t>(p) * nb;
+  float2* xsp = a.xs + static_cast<int64_t>(p) * N;
+  float2* ysp = a.ys + static_cast<int64_t>(p) * M;
+  if (tid == 0) { a.bpar[p * 2 + 0] = zmin; a.bpar[p * 2 + 1] = scale; }
   // P0
-  for (int b = tid; b < nb; b += BK_THREADS) {
-    cur[b] = 0;
+  for (int b = tid; b < nb; b += SS_THREADS) {
+    cx[b] = 0;
+    cy[b] = 0;
     reinterpret_cast<double2*>(rp + b)[0] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   // P1
-  for (int64_t i = tid; i < N; i += BK_THREADS) atomicAdd(&cur[bucket_of(__ldg(zx + i), zmin, scale, nb)], 1);
+  for (int64_t i = tid; i < N; i += SS_THREADS) atomicAdd(&cx[bucket_of(__ldg(zx + i), zmin, scale, nb)], 1);
+  for (int64_t i = tid; i < M; i += SS_THREADS) atomicAdd(&cy[bucket_of(__ldg(zy + i), zmin, scale, nb)], 1);
   __syncthreads();
-  // P2: exclusive scan (E consecutive counters per thread)
-  const int E = nb / BK_THREADS;
-  const int b0 = tid * E;
-  {
-    int loc = 0;
-    for (int e = 0; e < E; ++e) loc += cur[b0 + e];
-    const int inc = warp_incl_scan(loc);
-    if (lane == 31) wsum_i[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      const int v = lane < BK_WARPS ? wsum_i[lane] : 0;
-      const int vi = warp_incl_scan(v);
-      if (lane < BK_WARPS) wsum_i[lane] = vi - v;
-    }
-    __syncthreads();
-    int run = wsum_i[wid] + inc - loc;
-    for (int e = 0; e < E; ++e) {
-      const int c = cur[b0 + e];
-      cur[b0 + e] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
-  // P3: scatter; afterwards cur[b] = end of bucket b = start of bucket b+1
-  for (int64_t i = tid; i < N; i += BK_THREADS) {
+  // P2
+  const int E = nb / SS_THREADS;
+  block_excl_scan_int(cx, E, wsum_i);
+  block_excl_scan_int(cy, E, wsum_i);
+  // P3 (afterwards cx[b] / cy[b] = end of bucket b = start of bucket b+1)
+  for (int64_t i = tid; i < N; i += SS_THREADS) {
     const float z = __ldg(zx + i);
-    const int pos = atomicAdd(&cur[bucket_of(z, zmin, scale, nb)], 1);
-    xsp[pos] = make_float2(z, __ldg(w + i));
+    const int pos = atomicAdd(&cx[bucket_of(z, zmin, scale, nb)], 1);
+    xsp[pos] = make_float2(z, __ldg(a.w + i));
+  }
+  for (int64_t i = tid; i < M; i += SS_THREADS) {
+    const float z = __ldg(zy + i);
+    const int pos = atomicAdd(&cy[bucket_of(z, zmin, scale, nb)], 1);
+    ysp[pos] = make_float2(z, __int_as_float(static_cast<int>(i)));
   }
   __syncthreads();
-  // P4: warp-segmented fp64 bucket sums over xs (bucket ids are non-decreasing along xs)
+  // P4
   double tA = 0.0, tB = 0.0, tC = 0.0;
   {
-    const int64_t per = (N + BK_WARPS - 1) / BK_WARPS;
+    const int64_t per = ((N + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;
     const int64_t s0 = min(N, wid * per), s1 = min(N, s0 + per);
     for (int64_t base = s0; base < s1; base += 32) {
       const int64_t i = base + lane;
       const bool valid = i < s1;
-      float2 e = valid ? xsp[i] : make_float2(0.f, 0.f);
-      const int key = valid ? bucket_of(e.x, zmin, scale, nb) : -1 - lane;   // invalid lanes: unique keys
-      double a = e.y, bz = static_cast<double>(e.y) * e.x;
-      tA += a;
-      tB += bz;
-      tC += bz * e.x;
+      const float2 e = valid ? xsp[i] : make_float2(0.f, 0.f);
+      const int key = valid ? bucket_of(e.x, zmin, scale, nb) : -1 - lane;
+      double sa = e.y, sb = static_cast<double>(e.y) * e.x;
+      tA += sa;
+      tB += sb;
+      tC += sb * e.x;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const double na = __shfl_up_sync(0xffffffffu, a, o), nbz = __shfl_up_sync(0xffffffffu, bz, o);
+        const double na = __shfl_up_sync(0xffffffffu, sa, o), nbz = __shfl_up_sync(0xffffffffu, sb, o);
         const int nk = __shfl_up_sync(0xffffffffu, key, o);
-        // keys are sorted, so equal key o lanes back means the whole run in between shares it
-        if (lane >= o && nk == key) { a += na; bz += nbz; }
+        if (lane >= o && nk == key) { sa += na; sb += nbz; }   // keys are sorted along xs
       }
       const int next = __shfl_down_sync(0xffffffffu, key, 1);
-      const bool seg_end = valid && (lane == 31 || next != key);
-      if (seg_end) {
-        atomicAdd(&rp[key].A, a);
-        atomicAdd(&rp[key].B, bz);
+      if (valid && (lane == 31 || next != key)) {
+        atomicAdd(&rp[key].A, sa);
+        atomicAdd(&rp[key].B, sb);
       }
     }
   }
@@ -309,14 +325,13 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bucket_build(ZView zv, const 
   tC = warp_sum(tC);
   if (lane == 0) { wsum_d[0][wid] = tA; wsum_d[1][wid] = tB; wsum_d[2][wid] = tC; }
   __syncthreads();
-  if (tid == 0) {
-    double a = 0, b = 0, c = 0;
-    for (int q = 0; q < BK_WARPS; ++q) { a += wsum_d[0][q]; b += wsum_d[1][q]; c += wsum_d[2][q]; }
-    tot[p] = SliceTot{a, b, c, 0.0};
-  }
+  double TA = 0.0, TB = 0.0, TC = 0.0;
+  for (int q = 0; q < SS_WARPS; ++q) { TA += wsum_d[0][q]; TB += wsum_d[1][q]; TC += wsum_d[2][q]; }
+  if (tid == 0) a.tot[p] = SliceTot{TA, TB, TC, 0.0};
   __syncthreads();
-  // P5: exclusive fp64 scan over buckets, write the records
+  // P5
   {
+    const int b0 = tid * E;
     double lA = 0.0, lB = 0.0;
     for (int e = 0; e < E; ++e) {
       const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + b0 + e));
@@ -327,21 +342,21 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bucket_build(ZView zv, const 
     if (lane == 31) { wsum_d[0][wid] = iA; wsum_d[1][wid] = iB; }
     __syncthreads();
     if (wid == 0) {
-      const double a = lane < BK_WARPS ? wsum_d[0][lane] : 0.0, b = lane < BK_WARPS ? wsum_d[1][lane] : 0.0;
-      const double ia = warp_incl_scan(a), ib = warp_incl_scan(b);
-      if (lane < BK_WARPS) { wsum_d[0][lane] = ia - a; wsum_d[1][lane] = ib - b; }
+      const double va = lane < SS_WARPS ? wsum_d[0][lane] : 0.0, vb = lane < SS_WARPS ? wsum_d[1][lane] : 0.0;
+      const double ia = warp_incl_scan(va), ib = warp_incl_scan(vb);
+      if (lane < SS_WARPS) { wsum_d[0][lane] = ia - va; wsum_d[1][lane] = ib - vb; }
     }
     __syncthreads();
     double rA = wsum_d[0][wid] + iA - lA, rB = wsum_d[1][wid] + iB - lB;
     for (int e = 0; e < E; ++e) {
       const int b = b0 + e;
       const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + b));
-      const int off = (b == 0) ? 0 : cur[b - 1];
+      const int off = (b == 0) ? 0 : cx[b - 1];
       BucketRec r;
       r.A = rA;
       r.B = rB;
       r.off = off;
-      r.cnt = cur[b] - off;
+      r.cnt = cx[b] - off;
       r.w = static_cast<float>(v.x);
       r.wz = static_cast<float>(v.y);
       rp[b] = r;
@@ -349,17 +364,37 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bucket_build(ZView zv, const 
       rB += v.y;
     }
   }
+  __syncthreads();
+  // P6: targets in bucket order
+  for (int64_t i = tid; i < M; i += SS_THREADS) {
+    const float2 e = ysp[i];
+    const float z = e.x;
+    const int64_t m = __float_as_int(e.y);
+    const int b = bucket_of(z, zmin, scale, nb);
+    const double2 AB = __ldcg(reinterpret_cast<const double2*>(rp + b));
+    const int4 oc = __ldcg(reinterpret_cast<const int4*>(rp + b) + 1);
+    const double zd = z;
+    const double Ahi = TA - AB.x - __int_as_float(oc.z), Bhi = TB - AB.y - __int_as_float(oc.w);
+    float same = 0.f;
+    const float2* xp = xsp + oc.x;
+    for (int j = 0; j < oc.y; ++j) {
+      const float2 q = __ldcg(xp + j);
+      same = fmaf(q.y, fabsf(q.x - z), same);
+    }
+    const double t = -a.coef * ((zd * AB.x - AB.y) + (Bhi - zd * Ahi) + static_cast<double>(same));
+    if (a.s64) atomicAdd(a.s64 + m, t);
+    if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
+  }
 }
 
-cudaError_t launch_bucket_build(ZView zv, const float* w, int np, int nb, const unsigned* mm, float2* xs,
-                                BucketRec* rec, SliceTot* tot, float* bpar, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(nb) * sizeof(int);
+cudaError_t launch_sortsum(const SortArgs& a, cudaStream_t st) {
+  const size_t smem = 2 * static_cast<size_t>(a.nb) * sizeof(int);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_bucket_build, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4);
+    cudaFuncSetAttribute(k_sortsum, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16384 * 4);
     attr_set = true;
   }
-  k_bucket_build<<<np, BK_THREADS, smem, st>>>(zv, w, nb, mm, xs, rec, tot, bpar);
+  k_sortsum<<<a.np, SS_THREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -590,25 +625,9 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
     const float z = __ldg(a.zv.zy + p * a.zv.ldy + m);
     const double zd = z;
     double t = 0.0;
-    if (a.sort || a.moment) {
+    if (a.moment) {
       const SliceTot T = a.tot[p];
-      if (a.sort) {
-        const int b = bucket_of(z, a.bpar[p * 2 + 0], a.bpar[p * 2 + 1], a.nb);
-        const BucketRec* rp = a.rec + static_cast<int64_t>(p) * a.nb + b;
-        const double2 AB = __ldg(reinterpret_cast<const double2*>(rp));
-        const int4 oc = __ldg(reinterpret_cast<const int4*>(rp) + 1);
-        const float wb = __int_as_float(oc.z), wzb = __int_as_float(oc.w);
-        const double Ahi = T.A - AB.x - wb, Bhi = T.B - AB.y - wzb;
-        // sum_n w_n |z_n - z| = [z A_lo - B_lo] + [B_hi - z A_hi] + (same-bucket terms, summed directly)
-        double same = 0.0;
-        const float2* xp = a.xs + static_cast<int64_t>(p) * a.zv.N + oc.x;
-        for (int j = 0; j < oc.y; ++j) {
-          const float2 q = __ldg(xp + j);
-          same += static_cast<double>(q.y) * fabs(static_cast<double>(q.x) - zd);
-        }
-        t -= a.sort_coef * ((zd * AB.x - AB.y) + (Bhi - zd * Ahi) + same);
-      }
-      if (a.moment) t += a.mom_coef * static_cast<double>(a.fp[p].tau) * (T.C - 2.0 * zd * T.B + zd * zd * T.A);
+      t += a.mom_coef * static_cast<double>(a.fp[p].tau) * (T.C - 2.0 * zd * T.B + zd * zd * T.A);
     }
     if (a.fourier) {
       const FPar f = a.fp[p];
@@ -623,7 +642,10 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
       }
       t += tf;
     }
-    if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
+    if (a.per_slice_out) {
+      float* o = a.per_slice_out + static_cast<int64_t>(p) * M + m;
+      *o = a.accumulate_out ? *o + static_cast<float>(t) : static_cast<float>(t);
+    }
     acc += t;
   }
   if (a.s64) atomicAdd(a.s64 + m, acc);

@@ -51,8 +51,21 @@ struct BucketRec {
 struct SliceTot {
   double A, B, C, pad;
 };
-cudaError_t launch_bucket_build(ZView zv, const float* w, int np, int nb, const unsigned* mm, float2* xs,
-                                BucketRec* rec, SliceTot* tot, float* bpar, cudaStream_t st);
+struct SortArgs {
+  ZView zv;
+  const float* w;
+  int np, nb;
+  const unsigned* mm;
+  float2* xs;          // [np][N] (z, w) in bucket order
+  float2* ys;          // [np][M] (z, m) in bucket order
+  BucketRec* rec;      // [np][nb]
+  SliceTot* tot;       // [np]
+  float* bpar;         // [np][2] bucket map (zmin, scale)
+  double coef;         // t = -coef * sum_n w_n |x_n - z|   (c_d, or alpha c_d for the Laplacian part)
+  double* s64;         // accumulate t into s64[m] (fp64 atomics), or
+  float* per_slice_out;   // store t into per_slice_out[p*M + m]
+};
+cudaError_t launch_sortsum(const SortArgs& a, cudaStream_t st);
 
 // row a2: D[p][k] = c_k(tau_p) / Phi_k^2 on the band of slice p, else 0  (k = 0..n/2)
 cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* phi2inv, int n, float* D,
@@ -63,20 +76,13 @@ cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int 
 // row a6: h[p] = IFFT_n(D[p] * FFT_n(g[p]))   (unnormalised, one CTA per slice, smem radix-2)
 cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, cudaStream_t st);
 
-// rows a4 + a7 (+ Laplacian moment term) + slice accumulation:
-//   per y_m: acc = sum_p [ sort_coef * S_sort + Fourier interp + mom_coef * tau_p * S_moment ]
+// row a7 (+ Laplacian moment term) + slice accumulation:
+//   per y_m: acc = sum_p [ Fourier interp + mom_coef * tau_p * S_moment ]
 //   s64[m] += acc   (per_slice_out == nullptr)   or   per_slice_out[p*M + m] = t_{m,p}
 struct EvalArgs {
   ZView zv;
   int np;
-  // sort part
-  bool sort;
-  int nb;
-  const float2* xs;
-  const BucketRec* rec;
-  const SliceTot* tot;
-  const float* bpar;
-  double sort_coef;   // t += -sort_coef * sum_n w_n |z_n - z_m|
+  const SliceTot* tot;   // slice totals (moment part)
   // Fourier part
   bool fourier;
   const FPar* fp;
@@ -89,6 +95,7 @@ struct EvalArgs {
   // outputs
   double* s64;
   float* per_slice_out;
+  bool accumulate_out;   // per_slice_out += t (after the sort path stored its part)
 };
 cudaError_t launch_eval(const EvalArgs& a, cudaStream_t st);
 cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t st);
