@@ -365,23 +365,33 @@ __global__ void __launch_bounds__(SS_THREADS, 1) k_sortsum(SortArgs a) {
     }
   }
   __syncthreads();
-  // P6: targets in bucket order
+  // P6: targets in bucket order.  xs / records were written by this CTA (same SM, same L1), so plain
+  // cached loads are coherent here; the bucket's x's are loaded 4 at a time (independent accumulators).
   for (int64_t i = tid; i < M; i += SS_THREADS) {
     const float2 e = ysp[i];
     const float z = e.x;
     const int64_t m = __float_as_int(e.y);
     const int b = bucket_of(z, zmin, scale, nb);
-    const double2 AB = __ldcg(reinterpret_cast<const double2*>(rp + b));
-    const int4 oc = __ldcg(reinterpret_cast<const int4*>(rp + b) + 1);
+    const double2 AB = reinterpret_cast<const double2*>(rp + b)[0];
+    const int4 oc = reinterpret_cast<const int4*>(rp + b)[1];
     const double zd = z;
     const double Ahi = TA - AB.x - __int_as_float(oc.z), Bhi = TB - AB.y - __int_as_float(oc.w);
-    float same = 0.f;
     const float2* xp = xsp + oc.x;
-    for (int j = 0; j < oc.y; ++j) {
-      const float2 q = __ldcg(xp + j);
-      same = fmaf(q.y, fabsf(q.x - z), same);
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int j = 0;
+    for (; j + 4 <= oc.y; j += 4) {
+      const float2 q0 = xp[j], q1 = xp[j + 1], q2 = xp[j + 2], q3 = xp[j + 3];
+      s0 = fmaf(q0.y, fabsf(q0.x - z), s0);
+      s1 = fmaf(q1.y, fabsf(q1.x - z), s1);
+      s2 = fmaf(q2.y, fabsf(q2.x - z), s2);
+      s3 = fmaf(q3.y, fabsf(q3.x - z), s3);
     }
-    const double t = -a.coef * ((zd * AB.x - AB.y) + (Bhi - zd * Ahi) + static_cast<double>(same));
+    for (; j < oc.y; ++j) {
+      const float2 q = xp[j];
+      s0 = fmaf(q.y, fabsf(q.x - z), s0);
+    }
+    const double same = static_cast<double>((s0 + s1) + (s2 + s3));
+    const double t = -a.coef * ((zd * AB.x - AB.y) + (Bhi - zd * Ahi) + same);
     if (a.s64) atomicAdd(a.s64 + m, t);
     if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
   }
