@@ -273,24 +273,66 @@ __global__ void __launch_bounds__(SS_THREADS, 1) k_sortsum(SortArgs a) {
     reinterpret_cast<double2*>(rp + b)[0] = make_double2(0.0, 0.0);
   }
   __syncthreads();
-  // P1
-  for (int64_t i = tid; i < N; i += SS_THREADS) atomicAdd(&cx[bucket_of(__ldg(zx + i), zmin, scale, nb)], 1);
-  for (int64_t i = tid; i < M; i += SS_THREADS) atomicAdd(&cy[bucket_of(__ldg(zy + i), zmin, scale, nb)], 1);
+  // P1 (8 independent loads in flight per thread before their atomics)
+  constexpr int U = 8;
+  for (int64_t base = 0; base < N; base += U * SS_THREADS) {
+    float zz[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SS_THREADS;
+      zz[k] = (i < N) ? __ldg(zx + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (base + tid + k * SS_THREADS < N) atomicAdd(&cx[bucket_of(zz[k], zmin, scale, nb)], 1);
+  }
+  for (int64_t base = 0; base < M; base += U * SS_THREADS) {
+    float zz[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SS_THREADS;
+      zz[k] = (i < M) ? __ldg(zy + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (base + tid + k * SS_THREADS < M) atomicAdd(&cy[bucket_of(zz[k], zmin, scale, nb)], 1);
+  }
   __syncthreads();
   // P2
   const int E = nb / SS_THREADS;
   block_excl_scan_int(cx, E, wsum_i);
   block_excl_scan_int(cy, E, wsum_i);
   // P3 (afterwards cx[b] / cy[b] = end of bucket b = start of bucket b+1)
-  for (int64_t i = tid; i < N; i += SS_THREADS) {
-    const float z = __ldg(zx + i);
-    const int pos = atomicAdd(&cx[bucket_of(z, zmin, scale, nb)], 1);
-    xsp[pos] = make_float2(z, __ldg(a.w + i));
+  for (int64_t base = 0; base < N; base += U * SS_THREADS) {
+    float zz[U], ww[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SS_THREADS;
+      zz[k] = (i < N) ? __ldg(zx + i) : 0.f;
+      ww[k] = (i < N) ? __ldg(a.w + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (base + tid + k * SS_THREADS < N) {
+        const int pos = atomicAdd(&cx[bucket_of(zz[k], zmin, scale, nb)], 1);
+        xsp[pos] = make_float2(zz[k], ww[k]);
+      }
   }
-  for (int64_t i = tid; i < M; i += SS_THREADS) {
-    const float z = __ldg(zy + i);
-    const int pos = atomicAdd(&cy[bucket_of(z, zmin, scale, nb)], 1);
-    ysp[pos] = make_float2(z, __int_as_float(static_cast<int>(i)));
+  for (int64_t base = 0; base < M; base += U * SS_THREADS) {
+    float zz[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SS_THREADS;
+      zz[k] = (i < M) ? __ldg(zy + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SS_THREADS;
+      if (i < M) {
+        const int pos = atomicAdd(&cy[bucket_of(zz[k], zmin, scale, nb)], 1);
+        ysp[pos] = make_float2(zz[k], __int_as_float(static_cast<int>(i)));
+      }
+    }
   }
   __syncthreads();
   // P4
@@ -298,25 +340,34 @@ __global__ void __launch_bounds__(SS_THREADS, 1) k_sortsum(SortArgs a) {
   {
     const int64_t per = ((N + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;
     const int64_t s0 = min(N, wid * per), s1 = min(N, s0 + per);
-    for (int64_t base = s0; base < s1; base += 32) {
-      const int64_t i = base + lane;
-      const bool valid = i < s1;
-      const float2 e = valid ? xsp[i] : make_float2(0.f, 0.f);
-      const int key = valid ? bucket_of(e.x, zmin, scale, nb) : -1 - lane;
-      double sa = e.y, sb = static_cast<double>(e.y) * e.x;
-      tA += sa;
-      tB += sb;
-      tC += sb * e.x;
+    for (int64_t base0 = s0; base0 < s1; base0 += 4 * 32) {
+      float2 ee[4];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double na = __shfl_up_sync(0xffffffffu, sa, o), nbz = __shfl_up_sync(0xffffffffu, sb, o);
-        const int nk = __shfl_up_sync(0xffffffffu, key, o);
-        if (lane >= o && nk == key) { sa += na; sb += nbz; }   // keys are sorted along xs
+      for (int k = 0; k < 4; ++k) {
+        const int64_t i = base0 + k * 32 + lane;
+        ee[k] = (i < s1) ? xsp[i] : make_float2(0.f, 0.f);
       }
-      const int next = __shfl_down_sync(0xffffffffu, key, 1);
-      if (valid && (lane == 31 || next != key)) {
-        atomicAdd(&rp[key].A, sa);
-        atomicAdd(&rp[key].B, sb);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t i = base0 + k * 32 + lane;
+        const bool valid = i < s1;
+        const float2 e = ee[k];
+        const int key = valid ? bucket_of(e.x, zmin, scale, nb) : -1 - lane;
+        double sa = e.y, sb = static_cast<double>(e.y) * e.x;
+        tA += sa;
+        tB += sb;
+        tC += sb * e.x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double na = __shfl_up_sync(0xffffffffu, sa, o), nbz = __shfl_up_sync(0xffffffffu, sb, o);
+          const int nk = __shfl_up_sync(0xffffffffu, key, o);
+          if (lane >= o && nk == key) { sa += na; sb += nbz; }   // keys are sorted along xs
+        }
+        const int next = __shfl_down_sync(0xffffffffu, key, 1);
+        if (valid && (lane == 31 || next != key)) {
+          atomicAdd(&rp[key].A, sa);
+          atomicAdd(&rp[key].B, sb);
+        }
       }
     }
   }
@@ -367,33 +418,50 @@ __global__ void __launch_bounds__(SS_THREADS, 1) k_sortsum(SortArgs a) {
   __syncthreads();
   // P6: targets in bucket order.  xs / records were written by this CTA (same SM, same L1), so plain
   // cached loads are coherent here; the bucket's x's are loaded 4 at a time (independent accumulators).
-  for (int64_t i = tid; i < M; i += SS_THREADS) {
-    const float2 e = ysp[i];
-    const float z = e.x;
-    const int64_t m = __float_as_int(e.y);
-    const int b = bucket_of(z, zmin, scale, nb);
-    const double2 AB = reinterpret_cast<const double2*>(rp + b)[0];
-    const int4 oc = reinterpret_cast<const int4*>(rp + b)[1];
-    const double zd = z;
-    const double Ahi = TA - AB.x - __int_as_float(oc.z), Bhi = TB - AB.y - __int_as_float(oc.w);
-    const float2* xp = xsp + oc.x;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    int j = 0;
-    for (; j + 4 <= oc.y; j += 4) {
-      const float2 q0 = xp[j], q1 = xp[j + 1], q2 = xp[j + 2], q3 = xp[j + 3];
-      s0 = fmaf(q0.y, fabsf(q0.x - z), s0);
-      s1 = fmaf(q1.y, fabsf(q1.x - z), s1);
-      s2 = fmaf(q2.y, fabsf(q2.x - z), s2);
-      s3 = fmaf(q3.y, fabsf(q3.x - z), s3);
+  for (int64_t base = 0; base < M; base += 4 * SS_THREADS) {
+    float2 ee[4];
+    int bb[4];
+    double2 AB[4];
+    int4 oc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = base + tid + k * SS_THREADS;
+      ee[k] = (i < M) ? ysp[i] : make_float2(zmin, 0.f);
+      bb[k] = bucket_of(ee[k].x, zmin, scale, nb);
     }
-    for (; j < oc.y; ++j) {
-      const float2 q = xp[j];
-      s0 = fmaf(q.y, fabsf(q.x - z), s0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      AB[k] = reinterpret_cast<const double2*>(rp + bb[k])[0];
+      oc[k] = reinterpret_cast<const int4*>(rp + bb[k])[1];
     }
-    const double same = static_cast<double>((s0 + s1) + (s2 + s3));
-    const double t = -a.coef * ((zd * AB.x - AB.y) + (Bhi - zd * Ahi) + same);
-    if (a.s64) atomicAdd(a.s64 + m, t);
-    if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = base + tid + k * SS_THREADS;
+      if (i >= M) continue;
+      const float z = ee[k].x;
+      const int64_t m = __float_as_int(ee[k].y);
+      const double zd = z;
+      const double Ahi = TA - AB[k].x - __int_as_float(oc[k].z), Bhi = TB - AB[k].y - __int_as_float(oc[k].w);
+      const float2* xp = xsp + oc[k].x;
+      const int cnt = oc[k].y;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      int j = 0;
+      for (; j + 4 <= cnt; j += 4) {
+        const float2 q0 = xp[j], q1 = xp[j + 1], q2 = xp[j + 2], q3 = xp[j + 3];
+        s0 = fmaf(q0.y, fabsf(q0.x - z), s0);
+        s1 = fmaf(q1.y, fabsf(q1.x - z), s1);
+        s2 = fmaf(q2.y, fabsf(q2.x - z), s2);
+        s3 = fmaf(q3.y, fabsf(q3.x - z), s3);
+      }
+      for (; j < cnt; ++j) {
+        const float2 q = xp[j];
+        s0 = fmaf(q.y, fabsf(q.x - z), s0);
+      }
+      const double same = static_cast<double>((s0 + s1) + (s2 + s3));
+      const double t = -a.coef * ((zd * AB[k].x - AB[k].y) + (Bhi - zd * Ahi) + same);
+      if (a.s64) atomicAdd(a.s64 + m, t);
+      if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
+    }
   }
 }
 
