@@ -3,8 +3,7 @@
 // Row map (SURVEY.md Sec. 8a / DESIGN.md):
 //   a1 projection ............ k_project            (Alg.1)
 //   a2 torus plan (D_k) ....... k_plan_D             (R3-R7b)
-//   a3 sort (counting sort) ... k_bucket_build       (Sec. 3.2, Alg. 2)
-//   a4 scans + evaluate ....... k_bucket_build (fp64 prefix sums) + k_eval (sort part)
+//   a3 sort + a4 scans/evaluate: sortpath.cu (two-level counting sort, fp64 prefix sums; Sec. 3.2, Alg. 2)
 //   a5 spread ................. k_spread_private / k_spread_shared   (NFFT adjoint)
 //   a6 FFT x D iFFT ........... k_fft_filter
 //   a7 interpolate + mean ..... k_eval (Fourier part) + k_finalize   (Alg.1)
@@ -189,290 +188,6 @@ cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_
   int bx = static_cast<int>((L + 255) / 256);
   if (bx > 64) bx = 64;
   k_minmax<<<dim3(bx, np), 256, 0, st>>>(zv, mm, flag);
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------ a3/a4: fused sort path (one CTA per slice)
-// Sec. 3.2 / Alg. 2 as a one-pass MSD counting sort of BOTH point sets into nb monotone buckets
-// of the slice's x range, fp64 prefix sums over the x buckets, and a bucket-ordered evaluation of the
-// targets:  sum_n w_n |x_n - z| = [z A_lo - B_lo] + [B_hi - z A_hi] + sum_{x in z's bucket} w |x - z|.
-//  P0 zero counters and bucket sums        P1 count x and y per bucket (smem atomics)
-//  P2 exclusive scans -> cursors           P3 scatter (z,w) -> xs, (z,m) -> ys in bucket order
-//  P4 warp-segmented fp64 bucket sums of x (coalesced; one fp64 atomic per segment) + slice totals
-//  P5 exclusive fp64 scan -> 32-byte records {A_excl, B_excl, off, cnt, w_b, wz_b}
-//  P6 targets in bucket order: lanes of a warp share buckets (broadcast loads of the bucket's x's);
-//     t_{m,p} -> fp64 atomic into s64[m] (or per-slice output)
-// All scratch (xs, ys, records) is written and re-read by the same CTA: it stays in L2.
-constexpr int SS_THREADS = 1024;
-constexpr int SS_WARPS = SS_THREADS / 32;
-
-template <typename T>
-__device__ __forceinline__ T warp_incl_scan(T v) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    T n = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += n;
-  }
-  return v;
-}
-
-template <typename T>
-__device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// block-wide exclusive scan of E consecutive ints per thread, in place; returns nothing
-__device__ __forceinline__ void block_excl_scan_int(int* a, int E, int* wsum) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int b0 = tid * E;
-  int loc = 0;
-  for (int e = 0; e < E; ++e) loc += a[b0 + e];
-  const int inc = warp_incl_scan(loc);
-  if (lane == 31) wsum[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    const int v = lane < SS_WARPS ? wsum[lane] : 0;
-    const int vi = warp_incl_scan(v);
-    if (lane < SS_WARPS) wsum[lane] = vi - v;
-  }
-  __syncthreads();
-  int run = wsum[wid] + inc - loc;
-  for (int e = 0; e < E; ++e) {
-    const int c = a[b0 + e];
-    a[b0 + e] = run;
-    run += c;
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(SS_THREADS, 1) k_sortsum(SortArgs a) {
-  extern __shared__ int smem_i[];
-  int* cx = smem_i;            // [nb] x counters -> cursors -> bucket ends
-  int* cy = smem_i + a.nb;     // [nb] y counters -> cursors -> bucket ends
-  __shared__ int wsum_i[SS_WARPS];
-  __shared__ double wsum_d[3][SS_WARPS];
-  const int nb = a.nb;
-  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t N = a.zv.N, M = a.zv.M;
-  const float* zx = a.zv.zx + p * a.zv.ldx;
-  const float* zy = a.zv.zy + p * a.zv.ldy;
-  const float zmin = key2f(a.mm[p * 4 + 0]), zmax = key2f(a.mm[p * 4 + 1]);
-  const float range = zmax - zmin;
-  const float scale = (range > 0.f) ? static_cast<float>(nb) / range : 0.f;
-  BucketRec* rp = a.rec + static_cast<int64_t>(p) * nb;
-  float2* xsp = a.xs + static_cast<int64_t>(p) * N;
-  float2* ysp = a.ys + static_cast<int64_t>(p) * M;
-  if (tid == 0) { a.bpar[p * 2 + 0] = zmin; a.bpar[p * 2 + 1] = scale; }
-  // P0
-  for (int b = tid; b < nb; b += SS_THREADS) {
-    cx[b] = 0;
-    cy[b] = 0;
-    reinterpret_cast<double2*>(rp + b)[0] = make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  // P1 (8 independent loads in flight per thread before their atomics)
-  constexpr int U = 8;
-  for (int64_t base = 0; base < N; base += U * SS_THREADS) {
-    float zz[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SS_THREADS;
-      zz[k] = (i < N) ? __ldg(zx + i) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (base + tid + k * SS_THREADS < N) atomicAdd(&cx[bucket_of(zz[k], zmin, scale, nb)], 1);
-  }
-  for (int64_t base = 0; base < M; base += U * SS_THREADS) {
-    float zz[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SS_THREADS;
-      zz[k] = (i < M) ? __ldg(zy + i) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (base + tid + k * SS_THREADS < M) atomicAdd(&cy[bucket_of(zz[k], zmin, scale, nb)], 1);
-  }
-  __syncthreads();
-  // P2
-  const int E = nb / SS_THREADS;
-  block_excl_scan_int(cx, E, wsum_i);
-  block_excl_scan_int(cy, E, wsum_i);
-  // P3 (afterwards cx[b] / cy[b] = end of bucket b = start of bucket b+1)
-  for (int64_t base = 0; base < N; base += U * SS_THREADS) {
-    float zz[U], ww[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SS_THREADS;
-      zz[k] = (i < N) ? __ldg(zx + i) : 0.f;
-      ww[k] = (i < N) ? __ldg(a.w + i) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (base + tid + k * SS_THREADS < N) {
-        const int pos = atomicAdd(&cx[bucket_of(zz[k], zmin, scale, nb)], 1);
-        xsp[pos] = make_float2(zz[k], ww[k]);
-      }
-  }
-  for (int64_t base = 0; base < M; base += U * SS_THREADS) {
-    float zz[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SS_THREADS;
-      zz[k] = (i < M) ? __ldg(zy + i) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SS_THREADS;
-      if (i < M) {
-        const int pos = atomicAdd(&cy[bucket_of(zz[k], zmin, scale, nb)], 1);
-        ysp[pos] = make_float2(zz[k], __int_as_float(static_cast<int>(i)));
-      }
-    }
-  }
-  __syncthreads();
-  // P4
-  double tA = 0.0, tB = 0.0, tC = 0.0;
-  {
-    const int64_t per = ((N + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;
-    const int64_t s0 = min(N, wid * per), s1 = min(N, s0 + per);
-    for (int64_t base0 = s0; base0 < s1; base0 += 4 * 32) {
-      float2 ee[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t i = base0 + k * 32 + lane;
-        ee[k] = (i < s1) ? xsp[i] : make_float2(0.f, 0.f);
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t i = base0 + k * 32 + lane;
-        const bool valid = i < s1;
-        const float2 e = ee[k];
-        const int key = valid ? bucket_of(e.x, zmin, scale, nb) : -1 - lane;
-        double sa = e.y, sb = static_cast<double>(e.y) * e.x;
-        tA += sa;
-        tB += sb;
-        tC += sb * e.x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double na = __shfl_up_sync(0xffffffffu, sa, o), nbz = __shfl_up_sync(0xffffffffu, sb, o);
-          const int nk = __shfl_up_sync(0xffffffffu, key, o);
-          if (lane >= o && nk == key) { sa += na; sb += nbz; }   // keys are sorted along xs
-        }
-        const int next = __shfl_down_sync(0xffffffffu, key, 1);
-        if (valid && (lane == 31 || next != key)) {
-          atomicAdd(&rp[key].A, sa);
-          atomicAdd(&rp[key].B, sb);
-        }
-      }
-    }
-  }
-  tA = warp_sum(tA);
-  tB = warp_sum(tB);
-  tC = warp_sum(tC);
-  if (lane == 0) { wsum_d[0][wid] = tA; wsum_d[1][wid] = tB; wsum_d[2][wid] = tC; }
-  __syncthreads();
-  double TA = 0.0, TB = 0.0, TC = 0.0;
-  for (int q = 0; q < SS_WARPS; ++q) { TA += wsum_d[0][q]; TB += wsum_d[1][q]; TC += wsum_d[2][q]; }
-  if (tid == 0) a.tot[p] = SliceTot{TA, TB, TC, 0.0};
-  __syncthreads();
-  // P5
-  {
-    const int b0 = tid * E;
-    double lA = 0.0, lB = 0.0;
-    for (int e = 0; e < E; ++e) {
-      const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + b0 + e));
-      lA += v.x;
-      lB += v.y;
-    }
-    const double iA = warp_incl_scan(lA), iB = warp_incl_scan(lB);
-    if (lane == 31) { wsum_d[0][wid] = iA; wsum_d[1][wid] = iB; }
-    __syncthreads();
-    if (wid == 0) {
-      const double va = lane < SS_WARPS ? wsum_d[0][lane] : 0.0, vb = lane < SS_WARPS ? wsum_d[1][lane] : 0.0;
-      const double ia = warp_incl_scan(va), ib = warp_incl_scan(vb);
-      if (lane < SS_WARPS) { wsum_d[0][lane] = ia - va; wsum_d[1][lane] = ib - vb; }
-    }
-    __syncthreads();
-    double rA = wsum_d[0][wid] + iA - lA, rB = wsum_d[1][wid] + iB - lB;
-    for (int e = 0; e < E; ++e) {
-      const int b = b0 + e;
-      const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + b));
-      const int off = (b == 0) ? 0 : cx[b - 1];
-      BucketRec r;
-      r.A = rA;
-      r.B = rB;
-      r.off = off;
-      r.cnt = cx[b] - off;
-      r.w = static_cast<float>(v.x);
-      r.wz = static_cast<float>(v.y);
-      rp[b] = r;
-      rA += v.x;
-      rB += v.y;
-    }
-  }
-  __syncthreads();
-  // P6: targets in bucket order.  xs / records were written by this CTA (same SM, same L1), so plain
-  // cached loads are coherent here; the bucket's x's are loaded 4 at a time (independent accumulators).
-  for (int64_t base = 0; base < M; base += 4 * SS_THREADS) {
-    float2 ee[4];
-    int bb[4];
-    double2 AB[4];
-    int4 oc[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t i = base + tid + k * SS_THREADS;
-      ee[k] = (i < M) ? ysp[i] : make_float2(zmin, 0.f);
-      bb[k] = bucket_of(ee[k].x, zmin, scale, nb);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      AB[k] = reinterpret_cast<const double2*>(rp + bb[k])[0];
-      oc[k] = reinterpret_cast<const int4*>(rp + bb[k])[1];
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t i = base + tid + k * SS_THREADS;
-      if (i >= M) continue;
-      const float z = ee[k].x;
-      const int64_t m = __float_as_int(ee[k].y);
-      const double zd = z;
-      const double Ahi = TA - AB[k].x - __int_as_float(oc[k].z), Bhi = TB - AB[k].y - __int_as_float(oc[k].w);
-      const float2* xp = xsp + oc[k].x;
-      const int cnt = oc[k].y;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-      int j = 0;
-      for (; j + 4 <= cnt; j += 4) {
-        const float2 q0 = xp[j], q1 = xp[j + 1], q2 = xp[j + 2], q3 = xp[j + 3];
-        s0 = fmaf(q0.y, fabsf(q0.x - z), s0);
-        s1 = fmaf(q1.y, fabsf(q1.x - z), s1);
-        s2 = fmaf(q2.y, fabsf(q2.x - z), s2);
-        s3 = fmaf(q3.y, fabsf(q3.x - z), s3);
-      }
-      for (; j < cnt; ++j) {
-        const float2 q = xp[j];
-        s0 = fmaf(q.y, fabsf(q.x - z), s0);
-      }
-      const double same = static_cast<double>((s0 + s1) + (s2 + s3));
-      const double t = -a.coef * ((zd * AB[k].x - AB[k].y) + (Bhi - zd * Ahi) + same);
-      if (a.s64) atomicAdd(a.s64 + m, t);
-      if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
-    }
-  }
-}
-
-cudaError_t launch_sortsum(const SortArgs& a, cudaStream_t st) {
-  const size_t smem = 2 * static_cast<size_t>(a.nb) * sizeof(int);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_sortsum, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16384 * 4);
-    attr_set = true;
-  }
-  k_sortsum<<<a.np, SS_THREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -686,7 +401,7 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, 
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ a4 + a7: evaluation at the targets
+// ------------------------------------------------------------------ a7: interpolation at the targets
 // grid (target blocks, slice groups): each thread handles one target over EV_SG slices, then one fp64
 // atomic into s64 (or per-slice stores for sks_sum_1d).  Target blocks vary fastest, so the CTAs resident
 // at a time work on the same slice group and its bucket records / grids stay in L2.
