@@ -112,7 +112,10 @@ Path path_of(int kind) {
   return Path{kind == SKS_NEGDIST || kind == SKS_LAPLACIAN, kind != SKS_NEGDIST, kind == SKS_LAPLACIAN};
 }
 
-int buckets_for(int64_t N) { return sks::sortpath_coarse_buckets(N); }
+int buckets_for(int64_t N) {
+  (void)N;
+  return sks::sortpath_buckets();
+}
 
 constexpr int kNmax = 16384;   // largest NFFT grid the kernels are built for
 constexpr size_t kAlign = 256;
@@ -120,22 +123,9 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, mm = 0, xs = 0, ys = 0, ccnt = 0, csum = 0, crec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
+  size_t Z = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
          flag = 0, total = 0;
 };
-
-constexpr int kChunk = 16384;            // level-1 chunk of the sort path
-constexpr size_t kSortL2Budget = size_t(48) << 20;   // scratch of one sort sub-batch (stays in L2)
-
-size_t sort_bytes_per_slice(int64_t N, int64_t M, int B1) {
-  const int64_t nchunks = (std::max(N, M) + kChunk - 1) / kChunk;
-  return al(8 * N) + al(8 * M) + al(8 * nchunks * B1) + al(24 * nchunks * B1) + al(sizeof(sks::CoarseRec) * B1);
-}
-
-int sort_subbatch(int64_t N, int64_t M, int B1, int nbat) {
-  const size_t per = sort_bytes_per_slice(N, M, B1);
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nbat, static_cast<int64_t>(kSortL2Budget / per))));
-}
 
 Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb) {
   Layout L;
@@ -150,14 +140,9 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb)
   L.mm = take(sizeof(unsigned) * 4 * nbat);
   if (with_Z) L.Z = take(sizeof(float) * (N + M) * nbat);
   if (pt.sort || pt.moment) {
-    const int B1 = nb;
-    const int sb = sort_subbatch(N, M, B1, nbat);
-    const int64_t nchunks = (std::max(N, M) + kChunk - 1) / kChunk;
-    L.xs = take(sizeof(float2) * N * sb);
-    L.ys = take(sizeof(float2) * M * sb);
-    L.ccnt = take(sizeof(int) * 2 * nchunks * B1 * sb);
-    L.csum = take(sizeof(double) * 3 * nchunks * B1 * sb);
-    L.crec = take(sizeof(sks::CoarseRec) * B1 * static_cast<size_t>(sb));
+    L.xs = take(sizeof(float2) * N * nbat);
+    L.ys = take(sizeof(float2) * M * nbat);
+    L.rec = take(sizeof(sks::BucketRec) * nb * static_cast<size_t>(nbat));
     L.tot = take(sizeof(sks::SliceTot) * static_cast<size_t>(nbat));
     L.bpar = take(sizeof(float) * 2 * nbat);
   }
@@ -388,33 +373,23 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     float* tps = t_out ? t_out + static_cast<int64_t>(b0) * pr.M : nullptr;
     if (pt.sort) {
       // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)
-      const int sb = sort_subbatch(pr.N, pr.M, nb, batch);
+      sks::SortArgs sa{};
+      sa.zv = zv;
+      sa.w = w;
+      sa.np = nbat;
+      sa.mm = mm;
+      sa.xs = reinterpret_cast<float2*>(ws + L.xs);
+      sa.ys = reinterpret_cast<float2*>(ws + L.ys);
+      sa.rec = reinterpret_cast<sks::BucketRec*>(ws + L.rec);
+      sa.tot = reinterpret_cast<sks::SliceTot*>(ws + L.tot);
+      sa.bpar = reinterpret_cast<float*>(ws + L.bpar);
+      sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
+      sa.s64 = s64;
+      sa.per_slice_out = tps;
       ProfScope ps(PS_BUCKET, st);
-      for (int q0 = 0; q0 < nbat; q0 += sb) {
-        const int nq = std::min(sb, nbat - q0);
-        sks::SortArgs sa{};
-        sa.zv = sks::ZView{zv.zx + static_cast<int64_t>(q0) * zv.ldx, zv.zy + static_cast<int64_t>(q0) * zv.ldy, zv.ldx,
-                           zv.ldy, zv.N, zv.M};
-        sa.w = w;
-        sa.np = nq;
-        sa.B1 = nb;
-        sa.chunk = kChunk;
-        sa.nchunks = static_cast<int>((std::max(pr.N, pr.M) + kChunk - 1) / kChunk);
-        sa.mm = mm + 4 * q0;
-        sa.ccnt = reinterpret_cast<int*>(ws + L.ccnt);
-        sa.csum = reinterpret_cast<double*>(ws + L.csum);
-        sa.xs = reinterpret_cast<float2*>(ws + L.xs);
-        sa.ys = reinterpret_cast<float2*>(ws + L.ys);
-        sa.crec = reinterpret_cast<sks::CoarseRec*>(ws + L.crec);
-        sa.tot = reinterpret_cast<sks::SliceTot*>(ws + L.tot) + q0;
-        sa.bpar = reinterpret_cast<float*>(ws + L.bpar) + 2 * q0;
-        sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
-        sa.s64 = s64;
-        sa.per_slice_out = tps ? tps + static_cast<int64_t>(q0) * pr.M : nullptr;
-        SKS_CUDA(sks::launch_sortpath(sa, st));
-        launches += 4;
-      }
-      ea.tot = reinterpret_cast<const sks::SliceTot*>(ws + L.tot);
+      SKS_CUDA(sks::launch_sortpath(sa, st));
+      ++launches;
+      ea.tot = sa.tot;
     }
     if (pt.fourier) {
       sks_status s = fourier_batch(pr.k, pr.d, o, zv, w, nbat, ws, L, st, &plan, &launches);

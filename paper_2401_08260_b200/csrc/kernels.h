@@ -39,36 +39,32 @@ cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_
 cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st);
 void decode_minmax(const unsigned* enc, float* dec, int n);
 
-// rows a3 + a4 (sortpath.cu): two-level MSD counting sort of the x and y projections, fp64 prefix sums,
-// exact evaluation of t_m = -coef sum_n w_n |x_n - y_m| for every target; results into s64 (fp64 atomics)
-// or per-slice outputs.
+// rows a3 + a4 (sortpath.cu): per slice, one 4-CTA cluster counting-sorts the x and y projections into
+// NB monotone buckets, builds fp64 bucket prefix sums and evaluates t_m = -coef sum_n w_n |x_n - y_m| for
+// every target exactly; results into s64 (fp64 atomics) or per-slice outputs.
 struct SliceTot {
   double A, B, C, pad;   // sum w, sum w z, sum w z^2 over the slice's sources
 };
-struct CoarseRec {
-  double A, B;           // exclusive prefix over coarse buckets < b: sum w, sum w z
-  double W, Z;           // this bucket: sum w, sum w z
-  int xoff, xcnt, yoff, ycnt;
+struct BucketRec {       // 32 bytes: one sector per target lookup
+  double A, B;           // exclusive prefix over buckets < b: sum w, sum w z (fp64)
+  int off, cnt;          // slot range of the bucket in xs
+  float w, wz;           // the bucket's own sums (rounded)
 };
 struct SortArgs {
-  ZView zv;              // projections of the np slices of this sub-batch
+  ZView zv;              // projections of the np slices
   const float* w;
   int np;
-  int B1;                // coarse buckets (power of two, 256..4096)
-  int chunk, nchunks;    // level-1 chunking of max(N, M)
   const unsigned* mm;    // [np][4] ranges
-  int* ccnt;             // [np][nchunks][B1] int2 counts -> absolute chunk cursors
-  double* csum;          // [np][nchunks][B1][3]
-  float2* xs;            // [np][N] (z, w) in coarse-bucket order
-  float2* ys;            // [np][M] (z, m) in coarse-bucket order
-  CoarseRec* crec;       // [np][B1]
+  float2* xs;            // [np][N] (z, w) in bucket order
+  float2* ys;            // [np][M] (z, m) in bucket order
+  BucketRec* rec;        // [np][NB]
   SliceTot* tot;         // [np]
-  float* bpar;           // [np][2] coarse map (zmin, scale)
+  float* bpar;           // [np][2] bucket map (zmin, scale)
   double coef;           // t = -coef * sum_n w_n |x_n - z|   (c_d, or alpha c_d for the Laplacian part)
   double* s64;           // accumulate t into s64[m] (fp64 atomics), or
   float* per_slice_out;  // store t into per_slice_out[p*M + m]
 };
-int sortpath_coarse_buckets(int64_t N);
+int sortpath_buckets();
 cudaError_t launch_sortpath(const SortArgs& a, cudaStream_t st);
 
 // row a2: D[p][k] = c_k(tau_p) / Phi_k^2 on the band of slice p, else 0  (k = 0..n/2)

@@ -1,45 +1,52 @@
 // sortpath.cu -- the sort path (rows a3 + a4) for the negative distance kernel and the sorting part of the
-// Laplacian decomposition: Sec. 3.2 / Alg. 2 computes, exactly,
-//     t_m = -c sum_n w_n |x_n - y_m|                                             (c = c_d or alpha c_d)
-// by sorting the merged projections and running prefix sums.  Here the sort is a two-level MSD counting
-// sort (both levels in shared memory) and the prefix sums are fp64:
-//   level 1 (coarse, B1 value buckets over the slice's x range; many CTAs per slice):
-//     K1 k_sp_count   per (chunk, slice): coarse histograms of x and y + fp64 coarse sums of w, wz, wz^2
-//     K2 k_sp_scan    per slice: chunk offsets, coarse records {A_excl, B_excl, W, Z, offsets}, slice totals
-//     K3 k_sp_scatter per (chunk, slice): x -> (z, w), y -> (z, m) in coarse-bucket order
-//   level 2 (fine, one CTA per (coarse bucket, slice), everything in shared memory):
-//     K4 k_sp_fine    fine counting sort of the bucket's x and y, fp64 fine prefix sums, and for every target
-//                     t = -c [ z (A_lo - A_hi) - B_lo + B_hi + sum_{x in its fine bucket} w |x - z| ]
-//                     with A/B = sum w / sum w z over the x strictly below (lo) / above (hi) its fine bucket.
-// A bucket map b(z) = floor((z - zmin) * scale) computed with explicitly rounded fp32 ops is monotone in z,
-// which is all the identity needs (ties contribute |x - z| = 0 on either side).  The host runs the four
-// kernels over L2-sized slice sub-batches so that all scratch stays in the 126 MB L2.
+// Laplacian decomposition.  Sec. 3.2 / Alg. 2 computes, exactly,
+//     t_m = -c sum_n w_n |x_n - y_m|                                       (c = c_d, or alpha c_d)
+// by sorting the merged projections and running prefix sums.  Here: one thread-block CLUSTER of SP_C CTAs
+// per slice performs a one-pass MSD counting sort of both point sets into NB monotone value buckets of the
+// slice's x range, fp64 prefix sums over the x buckets, and a bucket-ordered evaluation of the targets:
+//     sum_n w_n |x_n - z| = [z A_lo - B_lo] + [B_hi - z A_hi] + sum_{x in z's bucket} w |x - z|
+// (A/B = sum w / sum w z over the x in buckets strictly left (lo) / right (hi) of z's bucket).
+//
+//  P0 zero local histograms (and this slice's bucket sums)
+//  P1 each CTA counts its quarter of x and y into local smem histograms
+//  P2 bucket ownership balanced by element count (coarse histograms exchanged through DSMEM); every owner
+//     sums the C histograms of its buckets (DSMEM reads), scans them, and writes each CTA's scatter cursors
+//     back into that CTA's shared memory (DSMEM writes)
+//  P3 each CTA scatters its quarter: (z,w) -> xs, (z,m) -> ys, bucket order (smem cursor atomics)
+//  P4 owners: warp-segmented fp64 sums of their buckets (coalesced) -> bucket records; slice totals
+//  P5 owners: exclusive fp64 scan (cross-CTA offsets through DSMEM) -> records {A_excl, B_excl, off, cnt, w, wz}
+//  P6 owners evaluate their targets in bucket order (lanes share buckets: broadcast loads), fp64 atomics
+// Only ~148/SP_C slices are live at a time, so the scratch (xs, ys, records: ~2 MB per slice) stays in L2.
+// The bucket map b(z) = floor((z - zmin) * scale) with explicitly rounded fp32 ops is monotone in z, which is
+// all the identity needs (ties contribute |x - z| = 0 on either side).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "kernels.h"
 
+namespace cg = cooperative_groups;
+
 namespace sks {
 
 namespace {
+
+constexpr int SP_C = 4;            // CTAs per slice (cluster)
+constexpr int SP_T = 1024;         // threads per CTA
+constexpr int SP_W = SP_T / 32;
+constexpr int NB = 8192;           // buckets per slice
+constexpr int NG = 256;            // ownership granules (NB / NG buckets each)
+constexpr int GB = NB / NG;
 
 __device__ __forceinline__ float key2f_dev(unsigned k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-__device__ __forceinline__ int coarse_of(float z, float zmin, float scale, int B1) {
+__device__ __forceinline__ int bin_of(float z, float zmin, float scale) {
   const float t = __fmul_rn(__fsub_rn(z, zmin), scale);
   const int b = (t >= 0.f) ? static_cast<int>(fminf(t, 2.0e9f)) : 0;
-  return b < B1 ? b : B1 - 1;
-}
-
-// fine index inside coarse bucket b1: monotone in z (each fp32 op rounds monotonically)
-__device__ __forceinline__ int fine_of(float z, float zmin, float scale, int b1, int F) {
-  const float t = __fmul_rn(__fsub_rn(z, zmin), scale);
-  const float u = __fmul_rn(__fsub_rn(t, static_cast<float>(b1)), static_cast<float>(F));
-  const int f = (u >= 0.f) ? static_cast<int>(fminf(u, 2.0e9f)) : 0;
-  return f < F ? f : F - 1;
+  return b < NB ? b : NB - 1;
 }
 
 template <typename T>
@@ -53,11 +60,17 @@ __device__ __forceinline__ T warp_incl_scan(T v) {
   return v;
 }
 
-// exclusive scan of n ints in smem by a CTA of NT threads (NT multiple of 32, <= 1024); returns the total
-template <int NT>
-__device__ int block_excl_scan(int* a, int n, int* wbuf) {
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block exclusive scan of a[0..n) (ints, smem) by all SP_T threads; returns the total
+__device__ int block_scan_int(int* a, int n, int* wbuf) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int per = (n + NT - 1) / NT;
+  const int per = (n + SP_T - 1) / SP_T;
   const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
   int loc = 0;
   for (int i = b0; i < b1; ++i) loc += a[i];
@@ -65,9 +78,9 @@ __device__ int block_excl_scan(int* a, int n, int* wbuf) {
   if (lane == 31) wbuf[wid] = inc;
   __syncthreads();
   if (wid == 0) {
-    const int v = lane < NT / 32 ? wbuf[lane] : 0;
+    const int v = wbuf[lane];
     const int vi = warp_incl_scan(v);
-    if (lane < NT / 32) wbuf[lane] = vi - v;
+    wbuf[lane] = vi - v;
     if (lane == 31) wbuf[32] = vi;
   }
   __syncthreads();
@@ -82,295 +95,329 @@ __device__ int block_excl_scan(int* a, int n, int* wbuf) {
   return total;
 }
 
-constexpr int SP_T = 256;     // threads of K1/K3/K4
-constexpr int K2_T = 256;     // threads of K2
-constexpr int FINE_CAP = 1024;
+struct __align__(16) Shared {
+  int hx[NB];          // local x histogram -> scatter cursors
+  int hy[NB];          // local y histogram -> scatter cursors
+  int ox[NB + 1];      // owner: absolute start of each owned x bucket (relative index b - lo)
+  int oy[NB + 1];
+  int gcount[NG];      // local granule counts (x + y), read by all ranks
+  int wbuf[33];
+  int tot_i[4];        // owner totals (x count, y count)
+  double tot_d[4];     // owner partial sums (W, Z, C)
+  double wsd[3][SP_W];
+};
 
-// ---------------------------------------------------------------- K1: coarse histograms + coarse fp64 sums
-__global__ void __launch_bounds__(SP_T) k_sp_count(SortArgs a) {
-  extern __shared__ unsigned char sm1[];
-  const int B1 = a.B1;
-  double* sums = reinterpret_cast<double*>(sm1);              // [B1][3]
-  int* cnt = reinterpret_cast<int*>(sums + 3 * B1);           // [B1][2]
-  const int c = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
-  for (int i = tid; i < 3 * B1; i += SP_T) sums[i] = 0.0;
-  for (int i = tid; i < 2 * B1; i += SP_T) cnt[i] = 0;
+__global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsum(SortArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Shared& S = *reinterpret_cast<Shared*>(smraw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int p = blockIdx.x / SP_C;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t N = a.zv.N, M = a.zv.M;
+  const float* zx = a.zv.zx + p * a.zv.ldx;
+  const float* zy = a.zv.zy + p * a.zv.ldy;
   const float zmin = key2f_dev(a.mm[p * 4 + 0]), zmax = key2f_dev(a.mm[p * 4 + 1]);
   const float range = zmax - zmin;
-  const float scale = (range > 0.f) ? static_cast<float>(B1) / range : 0.f;
-  if (c == 0 && tid == 0) { a.bpar[p * 2 + 0] = zmin; a.bpar[p * 2 + 1] = scale; }
-  __syncthreads();
-  const int64_t i0 = static_cast<int64_t>(c) * a.chunk;
-  const float* zx = a.zv.zx + p * a.zv.ldx;
-  const float* zy = a.zv.zy + p * a.zv.ldy;
-  const int64_t xe = min(a.zv.N, i0 + a.chunk), ye = min(a.zv.M, i0 + a.chunk);
-  for (int64_t i = i0 + tid; i < xe; i += SP_T) {
-    const float z = __ldg(zx + i), w = __ldg(a.w + i);
-    const int b = coarse_of(z, zmin, scale, B1);
-    const double wz = static_cast<double>(w) * z;
-    atomicAdd(&cnt[2 * b], 1);
-    atomicAdd(&sums[3 * b + 0], static_cast<double>(w));
-    atomicAdd(&sums[3 * b + 1], wz);
-    atomicAdd(&sums[3 * b + 2], wz * z);
-  }
-  for (int64_t i = i0 + tid; i < ye; i += SP_T) atomicAdd(&cnt[2 * coarse_of(__ldg(zy + i), zmin, scale, B1) + 1], 1);
-  __syncthreads();
-  const int64_t base = (static_cast<int64_t>(p) * a.nchunks + c) * B1;
-  for (int b = tid; b < B1; b += SP_T) {
-    reinterpret_cast<int2*>(a.ccnt)[base + b] = make_int2(cnt[2 * b], cnt[2 * b + 1]);
-    double* s = a.csum + (base + b) * 3;
-    s[0] = sums[3 * b];
-    s[1] = sums[3 * b + 1];
-    s[2] = sums[3 * b + 2];
-  }
-}
+  const float scale = (range > 0.f) ? static_cast<float>(NB) / range : 0.f;
+  BucketRec* rp = a.rec + static_cast<int64_t>(p) * NB;
+  float2* xsp = a.xs + static_cast<int64_t>(p) * N;
+  float2* ysp = a.ys + static_cast<int64_t>(p) * M;
+  if (rank == 0 && tid == 0) { a.bpar[p * 2 + 0] = zmin; a.bpar[p * 2 + 1] = scale; }
 
-// ---------------------------------------------------------------- K2: per-slice offsets + coarse records
-__global__ void __launch_bounds__(K2_T) k_sp_scan(SortArgs a) {
-  __shared__ int wi[33];
-  __shared__ double wd[3][K2_T / 32];
-  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int B1 = a.B1, nc = a.nchunks;
-  const int E = B1 / K2_T;   // B1 is a power of two >= 256
-  const int b0 = tid * E;
-  int2* cc = reinterpret_cast<int2*>(a.ccnt) + static_cast<int64_t>(p) * nc * B1;
-  const double* cs = a.csum + static_cast<int64_t>(p) * nc * B1 * 3;
-  CoarseRec* cr = a.crec + static_cast<int64_t>(p) * B1;
-  // per bucket: chunk-local exclusive offsets (in place) and totals
-  int tx = 0, ty = 0;
-  double tW = 0.0, tZ = 0.0, tC = 0.0;
-  for (int e = 0; e < E; ++e) {
-    const int b = b0 + e;
-    int rx = 0, ry = 0;
-    double W = 0.0, Z = 0.0, C = 0.0;
-    for (int c = 0; c < nc; ++c) {
-      const int2 v = cc[static_cast<int64_t>(c) * B1 + b];
-      cc[static_cast<int64_t>(c) * B1 + b] = make_int2(rx, ry);
-      rx += v.x;
-      ry += v.y;
-      const double* s = cs + (static_cast<int64_t>(c) * B1 + b) * 3;
-      W += s[0];
-      Z += s[1];
-      C += s[2];
+  // ---- P0
+  for (int b = tid; b < NB; b += SP_T) { S.hx[b] = 0; S.hy[b] = 0; }
+  for (int b = rank * (NB / SP_C) + tid; b < (rank + 1) * (NB / SP_C); b += SP_T)
+    reinterpret_cast<double2*>(rp + b)[0] = make_double2(0.0, 0.0);
+  __syncthreads();
+
+  // ---- P1: count my quarter
+  const int64_t x0 = N * rank / SP_C, x1 = N * (rank + 1) / SP_C;
+  const int64_t y0 = M * rank / SP_C, y1 = M * (rank + 1) / SP_C;
+  constexpr int U = 8;
+  for (int64_t base = x0; base < x1; base += U * SP_T) {
+    float zz[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SP_T;
+      zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
     }
-    CoarseRec r;
-    r.A = 0.0; r.B = 0.0; r.W = W; r.Z = Z;
-    r.xoff = 0; r.xcnt = rx; r.yoff = 0; r.ycnt = ry;
-    cr[b] = r;
-    tx += rx; ty += ry;
-    tW += W; tZ += Z; tC += C;
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (base + tid + k * SP_T < x1) atomicAdd(&S.hx[bin_of(zz[k], zmin, scale)], 1);
   }
-  // block exclusive scans of (x count, y count) and (W, Z); totals
-  const int ix = warp_incl_scan(tx), iy = warp_incl_scan(ty);
-  const double iW = warp_incl_scan(tW), iZ = warp_incl_scan(tZ), iC = warp_incl_scan(tC);
-  __shared__ int wix[K2_T / 32], wiy[K2_T / 32];
-  if (lane == 31) { wix[wid] = ix; wiy[wid] = iy; wd[0][wid] = iW; wd[1][wid] = iZ; wd[2][wid] = iC; }
+  for (int64_t base = y0; base < y1; base += U * SP_T) {
+    float zz[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SP_T;
+      zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (base + tid + k * SP_T < y1) atomicAdd(&S.hy[bin_of(zz[k], zmin, scale)], 1);
+  }
+  __syncthreads();
+  for (int g = tid; g < NG; g += SP_T) {
+    int c = 0;
+    for (int b = g * GB; b < (g + 1) * GB; ++b) c += S.hx[b] + S.hy[b];
+    S.gcount[g] = c;
+  }
+  cluster.sync();
+
+  // ---- P2: ownership by element count (all ranks compute the same split), owner scans, cursors
+  int glo[SP_C + 1];
+  {
+    // every thread walks the global granule counts (NG x SP_C remote reads, tiny)
+    __shared__ int gtot[NG];
+    for (int g = tid; g < NG; g += SP_T) {
+      int c = 0;
+      for (int r = 0; r < SP_C; ++r) c += cluster.map_shared_rank(&S, r)->gcount[g];
+      gtot[g] = c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int total = 0;
+      for (int g = 0; g < NG; ++g) total += gtot[g];
+      int run = 0, r = 1;
+      S.wbuf[0] = 0;
+      for (int g = 0; g < NG && r < SP_C; ++g) {
+        run += gtot[g];
+        while (r < SP_C && static_cast<int64_t>(run) * SP_C >= static_cast<int64_t>(total) * r) S.wbuf[r++] = g + 1;
+      }
+      while (r < SP_C) S.wbuf[r++] = NG;
+      S.wbuf[SP_C] = NG;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r <= SP_C; ++r) glo[r] = S.wbuf[r] * GB;
+    __syncthreads();
+  }
+  const int lo = glo[rank], hi = glo[rank + 1], nown = hi - lo;
+  // owner: totals of its buckets over all ranks
+  for (int j = tid; j < nown; j += SP_T) {
+    int tx = 0, ty = 0;
+#pragma unroll
+    for (int r = 0; r < SP_C; ++r) {
+      const Shared* R = cluster.map_shared_rank(&S, r);
+      tx += R->hx[lo + j];
+      ty += R->hy[lo + j];
+    }
+    S.ox[j] = tx;
+    S.oy[j] = ty;
+  }
+  __syncthreads();
+  const int Sx = block_scan_int(S.ox, nown, S.wbuf);
+  const int Sy = block_scan_int(S.oy, nown, S.wbuf);
+  if (tid == 0) { S.tot_i[0] = Sx; S.tot_i[1] = Sy; }
+  cluster.sync();   // all owners' totals published; all histogram reads of P2 done
+  int bx = 0, by = 0;
+  for (int r = 0; r < rank; ++r) {
+    const Shared* R = cluster.map_shared_rank(&S, r);
+    bx += R->tot_i[0];
+    by += R->tot_i[1];
+  }
+  for (int j = tid; j < nown; j += SP_T) {
+    S.ox[j] += bx;
+    S.oy[j] += by;
+  }
+  if (tid == 0) { S.ox[nown] = bx + Sx; S.oy[nown] = by + Sy; }
+  __syncthreads();
+  for (int j = tid; j < nown; j += SP_T) {
+    int rx = S.ox[j], ry = S.oy[j];
+#pragma unroll
+    for (int r = 0; r < SP_C; ++r) {
+      Shared* R = cluster.map_shared_rank(&S, r);
+      const int hx = R->hx[lo + j], hy = R->hy[lo + j];
+      R->hx[lo + j] = rx;
+      R->hy[lo + j] = ry;
+      rx += hx;
+      ry += hy;
+    }
+  }
+  cluster.sync();   // cursors written into every rank
+
+  // ---- P3: scatter my quarter
+  for (int64_t base = x0; base < x1; base += U * SP_T) {
+    float zz[U], ww[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SP_T;
+      zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
+      ww[k] = (i < x1) ? __ldg(a.w + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (base + tid + k * SP_T < x1) {
+        const int pos = atomicAdd(&S.hx[bin_of(zz[k], zmin, scale)], 1);
+        xsp[pos] = make_float2(zz[k], ww[k]);
+      }
+  }
+  for (int64_t base = y0; base < y1; base += U * SP_T) {
+    float zz[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SP_T;
+      zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + tid + k * SP_T;
+      if (i < y1) {
+        const int pos = atomicAdd(&S.hy[bin_of(zz[k], zmin, scale)], 1);
+        ysp[pos] = make_float2(zz[k], __int_as_float(static_cast<int>(i)));
+      }
+    }
+  }
+  cluster.sync();   // (release/acquire at cluster scope: the scattered xs/ys are visible to the owners)
+
+  // ---- P4: owner bucket sums (fp64), coalesced over its contiguous x range
+  double tA = 0.0, tB = 0.0, tC = 0.0;
+  {
+    const int s0g = S.ox[0], s1g = S.ox[nown];
+    const int per = ((s1g - s0g + SP_W - 1) / SP_W + 31) / 32 * 32;
+    const int s0 = min(s1g, s0g + wid * per), s1 = min(s1g, s0 + per);
+    for (int base0 = s0; base0 < s1; base0 += 4 * 32) {
+      float2 ee[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = base0 + k * 32 + lane;
+        ee[k] = (i < s1) ? __ldcg(xsp + i) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = base0 + k * 32 + lane;
+        const bool valid = i < s1;
+        const float2 e = ee[k];
+        const int key = valid ? bin_of(e.x, zmin, scale) : -1 - lane;
+        double sa = e.y, sb = static_cast<double>(e.y) * e.x;
+        tA += sa;
+        tB += sb;
+        tC += sb * e.x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double na = __shfl_up_sync(0xffffffffu, sa, o), nbz = __shfl_up_sync(0xffffffffu, sb, o);
+          const int nk = __shfl_up_sync(0xffffffffu, key, o);
+          if (lane >= o && nk == key) { sa += na; sb += nbz; }   // keys are sorted along xs
+        }
+        const int next = __shfl_down_sync(0xffffffffu, key, 1);
+        if (valid && (lane == 31 || next != key)) {
+          atomicAdd(&rp[key].A, sa);
+          atomicAdd(&rp[key].B, sb);
+        }
+      }
+    }
+  }
+  tA = warp_sum(tA);
+  tB = warp_sum(tB);
+  tC = warp_sum(tC);
+  if (lane == 0) { S.wsd[0][wid] = tA; S.wsd[1][wid] = tB; S.wsd[2][wid] = tC; }
   __syncthreads();
   if (tid == 0) {
-    int sx = 0, sy = 0;
-    double sW = 0, sZ = 0, sC = 0;
-    for (int q = 0; q < K2_T / 32; ++q) {
-      const int vx = wix[q], vy = wiy[q];
-      const double vW = wd[0][q], vZ = wd[1][q], vC = wd[2][q];
-      wix[q] = sx; wiy[q] = sy; wd[0][q] = sW; wd[1][q] = sZ; wd[2][q] = sC;
-      sx += vx; sy += vy; sW += vW; sZ += vZ; sC += vC;
+    double sa = 0, sb = 0, sc = 0;
+    for (int q = 0; q < SP_W; ++q) { sa += S.wsd[0][q]; sb += S.wsd[1][q]; sc += S.wsd[2][q]; }
+    S.tot_d[0] = sa; S.tot_d[1] = sb; S.tot_d[2] = sc;
+  }
+  cluster.sync();   // partial sums of all owners published (and all bucket-sum atomics done)
+  double TA = 0, TB = 0, TC = 0, PA = 0, PB = 0;
+#pragma unroll
+  for (int r = 0; r < SP_C; ++r) {
+    const Shared* R = cluster.map_shared_rank(&S, r);
+    TA += R->tot_d[0]; TB += R->tot_d[1]; TC += R->tot_d[2];
+    if (r < rank) { PA += R->tot_d[0]; PB += R->tot_d[1]; }
+  }
+  if (rank == 0 && tid == 0) a.tot[p] = SliceTot{TA, TB, TC, 0.0};
+
+  // ---- P5: exclusive fp64 scan over my buckets -> records
+  {
+    const int per = (nown + SP_T - 1) / SP_T;
+    const int j0 = min(nown, tid * per), j1 = min(nown, j0 + per);
+    double lA = 0.0, lB = 0.0;
+    for (int j = j0; j < j1; ++j) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + lo + j));
+      lA += v.x;
+      lB += v.y;
     }
-    a.tot[p] = SliceTot{sW, sZ, sC, 0.0};
-    wi[0] = sx;
+    const double iA = warp_incl_scan(lA), iB = warp_incl_scan(lB);
+    if (lane == 31) { S.wsd[0][wid] = iA; S.wsd[1][wid] = iB; }
+    __syncthreads();
+    if (wid == 0) {
+      const double va = S.wsd[0][lane], vb = S.wsd[1][lane];
+      const double ia = warp_incl_scan(va), ib = warp_incl_scan(vb);
+      S.wsd[0][lane] = ia - va;
+      S.wsd[1][lane] = ib - vb;
+    }
+    __syncthreads();
+    double rA = PA + S.wsd[0][wid] + iA - lA, rB = PB + S.wsd[1][wid] + iB - lB;
+    for (int j = j0; j < j1; ++j) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + lo + j));
+      BucketRec r;
+      r.A = rA;
+      r.B = rB;
+      r.off = S.ox[j];
+      r.cnt = S.ox[j + 1] - S.ox[j];
+      r.w = static_cast<float>(v.x);
+      r.wz = static_cast<float>(v.y);
+      rp[lo + j] = r;
+      rA += v.x;
+      rB += v.y;
+    }
   }
   __syncthreads();
-  int ox = wix[wid] + ix - tx, oy = wiy[wid] + iy - ty;
-  double oW = wd[0][wid] + iW - tW, oZ = wd[1][wid] + iZ - tZ;
-  for (int e = 0; e < E; ++e) {
-    const int b = b0 + e;
-    CoarseRec r = cr[b];
-    r.A = oW; r.B = oZ; r.xoff = ox; r.yoff = oy;
-    cr[b] = r;
-    for (int c = 0; c < nc; ++c) {
-      int2 v = cc[static_cast<int64_t>(c) * B1 + b];
-      cc[static_cast<int64_t>(c) * B1 + b] = make_int2(v.x + ox, v.y + oy);
+
+  // ---- P6: my targets in bucket order
+  const int t0 = S.oy[0], t1 = S.oy[nown];
+  for (int base = t0; base < t1; base += 2 * SP_T) {
+    float2 ee[2];
+    int bb[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = base + tid + k * SP_T;
+      ee[k] = (i < t1) ? __ldcg(ysp + i) : make_float2(zmin, 0.f);
+      bb[k] = bin_of(ee[k].x, zmin, scale);
     }
-    ox += r.xcnt; oy += r.ycnt; oW += r.W; oZ += r.Z;
-  }
-}
-
-// ---------------------------------------------------------------- K3: scatter into coarse-bucket order
-__global__ void __launch_bounds__(SP_T) k_sp_scatter(SortArgs a) {
-  extern __shared__ int cur[];   // [B1][2]
-  const int B1 = a.B1;
-  const int c = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
-  const int64_t base = (static_cast<int64_t>(p) * a.nchunks + c) * B1;
-  for (int b = tid; b < B1; b += SP_T) {
-    const int2 v = reinterpret_cast<const int2*>(a.ccnt)[base + b];
-    cur[2 * b] = v.x;
-    cur[2 * b + 1] = v.y;
-  }
-  __syncthreads();
-  const float zmin = a.bpar[p * 2 + 0], scale = a.bpar[p * 2 + 1];
-  const int64_t i0 = static_cast<int64_t>(c) * a.chunk;
-  const float* zx = a.zv.zx + p * a.zv.ldx;
-  const float* zy = a.zv.zy + p * a.zv.ldy;
-  float2* xs = a.xs + static_cast<int64_t>(p) * a.zv.N;
-  float2* ys = a.ys + static_cast<int64_t>(p) * a.zv.M;
-  const int64_t xe = min(a.zv.N, i0 + a.chunk), ye = min(a.zv.M, i0 + a.chunk);
-  for (int64_t i = i0 + tid; i < xe; i += SP_T) {
-    const float z = __ldg(zx + i);
-    const int pos = atomicAdd(&cur[2 * coarse_of(z, zmin, scale, B1)], 1);
-    xs[pos] = make_float2(z, __ldg(a.w + i));
-  }
-  for (int64_t i = i0 + tid; i < ye; i += SP_T) {
-    const float z = __ldg(zy + i);
-    const int pos = atomicAdd(&cur[2 * coarse_of(z, zmin, scale, B1) + 1], 1);
-    ys[pos] = make_float2(z, __int_as_float(static_cast<int>(i)));
-  }
-}
-
-// ---------------------------------------------------------------- K4: fine level + evaluation
-constexpr size_t FINE_SMEM = FINE_CAP * (2 * sizeof(float2) + 2 * sizeof(int) + 2 * sizeof(double) + 2 * sizeof(float));
-
-__global__ void __launch_bounds__(SP_T) k_sp_fine(SortArgs a) {
-  extern __shared__ double sm4[];
-  double* fA = sm4;
-  double* fB = fA + FINE_CAP;
-  float2* xsrt = reinterpret_cast<float2*>(fB + FINE_CAP);
-  float2* ysrt = xsrt + FINE_CAP;
-  int* cx = reinterpret_cast<int*>(ysrt + FINE_CAP);
-  int* cy = cx + FINE_CAP;
-  float* fW = reinterpret_cast<float*>(cy + FINE_CAP);
-  float* fZ = fW + FINE_CAP;
-  __shared__ int wbuf[33];
-  __shared__ double wdd[2][SP_T / 32];
-  const int b1 = blockIdx.x, p = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const CoarseRec r = a.crec[static_cast<int64_t>(p) * a.B1 + b1];
-  const int nx = r.xcnt, ny = r.ycnt;
-  if (ny == 0) return;
-  const SliceTot T = a.tot[p];
-  const float zmin = a.bpar[p * 2 + 0], scale = a.bpar[p * 2 + 1];
-  const float2* xg = a.xs + static_cast<int64_t>(p) * a.zv.N + r.xoff;
-  const float2* yg = a.ys + static_cast<int64_t>(p) * a.zv.M + r.yoff;
-  const int64_t M = a.zv.M;
-  if (nx > FINE_CAP || ny > FINE_CAP) {
-    // oversize coarse bucket (extreme concentration / duplicates): direct sums over the bucket's x's
-    const double Ahi = T.A - r.A - r.W, Bhi = T.B - r.B - r.Z;
-    for (int j = tid; j < ny; j += SP_T) {
-      const float2 e = yg[j];
-      const float z = e.x;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = base + tid + k * SP_T;
+      if (i >= t1) continue;
+      const BucketRec R = rp[bb[k]];
+      const float z = ee[k].x;
+      const int64_t m = __float_as_int(ee[k].y);
       const double zd = z;
-      double same = 0.0;
-      for (int i = 0; i < nx; ++i) {
-        const float2 q = xg[i];
-        same += static_cast<double>(q.y) * fabs(static_cast<double>(q.x) - zd);
+      const double Ahi = TA - R.A - R.w, Bhi = TB - R.B - R.wz;
+      const float2* xp = xsp + R.off;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      int j = 0;
+      for (; j + 4 <= R.cnt; j += 4) {
+        const float2 q0 = xp[j], q1 = xp[j + 1], q2 = xp[j + 2], q3 = xp[j + 3];
+        s0 = fmaf(q0.y, fabsf(q0.x - z), s0);
+        s1 = fmaf(q1.y, fabsf(q1.x - z), s1);
+        s2 = fmaf(q2.y, fabsf(q2.x - z), s2);
+        s3 = fmaf(q3.y, fabsf(q3.x - z), s3);
       }
-      const double t = -a.coef * ((zd * r.A - r.B) + (Bhi - zd * Ahi) + same);
-      const int64_t m = __float_as_int(e.y);
+      for (; j < R.cnt; ++j) {
+        const float2 q = xp[j];
+        s0 = fmaf(q.y, fabsf(q.x - z), s0);
+      }
+      const double same = static_cast<double>((s0 + s1) + (s2 + s3));
+      const double t = -a.coef * ((zd * R.A - R.B) + (Bhi - zd * Ahi) + same);
       if (a.s64) atomicAdd(a.s64 + m, t);
       if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
     }
-    return;
-  }
-  int F = 16;
-  while (F < nx && F < FINE_CAP) F <<= 1;
-  for (int f = tid; f < F; f += SP_T) { cx[f] = 0; cy[f] = 0; }
-  __syncthreads();
-  for (int i = tid; i < nx; i += SP_T) atomicAdd(&cx[fine_of(xg[i].x, zmin, scale, b1, F)], 1);
-  for (int j = tid; j < ny; j += SP_T) atomicAdd(&cy[fine_of(yg[j].x, zmin, scale, b1, F)], 1);
-  __syncthreads();
-  block_excl_scan<SP_T>(cx, F, wbuf);
-  block_excl_scan<SP_T>(cy, F, wbuf);
-  for (int i = tid; i < nx; i += SP_T) {
-    const float2 e = xg[i];
-    xsrt[atomicAdd(&cx[fine_of(e.x, zmin, scale, b1, F)], 1)] = e;
-  }
-  for (int j = tid; j < ny; j += SP_T) {
-    const float2 e = yg[j];
-    ysrt[atomicAdd(&cy[fine_of(e.x, zmin, scale, b1, F)], 1)] = e;
-  }
-  __syncthreads();
-  // fine bucket sums (fp64) and exclusive prefix; after the scatter cx[f] = end of fine bucket f
-  {
-    const int per = (F + SP_T - 1) / SP_T;
-    const int f0 = min(F, tid * per), f1 = min(F, f0 + per);
-    double lA = 0.0, lB = 0.0;
-    for (int f = f0; f < f1; ++f) {
-      const int lo = f ? cx[f - 1] : 0, hi = cx[f];
-      double W = 0.0, Z = 0.0;
-      for (int i = lo; i < hi; ++i) {
-        const float2 q = xsrt[i];
-        W += q.y;
-        Z += static_cast<double>(q.y) * q.x;
-      }
-      fW[f] = static_cast<float>(W);
-      fZ[f] = static_cast<float>(Z);
-      fA[f] = W;   // temporarily the bucket sums
-      fB[f] = Z;
-      lA += W;
-      lB += Z;
-    }
-    const double iA = warp_incl_scan(lA), iB = warp_incl_scan(lB);
-    if (lane == 31) { wdd[0][wid] = iA; wdd[1][wid] = iB; }
-    __syncthreads();
-    if (tid == 0) {
-      double sa = 0.0, sb = 0.0;
-      for (int q = 0; q < SP_T / 32; ++q) {
-        const double va = wdd[0][q], vb = wdd[1][q];
-        wdd[0][q] = sa;
-        wdd[1][q] = sb;
-        sa += va;
-        sb += vb;
-      }
-    }
-    __syncthreads();
-    double rA = wdd[0][wid] + iA - lA, rB = wdd[1][wid] + iB - lB;
-    for (int f = f0; f < f1; ++f) {
-      const double W = fA[f], Z = fB[f];
-      fA[f] = rA;
-      fB[f] = rB;
-      rA += W;
-      rB += Z;
-    }
-  }
-  __syncthreads();
-  // targets in fine-bucket order (lanes share fine buckets: broadcast smem reads)
-  for (int j = tid; j < ny; j += SP_T) {
-    const float2 e = ysrt[j];
-    const float z = e.x;
-    const int f = fine_of(z, zmin, scale, b1, F);
-    const int lo = f ? cx[f - 1] : 0, hi = cx[f];
-    float same = 0.f;
-    for (int i = lo; i < hi; ++i) {
-      const float2 q = xsrt[i];
-      same = fmaf(q.y, fabsf(q.x - z), same);
-    }
-    const double zd = z;
-    const double Alo = r.A + fA[f], Blo = r.B + fB[f];
-    const double Ahi = T.A - Alo - fW[f], Bhi = T.B - Blo - fZ[f];
-    const double t = -a.coef * ((zd * Alo - Blo) + (Bhi - zd * Ahi) + static_cast<double>(same));
-    const int64_t m = __float_as_int(e.y);
-    if (a.s64) atomicAdd(a.s64 + m, t);
-    if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
   }
 }
 
 }  // namespace
 
-int sortpath_coarse_buckets(int64_t N) {
-  int64_t b = 256;
-  while (b < N / 64 && b < 4096) b <<= 1;
-  return static_cast<int>(b);
-}
+int sortpath_buckets() { return NB; }
 
 cudaError_t launch_sortpath(const SortArgs& a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sp_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 32);
-    cudaFuncSetAttribute(k_sp_fine, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(FINE_SMEM));
+    cudaFuncSetAttribute(k_sortsum, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Shared)));
     attr = true;
   }
-  const dim3 gc(static_cast<unsigned>(a.nchunks), static_cast<unsigned>(a.np));
-  k_sp_count<<<gc, SP_T, static_cast<size_t>(a.B1) * 32, st>>>(a);
-  k_sp_scan<<<a.np, K2_T, 0, st>>>(a);
-  k_sp_scatter<<<gc, SP_T, static_cast<size_t>(a.B1) * 8, st>>>(a);
-  k_sp_fine<<<dim3(static_cast<unsigned>(a.B1), static_cast<unsigned>(a.np)), SP_T, FINE_SMEM, st>>>(a);
+  k_sortsum<<<a.np * SP_C, SP_T, sizeof(Shared), st>>>(a);
   return cudaGetLastError();
 }
 
