@@ -140,9 +140,10 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb)
   L.mm = take(sizeof(unsigned) * 4 * nbat);
   if (with_Z) L.Z = take(sizeof(float) * (N + M) * nbat);
   if (pt.sort || pt.moment) {
-    L.xs = take(sizeof(float2) * N * nbat);
-    L.ys = take(sizeof(float2) * M * nbat);
-    L.rec = take(sizeof(sks::BucketRec) * nb * static_cast<size_t>(nbat));
+    const int slots = sks::sortpath_slots(nbat);
+    L.xs = take(sizeof(float2) * N * slots);
+    L.ys = take(sizeof(float2) * M * slots);
+    L.rec = take(sizeof(sks::BucketRec) * nb * static_cast<size_t>(slots));
     L.tot = take(sizeof(sks::SliceTot) * static_cast<size_t>(nbat));
     L.bpar = take(sizeof(float) * 2 * nbat);
   }
@@ -387,7 +388,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       sa.s64 = s64;
       sa.per_slice_out = tps;
       ProfScope ps(PS_BUCKET, st);
-      SKS_CUDA(sks::launch_sortpath(sa, st));
+      SKS_CUDA(sks::launch_sortpath(sa, sks::sortpath_slots(nbat), st));
       ++launches;
       ea.tot = sa.tot;
     }

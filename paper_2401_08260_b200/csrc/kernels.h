@@ -55,17 +55,18 @@ struct SortArgs {
   const float* w;
   int np;
   const unsigned* mm;    // [np][4] ranges
-  float2* xs;            // [np][N] (z, w) in bucket order
-  float2* ys;            // [np][M] (z, m) in bucket order
-  BucketRec* rec;        // [np][NB]
+  float2* xs;            // [slots][N] (z, w) in bucket order
+  float2* ys;            // [slots][M] (z, m) in bucket order
+  BucketRec* rec;        // [slots][NB]
   SliceTot* tot;         // [np]
-  float* bpar;           // [np][2] bucket map (zmin, scale)
+  float* bpar;           // [np][2] (zmin, granule scale)
   double coef;           // t = -coef * sum_n w_n |x_n - z|   (c_d, or alpha c_d for the Laplacian part)
   double* s64;           // accumulate t into s64[m] (fp64 atomics), or
   float* per_slice_out;  // store t into per_slice_out[p*M + m]
 };
 int sortpath_buckets();
-cudaError_t launch_sortpath(const SortArgs& a, cudaStream_t st);
+int sortpath_slots(int np);   // scratch slots (co-resident clusters) used for np slices
+cudaError_t launch_sortpath(const SortArgs& a, int slots, cudaStream_t st);
 
 // row a2: D[p][k] = c_k(tau_p) / Phi_k^2 on the band of slice p, else 0  (k = 0..n/2)
 cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* phi2inv, int n, float* D,

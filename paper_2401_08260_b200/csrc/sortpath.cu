@@ -7,16 +7,18 @@
 //     sum_n w_n |x_n - z| = [z A_lo - B_lo] + [B_hi - z A_hi] + sum_{x in z's bucket} w |x - z|
 // (A/B = sum w / sum w z over the x in buckets strictly left (lo) / right (hi) of z's bucket).
 //
-//  P0 zero local histograms (and this slice's bucket sums)
-//  P1 each CTA counts its quarter of x and y into local smem histograms
+//  P0 granule histograms -> count-balanced bucket map (NB buckets allotted to NG equal-width granules in
+//     proportion to their x counts; linear inside a granule) and bucket ownership (balanced by x + y count)
+//  P1 each CTA counts its quarter of x and y into local smem bucket histograms
 //  P2 bucket ownership balanced by element count (coarse histograms exchanged through DSMEM); every owner
 //     sums the C histograms of its buckets (DSMEM reads), scans them, and writes each CTA's scatter cursors
 //     back into that CTA's shared memory (DSMEM writes)
 //  P3 each CTA scatters its quarter: (z,w) -> xs, (z,m) -> ys, bucket order (smem cursor atomics)
-//  P4 owners: warp-segmented fp64 sums of their buckets (coalesced) -> bucket records; slice totals
-//  P5 owners: exclusive fp64 scan (cross-CTA offsets through DSMEM) -> records {A_excl, B_excl, off, cnt, w, wz}
+//  P4 owners: fp64 sums of their buckets, exclusive scan (cross-CTA offsets through DSMEM)
+//  P5 records {A_excl, B_excl, off, cnt, w, wz}; slice totals
 //  P6 owners evaluate their targets in bucket order (lanes share buckets: broadcast loads), fp64 atomics
-// Only ~148/SP_C slices are live at a time, so the scratch (xs, ys, records: ~2 MB per slice) stays in L2.
+// Persistent: one cluster per scratch slot (as many as can be co-resident, ~148/SP_C), each walking its
+// slices; the slots' scratch (xs, ys, records: ~2 MB each) is reused and stays in L2.
 // The bucket map b(z) = floor((z - zmin) * scale) with explicitly rounded fp32 ops is monotone in z, which is
 // all the identity needs (ties contribute |x - z| = 0 on either side).
 #include <cooperative_groups.h>
@@ -36,17 +38,36 @@ constexpr int SP_C = 4;            // CTAs per slice (cluster)
 constexpr int SP_T = 1024;         // threads per CTA
 constexpr int SP_W = SP_T / 32;
 constexpr int NB = 8192;           // buckets per slice
-constexpr int NG = 256;            // ownership granules (NB / NG buckets each)
-constexpr int GB = NB / NG;
+constexpr int NG = 256;            // equal-width granules; buckets are allotted to granules by x count
 
 __device__ __forceinline__ float key2f_dev(unsigned k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-__device__ __forceinline__ int bin_of(float z, float zmin, float scale) {
-  const float t = __fmul_rn(__fsub_rn(z, zmin), scale);
-  const int b = (t >= 0.f) ? static_cast<int>(fminf(t, 2.0e9f)) : 0;
-  return b < NB ? b : NB - 1;
+// granule of z: t = (z - zmin) * gscale in [0, NG) for z in the x range (clamped outside)
+__device__ __forceinline__ float gran_t(float z, float zmin, float gscale) {
+  return __fmul_rn(__fsub_rn(z, zmin), gscale);
+}
+
+// count-balanced bucket map: granule g owns buckets [gb.x, gb.x + gb.y); inside a granule the map is linear.
+// Monotone non-decreasing in z: t is monotone (rounded fp32 ops), floor(t) is monotone, and every bucket of
+// granule g precedes every bucket of granule g+1.
+__device__ __forceinline__ int bin_of(float z, float zmin, float gscale, const int2* __restrict__ gtab) {
+  const float t = gran_t(z, zmin, gscale);
+  int g = (t >= 0.f) ? static_cast<int>(fminf(t, 1.0e9f)) : 0;
+  g = g < NG ? g : NG - 1;
+  const int2 gb = gtab[g];
+  if (gb.y == 0) return min(gb.x, NB - 1);
+  const float u = __fmul_rn(__fsub_rn(t, static_cast<float>(g)), static_cast<float>(gb.y));
+  int f = (u >= 0.f) ? static_cast<int>(fminf(u, 1.0e9f)) : 0;
+  f = f < gb.y ? f : gb.y - 1;
+  return gb.x + f;
+}
+
+__device__ __forceinline__ int gran_of(float z, float zmin, float gscale) {
+  const float t = gran_t(z, zmin, gscale);
+  const int g = (t >= 0.f) ? static_cast<int>(fminf(t, 1.0e9f)) : 0;
+  return g < NG ? g : NG - 1;
 }
 
 template <typename T>
@@ -98,12 +119,14 @@ __device__ int block_scan_int(int* a, int n, int* wbuf) {
 struct __align__(16) Shared {
   int hx[NB];          // local x histogram -> scatter cursors
   int hy[NB];          // local y histogram -> scatter cursors
-  int ox[NB + 1];      // owner: absolute start of each owned x bucket (relative index b - lo)
+  int ox[NB + 1];      // owner: absolute start of each owned x bucket (index b - lo)
   int oy[NB + 1];
-  int gcount[NG];      // local granule counts (x + y), read by all ranks
-  int wbuf[33];
-  int tot_i[4];        // owner totals (x count, y count)
-  double tot_d[4];     // owner partial sums (W, Z, C)
+  int2 gtab[NG];       // bucket map: granule -> (first bucket, #buckets)
+  int gx[NG];          // local granule counts of x (then: global, all ranks)
+  int gxy[NG];         // local granule counts of x + y (work balance)
+  int wbuf[34];
+  int tot_i[4];
+  double tot_d[4];
   double wsd[3][SP_W];
 };
 
@@ -112,298 +135,293 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
   Shared& S = *reinterpret_cast<Shared*>(smraw);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
-  const int p = blockIdx.x / SP_C;
+  const int slot = blockIdx.x / SP_C, nslots = gridDim.x / SP_C;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t N = a.zv.N, M = a.zv.M;
-  const float* zx = a.zv.zx + p * a.zv.ldx;
-  const float* zy = a.zv.zy + p * a.zv.ldy;
-  const float zmin = key2f_dev(a.mm[p * 4 + 0]), zmax = key2f_dev(a.mm[p * 4 + 1]);
-  const float range = zmax - zmin;
-  const float scale = (range > 0.f) ? static_cast<float>(NB) / range : 0.f;
-  BucketRec* rp = a.rec + static_cast<int64_t>(p) * NB;
-  float2* xsp = a.xs + static_cast<int64_t>(p) * N;
-  float2* ysp = a.ys + static_cast<int64_t>(p) * M;
-  if (rank == 0 && tid == 0) { a.bpar[p * 2 + 0] = zmin; a.bpar[p * 2 + 1] = scale; }
-
-  // ---- P0
-  for (int b = tid; b < NB; b += SP_T) { S.hx[b] = 0; S.hy[b] = 0; }
-  for (int b = rank * (NB / SP_C) + tid; b < (rank + 1) * (NB / SP_C); b += SP_T)
-    reinterpret_cast<double2*>(rp + b)[0] = make_double2(0.0, 0.0);
-  __syncthreads();
-
-  // ---- P1: count my quarter
+  // persistent: this cluster owns scratch slot `slot` and walks the slices slot, slot + nslots, ...
+  BucketRec* rp = a.rec + static_cast<int64_t>(slot) * NB;
+  float2* xsp = a.xs + static_cast<int64_t>(slot) * N;
+  float2* ysp = a.ys + static_cast<int64_t>(slot) * M;
+  constexpr int U = 8;
   const int64_t x0 = N * rank / SP_C, x1 = N * (rank + 1) / SP_C;
   const int64_t y0 = M * rank / SP_C, y1 = M * (rank + 1) / SP_C;
-  constexpr int U = 8;
-  for (int64_t base = x0; base < x1; base += U * SP_T) {
-    float zz[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SP_T;
-      zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (base + tid + k * SP_T < x1) atomicAdd(&S.hx[bin_of(zz[k], zmin, scale)], 1);
-  }
-  for (int64_t base = y0; base < y1; base += U * SP_T) {
-    float zz[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SP_T;
-      zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (base + tid + k * SP_T < y1) atomicAdd(&S.hy[bin_of(zz[k], zmin, scale)], 1);
-  }
-  __syncthreads();
-  for (int g = tid; g < NG; g += SP_T) {
-    int c = 0;
-    for (int b = g * GB; b < (g + 1) * GB; ++b) c += S.hx[b] + S.hy[b];
-    S.gcount[g] = c;
-  }
-  cluster.sync();
 
-  // ---- P2: ownership by element count (all ranks compute the same split), owner scans, cursors
-  int glo[SP_C + 1];
-  {
-    // every thread walks the global granule counts (NG x SP_C remote reads, tiny)
-    __shared__ int gtot[NG];
-    for (int g = tid; g < NG; g += SP_T) {
-      int c = 0;
-      for (int r = 0; r < SP_C; ++r) c += cluster.map_shared_rank(&S, r)->gcount[g];
-      gtot[g] = c;
-    }
+  for (int p = slot; p < a.np; p += nslots) {
+    const float* zx = a.zv.zx + p * a.zv.ldx;
+    const float* zy = a.zv.zy + p * a.zv.ldy;
+    const float zmin = key2f_dev(a.mm[p * 4 + 0]), zmax = key2f_dev(a.mm[p * 4 + 1]);
+    const float range = zmax - zmin;
+    const float gscale = (range > 0.f) ? static_cast<float>(NG) / range : 0.f;
+    if (rank == 0 && tid == 0) { a.bpar[p * 2 + 0] = zmin; a.bpar[p * 2 + 1] = gscale; }
+
+    // ---- P0: granule histograms of my quarter (x; x + y)
+    for (int b = tid; b < NB; b += SP_T) { S.hx[b] = 0; S.hy[b] = 0; }
+    for (int g = tid; g < NG; g += SP_T) { S.gx[g] = 0; S.gxy[g] = 0; }
     __syncthreads();
-    if (tid == 0) {
-      int total = 0;
-      for (int g = 0; g < NG; ++g) total += gtot[g];
-      int run = 0, r = 1;
-      S.wbuf[0] = 0;
-      for (int g = 0; g < NG && r < SP_C; ++g) {
-        run += gtot[g];
-        while (r < SP_C && static_cast<int64_t>(run) * SP_C >= static_cast<int64_t>(total) * r) S.wbuf[r++] = g + 1;
+    for (int64_t base = x0; base < x1; base += U * SP_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * SP_T;
+        zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
       }
-      while (r < SP_C) S.wbuf[r++] = NG;
-      S.wbuf[SP_C] = NG;
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * SP_T < x1) atomicAdd(&S.gx[gran_of(zz[k], zmin, gscale)], 1);
+    }
+    for (int64_t base = y0; base < y1; base += U * SP_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * SP_T;
+        zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * SP_T < y1) atomicAdd(&S.gxy[gran_of(zz[k], zmin, gscale)], 1);
     }
     __syncthreads();
+    for (int g = tid; g < NG; g += SP_T) S.gxy[g] += S.gx[g];
+    cluster.sync();
+    // global granule counts (identical in every rank) -> bucket map and ownership
+    int own_g0, own_g1;
+    {
+      __shared__ int gtx[NG], gtxy[NG];
+      for (int g = tid; g < NG; g += SP_T) {
+        int cx = 0, cxy = 0;
 #pragma unroll
-    for (int r = 0; r <= SP_C; ++r) glo[r] = S.wbuf[r] * GB;
+        for (int r = 0; r < SP_C; ++r) {
+          const Shared* R = cluster.map_shared_rank(&S, r);
+          cx += R->gx[g];
+          cxy += R->gxy[g];
+        }
+        gtx[g] = cx;
+        gtxy[g] = cxy;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int64_t cum = 0;
+        int prev = 0;
+        for (int g = 0; g < NG; ++g) {
+          cum += gtx[g];
+          const int next = (N > 0) ? static_cast<int>((cum * NB) / N) : NB;
+          S.gtab[g] = make_int2(prev, next - prev);
+          prev = next;
+        }
+        int64_t total = 0;
+        for (int g = 0; g < NG; ++g) total += gtxy[g];
+        int64_t run = 0;
+        int r = 1;
+        S.wbuf[0] = 0;
+        for (int g = 0; g < NG && r < SP_C; ++g) {
+          run += gtxy[g];
+          while (r < SP_C && run * SP_C >= total * r) S.wbuf[r++] = g + 1;
+        }
+        while (r < SP_C) S.wbuf[r++] = NG;
+        S.wbuf[SP_C] = NG;
+      }
+      __syncthreads();
+      own_g0 = S.wbuf[rank];
+      own_g1 = S.wbuf[rank + 1];
+    }
+    const int lo = (own_g0 < NG) ? S.gtab[own_g0].x : NB;
+    const int hi = (own_g1 < NG) ? S.gtab[own_g1].x : NB;
+    const int nown = hi - lo;
+
+    // ---- P1: bucket histograms of my quarter
+    for (int64_t base = x0; base < x1; base += U * SP_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * SP_T;
+        zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * SP_T < x1) atomicAdd(&S.hx[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
+    }
+    for (int64_t base = y0; base < y1; base += U * SP_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * SP_T;
+        zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * SP_T < y1) atomicAdd(&S.hy[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
+    }
+    cluster.sync();
+
+    // ---- P2: owners sum the ranks' histograms of their buckets, scan, write every rank's cursors
+    for (int j = tid; j < nown; j += SP_T) {
+      int tx = 0, ty = 0;
+#pragma unroll
+      for (int r = 0; r < SP_C; ++r) {
+        const Shared* R = cluster.map_shared_rank(&S, r);
+        tx += R->hx[lo + j];
+        ty += R->hy[lo + j];
+      }
+      S.ox[j] = tx;
+      S.oy[j] = ty;
+    }
     __syncthreads();
-  }
-  const int lo = glo[rank], hi = glo[rank + 1], nown = hi - lo;
-  // owner: totals of its buckets over all ranks
-  for (int j = tid; j < nown; j += SP_T) {
-    int tx = 0, ty = 0;
-#pragma unroll
-    for (int r = 0; r < SP_C; ++r) {
+    const int Sx = block_scan_int(S.ox, nown, S.wbuf);
+    const int Sy = block_scan_int(S.oy, nown, S.wbuf);
+    if (tid == 0) { S.tot_i[0] = Sx; S.tot_i[1] = Sy; }
+    cluster.sync();
+    int bx = 0, by = 0;
+    for (int r = 0; r < rank; ++r) {
       const Shared* R = cluster.map_shared_rank(&S, r);
-      tx += R->hx[lo + j];
-      ty += R->hy[lo + j];
+      bx += R->tot_i[0];
+      by += R->tot_i[1];
     }
-    S.ox[j] = tx;
-    S.oy[j] = ty;
-  }
-  __syncthreads();
-  const int Sx = block_scan_int(S.ox, nown, S.wbuf);
-  const int Sy = block_scan_int(S.oy, nown, S.wbuf);
-  if (tid == 0) { S.tot_i[0] = Sx; S.tot_i[1] = Sy; }
-  cluster.sync();   // all owners' totals published; all histogram reads of P2 done
-  int bx = 0, by = 0;
-  for (int r = 0; r < rank; ++r) {
-    const Shared* R = cluster.map_shared_rank(&S, r);
-    bx += R->tot_i[0];
-    by += R->tot_i[1];
-  }
-  for (int j = tid; j < nown; j += SP_T) {
-    S.ox[j] += bx;
-    S.oy[j] += by;
-  }
-  if (tid == 0) { S.ox[nown] = bx + Sx; S.oy[nown] = by + Sy; }
-  __syncthreads();
-  for (int j = tid; j < nown; j += SP_T) {
-    int rx = S.ox[j], ry = S.oy[j];
+    for (int j = tid; j < nown; j += SP_T) { S.ox[j] += bx; S.oy[j] += by; }
+    if (tid == 0) { S.ox[nown] = bx + Sx; S.oy[nown] = by + Sy; }
+    __syncthreads();
+    for (int j = tid; j < nown; j += SP_T) {
+      int rx = S.ox[j], ry = S.oy[j];
 #pragma unroll
-    for (int r = 0; r < SP_C; ++r) {
-      Shared* R = cluster.map_shared_rank(&S, r);
-      const int hx = R->hx[lo + j], hy = R->hy[lo + j];
-      R->hx[lo + j] = rx;
-      R->hy[lo + j] = ry;
-      rx += hx;
-      ry += hy;
+      for (int r = 0; r < SP_C; ++r) {
+        Shared* R = cluster.map_shared_rank(&S, r);
+        const int hx = R->hx[lo + j], hy = R->hy[lo + j];
+        R->hx[lo + j] = rx;
+        R->hy[lo + j] = ry;
+        rx += hx;
+        ry += hy;
+      }
     }
-  }
-  cluster.sync();   // cursors written into every rank
+    cluster.sync();
 
-  // ---- P3: scatter my quarter
-  for (int64_t base = x0; base < x1; base += U * SP_T) {
-    float zz[U], ww[U];
+    // ---- P3: scatter my quarter
+    for (int64_t base = x0; base < x1; base += U * SP_T) {
+      float zz[U], ww[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SP_T;
-      zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
-      ww[k] = (i < x1) ? __ldg(a.w + i) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (base + tid + k * SP_T < x1) {
-        const int pos = atomicAdd(&S.hx[bin_of(zz[k], zmin, scale)], 1);
-        xsp[pos] = make_float2(zz[k], ww[k]);
-      }
-  }
-  for (int64_t base = y0; base < y1; base += U * SP_T) {
-    float zz[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SP_T;
-      zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t i = base + tid + k * SP_T;
-      if (i < y1) {
-        const int pos = atomicAdd(&S.hy[bin_of(zz[k], zmin, scale)], 1);
-        ysp[pos] = make_float2(zz[k], __int_as_float(static_cast<int>(i)));
-      }
-    }
-  }
-  cluster.sync();   // (release/acquire at cluster scope: the scattered xs/ys are visible to the owners)
-
-  // ---- P4: owner bucket sums (fp64), coalesced over its contiguous x range
-  double tA = 0.0, tB = 0.0, tC = 0.0;
-  {
-    const int s0g = S.ox[0], s1g = S.ox[nown];
-    const int per = ((s1g - s0g + SP_W - 1) / SP_W + 31) / 32 * 32;
-    const int s0 = min(s1g, s0g + wid * per), s1 = min(s1g, s0 + per);
-    for (int base0 = s0; base0 < s1; base0 += 4 * 32) {
-      float2 ee[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int i = base0 + k * 32 + lane;
-        ee[k] = (i < s1) ? __ldcg(xsp + i) : make_float2(0.f, 0.f);
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * SP_T;
+        zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
+        ww[k] = (i < x1) ? __ldg(a.w + i) : 0.f;
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int i = base0 + k * 32 + lane;
-        const bool valid = i < s1;
-        const float2 e = ee[k];
-        const int key = valid ? bin_of(e.x, zmin, scale) : -1 - lane;
-        double sa = e.y, sb = static_cast<double>(e.y) * e.x;
-        tA += sa;
-        tB += sb;
-        tC += sb * e.x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double na = __shfl_up_sync(0xffffffffu, sa, o), nbz = __shfl_up_sync(0xffffffffu, sb, o);
-          const int nk = __shfl_up_sync(0xffffffffu, key, o);
-          if (lane >= o && nk == key) { sa += na; sb += nbz; }   // keys are sorted along xs
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * SP_T < x1) {
+          const int pos = atomicAdd(&S.hx[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
+          xsp[pos] = make_float2(zz[k], ww[k]);
         }
-        const int next = __shfl_down_sync(0xffffffffu, key, 1);
-        if (valid && (lane == 31 || next != key)) {
-          atomicAdd(&rp[key].A, sa);
-          atomicAdd(&rp[key].B, sb);
+    }
+    for (int64_t base = y0; base < y1; base += U * SP_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * SP_T;
+        zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * SP_T;
+        if (i < y1) {
+          const int pos = atomicAdd(&S.hy[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
+          ysp[pos] = make_float2(zz[k], __int_as_float(static_cast<int>(i)));
         }
       }
     }
-  }
-  tA = warp_sum(tA);
-  tB = warp_sum(tB);
-  tC = warp_sum(tC);
-  if (lane == 0) { S.wsd[0][wid] = tA; S.wsd[1][wid] = tB; S.wsd[2][wid] = tC; }
-  __syncthreads();
-  if (tid == 0) {
-    double sa = 0, sb = 0, sc = 0;
-    for (int q = 0; q < SP_W; ++q) { sa += S.wsd[0][q]; sb += S.wsd[1][q]; sc += S.wsd[2][q]; }
-    S.tot_d[0] = sa; S.tot_d[1] = sb; S.tot_d[2] = sc;
-  }
-  cluster.sync();   // partial sums of all owners published (and all bucket-sum atomics done)
-  double TA = 0, TB = 0, TC = 0, PA = 0, PB = 0;
-#pragma unroll
-  for (int r = 0; r < SP_C; ++r) {
-    const Shared* R = cluster.map_shared_rank(&S, r);
-    TA += R->tot_d[0]; TB += R->tot_d[1]; TC += R->tot_d[2];
-    if (r < rank) { PA += R->tot_d[0]; PB += R->tot_d[1]; }
-  }
-  if (rank == 0 && tid == 0) a.tot[p] = SliceTot{TA, TB, TC, 0.0};
+    cluster.sync();   // release/acquire at cluster scope: the scattered xs/ys are visible to the owners
 
-  // ---- P5: exclusive fp64 scan over my buckets -> records
-  {
+    // ---- P4 + P5: owner bucket sums (thread per run of consecutive buckets, fp64), exclusive scan, records
     const int per = (nown + SP_T - 1) / SP_T;
     const int j0 = min(nown, tid * per), j1 = min(nown, j0 + per);
-    double lA = 0.0, lB = 0.0;
-    for (int j = j0; j < j1; ++j) {
-      const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + lo + j));
-      lA += v.x;
-      lB += v.y;
+    double lA = 0.0, lB = 0.0, lC = 0.0;
+    for (int i = S.ox[j0]; i < S.ox[j1]; ++i) {
+      const float2 q = __ldcg(xsp + i);
+      const double wz = static_cast<double>(q.y) * q.x;
+      lA += q.y;
+      lB += wz;
+      lC += wz * q.x;
     }
-    const double iA = warp_incl_scan(lA), iB = warp_incl_scan(lB);
-    if (lane == 31) { S.wsd[0][wid] = iA; S.wsd[1][wid] = iB; }
-    __syncthreads();
-    if (wid == 0) {
-      const double va = S.wsd[0][lane], vb = S.wsd[1][lane];
-      const double ia = warp_incl_scan(va), ib = warp_incl_scan(vb);
-      S.wsd[0][lane] = ia - va;
-      S.wsd[1][lane] = ib - vb;
-    }
-    __syncthreads();
-    double rA = PA + S.wsd[0][wid] + iA - lA, rB = PB + S.wsd[1][wid] + iB - lB;
-    for (int j = j0; j < j1; ++j) {
-      const double2 v = __ldcg(reinterpret_cast<const double2*>(rp + lo + j));
-      BucketRec r;
-      r.A = rA;
-      r.B = rB;
-      r.off = S.ox[j];
-      r.cnt = S.ox[j + 1] - S.ox[j];
-      r.w = static_cast<float>(v.x);
-      r.wz = static_cast<float>(v.y);
-      rp[lo + j] = r;
-      rA += v.x;
-      rB += v.y;
-    }
-  }
-  __syncthreads();
+    {
+      const double iA = warp_incl_scan(lA), iB = warp_incl_scan(lB);
+      const double sC = warp_sum(lC);
+      if (lane == 31) { S.wsd[0][wid] = iA; S.wsd[1][wid] = iB; }
+      if (lane == 0) S.wsd[2][wid] = sC;
+      __syncthreads();
+      if (wid == 0) {
+        const double va = S.wsd[0][lane], vb = S.wsd[1][lane], vc = S.wsd[2][lane];
+        const double ia = warp_incl_scan(va), ib = warp_incl_scan(vb), sc = warp_sum(vc);
+        S.wsd[0][lane] = ia - va;
+        S.wsd[1][lane] = ib - vb;
+        if (lane == 31) { S.tot_d[0] = ia; S.tot_d[1] = ib; }
+        if (lane == 0) S.tot_d[2] = sc;
+      }
+      cluster.sync();   // owners' partial totals published
+      double TA = 0, TB = 0, TC = 0, PA = 0, PB = 0;
+#pragma unroll
+      for (int r = 0; r < SP_C; ++r) {
+        const Shared* R = cluster.map_shared_rank(&S, r);
+        TA += R->tot_d[0]; TB += R->tot_d[1]; TC += R->tot_d[2];
+        if (r < rank) { PA += R->tot_d[0]; PB += R->tot_d[1]; }
+      }
+      if (rank == 0 && tid == 0) a.tot[p] = SliceTot{TA, TB, TC, 0.0};
+      double rA = PA + S.wsd[0][wid] + iA - lA, rB = PB + S.wsd[1][wid] + iB - lB;
+      for (int j = j0; j < j1; ++j) {
+        double W = 0.0, Z = 0.0;
+        for (int i = S.ox[j]; i < S.ox[j + 1]; ++i) {
+          const float2 q = __ldcg(xsp + i);
+          W += q.y;
+          Z += static_cast<double>(q.y) * q.x;
+        }
+        BucketRec r;
+        r.A = rA;
+        r.B = rB;
+        r.off = S.ox[j];
+        r.cnt = S.ox[j + 1] - S.ox[j];
+        r.w = static_cast<float>(W);
+        r.wz = static_cast<float>(Z);
+        rp[lo + j] = r;
+        rA += W;
+        rB += Z;
+      }
+      __syncthreads();
 
-  // ---- P6: my targets in bucket order
-  const int t0 = S.oy[0], t1 = S.oy[nown];
-  for (int base = t0; base < t1; base += 2 * SP_T) {
-    float2 ee[2];
-    int bb[2];
+      // ---- P6: my targets in bucket order
+      const int t0 = S.oy[0], t1 = S.oy[nown];
+      for (int base = t0; base < t1; base += 2 * SP_T) {
+        float2 ee[2];
+        int bb[2];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int i = base + tid + k * SP_T;
-      ee[k] = (i < t1) ? __ldcg(ysp + i) : make_float2(zmin, 0.f);
-      bb[k] = bin_of(ee[k].x, zmin, scale);
-    }
+        for (int k = 0; k < 2; ++k) {
+          const int i = base + tid + k * SP_T;
+          ee[k] = (i < t1) ? __ldcg(ysp + i) : make_float2(zmin, 0.f);
+          bb[k] = bin_of(ee[k].x, zmin, gscale, S.gtab);
+        }
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int i = base + tid + k * SP_T;
-      if (i >= t1) continue;
-      const BucketRec R = rp[bb[k]];
-      const float z = ee[k].x;
-      const int64_t m = __float_as_int(ee[k].y);
-      const double zd = z;
-      const double Ahi = TA - R.A - R.w, Bhi = TB - R.B - R.wz;
-      const float2* xp = xsp + R.off;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-      int j = 0;
-      for (; j + 4 <= R.cnt; j += 4) {
-        const float2 q0 = xp[j], q1 = xp[j + 1], q2 = xp[j + 2], q3 = xp[j + 3];
-        s0 = fmaf(q0.y, fabsf(q0.x - z), s0);
-        s1 = fmaf(q1.y, fabsf(q1.x - z), s1);
-        s2 = fmaf(q2.y, fabsf(q2.x - z), s2);
-        s3 = fmaf(q3.y, fabsf(q3.x - z), s3);
+        for (int k = 0; k < 2; ++k) {
+          const int i = base + tid + k * SP_T;
+          if (i >= t1) continue;
+          const BucketRec R = rp[bb[k]];
+          const float z = ee[k].x;
+          const int64_t m = __float_as_int(ee[k].y);
+          const double zd = z;
+          const double Ahi = TA - R.A - R.w, Bhi = TB - R.B - R.wz;
+          const float2* xp = xsp + R.off;
+          float s0 = 0.f, s1 = 0.f;
+          int j = 0;
+          for (; j + 2 <= R.cnt; j += 2) {
+            const float2 q0 = __ldcg(xp + j), q1 = __ldcg(xp + j + 1);
+            s0 = fmaf(q0.y, fabsf(q0.x - z), s0);
+            s1 = fmaf(q1.y, fabsf(q1.x - z), s1);
+          }
+          if (j < R.cnt) {
+            const float2 q = __ldcg(xp + j);
+            s0 = fmaf(q.y, fabsf(q.x - z), s0);
+          }
+          const double same = static_cast<double>(s0 + s1);
+          const double t = -a.coef * ((zd * R.A - R.B) + (Bhi - zd * Ahi) + same);
+          if (a.s64) atomicAdd(a.s64 + m, t);
+          if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
+        }
       }
-      for (; j < R.cnt; ++j) {
-        const float2 q = xp[j];
-        s0 = fmaf(q.y, fabsf(q.x - z), s0);
-      }
-      const double same = static_cast<double>((s0 + s1) + (s2 + s3));
-      const double t = -a.coef * ((zd * R.A - R.B) + (Bhi - zd * Ahi) + same);
-      if (a.s64) atomicAdd(a.s64 + m, t);
-      if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
     }
+    cluster.sync();   // slot scratch and smem are reused by the next slice
   }
 }
 
@@ -411,13 +429,30 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
 
 int sortpath_buckets() { return NB; }
 
-cudaError_t launch_sortpath(const SortArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+int sortpath_slots(int np) {
+  static int nclusters = 0;
+  if (nclusters == 0) {
     cudaFuncSetAttribute(k_sortsum, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Shared)));
-    attr = true;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(SP_C * 64);
+    cfg.blockDim = dim3(SP_T);
+    cfg.dynamicSmemBytes = sizeof(Shared);
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = SP_C;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_sortsum, &cfg) != cudaSuccess || n <= 0) n = 148 / SP_C;
+    nclusters = n;
   }
-  k_sortsum<<<a.np * SP_C, SP_T, sizeof(Shared), st>>>(a);
+  return np < nclusters ? np : nclusters;
+}
+
+cudaError_t launch_sortpath(const SortArgs& a, int slots, cudaStream_t st) {
+  k_sortsum<<<slots * SP_C, SP_T, sizeof(Shared), st>>>(a);
   return cudaGetLastError();
 }
 
