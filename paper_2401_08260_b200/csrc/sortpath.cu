@@ -199,26 +199,31 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
         gtxy[g] = cxy;
       }
       __syncthreads();
-      if (tid == 0) {
-        int64_t cum = 0;
-        int prev = 0;
-        for (int g = 0; g < NG; ++g) {
+      if (wid == 0) {   // warp-parallel: lane l handles granules [8l, 8l + 8)
+        constexpr int PG = NG / 32;
+        long long cx = 0, cxy = 0;
+        for (int q = 0; q < PG; ++q) { cx += gtx[lane * PG + q]; cxy += gtxy[lane * PG + q]; }
+        const long long ix = warp_incl_scan(cx), ixy = warp_incl_scan(cxy);
+        const long long total = __shfl_sync(0xffffffffu, ixy, 31);
+        long long cum = ix - cx, run = ixy - cxy;
+        int prev = (N > 0) ? static_cast<int>((cum * NB) / N) : 0;
+        for (int q = 0; q < PG; ++q) {
+          const int g = lane * PG + q;
           cum += gtx[g];
           const int next = (N > 0) ? static_cast<int>((cum * NB) / N) : NB;
           S.gtab[g] = make_int2(prev, next - prev);
           prev = next;
-        }
-        int64_t total = 0;
-        for (int g = 0; g < NG; ++g) total += gtxy[g];
-        int64_t run = 0;
-        int r = 1;
-        S.wbuf[0] = 0;
-        for (int g = 0; g < NG && r < SP_C; ++g) {
+          const long long before = run;
           run += gtxy[g];
-          while (r < SP_C && run * SP_C >= total * r) S.wbuf[r++] = g + 1;
+          for (int r = 1; r < SP_C; ++r)   // boundary r = first granule end with run*C >= total*r
+            if (before * SP_C < total * r && run * SP_C >= total * r) S.wbuf[r] = g + 1;
         }
-        while (r < SP_C) S.wbuf[r++] = NG;
-        S.wbuf[SP_C] = NG;
+        if (lane == 0) {
+          S.wbuf[0] = 0;
+          S.wbuf[SP_C] = NG;
+          if (total == 0)
+            for (int r = 1; r < SP_C; ++r) S.wbuf[r] = NG;
+        }
       }
       __syncthreads();
       own_g0 = S.wbuf[rank];
