@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -123,11 +124,20 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
+  size_t Z = 0, xs3 = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
          flag = 0, total = 0;
 };
 
-Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb) {
+bool use_tc_projection() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SKS_PROJECTION");
+    v = (e && std::strcmp(e, "simt") == 0) ? 0 : 1;   // A/B switch for measurements; tensor cores by default
+  }
+  return v == 1;
+}
+
+Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb, int d) {
   Layout L;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -138,7 +148,10 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb)
   L.flag = take(16);
   L.s64 = take(sizeof(double) * M);
   L.mm = take(sizeof(unsigned) * 4 * nbat);
-  if (with_Z) L.Z = take(sizeof(float) * (N + M) * nbat);
+  if (with_Z) {
+    L.Z = take(sizeof(float) * (N + M) * nbat);
+    if (use_tc_projection()) L.xs3 = take(sizeof(uint16_t) * 3 * static_cast<size_t>(sks::proj_tc_dpad(d)) * (N + M));
+  }
   if (pt.sort || pt.moment) {
     const int slots = sks::sortpath_slots(nbat);
     L.xs = take(sizeof(float2) * N * slots);
@@ -158,12 +171,12 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb)
   return L;
 }
 
-int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int nb, int req) {
+int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int nb, int req, int d) {
   if (req > 0) return std::min(req, np);
   // auto: all local slices unless the batch working set would exceed 64 GiB of HBM
   const size_t budget = size_t(64) << 30;
   int b = np;
-  while (b > 1 && make_layout(N, M, pt, b, with_Z, nb).total > budget) b = (b + 1) / 2;
+  while (b > 1 && make_layout(N, M, pt, b, with_Z, nb, d).total > budget) b = (b + 1) / 2;
   return b;
 }
 
@@ -171,6 +184,8 @@ int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int nb, int
 struct DirEntry {
   float* g = nullptr;      // np x d
   float* inv = nullptr;    // np
+  void* g3 = nullptr;      // np x 3*dp bf16: [g | g | g] zero padded (tensor-core projection operand)
+  int K3 = 0;
 };
 std::mutex g_dir_mu;
 std::map<std::tuple<int, uint64_t, int, int, int, int>, DirEntry> g_dirs;
@@ -196,6 +211,20 @@ sks_status get_dirs(int P, int d, uint64_t seed, int p0, int p1, DirEntry* out) 
   SKS_CUDA(cudaMalloc(&e.inv, sizeof(float) * np));
   SKS_CUDA(cudaMemcpy(e.g, g.data(), sizeof(float) * g.size(), cudaMemcpyHostToDevice));
   SKS_CUDA(cudaMemcpy(e.inv, invf.data(), sizeof(float) * np, cudaMemcpyHostToDevice));
+  {
+    const int dp = sks::proj_tc_dpad(d);
+    e.K3 = 3 * dp;
+    std::vector<uint16_t> g3(static_cast<size_t>(np) * e.K3, 0);
+    for (int p = 0; p < np; ++p)
+      for (int j = 0; j < d; ++j) {
+        uint32_t u;
+        std::memcpy(&u, &g[static_cast<size_t>(p) * d + j], 4);
+        const uint16_t b = static_cast<uint16_t>(u >> 16);   // exact: g is bf16-representable (R1)
+        for (int piece = 0; piece < 3; ++piece) g3[static_cast<size_t>(p) * e.K3 + piece * dp + j] = b;
+      }
+    SKS_CUDA(cudaMalloc(&e.g3, sizeof(uint16_t) * g3.size()));
+    SKS_CUDA(cudaMemcpy(e.g3, g3.data(), sizeof(uint16_t) * g3.size(), cudaMemcpyHostToDevice));
+  }
   g_dirs[key] = e;
   *out = e;
   return SKS_OK;
@@ -323,8 +352,8 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
                        double inv_P, void* workspace, size_t ws_bytes, cudaStream_t st) {
   const Path pt = path_of(pr.k.kind);
   const int nb = (pt.sort || pt.moment) ? buckets_for(pr.N) : 0;
-  const int batch = choose_batch(pr.N, pr.M, pt, pr.nslices, pr.with_Z, nb, o.batch);
-  const Layout L = make_layout(pr.N, pr.M, pt, batch, pr.with_Z, nb);
+  const int batch = choose_batch(pr.N, pr.M, pt, pr.nslices, pr.with_Z, nb, o.batch, pr.d);
+  const Layout L = make_layout(pr.N, pr.M, pt, batch, pr.with_Z, nb, pr.d);
   if (!workspace || ws_bytes < L.total)
     return fail(SKS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(SKS_ERR_INVALID, "workspace must be 256-byte aligned");
@@ -343,6 +372,12 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     SKS_CUDA(sks::launch_zero(ws + L.s64, al(sizeof(double) * pr.M), st));
   }
   launches += s_out ? 2 : 1;
+  const bool tc = pr.with_Z && use_tc_projection();
+  if (tc) {
+    ProfScope ps(PS_PROJECT, st);
+    SKS_CUDA(sks::launch_split3(x, pr.N, y, pr.M, pr.d, ws + L.xs3, st));
+    ++launches;
+  }
   for (int b0 = 0; b0 < pr.nslices; b0 += batch) {
     const int nbat = std::min(batch, pr.nslices - b0);
     ++nbatches;
@@ -357,8 +392,13 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       float* Z = reinterpret_cast<float*>(ws + L.Z);
       const int64_t ldz = pr.N + pr.M;
       ProfScope ps(PS_PROJECT, st);
-      SKS_CUDA(sks::launch_project(x, pr.N, y, pr.M, pr.d, dirs->g + static_cast<int64_t>(b0) * pr.d, dirs->inv + b0,
-                                   nbat, Z, ldz, mm, flag, st));
+      if (tc)
+        SKS_CUDA(sks::launch_project_tc(ws + L.xs3, pr.N + pr.M, pr.N, pr.d,
+                                        static_cast<const uint16_t*>(dirs->g3) + static_cast<int64_t>(b0) * dirs->K3,
+                                        nbat, dirs->inv + b0, Z, ldz, mm, flag, st));
+      else
+        SKS_CUDA(sks::launch_project(x, pr.N, y, pr.M, pr.d, dirs->g + static_cast<int64_t>(b0) * pr.d,
+                                     dirs->inv + b0, nbat, Z, ldz, mm, flag, st));
       zv = sks::ZView{Z, Z + pr.N, ldz, ldz, pr.N, pr.M};
     } else {
       zv = sks::ZView{zx_in + static_cast<int64_t>(b0) * pr.N, zy_in + static_cast<int64_t>(b0) * pr.M, pr.N, pr.M,
@@ -519,8 +559,8 @@ sks_status sks_workspace_size(int64_t N, int64_t M, int32_t d, sks_kernel kernel
   if (!bytes) return fail(SKS_ERR_INVALID, "bytes is NULL");
   const Path pt = path_of(kernel.kind);
   const int nb = (pt.sort || pt.moment) ? buckets_for(N) : 0;
-  const int batch = choose_batch(N, M, pt, p_end - p_begin, true, nb, o.batch);
-  *bytes = make_layout(N, M, pt, batch, true, nb).total;
+  const int batch = choose_batch(N, M, pt, p_end - p_begin, true, nb, o.batch, d);
+  *bytes = make_layout(N, M, pt, batch, true, nb, d).total;
   return SKS_OK;
 }
 
@@ -583,17 +623,28 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
   if (st != SKS_OK) return st;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   const int np = p_end - p_begin;
-  // ranges / flag are not needed by the caller: use a small scratch in the direction cache's stream order
+  // ranges / flag / split scratch are not needed by the caller: a small per-thread scratch (allocated on
+  // first use, grown on demand; this entry point is a test/inspection aid, not the hot path)
   static thread_local unsigned* scratch = nullptr;
-  static thread_local int scratch_np = 0;
-  if (scratch_np < np) {
+  static thread_local size_t scratch_bytes = 0;
+  const bool tc = use_tc_projection();
+  const size_t need = al(sizeof(unsigned) * 4 * np + 16) + (tc ? al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n) : 0);
+  if (scratch_bytes < need) {
     if (scratch) cudaFree(scratch);
-    SKS_CUDA(cudaMalloc(&scratch, sizeof(unsigned) * 4 * np + 16));
-    scratch_np = np;
+    scratch = nullptr;
+    SKS_CUDA(cudaMalloc(&scratch, need));
+    scratch_bytes = need;
   }
-  SKS_CUDA(sks::launch_init_minmax(scratch, np, cs));
-  SKS_CUDA(sks::launch_project(pts, n, pts, 0, d, dirs.g, dirs.inv, np, z, n, scratch,
-                               reinterpret_cast<int*>(scratch + 4 * np), cs));
+  unsigned* mm = scratch;
+  int* flag = reinterpret_cast<int*>(scratch + 4 * np);
+  SKS_CUDA(sks::launch_init_minmax(mm, np, cs));
+  if (tc) {
+    char* xs3 = reinterpret_cast<char*>(scratch) + al(sizeof(unsigned) * 4 * np + 16);
+    SKS_CUDA(sks::launch_split3(pts, n, pts, 0, d, xs3, cs));
+    SKS_CUDA(sks::launch_project_tc(xs3, n, n, d, dirs.g3, np, dirs.inv, z, n, mm, flag, cs));
+  } else {
+    SKS_CUDA(sks::launch_project(pts, n, pts, 0, d, dirs.g, dirs.inv, np, z, n, mm, flag, cs));
+  }
   return SKS_OK;
 }
 
@@ -606,8 +657,8 @@ sks_status sks_workspace_size_1d(int64_t N, int64_t M, int32_t d, sks_kernel ker
   if (!bytes) return fail(SKS_ERR_INVALID, "bytes is NULL");
   const Path pt = path_of(kernel.kind);
   const int nb = (pt.sort || pt.moment) ? buckets_for(N) : 0;
-  const int batch = choose_batch(N, M, pt, n_slices, false, nb, o.batch);
-  *bytes = make_layout(N, M, pt, batch, false, nb).total;
+  const int batch = choose_batch(N, M, pt, n_slices, false, nb, o.batch, d);
+  *bytes = make_layout(N, M, pt, batch, false, nb, d).total;
   return SKS_OK;
 }
 

@@ -34,6 +34,12 @@ struct ZView {
 cudaError_t launch_project(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g,
                            const float* inv_norm, int np, float* Z, int64_t ldz, unsigned* mm, int* flag,
                            cudaStream_t st);
+// row a1 on tensor cores (proj_tc.cu): split fp32 points into 3 bf16 pieces (K-concatenated, d padded to
+// dp = proj_tc_dpad(d)), then Z = Xs . G3^T on tcgen05 with TMA/TMEM, same epilogue contract as above.
+int proj_tc_dpad(int d);
+cudaError_t launch_split3(const float* x, int64_t N, const float* y, int64_t M, int d, void* xs, cudaStream_t st);
+cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, const void* g3, int np,
+                              const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, cudaStream_t st);
 // per-slice ranges of given projections (sks_sum_1d)
 cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_t st);
 cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st);

@@ -1,0 +1,302 @@
+// proj_tc.cu -- row a1 on the 5th-generation tensor cores: the projection Z[p][i] = <xi_p, z_i> (P:129,
+// Alg. 1) as one bf16 GEMM with fp32 accumulation that is fp32-accurate (reading R2):
+//   * directions g_p are bf16-exact by construction (R1), xi_p = g_p / ||g_p|| is applied in the epilogue;
+//   * each fp32 coordinate is split exactly-enough into three bf16 pieces x = hi + mid + lo (+ O(2^-24 |x|)),
+//     stored K-concatenated: Xs[i] = [hi(0..dp) | mid(0..dp) | lo(0..dp)], G3[p] = [g_p | g_p | g_p];
+//   * every bf16 x bf16 product is exact in fp32, so D = Xs . G3^T is <g_p, x_i> with fp32 accumulation.
+// Kernel: TMA (cp.async.bulk.tensor, 128B swizzle) -> smem ring -> tcgen05.mma.cta_group::1.kind::f16
+// (M=128 points x N=BN slices x K=16) accumulating in TMEM -> tcgen05.ld epilogue (scale by 1/||g_p||,
+// coalesced stores along points, per-slice x / all ranges, non-finite flag).  Warp roles: w0 TMA producer,
+// w1 MMA issuer, w2 TMEM allocator, w4..w7 epilogue (TMEM lane quadrants 0..3).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "kernels.h"
+
+namespace sks {
+
+namespace {
+
+constexpr int TC_M = 128;   // points per tile (UMMA M)
+constexpr int TC_BK = 64;   // bf16 elements per k-block = 128 bytes (one swizzle row)
+
+__device__ __forceinline__ unsigned f2key_tc(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: SBO = 1024 B (8 rows x 128 B), LBO = 16 B
+// (ignored for swizzled K-major), version 1, layout type 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t umma_desc_sw128(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+// instruction descriptor kind::f16: D f32, A/B bf16, both K-major, N, M
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+template <int BN, int STAGES>
+struct TcSmem {
+  static constexpr int A_BYTES = TC_M * TC_BK * 2;
+  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int TOTAL = BAR_OFF + 8 * (2 * STAGES + 1) + 16 + 1024;   // + alignment slack
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    k_proj_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nk, int64_t L,
+              int64_t Nx, int np, const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz,
+              unsigned* __restrict__ mm, int* __restrict__ flag) {
+  using SM = TcSmem<BN, STAGES>;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + SM::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * TC_M;
+  const int n0 = blockIdx.y * BN;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_d = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      unsigned char* sa = sm + s * SM::STAGE;
+      unsigned char* sb = sa + SM::A_BYTES;
+      mbar_expect_tx(&full[s], SM::STAGE);
+      tma_load_2d(&tmA, &full[s], sa, kb * TC_BK, static_cast<int>(m0));
+      tma_load_2d(&tmB, &full[s], sb, kb * TC_BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer (single thread)
+    constexpr uint32_t idesc = idesc_bf16(TC_M, BN);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const unsigned char* sa = sm + s * SM::STAGE;
+      const unsigned char* sb = sa + SM::A_BYTES;
+      const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sb);
+#pragma unroll
+      for (int k = 0; k < TC_BK / 16; ++k) {
+        const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+        const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);   // +32 bytes along K inside the swizzle row
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&empty[s]))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(tfull))
+                 : "memory");
+  } else if (warp >= 4) {
+    // ---- epilogue: TMEM lane quadrant q = warp - 4 holds points m0 + 32q + lane
+    const int q = warp - 4;
+    const int64_t i = m0 + 32 * q + lane;
+    const bool valid = i < L;
+    const bool isx = i < Nx;
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    bool bad = false;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t v[16];
+      const uint32_t taddr = tmem_d + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(c0);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+          "%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int s = n0 + c0 + j;
+        if (s >= np) break;   // warp-uniform
+        const float z = __uint_as_float(v[j]) * __ldg(inv_norm + s);
+        if (valid) {
+          Z[static_cast<int64_t>(s) * ldz + i] = z;
+          bad |= !isfinite(z);
+        }
+        float xmn = (valid && isx) ? z : CUDART_INF_F, xmx = (valid && isx) ? z : -CUDART_INF_F;
+        float amn = valid ? z : CUDART_INF_F, amx = valid ? z : -CUDART_INF_F;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          xmn = fminf(xmn, __shfl_xor_sync(0xffffffffu, xmn, o));
+          xmx = fmaxf(xmx, __shfl_xor_sync(0xffffffffu, xmx, o));
+          amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, o));
+          amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+        }
+        if (lane == 0) {
+          if (xmn <= xmx) { atomicMin(&mm[s * 4 + 0], f2key_tc(xmn)); atomicMax(&mm[s * 4 + 1], f2key_tc(xmx)); }
+          if (amn <= amx) { atomicMin(&mm[s * 4 + 2], f2key_tc(amn)); atomicMax(&mm[s * 4 + 3], f2key_tc(amx)); }
+        }
+      }
+    }
+    if (bad) atomicOr(flag, 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN));
+}
+
+// fp32 -> three bf16 pieces, K-concatenated:  Xs[i][j] = hi, Xs[i][dp+j] = mid, Xs[i][2dp+j] = lo
+__global__ void k_split3(const float* __restrict__ x, int64_t N, const float* __restrict__ y, int64_t M, int d, int dp,
+                         __nv_bfloat16* __restrict__ xs) {
+  const int64_t L = N + M;
+  const int64_t total = L * dp;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / dp;
+    const int j = static_cast<int>(e - i * dp);
+    float v = 0.f;
+    if (j < d) v = (i < N) ? __ldg(x + i * d + j) : __ldg(y + (i - N) * d + j);
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const float r1 = v - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    __nv_bfloat16* row = xs + i * (3 * static_cast<int64_t>(dp));
+    row[j] = hi;
+    row[dp + j] = mid;
+    row[2 * dp + j] = lo;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_k, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t gdim[2] = {cols_k, rows};
+  const cuuint64_t gstride[1] = {cols_k * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(TC_BK), box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, int STAGES>
+cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int64_t L, int64_t Nx, int np,
+                      const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, cudaStream_t st) {
+  using SM = TcSmem<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_proj_tc<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>((L + TC_M - 1) / TC_M), static_cast<unsigned>((np + BN - 1) / BN));
+  k_proj_tc<BN, STAGES><<<grid, 256, SM::TOTAL, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int proj_tc_dpad(int d) { return (d + TC_BK - 1) / TC_BK * TC_BK; }
+
+cudaError_t launch_split3(const float* x, int64_t N, const float* y, int64_t M, int d, void* xs, cudaStream_t st) {
+  const int dp = proj_tc_dpad(d);
+  const int64_t total = (N + M) * dp;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_split3<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, N, y, M, d, dp, static_cast<__nv_bfloat16*>(xs));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, const void* g3, int np,
+                              const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, cudaStream_t st) {
+  const int dp = proj_tc_dpad(d);
+  const int K = 3 * dp;
+  const int nk = K / TC_BK;
+  const int BN = np > 128 ? 256 : (np > 64 ? 128 : 64);
+  CUtensorMap ta, tb;
+  if (!make_map(&ta, xs, static_cast<uint64_t>(L), static_cast<uint64_t>(K), TC_M)) return cudaErrorInvalidValue;
+  if (!make_map(&tb, g3, static_cast<uint64_t>(np), static_cast<uint64_t>(K), static_cast<uint32_t>(BN)))
+    return cudaErrorInvalidValue;
+  if (BN == 256) {
+    return nk <= 4 ? launch_tc<256, 2>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st)
+                   : launch_tc<256, 4>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
+  }
+  if (BN == 128) return launch_tc<128, 4>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
+  return launch_tc<64, 4>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
+}
+
+}  // namespace sks
