@@ -162,6 +162,9 @@ __global__ void __launch_bounds__(256, 1)
     const int64_t i = m0 + 32 * q + lane;
     const bool valid = i < L;
     const bool isx = i < Nx;
+    const int64_t w0 = m0 + 32 * q;                       // this warp's 32 points
+    const bool tile_all_x = (w0 + 32 <= Nx);              // warp-uniform
+    const bool tile_any_x = (w0 < Nx);
     mbar_wait(tfull, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     bool bad = false;
@@ -185,18 +188,18 @@ __global__ void __launch_bounds__(256, 1)
           Z[static_cast<int64_t>(s) * ldz + i] = z;
           bad |= !isfinite(z);
         }
-        float xmn = (valid && isx) ? z : CUDART_INF_F, xmx = (valid && isx) ? z : -CUDART_INF_F;
-        float amn = valid ? z : CUDART_INF_F, amx = valid ? z : -CUDART_INF_F;
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-          xmn = fminf(xmn, __shfl_xor_sync(0xffffffffu, xmn, o));
-          xmx = fmaxf(xmx, __shfl_xor_sync(0xffffffffu, xmx, o));
-          amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, o));
-          amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+        // per-slice ranges: one redux.sync per bound on order-preserving keys (x range and all range)
+        const unsigned key = f2key_tc(z);
+        const unsigned amn = __reduce_min_sync(0xffffffffu, valid ? key : 0xffffffffu);
+        const unsigned amx = __reduce_max_sync(0xffffffffu, valid ? key : 0u);
+        unsigned xmn = amn, xmx = amx;
+        if (!tile_all_x) {
+          xmn = __reduce_min_sync(0xffffffffu, (valid && isx) ? key : 0xffffffffu);
+          xmx = __reduce_max_sync(0xffffffffu, (valid && isx) ? key : 0u);
         }
         if (lane == 0) {
-          if (xmn <= xmx) { atomicMin(&mm[s * 4 + 0], f2key_tc(xmn)); atomicMax(&mm[s * 4 + 1], f2key_tc(xmx)); }
-          if (amn <= amx) { atomicMin(&mm[s * 4 + 2], f2key_tc(amn)); atomicMax(&mm[s * 4 + 3], f2key_tc(amx)); }
+          if (amn <= amx) { atomicMin(&mm[s * 4 + 2], amn); atomicMax(&mm[s * 4 + 3], amx); }
+          if (tile_any_x && xmn <= xmx) { atomicMin(&mm[s * 4 + 0], xmn); atomicMax(&mm[s * 4 + 1], xmx); }
         }
       }
     }
