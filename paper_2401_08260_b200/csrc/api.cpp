@@ -184,8 +184,8 @@ int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int nb, int
 struct DirEntry {
   float* g = nullptr;      // np x d
   float* inv = nullptr;    // np
-  void* g3 = nullptr;      // np x 3*dp bf16: [g | g | g] zero padded (tensor-core projection operand)
-  int K3 = 0;
+  void* g3 = nullptr;      // np x dp bf16: g zero padded (tensor-core projection operand)
+  int K3 = 0;              // dp
 };
 std::mutex g_dir_mu;
 std::map<std::tuple<int, uint64_t, int, int, int, int>, DirEntry> g_dirs;
@@ -213,14 +213,13 @@ sks_status get_dirs(int P, int d, uint64_t seed, int p0, int p1, DirEntry* out) 
   SKS_CUDA(cudaMemcpy(e.inv, invf.data(), sizeof(float) * np, cudaMemcpyHostToDevice));
   {
     const int dp = sks::proj_tc_dpad(d);
-    e.K3 = 3 * dp;
+    e.K3 = dp;
     std::vector<uint16_t> g3(static_cast<size_t>(np) * e.K3, 0);
     for (int p = 0; p < np; ++p)
       for (int j = 0; j < d; ++j) {
         uint32_t u;
         std::memcpy(&u, &g[static_cast<size_t>(p) * d + j], 4);
-        const uint16_t b = static_cast<uint16_t>(u >> 16);   // exact: g is bf16-representable (R1)
-        for (int piece = 0; piece < 3; ++piece) g3[static_cast<size_t>(p) * e.K3 + piece * dp + j] = b;
+        g3[static_cast<size_t>(p) * e.K3 + j] = static_cast<uint16_t>(u >> 16);   // exact: g is bf16 (R1)
       }
     SKS_CUDA(cudaMalloc(&e.g3, sizeof(uint16_t) * g3.size()));
     SKS_CUDA(cudaMemcpy(e.g3, g3.data(), sizeof(uint16_t) * g3.size(), cudaMemcpyHostToDevice));

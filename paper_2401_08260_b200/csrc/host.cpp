@@ -52,7 +52,15 @@ void make_directions(int P, int d, uint64_t seed, int p0, int p1, float* g, doub
 }
 
 // ------------------------------------------------------------------ kernel model
-double cd(int d) { return std::sqrt(kPi) * std::exp(std::lgamma(0.5 * (d + 1)) - std::lgamma(0.5 * d)); }
+double cd(int d) {
+  thread_local int last_d = -1;
+  thread_local double last_v = 0.0;
+  if (d != last_d) {
+    last_v = std::sqrt(kPi) * std::exp(std::lgamma(0.5 * (d + 1)) - std::lgamma(0.5 * d));
+    last_d = d;
+  }
+  return last_v;
+}
 
 // unit-scale fhat (scale = 1)
 double fhat1(const KernelModel& k, double rho) {
@@ -258,11 +266,22 @@ bool build_fourier_plan(const KernelModel& k, double eps, int w, int oversample,
     SlicePlan& sp = out.slices[p];
     sp.tau = static_cast<float>(tau);
     sp.cen = static_cast<float>(0.5 * (static_cast<double>(amin[p]) + static_cast<double>(amax[p])));
-    select_band(k, static_cast<double>(sp.tau), eps, 1 << 16, &sp.klo, &sp.khi);
-    kmax = std::max(kmax, sp.khi);
-    lomin = std::min(lomin, sp.klo);
     tmin = std::min(tmin, tau);
     tmax = std::max(tmax, tau);
+  }
+  // Band edges move monotonically with tau (c_k = tau fhat(tau k) [+ companion]: the spectrum stretches as
+  // 1/tau), so the union of the bands at the extreme tau covers every slice; a wider band than a slice
+  // strictly needs only adds (tiny) coefficients.
+  {
+    int lo1, hi1, lo2, hi2;
+    select_band(k, static_cast<double>(static_cast<float>(tmin)), eps, 1 << 16, &lo1, &hi1);
+    select_band(k, static_cast<double>(static_cast<float>(tmax)), eps, 1 << 16, &lo2, &hi2);
+    lomin = std::min(lo1, lo2);
+    kmax = std::max(hi1, hi2);
+    for (int p = 0; p < ns; ++p) {
+      out.slices[p].klo = lomin;
+      out.slices[p].khi = kmax;
+    }
   }
   const int n = std::max(16, ceil_pow2(static_cast<int64_t>(oversample) * 2 * (kmax + 1)));
   if (n > 16384) {
@@ -277,11 +296,23 @@ bool build_fourier_plan(const KernelModel& k, double eps, int w, int oversample,
   // ES shape for the actual oversampling (Barnett et al. 2019 choice beta = 0.97 pi (1 - 1/(2 os)) w)
   const double os = static_cast<double>(n) / (2.0 * (kmax + 1));
   out.beta = static_cast<float>(0.97 * kPi * (1.0 - 1.0 / (2.0 * std::min(os, 8.0))) * w);
-  std::vector<double> gx, gw;
-  gauss_legendre(128, gx, gw);
   const int nh = n / 2 + 1;
-  std::vector<double> Phi(nh);
-  for (int kk = 0; kk < nh; ++kk) Phi[kk] = window_ft(static_cast<double>(kk) / n, w, out.beta, gx, gw);
+  std::vector<double> Phi;
+  {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, float>, std::vector<double>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(n, w, out.beta);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      std::vector<double> gx, gw;
+      gauss_legendre(128, gx, gw);
+      std::vector<double> ph(nh);
+      for (int kk = 0; kk < nh; ++kk) ph[kk] = window_ft(static_cast<double>(kk) / n, w, out.beta, gx, gw);
+      it = cache.emplace(key, std::move(ph)).first;
+    }
+    Phi = it->second;
+  }
   out.phi2inv.assign(nh, 0.0f);
   for (int kk = 0; kk < nh; ++kk) out.phi2inv[kk] = static_cast<float>(1.0 / (Phi[kk] * Phi[kk]));
   int W = 0;

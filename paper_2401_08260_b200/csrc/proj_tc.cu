@@ -77,11 +77,12 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 
 template <int BN, int STAGES>
 struct TcSmem {
-  static constexpr int A_BYTES = TC_M * TC_BK * 2;
-  static constexpr int B_BYTES = BN * TC_BK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int A_BYTES = TC_M * TC_BK * 2;          // one bf16 piece of 128 points x 64 dims
+  static constexpr int B_BYTES = BN * TC_BK * 2;            // BN directions x 64 dims
+  static constexpr int STAGE = 3 * A_BYTES + B_BYTES;       // hi, mid, lo pieces share one direction tile
   static constexpr int BAR_OFF = STAGES * STAGE;
-  static constexpr int TOTAL = BAR_OFF + 8 * (2 * STAGES + 1) + 16 + 1024;   // + alignment slack
+  static constexpr int RANGE_OFF = BAR_OFF + 8 * (2 * STAGES + 1) + 16;
+  static constexpr int TOTAL = RANGE_OFF + 4 * 4 * BN + 1024;   // + per-CTA range partials + alignment slack
 };
 
 template <int BN, int STAGES>
@@ -96,6 +97,10 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  unsigned* rng = reinterpret_cast<unsigned*>(sm + SM::RANGE_OFF);   // [BN][4] per-CTA range partials (keys)
+  for (int c = threadIdx.x; c < BN; c += blockDim.x) {
+    rng[4 * c + 0] = 0xffffffffu; rng[4 * c + 1] = 0u; rng[4 * c + 2] = 0xffffffffu; rng[4 * c + 3] = 0u;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * TC_M;
   const int n0 = blockIdx.y * BN;
@@ -119,14 +124,16 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
+    for (int kb = 0; kb < nk; ++kb) {   // nk = dp / 64 k-blocks; piece q of x lives at column q*dp
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
       mbar_wait(&empty[s], ph ^ 1);
       unsigned char* sa = sm + s * SM::STAGE;
-      unsigned char* sb = sa + SM::A_BYTES;
+      unsigned char* sb = sa + 3 * SM::A_BYTES;
       mbar_expect_tx(&full[s], SM::STAGE);
-      tma_load_2d(&tmA, &full[s], sa, kb * TC_BK, static_cast<int>(m0));
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        tma_load_2d(&tmA, &full[s], sa + q * SM::A_BYTES, q * nk * TC_BK + kb * TC_BK, static_cast<int>(m0));
       tma_load_2d(&tmB, &full[s], sb, kb * TC_BK, n0);
     }
   } else if (warp == 1 && lane == 0) {
@@ -138,17 +145,21 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&full[s], ph);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const unsigned char* sa = sm + s * SM::STAGE;
-      const unsigned char* sb = sa + SM::A_BYTES;
-      const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sb);
+      const unsigned char* sb = sa + 3 * SM::A_BYTES;
+      const uint64_t db = umma_desc_sw128(sb);
 #pragma unroll
-      for (int k = 0; k < TC_BK / 16; ++k) {
-        const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-        const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);   // +32 bytes along K inside the swizzle row
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+      for (int q = 0; q < 3; ++q) {
+        const uint64_t da = umma_desc_sw128(sa + q * SM::A_BYTES);
+#pragma unroll
+        for (int k = 0; k < TC_BK / 16; ++k) {
+          const uint32_t acc = (kb > 0 || q > 0 || k > 0) ? 1u : 0u;
+          const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);   // +32 bytes along K inside the swizzle row
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+              "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_u32(&empty[s]))
@@ -198,8 +209,9 @@ __global__ void __launch_bounds__(256, 1)
           xmx = __reduce_max_sync(0xffffffffu, (valid && isx) ? key : 0u);
         }
         if (lane == 0) {
-          if (amn <= amx) { atomicMin(&mm[s * 4 + 2], amn); atomicMax(&mm[s * 4 + 3], amx); }
-          if (tile_any_x && xmn <= xmx) { atomicMin(&mm[s * 4 + 0], xmn); atomicMax(&mm[s * 4 + 1], xmx); }
+          const int c = c0 + j;
+          if (amn <= amx) { atomicMin(&rng[4 * c + 2], amn); atomicMax(&rng[4 * c + 3], amx); }
+          if (tile_any_x && xmn <= xmx) { atomicMin(&rng[4 * c + 0], xmn); atomicMax(&rng[4 * c + 1], xmx); }
         }
       }
     }
@@ -208,6 +220,20 @@ __global__ void __launch_bounds__(256, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
+  // one global update per slice and bound, only when this CTA improves the current extreme
+  for (int c = threadIdx.x; c < BN; c += blockDim.x) {
+    const int s = n0 + c;
+    if (s >= np) break;
+    const unsigned v0 = rng[4 * c + 0], v1 = rng[4 * c + 1], v2 = rng[4 * c + 2], v3 = rng[4 * c + 3];
+    if (v0 <= v1) {
+      if (v0 < *reinterpret_cast<volatile unsigned*>(&mm[s * 4 + 0])) atomicMin(&mm[s * 4 + 0], v0);
+      if (v1 > *reinterpret_cast<volatile unsigned*>(&mm[s * 4 + 1])) atomicMax(&mm[s * 4 + 1], v1);
+    }
+    if (v2 <= v3) {
+      if (v2 < *reinterpret_cast<volatile unsigned*>(&mm[s * 4 + 2])) atomicMin(&mm[s * 4 + 2], v2);
+      if (v3 > *reinterpret_cast<volatile unsigned*>(&mm[s * 4 + 3])) atomicMax(&mm[s * 4 + 3], v3);
+    }
+  }
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN));
 }
 
@@ -284,22 +310,18 @@ cudaError_t launch_split3(const float* x, int64_t N, const float* y, int64_t M, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, const void* g3, int np,
+cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, const void* g3 /* bf16 [np][dp] */, int np,
                               const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, cudaStream_t st) {
   const int dp = proj_tc_dpad(d);
-  const int K = 3 * dp;
-  const int nk = K / TC_BK;
+  const int nk = dp / TC_BK;
   const int BN = np > 128 ? 256 : (np > 64 ? 128 : 64);
   CUtensorMap ta, tb;
-  if (!make_map(&ta, xs, static_cast<uint64_t>(L), static_cast<uint64_t>(K), TC_M)) return cudaErrorInvalidValue;
-  if (!make_map(&tb, g3, static_cast<uint64_t>(np), static_cast<uint64_t>(K), static_cast<uint32_t>(BN)))
+  if (!make_map(&ta, xs, static_cast<uint64_t>(L), static_cast<uint64_t>(3 * dp), TC_M)) return cudaErrorInvalidValue;
+  if (!make_map(&tb, g3, static_cast<uint64_t>(np), static_cast<uint64_t>(dp), static_cast<uint32_t>(BN)))
     return cudaErrorInvalidValue;
-  if (BN == 256) {
-    return nk <= 4 ? launch_tc<256, 2>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st)
-                   : launch_tc<256, 4>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
-  }
-  if (BN == 128) return launch_tc<128, 4>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
-  return launch_tc<64, 4>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
+  if (BN == 256) return launch_tc<256, 2>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
+  if (BN == 128) return launch_tc<128, 3>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
+  return launch_tc<64, 3>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
 }
 
 }  // namespace sks
