@@ -124,7 +124,7 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, xs3 = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
+  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
          flag = 0, total = 0;
 };
 
@@ -150,7 +150,10 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb,
   L.mm = take(sizeof(unsigned) * 4 * nbat);
   if (with_Z) {
     L.Z = take(sizeof(float) * (N + M) * nbat);
-    if (use_tc_projection()) L.xs3 = take(sizeof(uint16_t) * 3 * static_cast<size_t>(sks::proj_tc_dpad(d)) * (N + M));
+    if (use_tc_projection()) {
+      L.xs3 = take(sizeof(uint16_t) * 3 * static_cast<size_t>(sks::proj_tc_dpad(d)) * (N + M));
+      L.part = take(sks::proj_tc_part_bytes(nbat));
+    }
   }
   if (pt.sort || pt.moment) {
     const int slots = sks::sortpath_slots(nbat);
@@ -394,7 +397,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       if (tc)
         SKS_CUDA(sks::launch_project_tc(ws + L.xs3, pr.N + pr.M, pr.N, pr.d,
                                         static_cast<const uint16_t*>(dirs->g3) + static_cast<int64_t>(b0) * dirs->K3,
-                                        nbat, dirs->inv + b0, Z, ldz, mm, flag, st));
+                                        nbat, dirs->inv + b0, Z, ldz, mm, flag, ws + L.part, st));
       else
         SKS_CUDA(sks::launch_project(x, pr.N, y, pr.M, pr.d, dirs->g + static_cast<int64_t>(b0) * pr.d,
                                      dirs->inv + b0, nbat, Z, ldz, mm, flag, st));
@@ -627,7 +630,8 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
   static thread_local unsigned* scratch = nullptr;
   static thread_local size_t scratch_bytes = 0;
   const bool tc = use_tc_projection();
-  const size_t need = al(sizeof(unsigned) * 4 * np + 16) + (tc ? al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n) : 0);
+  const size_t need = al(sizeof(unsigned) * 4 * np + 16) +
+                      (tc ? al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n) + al(sks::proj_tc_part_bytes(np)) : 0);
   if (scratch_bytes < need) {
     if (scratch) cudaFree(scratch);
     scratch = nullptr;
@@ -639,8 +643,9 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
   SKS_CUDA(sks::launch_init_minmax(mm, np, cs));
   if (tc) {
     char* xs3 = reinterpret_cast<char*>(scratch) + al(sizeof(unsigned) * 4 * np + 16);
+    char* part = xs3 + al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n);
     SKS_CUDA(sks::launch_split3(pts, n, pts, 0, d, xs3, cs));
-    SKS_CUDA(sks::launch_project_tc(xs3, n, n, d, dirs.g3, np, dirs.inv, z, n, mm, flag, cs));
+    SKS_CUDA(sks::launch_project_tc(xs3, n, n, d, dirs.g3, np, dirs.inv, z, n, mm, flag, part, cs));
   } else {
     SKS_CUDA(sks::launch_project(pts, n, pts, 0, d, dirs.g, dirs.inv, np, z, n, mm, flag, cs));
   }

@@ -38,8 +38,10 @@ cudaError_t launch_project(const float* x, int64_t N, const float* y, int64_t M,
 // dp = proj_tc_dpad(d)), then Z = Xs . G3^T on tcgen05 with TMA/TMEM, same epilogue contract as above.
 int proj_tc_dpad(int d);
 cudaError_t launch_split3(const float* x, int64_t N, const float* y, int64_t M, int d, void* xs, cudaStream_t st);
+size_t proj_tc_part_bytes(int np);   // scratch for per-CTA range partials
 cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, const void* g3, int np,
-                              const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, cudaStream_t st);
+                              const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, void* part,
+                              cudaStream_t st);
 // per-slice ranges of given projections (sks_sum_1d)
 cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_t st);
 cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st);

@@ -25,6 +25,7 @@ namespace {
 
 constexpr int TC_M = 128;   // points per tile (UMMA M)
 constexpr int TC_BK = 64;   // bf16 elements per k-block = 128 bytes (one swizzle row)
+constexpr int kProjMaxCtas = 148;   // persistent grid: one CTA per SM
 
 __device__ __forceinline__ unsigned f2key_tc(float f) {
   const unsigned u = __float_as_uint(f);
@@ -81,160 +82,185 @@ struct TcSmem {
   static constexpr int B_BYTES = BN * TC_BK * 2;            // BN directions x 64 dims
   static constexpr int STAGE = 3 * A_BYTES + B_BYTES;       // hi, mid, lo pieces share one direction tile
   static constexpr int BAR_OFF = STAGES * STAGE;
-  static constexpr int RANGE_OFF = BAR_OFF + 8 * (2 * STAGES + 1) + 16;
-  static constexpr int TOTAL = RANGE_OFF + 4 * 4 * BN + 1024;   // + per-CTA range partials + alignment slack
+  static constexpr int RANGE_OFF = BAR_OFF + 8 * (2 * STAGES + 4) + 16;
+  static constexpr int FIXED = RANGE_OFF + 1024;            // + per-CTA range partials [np_pad][4] + slack
 };
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Persistent: grid = min(#tiles, #SMs) CTAs, tiles t = blockIdx.x + i*gridDim.x (slice tiles fastest, so the
+// CTAs that share a point tile run together and its TMA loads hit L2).  Two TMEM accumulators: the epilogue
+// of tile i overlaps the MMAs of tile i+1.  Per-slice ranges: per-CTA partials in smem -> part[cta][s][4].
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nk, int64_t L,
               int64_t Nx, int np, const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz,
-              unsigned* __restrict__ mm, int* __restrict__ flag) {
+              unsigned* __restrict__ part, int* __restrict__ flag) {
   using SM = TcSmem<BN, STAGES>;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + SM::BAR_OFF);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-  unsigned* rng = reinterpret_cast<unsigned*>(sm + SM::RANGE_OFF);   // [BN][4] per-CTA range partials (keys)
-  for (int c = threadIdx.x; c < BN; c += blockDim.x) {
+  uint64_t* tfull = empty + STAGES;     // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  unsigned* rng = reinterpret_cast<unsigned*>(sm + SM::RANGE_OFF);   // [np_pad][4] keys
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntn = (np + BN - 1) / BN;
+  const int64_t ntm = (L + TC_M - 1) / TC_M;
+  const int64_t ntiles = ntm * ntn;
+  for (int c = threadIdx.x; c < ntn * BN; c += blockDim.x) {
     rng[4 * c + 0] = 0xffffffffu; rng[4 * c + 1] = 0u; rng[4 * c + 2] = 0xffffffffu; rng[4 * c + 3] = 0u;
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * TC_M;
-  const int n0 = blockIdx.y * BN;
-
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem_d = *tmem_slot;
+  const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer
-    for (int kb = 0; kb < nk; ++kb) {   // nk = dp / 64 k-blocks; piece q of x lives at column q*dp
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      unsigned char* sa = sm + s * SM::STAGE;
-      unsigned char* sb = sa + 3 * SM::A_BYTES;
-      mbar_expect_tx(&full[s], SM::STAGE);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int m0 = static_cast<int>((t / ntn) * TC_M), n0 = static_cast<int>(t % ntn) * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char* sa = sm + stage * SM::STAGE;
+        mbar_expect_tx(&full[stage], SM::STAGE);
 #pragma unroll
-      for (int q = 0; q < 3; ++q)
-        tma_load_2d(&tmA, &full[s], sa + q * SM::A_BYTES, q * nk * TC_BK + kb * TC_BK, static_cast<int>(m0));
-      tma_load_2d(&tmB, &full[s], sb, kb * TC_BK, n0);
+        for (int q = 0; q < 3; ++q) tma_load_2d(&tmA, &full[stage], sa + q * SM::A_BYTES, (q * nk + kb) * TC_BK, m0);
+        tma_load_2d(&tmB, &full[stage], sa + 3 * SM::A_BYTES, kb * TC_BK, n0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (single thread)
     constexpr uint32_t idesc = idesc_bf16(TC_M, BN);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&full[s], ph);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int b = it & 1;
+      const uint32_t tph = (it >> 1) & 1;
+      mbar_wait(&tempty[b], tph ^ 1);   // epilogue drained this accumulator
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const unsigned char* sa = sm + s * SM::STAGE;
-      const unsigned char* sb = sa + 3 * SM::A_BYTES;
-      const uint64_t db = umma_desc_sw128(sb);
+      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(b * BN);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const unsigned char* sa = sm + stage * SM::STAGE;
+        const uint64_t db = umma_desc_sw128(sa + 3 * SM::A_BYTES);
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const uint64_t da = umma_desc_sw128(sa + q * SM::A_BYTES);
+        for (int q = 0; q < 3; ++q) {
+          const uint64_t da = umma_desc_sw128(sa + q * SM::A_BYTES);
 #pragma unroll
-        for (int k = 0; k < TC_BK / 16; ++k) {
-          const uint32_t acc = (kb > 0 || q > 0 || k > 0) ? 1u : 0u;
-          const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);   // +32 bytes along K inside the swizzle row
-          asm volatile(
-              "{\n\t.reg .pred p;\n\t"
-              "setp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-              "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            const uint32_t acc = (kb > 0 || q > 0 || k > 0) ? 1u : 0u;
+            const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);   // +32 B along K inside the swizzle row
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+          }
         }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[stage]))
+                     : "memory");
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(&empty[s]))
+                       smem_u32(&tfull[b]))
                    : "memory");
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(tfull))
-                 : "memory");
   } else if (warp >= 4) {
     // ---- epilogue: TMEM lane quadrant q = warp - 4 holds points m0 + 32q + lane
     const int q = warp - 4;
-    const int64_t i = m0 + 32 * q + lane;
-    const bool valid = i < L;
-    const bool isx = i < Nx;
-    const int64_t w0 = m0 + 32 * q;                       // this warp's 32 points
-    const bool tile_all_x = (w0 + 32 <= Nx);              // warp-uniform
-    const bool tile_any_x = (w0 < Nx);
-    mbar_wait(tfull, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
     bool bad = false;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int b = it & 1;
+      const uint32_t tph = (it >> 1) & 1;
+      const int64_t m0 = (t / ntn) * TC_M;
+      const int n0 = static_cast<int>(t % ntn) * BN;
+      const int64_t w0 = m0 + 32 * q;
+      const int64_t i = w0 + lane;
+      const bool valid = i < L, isx = i < Nx;
+      const bool warp_all_x = (w0 + 32 <= Nx), warp_any_x = (w0 < Nx);
+      mbar_wait(&tfull[b], tph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tbase = tmem_base + static_cast<uint32_t>(b * BN) + (static_cast<uint32_t>(32 * q) << 16);
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t v[16];
-      const uint32_t taddr = tmem_d + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(c0);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-          "%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        if (n0 + c0 >= np) break;   // warp-uniform
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(tbase + static_cast<uint32_t>(c0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int s = n0 + c0 + j;
-        if (s >= np) break;   // warp-uniform
-        const float z = __uint_as_float(v[j]) * __ldg(inv_norm + s);
-        if (valid) {
-          Z[static_cast<int64_t>(s) * ldz + i] = z;
-          bad |= !isfinite(z);
-        }
-        // per-slice ranges: one redux.sync per bound on order-preserving keys (x range and all range)
-        const unsigned key = f2key_tc(z);
-        const unsigned amn = __reduce_min_sync(0xffffffffu, valid ? key : 0xffffffffu);
-        const unsigned amx = __reduce_max_sync(0xffffffffu, valid ? key : 0u);
-        unsigned xmn = amn, xmx = amx;
-        if (!tile_all_x) {
-          xmn = __reduce_min_sync(0xffffffffu, (valid && isx) ? key : 0xffffffffu);
-          xmx = __reduce_max_sync(0xffffffffu, (valid && isx) ? key : 0u);
-        }
-        if (lane == 0) {
-          const int c = c0 + j;
-          if (amn <= amx) { atomicMin(&rng[4 * c + 2], amn); atomicMax(&rng[4 * c + 3], amx); }
-          if (tile_any_x && xmn <= xmx) { atomicMin(&rng[4 * c + 0], xmn); atomicMax(&rng[4 * c + 1], xmx); }
+        for (int j = 0; j < 16; ++j) {
+          const int s = n0 + c0 + j;
+          if (s >= np) break;   // warp-uniform
+          const float z = __uint_as_float(v[j]) * __ldg(inv_norm + s);
+          if (valid) {
+            Z[static_cast<int64_t>(s) * ldz + i] = z;
+            bad |= !isfinite(z);
+          }
+          const unsigned key = f2key_tc(z);
+          const unsigned amn = __reduce_min_sync(0xffffffffu, valid ? key : 0xffffffffu);
+          const unsigned amx = __reduce_max_sync(0xffffffffu, valid ? key : 0u);
+          unsigned xmn = amn, xmx = amx;
+          if (!warp_all_x) {
+            xmn = __reduce_min_sync(0xffffffffu, (valid && isx) ? key : 0xffffffffu);
+            xmx = __reduce_max_sync(0xffffffffu, (valid && isx) ? key : 0u);
+          }
+          if (lane == 0) {
+            if (amn <= amx) { atomicMin(&rng[4 * s + 2], amn); atomicMax(&rng[4 * s + 3], amx); }
+            if (warp_any_x && xmn <= xmx) { atomicMin(&rng[4 * s + 0], xmn); atomicMax(&rng[4 * s + 1], xmx); }
+          }
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
     }
     if (bad) atomicOr(flag, 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  // one global update per slice and bound, only when this CTA improves the current extreme
-  for (int c = threadIdx.x; c < BN; c += blockDim.x) {
-    const int s = n0 + c;
-    if (s >= np) break;
-    const unsigned v0 = rng[4 * c + 0], v1 = rng[4 * c + 1], v2 = rng[4 * c + 2], v3 = rng[4 * c + 3];
-    if (v0 <= v1) {
-      if (v0 < *reinterpret_cast<volatile unsigned*>(&mm[s * 4 + 0])) atomicMin(&mm[s * 4 + 0], v0);
-      if (v1 > *reinterpret_cast<volatile unsigned*>(&mm[s * 4 + 1])) atomicMax(&mm[s * 4 + 1], v1);
-    }
-    if (v2 <= v3) {
-      if (v2 < *reinterpret_cast<volatile unsigned*>(&mm[s * 4 + 2])) atomicMin(&mm[s * 4 + 2], v2);
-      if (v3 > *reinterpret_cast<volatile unsigned*>(&mm[s * 4 + 3])) atomicMax(&mm[s * 4 + 3], v3);
-    }
+  for (int e = threadIdx.x; e < 4 * np; e += blockDim.x) part[static_cast<int64_t>(blockIdx.x) * 4 * np + e] = rng[e];
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+}
+
+__global__ void k_range_reduce(const unsigned* __restrict__ part, int nparts, int np, unsigned* __restrict__ mm) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 4 * np) return;
+  const bool is_min = (e & 1) == 0;
+  unsigned v = mm[e];
+  for (int c = 0; c < nparts; ++c) {
+    const unsigned u = part[static_cast<int64_t>(c) * 4 * np + e];
+    v = is_min ? min(v, u) : max(v, u);
   }
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN));
+  mm[e] = v;
 }
 
 // fp32 -> three bf16 pieces, K-concatenated:  Xs[i][j] = hi, Xs[i][dp+j] = mid, Xs[i][2dp+j] = lo
@@ -285,15 +311,20 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_k, 
 
 template <int BN, int STAGES>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int64_t L, int64_t Nx, int np,
-                      const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, cudaStream_t st) {
+                      const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, unsigned* part,
+                      cudaStream_t st) {
   using SM = TcSmem<BN, STAGES>;
+  const int ntn = (np + BN - 1) / BN;
+  const size_t smem = SM::FIXED + static_cast<size_t>(16) * ntn * BN;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_proj_tc<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
+    cudaFuncSetAttribute(k_proj_tc<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  dim3 grid(static_cast<unsigned>((L + TC_M - 1) / TC_M), static_cast<unsigned>((np + BN - 1) / BN));
-  k_proj_tc<BN, STAGES><<<grid, 256, SM::TOTAL, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag);
+  const int64_t ntiles = ((L + TC_M - 1) / TC_M) * ntn;
+  const int grid = static_cast<int>(ntiles < kProjMaxCtas ? ntiles : kProjMaxCtas);
+  k_proj_tc<BN, STAGES><<<grid, 256, smem, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, part, flag);
+  k_range_reduce<<<(4 * np + 255) / 256, 256, 0, st>>>(part, grid, np, mm);
   return cudaGetLastError();
 }
 
@@ -310,8 +341,11 @@ cudaError_t launch_split3(const float* x, int64_t N, const float* y, int64_t M, 
   return cudaGetLastError();
 }
 
+size_t proj_tc_part_bytes(int np) { return static_cast<size_t>(kProjMaxCtas) * 16 * np; }
+
 cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, const void* g3 /* bf16 [np][dp] */, int np,
-                              const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, cudaStream_t st) {
+                              const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, void* part,
+                              cudaStream_t st) {
   const int dp = proj_tc_dpad(d);
   const int nk = dp / TC_BK;
   const int BN = np > 128 ? 256 : (np > 64 ? 128 : 64);
@@ -319,9 +353,11 @@ cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, cons
   if (!make_map(&ta, xs, static_cast<uint64_t>(L), static_cast<uint64_t>(3 * dp), TC_M)) return cudaErrorInvalidValue;
   if (!make_map(&tb, g3, static_cast<uint64_t>(np), static_cast<uint64_t>(dp), static_cast<uint32_t>(BN)))
     return cudaErrorInvalidValue;
-  if (BN == 256) return launch_tc<256, 2>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
-  if (BN == 128) return launch_tc<128, 3>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
-  return launch_tc<64, 3>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, st);
+  unsigned* pp = static_cast<unsigned*>(part);
+  if (np > 4096) return cudaErrorInvalidValue;   // range partials live in shared memory
+  if (BN == 256) return launch_tc<256, 2>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, pp, st);
+  if (BN == 128) return launch_tc<128, 3>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, pp, st);
+  return launch_tc<64, 3>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, pp, st);
 }
 
 }  // namespace sks
