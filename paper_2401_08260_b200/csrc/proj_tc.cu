@@ -83,7 +83,7 @@ struct TcSmem {
   static constexpr int STAGE = 3 * A_BYTES + B_BYTES;       // hi, mid, lo pieces share one direction tile
   static constexpr int BAR_OFF = STAGES * STAGE;
   static constexpr int RANGE_OFF = BAR_OFF + 8 * (2 * STAGES + 4) + 16;
-  static constexpr int FIXED = RANGE_OFF + 1024;            // + per-CTA range partials [np_pad][4] + slack
+  static constexpr int FIXED = RANGE_OFF + 1024;            // + per-CTA range partials [np_pad][4], 1/||g|| + slack
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -93,8 +93,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Persistent: grid = min(#tiles, #SMs) CTAs, tiles t = blockIdx.x + i*gridDim.x (slice tiles fastest, so the
 // CTAs that share a point tile run together and its TMA loads hit L2).  Two TMEM accumulators: the epilogue
 // of tile i overlaps the MMAs of tile i+1.  Per-slice ranges: per-CTA partials in smem -> part[cta][s][4].
+constexpr int TC_THREADS = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue (2 warpgroups)
+
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(TC_THREADS, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nk, int64_t L,
               int64_t Nx, int np, const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz,
               unsigned* __restrict__ part, int* __restrict__ flag) {
@@ -109,6 +111,8 @@ __global__ void __launch_bounds__(256, 1)
   unsigned* rng = reinterpret_cast<unsigned*>(sm + SM::RANGE_OFF);   // [np_pad][4] keys
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntn = (np + BN - 1) / BN;
+  float* sinv = reinterpret_cast<float*>(rng + 4 * ntn * BN);          // [np_pad] 1/||g_p||
+  for (int c = threadIdx.x; c < ntn * BN; c += blockDim.x) sinv[c] = (c < np) ? inv_norm[c] : 0.f;
   const int64_t ntm = (L + TC_M - 1) / TC_M;
   const int64_t ntiles = ntm * ntn;
   for (int c = threadIdx.x; c < ntn * BN; c += blockDim.x) {
@@ -116,7 +120,7 @@ __global__ void __launch_bounds__(256, 1)
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -188,38 +192,53 @@ __global__ void __launch_bounds__(256, 1)
                    : "memory");
     }
   } else if (warp >= 4) {
-    // ---- epilogue: TMEM lane quadrant q = warp - 4 holds points m0 + 32q + lane
-    const int q = warp - 4;
+    // ---- epilogue: warp w handles TMEM lane quadrant q = w % 4 (points m0 + 32q + lane) and the column half
+    //      h = (w - 4) / 4 of the accumulator
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    constexpr int HALF = BN / 2;
     bool bad = false;
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int b = it & 1;
       const uint32_t tph = (it >> 1) & 1;
       const int64_t m0 = (t / ntn) * TC_M;
-      const int n0 = static_cast<int>(t % ntn) * BN;
+      const int n0 = static_cast<int>(t % ntn) * BN + h * HALF;
       const int64_t w0 = m0 + 32 * q;
       const int64_t i = w0 + lane;
       const bool valid = i < L, isx = i < Nx;
       const bool warp_all_x = (w0 + 32 <= Nx), warp_any_x = (w0 < Nx);
+      const int ncols = min(HALF, np - n0);   // may be <= 0
       mbar_wait(&tfull[b], tph);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t tbase = tmem_base + static_cast<uint32_t>(b * BN) + (static_cast<uint32_t>(32 * q) << 16);
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        if (n0 + c0 >= np) break;   // warp-uniform
-        uint32_t v[16];
+      const uint32_t tbase =
+          tmem_base + static_cast<uint32_t>(b * BN + h * HALF) + (static_cast<uint32_t>(32 * q) << 16);
+      uint32_t v[16];
+      if (ncols > 0)
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
             "%14, %15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(tbase + static_cast<uint32_t>(c0)));
+            : "r"(tbase));
+#pragma unroll 1
+      for (int c0 = 0; c0 < ncols; c0 += 16) {
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t cur[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cur[j] = v[j];
+        if (c0 + 16 < ncols)   // prefetch the next 16 columns while this chunk is processed
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+              "%14, %15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(tbase + static_cast<uint32_t>(c0 + 16)));
+        unsigned my_amn = 0xffffffffu, my_amx = 0u, my_xmn = 0xffffffffu, my_xmx = 0u;   // lane j keeps column j
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int s = n0 + c0 + j;
-          if (s >= np) break;   // warp-uniform
-          const float z = __uint_as_float(v[j]) * __ldg(inv_norm + s);
+          if (c0 + j >= ncols) break;   // warp-uniform
+          const float z = __uint_as_float(cur[j]) * sinv[s];
           if (valid) {
             Z[static_cast<int64_t>(s) * ldz + i] = z;
             bad |= !isfinite(z);
@@ -232,10 +251,12 @@ __global__ void __launch_bounds__(256, 1)
             xmn = __reduce_min_sync(0xffffffffu, (valid && isx) ? key : 0xffffffffu);
             xmx = __reduce_max_sync(0xffffffffu, (valid && isx) ? key : 0u);
           }
-          if (lane == 0) {
-            if (amn <= amx) { atomicMin(&rng[4 * s + 2], amn); atomicMax(&rng[4 * s + 3], amx); }
-            if (warp_any_x && xmn <= xmx) { atomicMin(&rng[4 * s + 0], xmn); atomicMax(&rng[4 * s + 1], xmx); }
-          }
+          if (lane == j) { my_amn = amn; my_amx = amx; my_xmn = xmn; my_xmx = xmx; }
+        }
+        if (lane < 16 && c0 + lane < ncols) {   // one lane per column: no divergent per-column branches
+          const int s = n0 + c0 + lane;
+          if (my_amn <= my_amx) { atomicMin(&rng[4 * s + 2], my_amn); atomicMax(&rng[4 * s + 3], my_amx); }
+          if (warp_any_x && my_xmn <= my_xmx) { atomicMin(&rng[4 * s + 0], my_xmn); atomicMax(&rng[4 * s + 1], my_xmx); }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -315,7 +336,7 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int6
                       cudaStream_t st) {
   using SM = TcSmem<BN, STAGES>;
   const int ntn = (np + BN - 1) / BN;
-  const size_t smem = SM::FIXED + static_cast<size_t>(16) * ntn * BN;
+  const size_t smem = SM::FIXED + static_cast<size_t>(20) * ntn * BN;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_proj_tc<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -323,7 +344,7 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int6
   }
   const int64_t ntiles = ((L + TC_M - 1) / TC_M) * ntn;
   const int grid = static_cast<int>(ntiles < kProjMaxCtas ? ntiles : kProjMaxCtas);
-  k_proj_tc<BN, STAGES><<<grid, 256, smem, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, part, flag);
+  k_proj_tc<BN, STAGES><<<grid, TC_THREADS, smem, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, part, flag);
   k_range_reduce<<<(4 * np + 255) / 256, 256, 0, st>>>(part, grid, np, mm);
   return cudaGetLastError();
 }
