@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -429,8 +430,28 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
       sa.s64 = s64;
       sa.per_slice_out = tps;
-      ProfScope ps(PS_BUCKET, st);
-      SKS_CUDA(sks::launch_sortpath(sa, sks::sortpath_slots(nbat), st));
+      static const bool phase_timing = std::getenv("SKS_PHASE_TIMING") != nullptr;
+      static long long* dbg = nullptr;
+      const int slots = sks::sortpath_slots(nbat);
+      if (phase_timing) {
+        if (!dbg) SKS_CUDA(cudaMalloc(&dbg, sizeof(long long) * 8 * 4 * 160));
+        SKS_CUDA(cudaMemsetAsync(dbg, 0, sizeof(long long) * 8 * 4 * 160, st));
+        sa.dbg = dbg;
+      }
+      {
+        ProfScope ps(PS_BUCKET, st);
+        SKS_CUDA(sks::launch_sortpath(sa, slots, st));
+      }
+      if (phase_timing) {
+        std::vector<long long> h(8 * 4 * slots);
+        SKS_CUDA(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
+        SKS_CUDA(cudaStreamSynchronize(st));
+        double avg[8] = {0};
+        for (int c = 0; c < 4 * slots; ++c)
+          for (int k = 0; k < 8; ++k) avg[k] += h[8 * c + k] / (4.0 * slots);
+        std::fprintf(stderr, "[sks phase cycles per slice] P0+map %.0f  P1 %.0f  P2 %.0f  P3 %.0f  P4/5 %.0f  P6 %.0f\n",
+                     avg[0], avg[1], avg[2], avg[3], avg[4], avg[5]);
+      }
       ++launches;
       ea.tot = sa.tot;
     }

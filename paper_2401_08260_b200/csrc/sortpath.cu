@@ -146,7 +146,11 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
   const int64_t x0 = N * rank / SP_C, x1 = N * (rank + 1) / SP_C;
   const int64_t y0 = M * rank / SP_C, y1 = M * (rank + 1) / SP_C;
 
+  long long tph[10];
+  int nph = 0;
+#define PHASE() do { if (a.dbg && tid == 0 && p == slot) tph[nph++] = clock64(); } while (0)
   for (int p = slot; p < a.np; p += nslots) {
+    PHASE();
     const float* zx = a.zv.zx + p * a.zv.ldx;
     const float* zy = a.zv.zy + p * a.zv.ldy;
     const float zmin = key2f_dev(a.mm[p * 4 + 0]), zmax = key2f_dev(a.mm[p * 4 + 1]);
@@ -233,6 +237,7 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
     const int hi = (own_g1 < NG) ? S.gtab[own_g1].x : NB;
     const int nown = hi - lo;
 
+    PHASE();
     // ---- P1: bucket histograms of my quarter
     for (int64_t base = x0; base < x1; base += U * SP_T) {
       float zz[U];
@@ -258,6 +263,7 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
     }
     cluster.sync();
 
+    PHASE();
     // ---- P2: owners sum the ranks' histograms of their buckets, scan, write every rank's cursors
     for (int j = tid; j < nown; j += SP_T) {
       int tx = 0, ty = 0;
@@ -298,6 +304,7 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
     }
     cluster.sync();
 
+    PHASE();
     // ---- P3: scatter my quarter
     for (int64_t base = x0; base < x1; base += U * SP_T) {
       float zz[U], ww[U];
@@ -332,6 +339,7 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
     }
     cluster.sync();   // release/acquire at cluster scope: the scattered xs/ys are visible to the owners
 
+    PHASE();
     // ---- P4 + P5: owner bucket sums (thread per run of consecutive buckets, fp64), exclusive scan, records
     const int per = (nown + SP_T - 1) / SP_T;
     const int j0 = min(nown, tid * per), j1 = min(nown, j0 + per);
@@ -387,6 +395,7 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
       }
       __syncthreads();
 
+      PHASE();
       // ---- P6: my targets in bucket order
       const int t0 = S.oy[0], t1 = S.oy[nown];
       for (int base = t0; base < t1; base += 2 * SP_T) {
@@ -426,8 +435,12 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
         }
       }
     }
+    PHASE();
     cluster.sync();   // slot scratch and smem are reused by the next slice
   }
+  if (a.dbg && tid == 0)
+    for (int k = 0; k + 1 < nph; ++k) a.dbg[static_cast<int64_t>(blockIdx.x) * 8 + k] = tph[k + 1] - tph[k];
+#undef PHASE
 }
 
 }  // namespace
