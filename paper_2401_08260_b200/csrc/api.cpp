@@ -433,6 +433,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       static const bool phase_timing = std::getenv("SKS_PHASE_TIMING") != nullptr;
       static long long* dbg = nullptr;
       const int slots = sks::sortpath_slots(nbat);
+      if (const char* v = std::getenv("SKS_SORT_VARIANT")) sa.variant = std::atoi(v);
       if (phase_timing) {
         if (!dbg) SKS_CUDA(cudaMalloc(&dbg, sizeof(long long) * 8 * 4 * 160));
         SKS_CUDA(cudaMemsetAsync(dbg, 0, sizeof(long long) * 8 * 4 * 160, st));

@@ -317,8 +317,13 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
 #pragma unroll
       for (int k = 0; k < U; ++k)
         if (base + tid + k * SP_T < x1) {
-          const int pos = atomicAdd(&S.hx[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
-          xsp[pos] = make_float2(zz[k], ww[k]);
+          if (a.variant == 2) {
+            atomicAdd(&S.hx[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
+            xsp[base + tid + k * SP_T] = make_float2(zz[k], ww[k]);
+          } else {
+            const int pos = atomicAdd(&S.hx[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
+            if (a.variant != 1) xsp[pos] = make_float2(zz[k], ww[k]);
+          }
         }
     }
     for (int64_t base = y0; base < y1; base += U * SP_T) {
@@ -332,8 +337,13 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
       for (int k = 0; k < U; ++k) {
         const int64_t i = base + tid + k * SP_T;
         if (i < y1) {
-          const int pos = atomicAdd(&S.hy[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
-          ysp[pos] = make_float2(zz[k], __int_as_float(static_cast<int>(i)));
+          if (a.variant == 2) {
+            atomicAdd(&S.hy[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
+            ysp[i] = make_float2(zz[k], __int_as_float(static_cast<int>(i)));
+          } else {
+            const int pos = atomicAdd(&S.hy[bin_of(zz[k], zmin, gscale, S.gtab)], 1);
+            if (a.variant != 1) ysp[pos] = make_float2(zz[k], __int_as_float(static_cast<int>(i)));
+          }
         }
       }
     }
