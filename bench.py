@@ -210,7 +210,8 @@ def main():
     x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
     param = I.kernel_param(cfg)
     scale = param if cfg.kind != "negdist" else 1.0
-    p0, p1 = rank * cfg.P // G, (rank + 1) * cfg.P // G
+    from paper_2401_08260_b200.parallel import slice_range
+    p0, p1 = slice_range(rank, G, cfg.P)
     xd, yd, wd = (torch.from_numpy(a).to(dev) for a in (x, y, w))
     ws = torch.empty(S.sks_workspace_size(cfg.N, cfg.M, cfg.d, cfg.kind, scale, cfg.P, p0, p1, cfg.matern_p),
                      dtype=torch.uint8, device=dev)
