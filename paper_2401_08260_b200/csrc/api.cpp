@@ -125,7 +125,7 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
+  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, ovf = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
          flag = 0, total = 0;
 };
 
@@ -162,6 +162,7 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb,
     L.ys = take(sizeof(float2) * M * slots);
     L.rec = take(sizeof(sks::BucketRec) * nb * static_cast<size_t>(slots));
     L.tot = take(sizeof(sks::SliceTot) * static_cast<size_t>(nbat));
+    L.ovf = take(sizeof(int) * static_cast<size_t>(nbat));
     L.bpar = take(sizeof(float) * 2 * nbat);
   }
   if (pt.fourier) {
@@ -430,6 +431,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
       sa.s64 = s64;
       sa.per_slice_out = tps;
+      sa.ovf = reinterpret_cast<int*>(ws + L.ovf);
       static const bool phase_timing = std::getenv("SKS_PHASE_TIMING") != nullptr;
       static long long* dbg = nullptr;
       const int slots = sks::sortpath_slots(nbat);

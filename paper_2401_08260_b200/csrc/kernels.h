@@ -71,6 +71,8 @@ struct SortArgs {
   double coef;           // t = -coef * sum_n w_n |x_n - z|   (c_d, or alpha c_d for the Laplacian part)
   double* s64;           // accumulate t into s64[m] (fp64 atomics), or
   float* per_slice_out;  // store t into per_slice_out[p*M + m]
+  int* ovf;              // [np] slices the DSMEM-resident kernel could not hold (done by the global kernel)
+  int only_flagged;      // global kernel: process only slices with ovf[p] != 0
   int variant;           // debug/measurement variants of the scatter (0 = normal)
   long long* dbg;        // optional [grid][8] per-phase cycle counts of each CTA's first slice (SKS_PHASE_TIMING)
 };

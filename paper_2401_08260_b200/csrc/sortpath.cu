@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -150,6 +151,7 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
   int nph = 0;
 #define PHASE() do { if (a.dbg && tid == 0 && p == slot) tph[nph++] = clock64(); } while (0)
   for (int p = slot; p < a.np; p += nslots) {
+    if (a.only_flagged && !a.ovf[p]) continue;   // uniform across the cluster
     PHASE();
     const float* zx = a.zv.zx + p * a.zv.ldx;
     const float* zy = a.zv.zy + p * a.zv.ldy;
@@ -453,6 +455,334 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
 #undef PHASE
 }
 
+// ======================================================================================================
+// DSMEM-resident variant (default when a slice fits): a cluster of C = 8 or 16 CTAs per slice; every owner
+// CTA keeps ITS buckets' x entries (z, w) and y entries (z, m) in its own shared memory.  The scatter is a
+// DSMEM store into the owner, the bucket sums / scans / target evaluation read local shared memory only.
+// Local histograms are packed 16-bit x|y counters (one u32 per bucket).  A slice whose owners would exceed
+// the capacity (extreme concentration, duplicates) is flagged in a.ovf and done by k_sortsum above.
+constexpr int DS_T = 1024;
+constexpr int DS_CAP = 16384;      // x + y entries an owner holds (128 KB)
+constexpr int DS_OWN = 2048;       // buckets an owner can own
+
+struct DsRec {
+  double A, B;   // exclusive prefix over all buckets left of this one (fp64)
+  float W, Z;    // this bucket's sums (rounded)
+};
+
+struct __align__(16) DsShared {
+  float2 buf[DS_CAP];          // owner: x entries [0, Sx) then y entries [Sx, Sx + Sy), bucket order
+  unsigned hxy[NB];            // local counters -> scatter cursors (x: low 16 bits, y: high 16 bits)
+  unsigned oxy[DS_OWN + 1];    // owner: bucket starts (x | y << 16), y relative to Sx
+  DsRec rec[DS_OWN];
+  int2 gtab[NG];
+  int gx[NG];
+  int gxy[NG];
+  int bnd[17];                 // bucket boundaries of the C owners
+  int wbuf[34];
+  int tot_i[4];
+  double tot_d[4];
+  double wsd[3][DS_T / 32];
+  int ovf;
+};
+
+__device__ __forceinline__ int owner_of(int b, const int* bnd, int C) {
+  int r = 0;
+#pragma unroll
+  for (int step = 8; step >= 1; step >>= 1)
+    if (r + step < C && b >= bnd[r + step]) r += step;
+  return r;
+}
+
+template <int C>
+__global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  DsShared& S = *reinterpret_cast<DsShared*>(smraw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int slot = blockIdx.x / C, nslots = gridDim.x / C;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int W = DS_T / 32;
+  const int64_t N = a.zv.N, M = a.zv.M;
+  const int64_t x0 = N * rank / C, x1 = N * (rank + 1) / C;
+  const int64_t y0 = M * rank / C, y1 = M * (rank + 1) / C;
+  constexpr int U = 8;
+
+  for (int p = slot; p < a.np; p += nslots) {
+    const float* zx = a.zv.zx + p * a.zv.ldx;
+    const float* zy = a.zv.zy + p * a.zv.ldy;
+    const float zmin = key2f_dev(a.mm[p * 4 + 0]), zmax = key2f_dev(a.mm[p * 4 + 1]);
+    const float range = zmax - zmin;
+    const float gscale = (range > 0.f) ? static_cast<float>(NG) / range : 0.f;
+    if (rank == 0 && tid == 0) { a.bpar[p * 2 + 0] = zmin; a.bpar[p * 2 + 1] = gscale; }
+
+    // ---- P0: granule histograms of my 1/C share -> bucket map + ownership (identical in every rank)
+    for (int b = tid; b < NB; b += DS_T) S.hxy[b] = 0u;
+    for (int g = tid; g < NG; g += DS_T) { S.gx[g] = 0; S.gxy[g] = 0; }
+    if (tid == 0) S.ovf = 0;
+    __syncthreads();
+    for (int64_t base = x0; base < x1; base += U * DS_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * DS_T;
+        zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * DS_T < x1) atomicAdd(&S.gx[gran_of(zz[k], zmin, gscale)], 1);
+    }
+    for (int64_t base = y0; base < y1; base += U * DS_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * DS_T;
+        zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * DS_T < y1) atomicAdd(&S.gxy[gran_of(zz[k], zmin, gscale)], 1);
+    }
+    __syncthreads();
+    for (int g = tid; g < NG; g += DS_T) S.gxy[g] += S.gx[g];
+    cluster.sync();
+    {
+      __shared__ int gtx[NG], gtxy[NG];
+      for (int g = tid; g < NG; g += DS_T) {
+        int cx = 0, cxy = 0;
+        for (int r = 0; r < C; ++r) {
+          const DsShared* R = cluster.map_shared_rank(&S, r);
+          cx += R->gx[g];
+          cxy += R->gxy[g];
+        }
+        gtx[g] = cx;
+        gtxy[g] = cxy;
+      }
+      __syncthreads();
+      if (wid == 0) {
+        constexpr int PG = NG / 32;
+        long long cx = 0, cxy = 0;
+        for (int q = 0; q < PG; ++q) { cx += gtx[lane * PG + q]; cxy += gtxy[lane * PG + q]; }
+        const long long ix = warp_incl_scan(cx), ixy = warp_incl_scan(cxy);
+        const long long total = __shfl_sync(0xffffffffu, ixy, 31);
+        long long cum = ix - cx, run = ixy - cxy;
+        int prev = (N > 0) ? static_cast<int>((cum * NB) / N) : 0;
+        for (int q = 0; q < PG; ++q) {
+          const int g = lane * PG + q;
+          cum += gtx[g];
+          const int next = (N > 0) ? static_cast<int>((cum * NB) / N) : NB;
+          S.gtab[g] = make_int2(prev, next - prev);
+          prev = next;
+          const long long before = run;
+          run += gtxy[g];
+          for (int r = 1; r < C; ++r)
+            if (before * C < total * r && run * C >= total * r) S.wbuf[r] = g + 1;
+        }
+        if (lane == 0) {
+          S.wbuf[0] = 0;
+          S.wbuf[C] = NG;
+          if (total == 0)
+            for (int r = 1; r < C; ++r) S.wbuf[r] = NG;
+        }
+      }
+      __syncthreads();
+      if (tid <= C) S.bnd[tid] = (S.wbuf[tid] < NG) ? S.gtab[S.wbuf[tid]].x : NB;
+      __syncthreads();
+    }
+    const int lo = S.bnd[rank], hi = S.bnd[rank + 1], nown = hi - lo;
+
+    // ---- P1: packed local counting
+    for (int64_t base = x0; base < x1; base += U * DS_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * DS_T;
+        zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * DS_T < x1) atomicAdd(&S.hxy[bin_of(zz[k], zmin, gscale, S.gtab)], 1u);
+    }
+    for (int64_t base = y0; base < y1; base += U * DS_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * DS_T;
+        zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * DS_T < y1) atomicAdd(&S.hxy[bin_of(zz[k], zmin, gscale, S.gtab)], 0x10000u);
+    }
+    cluster.sync();
+
+    // ---- P2: owner totals, scans, capacity check, cursors into every rank
+    int* tx = reinterpret_cast<int*>(S.rec);   // scratch: [DS_OWN] x totals, [DS_OWN] y totals
+    int* ty = tx + DS_OWN;
+    const bool own_ok = nown <= DS_OWN;
+    if (own_ok) {
+      for (int j = tid; j < nown; j += DS_T) {
+        int cxs = 0, cys = 0;
+        for (int r = 0; r < C; ++r) {
+          const unsigned v = cluster.map_shared_rank(&S, r)->hxy[lo + j];
+          cxs += v & 0xffffu;
+          cys += v >> 16;
+        }
+        tx[j] = cxs;
+        ty[j] = cys;
+      }
+    }
+    __syncthreads();
+    int Sx = 0, Sy = 0;
+    if (own_ok) {
+      Sx = block_scan_int(tx, nown, S.wbuf);
+      Sy = block_scan_int(ty, nown, S.wbuf);
+    }
+    if (tid == 0) S.ovf = (!own_ok || Sx + Sy > DS_CAP) ? 1 : 0;
+    cluster.sync();
+    int any_ovf = 0;
+    for (int r = 0; r < C; ++r) any_ovf |= cluster.map_shared_rank(&S, r)->ovf;
+    if (any_ovf) {
+      if (rank == 0 && tid == 0) a.ovf[p] = 1;
+      cluster.sync();   // nobody still reads this slice's shared state
+      continue;
+    }
+    for (int j = tid; j < nown; j += DS_T) {
+      unsigned bx = static_cast<unsigned>(tx[j]), by = static_cast<unsigned>(Sx + ty[j]);
+      S.oxy[j] = static_cast<unsigned>(tx[j]) | (static_cast<unsigned>(ty[j]) << 16);
+      for (int r = 0; r < C; ++r) {
+        DsShared* R = cluster.map_shared_rank(&S, r);
+        const unsigned v = R->hxy[lo + j];
+        R->hxy[lo + j] = bx | (by << 16);
+        bx += v & 0xffffu;
+        by += v >> 16;
+      }
+    }
+    if (tid == 0) S.oxy[nown] = static_cast<unsigned>(Sx) | (static_cast<unsigned>(Sy) << 16);
+    cluster.sync();
+
+    // ---- P3: scatter my share into the owners' shared memory (DSMEM stores)
+    for (int64_t base = x0; base < x1; base += U * DS_T) {
+      float zz[U], ww[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * DS_T;
+        zz[k] = (i < x1) ? __ldg(zx + i) : 0.f;
+        ww[k] = (i < x1) ? __ldg(a.w + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (base + tid + k * DS_T < x1) {
+          const int b = bin_of(zz[k], zmin, gscale, S.gtab);
+          const unsigned pos = atomicAdd(&S.hxy[b], 1u) & 0xffffu;
+          cluster.map_shared_rank(&S, owner_of(b, S.bnd, C))->buf[pos] = make_float2(zz[k], ww[k]);
+        }
+    }
+    for (int64_t base = y0; base < y1; base += U * DS_T) {
+      float zz[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * DS_T;
+        zz[k] = (i < y1) ? __ldg(zy + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + tid + k * DS_T;
+        if (i < y1) {
+          const int b = bin_of(zz[k], zmin, gscale, S.gtab);
+          const unsigned pos = atomicAdd(&S.hxy[b], 0x10000u) >> 16;
+          cluster.map_shared_rank(&S, owner_of(b, S.bnd, C))->buf[pos] =
+              make_float2(zz[k], __int_as_float(static_cast<int>(i)));
+        }
+      }
+    }
+    cluster.sync();
+
+    // ---- P4/P5: owner bucket sums (fp64, from shared memory), exclusive scan with cross-rank offsets
+    const int per = (nown + DS_T - 1) / DS_T;
+    const int j0 = min(nown, tid * per), j1 = min(nown, j0 + per);
+    double lA = 0.0, lB = 0.0, lC = 0.0;
+    for (int j = j0; j < j1; ++j) {
+      const int xs0 = S.oxy[j] & 0xffff, xs1 = S.oxy[j + 1] & 0xffff;
+      double Wb = 0.0, Zb = 0.0, Cb = 0.0;
+      for (int i = xs0; i < xs1; ++i) {
+        const float2 q = S.buf[i];
+        const double wz = static_cast<double>(q.y) * q.x;
+        Wb += q.y;
+        Zb += wz;
+        Cb += wz * q.x;
+      }
+      S.rec[j].W = static_cast<float>(Wb);   // rec[j].W / .Z overlap the tx/ty scratch only for j < DS_OWN/..:
+      S.rec[j].Z = static_cast<float>(Zb);   // tx/ty are dead after P2 (their values live in oxy)
+      S.rec[j].A = Wb;                       // temporarily the bucket sums (fp64)
+      S.rec[j].B = Zb;
+      lA += Wb;
+      lB += Zb;
+      lC += Cb;
+    }
+    {
+      const double iA = warp_incl_scan(lA), iB = warp_incl_scan(lB);
+      const double sC = warp_sum(lC);
+      if (lane == 31) { S.wsd[0][wid] = iA; S.wsd[1][wid] = iB; }
+      if (lane == 0) S.wsd[2][wid] = sC;
+      __syncthreads();
+      if (wid == 0) {
+        const double va = S.wsd[0][lane], vb = S.wsd[1][lane], vc = S.wsd[2][lane];
+        const double ia = warp_incl_scan(va), ib = warp_incl_scan(vb), sc = warp_sum(vc);
+        S.wsd[0][lane] = ia - va;
+        S.wsd[1][lane] = ib - vb;
+        if (lane == 31) { S.tot_d[0] = ia; S.tot_d[1] = ib; }
+        if (lane == 0) S.tot_d[2] = sc;
+      }
+      cluster.sync();
+      double TA = 0, TB = 0, TC = 0, PA = 0, PB = 0;
+      for (int r = 0; r < C; ++r) {
+        const DsShared* R = cluster.map_shared_rank(&S, r);
+        TA += R->tot_d[0]; TB += R->tot_d[1]; TC += R->tot_d[2];
+        if (r < rank) { PA += R->tot_d[0]; PB += R->tot_d[1]; }
+      }
+      if (rank == 0 && tid == 0) a.tot[p] = SliceTot{TA, TB, TC, 0.0};
+      double rA = PA + S.wsd[0][wid] + iA - lA, rB = PB + S.wsd[1][wid] + iB - lB;
+      for (int j = j0; j < j1; ++j) {
+        const double Wb = S.rec[j].A, Zb = S.rec[j].B;
+        S.rec[j].A = rA;
+        S.rec[j].B = rB;
+        rA += Wb;
+        rB += Zb;
+      }
+      __syncthreads();
+
+      // ---- P6: my targets in bucket order, everything from shared memory
+      const int Sy0 = Sx;
+      for (int e = tid; e < Sy; e += DS_T) {
+        const float2 y = S.buf[Sy0 + e];
+        const float z = y.x;
+        const int64_t m = __float_as_int(y.y);
+        const int jb = bin_of(z, zmin, gscale, S.gtab) - lo;
+        const DsRec R = S.rec[jb];
+        const int xs0 = S.oxy[jb] & 0xffff, xs1 = S.oxy[jb + 1] & 0xffff;
+        float s0 = 0.f, s1 = 0.f;
+        int i = xs0;
+        for (; i + 2 <= xs1; i += 2) {
+          const float2 q0 = S.buf[i], q1 = S.buf[i + 1];
+          s0 = fmaf(q0.y, fabsf(q0.x - z), s0);
+          s1 = fmaf(q1.y, fabsf(q1.x - z), s1);
+        }
+        if (i < xs1) {
+          const float2 q = S.buf[i];
+          s0 = fmaf(q.y, fabsf(q.x - z), s0);
+        }
+        const double zd = z;
+        const double Ahi = TA - R.A - R.W, Bhi = TB - R.B - R.Z;
+        const double t = -a.coef * ((zd * R.A - R.B) + (Bhi - zd * Ahi) + static_cast<double>(s0 + s1));
+        if (a.s64) atomicAdd(a.s64 + m, t);
+        if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
+      }
+    }
+    cluster.sync();   // shared state is reused by the next slice
+  }
+}
+
 }  // namespace
 
 int sortpath_buckets() { return NB; }
@@ -479,7 +809,69 @@ int sortpath_slots(int np) {
   return np < nclusters ? np : nclusters;
 }
 
-cudaError_t launch_sortpath(const SortArgs& a, int slots, cudaStream_t st) {
+namespace {
+template <int C>
+int dsm_clusters() {
+  static int n = -1;
+  if (n < 0) {
+    cudaFuncSetAttribute(k_sortsum_dsm<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(DsShared)));
+    if (C > 8) cudaFuncSetAttribute(k_sortsum_dsm<C>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(C * 16);
+    cfg.blockDim = dim3(DS_T);
+    cfg.dynamicSmemBytes = sizeof(DsShared);
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = C;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int k = 0;
+    if (cudaOccupancyMaxActiveClusters(&k, k_sortsum_dsm<C>, &cfg) != cudaSuccess) k = 0;
+    cudaGetLastError();
+    n = k;
+  }
+  return n;
+}
+
+template <int C>
+cudaError_t launch_dsm(const SortArgs& a, int nclusters, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(C * nclusters));
+  cfg.blockDim = dim3(DS_T);
+  cfg.dynamicSmemBytes = sizeof(DsShared);
+  cfg.stream = st;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = C;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_sortsum_dsm<C>, a);
+}
+}  // namespace
+
+cudaError_t launch_sortpath(const SortArgs& a0, int slots, cudaStream_t st) {
+  SortArgs a = a0;
+  const int64_t L = a.zv.N + a.zv.M;
+  // DSMEM-resident path when an evenly balanced owner holds <= 80% of its capacity
+  int C = 0;
+  if (L * 10 <= static_cast<int64_t>(DS_CAP) * 8 * 8) C = 8;
+  else if (L * 10 <= static_cast<int64_t>(DS_CAP) * 16 * 8) C = 16;
+  if (std::getenv("SKS_SORT_GLOBAL")) C = 0;
+  if (C) {
+    const int ncl = (C == 8) ? dsm_clusters<8>() : dsm_clusters<16>();
+    if (ncl > 0) {
+      cudaError_t e = cudaMemsetAsync(a.ovf, 0, sizeof(int) * a.np, st);
+      if (e != cudaSuccess) return e;
+      const int n = a.np < ncl ? a.np : ncl;
+      e = (C == 8) ? launch_dsm<8>(a, n, st) : launch_dsm<16>(a, n, st);
+      if (e != cudaSuccess) return e;
+      a.only_flagged = 1;   // the global kernel redoes only the slices the DSMEM kernel flagged
+    }
+  }
   k_sortsum<<<slots * SP_C, SP_T, sizeof(Shared), st>>>(a);
   return cudaGetLastError();
 }
