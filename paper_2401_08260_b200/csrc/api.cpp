@@ -437,8 +437,8 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       const int slots = sks::sortpath_slots(nbat);
       if (const char* v = std::getenv("SKS_SORT_VARIANT")) sa.variant = std::atoi(v);
       if (phase_timing) {
-        if (!dbg) SKS_CUDA(cudaMalloc(&dbg, sizeof(long long) * 8 * 4 * 160));
-        SKS_CUDA(cudaMemsetAsync(dbg, 0, sizeof(long long) * 8 * 4 * 160, st));
+        if (!dbg) SKS_CUDA(cudaMalloc(&dbg, sizeof(long long) * 8 * 16 * 160));
+        SKS_CUDA(cudaMemsetAsync(dbg, 0, sizeof(long long) * 8 * 16 * 160, st));
         sa.dbg = dbg;
       }
       {
@@ -446,12 +446,17 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
         SKS_CUDA(sks::launch_sortpath(sa, slots, st));
       }
       if (phase_timing) {
-        std::vector<long long> h(8 * 4 * slots);
+        std::vector<long long> h(8 * 16 * 160);
         SKS_CUDA(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
         SKS_CUDA(cudaStreamSynchronize(st));
         double avg[8] = {0};
-        for (int c = 0; c < 4 * slots; ++c)
-          for (int k = 0; k < 8; ++k) avg[k] += h[8 * c + k] / (4.0 * slots);
+        int ncta = 0;
+        for (int c = 0; c < 16 * 160; ++c)
+          if (h[8 * c] > 0) {
+            ++ncta;
+            for (int k = 0; k < 8; ++k) avg[k] += h[8 * c + k];
+          }
+        for (int k = 0; k < 8; ++k) avg[k] /= (ncta ? ncta : 1);
         std::fprintf(stderr, "[sks phase cycles per slice] P0+map %.0f  P1 %.0f  P2 %.0f  P3 %.0f  P4/5 %.0f  P6 %.0f\n",
                      avg[0], avg[1], avg[2], avg[3], avg[4], avg[5]);
       }

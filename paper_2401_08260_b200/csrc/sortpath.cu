@@ -508,7 +508,11 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
   const int64_t y0 = M * rank / C, y1 = M * (rank + 1) / C;
   constexpr int U = 8;
 
+  long long tph[10];
+  int nph = 0;
+#define PHASE() do { if (a.dbg && tid == 0 && p == slot) tph[nph++] = clock64(); } while (0)
   for (int p = slot; p < a.np; p += nslots) {
+    PHASE();
     const float* zx = a.zv.zx + p * a.zv.ldx;
     const float* zy = a.zv.zy + p * a.zv.ldy;
     const float zmin = key2f_dev(a.mm[p * 4 + 0]), zmax = key2f_dev(a.mm[p * 4 + 1]);
@@ -591,6 +595,7 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
     }
     const int lo = S.bnd[rank], hi = S.bnd[rank + 1], nown = hi - lo;
 
+    PHASE();
     // ---- P1: packed local counting
     for (int64_t base = x0; base < x1; base += U * DS_T) {
       float zz[U];
@@ -616,6 +621,7 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
     }
     cluster.sync();
 
+    PHASE();
     // ---- P2: owner totals, scans, capacity check, cursors into every rank
     int* tx = reinterpret_cast<int*>(S.rec);   // scratch: [DS_OWN] x totals, [DS_OWN] y totals
     int* ty = tx + DS_OWN;
@@ -661,6 +667,7 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
     if (tid == 0) S.oxy[nown] = static_cast<unsigned>(Sx) | (static_cast<unsigned>(Sy) << 16);
     cluster.sync();
 
+    PHASE();
     // ---- P3: scatter my share into the owners' shared memory (DSMEM stores)
     for (int64_t base = x0; base < x1; base += U * DS_T) {
       float zz[U], ww[U];
@@ -698,6 +705,7 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
     }
     cluster.sync();
 
+    PHASE();
     // ---- P4/P5: owner bucket sums (fp64, from shared memory), exclusive scan with cross-rank offsets
     const int per = (nown + DS_T - 1) / DS_T;
     const int j0 = min(nown, tid * per), j1 = min(nown, j0 + per);
@@ -752,6 +760,7 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
       }
       __syncthreads();
 
+      PHASE();
       // ---- P6: my targets in bucket order, everything from shared memory
       const int Sy0 = Sx;
       for (int e = tid; e < Sy; e += DS_T) {
@@ -779,8 +788,12 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
         if (a.per_slice_out) a.per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(t);
       }
     }
+    PHASE();
     cluster.sync();   // shared state is reused by the next slice
   }
+  if (a.dbg && tid == 0)
+    for (int k = 0; k + 1 < nph; ++k) a.dbg[static_cast<int64_t>(blockIdx.x) * 8 + k] = tph[k + 1] - tph[k];
+#undef PHASE
 }
 
 }  // namespace
