@@ -552,15 +552,14 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
     cluster.sync();
     {
       __shared__ int gtx[NG], gtxy[NG];
-      for (int g = tid; g < NG; g += DS_T) {
-        int cx = 0, cxy = 0;
-        for (int r = 0; r < C; ++r) {
-          const DsShared* R = cluster.map_shared_rank(&S, r);
-          cx += R->gx[g];
-          cxy += R->gxy[g];
-        }
-        gtx[g] = cx;
-        gtxy[g] = cxy;
+      for (int g = tid; g < NG; g += DS_T) { gtx[g] = 0; gtxy[g] = 0; }
+      __syncthreads();
+      for (int e = tid; e < NG * C; e += DS_T) {   // all (granule, rank) remote reads in flight at once
+        const int g = e % NG, r = e / NG;
+        const DsShared* R = cluster.map_shared_rank(&S, r);
+        const int vx = R->gx[g], vxy = R->gxy[g];
+        atomicAdd(&gtx[g], vx);
+        atomicAdd(&gtxy[g], vxy);
       }
       __syncthreads();
       if (wid == 0) {
@@ -627,15 +626,13 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
     int* ty = tx + DS_OWN;
     const bool own_ok = nown <= DS_OWN;
     if (own_ok) {
-      for (int j = tid; j < nown; j += DS_T) {
-        int cxs = 0, cys = 0;
-        for (int r = 0; r < C; ++r) {
-          const unsigned v = cluster.map_shared_rank(&S, r)->hxy[lo + j];
-          cxs += v & 0xffffu;
-          cys += v >> 16;
-        }
-        tx[j] = cxs;
-        ty[j] = cys;
+      for (int j = tid; j < nown; j += DS_T) { tx[j] = 0; ty[j] = 0; }
+      __syncthreads();
+      for (int e = tid; e < nown * C; e += DS_T) {   // (bucket, rank) pairs: independent remote reads
+        const int j = e % nown, r = e / nown;
+        const unsigned v = cluster.map_shared_rank(&S, r)->hxy[lo + j];
+        if (v & 0xffffu) atomicAdd(&tx[j], static_cast<int>(v & 0xffffu));
+        if (v >> 16) atomicAdd(&ty[j], static_cast<int>(v >> 16));
       }
     }
     __syncthreads();
@@ -647,21 +644,35 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
     if (tid == 0) S.ovf = (!own_ok || Sx + Sy > DS_CAP) ? 1 : 0;
     cluster.sync();
     int any_ovf = 0;
-    for (int r = 0; r < C; ++r) any_ovf |= cluster.map_shared_rank(&S, r)->ovf;
+    {
+      int f = 0;
+      if (lane < C) f = cluster.map_shared_rank(&S, lane)->ovf;
+      any_ovf = __any_sync(0xffffffffu, f != 0);
+    }
     if (any_ovf) {
       if (rank == 0 && tid == 0) a.ovf[p] = 1;
       cluster.sync();   // nobody still reads this slice's shared state
       continue;
     }
-    for (int j = tid; j < nown; j += DS_T) {
-      unsigned bx = static_cast<unsigned>(tx[j]), by = static_cast<unsigned>(Sx + ty[j]);
-      S.oxy[j] = static_cast<unsigned>(tx[j]) | (static_cast<unsigned>(ty[j]) << 16);
-      for (int r = 0; r < C; ++r) {
-        DsShared* R = cluster.map_shared_rank(&S, r);
-        const unsigned v = R->hxy[lo + j];
-        R->hxy[lo + j] = bx | (by << 16);
-        bx += v & 0xffffu;
-        by += v >> 16;
+    // C consecutive lanes handle one bucket: lane r reads rank r's counters, a segmented shuffle scan over
+    // the C lanes gives each rank's cursor base, lane r writes it back into rank r (all remote ops parallel)
+    for (int e0 = 0; e0 < nown * C; e0 += DS_T) {
+      const int e = e0 + tid;
+      const bool act = e < nown * C;
+      const int j = e / C, r = e % C;
+      unsigned v = 0;
+      if (act) v = cluster.map_shared_rank(&S, r)->hxy[lo + j];
+      unsigned cx = v & 0xffffu, cy = v >> 16;
+#pragma unroll
+      for (int o = 1; o < C; o <<= 1) {   // inclusive scan within groups of C lanes (C divides 32)
+        const unsigned nx = __shfl_up_sync(0xffffffffu, cx, o), ny = __shfl_up_sync(0xffffffffu, cy, o);
+        if ((lane % C) >= o) { cx += nx; cy += ny; }
+      }
+      if (act) {
+        const unsigned bx = static_cast<unsigned>(tx[j]) + cx - (v & 0xffffu);
+        const unsigned by = static_cast<unsigned>(Sx + ty[j]) + cy - (v >> 16);
+        cluster.map_shared_rank(&S, r)->hxy[lo + j] = bx | (by << 16);
+        if (r == 0) S.oxy[j] = static_cast<unsigned>(tx[j]) | (static_cast<unsigned>(ty[j]) << 16);
       }
     }
     if (tid == 0) S.oxy[nown] = static_cast<unsigned>(Sx) | (static_cast<unsigned>(Sy) << 16);
@@ -743,12 +754,19 @@ __global__ void __launch_bounds__(DS_T, 1) k_sortsum_dsm(SortArgs a) {
         if (lane == 0) S.tot_d[2] = sc;
       }
       cluster.sync();
-      double TA = 0, TB = 0, TC = 0, PA = 0, PB = 0;
-      for (int r = 0; r < C; ++r) {
-        const DsShared* R = cluster.map_shared_rank(&S, r);
-        TA += R->tot_d[0]; TB += R->tot_d[1]; TC += R->tot_d[2];
-        if (r < rank) { PA += R->tot_d[0]; PB += R->tot_d[1]; }
+      __shared__ double xt[5];
+      if (wid == 0) {   // lane r reads rank r's partial totals (parallel remote loads), warp reductions
+        double ta = 0, tb = 0, tc = 0;
+        if (lane < C) {
+          const DsShared* R = cluster.map_shared_rank(&S, lane);
+          ta = R->tot_d[0]; tb = R->tot_d[1]; tc = R->tot_d[2];
+        }
+        const double pa = warp_sum(lane < rank ? ta : 0.0), pb = warp_sum(lane < rank ? tb : 0.0);
+        ta = warp_sum(ta); tb = warp_sum(tb); tc = warp_sum(tc);
+        if (lane == 0) { xt[0] = ta; xt[1] = tb; xt[2] = tc; xt[3] = pa; xt[4] = pb; }
       }
+      __syncthreads();
+      const double TA = xt[0], TB = xt[1], TC = xt[2], PA = xt[3], PB = xt[4];
       if (rank == 0 && tid == 0) a.tot[p] = SliceTot{TA, TB, TC, 0.0};
       double rA = PA + S.wsd[0][wid] + iA - lA, rB = PB + S.wsd[1][wid] + iB - lB;
       for (int j = j0; j < j1; ++j) {
