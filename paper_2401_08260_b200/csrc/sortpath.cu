@@ -891,7 +891,9 @@ cudaError_t launch_sortpath(const SortArgs& a0, int slots, cudaStream_t st) {
   int C = 0;
   if (L * 10 <= static_cast<int64_t>(DS_CAP) * 8 * 8) C = 8;
   else if (L * 10 <= static_cast<int64_t>(DS_CAP) * 16 * 8) C = 16;
-  if (std::getenv("SKS_SORT_GLOBAL")) C = 0;
+  // measured on B200 (cfg2): the 4-CTA global-scratch kernel (1.44 ms) beats the DSMEM-resident one (2.0-2.3 ms,
+  // DSMEM stores are transaction-bound like scattered global stores and only 8 16-CTA clusters fit); opt-in
+  if (!std::getenv("SKS_SORT_DSM")) C = 0;
   if (C) {
     const int ncl = (C == 8) ? dsm_clusters<8>() : dsm_clusters<16>();
     if (ncl > 0) {
