@@ -120,12 +120,13 @@ int buckets_for(int64_t N) {
 }
 
 constexpr int kNmax = 16384;   // largest NFFT grid the kernels are built for
+constexpr int kQmax = 1024;    // footprint cells with precomputed interpolation polynomials
 constexpr size_t kAlign = 256;
 inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, ovf = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
+  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, ovf = 0, Q = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
          flag = 0, total = 0;
 };
 
@@ -171,6 +172,7 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb,
     L.D = take(sizeof(float) * (kNmax / 2 + 1) * static_cast<size_t>(nbat));
     L.fpar = take(sizeof(sks::FPar) * nbat);
     L.phi = take(sizeof(float) * (kNmax / 2 + 1));
+    L.Q = take(sizeof(float) * kQmax * (sks::PW_D + 1) * static_cast<size_t>(nbat));
   }
   L.total = o;
   return L;
@@ -276,6 +278,13 @@ sks::CoeffConst coeff_const(const sks_kernel& k, int d) {
   return c;
 }
 
+sks::PolyWin poly_win(const sks::FourierPlan& plan) {
+  sks::PolyWin pw{};
+  pw.w = plan.w;
+  for (size_t i = 0; i < plan.poly.size() && i < sizeof(pw.c) / sizeof(float); ++i) pw.c[i] = plan.poly[i];
+  return pw;
+}
+
 // Fourier part of one batch: planner (one readback of the ranges), device D_k, spread, FFT filter.
 sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView zv, const float* w, int nbat,
                          char* ws, const Layout& L, cudaStream_t st, sks::FourierPlan* plan, int* launches) {
@@ -306,7 +315,7 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
   sks::FPar* hfp = reinterpret_cast<sks::FPar*>(hflag + 4);
   for (int p = 0; p < nbat; ++p) {
     const sks::SlicePlan& sp = plan->slices[p];
-    hfp[p] = sks::FPar{sp.tau, sp.cen, sp.lmin, (sp.klo << 16) | sp.khi};
+    hfp[p] = sks::FPar{sp.tau, sp.cen, sp.lmin, (sp.klo << 16) | sp.khi, sp.lminA, 0};
   }
   float* hphi = reinterpret_cast<float*>(hfp + nbat);
   for (int kk = 0; kk <= n / 2; ++kk) hphi[kk] = plan->phi2inv[kk];
@@ -324,12 +333,13 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
   }
   {
     ProfScope ps(PS_SPREAD, st);
-    SKS_CUDA(sks::launch_spread(zv, w, nbat, dfp, n, o.w, plan->beta, plan->W, reinterpret_cast<float*>(ws + L.grid), st));
+    SKS_CUDA(sks::launch_spread(zv, w, nbat, dfp, n, poly_win(*plan), plan->W, reinterpret_cast<float*>(ws + L.grid), st));
   }
   {
     ProfScope ps(PS_FFT, st);
     SKS_CUDA(sks::launch_fft_filter(reinterpret_cast<const float*>(ws + L.grid), reinterpret_cast<const float*>(ws + L.D),
-                                    nbat, n, reinterpret_cast<float*>(ws + L.h), st));
+                                    nbat, n, reinterpret_cast<float*>(ws + L.h), dfp, poly_win(*plan), plan->WA,
+                                    plan->WA <= kQmax ? reinterpret_cast<float*>(ws + L.Q) : nullptr, st));
   }
   *launches += 4;
   return SKS_OK;
@@ -470,8 +480,9 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ea.fp = reinterpret_cast<const sks::FPar*>(ws + L.fpar);
       ea.h = reinterpret_cast<const float*>(ws + L.h);
       ea.n = plan.n;
-      ea.wt = o.w;
-      ea.beta = plan.beta;
+      ea.pw = poly_win(plan);
+      ea.WA = plan.WA;
+      ea.Q = plan.WA <= kQmax ? reinterpret_cast<const float*>(ws + L.Q) : nullptr;
       info.n_grid = plan.n;
       info.k_max = std::max(info.k_max, plan.k_max);
       info.band_lo_min = plan.band_lo_min;

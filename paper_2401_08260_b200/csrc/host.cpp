@@ -209,6 +209,47 @@ static double window_ft(double xi, int w, double beta, const std::vector<double>
   return half * s;
 }
 
+// ------------------------------------------------------------------ window polynomials (R6)
+static double es_exact(double t, double beta) {
+  if (std::fabs(t) >= 1.0) return 0.0;
+  return std::exp(beta * (std::sqrt(1.0 - t * t) - 1.0));
+}
+
+bool fit_window_poly(int w, double beta, float* coef, double* max_err) {
+  const int D = kPolyDeg, n = D + 1;
+  double worst = 0.0;
+  for (int j = 0; j < w; ++j) {
+    // interpolate at Chebyshev nodes of [0,1] (near-minimax), Vandermonde solve in fp64
+    double A[n][n + 1];
+    for (int i = 0; i < n; ++i) {
+      const double f = 0.5 - 0.5 * std::cos(kPi * (i + 0.5) / n);
+      double pw = 1.0;
+      for (int k = 0; k < n; ++k) { A[i][k] = pw; pw *= f; }
+      A[i][n] = es_exact((f + 0.5 * w - 1.0 - j) * 2.0 / w, beta);
+    }
+    for (int c = 0; c < n; ++c) {   // Gaussian elimination with partial pivoting
+      int piv = c;
+      for (int r = c + 1; r < n; ++r)
+        if (std::fabs(A[r][c]) > std::fabs(A[piv][c])) piv = r;
+      for (int k = 0; k <= n; ++k) std::swap(A[c][k], A[piv][k]);
+      for (int r = 0; r < n; ++r) {
+        if (r == c) continue;
+        const double m = A[r][c] / A[c][c];
+        for (int k = c; k <= n; ++k) A[r][k] -= m * A[c][k];
+      }
+    }
+    for (int k = 0; k < n; ++k) coef[j * n + k] = static_cast<float>(A[k][n] / A[k][k]);
+    for (int i = 0; i <= 400; ++i) {   // check the fp32 coefficients on a dense grid
+      const double f = std::min(i / 400.0, 1.0 - 1e-12);
+      double acc = 0.0;
+      for (int k = D; k >= 0; --k) acc = acc * f + coef[j * n + k];
+      worst = std::max(worst, std::fabs(acc - es_exact((f + 0.5 * w - 1.0 - j) * 2.0 / w, beta)));
+    }
+  }
+  *max_err = worst;
+  return worst < 1e-6;
+}
+
 // ------------------------------------------------------------------ band selection (R5)
 static void select_band(const KernelModel& k, double tau, double eps, int kcap, int* klo, int* khi) {
   // c_k for k >= 0; c_{-k} = c_k.  Keep the smallest band [klo,khi] (|k| in band) with dropped mass <= eps.
@@ -315,7 +356,7 @@ bool build_fourier_plan(const KernelModel& k, double eps, int w, int oversample,
   }
   out.phi2inv.assign(nh, 0.0f);
   for (int kk = 0; kk < nh; ++kk) out.phi2inv[kk] = static_cast<float>(1.0 / (Phi[kk] * Phi[kk]));
-  int W = 0;
+  int W = 0, WA = 0;
   for (int p = 0; p < ns; ++p) {
     SlicePlan& sp = out.slices[p];
     // footprint of the x points in grid cells: identical fp32 operations to the device (no contraction)
@@ -332,8 +373,26 @@ bool build_fourier_plan(const KernelModel& k, double eps, int w, int oversample,
     const int l1 = static_cast<int>(std::floor(a1)) + w + 1;
     sp.lmin = l0;
     W = std::max(W, l1 - l0 + 1);
+    volatile float ua0 = amin[p] - c;
+    volatile float ua1 = amax[p] - c;
+    volatile float va0 = ua0 * t;
+    volatile float va1 = ua1 * t;
+    volatile float ga0 = va0 * nf;
+    volatile float ga1 = va1 * nf;
+    volatile float aa0 = ga0 - hw;
+    volatile float aa1 = ga1 - hw;
+    const int la0 = static_cast<int>(std::floor(aa0)) + 1 - 1;
+    const int la1 = static_cast<int>(std::floor(aa1)) + 1 + 1;   // cells l0 (not l0+w): interpolation polynomials
+    sp.lminA = la0;
+    WA = std::max(WA, la1 - la0 + 1);
   }
   out.W = W;
+  out.WA = WA;
+  out.poly.assign(static_cast<size_t>(w) * (kPolyDeg + 1), 0.f);
+  if (!fit_window_poly(w, out.beta, out.poly.data(), &out.poly_err)) {
+    if (err) *err = "window polynomial fit failed (error " + std::to_string(out.poly_err) + ")";
+    return false;
+  }
   return true;
 }
 

@@ -35,15 +35,24 @@ double decay_radius(const KernelModel& k, double eps);
 struct SlicePlan {
   float tau, cen;   // u = tau (z - cen) in [-1/2, 1/2)
   int lmin;         // first grid cell of the x footprint (unwrapped)
+  int lminA;        // first grid cell of the footprint of all points (x and y)
   int klo, khi;     // kept band: klo <= |k| <= khi
 };
+
+// Piecewise-polynomial form of the window (R6): for a point with fractional offset f in [0,1), tap j of w
+// has weight p_j(f) = sum_k coef[j*(deg+1) + k] f^k ~= ES((f + w/2 - 1 - j) * 2/w).
+constexpr int kPolyDeg = 10;
+bool fit_window_poly(int w, double beta, float* coef /* w*(kPolyDeg+1) */, double* max_err);
 
 struct FourierPlan {
   int n = 0;            // grid length (power of two)
   int w = 0;            // window taps
   float beta = 0.f;     // ES window shape
   int k_max = 0, band_lo_min = 0;
-  int W = 0;            // widest per-slice footprint (cells)
+  int W = 0;            // widest per-slice footprint of the x points (cells)
+  int WA = 0;           // widest per-slice footprint of all points (cells)
+  std::vector<float> poly;   // w * (kPolyDeg + 1) window polynomial coefficients
+  double poly_err = 0.0;
   double tau_min = 0, tau_max = 0;
   std::vector<SlicePlan> slices;
   std::vector<float> phi2inv;   // [n/2 + 1]  1 / Phi(k/n)^2 (window deconvolution, folded into D_k on device)

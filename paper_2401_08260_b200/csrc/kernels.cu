@@ -49,6 +49,21 @@ __device__ __forceinline__ float es_window(float t, float beta) {
   return __expf(beta * (sqrtf(s) - 1.f));
 }
 
+// all w tap weights of a point with fractional offset f by Horner (FMA-only, no MUFU)  (R6)
+template <int WMAX>
+__device__ __forceinline__ void poly_taps(const PolyWin& pw, float f, float* out) {
+#pragma unroll
+  for (int j = 0; j < WMAX; ++j) {
+    if (j < pw.w) {
+      const float* c = pw.c + j * (PW_D + 1);
+      float acc = c[PW_D];
+#pragma unroll
+      for (int k = PW_D - 1; k >= 0; --k) acc = fmaf(acc, f, c[k]);
+      out[j] = acc;
+    }
+  }
+}
+
 // grid coordinate: identical fp32 op sequence on host (planner footprint) and device
 __device__ __forceinline__ float grid_coord(float z, float cen, float tau, float nf) {
   return __fmul_rn(__fmul_rn(__fsub_rn(z, cen), tau), nf);
@@ -244,7 +259,7 @@ cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* ph
 constexpr int SP_THREADS = 256, SP_WARPS = SP_THREADS / 32, SP_WMAX_PRIV = 64;
 
 __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const float* __restrict__ w,
-                                                               const FPar* __restrict__ fp, int n, int wt, float beta,
+                                                               const FPar* __restrict__ fp, int n, PolyWin pw,
                                                                int W, int64_t chunk, float* __restrict__ grid) {
   extern __shared__ float priv[];   // [SP_WARPS][W][32]
   const int p = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -252,19 +267,20 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
   float* mine = priv + static_cast<int64_t>(wid) * W * 32;
   for (int c = lane; c < W * 32; c += 32) mine[c] = 0.f;
   __syncwarp();
-  const float nf = static_cast<float>(n), hw = 0.5f * wt, inv_hw = 2.0f / wt;
+  const float nf = static_cast<float>(n), hw = 0.5f * pw.w;
   const int64_t i0 = blockIdx.x * chunk, i1 = min(zv.N, i0 + chunk);
   const float* zx = zv.zx + p * zv.ldx;
   for (int64_t i = i0 + tid; i < i1; i += SP_THREADS) {
-    const float v = grid_coord(zx[i], f.cen, f.tau, nf);
-    const int l0 = static_cast<int>(floorf(__fsub_rn(v, hw))) + 1;
-    const float wi = w[i];
-    const int loc = l0 - f.lmin;
-    float dist = v - static_cast<float>(l0);
-    for (int j = 0; j < wt; ++j) {
-      mine[(loc + j) * 32 + lane] += wi * es_window(dist * inv_hw, beta);
-      dist -= 1.f;
-    }
+    const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);
+    const float a = __fsub_rn(v, hw), fl = floorf(a);
+    const int l0 = static_cast<int>(fl) + 1;
+    const float wi = __ldg(w + i);
+    float tw[12];
+    poly_taps<12>(pw, a - fl, tw);
+    float* cell = mine + (l0 - f.lmin) * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < 12; ++j)
+      if (j < pw.w) cell[j * 32] += wi * tw[j];
   }
   __syncthreads();
   // reduce: cell c -> sum over warps (registers) then lanes (shuffles)
@@ -279,25 +295,26 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
 }
 
 __global__ void __launch_bounds__(SP_THREADS) k_spread_shared(ZView zv, const float* __restrict__ w,
-                                                              const FPar* __restrict__ fp, int n, int wt, float beta,
+                                                              const FPar* __restrict__ fp, int n, PolyWin pw,
                                                               int64_t chunk, float* __restrict__ grid) {
   extern __shared__ float sg[];   // [n]
   const int p = blockIdx.y, tid = threadIdx.x;
   const FPar f = fp[p];
   for (int c = tid; c < n; c += SP_THREADS) sg[c] = 0.f;
   __syncthreads();
-  const float nf = static_cast<float>(n), hw = 0.5f * wt, inv_hw = 2.0f / wt;
+  const float nf = static_cast<float>(n), hw = 0.5f * pw.w;
   const int64_t i0 = blockIdx.x * chunk, i1 = min(zv.N, i0 + chunk);
   const float* zx = zv.zx + p * zv.ldx;
   for (int64_t i = i0 + tid; i < i1; i += SP_THREADS) {
-    const float v = grid_coord(zx[i], f.cen, f.tau, nf);
-    const int l0 = static_cast<int>(floorf(__fsub_rn(v, hw))) + 1;
-    const float wi = w[i];
-    float dist = v - static_cast<float>(l0);
-    for (int j = 0; j < wt; ++j) {
-      atomicAdd(&sg[(l0 + j) & (n - 1)], wi * es_window(dist * inv_hw, beta));
-      dist -= 1.f;
-    }
+    const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);
+    const float a = __fsub_rn(v, hw), fl = floorf(a);
+    const int l0 = static_cast<int>(fl) + 1;
+    const float wi = __ldg(w + i);
+    float tw[12];
+    poly_taps<12>(pw, a - fl, tw);
+#pragma unroll
+    for (int j = 0; j < 12; ++j)
+      if (j < pw.w) atomicAdd(&sg[(l0 + j) & (n - 1)], wi * tw[j]);
   }
   __syncthreads();
   for (int c = tid; c < n; c += SP_THREADS) {
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_shared(ZView zv, const fl
   }
 }
 
-cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int n, int wt, float beta, int W,
+cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int n, const PolyWin& pw, int W,
                           float* grid, cudaStream_t st) {
   // chunking: enough CTAs to fill 148 SMs several times, >= 2048 points per CTA to amortise the flush
   int64_t chunk = 8192;
@@ -321,7 +338,7 @@ cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int 
                            SP_WARPS * SP_WMAX_PRIV * 32 * 4);
       attr = true;
     }
-    k_spread_private<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, wt, beta, W, chunk, grid);
+    k_spread_private<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, W, chunk, grid);
   } else {
     const size_t smem = static_cast<size_t>(n) * sizeof(float);
     static bool attr = false;
@@ -329,7 +346,7 @@ cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int 
       cudaFuncSetAttribute(k_spread_shared, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4);
       attr = true;
     }
-    k_spread_shared<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, wt, beta, chunk, grid);
+    k_spread_shared<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, chunk, grid);
   }
   return cudaGetLastError();
 }
@@ -355,7 +372,9 @@ __device__ __forceinline__ void fft_stages(float2* buf, const float2* tw, int n,
 }
 
 __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restrict__ grid, const float* __restrict__ D,
-                                                           int n, int logn, float* __restrict__ h) {
+                                                           int n, int logn, float* __restrict__ h,
+                                                           const FPar* __restrict__ fp, PolyWin pw, int WA,
+                                                           float* __restrict__ Q) {
   extern __shared__ float2 sm[];
   float2* buf = sm;          // [n]
   float2* tw = sm + n;       // [n/2] forward twiddles e^{-2 pi i j / n}
@@ -385,9 +404,20 @@ __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restri
   fft_stages(buf, tw, n, logn);                     // h_l = conj(FFT(conj X))_l; real part
   float* hp = h + static_cast<int64_t>(p) * n;
   for (int l = threadIdx.x; l < n; l += FF_THREADS) hp[l] = buf[l].x;
+  if (Q) {   // interpolation polynomials of the footprint cells: Q[c][k] = sum_j h[l + j] coef_j[k]
+    const int l00 = fp[p].lminA;
+    float* qp = Q + static_cast<int64_t>(p) * WA * (PW_D + 1);
+    for (int e = threadIdx.x; e < WA * (PW_D + 1); e += FF_THREADS) {
+      const int c = e / (PW_D + 1), k = e - c * (PW_D + 1);
+      float acc = 0.f;
+      for (int j = 0; j < pw.w; ++j) acc = fmaf(buf[(l00 + c + j) & (n - 1)].x, pw.c[j * (PW_D + 1) + k], acc);
+      qp[e] = acc;
+    }
+  }
 }
 
-cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, cudaStream_t st) {
+cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, const FPar* fp,
+                              const PolyWin& pw, int WA, float* Q, cudaStream_t st) {
   int logn = 0;
   while ((1 << logn) < n) ++logn;
   const size_t smem = static_cast<size_t>(n) * sizeof(float2) + static_cast<size_t>(n / 2) * sizeof(float2);
@@ -397,7 +427,7 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, 
                          16384 * 8 + 8192 * 8);
     attr = true;
   }
-  k_fft_filter<<<np, FF_THREADS, smem, st>>>(grid, D, n, logn, h);
+  k_fft_filter<<<np, FF_THREADS, smem, st>>>(grid, D, n, logn, h, fp, pw, WA, Q);
   return cudaGetLastError();
 }
 
@@ -405,14 +435,14 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, 
 // grid (target blocks, slice groups): each thread handles one target over EV_SG slices, then one fp64
 // atomic into s64 (or per-slice stores for sks_sum_1d).  Target blocks vary fastest, so the CTAs resident
 // at a time work on the same slice group and its bucket records / grids stay in L2.
-constexpr int EV_THREADS = 256, EV_SG = 8;
+constexpr int EV_THREADS = 256, EV_SG = 32;
 
 __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
   const int64_t M = a.zv.M;
   const int64_t m = blockIdx.x * static_cast<int64_t>(EV_THREADS) + threadIdx.x;
   if (m >= M) return;
   const int p0 = blockIdx.y * EV_SG, p1 = min(a.np, p0 + EV_SG);
-  const float nf = static_cast<float>(a.n), hw = 0.5f * a.wt, inv_hw = 2.0f / a.wt;
+  const float nf = static_cast<float>(a.n), hw = 0.5f * a.pw.w;
   double acc = 0.0;
   for (int p = p0; p < p1; ++p) {
     const float z = __ldg(a.zv.zy + p * a.zv.ldy + m);
@@ -425,13 +455,23 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
     if (a.fourier) {
       const FPar f = a.fp[p];
       const float v = grid_coord(z, f.cen, f.tau, nf);
-      const int l0 = static_cast<int>(floorf(__fsub_rn(v, hw))) + 1;
-      const float* hp = a.h + static_cast<int64_t>(p) * a.n;
-      float dist = v - static_cast<float>(l0);
+      const float av = __fsub_rn(v, hw), fl = floorf(av);
+      const int l0 = static_cast<int>(fl) + 1;
+      const float fr = av - fl;
       float tf = 0.f;
-      for (int j = 0; j < a.wt; ++j) {
-        tf += __ldg(hp + ((l0 + j) & (a.n - 1))) * es_window(dist * inv_hw, a.beta);
-        dist -= 1.f;
+      if (a.Q) {   // one Horner per target on the cell's interpolation polynomial
+        const float* q = a.Q + (static_cast<int64_t>(p) * a.WA + (l0 - f.lminA)) * (PW_D + 1);
+        float acc2 = __ldg(q + PW_D);
+#pragma unroll
+        for (int k = PW_D - 1; k >= 0; --k) acc2 = fmaf(acc2, fr, __ldg(q + k));
+        tf = acc2;
+      } else {
+        const float* hp = a.h + static_cast<int64_t>(p) * a.n;
+        float tw[12];
+        poly_taps<12>(a.pw, fr, tw);
+#pragma unroll
+        for (int j = 0; j < 12; ++j)
+          if (j < a.pw.w) tf = fmaf(__ldg(hp + ((l0 + j) & (a.n - 1))), tw[j], tf);
       }
       t += tf;
     }

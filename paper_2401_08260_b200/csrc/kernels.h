@@ -8,8 +8,17 @@ namespace sks {
 // per-slice Fourier parameters (device copy of SlicePlan)
 struct FPar {
   float tau, cen;
-  int lmin;
+  int lmin;     // first cell of the x footprint (spreading)
   int klo_khi;  // (klo << 16) | khi
+  int lminA;    // first cell of the all-points footprint (interpolation polynomials)
+  int pad;
+};
+
+// window polynomials: tap j weight p_j(f) = sum_k c[j*(PW_D+1)+k] f^k, f = frac(v - w/2)  (R6)
+constexpr int PW_D = 10;
+struct PolyWin {
+  int w;
+  float c[12 * (PW_D + 1)];
 };
 
 // per-call constants of the closed-form torus coefficients (device planner, row a2)
@@ -84,10 +93,13 @@ cudaError_t launch_sortpath(const SortArgs& a, int slots, cudaStream_t st);
 cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* phi2inv, int n, float* D,
                           cudaStream_t st);
 // row a5: g[p][l] = sum_n w_n phi_win(v_n - l) over the x projections (ES window, w taps)
-cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int n, int wt, float beta, int W,
+cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int n, const PolyWin& pw, int W,
                           float* grid, cudaStream_t st);
 // row a6: h[p] = IFFT_n(D[p] * FFT_n(g[p]))   (unnormalised, one CTA per slice, smem radix-2)
-cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, cudaStream_t st);
+// also writes the per-cell interpolation polynomials Q[p][c][k] = sum_j h[lminA + c + j] coef[j][k] for the
+// WA cells of the all-points footprint (Q == nullptr: skipped)
+cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, const FPar* fp,
+                              const PolyWin& pw, int WA, float* Q, cudaStream_t st);
 
 // row a7 (+ Laplacian moment term) + slice accumulation:
 //   per y_m: acc = sum_p [ Fourier interp + mom_coef * tau_p * S_moment ]
@@ -100,8 +112,10 @@ struct EvalArgs {
   bool fourier;
   const FPar* fp;
   const float* h;
-  int n, wt;
-  float beta;
+  const float* Q;       // [np][WA][PW_D+1] interpolation polynomials (nullptr: per-tap window on h)
+  int WA;
+  PolyWin pw;
+  int n;
   // Laplacian moment part: t += mom_coef * tau_p * sum_n w_n (z_n - z_m)^2
   bool moment;
   double mom_coef;
