@@ -281,7 +281,7 @@ sks::CoeffConst coeff_const(const sks_kernel& k, int d) {
 sks::PolyWin poly_win(const sks::FourierPlan& plan) {
   sks::PolyWin pw{};
   pw.w = plan.w;
-  for (size_t i = 0; i < plan.poly.size() && i < sizeof(pw.c) / sizeof(float); ++i) pw.c[i] = plan.poly[i];
+  for (size_t i = 0; i < sizeof(pw.c) / sizeof(float); ++i) pw.c[i] = i < plan.poly.size() ? plan.poly[i] : 0.f;
   return pw;
 }
 

@@ -44,17 +44,15 @@ __device__ __forceinline__ int bucket_of(float z, float zmin, float scale, int n
 }
 
 // all w tap weights of a point with fractional offset f by Horner (FMA-only, no MUFU)  (R6)
-template <int WMAX>
+template <int WT>
 __device__ __forceinline__ void poly_taps(const PolyWin& pw, float f, float* out) {
 #pragma unroll
-  for (int j = 0; j < WMAX; ++j) {
-    if (j < pw.w) {
-      const float* c = pw.c + j * (PW_D + 1);
-      float acc = c[PW_D];
+  for (int j = 0; j < WT; ++j) {
+    const float* c = pw.c + j * (PW_D + 1);
+    float acc = c[PW_D];
 #pragma unroll
-      for (int k = PW_D - 1; k >= 0; --k) acc = fmaf(acc, f, c[k]);
-      out[j] = acc;
-    }
+    for (int k = PW_D - 1; k >= 0; --k) acc = fmaf(acc, f, c[k]);
+    out[j] = acc;
   }
 }
 
@@ -252,6 +250,7 @@ cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* ph
 // of W cells; one CTA = (chunk of points, slice).  Fallback for wide footprints: CTA grid + smem atomics.
 constexpr int SP_THREADS = 256, SP_WARPS = SP_THREADS / 32, SP_WMAX_PRIV = 64;
 
+template <int WT>
 __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const float* __restrict__ w,
                                                                const FPar* __restrict__ fp, int n, PolyWin pw,
                                                                int W, int64_t chunk, float* __restrict__ grid) {
@@ -269,12 +268,11 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
     const float a = __fsub_rn(v, hw), fl = floorf(a);
     const int l0 = static_cast<int>(fl) + 1;
     const float wi = __ldg(w + i);
-    float tw[12];
-    poly_taps<12>(pw, a - fl, tw);
+    float tw[WT];
+    poly_taps<WT>(pw, a - fl, tw);
     float* cell = mine + (l0 - f.lmin) * 32 + lane;
 #pragma unroll
-    for (int j = 0; j < 12; ++j)
-      if (j < pw.w) cell[j * 32] += wi * tw[j];
+    for (int j = 0; j < WT; ++j) cell[j * 32] += wi * tw[j];
   }
   __syncthreads();
   // reduce: cell c -> sum over warps (registers) then lanes (shuffles)
@@ -288,6 +286,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
   }
 }
 
+template <int WT>
 __global__ void __launch_bounds__(SP_THREADS) k_spread_shared(ZView zv, const float* __restrict__ w,
                                                               const FPar* __restrict__ fp, int n, PolyWin pw,
                                                               int64_t chunk, float* __restrict__ grid) {
@@ -304,11 +303,10 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_shared(ZView zv, const fl
     const float a = __fsub_rn(v, hw), fl = floorf(a);
     const int l0 = static_cast<int>(fl) + 1;
     const float wi = __ldg(w + i);
-    float tw[12];
-    poly_taps<12>(pw, a - fl, tw);
+    float tw[WT];
+    poly_taps<WT>(pw, a - fl, tw);
 #pragma unroll
-    for (int j = 0; j < 12; ++j)
-      if (j < pw.w) atomicAdd(&sg[(l0 + j) & (n - 1)], wi * tw[j]);
+    for (int j = 0; j < WT; ++j) atomicAdd(&sg[(l0 + j) & (n - 1)], wi * tw[j]);
   }
   __syncthreads();
   for (int c = tid; c < n; c += SP_THREADS) {
@@ -326,21 +324,28 @@ cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int 
   if (nchunk == 0) return cudaSuccess;
   if (W <= SP_WMAX_PRIV) {
     const size_t smem = static_cast<size_t>(SP_WARPS) * W * 32 * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_spread_private, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SP_WARPS * SP_WMAX_PRIV * 32 * 4);
-      attr = true;
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP_WARPS * SP_WMAX_PRIV * 32 * 4);
+      kern<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, W, chunk, grid);
+    };
+    switch (pw.w) {
+      case 4: go(k_spread_private<4>); break;
+      case 6: go(k_spread_private<6>); break;
+      case 8: go(k_spread_private<8>); break;
+      default: go(k_spread_private<12>); break;   // taps beyond w have zero coefficients
     }
-    k_spread_private<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, W, chunk, grid);
   } else {
     const size_t smem = static_cast<size_t>(n) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_spread_shared, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4);
-      attr = true;
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4);
+      kern<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, chunk, grid);
+    };
+    switch (pw.w) {
+      case 4: go(k_spread_shared<4>); break;
+      case 6: go(k_spread_shared<6>); break;
+      case 8: go(k_spread_shared<8>); break;
+      default: go(k_spread_shared<12>); break;
     }
-    k_spread_shared<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, chunk, grid);
   }
   return cudaGetLastError();
 }
@@ -431,6 +436,43 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, 
 // at a time work on the same slice group and its bucket records / grids stay in L2.
 constexpr int EV_THREADS = 256, EV_SG = 32;
 
+__device__ __forceinline__ double eval_one(const EvalArgs& a, int p, float z, float nf, float hw, int64_t m,
+                                           int64_t M) {
+  const double zd = z;
+  double t = 0.0;
+  if (a.moment) {
+    const SliceTot T = a.tot[p];
+    t += a.mom_coef * static_cast<double>(a.fp[p].tau) * (T.C - 2.0 * zd * T.B + zd * zd * T.A);
+  }
+  if (a.fourier) {
+    const FPar f = a.fp[p];
+    const float v = grid_coord(z, f.cen, f.tau, nf);
+    const float av = __fsub_rn(v, hw), fl = floorf(av);
+    const int l0 = static_cast<int>(fl) + 1;
+    const float fr = av - fl;
+    float tf = 0.f;
+    if (a.Q) {   // one Horner per target on the cell's interpolation polynomial
+      const float* q = a.Q + (static_cast<int64_t>(p) * a.WA + (l0 - f.lminA)) * (PW_D + 1);
+      float acc2 = __ldg(q + PW_D);
+#pragma unroll
+      for (int k = PW_D - 1; k >= 0; --k) acc2 = fmaf(acc2, fr, __ldg(q + k));
+      tf = acc2;
+    } else {
+      const float* hp = a.h + static_cast<int64_t>(p) * a.n;
+      float tw[12];
+      poly_taps<12>(a.pw, fr, tw);   // taps beyond w have zero coefficients
+#pragma unroll
+      for (int j = 0; j < 12; ++j) tf = fmaf(__ldg(hp + ((l0 + j) & (a.n - 1))), tw[j], tf);
+    }
+    t += tf;
+  }
+  if (a.per_slice_out) {
+    float* o = a.per_slice_out + static_cast<int64_t>(p) * M + m;
+    *o = a.accumulate_out ? *o + static_cast<float>(t) : static_cast<float>(t);
+  }
+  return t;
+}
+
 __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
   const int64_t M = a.zv.M;
   const int64_t m = blockIdx.x * static_cast<int64_t>(EV_THREADS) + threadIdx.x;
@@ -438,43 +480,15 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
   const int p0 = blockIdx.y * EV_SG, p1 = min(a.np, p0 + EV_SG);
   const float nf = static_cast<float>(a.n), hw = 0.5f * a.pw.w;
   double acc = 0.0;
-  for (int p = p0; p < p1; ++p) {
-    const float z = __ldg(a.zv.zy + p * a.zv.ldy + m);
-    const double zd = z;
-    double t = 0.0;
-    if (a.moment) {
-      const SliceTot T = a.tot[p];
-      t += a.mom_coef * static_cast<double>(a.fp[p].tau) * (T.C - 2.0 * zd * T.B + zd * zd * T.A);
-    }
-    if (a.fourier) {
-      const FPar f = a.fp[p];
-      const float v = grid_coord(z, f.cen, f.tau, nf);
-      const float av = __fsub_rn(v, hw), fl = floorf(av);
-      const int l0 = static_cast<int>(fl) + 1;
-      const float fr = av - fl;
-      float tf = 0.f;
-      if (a.Q) {   // one Horner per target on the cell's interpolation polynomial
-        const float* q = a.Q + (static_cast<int64_t>(p) * a.WA + (l0 - f.lminA)) * (PW_D + 1);
-        float acc2 = __ldg(q + PW_D);
+  int p = p0;
+  for (; p + 4 <= p1; p += 4) {   // 4 independent slices in flight per target
+    float z[4];
 #pragma unroll
-        for (int k = PW_D - 1; k >= 0; --k) acc2 = fmaf(acc2, fr, __ldg(q + k));
-        tf = acc2;
-      } else {
-        const float* hp = a.h + static_cast<int64_t>(p) * a.n;
-        float tw[12];
-        poly_taps<12>(a.pw, fr, tw);
+    for (int k = 0; k < 4; ++k) z[k] = __ldg(a.zv.zy + (p + k) * a.zv.ldy + m);
 #pragma unroll
-        for (int j = 0; j < 12; ++j)
-          if (j < a.pw.w) tf = fmaf(__ldg(hp + ((l0 + j) & (a.n - 1))), tw[j], tf);
-      }
-      t += tf;
-    }
-    if (a.per_slice_out) {
-      float* o = a.per_slice_out + static_cast<int64_t>(p) * M + m;
-      *o = a.accumulate_out ? *o + static_cast<float>(t) : static_cast<float>(t);
-    }
-    acc += t;
+    for (int k = 0; k < 4; ++k) acc += eval_one(a, p + k, z[k], nf, hw, m, M);
   }
+  for (; p < p1; ++p) acc += eval_one(a, p, __ldg(a.zv.zy + p * a.zv.ldy + m), nf, hw, m, M);
   if (a.s64) atomicAdd(a.s64 + m, acc);
 }
 
