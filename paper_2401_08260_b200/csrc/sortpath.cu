@@ -356,12 +356,17 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
     const int per = (nown + SP_T - 1) / SP_T;
     const int j0 = min(nown, tid * per), j1 = min(nown, j0 + per);
     double lA = 0.0, lB = 0.0, lC = 0.0;
-    for (int i = S.ox[j0]; i < S.ox[j1]; ++i) {
-      const float2 q = __ldcg(xsp + i);
-      const double wz = static_cast<double>(q.y) * q.x;
-      lA += q.y;
-      lB += wz;
-      lC += wz * q.x;
+    for (int i0 = S.ox[j0], i1 = S.ox[j1]; i0 < i1; i0 += 8) {   // 8 loads in flight
+      float2 qq[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) qq[u] = (i0 + u < i1) ? __ldcg(xsp + i0 + u) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double wz = static_cast<double>(qq[u].y) * qq[u].x;
+        lA += qq[u].y;
+        lB += wz;
+        lC += wz * qq[u].x;
+      }
     }
     {
       const double iA = warp_incl_scan(lA), iB = warp_incl_scan(lB);
@@ -389,10 +394,15 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
       double rA = PA + S.wsd[0][wid] + iA - lA, rB = PB + S.wsd[1][wid] + iB - lB;
       for (int j = j0; j < j1; ++j) {
         double W = 0.0, Z = 0.0;
-        for (int i = S.ox[j]; i < S.ox[j + 1]; ++i) {
-          const float2 q = __ldcg(xsp + i);
-          W += q.y;
-          Z += static_cast<double>(q.y) * q.x;
+        for (int i0 = S.ox[j], i1 = S.ox[j + 1]; i0 < i1; i0 += 8) {
+          float2 qq[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) qq[u] = (i0 + u < i1) ? __ldcg(xsp + i0 + u) : make_float2(0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            W += qq[u].y;
+            Z += static_cast<double>(qq[u].y) * qq[u].x;
+          }
         }
         BucketRec r;
         r.A = rA;
@@ -430,15 +440,15 @@ __global__ void __cluster_dims__(SP_C, 1, 1) __launch_bounds__(SP_T, 1) k_sortsu
           const double Ahi = TA - R.A - R.w, Bhi = TB - R.B - R.wz;
           const float2* xp = xsp + R.off;
           float s0 = 0.f, s1 = 0.f;
-          int j = 0;
-          for (; j + 2 <= R.cnt; j += 2) {
-            const float2 q0 = __ldcg(xp + j), q1 = __ldcg(xp + j + 1);
-            s0 = fmaf(q0.y, fabsf(q0.x - z), s0);
-            s1 = fmaf(q1.y, fabsf(q1.x - z), s1);
-          }
-          if (j < R.cnt) {
-            const float2 q = __ldcg(xp + j);
-            s0 = fmaf(q.y, fabsf(q.x - z), s0);
+          for (int j0c = 0; j0c < R.cnt; j0c += 16) {   // up to 16 bucket entries in flight
+            float2 qq[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) qq[u] = (j0c + u < R.cnt) ? __ldcg(xp + j0c + u) : make_float2(z, 0.f);
+#pragma unroll
+            for (int u = 0; u < 16; u += 2) {
+              s0 = fmaf(qq[u].y, fabsf(qq[u].x - z), s0);
+              s1 = fmaf(qq[u + 1].y, fabsf(qq[u + 1].x - z), s1);
+            }
           }
           const double same = static_cast<double>(s0 + s1);
           const double t = -a.coef * ((zd * R.A - R.B) + (Bhi - zd * Ahi) + same);
