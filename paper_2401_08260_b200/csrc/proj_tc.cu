@@ -284,25 +284,57 @@ __global__ void k_range_reduce(const unsigned* __restrict__ part, int nparts, in
   mm[e] = v;
 }
 
-// fp32 -> three bf16 pieces, K-concatenated:  Xs[i][j] = hi, Xs[i][dp+j] = mid, Xs[i][2dp+j] = lo
+// fp32 -> three bf16 pieces, K-concatenated:  Xs[i][j] = hi, Xs[i][dp+j] = mid, Xs[i][2dp+j] = lo.
+// One thread per 8 consecutive coordinates of a row: vector loads when the row is 16-byte aligned,
+// three 16-byte stores (dp is a multiple of 64, so every 8-group is aligned in Xs).
+__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& mid, uint4& lo) {
+  uint32_t h[4], m[4], l[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    __nv_bfloat16 hh[2], mm[2], ll[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float x = v[2 * q + r];
+      hh[r] = __float2bfloat16_rn(x);
+      const float r1 = x - __bfloat162float(hh[r]);
+      mm[r] = __float2bfloat16_rn(r1);
+      ll[r] = __float2bfloat16_rn(r1 - __bfloat162float(mm[r]));
+    }
+    h[q] = static_cast<uint32_t>(__bfloat16_as_ushort(hh[0])) | (static_cast<uint32_t>(__bfloat16_as_ushort(hh[1])) << 16);
+    m[q] = static_cast<uint32_t>(__bfloat16_as_ushort(mm[0])) | (static_cast<uint32_t>(__bfloat16_as_ushort(mm[1])) << 16);
+    l[q] = static_cast<uint32_t>(__bfloat16_as_ushort(ll[0])) | (static_cast<uint32_t>(__bfloat16_as_ushort(ll[1])) << 16);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  mid = make_uint4(m[0], m[1], m[2], m[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 __global__ void k_split3(const float* __restrict__ x, int64_t N, const float* __restrict__ y, int64_t M, int d, int dp,
                          __nv_bfloat16* __restrict__ xs) {
   const int64_t L = N + M;
-  const int64_t total = L * dp;
+  const int g8 = dp / 8;   // 8-groups per row
+  const int64_t total = L * g8;
+  const bool vec = (d % 4) == 0;   // rows 16-byte aligned (base pointers from cudaMalloc/torch are 256-aligned)
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = e / dp;
-    const int j = static_cast<int>(e - i * dp);
-    float v = 0.f;
-    if (j < d) v = (i < N) ? __ldg(x + i * d + j) : __ldg(y + (i - N) * d + j);
-    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-    const float r1 = v - __bfloat162float(hi);
-    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-    __nv_bfloat16* row = xs + i * (3 * static_cast<int64_t>(dp));
-    row[j] = hi;
-    row[dp + j] = mid;
-    row[2 * dp + j] = lo;
+    const int64_t i = e / g8;
+    const int j0 = static_cast<int>(e - i * g8) * 8;
+    const float* row = (i < N) ? x + i * d : y + (i - N) * d;
+    float v[8];
+    if (vec && j0 + 8 <= d) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(row + j0));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(row + j0 + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = (j0 + u < d) ? __ldg(row + j0 + u) : 0.f;
+    }
+    uint4 hi, mid, lo;
+    split8(v, hi, mid, lo);
+    uint4* out = reinterpret_cast<uint4*>(xs + i * (3 * static_cast<int64_t>(dp)) + j0);
+    out[0] = hi;
+    out[dp / 8] = mid;
+    out[2 * (dp / 8)] = lo;
   }
 }
 
@@ -355,9 +387,9 @@ int proj_tc_dpad(int d) { return (d + TC_BK - 1) / TC_BK * TC_BK; }
 
 cudaError_t launch_split3(const float* x, int64_t N, const float* y, int64_t M, int d, void* xs, cudaStream_t st) {
   const int dp = proj_tc_dpad(d);
-  const int64_t total = (N + M) * dp;
+  const int64_t total = (N + M) * (dp / 8);
   int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > 148 * 32) blocks = 148 * 32;
   k_split3<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, N, y, M, d, dp, static_cast<__nv_bfloat16*>(xs));
   return cudaGetLastError();
 }
