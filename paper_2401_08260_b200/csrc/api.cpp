@@ -126,9 +126,19 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, ovf = 0, Q = 0, grid = 0, h = 0, D = 0, fpar = 0, phi = 0, s64 = 0,
-         flag = 0, total = 0;
+  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, ovf = 0, sp = 0, Q = 0, grid = 0,
+         h = 0, D = 0, fpar = 0, phi = 0, s64 = 0, flag = 0, total = 0;
 };
+
+// sort path: owner-partitioned (sortpart.cu) by default; SKS_SORT_V1=1 selects the earlier cluster kernel
+bool use_sort_v1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SKS_SORT_V1");
+    v = (e && std::strcmp(e, "0") != 0) ? 1 : 0;
+  }
+  return v == 1;
+}
 
 bool use_tc_projection() {
   static int v = -1;
@@ -158,13 +168,17 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb,
     }
   }
   if (pt.sort || pt.moment) {
-    const int slots = sks::sortpath_slots(nbat);
-    L.xs = take(sizeof(float2) * N * slots);
-    L.ys = take(sizeof(float2) * M * slots);
-    L.rec = take(sizeof(sks::BucketRec) * nb * static_cast<size_t>(slots));
     L.tot = take(sizeof(sks::SliceTot) * static_cast<size_t>(nbat));
-    L.ovf = take(sizeof(int) * static_cast<size_t>(nbat));
-    L.bpar = take(sizeof(float) * 2 * nbat);
+    if (use_sort_v1()) {
+      const int slots = sks::sortpath_slots(nbat);
+      L.xs = take(sizeof(float2) * N * slots);
+      L.ys = take(sizeof(float2) * M * slots);
+      L.rec = take(sizeof(sks::BucketRec) * nb * static_cast<size_t>(slots));
+      L.ovf = take(sizeof(int) * static_cast<size_t>(nbat));
+      L.bpar = take(sizeof(float) * 2 * nbat);
+    } else {
+      L.sp = take(sks::sortpart_bytes(N, M, nbat));
+    }
   }
   if (pt.fourier) {
     L.grid = take(sizeof(float) * kNmax * static_cast<size_t>(nbat));
@@ -426,7 +440,24 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     ea.np = nbat;
     double* s64 = s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr;
     float* tps = t_out ? t_out + static_cast<int64_t>(b0) * pr.M : nullptr;
-    if (pt.sort) {
+    if (pt.sort && !use_sort_v1()) {
+      // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)
+      sks::SortPartArgs sa{};
+      sa.zv = zv;
+      sa.w = w;
+      sa.np = nbat;
+      sa.mm = mm;
+      sa.tot = reinterpret_cast<sks::SliceTot*>(ws + L.tot);
+      sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
+      sa.s64 = s64;
+      sa.per_slice_out = tps;
+      {
+        ProfScope ps(PS_BUCKET, st);
+        SKS_CUDA(sks::launch_sortpart(sa, ws + L.sp, st));
+      }
+      launches += 4 * sks::sortpart_groups(pr.N, pr.M, nbat);
+      ea.tot = sa.tot;
+    } else if (pt.sort) {
       // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)
       sks::SortArgs sa{};
       sa.zv = zv;

@@ -89,6 +89,38 @@ int sortpath_buckets();
 int sortpath_slots(int np);   // scratch slots (co-resident clusters) used for np slices
 cudaError_t launch_sortpath(const SortArgs& a, int slots, cudaStream_t st);
 
+// rows a3 + a4, owner-partitioned (sortpart.cu, default): histogram -> G owners per slice (contiguous value
+// ranges balanced by x count) -> coalesced partition into per-owner mailboxes -> per-owner fine-bucket
+// counting sort, fp64 prefix sums and target evaluation in shared memory -> gather back to target order.
+struct SpOwner {         // one owner (contiguous bin range [blo, blo + NBF/fmul)) of one slice
+  int xoff, xcnt;        // its x in the slice's x mailbox
+  int yoff, ycnt;        // its y in the slice's y mailbox
+  float blo, fmul;       // fine bucket = floor((u - blo) * fmul), u = bin coordinate
+  int pad0, pad1;
+};
+struct SpDims {
+  int NH = 0;            // histogram bins per slice
+  int G = 0;             // owners per slice
+};
+struct SortPartArgs {
+  ZView zv;
+  const float* w;
+  int np;
+  const unsigned* mm;    // [np][4] ranges
+  SliceTot* tot;         // [np] sum w, sum w z, sum w z^2 (fp64)
+  double coef;           // t = -coef * sum_n w_n |x_n - z|
+  double* s64;           // accumulate sum_p t into s64[m] (fp64 atomics, coalesced), or
+  float* per_slice_out;  // store t into per_slice_out[p*M + m]
+};
+SpDims sortpart_dims(int64_t N, int64_t M);
+size_t sortpart_bytes(int64_t N, int64_t M, int np);   // scratch of launch_sortpart
+int sortpart_group(int64_t N, int64_t M, int np);      // slices per L2-resident group
+inline int sortpart_groups(int64_t N, int64_t M, int np) {
+  const int g = sortpart_group(N, M, np);
+  return (np + g - 1) / g;
+}
+cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st);
+
 // row a2: D[p][k] = c_k(tau_p) / Phi_k^2 on the band of slice p, else 0  (k = 0..n/2)
 cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* phi2inv, int n, float* D,
                           cudaStream_t st);

@@ -1,0 +1,675 @@
+// sortpart.cu -- the sort path (rows a3 + a4) as an owner-partitioned counting sort.
+//
+// Sec. 3.2 / Alg. 2 computes, exactly,
+//     t_m = -c sum_n w_n |x_n - y_m|                               (c = c_d, or alpha c_d, Laplacian)
+// by sorting the projections and taking prefix sums of w and w x.  Any monotone non-decreasing key map
+// k(z) gives the same identity: for a target z,
+//     sum_n w_n |x_n - z| = [z A_lo - B_lo] + [B_hi - z A_hi] + sum_{x: k(x) = k(z)} w |x - z|
+// where (A, B)_{lo/hi} = (sum w, sum w x) over the x with k(x) < k(z) (which are <= z) / k(x) > k(z)
+// (which are >= z); ties contribute |x - z| = 0 on either side.
+//
+// B200 design (measured, scratch/ubench_scatter.cu): a scattered 4-8 byte global or DSMEM access costs
+// 1-3 SM cycles per element, a random local shared-memory access 0.2.  So every random access of the
+// method is kept in the local shared memory of one CTA, and data moves between CTAs only in coalesced runs:
+//   S0 k_sp_hist   per slice: histogram of the x and y projections over NH equal bins of [xmin, xmax]
+//                  (+ slice totals sum w, sum w x, sum w x^2 in fp64 for the Laplacian moment term)
+//   S1 k_sp_plan   per slice: bins -> G owners balanced by x count (owner = contiguous bin range, so the
+//                  key k = (owner, fine bucket) stays monotone); region offsets of every owner
+//   S2 k_sp_part   per chunk: local counting sort of the chunk by owner in shared memory, runs appended to
+//                  the owners' mailbox regions (x: (z, w); y: z) with coalesced stores; y positions recorded;
+//                  per-owner fp64 sums of w and w x
+//   S3 k_sp_owner  per (owner, slice): the owner's x into NBF fine buckets in shared memory (counting sort),
+//                  fp64 exclusive bucket prefix sums, then every y of the owner evaluated from shared memory
+//                  only; t (fp32) written at the y's mailbox position (coalesced)
+//   S4 k_sp_gather per (target chunk, slice group): t gathered back to target order through the recorded
+//                  positions, accumulated over slices in fp64 registers, one coalesced atomic per target
+// An owner whose x exceed the shared-memory capacity (degenerate data: one bin holding > SP_CAP points) is
+// processed in several passes over subsets of its x (the identity is additive over the sources).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+
+#include "kernels.h"
+
+namespace sks {
+
+namespace {
+
+constexpr int S0_T = 512, S0_CH = 16384;      // histogram: elements per CTA
+constexpr int S2_T = 512, S2_PER = 8, S2_CH = S2_T * S2_PER;   // partition: elements per CTA
+constexpr int S3_T = 512, SP_CAP = 8192, SP_NBF = 2048;        // owner: x capacity, fine buckets
+constexpr int S3_PER = SP_CAP / S3_T;
+constexpr int S4_T = 256, S4_PER = 4, S4_CH = S4_T * S4_PER, S4_SG = 8;    // gather
+
+__device__ __forceinline__ float key2f_sp(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// L2-cached loads (no L1 allocation); plain loads so that the compiler can keep many in flight
+__device__ __forceinline__ float ldg_cg(const float* p) {
+  float v;
+  asm("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float2 ldg_cg2(const float2* p) {
+  float2 v;
+  asm("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+
+// bin coordinate u = (z - xmin) * hscale with explicitly rounded fp32 ops: monotone non-decreasing in z
+__device__ __forceinline__ float ucoord(float z, float xmin, float hscale) {
+  return __fmul_rn(__fsub_rn(z, xmin), hscale);
+}
+// floor(v) clamped to [0, n): monotone; NaN -> 0
+__device__ __forceinline__ int clamp_floor(float v, int n) {
+  const int b = (v >= 0.f) ? static_cast<int>(fminf(v, 2.0e9f)) : 0;
+  return b < n ? b : n - 1;
+}
+// fine bucket inside an owner: monotone in u (hence in z)
+__device__ __forceinline__ int fine_of(float u, float blo, float fmul) {
+  return clamp_floor(__fmul_rn(__fsub_rn(u, blo), fmul), SP_NBF);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan_sp(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_sum_sp(T v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// exclusive scan of one value per thread over the CTA (NT threads); returns the exclusive prefix, *total
+// gets the CTA total.  wbuf: >= NT/32 + 1 elements of shared memory.
+template <int NT, typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* wbuf, T* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  const T inc = warp_incl_scan_sp(v);
+  if (lane == 31) wbuf[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const T x = (lane < NW) ? wbuf[lane] : T(0);
+    const T xi = warp_incl_scan_sp(x);
+    if (lane < NW) wbuf[lane] = xi - x;
+    if (lane == NW - 1) wbuf[NW] = xi;
+  }
+  __syncthreads();
+  const T r = wbuf[wid] + inc - v;
+  *total = wbuf[NW];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------------------------- S0 + S1
+// Histogram of one chunk (x or y part of a slice); the last CTA of a slice to finish builds the slice's plan
+// (ticket counter per slice): owner of bin b = floor(cx[b] G / Nx) with cx the exclusive prefix x count, so
+// the owners are contiguous bin ranges (monotone) holding <= Nx/G + (largest bin) x each.
+__global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __restrict__ mm, int NH, int G,
+                                                  int ncx, int nchunks, int* __restrict__ H, int* __restrict__ done,
+                                                  uint16_t* __restrict__ om, SpOwner* __restrict__ own) {
+  extern __shared__ int hs[];   // [NH] histogram; in the plan: cx[NH + 1], cy[NH + 1], blo[G + 1]
+  __shared__ int wbuf[S0_T / 32 + 1];
+  __shared__ int last;
+  const int p = blockIdx.y, tid = threadIdx.x;
+  const bool isx = static_cast<int>(blockIdx.x) < ncx;
+  const int c = isx ? blockIdx.x : blockIdx.x - ncx;
+  const int n = static_cast<int>(isx ? zv.N : zv.M);
+  const float* z = isx ? zv.zx + p * zv.ldx : zv.zy + p * zv.ldy;
+  const int i0 = c * S0_CH, i1 = min(n, i0 + S0_CH);
+  const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
+  const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
+  for (int b = tid; b < NH; b += S0_T) hs[b] = 0;
+  __syncthreads();
+  constexpr int U = 8;
+  for (int base = i0; base < i1; base += U * S0_T) {
+    float zz[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int i = base + tid + k * S0_T;
+      zz[k] = (i < i1) ? __ldg(z + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (base + tid + k * S0_T < i1) atomicAdd(&hs[clamp_floor(ucoord(zz[k], xmin, hscale), NH)], 1);
+  }
+  __syncthreads();
+  int* Hp = H + (static_cast<int64_t>(p) * 2 + (isx ? 0 : 1)) * NH;
+  for (int b = tid; b < NH; b += S0_T)
+    if (hs[b]) atomicAdd(Hp + b, hs[b]);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(done + p, 1) == nchunks - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // ---- plan of slice p (this CTA saw every chunk's histogram)
+  int* cx = hs;
+  int* cy = cx + NH + 1;
+  int* blo = cy + NH + 1;
+  const int* hx = H + static_cast<int64_t>(p) * 2 * NH;
+  const int* hy = hx + NH;
+  const int per = (NH + S0_T - 1) / S0_T;
+  const int b0 = min(NH, tid * per), b1 = min(NH, b0 + per);
+  int lx = 0, ly = 0;
+  for (int b = b0; b < b1; ++b) { lx += __ldcg(hx + b); ly += __ldcg(hy + b); }
+  int tx, ty;
+  int rx = block_excl_scan<S0_T>(lx, wbuf, &tx);
+  int ry = block_excl_scan<S0_T>(ly, wbuf, &ty);
+  for (int b = b0; b < b1; ++b) {
+    cx[b] = rx; cy[b] = ry;
+    rx += __ldcg(hx + b); ry += __ldcg(hy + b);
+  }
+  if (tid == 0) { cx[NH] = tx; cy[NH] = ty; }
+  for (int o = tid; o <= G; o += S0_T) blo[o] = (o == 0) ? 0 : NH;
+  __syncthreads();
+  const int64_t Nx = (tx > 0) ? tx : 1;
+  for (int b = tid; b < NH; b += S0_T) {
+    const int oo = min(G - 1, static_cast<int>((static_cast<int64_t>(cx[b]) * G) / Nx));
+    om[static_cast<int64_t>(p) * NH + b] = static_cast<uint16_t>(oo);
+    const int prev = (b == 0) ? -1 : min(G - 1, static_cast<int>((static_cast<int64_t>(cx[b - 1]) * G) / Nx));
+    for (int q = prev + 1; q <= oo; ++q) blo[q] = b;   // owners prev+1 .. oo start at bin b (skipped ones empty)
+  }
+  __syncthreads();
+  for (int o = tid; o < G; o += S0_T) {
+    const int lo = blo[o];
+    const int hi = (o + 1 < G) ? blo[o + 1] : NH;
+    SpOwner r;
+    r.xoff = cx[lo];
+    r.xcnt = cx[hi] - cx[lo];
+    r.yoff = cy[lo];
+    r.ycnt = cy[hi] - cy[lo];
+    r.blo = static_cast<float>(lo);
+    r.fmul = (hi > lo) ? static_cast<float>(SP_NBF) / static_cast<float>(hi - lo) : 0.f;
+    r.pad0 = r.pad1 = 0;
+    own[static_cast<int64_t>(p) * G + o] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------- S2
+// Local counting sort of chunks of one slice part by owner (CPB chunks of S2_CH per CTA).  Shared memory:
+// stage[S2_CH] float2, sown[S2_CH] u16 (owner of each staged slot), om[NH] u16, ooff/cnt/start/gpos [G] ints.
+__global__ void __launch_bounds__(S2_T) k_sp_part(ZView zv, const float* __restrict__ w, const unsigned* __restrict__ mm,
+                                                  int NH, int G, int ncx, int cpb, const uint16_t* __restrict__ om_g,
+                                                  const SpOwner* __restrict__ own, int* __restrict__ cursor,
+                                                  double* __restrict__ osum, float2* __restrict__ Xmb,
+                                                  float* __restrict__ Ymb, int* __restrict__ ypos) {
+  extern __shared__ __align__(16) unsigned char sh2[];
+  float2* stage = reinterpret_cast<float2*>(sh2);                       // [S2_CH]
+  int* ooff = reinterpret_cast<int*>(stage + S2_CH);                   // [G] region start of each owner
+  int* cnt = ooff + G;                                                  // [G]
+  int* start = cnt + G;                                                 // [G]
+  int* gpos = start + G;                                                // [G]
+  uint16_t* sown = reinterpret_cast<uint16_t*>(gpos + G);              // [S2_CH]
+  uint16_t* om = sown + S2_CH;                                          // [NH] (16-byte aligned: G, S2_CH even)
+  __shared__ int wbuf[S2_T / 32 + 1];
+  const int p = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool isx = static_cast<int>(blockIdx.x) < ncx;
+  const int cb = isx ? blockIdx.x : blockIdx.x - ncx;   // chunk block
+  const int n = static_cast<int>(isx ? zv.N : zv.M);
+  const float* z = isx ? zv.zx + p * zv.ldx : zv.zy + p * zv.ldy;
+  const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
+  const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(om_g + static_cast<int64_t>(p) * NH);   // NH % 8 == 0
+    uint4* dst = reinterpret_cast<uint4*>(om);
+    for (int b = tid; b < NH / 8; b += S2_T) dst[b] = __ldg(src + b);
+    const SpOwner* ownp = own + static_cast<int64_t>(p) * G;
+    for (int o = tid; o < G; o += S2_T) ooff[o] = isx ? ownp[o].xoff : ownp[o].yoff;
+  }
+  int* curp = cursor + static_cast<int64_t>(p) * 2 * G + (isx ? 0 : G);
+  double* osp = osum + static_cast<int64_t>(p) * G * 4;
+  for (int ch = 0; ch < cpb; ++ch) {
+    const int i0 = (cb * cpb + ch) * S2_CH;
+    if (i0 >= n) break;
+    for (int o = tid; o < G; o += S2_T) cnt[o] = 0;
+    float zz[S2_PER], ww[S2_PER];
+#pragma unroll
+    for (int k = 0; k < S2_PER; ++k) {
+      const int i = i0 + tid + k * S2_T;
+      zz[k] = (i < n) ? __ldg(z + i) : 0.f;
+      ww[k] = (isx && i < n) ? __ldg(w + i) : 0.f;
+    }
+    __syncthreads();
+    int ow[S2_PER], rk[S2_PER];
+#pragma unroll
+    for (int k = 0; k < S2_PER; ++k) {
+      ow[k] = -1;
+      if (i0 + tid + k * S2_T < n) {
+        ow[k] = om[clamp_floor(ucoord(zz[k], xmin, hscale), NH)];
+        rk[k] = atomicAdd(&cnt[ow[k]], 1);
+      }
+    }
+    __syncthreads();
+    {   // exclusive scan of cnt over the owners; reserve this chunk's run in every owner's region
+      const int per = (G + S2_T - 1) / S2_T;
+      const int o0 = min(G, tid * per), o1 = min(G, o0 + per);
+      int loc = 0;
+      for (int o = o0; o < o1; ++o) loc += cnt[o];
+      int total;
+      int r = block_excl_scan<S2_T>(loc, wbuf, &total);
+      for (int o = o0; o < o1; ++o) {
+        start[o] = r;
+        r += cnt[o];
+        gpos[o] = ooff[o] + (cnt[o] ? atomicAdd(curp + o, cnt[o]) : 0);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < S2_PER; ++k) {
+      if (ow[k] < 0) continue;
+      const int s = start[ow[k]] + rk[k];
+      stage[s] = make_float2(zz[k], ww[k]);
+      sown[s] = static_cast<uint16_t>(ow[k]);
+      // the y's mailbox position, stored in target order (coalesced)
+      if (!isx) ypos[static_cast<int64_t>(p) * zv.M + i0 + tid + k * S2_T] = gpos[ow[k]] + rk[k];
+    }
+    __syncthreads();
+    const int nloc = min(S2_CH, n - i0);
+    for (int s = tid; s < nloc; s += S2_T) {   // staged slots are sorted by owner: runs, coalesced stores
+      const int o = sown[s];
+      const int dst = gpos[o] + (s - start[o]);
+      const float2 e = stage[s];
+      if (isx) Xmb[static_cast<int64_t>(p) * zv.N + dst] = e;
+      else Ymb[static_cast<int64_t>(p) * zv.M + dst] = e.x;
+    }
+    if (isx) {
+      // per-owner fp64 sums (w, w z, w z^2): warp q reduces the runs of owners q, q + 16, ... (coalesced)
+      for (int o = wid; o < G; o += S2_T / 32) {
+        const int c = cnt[o];
+        if (c == 0) continue;
+        double a = 0.0, b = 0.0, cc = 0.0;
+        for (int j = lane; j < c; j += 32) {
+          const float2 e = stage[start[o] + j];
+          const double wz = static_cast<double>(e.y) * e.x;
+          a += e.y;
+          b += wz;
+          cc += wz * e.x;
+        }
+        a = warp_sum_sp(a);
+        b = warp_sum_sp(b);
+        cc = warp_sum_sp(cc);
+        if (lane == 0) {
+          atomicAdd(osp + 4 * o, a);
+          atomicAdd(osp + 4 * o + 1, b);
+          atomicAdd(osp + 4 * o + 2, cc);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------- S3
+struct __align__(16) OwnerShared {
+  float2 xs[SP_CAP];          // the pass's x (z, w) in fine-bucket order
+  double2 rec[SP_NBF + 1];    // exclusive prefix (sum w, sum w x) over the pass's buckets; [NBF] = pass totals
+  int start[SP_NBF + 1];      // bucket b holds xs[start[b], start[b+1])
+  int wbuf[S3_T / 32 + 1];
+  double2 dbuf[S3_T / 32 + 1];
+  double outer[4];            // Alo, Blo, Ahi, Bhi (other owners)
+};
+
+__device__ __forceinline__ double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 operator-(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 shfl_up_d2(double2 v, int d) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+
+// exclusive block scan of a double2 per thread (S3_T threads)
+__device__ __forceinline__ double2 block_excl_scan_d2(double2 v, double2* wbuf, double2* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NW = S3_T / 32;
+  double2 inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double2 nb = shfl_up_d2(inc, o);
+    if (lane >= o) inc = inc + nb;
+  }
+  if (lane == 31) wbuf[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const double2 x = (lane < NW) ? wbuf[lane] : make_double2(0.0, 0.0);
+    double2 xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double2 nb = shfl_up_d2(xi, o);
+      if (lane >= o) xi = xi + nb;
+    }
+    if (lane < NW) wbuf[lane] = xi - x;
+    if (lane == NW - 1) wbuf[NW] = xi;
+  }
+  __syncthreads();
+  const double2 r = wbuf[wid] + inc - v;
+  *total = wbuf[NW];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(S3_T, 2) k_sp_owner(const SpOwner* __restrict__ own, const double* __restrict__ osum,
+                                                      const unsigned* __restrict__ mm, int NH, int G, int64_t N,
+                                                      int64_t M, const float2* __restrict__ Xmb,
+                                                      const float* __restrict__ Ymb, double coef, float* __restrict__ R,
+                                                      SliceTot* __restrict__ tot) {
+  extern __shared__ __align__(16) unsigned char sh3[];
+  OwnerShared& S = *reinterpret_cast<OwnerShared*>(sh3);
+  const int o = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
+  const SpOwner r = own[static_cast<int64_t>(p) * G + o];
+  if (r.ycnt == 0 && o != 0) return;
+  const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
+  const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
+  // sums over the other owners: lo = owners < o, hi = owners > o (fp64, from the partition kernel)
+  {
+    const double* os = osum + static_cast<int64_t>(p) * G * 4;
+    double la = 0.0, lb = 0.0, ha = 0.0, hb = 0.0, tc = 0.0;
+    for (int q = tid; q < G; q += S3_T) {
+      const double a = os[4 * q], b = os[4 * q + 1];
+      if (q < o) { la += a; lb += b; }
+      if (q > o) { ha += a; hb += b; }
+      tc += os[4 * q + 2];
+    }
+    la = warp_sum_sp(la); lb = warp_sum_sp(lb); ha = warp_sum_sp(ha); hb = warp_sum_sp(hb); tc = warp_sum_sp(tc);
+    const int lane = tid & 31, wid = tid >> 5;
+    __shared__ double part[5][S3_T / 32];
+    if (lane == 0) { part[0][wid] = la; part[1][wid] = lb; part[2][wid] = ha; part[3][wid] = hb; part[4][wid] = tc; }
+    __syncthreads();
+    if (tid < 5) {
+      double s = 0.0;
+      for (int q = 0; q < S3_T / 32; ++q) s += part[tid][q];
+      if (tid < 4) S.outer[tid] = s;
+      else if (o == 0) {   // slice totals (Laplacian moment term): sum over all owners
+        double a = 0.0, b = 0.0;
+        for (int q = 0; q < S3_T / 32; ++q) { a += part[2][q]; b += part[3][q]; }
+        const double a0 = os[0], b0 = os[1];
+        tot[p] = SliceTot{a + a0, b + b0, s, 0.0};
+      }
+    }
+  }
+  if (r.ycnt == 0) return;   // owner 0 with no targets: only the slice totals
+  const float2* xsrc = Xmb + static_cast<int64_t>(p) * N + r.xoff;
+  const float* ysrc = Ymb + static_cast<int64_t>(p) * M + r.yoff;
+  float* rdst = R + static_cast<int64_t>(p) * M + r.yoff;
+  const int npass = (r.xcnt + SP_CAP - 1) / SP_CAP;
+  for (int pass = 0; pass < (npass > 0 ? npass : 1); ++pass) {
+    const int nk = (npass > 0) ? min(SP_CAP, r.xcnt - pass * SP_CAP) : 0;
+    const float2* xp = xsrc + pass * SP_CAP;
+    for (int b = tid; b <= SP_NBF; b += S3_T) S.start[b] = 0;
+    __syncthreads();
+    // ---- fine-bucket counting sort of this pass's x into shared memory
+    int fr[S3_PER];   // (fine bucket << 13) | rank inside the bucket, -1: none
+    {
+      float zx[S3_PER];   // all loads in flight before the first use
+#pragma unroll
+      for (int k = 0; k < S3_PER; ++k) {
+        const int i = tid + k * S3_T;
+        zx[k] = (i < nk) ? ldg_cg(&xp[i].x) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < S3_PER; ++k) {
+        fr[k] = -1;
+        if (tid + k * S3_T < nk) {
+          const int b = fine_of(ucoord(zx[k], xmin, hscale), r.blo, r.fmul);
+          fr[k] = (b << 13) | atomicAdd(&S.start[b], 1);
+        }
+      }
+    }
+    __syncthreads();
+    {
+      constexpr int PB = SP_NBF / S3_T;   // 4 buckets per thread
+      int c[PB], loc = 0;
+      const int4 cv = reinterpret_cast<const int4*>(S.start)[tid];
+      c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
+#pragma unroll
+      for (int j = 0; j < PB; ++j) loc += c[j];
+      int total;
+      int run = block_excl_scan<S3_T>(loc, S.wbuf, &total);
+      int4 ov;
+      ov.x = run; run += c[0];
+      ov.y = run; run += c[1];
+      ov.z = run; run += c[2];
+      ov.w = run;
+      reinterpret_cast<int4*>(S.start)[tid] = ov;
+      if (tid == 0) S.start[SP_NBF] = total;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < S3_PER; h += 8) {   // second read of the pass's x (L2), 8 in flight per thread
+      float2 e8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e8[k] = (fr[h + k] >= 0) ? ldg_cg2(xp + tid + (h + k) * S3_T) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (fr[h + k] >= 0) S.xs[S.start[fr[h + k] >> 13] + (fr[h + k] & 8191)] = e8[k];
+    }
+    __syncthreads();
+    // ---- fp64 bucket sums (thread t: buckets t, t + S3_T, ...: neighbouring lanes read neighbouring buckets)
+    //      into rec[], then one blocked exclusive scan (thread t: buckets 4t .. 4t+3)
+#pragma unroll
+    for (int c0 = 0; c0 < SP_NBF; c0 += S3_T) {
+      const int b = c0 + tid;
+      double2 v = make_double2(0.0, 0.0);
+      for (int i = S.start[b], e = S.start[b + 1]; i < e; ++i) {
+        const float2 q = S.xs[i];
+        v.x += q.y;
+        v.y += static_cast<double>(q.y) * q.x;
+      }
+      S.rec[b] = v;
+    }
+    __syncthreads();
+    {
+      constexpr int PB = SP_NBF / S3_T;
+      double2 v[PB], loc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < PB; ++j) { v[j] = S.rec[tid * PB + j]; loc = loc + v[j]; }
+      double2 tch;
+      double2 run = block_excl_scan_d2(loc, S.dbuf, &tch);
+#pragma unroll
+      for (int j = 0; j < PB; ++j) { S.rec[tid * PB + j] = run; run = run + v[j]; }
+      if (tid == 0) S.rec[SP_NBF] = tch;
+    }
+    __syncthreads();
+    // ---- targets of this owner, all lookups in shared memory:
+    //   sum_n w|x - z| = z(2A_b - A) - 2B_b + B + 2 sum_{x in b, x < z} w (z - x) + [other owners]
+    const double dA = S.outer[0] - S.outer[2], dB = S.outer[3] - S.outer[1];   // z(Alo - Ahi) + (Bhi - Blo)
+    const double2 Tp = S.rec[SP_NBF];
+    constexpr int YB = 8;   // targets per thread per batch; the next batch's loads are issued first
+    float zn[YB];
+#pragma unroll
+    for (int k = 0; k < YB; ++k) {
+      const int i = tid + k * S3_T;
+      zn[k] = (i < r.ycnt) ? ldg_cg(ysrc + i) : 0.f;
+    }
+    for (int i0 = 0; i0 < r.ycnt; i0 += YB * S3_T) {
+      float zy[YB];
+#pragma unroll
+      for (int k = 0; k < YB; ++k) zy[k] = zn[k];
+#pragma unroll
+      for (int k = 0; k < YB; ++k) {
+        const int i = i0 + YB * S3_T + tid + k * S3_T;
+        zn[k] = (i < r.ycnt) ? ldg_cg(ysrc + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < YB; ++k) {
+        const int i = i0 + tid + k * S3_T;
+        if (i >= r.ycnt) continue;
+        const float zf = zy[k];
+        const int b = fine_of(ucoord(zf, xmin, hscale), r.blo, r.fmul);
+        const double2 rb = S.rec[b];
+        const int j0 = S.start[b], j1 = S.start[b + 1];
+        float s0 = 0.f, s1 = 0.f;
+        int j = j0;
+        for (; j + 2 <= j1; j += 2) {
+          const float2 q0 = S.xs[j], q1 = S.xs[j + 1];
+          s0 = fmaf(q0.y, fmaxf(zf - q0.x, 0.f), s0);
+          s1 = fmaf(q1.y, fmaxf(zf - q1.x, 0.f), s1);
+        }
+        if (j < j1) {
+          const float2 q = S.xs[j];
+          s0 = fmaf(q.y, fmaxf(zf - q.x, 0.f), s0);
+        }
+        const double zd = zf;
+        double v = zd * (2.0 * rb.x - Tp.x) - 2.0 * rb.y + Tp.y + 2.0 * static_cast<double>(s0 + s1);
+        if (pass == 0) v += zd * dA + dB;
+        const float t = static_cast<float>(-coef * v);
+        if (pass == 0) rdst[i] = t;
+        else rdst[i] += t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------- S4
+__global__ void __launch_bounds__(S4_T) k_sp_gather(int np, int64_t M, const int* __restrict__ ypos,
+                                                    const float* __restrict__ R, double* __restrict__ s64,
+                                                    float* __restrict__ per_slice_out) {
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * S4_CH + threadIdx.x;
+  const int p0 = blockIdx.y * S4_SG, p1 = min(np, p0 + S4_SG);
+  double acc[S4_PER];
+#pragma unroll
+  for (int k = 0; k < S4_PER; ++k) acc[k] = 0.0;
+  for (int p = p0; p < p1; ++p) {
+    int q[S4_PER];
+#pragma unroll
+    for (int k = 0; k < S4_PER; ++k) {
+      const int64_t m = m0 + k * S4_T;
+      q[k] = (m < M) ? __ldcs(ypos + static_cast<int64_t>(p) * M + m) : 0;
+    }
+    float t[S4_PER];
+#pragma unroll
+    for (int k = 0; k < S4_PER; ++k) {
+      const int64_t m = m0 + k * S4_T;
+      t[k] = (m < M) ? __ldcs(R + static_cast<int64_t>(p) * M + q[k]) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < S4_PER; ++k) {
+      const int64_t m = m0 + k * S4_T;
+      if (m >= M) continue;
+      acc[k] += t[k];
+      if (per_slice_out) per_slice_out[static_cast<int64_t>(p) * M + m] = t[k];
+    }
+  }
+  if (s64)
+#pragma unroll
+    for (int k = 0; k < S4_PER; ++k) {
+      const int64_t m = m0 + k * S4_T;
+      if (m < M) atomicAdd(s64 + m, acc[k]);
+    }
+}
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+SpDims sortpart_dims(int64_t N, int64_t M) {
+  SpDims d;
+  // histogram bins: ~16 x per bin on average, at least 2048, at most 16384 (u16 owner map in shared memory)
+  int nh = 2048;
+  while (nh < 16384 && nh * 16 < N) nh *= 2;
+  d.NH = nh;
+  // owners: ~6k x each (capacity SP_CAP = 8k leaves room for the bin granularity of the balance)
+  int64_t g = cdiv(N, SP_CAP * 3 / 4);
+  if (g < 1) g = 1;
+  if (g > 1024) g = 1024;   // beyond: owners take several passes
+  d.G = static_cast<int>(g);
+  (void)M;
+  return d;
+}
+
+// slices per group (SKS_SORT_GROUP; default: the whole batch).  A small group keeps its mailboxes
+// (8N + 12M bytes per slice) resident in L2 between the partition, owner and gather kernels.
+int sortpart_group(int64_t N, int64_t M, int np) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = std::getenv("SKS_SORT_GROUP");
+    env = e ? std::max(1, std::atoi(e)) : 0;
+  }
+  // measured on B200 (cfg2): groups of 4 / 12 / 48 / all 256 slices: 7.2 / 3.2 / 1.49 / 0.95 ms -- the kernels
+  // are latency-bound, and the per-group tails cost more than the DRAM round trip of the mailboxes saves
+  const int64_t g = env ? env : np;
+  return static_cast<int>(std::min<int64_t>(g, np));
+}
+
+size_t sortpart_bytes(int64_t N, int64_t M, int np_all) {
+  const SpDims d = sortpart_dims(N, M);
+  const int np = sortpart_group(N, M, np_all);
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  size_t s = 0;
+  s += al(sizeof(int) * 2 * d.NH * static_cast<size_t>(np));          // H
+  s += al(sizeof(int) * 2 * d.G * static_cast<size_t>(np));           // cursors
+  s += al(sizeof(int) * static_cast<size_t>(np));                     // done tickets
+  s += al(sizeof(double) * 4 * d.G * static_cast<size_t>(np));        // owner sums
+  s += al(sizeof(uint16_t) * d.NH * static_cast<size_t>(np));         // owner map
+  s += al(sizeof(SpOwner) * d.G * static_cast<size_t>(np));           // owners
+  s += al(sizeof(float2) * N * static_cast<size_t>(np));              // x mailbox
+  s += al(sizeof(float) * M * static_cast<size_t>(np));               // y mailbox
+  s += al(sizeof(float) * M * static_cast<size_t>(np));               // results
+  s += al(sizeof(int) * M * static_cast<size_t>(np));                 // y positions
+  return s;
+}
+
+cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
+  const int64_t N = a.zv.N, M = a.zv.M;
+  const SpDims d = sortpart_dims(N, M);
+  const int NH = d.NH, G = d.G;
+  const int gs = sortpart_group(N, M, a.np);
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  char* w = static_cast<char*>(ws);
+  int* H = reinterpret_cast<int*>(w);                 w += al(sizeof(int) * 2 * NH * static_cast<size_t>(gs));
+  int* cursor = reinterpret_cast<int*>(w);            w += al(sizeof(int) * 2 * G * static_cast<size_t>(gs));
+  int* done = reinterpret_cast<int*>(w);              w += al(sizeof(int) * static_cast<size_t>(gs));
+  double* osum = reinterpret_cast<double*>(w);        w += al(sizeof(double) * 4 * G * static_cast<size_t>(gs));
+  const size_t zero_bytes = static_cast<size_t>(w - static_cast<char*>(ws));
+  uint16_t* om = reinterpret_cast<uint16_t*>(w);      w += al(sizeof(uint16_t) * NH * static_cast<size_t>(gs));
+  SpOwner* own = reinterpret_cast<SpOwner*>(w);       w += al(sizeof(SpOwner) * G * static_cast<size_t>(gs));
+  float2* Xmb = reinterpret_cast<float2*>(w);         w += al(sizeof(float2) * N * static_cast<size_t>(gs));
+  float* Ymb = reinterpret_cast<float*>(w);           w += al(sizeof(float) * M * static_cast<size_t>(gs));
+  float* R = reinterpret_cast<float*>(w);             w += al(sizeof(float) * M * static_cast<size_t>(gs));
+  int* ypos = reinterpret_cast<int*>(w);
+
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sp_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(OwnerShared)));
+    attr = true;
+  }
+  constexpr int cpb = 4;   // partition chunks per CTA
+  const int ncx0 = static_cast<int>(cdiv(N, S0_CH)), ncy0 = static_cast<int>(cdiv(M, S0_CH));
+  const int ncx2 = static_cast<int>(cdiv(cdiv(N, S2_CH), cpb)), ncy2 = static_cast<int>(cdiv(cdiv(M, S2_CH), cpb));
+  const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1);
+  const size_t sm2 = sizeof(float2) * S2_CH + sizeof(int) * 4 * G + sizeof(uint16_t) * (S2_CH + NH);
+  for (int g0 = 0; g0 < a.np; g0 += gs) {
+    const int np = std::min(gs, a.np - g0);
+    ZView zv = a.zv;
+    zv.zx += g0 * zv.ldx;
+    zv.zy += g0 * zv.ldy;
+    const unsigned* mm = a.mm + 4 * g0;
+    float* pso = a.per_slice_out ? a.per_slice_out + static_cast<int64_t>(g0) * M : nullptr;
+    cudaError_t e = cudaMemsetAsync(ws, 0, zero_bytes, st);
+    if (e != cudaSuccess) return e;
+    k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, H, done, om, own);
+    k_sp_part<<<dim3(ncx2 + ncy2, np), S2_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, cpb, om, own, cursor, osum, Xmb,
+                                                         Ymb, ypos);
+    k_sp_owner<<<dim3(G, np), S3_T, sizeof(OwnerShared), st>>>(own, osum, mm, NH, G, N, M, Xmb, Ymb, a.coef, R,
+                                                                a.tot + g0);
+    k_sp_gather<<<dim3(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG))), S4_T, 0, st>>>(
+        np, M, ypos, R, a.s64, pso);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace sks

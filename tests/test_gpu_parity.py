@@ -52,6 +52,7 @@ CASES_1D = [
     ("negdist", 0.0, 50, 3001, 1537, 5),
     ("negdist", 0.0, 3, 1, 1, 2),
     ("negdist", 0.0, 3, 70000, 333, 2),
+    ("negdist", 0.0, 50, 200000, 400, 2),   # 33 owners per slice, 16384 histogram bins (sortpart.cu)
     ("gaussian", 1.0, 3, 2003, 1001, 4),
     ("gaussian", 11.0, 784, 4097, 515, 3),
     ("gaussian", 30.0, 100, 5000, 700, 3),
@@ -89,6 +90,38 @@ def test_sum_1d_degenerate_identical_points():
             ref = O.sum_1d(kind, scale if kind != "negdist" else 0.0, d, zx[q].astype(np.float64),
                            w.astype(np.float64), zy[q].astype(np.float64))
             assert rel_err(t[q], ref, w) <= TOL[kind], kind
+
+
+def test_sum_1d_owner_overflow_multipass():
+    # more identical sources than one owner's shared memory holds (8192): that owner runs several passes over
+    # subsets of its sources (sortpart.cu S3); the rest of the slice is spread normally
+    rng = np.random.default_rng(11)
+    N, M = 21000, 600
+    zx = np.stack([np.concatenate([np.full(13000, 0.3), rng.standard_normal(8000)]),
+                   np.concatenate([rng.standard_normal(8000), np.full(13000, -1.25)])]).astype(np.float32)
+    zy = np.stack([np.concatenate([np.full(50, 0.3), rng.standard_normal(550)]),
+                   np.concatenate([np.full(50, -1.25), rng.standard_normal(550)])]).astype(np.float32)
+    w = rng.uniform(-1, 1, N).astype(np.float32)
+    for kind, scale in [("negdist", 1.0), ("laplacian", 2.0)]:
+        t = S.sks_sum_1d(dev(zx), dev(zy), dev(w), 50, kind, scale).cpu().numpy()
+        for q in range(2):
+            ref = O.sum_1d(kind, scale if kind != "negdist" else 0.0, 50, zx[q].astype(np.float64),
+                           w.astype(np.float64), zy[q].astype(np.float64))
+            assert rel_err(t[q], ref, w) <= TOL[kind], (kind, q)
+
+
+def test_sum_1d_targets_outside_source_range():
+    # targets below / above every source (clamped to the first / last owner and bucket); |t| stays within
+    # ~100 sum|w| so that the fp32 output itself resolves 1e-5 sum|w|
+    rng = np.random.default_rng(12)
+    N, M = 9000, 400
+    zx = rng.standard_normal((2, N)).astype(np.float32)
+    zy = np.concatenate([rng.uniform(-10, -5, (2, 200)), rng.uniform(5, 10, (2, 200))], 1).astype(np.float32)
+    w = rng.uniform(0, 1, N).astype(np.float32)
+    t = S.sks_sum_1d(dev(zx), dev(zy), dev(w), 50, "negdist", 1.0).cpu().numpy()
+    for q in range(2):
+        ref = O.sum_1d("negdist", 0.0, 50, zx[q].astype(np.float64), w.astype(np.float64), zy[q].astype(np.float64))
+        assert rel_err(t[q], ref, w) <= TOL["negdist"]
 
 
 # ---------------------------------------------------------------- end to end (Alg. 1) vs oracle (b)
