@@ -90,16 +90,52 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// min / max of 16 columns (kmn[j] / kmx[j] = this lane's key of column j) over the 32 lanes of a warp: five
+// butterfly stages, each halving the columns a lane keeps; afterwards lanes 2c and 2c + 1 hold column
+// c = 8 b4 + 4 b3 + 2 b2 + b1 (b_k = bit k of the lane).  Destroys kmn / kmx.
+__device__ __forceinline__ void colrange16(uint32_t* kmn, uint32_t* kmx, int b4, int b3, int b2, int b1, uint32_t* omn,
+                                           uint32_t* omx) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {   // offset 16: keep columns 8 b4 + k
+    const uint32_t smn = b4 ? kmn[k] : kmn[8 + k], smx = b4 ? kmx[k] : kmx[8 + k];
+    const uint32_t rmn = __shfl_xor_sync(0xffffffffu, smn, 16), rmx = __shfl_xor_sync(0xffffffffu, smx, 16);
+    kmn[k] = min(b4 ? kmn[8 + k] : kmn[k], rmn);
+    kmx[k] = max(b4 ? kmx[8 + k] : kmx[k], rmx);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {   // offset 8
+    const uint32_t smn = b3 ? kmn[k] : kmn[4 + k], smx = b3 ? kmx[k] : kmx[4 + k];
+    const uint32_t rmn = __shfl_xor_sync(0xffffffffu, smn, 8), rmx = __shfl_xor_sync(0xffffffffu, smx, 8);
+    kmn[k] = min(b3 ? kmn[4 + k] : kmn[k], rmn);
+    kmx[k] = max(b3 ? kmx[4 + k] : kmx[k], rmx);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {   // offset 4
+    const uint32_t smn = b2 ? kmn[k] : kmn[2 + k], smx = b2 ? kmx[k] : kmx[2 + k];
+    const uint32_t rmn = __shfl_xor_sync(0xffffffffu, smn, 4), rmx = __shfl_xor_sync(0xffffffffu, smx, 4);
+    kmn[k] = min(b2 ? kmn[2 + k] : kmn[k], rmn);
+    kmx[k] = max(b2 ? kmx[2 + k] : kmx[k], rmx);
+  }
+  {   // offset 2
+    const uint32_t smn = b1 ? kmn[0] : kmn[1], smx = b1 ? kmx[0] : kmx[1];
+    const uint32_t rmn = __shfl_xor_sync(0xffffffffu, smn, 2), rmx = __shfl_xor_sync(0xffffffffu, smx, 2);
+    kmn[0] = min(b1 ? kmn[1] : kmn[0], rmn);
+    kmx[0] = max(b1 ? kmx[1] : kmx[0], rmx);
+  }
+  *omn = min(kmn[0], __shfl_xor_sync(0xffffffffu, kmn[0], 1));   // offset 1: both lanes of the pair
+  *omx = max(kmx[0], __shfl_xor_sync(0xffffffffu, kmx[0], 1));
+}
+
 // Persistent: grid = min(#tiles, #SMs) CTAs, tiles t = blockIdx.x + i*gridDim.x (slice tiles fastest, so the
 // CTAs that share a point tile run together and its TMA loads hit L2).  Two TMEM accumulators: the epilogue
-// of tile i overlaps the MMAs of tile i+1.  Per-slice ranges: per-CTA partials in smem -> part[cta][s][4].
+// of tile i overlaps the MMAs of tile i+1.  Per-slice ranges: per-CTA partials in smem -> global atomics.
 constexpr int TC_THREADS = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue (2 warpgroups)
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nk, int64_t L,
               int64_t Nx, int np, const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz,
-              unsigned* __restrict__ part, int* __restrict__ flag) {
+              unsigned* __restrict__ mm, int* __restrict__ flag) {
   using SM = TcSmem<BN, STAGES>;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -193,10 +229,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---- epilogue: warp w handles TMEM lane quadrant q = w % 4 (points m0 + 32q + lane) and the column half
-    //      h = (w - 4) / 4 of the accumulator
+    //      h = (w - 4) / 4 of the accumulator.  Per 16-column chunk: scale, store (coalesced along points),
+    //      order-preserving keys, and the per-column min / max over the warp's 32 points by a butterfly that
+    //      halves the columns at every shuffle stage (16 columns -> one column per lane pair in 5 stages).
     const int q = warp & 3, h = (warp - 4) >> 2;
     constexpr int HALF = BN / 2;
-    bool bad = false;
+    const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+    const int my_col = 8 * b4 + 4 * b3 + 2 * b2 + b1;   // column of the chunk this lane pair ends up holding
+    bool bad = false;   // a non-finite projection (NaN / Inf in x, y or an overflow)
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int b = it & 1;
@@ -206,7 +246,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int64_t w0 = m0 + 32 * q;
       const int64_t i = w0 + lane;
       const bool valid = i < L, isx = i < Nx;
-      const bool warp_all_x = (w0 + 32 <= Nx), warp_any_x = (w0 < Nx);
+      const bool warp_any_x = (w0 < Nx), mixed = warp_any_x && (w0 + 32 > Nx);
       const int ncols = min(HALF, np - n0);   // may be <= 0
       mbar_wait(&tfull[b], tph);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -220,6 +260,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(tbase));
+      float* zrow = Z + static_cast<int64_t>(n0) * ldz + i;
 #pragma unroll 1
       for (int c0 = 0; c0 < ncols; c0 += 16) {
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -233,55 +274,65 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
               : "r"(tbase + static_cast<uint32_t>(c0 + 16)));
-        unsigned my_amn = 0xffffffffu, my_amx = 0u, my_xmn = 0xffffffffu, my_xmx = 0u;   // lane j keeps column j
+        const int nc = min(16, ncols - c0);
+        const float4* sv = reinterpret_cast<const float4*>(sinv + n0 + c0);
+        float sc[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 f = sv[k];
+          sc[4 * k] = f.x; sc[4 * k + 1] = f.y; sc[4 * k + 2] = f.z; sc[4 * k + 3] = f.w;
+        }
+        uint32_t kmn[16], kmx[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int s = n0 + c0 + j;
-          if (c0 + j >= ncols) break;   // warp-uniform
-          const float z = __uint_as_float(cur[j]) * sinv[s];
-          if (valid) {
-            Z[static_cast<int64_t>(s) * ldz + i] = z;
+          const float z = __uint_as_float(cur[j]) * sc[j];
+          const bool ok = valid && j < nc;
+          if (ok) {
+            zrow[static_cast<int64_t>(c0 + j) * ldz] = z;
             bad |= !isfinite(z);
           }
-          const unsigned key = f2key_tc(z);
-          const unsigned amn = __reduce_min_sync(0xffffffffu, valid ? key : 0xffffffffu);
-          const unsigned amx = __reduce_max_sync(0xffffffffu, valid ? key : 0u);
-          unsigned xmn = amn, xmx = amx;
-          if (!warp_all_x) {
-            xmn = __reduce_min_sync(0xffffffffu, (valid && isx) ? key : 0xffffffffu);
-            xmx = __reduce_max_sync(0xffffffffu, (valid && isx) ? key : 0u);
-          }
-          if (lane == j) { my_amn = amn; my_amx = amx; my_xmn = xmn; my_xmx = xmx; }
+          const uint32_t key = f2key_tc(z);
+          kmn[j] = ok ? key : 0xffffffffu;
+          kmx[j] = ok ? key : 0u;
         }
-        if (lane < 16 && c0 + lane < ncols) {   // one lane per column: no divergent per-column branches
-          const int s = n0 + c0 + lane;
-          if (my_amn <= my_amx) { atomicMin(&rng[4 * s + 2], my_amn); atomicMax(&rng[4 * s + 3], my_amx); }
-          if (warp_any_x && my_xmn <= my_xmx) { atomicMin(&rng[4 * s + 0], my_xmn); atomicMax(&rng[4 * s + 1], my_xmx); }
+        uint32_t amn, amx;
+        colrange16(kmn, kmx, b4, b3, b2, b1, &amn, &amx);
+        uint32_t xmn = amn, xmx = amx;
+        if (mixed) {   // the warp holding the x/y boundary: x-only ranges separately
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t key = f2key_tc(__uint_as_float(cur[j]) * sc[j]);
+            const bool ok = valid && isx && j < nc;
+            kmn[j] = ok ? key : 0xffffffffu;
+            kmx[j] = ok ? key : 0u;
+          }
+          colrange16(kmn, kmx, b4, b3, b2, b1, &xmn, &xmx);
+        }
+        if ((lane & 1) == 0 && my_col < nc) {
+          const int s = n0 + c0 + my_col;
+          if (amn <= amx) { atomicMin(&rng[4 * s + 2], amn); atomicMax(&rng[4 * s + 3], amx); }
+          if (warp_any_x && xmn <= xmx) { atomicMin(&rng[4 * s + 0], xmn); atomicMax(&rng[4 * s + 1], xmx); }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
     }
-    if (bad) atomicOr(flag, 1);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  for (int e = threadIdx.x; e < 4 * np; e += blockDim.x) part[static_cast<int64_t>(blockIdx.x) * 4 * np + e] = rng[e];
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
-}
-
-__global__ void k_range_reduce(const unsigned* __restrict__ part, int nparts, int np, unsigned* __restrict__ mm) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= 4 * np) return;
-  const bool is_min = (e & 1) == 0;
-  unsigned v = mm[e];
-  for (int c = 0; c < nparts; ++c) {
-    const unsigned u = part[static_cast<int64_t>(c) * 4 * np + e];
-    v = is_min ? min(v, u) : max(v, u);
+  // this CTA's per-slice ranges into the global ranges (one atomic per slice and bound; ~148-way contention)
+  for (int e = threadIdx.x; e < 4 * np; e += blockDim.x) {
+    const unsigned v = rng[e];
+    if ((e & 1) == 0) {
+      if (v != 0xffffffffu) atomicMin(mm + e, v);
+    } else if (v != 0u) {
+      atomicMax(mm + e, v);
+    }
   }
-  mm[e] = v;
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
 }
 
 // fp32 -> three bf16 pieces, K-concatenated:  Xs[i][j] = hi, Xs[i][dp+j] = mid, Xs[i][2dp+j] = lo.
@@ -376,8 +427,8 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int6
   }
   const int64_t ntiles = ((L + TC_M - 1) / TC_M) * ntn;
   const int grid = static_cast<int>(ntiles < kProjMaxCtas ? ntiles : kProjMaxCtas);
-  k_proj_tc<BN, STAGES><<<grid, TC_THREADS, smem, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, part, flag);
-  k_range_reduce<<<(4 * np + 255) / 256, 256, 0, st>>>(part, grid, np, mm);
+  k_proj_tc<BN, STAGES><<<grid, TC_THREADS, smem, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag);
+  (void)part;
   return cudaGetLastError();
 }
 
