@@ -55,27 +55,56 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
 
 
-# ------------------------------------------------------------------ algorithmic bytes per launch
-def algorithmic_bytes(slot, cfg, np_local, plan):
-    """Compulsory HBM bytes of one launch of each kernel slot (inputs read once, outputs written once);
-    the per-unit figures and their derivation are in DESIGN.md "Roofline model"."""
-    N, M, d, P = cfg.N, cfg.M, cfg.d, np_local
+# ------------------------------------------------------------------ roofline model per kernel
+def roofline_model(slot, cfg, P, plan):
+    """(algorithmic HBM bytes, algorithmic flops) of ONE launch of each kernel slot over P slices: compulsory
+    traffic (each input read once, each output written once) and the method's own arithmetic; the per-unit
+    figures and their derivation are in DESIGN.md Sec. 6."""
+    N, M, d = cfg.N, cfg.M, cfg.d
     L = N + M
+    dp = (d + 63) // 64 * 64
     n = plan.get("n_grid", 0) or 0
-    nb = plan.get("n_buckets", 0) or 0
-    if slot == "project":
-        return 4 * L * d + 4 * L * P + 4 * P * d
-    if slot == "sortsum":   # fused sort path: its scratch (bucketed x/y, records) stays in L2
-        return 4 * (N + M) * P + 4 * N + 16 * M
+    if slot == "split3":        # fp32 points -> 3 bf16 pieces
+        return 4 * L * d + 6 * L * dp, 0
+    if slot == "project":       # Z = X G^T: read the pieces and G, write Z; 2 L d P fp32-accurate flops
+        return 6 * L * dp + 2 * P * dp + 4 * L * P, 2.0 * L * d * P
+    if slot == "sp_hist":       # read every projection
+        return 4 * L * P, 0
+    if slot == "sp_part":       # read projections and w, write x mailbox (z, w), y mailbox (z) + positions
+        return 4 * L * P + 4 * N + (8 * N + 8 * M) * P, 0
+    if slot == "sp_owner":      # read the mailboxes, write t per (slice, target)
+        return (8 * N + 8 * M) * P, 0
+    if slot == "sp_gather":     # read positions and t, accumulate s (fp64)
+        return 8 * M * P + 16 * M, 0
+    if slot == "sortsum_v1":
+        return 4 * L * P + 4 * N + 16 * M, 0
     if slot == "spread":
-        return 4 * N * P + 4 * N + 4 * n * P
+        return 4 * N * P + 4 * N + 4 * n * P, 0
     if slot == "fft_filter":
-        return 4 * n * P + 4 * (n // 2 + 1) * P + 4 * n * P
+        return 4 * n * P + 4 * (n // 2 + 1) * P + 4 * n * P, 0
     if slot == "plan_D":
-        return 4 * (n // 2 + 1) * P
-    if slot == "eval":       # Fourier interpolation (+ Laplacian moment term)
-        return 4 * M * P + 16 * M + 4 * n * P
-    return 0
+        return 4 * (n // 2 + 1) * P, 0
+    if slot == "eval":          # Fourier interpolation (+ Laplacian moment term)
+        return 4 * M * P + 16 * M + 4 * n * P, 0
+    return 0, 0
+
+
+def roofline(slot, cfg, P, plan, ms_per_launch, pk, traffic):
+    """achieved / peak of one kernel: bound = the larger of its HBM time and its tensor time at peak."""
+    by, fl = roofline_model(slot, cfg, P, plan)
+    t = ms_per_launch * 1e-3
+    tensor_peak = pk["bf16_tflops"] / 3.0   # fp32-accurate BF16x3: three bf16 MMAs per fp32 product (R2)
+    if fl and fl / (tensor_peak * 1e12) > by / (pk["hbm_gbs"] * 1e9):
+        r = {"kernel": slot, "bound": "tensor", "achieved": fl / t / 1e12, "peak": tensor_peak, "unit": "TFLOP/s",
+             "peak_source": "MEASURED_PEAKS.json bf16_tflops / 3 (BF16x3 fp32 emulation)",
+             "algorithmic_flops_per_launch": fl}
+    else:
+        r = {"kernel": slot, "bound": "hbm", "achieved": by / t / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+             "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else ""),
+             "algorithmic_bytes_per_launch": by}
+    r["frac"] = r["achieved"] / r["peak"]
+    r["traffic"] = traffic
+    return r
 
 
 class ClockSampler:
@@ -298,32 +327,26 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (live CUDA-event durations over the timed region)
+    # ---- roofline of every kernel, headline = the dominant one (live CUDA-event durations, timed region)
     pk = peaks()
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps} for k, v in prof.items()
                if v[1] > 0}
-    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
-    n_launch = prof[dom][1]
-    per_launch_ms = prof[dom][0] / max(1, n_launch)
     np_local = p1 - p0
-    alg = algorithmic_bytes(dom, cfg, np_local if plan.get("slice_batch", 0) in (0, np_local) else plan["slice_batch"],
-                            plan)
-    traffic = None
+    P_launch = plan["slice_batch"] if plan.get("slice_batch", 0) else np_local
+    traffic_all = {}
     tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom)
-    if dom == "project":
-        flops = 2.0 * (cfg.N + cfg.M) * cfg.d * np_local
-        fp32_peak = 148 * 128 * 2 * (pk.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
-        roof = {"kernel": dom, "bound": "alu", "achieved": flops / (per_launch_ms * 1e-3) / 1e12,
-                "peak": fp32_peak, "unit": "TFLOP/s",
-                "peak_source": "148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (MEASURED_PEAKS.json)",
-                "traffic": traffic}
-    else:
-        roof = {"kernel": dom, "bound": "hbm", "achieved": alg / (per_launch_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else ""),
-                "algorithmic_bytes_per_launch": alg, "traffic": traffic}
-    roof["frac"] = roof["achieved"] / roof["peak"]
+        traffic_all = json.load(open(tpath))
+    for k, v in kernels.items():
+        if k == "aux":
+            continue
+        r = roofline(k, cfg, P_launch, plan, v["ms_per_step"] / max(1e-9, v["launches_per_step"]), pk,
+                     traffic_all.get(k))
+        v["roofline_frac"] = r["frac"]
+        v["bound"] = r["bound"]
+    dom = max((k for k in kernels if k != "aux"), key=lambda k: kernels[k]["ms_per_step"])
+    roof = roofline(dom, cfg, P_launch, plan, kernels[dom]["ms_per_step"] / max(1e-9, kernels[dom]["launches_per_step"]),
+                    pk, traffic_all.get(dom))
     roof["share_of_step"] = kernels[dom]["ms_per_step"] / ms
 
     cpu = None
@@ -334,7 +357,7 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": config_dict(cfg, param, G), "roofline": roof, "cpu_baseline": cpu,
-            "e2e": e2e, "gpu_launches": int(sum(v[1] for v in prof.values())), "clocks": clk,
+            "e2e": e2e, "gpu_launches": int(plan.get("launches", 0)) * args.steps, "clocks": clk,
             "kernels": kernels, "plan": plan}
     print(json.dumps(line), flush=True)
     if G > 1:

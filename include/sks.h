@@ -146,7 +146,7 @@ sks_status sks_last_plan(sks_plan_info* info);
 sks_status sks_profile_enable(int32_t enable);
 /* Accumulated device time (ms) and launch count per kernel slot since the last read; waits for the
  * recorded events, then resets.  n_slots >= SKS_PROFILE_SLOTS; slot names: sks_profile_names(). */
-#define SKS_PROFILE_SLOTS 8
+#define SKS_PROFILE_SLOTS 16
 sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots);
 /* Comma-separated slot names: "project,minmax,sortsum,plan_D,spread,fft_filter,eval,aux". */
 const char* sks_profile_names(void);

@@ -170,9 +170,9 @@ def sks_profile_enable(enable: bool = True) -> None:
 def sks_profile_read() -> dict:
     """{slot: (ms, launches)} accumulated since the last read (blocks on the recorded events)."""
     L = _lib.load()
-    ms = np.zeros(8, np.float64)
-    cnt = np.zeros(8, np.int64)
-    check(L.sks_profile_read(ms.ctypes.data, cnt.ctypes.data, 8))
+    ms = np.zeros(16, np.float64)
+    cnt = np.zeros(16, np.int64)
+    check(L.sks_profile_read(ms.ctypes.data, cnt.ctypes.data, 16))
     names = L.sks_profile_names().decode().split(",")
     return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(names)}
 

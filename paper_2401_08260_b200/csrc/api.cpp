@@ -20,7 +20,7 @@
 namespace {
 
 // ---- opt-in kernel timing (sks_profile_*): event pairs per slot, resolved on read
-enum Slot { PS_PROJECT = 0, PS_MINMAX, PS_BUCKET, PS_PLAN, PS_SPREAD, PS_FFT, PS_EVAL, PS_AUX, PS_N };
+using namespace sks;   // ProfSlot
 struct Prof {
   std::mutex mu;
   bool on = false;
@@ -60,6 +60,28 @@ struct ProfScope {   // brackets one launch with events on its stream when profi
   }
 };
 #define PROF(slot) ProfScope prof_scope_##__LINE__(slot, st)
+
+}  // namespace
+
+namespace sks {
+ProfMark prof_begin(int slot, cudaStream_t st) {
+  ProfMark m{slot, st, nullptr};
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  if (!g_prof.on) return m;
+  m.a = prof_event();
+  cudaEventRecord(m.a, st);
+  return m;
+}
+void prof_end(const ProfMark& m) {
+  if (!m.a) return;
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  cudaEvent_t b = prof_event();
+  cudaEventRecord(b, m.st);
+  g_prof.pending.emplace_back(m.slot, m.a, b);
+}
+}  // namespace sks
+
+namespace {
 
 thread_local std::string g_err;
 thread_local sks_plan_info g_plan{};
@@ -402,7 +424,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
   launches += s_out ? 2 : 1;
   const bool tc = pr.with_Z && use_tc_projection();
   if (tc) {
-    ProfScope ps(PS_PROJECT, st);
+    ProfScope ps(PS_SPLIT, st);
     SKS_CUDA(sks::launch_split3(x, pr.N, y, pr.M, pr.d, ws + L.xs3, st));
     ++launches;
   }
@@ -451,10 +473,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
       sa.s64 = s64;
       sa.per_slice_out = tps;
-      {
-        ProfScope ps(PS_BUCKET, st);
-        SKS_CUDA(sks::launch_sortpart(sa, ws + L.sp, st));
-      }
+      SKS_CUDA(sks::launch_sortpart(sa, ws + L.sp, st));   // times its own launches (PS_SP_*)
       launches += 4 * sks::sortpart_groups(pr.N, pr.M, nbat);
       ea.tot = sa.tot;
     } else if (pt.sort) {
@@ -483,7 +502,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
         sa.dbg = dbg;
       }
       {
-        ProfScope ps(PS_BUCKET, st);
+        ProfScope ps(PS_SORT_V1, st);
         SKS_CUDA(sks::launch_sortpath(sa, slots, st));
       }
       if (phase_timing) {
@@ -597,7 +616,9 @@ sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots) {
   return SKS_OK;
 }
 
-const char* sks_profile_names(void) { return "project,minmax,sortsum,plan_D,spread,fft_filter,eval,aux"; }
+const char* sks_profile_names(void) {
+  return "split3,project,minmax,sp_hist,sp_part,sp_owner,sp_gather,sortsum_v1,plan_D,spread,fft_filter,eval,aux";
+}
 
 sks_status sks_last_plan(sks_plan_info* info) {
   if (!info) return fail(SKS_ERR_INVALID, "info is NULL");

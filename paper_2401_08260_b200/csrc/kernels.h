@@ -5,6 +5,19 @@
 
 namespace sks {
 
+// opt-in per-launch timing (sks_profile_*, api.cpp): CUDA events around launches, accumulated per slot
+enum ProfSlot {
+  PS_SPLIT = 0, PS_PROJECT, PS_MINMAX, PS_SP_HIST, PS_SP_PART, PS_SP_OWNER, PS_SP_GATHER, PS_SORT_V1, PS_PLAN,
+  PS_SPREAD, PS_FFT, PS_EVAL, PS_AUX, PS_N
+};
+struct ProfMark {
+  int slot;
+  cudaStream_t st;
+  cudaEvent_t a;   // nullptr when profiling is off
+};
+ProfMark prof_begin(int slot, cudaStream_t st);
+void prof_end(const ProfMark& m);
+
 // per-slice Fourier parameters (device copy of SlicePlan)
 struct FPar {
   float tau, cen;

@@ -39,8 +39,22 @@ namespace {
 
 constexpr int S0_T = 512, S0_CH = 16384;      // histogram: elements per CTA
 constexpr int S2_T = 512, S2_PER = 8, S2_CH = S2_T * S2_PER;   // partition: elements per CTA
-constexpr int S3_T = 512, SP_CAP = 8192, SP_NBF = 2048;        // owner: x capacity, fine buckets
-constexpr int S3_PER = SP_CAP / S3_T;
+constexpr int S3_T = 512;   // owner kernel threads
+// owner kernel variants (x capacity, fine buckets, CTAs per SM): SKS_SP_VARIANT selects (measurement aid).
+// Measured on B200, cfg2 sp_owner: {4096,2048,3} 418 us, {8192,2048,2} 438, {4096,1024,3} 374, {2048,1024,4} 465.
+struct SpVar {
+  int cap, nbf, minb;
+};
+constexpr SpVar kSpVars[] = {{4096, 1024, 3}, {8192, 2048, 2}, {4096, 2048, 3}, {2048, 1024, 4}};
+int sp_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SKS_SP_VARIANT");
+    v = e ? std::atoi(e) : 0;
+    if (v < 0 || v > 3) v = 0;
+  }
+  return v;
+}
 constexpr int S4_T = 256, S4_PER = 4, S4_CH = S4_T * S4_PER, S4_SG = 8;    // gather
 
 __device__ __forceinline__ float key2f_sp(unsigned k) {
@@ -69,8 +83,9 @@ __device__ __forceinline__ int clamp_floor(float v, int n) {
   return b < n ? b : n - 1;
 }
 // fine bucket inside an owner: monotone in u (hence in z)
+template <int NBF>
 __device__ __forceinline__ int fine_of(float u, float blo, float fmul) {
-  return clamp_floor(__fmul_rn(__fsub_rn(u, blo), fmul), SP_NBF);
+  return clamp_floor(__fmul_rn(__fsub_rn(u, blo), fmul), NBF);
 }
 
 template <typename T>
@@ -117,8 +132,9 @@ __device__ __forceinline__ T block_excl_scan(T v, T* wbuf, T* total) {
 // (ticket counter per slice): owner of bin b = floor(cx[b] G / Nx) with cx the exclusive prefix x count, so
 // the owners are contiguous bin ranges (monotone) holding <= Nx/G + (largest bin) x each.
 __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __restrict__ mm, int NH, int G,
-                                                  int ncx, int nchunks, int* __restrict__ H, int* __restrict__ done,
-                                                  uint16_t* __restrict__ om, SpOwner* __restrict__ own) {
+                                                  int ncx, int nchunks, int NBF, int* __restrict__ H,
+                                                  int* __restrict__ done, uint16_t* __restrict__ om,
+                                                  SpOwner* __restrict__ own) {
   extern __shared__ int hs[];   // [NH] histogram; in the plan: cx[NH + 1], cy[NH + 1], blo[G + 1]
   __shared__ int wbuf[S0_T / 32 + 1];
   __shared__ int last;
@@ -191,7 +207,7 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
     r.yoff = cy[lo];
     r.ycnt = cy[hi] - cy[lo];
     r.blo = static_cast<float>(lo);
-    r.fmul = (hi > lo) ? static_cast<float>(SP_NBF) / static_cast<float>(hi - lo) : 0.f;
+    r.fmul = (hi > lo) ? static_cast<float>(NBF) / static_cast<float>(hi - lo) : 0.f;
     r.pad0 = r.pad1 = 0;
     own[static_cast<int64_t>(p) * G + o] = r;
   }
@@ -312,6 +328,7 @@ __global__ void __launch_bounds__(S2_T) k_sp_part(ZView zv, const float* __restr
 }
 
 // ---------------------------------------------------------------------------------------------- S3
+template <int SP_CAP, int SP_NBF>
 struct __align__(16) OwnerShared {
   float2 xs[SP_CAP];          // the pass's x (z, w) in fine-bucket order
   double2 rec[SP_NBF + 1];    // exclusive prefix (sum w, sum w x) over the pass's buckets; [NBF] = pass totals
@@ -357,13 +374,15 @@ __device__ __forceinline__ double2 block_excl_scan_d2(double2 v, double2* wbuf, 
   return r;
 }
 
-__global__ void __launch_bounds__(S3_T, 2) k_sp_owner(const SpOwner* __restrict__ own, const double* __restrict__ osum,
+template <int SP_CAP, int SP_NBF, int MINB>
+__global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restrict__ own, const double* __restrict__ osum,
                                                       const unsigned* __restrict__ mm, int NH, int G, int64_t N,
                                                       int64_t M, const float2* __restrict__ Xmb,
                                                       const float* __restrict__ Ymb, double coef, float* __restrict__ R,
                                                       SliceTot* __restrict__ tot) {
   extern __shared__ __align__(16) unsigned char sh3[];
-  OwnerShared& S = *reinterpret_cast<OwnerShared*>(sh3);
+  constexpr int S3_PER = SP_CAP / S3_T;
+  OwnerShared<SP_CAP, SP_NBF>& S = *reinterpret_cast<OwnerShared<SP_CAP, SP_NBF>*>(sh3);
   const int o = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
   const SpOwner r = own[static_cast<int64_t>(p) * G + o];
   if (r.ycnt == 0 && o != 0) return;
@@ -419,37 +438,33 @@ __global__ void __launch_bounds__(S3_T, 2) k_sp_owner(const SpOwner* __restrict_
       for (int k = 0; k < S3_PER; ++k) {
         fr[k] = -1;
         if (tid + k * S3_T < nk) {
-          const int b = fine_of(ucoord(zx[k], xmin, hscale), r.blo, r.fmul);
-          fr[k] = (b << 13) | atomicAdd(&S.start[b], 1);
+          const int b = fine_of<SP_NBF>(ucoord(zx[k], xmin, hscale), r.blo, r.fmul);
+          fr[k] = (b << 13) | atomicAdd(&S.start[b], 1);   // rank < SP_CAP <= 8192
         }
       }
     }
     __syncthreads();
     {
-      constexpr int PB = SP_NBF / S3_T;   // 4 buckets per thread
+      constexpr int PB = SP_NBF / S3_T;   // buckets per thread (2 or 4)
       int c[PB], loc = 0;
-      const int4 cv = reinterpret_cast<const int4*>(S.start)[tid];
-      c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
 #pragma unroll
-      for (int j = 0; j < PB; ++j) loc += c[j];
+      for (int j = 0; j < PB; ++j) { c[j] = S.start[tid * PB + j]; loc += c[j]; }
       int total;
       int run = block_excl_scan<S3_T>(loc, S.wbuf, &total);
-      int4 ov;
-      ov.x = run; run += c[0];
-      ov.y = run; run += c[1];
-      ov.z = run; run += c[2];
-      ov.w = run;
-      reinterpret_cast<int4*>(S.start)[tid] = ov;
+#pragma unroll
+      for (int j = 0; j < PB; ++j) { S.start[tid * PB + j] = run; run += c[j]; }
       if (tid == 0) S.start[SP_NBF] = total;
     }
     __syncthreads();
 #pragma unroll
-    for (int h = 0; h < S3_PER; h += 8) {   // second read of the pass's x (L2), 8 in flight per thread
-      float2 e8[8];
+    constexpr int XB = S3_PER < 8 ? S3_PER : 8;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) e8[k] = (fr[h + k] >= 0) ? ldg_cg2(xp + tid + (h + k) * S3_T) : make_float2(0.f, 0.f);
+    for (int h = 0; h < S3_PER; h += XB) {   // second read of the pass's x (L2), XB in flight per thread
+      float2 e8[XB];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < XB; ++k) e8[k] = (fr[h + k] >= 0) ? ldg_cg2(xp + tid + (h + k) * S3_T) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < XB; ++k)
         if (fr[h + k] >= 0) S.xs[S.start[fr[h + k] >> 13] + (fr[h + k] & 8191)] = e8[k];
     }
     __syncthreads();
@@ -504,7 +519,7 @@ __global__ void __launch_bounds__(S3_T, 2) k_sp_owner(const SpOwner* __restrict_
         const int i = i0 + tid + k * S3_T;
         if (i >= r.ycnt) continue;
         const float zf = zy[k];
-        const int b = fine_of(ucoord(zf, xmin, hscale), r.blo, r.fmul);
+        const int b = fine_of<SP_NBF>(ucoord(zf, xmin, hscale), r.blo, r.fmul);
         const double2 rb = S.rec[b];
         const int j0 = S.start[b], j1 = S.start[b + 1];
         float s0 = 0.f, s1 = 0.f;
@@ -578,8 +593,8 @@ SpDims sortpart_dims(int64_t N, int64_t M) {
   int nh = 2048;
   while (nh < 16384 && nh * 16 < N) nh *= 2;
   d.NH = nh;
-  // owners: ~6k x each (capacity SP_CAP = 8k leaves room for the bin granularity of the balance)
-  int64_t g = cdiv(N, SP_CAP * 3 / 4);
+  // owners: 3/4 of the owner capacity each (room for the bin granularity of the balance)
+  int64_t g = cdiv(N, kSpVars[sp_variant()].cap * 3 / 4);
   if (g < 1) g = 1;
   if (g > 1024) g = 1024;   // beyond: owners take several passes
   d.G = static_cast<int>(g);
@@ -642,7 +657,14 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
   if (!attr) {
     cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sp_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(OwnerShared)));
+    cudaFuncSetAttribute(k_sp_owner<4096, 2048, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(OwnerShared<4096, 2048>)));
+    cudaFuncSetAttribute(k_sp_owner<8192, 2048, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(OwnerShared<8192, 2048>)));
+    cudaFuncSetAttribute(k_sp_owner<4096, 1024, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(OwnerShared<4096, 1024>)));
+    cudaFuncSetAttribute(k_sp_owner<2048, 1024, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(OwnerShared<2048, 1024>)));
     attr = true;
   }
   constexpr int cpb = 4;   // partition chunks per CTA
@@ -659,13 +681,30 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
     float* pso = a.per_slice_out ? a.per_slice_out + static_cast<int64_t>(g0) * M : nullptr;
     cudaError_t e = cudaMemsetAsync(ws, 0, zero_bytes, st);
     if (e != cudaSuccess) return e;
-    k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, H, done, om, own);
+    ProfMark pm = prof_begin(PS_SP_HIST, st);
+    k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, kSpVars[sp_variant()].nbf,
+                                                         H, done, om, own);
+    prof_end(pm);
+    pm = prof_begin(PS_SP_PART, st);
     k_sp_part<<<dim3(ncx2 + ncy2, np), S2_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, cpb, om, own, cursor, osum, Xmb,
                                                          Ymb, ypos);
-    k_sp_owner<<<dim3(G, np), S3_T, sizeof(OwnerShared), st>>>(own, osum, mm, NH, G, N, M, Xmb, Ymb, a.coef, R,
-                                                                a.tot + g0);
+    prof_end(pm);
+    pm = prof_begin(PS_SP_OWNER, st);
+    switch (sp_variant()) {
+#define SP_OWNER_LAUNCH(C, B, MB)                                                                                  \
+  k_sp_owner<C, B, MB><<<dim3(G, np), S3_T, sizeof(OwnerShared<C, B>), st>>>(own, osum, mm, NH, G, N, M, Xmb, Ymb, \
+                                                                            a.coef, R, a.tot + g0)
+      case 1: SP_OWNER_LAUNCH(8192, 2048, 2); break;
+      case 2: SP_OWNER_LAUNCH(4096, 2048, 3); break;
+      case 3: SP_OWNER_LAUNCH(2048, 1024, 4); break;
+      default: SP_OWNER_LAUNCH(4096, 1024, 3); break;
+#undef SP_OWNER_LAUNCH
+    }
+    prof_end(pm);
+    pm = prof_begin(PS_SP_GATHER, st);
     k_sp_gather<<<dim3(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG))), S4_T, 0, st>>>(
         np, M, ypos, R, a.s64, pso);
+    prof_end(pm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -1,0 +1,30 @@
+"""profiles/traffic_<cfg>.json from an ncu --csv launch list with dram__bytes_read.sum / dram__bytes_write.sum:
+per kernel slot of bench.py, the DRAM bytes (read + write) of one launch, averaged over the launches seen.
+
+    python tools/make_traffic.py launches.csv cfg2 > profiles/traffic_cfg2.json
+"""
+import csv
+import json
+import sys
+
+SLOTS = [("k_split3", "split3"), ("k_proj_tc", "project"), ("k_project", "project"), ("k_minmax", "minmax"),
+         ("k_sp_hist", "sp_hist"), ("k_sp_part", "sp_part"), ("k_sp_owner", "sp_owner"), ("k_sp_gather", "sp_gather"),
+         ("k_sortsum", "sortsum_v1"), ("k_plan_D", "plan_D"), ("k_spread", "spread"), ("k_fft_filter", "fft_filter"),
+         ("k_eval", "eval")]
+rows = list(csv.reader(open(sys.argv[1])))
+hdr, per = None, {}
+for r in rows:
+    if r and r[0] == "ID":
+        hdr = r
+        continue
+    if not hdr or len(r) < len(hdr):
+        continue
+    d = dict(zip(hdr, r))
+    slot = next((s for k, s in SLOTS if k in d["Kernel Name"]), None)
+    if slot is None or d["Metric Name"] not in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        continue
+    per.setdefault(slot, {}).setdefault(d["ID"], 0.0)
+    per[slot][d["ID"]] += float(d["Metric Value"].replace(",", ""))
+out = {s: sum(v.values()) / len(v) for s, v in per.items()}
+out["_source"] = f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum ({sys.argv[2]}); bytes per launch, cold L2"
+print(json.dumps(out, indent=1))
