@@ -171,6 +171,9 @@ bool use_tc_projection() {
   return v == 1;
 }
 
+// leading dimension of the slice-major projections Z: a multiple of 4 floats (16-byte rows for TMA stores)
+inline int64_t zld(int64_t N, int64_t M) { return (N + M + 3) / 4 * 4; }
+
 Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb, int d) {
   Layout L;
   size_t o = 0;
@@ -183,7 +186,7 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb,
   L.s64 = take(sizeof(double) * M);
   L.mm = take(sizeof(unsigned) * 4 * nbat);
   if (with_Z) {
-    L.Z = take(sizeof(float) * (N + M) * nbat);
+    L.Z = take(sizeof(float) * zld(N, M) * nbat);
     if (use_tc_projection()) {
       L.xs3 = take(sizeof(uint16_t) * 3 * static_cast<size_t>(sks::proj_tc_dpad(d)) * (N + M));
       L.part = take(sks::proj_tc_part_bytes(nbat));
@@ -440,7 +443,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     sks::ZView zv;
     if (pr.with_Z) {
       float* Z = reinterpret_cast<float*>(ws + L.Z);
-      const int64_t ldz = pr.N + pr.M;
+      const int64_t ldz = zld(pr.N, pr.M);
       ProfScope ps(PS_PROJECT, st);
       if (tc)
         SKS_CUDA(sks::launch_project_tc(ws + L.xs3, pr.N + pr.M, pr.N, pr.d,

@@ -15,6 +15,7 @@
 #include <math_constants.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.h"
@@ -135,7 +136,7 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nk, int64_t L,
               int64_t Nx, int np, const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz,
-              unsigned* __restrict__ mm, int* __restrict__ flag) {
+              unsigned* __restrict__ mm, int* __restrict__ flag, int emode) {
   using SM = TcSmem<BN, STAGES>;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
               : "r"(tbase + static_cast<uint32_t>(c0 + 16)));
         const int nc = min(16, ncols - c0);
+        if (emode == 1) { bad |= (cur[0] == 0x7fc00001u); continue; }   // measurement: TMEM drain only
         const float4* sv = reinterpret_cast<const float4*>(sinv + n0 + c0);
         float sc[16];
 #pragma unroll
@@ -295,6 +297,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           kmn[j] = ok ? key : 0xffffffffu;
           kmx[j] = ok ? key : 0u;
         }
+        if (emode == 2) { bad |= (kmn[0] == 1u); continue; }   // measurement: scale + store only
         uint32_t amn, amx;
         colrange16(kmn, kmx, b4, b3, b2, b1, &amn, &amx);
         uint32_t xmn = amn, xmx = amx;
@@ -427,7 +430,8 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int6
   }
   const int64_t ntiles = ((L + TC_M - 1) / TC_M) * ntn;
   const int grid = static_cast<int>(ntiles < kProjMaxCtas ? ntiles : kProjMaxCtas);
-  k_proj_tc<BN, STAGES><<<grid, TC_THREADS, smem, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag);
+  static const int emode = std::getenv("SKS_PROJ_EMODE") ? std::atoi(std::getenv("SKS_PROJ_EMODE")) : 0;
+  k_proj_tc<BN, STAGES><<<grid, TC_THREADS, smem, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, emode);
   (void)part;
   return cudaGetLastError();
 }
