@@ -73,7 +73,9 @@ typedef struct {
   int32_t window_w;      /* [6]  NFFT window width in grid cells (taps per point), 2..12              */
   int32_t oversample;    /* [2]  NFFT oversampling factor n >= oversample * 2 * (k_max + 1)           */
   int32_t slice_batch;   /* [0 = auto] slices processed per batch (memory bound, Remark P:973-979)   */
-  int32_t reserved;      /* must be 0                                                                 */
+  int32_t engine;        /* [0 = auto] Fourier engine for the Gaussian / Matern: 1 = NFFT (Remark P:519-525),
+                            2 = NDFT on the kept band (the paper's Gaussian engine; at most 32
+                            coefficients, else SKS_ERR_UNSUPPORTED); auto = NFFT (measured faster on B200)  */
 } sks_options;
 
 /* Diagnostic description of the last plan built on this thread (for reports and tests). */
@@ -89,6 +91,8 @@ typedef struct {
   int32_t n_batches;     /* batches in the call                                                         */
   int32_t launches;      /* CUDA kernels launched by the call                                           */
   double tau_min, tau_max;   /* torus scaling range over slices                                         */
+  int32_t engine;        /* Fourier engine used: 0 none, 1 NFFT, 2 NDFT                                  */
+  int32_t band_width;    /* widest kept band k_hi - k_lo + 1 over the slices                             */
 } sks_plan_info;
 
 /* Bytes of DEVICE workspace sks_sum needs for this problem (slice range [p_begin, p_end) of P).

@@ -24,10 +24,14 @@ def _torch():
     return torch
 
 
-def _opts(eps=0.0, window_w=0, oversample=0, slice_batch=0):
-    if not (eps or window_w or oversample or slice_batch):
+ENGINES = {"auto": 0, "nfft": 1, "ndft": 2}
+
+
+def _opts(eps=0.0, window_w=0, oversample=0, slice_batch=0, engine="auto"):
+    e = ENGINES[engine] if isinstance(engine, str) else int(engine)
+    if not (eps or window_w or oversample or slice_batch or e):
         return None
-    return options(eps, window_w, oversample, slice_batch)
+    return options(eps, window_w, oversample, slice_batch, e)
 
 
 def _stream_ptr(stream) -> Optional[int]:

@@ -21,14 +21,15 @@ class sks_kernel(ctypes.Structure):
 
 class sks_options(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("window_w", ctypes.c_int32), ("oversample", ctypes.c_int32),
-                ("slice_batch", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("slice_batch", ctypes.c_int32), ("engine", ctypes.c_int32)]
 
 
 class sks_plan_info(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("n_grid", ctypes.c_int32), ("k_max", ctypes.c_int32),
                 ("band_lo_min", ctypes.c_int32), ("window_w", ctypes.c_int32), ("spread_cells", ctypes.c_int32),
                 ("n_buckets", ctypes.c_int32), ("slice_batch", ctypes.c_int32), ("n_batches", ctypes.c_int32),
-                ("launches", ctypes.c_int32), ("tau_min", ctypes.c_double), ("tau_max", ctypes.c_double)]
+                ("launches", ctypes.c_int32), ("tau_min", ctypes.c_double), ("tau_max", ctypes.c_double),
+                ("engine", ctypes.c_int32), ("band_width", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -88,5 +89,5 @@ def kernel(kind: str, scale: float = 1.0, matern_p: int = 1) -> sks_kernel:
     return sks_kernel(KINDS[kind], int(matern_p), float(scale))
 
 
-def options(eps: float = 0.0, window_w: int = 0, oversample: int = 0, slice_batch: int = 0):
-    return ctypes.pointer(sks_options(float(eps), int(window_w), int(oversample), int(slice_batch), 0))
+def options(eps: float = 0.0, window_w: int = 0, oversample: int = 0, slice_batch: int = 0, engine: int = 0):
+    return ctypes.pointer(sks_options(float(eps), int(window_w), int(oversample), int(slice_batch), int(engine)))

@@ -102,6 +102,7 @@ struct Opts {
   int w = 6;
   int os = 2;
   int batch = 0;
+  int engine = 0;   // Fourier engine: 0 auto (NDFT when the band is narrow), 1 NFFT, 2 NDFT
 };
 
 sks_status resolve_opts(const sks_options* o, Opts* r) {
@@ -114,7 +115,8 @@ sks_status resolve_opts(const sks_options* o, Opts* r) {
     if (d.w < 2 || d.w > 12) return fail(SKS_ERR_INVALID, "window_w must be in [2, 12]");
     if (d.os < 2 || d.os > 16) return fail(SKS_ERR_INVALID, "oversample must be in [2, 16]");
     if (d.batch < 0) return fail(SKS_ERR_INVALID, "slice_batch must be >= 0");
-    if (o->reserved != 0) return fail(SKS_ERR_INVALID, "reserved option field must be 0");
+    d.engine = o->engine;
+    if (d.engine < 0 || d.engine > 2) return fail(SKS_ERR_INVALID, "engine must be 0 (auto), 1 (NFFT) or 2 (NDFT)");
   }
   *r = d;
   return SKS_OK;
@@ -148,7 +150,8 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, ovf = 0, sp = 0, Q = 0, grid = 0,
+  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, ovf = 0, sp = 0, Q = 0, what = 0,
+         grid = 0,
          h = 0, D = 0, fpar = 0, phi = 0, s64 = 0, flag = 0, total = 0;
 };
 
@@ -212,6 +215,7 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb,
     L.fpar = take(sizeof(sks::FPar) * nbat);
     L.phi = take(sizeof(float) * (kNmax / 2 + 1));
     L.Q = take(sizeof(float) * kQmax * (sks::PW_D + 1) * static_cast<size_t>(nbat));
+    L.what = take(sizeof(double) * 2 * 32 * static_cast<size_t>(nbat));
   }
   L.total = o;
   return L;
@@ -325,8 +329,11 @@ sks::PolyWin poly_win(const sks::FourierPlan& plan) {
 }
 
 // Fourier part of one batch: planner (one readback of the ranges), device D_k, spread, FFT filter.
+// Fourier part of one batch.  *ndft_kw = padded band width when the NDFT engine was chosen (rows a5 + a7 by
+// ndft.cu; evaluation is then launch_ndft_eval), 0 for the NFFT (spread + FFT filter here, k_eval later).
 sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView zv, const float* w, int nbat,
-                         char* ws, const Layout& L, cudaStream_t st, sks::FourierPlan* plan, int* launches) {
+                         char* ws, const Layout& L, cudaStream_t st, sks::FourierPlan* plan, int* launches,
+                         int* ndft_kw) {
   void* hbuf = nullptr;
   sks_status s = stage(sizeof(unsigned) * 4 * nbat + 16 + sizeof(sks::FPar) * nbat + sizeof(float) * (kNmax / 2 + 1), &hbuf);
   if (s != SKS_OK) return s;
@@ -352,12 +359,23 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
     return fail(err.rfind("non-finite", 0) == 0 ? SKS_ERR_NONFINITE : SKS_ERR_UNSUPPORTED, err);
   const int n = plan->n;
   sks::FPar* hfp = reinterpret_cast<sks::FPar*>(hflag + 4);
+  int kband = 0;
   for (int p = 0; p < nbat; ++p) {
     const sks::SlicePlan& sp = plan->slices[p];
     hfp[p] = sks::FPar{sp.tau, sp.cen, sp.lmin, (sp.klo << 16) | sp.khi, sp.lminA, 0};
+    kband = std::max(kband, sp.khi - sp.klo + 1);
   }
+  // engine (R6): the NFFT by default; the NDFT on the kept band (the paper's Gaussian engine) on request, for
+  // Gaussian / Matern bands of at most 32 coefficients.  Measured on B200, BJ cfg3 (band of 9): NDFT spread /
+  // eval 389 / 398 us vs NFFT spread / eval 250 / 231 us, so auto keeps the NFFT.
+  const bool smooth = k.kind == SKS_GAUSSIAN || k.kind == SKS_MATERN;
+  int kw = sks::ndft_width(kband);
+  if (o.engine == 2 && (!smooth || kw == 0))
+    return fail(SKS_ERR_UNSUPPORTED, "NDFT engine: Gaussian / Matern with at most 32 kept coefficients only");
+  if (o.engine != 2) kw = 0;
+  *ndft_kw = kw;
   float* hphi = reinterpret_cast<float*>(hfp + nbat);
-  for (int kk = 0; kk <= n / 2; ++kk) hphi[kk] = plan->phi2inv[kk];
+  for (int kk = 0; kk <= n / 2; ++kk) hphi[kk] = kw ? 1.0f : plan->phi2inv[kk];   // NDFT: no window to undo
   SKS_CUDA(cudaMemcpyAsync(ws + L.fpar, hfp, sizeof(sks::FPar) * nbat, cudaMemcpyHostToDevice, st));
   SKS_CUDA(cudaMemcpyAsync(ws + L.phi, hphi, sizeof(float) * (n / 2 + 1), cudaMemcpyHostToDevice, st));
   const sks::FPar* dfp = reinterpret_cast<const sks::FPar*>(ws + L.fpar);
@@ -365,6 +383,18 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
     ProfScope ps(PS_PLAN, st);
     SKS_CUDA(sks::launch_plan_D(dfp, nbat, coeff_const(k, d), reinterpret_cast<const float*>(ws + L.phi), n,
                                 reinterpret_cast<float*>(ws + L.D), st));
+  }
+  if (kw) {
+    {
+      ProfScope ps(PS_AUX, st);
+      SKS_CUDA(sks::launch_zero(ws + L.what, al(sizeof(double) * 2 * 32 * static_cast<size_t>(nbat)), st));
+    }
+    {
+      ProfScope ps(PS_NDFT_SPREAD, st);
+      SKS_CUDA(sks::launch_ndft_spread(zv, w, nbat, dfp, kw, reinterpret_cast<double*>(ws + L.what), st));
+    }
+    *launches += 3;
+    return SKS_OK;
   }
   {
     ProfScope ps(PS_AUX, st);
@@ -460,6 +490,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       SKS_CUDA(sks::launch_minmax(zv, nbat, mm, flag, st));
     }
     launches += 2;
+    int ndft_kw = 0;
     sks::EvalArgs ea{};
     ea.zv = zv;
     ea.np = nbat;
@@ -527,8 +558,11 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ea.tot = sa.tot;
     }
     if (pt.fourier) {
-      sks_status s = fourier_batch(pr.k, pr.d, o, zv, w, nbat, ws, L, st, &plan, &launches);
+      sks_status s = fourier_batch(pr.k, pr.d, o, zv, w, nbat, ws, L, st, &plan, &launches, &ndft_kw);
       if (s != SKS_OK) return s;
+      info.engine = ndft_kw ? 2 : 1;
+      info.band_width = 0;
+      for (const auto& sp : plan.slices) info.band_width = std::max(info.band_width, sp.khi - sp.klo + 1);
       ea.fourier = true;
       ea.fp = reinterpret_cast<const sks::FPar*>(ws + L.fpar);
       ea.h = reinterpret_cast<const float*>(ws + L.h);
@@ -550,7 +584,13 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     ea.s64 = s64;
     ea.per_slice_out = tps;
     ea.accumulate_out = pt.sort;
-    if (pt.fourier || pt.moment) {
+    if (ndft_kw) {   // Gaussian / Matern on the NDFT engine (no moment term)
+      ProfScope ps(PS_NDFT_EVAL, st);
+      SKS_CUDA(sks::launch_ndft_eval(zv, nbat, reinterpret_cast<const sks::FPar*>(ws + L.fpar),
+                                     reinterpret_cast<const float*>(ws + L.D), plan.n / 2 + 1, ndft_kw,
+                                     reinterpret_cast<const double*>(ws + L.what), s64, tps, pt.sort, st));
+      ++launches;
+    } else if (pt.fourier || pt.moment) {
       ProfScope ps(PS_EVAL, st);
       SKS_CUDA(sks::launch_eval(ea, st));
       ++launches;
@@ -571,6 +611,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     if (*static_cast<int*>(hb)) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
   }
   info.path = pt.fourier ? (pt.sort ? 2 : 0) : 1;
+  if (!pt.fourier) info.engine = 0;
   info.window_w = pt.fourier ? o.w : 0;
   info.n_buckets = nb;
   info.slice_batch = batch;
@@ -620,7 +661,8 @@ sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots) {
 }
 
 const char* sks_profile_names(void) {
-  return "split3,project,minmax,sp_hist,sp_part,sp_owner,sp_gather,sortsum_v1,plan_D,spread,fft_filter,eval,aux";
+  return "split3,project,minmax,sp_hist,sp_part,sp_owner,sp_gather,sortsum_v1,plan_D,spread,fft_filter,eval,aux,"
+         "ndft_spread,ndft_eval";
 }
 
 sks_status sks_last_plan(sks_plan_info* info) {

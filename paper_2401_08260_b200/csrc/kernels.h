@@ -8,7 +8,7 @@ namespace sks {
 // opt-in per-launch timing (sks_profile_*, api.cpp): CUDA events around launches, accumulated per slot
 enum ProfSlot {
   PS_SPLIT = 0, PS_PROJECT, PS_MINMAX, PS_SP_HIST, PS_SP_PART, PS_SP_OWNER, PS_SP_GATHER, PS_SORT_V1, PS_PLAN,
-  PS_SPREAD, PS_FFT, PS_EVAL, PS_AUX, PS_N
+  PS_SPREAD, PS_FFT, PS_EVAL, PS_AUX, PS_NDFT_SPREAD, PS_NDFT_EVAL, PS_N
 };
 struct ProfMark {
   int slot;
@@ -145,6 +145,14 @@ cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int 
 // WA cells of the all-points footprint (Q == nullptr: skipped)
 cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, const FPar* fp,
                               const PolyWin& pw, int WA, float* Q, cudaStream_t st);
+
+// rows a5 + a7 by the NDFT on the kept band (ndft.cu; the paper's Gaussian engine): KW = padded band
+// width (8, 16 or 32; ndft_width(K) = 0: too wide), what [np][2 KW] fp64 (zeroed by the caller)
+int ndft_width(int K);
+cudaError_t launch_ndft_spread(ZView zv, const float* w, int np, const FPar* fp, int KW, double* what,
+                               cudaStream_t st);
+cudaError_t launch_ndft_eval(ZView zv, int np, const FPar* fp, const float* D, int nh, int KW, const double* what,
+                             double* s64, float* per_slice_out, bool accumulate_out, cudaStream_t st);
 
 // row a7 (+ Laplacian moment term) + slice accumulation:
 //   per y_m: acc = sum_p [ Fourier interp + mom_coef * tau_p * S_moment ]

@@ -78,6 +78,45 @@ def test_sum_1d_parity(kind, scale, d, N, M, nsl):
         assert err <= TOL[kind], (q, err)
 
 
+@pytest.mark.parametrize("engine", ["nfft", "ndft"])
+@pytest.mark.parametrize("kind,scale,d,N,M,nsl", [c for c in CASES_1D if c[0] in ("gaussian", "matern")])
+def test_sum_1d_engines(kind, scale, d, N, M, nsl, engine):
+    # both Fourier engines (NFFT: Remark P:519-525; NDFT on the kept band: P:508-517) against oracle (b)
+    rng = np.random.default_rng(N + M + d + 1)
+    spread = {3: 1.0, 10: 1.0, 50: 1.0, 100: 2.2, 784: 0.28, 3072: 0.29}[d]
+    zx = (spread * rng.standard_normal((nsl, N))).astype(np.float32)
+    zy = (spread * rng.standard_normal((nsl, M)) - 0.05).astype(np.float32)
+    w = rng.uniform(-1, 1, N).astype(np.float32)
+    try:
+        t = S.sks_sum_1d(dev(zx), dev(zy), dev(w), d, kind, scale, engine=engine).cpu().numpy()
+    except S.SKSError as e:   # NDFT refuses bands wider than 32 coefficients
+        assert engine == "ndft" and e.status == 2, e
+        pytest.skip(f"band too wide for the NDFT: {e}")
+    info = S.sks_last_plan()
+    assert info["engine"] == (2 if engine == "ndft" else 1)
+    for q in range(nsl):
+        ref = O.sum_1d(kind, scale, d, zx[q].astype(np.float64), w.astype(np.float64), zy[q].astype(np.float64))
+        assert rel_err(t[q], ref, w) <= TOL[kind], (q, engine, rel_err(t[q], ref, w))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg5", "paper_gauss", "paper_matern"])
+def test_ndft_engine_end_to_end(name):
+    # Alg. 1 with the NDFT engine on the BASELINE-shaped Gaussian workloads, against oracle (b)
+    size = {"cfg1": {}, "cfg3": dict(N=3000, M=600, P=8), "cfg5": dict(N=20000, M=1000, P=8),
+            "paper_gauss": dict(N=3000, M=600, P=16), "paper_matern": dict(N=3000, M=600, P=16)}[name]
+    cfg = I.scaled(I.CONFIGS[name], **size) if size else I.CONFIGS[name]
+    try:
+        _, got, ref, w, _ = run_cfg(cfg, n_tgt=200, engine="ndft")
+    except S.SKSError as e:
+        assert e.status == 2, e
+        pytest.skip(f"band too wide for the NDFT: {e}")
+    info = S.sks_last_plan()
+    assert info["engine"] == 2 and info["band_width"] <= 32, info
+    assert rel_err(got, ref, w) <= TOL[cfg.kind], rel_err(got, ref, w)
+    run_cfg(cfg, n_tgt=10)
+    assert S.sks_last_plan()["engine"] == 1   # auto = NFFT
+
+
 def test_sum_1d_degenerate_identical_points():
     # all sources at one point (zero range) and targets on top of it / away from it
     N, M = 1000, 300
