@@ -507,7 +507,10 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
       sa.s64 = s64;
       sa.per_slice_out = tps;
-      SKS_CUDA(sks::launch_sortpart(sa, ws + L.sp, st));   // times its own launches (PS_SP_*)
+      {
+        ProfScope ps(PS_SORT, st);   // the whole sort stage (fork .. join); its kernels also time themselves
+        SKS_CUDA(sks::launch_sortpart(sa, ws + L.sp, st));
+      }
       launches += 4 * sks::sortpart_groups(pr.N, pr.M, nbat);
       ea.tot = sa.tot;
     } else if (pt.sort) {
@@ -662,7 +665,7 @@ sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots) {
 
 const char* sks_profile_names(void) {
   return "split3,project,minmax,sp_hist,sp_part,sp_owner,sp_gather,sortsum_v1,plan_D,spread,fft_filter,eval,aux,"
-         "ndft_spread,ndft_eval";
+         "ndft_spread,ndft_eval,sortsum";
 }
 
 sks_status sks_last_plan(sks_plan_info* info) {

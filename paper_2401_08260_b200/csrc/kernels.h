@@ -8,7 +8,7 @@ namespace sks {
 // opt-in per-launch timing (sks_profile_*, api.cpp): CUDA events around launches, accumulated per slot
 enum ProfSlot {
   PS_SPLIT = 0, PS_PROJECT, PS_MINMAX, PS_SP_HIST, PS_SP_PART, PS_SP_OWNER, PS_SP_GATHER, PS_SORT_V1, PS_PLAN,
-  PS_SPREAD, PS_FFT, PS_EVAL, PS_AUX, PS_NDFT_SPREAD, PS_NDFT_EVAL, PS_N
+  PS_SPREAD, PS_FFT, PS_EVAL, PS_AUX, PS_NDFT_SPREAD, PS_NDFT_EVAL, PS_SORT, PS_N
 };
 struct ProfMark {
   int slot;

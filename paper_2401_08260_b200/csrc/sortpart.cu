@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "kernels.h"
 
@@ -602,23 +603,35 @@ SpDims sortpart_dims(int64_t N, int64_t M) {
   return d;
 }
 
-// slices per group (SKS_SORT_GROUP; default: the whole batch).  A small group keeps its mailboxes
-// (8N + 12M bytes per slice) resident in L2 between the partition, owner and gather kernels.
+// The slices are processed in groups, the groups round-robin on SKS_SORT_STREAMS (default 2) streams forked
+// from the caller's stream, each stream with its own scratch region: the four kernels of one group are
+// latency-bound at their phase boundaries, and a second group's kernels fill the idle SMs.
+// Group size: SKS_SORT_GROUP, default ceil(P_batch / streams).
+int sortpart_streams() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SKS_SORT_STREAMS");
+    v = e ? std::atoi(e) : 2;
+    if (v < 1) v = 1;
+    if (v > 4) v = 4;
+  }
+  return v;
+}
+
 int sortpart_group(int64_t N, int64_t M, int np) {
   static int env = -1;
   if (env < 0) {
     const char* e = std::getenv("SKS_SORT_GROUP");
     env = e ? std::max(1, std::atoi(e)) : 0;
   }
-  // measured on B200 (cfg2): groups of 4 / 12 / 48 / all 256 slices: 7.2 / 3.2 / 1.49 / 0.95 ms -- the kernels
-  // are latency-bound, and the per-group tails cost more than the DRAM round trip of the mailboxes saves
-  const int64_t g = env ? env : np;
-  return static_cast<int>(std::min<int64_t>(g, np));
+  (void)N;
+  (void)M;
+  const int64_t g = env ? env : (np + sortpart_streams() - 1) / sortpart_streams();
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, np)));
 }
 
-size_t sortpart_bytes(int64_t N, int64_t M, int np_all) {
+static size_t region_bytes(int64_t N, int64_t M, int np) {
   const SpDims d = sortpart_dims(N, M);
-  const int np = sortpart_group(N, M, np_all);
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   size_t s = 0;
   s += al(sizeof(int) * 2 * d.NH * static_cast<size_t>(np));          // H
@@ -634,18 +647,61 @@ size_t sortpart_bytes(int64_t N, int64_t M, int np_all) {
   return s;
 }
 
+static int active_streams(int64_t N, int64_t M, int np) {
+  const int gs = sortpart_group(N, M, np);
+  return std::min(sortpart_streams(), (np + gs - 1) / gs);
+}
+
+size_t sortpart_bytes(int64_t N, int64_t M, int np) {
+  return region_bytes(N, M, sortpart_group(N, M, np)) * active_streams(N, M, np);
+}
+
+namespace {
+struct StreamPool {
+  cudaStream_t s[4] = {};
+  cudaEvent_t fork = nullptr, join[4] = {};
+  bool ok = false;
+};
+StreamPool& stream_pool() {   // per process (the library is used on one device per process)
+  static std::mutex mu;
+  static StreamPool pool;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pool.ok) {
+    bool good = cudaEventCreateWithFlags(&pool.fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 1; i < 4 && good; ++i)
+      good = cudaStreamCreateWithFlags(&pool.s[i], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&pool.join[i], cudaEventDisableTiming) == cudaSuccess;
+    pool.ok = good;
+  }
+  return pool;
+}
+}  // namespace
+
 cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
   const int64_t N = a.zv.N, M = a.zv.M;
   const SpDims d = sortpart_dims(N, M);
   const int NH = d.NH, G = d.G;
   const int gs = sortpart_group(N, M, a.np);
+  const int ns = active_streams(N, M, a.np);
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-  char* w = static_cast<char*>(ws);
+  StreamPool& pool = stream_pool();
+  if (ns > 1 && !pool.ok) return cudaErrorInitializationError;
+  if (ns > 1) {   // fork: the helper streams start after everything already queued on the caller's stream
+    cudaError_t e = cudaEventRecord(pool.fork, st);
+    if (e != cudaSuccess) return e;
+    for (int i = 1; i < ns; ++i)
+      if ((e = cudaStreamWaitEvent(pool.s[i], pool.fork, 0)) != cudaSuccess) return e;
+  }
+  const size_t rb = region_bytes(N, M, gs);
+  for (int g0 = 0, gi = 0; g0 < a.np; g0 += gs, ++gi) {
+  char* w = static_cast<char*>(ws) + rb * (gi % ns);
+  char* const wbase = w;
+  cudaStream_t sst = (gi % ns) ? pool.s[gi % ns] : st;
   int* H = reinterpret_cast<int*>(w);                 w += al(sizeof(int) * 2 * NH * static_cast<size_t>(gs));
   int* cursor = reinterpret_cast<int*>(w);            w += al(sizeof(int) * 2 * G * static_cast<size_t>(gs));
   int* done = reinterpret_cast<int*>(w);              w += al(sizeof(int) * static_cast<size_t>(gs));
   double* osum = reinterpret_cast<double*>(w);        w += al(sizeof(double) * 4 * G * static_cast<size_t>(gs));
-  const size_t zero_bytes = static_cast<size_t>(w - static_cast<char*>(ws));
+  const size_t zero_bytes = static_cast<size_t>(w - wbase);
   uint16_t* om = reinterpret_cast<uint16_t*>(w);      w += al(sizeof(uint16_t) * NH * static_cast<size_t>(gs));
   SpOwner* own = reinterpret_cast<SpOwner*>(w);       w += al(sizeof(SpOwner) * G * static_cast<size_t>(gs));
   float2* Xmb = reinterpret_cast<float2*>(w);         w += al(sizeof(float2) * N * static_cast<size_t>(gs));
@@ -672,14 +728,15 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
   const int ncx2 = static_cast<int>(cdiv(cdiv(N, S2_CH), cpb)), ncy2 = static_cast<int>(cdiv(cdiv(M, S2_CH), cpb));
   const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1);
   const size_t sm2 = sizeof(float2) * S2_CH + sizeof(int) * 4 * G + sizeof(uint16_t) * (S2_CH + NH);
-  for (int g0 = 0; g0 < a.np; g0 += gs) {
+  {
     const int np = std::min(gs, a.np - g0);
     ZView zv = a.zv;
     zv.zx += g0 * zv.ldx;
     zv.zy += g0 * zv.ldy;
     const unsigned* mm = a.mm + 4 * g0;
     float* pso = a.per_slice_out ? a.per_slice_out + static_cast<int64_t>(g0) * M : nullptr;
-    cudaError_t e = cudaMemsetAsync(ws, 0, zero_bytes, st);
+    cudaStream_t st = sst;
+    cudaError_t e = cudaMemsetAsync(wbase, 0, zero_bytes, st);
     if (e != cudaSuccess) return e;
     ProfMark pm = prof_begin(PS_SP_HIST, st);
     k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, kSpVars[sp_variant()].nbf,
@@ -707,6 +764,14 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
     prof_end(pm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+  }
+  }
+  if (ns > 1) {   // join
+    for (int i = 1; i < ns; ++i) {
+      cudaError_t e = cudaEventRecord(pool.join[i], pool.s[i]);
+      if (e != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(st, pool.join[i], 0)) != cudaSuccess) return e;
+    }
   }
   return cudaSuccess;
 }
