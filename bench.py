@@ -67,7 +67,7 @@ def roofline_model(slot, cfg, P, plan):
     if slot == "split3":        # fp32 points -> 3 bf16 pieces
         return 4 * L * d + 6 * L * dp, 0
     if slot == "project":       # Z = X G^T: read the pieces and G, write Z; 2 L d P fp32-accurate flops
-        return 6 * L * dp + 2 * P * dp + 4 * L * P, 2.0 * L * d * P
+        return 6 * L * dp + 2 * P * dp + 4 * L * P, ("tensor", 2.0 * L * d * P)
     if slot == "sp_hist":       # read every projection
         return 4 * L * P, 0
     if slot == "sp_part":       # read projections and w, write x mailbox (z, w), y mailbox (z) + positions
@@ -80,26 +80,31 @@ def roofline_model(slot, cfg, P, plan):
         return sum(roofline_model(k, cfg, P, plan)[0] for k in ("sp_hist", "sp_part", "sp_owner", "sp_gather")), 0
     if slot == "sortsum_v1":
         return 4 * L * P + 4 * N + 16 * M, 0
-    if slot == "spread":
-        return 4 * N * P + 4 * N + 4 * n * P, 0
+    if slot == "spread":        # per point and slice: w window taps, each a degree-7 Horner (7 FMA) and one FMA
+        w = plan.get("window_w", 6) or 6
+        return 4 * N * P + 4 * N + 4 * n * P, ("alu", 2.0 * N * P * w * 8)
     if slot == "fft_filter":
         return 4 * n * P + 4 * (n // 2 + 1) * P + 4 * n * P, 0
     if slot == "plan_D":
         return 4 * (n // 2 + 1) * P, 0
-    if slot == "eval":          # Fourier interpolation (+ Laplacian moment term)
-        return 4 * M * P + 16 * M + 4 * n * P, 0
+    if slot == "eval":          # Fourier interpolation: one degree-7 Horner per target and slice (+ moment term)
+        return 4 * M * P + 16 * M + 4 * n * P, ("alu", 2.0 * M * P * 7)
     return 0, 0
 
 
 def roofline(slot, cfg, P, plan, ms_per_launch, pk, traffic):
-    """achieved / peak of one kernel: bound = the larger of its HBM time and its tensor time at peak."""
+    """achieved / peak of one kernel: bound = the larger of its HBM time and its arithmetic time at peak
+    (tensor: fp32-accurate BF16x3 = three bf16 MMAs per fp32 product, R2; alu: FP32 FMA pipes)."""
     by, fl = roofline_model(slot, cfg, P, plan)
+    kind, fl = fl if fl else (None, 0.0)
     t = ms_per_launch * 1e-3
-    tensor_peak = pk["bf16_tflops"] / 3.0   # fp32-accurate BF16x3: three bf16 MMAs per fp32 product (R2)
-    if fl and fl / (tensor_peak * 1e12) > by / (pk["hbm_gbs"] * 1e9):
-        r = {"kernel": slot, "bound": "tensor", "achieved": fl / t / 1e12, "peak": tensor_peak, "unit": "TFLOP/s",
-             "peak_source": "MEASURED_PEAKS.json bf16_tflops / 3 (BF16x3 fp32 emulation)",
-             "algorithmic_flops_per_launch": fl}
+    peaks_tf = {"tensor": pk["bf16_tflops"] / 3.0,
+                "alu": 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12}
+    srcs = {"tensor": "MEASURED_PEAKS.json bf16_tflops / 3 (BF16x3 fp32 emulation)",
+            "alu": "148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (MEASURED_PEAKS.json; B200_PROFILING unit counts)"}
+    if fl and fl / (peaks_tf[kind] * 1e12) > by / (pk["hbm_gbs"] * 1e9):
+        r = {"kernel": slot, "bound": kind, "achieved": fl / t / 1e12, "peak": peaks_tf[kind], "unit": "TFLOP/s",
+             "peak_source": srcs[kind], "algorithmic_flops_per_launch": fl}
     else:
         r = {"kernel": slot, "bound": "hbm", "achieved": by / t / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
              "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else ""),

@@ -452,11 +452,16 @@ __device__ __forceinline__ double eval_one(const EvalArgs& a, int p, float z, fl
     const float fr = av - fl;
     float tf = 0.f;
     if (a.Q) {   // one Horner per target on the cell's interpolation polynomial
-      const float* q = a.Q + (static_cast<int64_t>(p) * a.WA + (l0 - f.lminA)) * (PW_D + 1);
-      float acc2 = __ldg(q + PW_D);
-#pragma unroll
-      for (int k = PW_D - 1; k >= 0; --k) acc2 = fmaf(acc2, fr, __ldg(q + k));
-      tf = acc2;
+      static_assert(PW_D == 7, "interpolation polynomials are read as two float4");
+      const float4* q = reinterpret_cast<const float4*>(a.Q + (static_cast<int64_t>(p) * a.WA + (l0 - f.lminA)) * 8);
+      const float4 c0 = __ldg(q), c1 = __ldg(q + 1);
+      float acc2 = fmaf(c1.w, fr, c1.z);
+      acc2 = fmaf(acc2, fr, c1.y);
+      acc2 = fmaf(acc2, fr, c1.x);
+      acc2 = fmaf(acc2, fr, c0.w);
+      acc2 = fmaf(acc2, fr, c0.z);
+      acc2 = fmaf(acc2, fr, c0.y);
+      tf = fmaf(acc2, fr, c0.x);
     } else {
       const float* hp = a.h + static_cast<int64_t>(p) * a.n;
       float tw[12];

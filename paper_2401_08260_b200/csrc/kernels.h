@@ -28,7 +28,7 @@ struct FPar {
 };
 
 // window polynomials: tap j weight p_j(f) = sum_k c[j*(PW_D+1)+k] f^k, f = frac(v - w/2)  (R6)
-constexpr int PW_D = 10;
+constexpr int PW_D = 7;   // == host kPolyDeg; 8 coefficients = two float4
 struct PolyWin {
   int w;
   float c[12 * (PW_D + 1)];
