@@ -75,18 +75,14 @@ __device__ __forceinline__ float2 ldg_cg2(const float2* p) {
 }
 
 // bin coordinate u = (z - xmin) * hscale with explicitly rounded fp32 ops: monotone non-decreasing in z
-__device__ __forceinline__ float ucoord(float z, float xmin, float hscale) {
-  return __fmul_rn(__fsub_rn(z, xmin), hscale);
-}
-// floor(v) clamped to [0, n): monotone; NaN -> 0
-__device__ __forceinline__ int clamp_floor(float v, int n) {
-  const int b = (v >= 0.f) ? static_cast<int>(fminf(v, 2.0e9f)) : 0;
-  return b < n ? b : n - 1;
-}
+// u = z hscale + uoff (uoff = -xmin hscale), one correctly rounded FMA: monotone non-decreasing in z
+__device__ __forceinline__ float ucoord(float z, float uoff, float hscale) { return fmaf(z, hscale, uoff); }
+// floor(v) clamped to [0, n): monotone (saturating truncation; equals floor for v >= 0); NaN -> 0
+__device__ __forceinline__ int clamp_floor(float v, int n) { return min(max(__float2int_rz(v), 0), n - 1); }
 // fine bucket inside an owner: monotone in u (hence in z)
 template <int NBF>
 __device__ __forceinline__ int fine_of(float u, float blo, float fmul) {
-  return clamp_floor(__fmul_rn(__fsub_rn(u, blo), fmul), NBF);
+  return clamp_floor(fmaf(u, fmul, -blo * fmul), NBF);
 }
 
 template <typename T>
@@ -147,19 +143,31 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
   const int i0 = c * S0_CH, i1 = min(n, i0 + S0_CH);
   const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
   const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
+  const float uoff = -xmin * hscale;
   for (int b = tid; b < NH; b += S0_T) hs[b] = 0;
   __syncthreads();
-  constexpr int U = 8;
-  for (int base = i0; base < i1; base += U * S0_T) {
-    float zz[U];
+  // 16-byte loads on the aligned body of the chunk, scalar head / tail
+  const int mis = static_cast<int>((reinterpret_cast<uintptr_t>(z + i0) >> 2) & 3);
+  const int ia = min(i1, i0 + ((4 - mis) & 3)), nv = (i1 - ia) >> 2, ib = ia + 4 * nv;
+  if (tid < ia - i0) atomicAdd(&hs[clamp_floor(ucoord(__ldg(z + i0 + tid), uoff, hscale), NH)], 1);
+  if (tid < i1 - ib) atomicAdd(&hs[clamp_floor(ucoord(__ldg(z + ib + tid), uoff, hscale), NH)], 1);
+  const float4* z4 = reinterpret_cast<const float4*>(z + ia);
+  constexpr int U = 4;
+  for (int base = 0; base < nv; base += U * S0_T) {
+    float4 q[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const int i = base + tid + k * S0_T;
-      zz[k] = (i < i1) ? __ldg(z + i) : 0.f;
+      const int v = base + tid + k * S0_T;
+      q[k] = (v < nv) ? __ldg(z4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int k = 0; k < U; ++k)
-      if (base + tid + k * S0_T < i1) atomicAdd(&hs[clamp_floor(ucoord(zz[k], xmin, hscale), NH)], 1);
+      if (base + tid + k * S0_T < nv) {
+        atomicAdd(&hs[clamp_floor(ucoord(q[k].x, uoff, hscale), NH)], 1);
+        atomicAdd(&hs[clamp_floor(ucoord(q[k].y, uoff, hscale), NH)], 1);
+        atomicAdd(&hs[clamp_floor(ucoord(q[k].z, uoff, hscale), NH)], 1);
+        atomicAdd(&hs[clamp_floor(ucoord(q[k].w, uoff, hscale), NH)], 1);
+      }
   }
   __syncthreads();
   int* Hp = H + (static_cast<int64_t>(p) * 2 + (isx ? 0 : 1)) * NH;
@@ -238,6 +246,7 @@ __global__ void __launch_bounds__(S2_T) k_sp_part(ZView zv, const float* __restr
   const float* z = isx ? zv.zx + p * zv.ldx : zv.zy + p * zv.ldy;
   const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
   const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
+  const float uoff = -xmin * hscale;
   {
     const uint4* src = reinterpret_cast<const uint4*>(om_g + static_cast<int64_t>(p) * NH);   // NH % 8 == 0
     uint4* dst = reinterpret_cast<uint4*>(om);
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(S2_T) k_sp_part(ZView zv, const float* __restr
     for (int k = 0; k < S2_PER; ++k) {
       ow[k] = -1;
       if (i0 + tid + k * S2_T < n) {
-        ow[k] = om[clamp_floor(ucoord(zz[k], xmin, hscale), NH)];
+        ow[k] = om[clamp_floor(ucoord(zz[k], uoff, hscale), NH)];
         rk[k] = atomicAdd(&cnt[ow[k]], 1);
       }
     }
@@ -389,6 +398,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
   if (r.ycnt == 0 && o != 0) return;
   const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
   const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
+  const float uoff = -xmin * hscale;
   // sums over the other owners: lo = owners < o, hi = owners > o (fp64, from the partition kernel)
   {
     const double* os = osum + static_cast<int64_t>(p) * G * 4;
@@ -439,7 +449,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
       for (int k = 0; k < S3_PER; ++k) {
         fr[k] = -1;
         if (tid + k * S3_T < nk) {
-          const int b = fine_of<SP_NBF>(ucoord(zx[k], xmin, hscale), r.blo, r.fmul);
+          const int b = fine_of<SP_NBF>(ucoord(zx[k], uoff, hscale), r.blo, r.fmul);
           fr[k] = (b << 13) | atomicAdd(&S.start[b], 1);   // rank < SP_CAP <= 8192
         }
       }
@@ -520,7 +530,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
         const int i = i0 + tid + k * S3_T;
         if (i >= r.ycnt) continue;
         const float zf = zy[k];
-        const int b = fine_of<SP_NBF>(ucoord(zf, xmin, hscale), r.blo, r.fmul);
+        const int b = fine_of<SP_NBF>(ucoord(zf, uoff, hscale), r.blo, r.fmul);
         const double2 rb = S.rec[b];
         const int j0 = S.start[b], j1 = S.start[b + 1];
         float s0 = 0.f, s1 = 0.f;
