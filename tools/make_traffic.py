@@ -26,5 +26,10 @@ for r in rows:
     per.setdefault(slot, {}).setdefault(d["ID"], 0.0)
     per[slot][d["ID"]] += float(d["Metric Value"].replace(",", ""))
 out = {s: sum(v.values()) / len(v) for s, v in per.items()}
+# the sort stage (bench.py slot "sortsum"): all its kernel launches of one call (groups per call = sp_hist
+# launches / k_finalize launches)
+calls = len({r[0] for r in rows if len(r) > 4 and "k_finalize" in r[4]}) or 1
+if "sp_hist" in per:
+    out["sortsum"] = sum(sum(per[k].values()) for k in ("sp_hist", "sp_part", "sp_owner", "sp_gather") if k in per) / calls
 out["_source"] = f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum ({sys.argv[2]}); bytes per launch, cold L2"
 print(json.dumps(out, indent=1))
