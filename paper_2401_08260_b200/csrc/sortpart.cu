@@ -223,117 +223,82 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
 }
 
 // ---------------------------------------------------------------------------------------------- S2
-// Local counting sort of chunks of one slice part by owner (CPB chunks of S2_CH per CTA).  Shared memory:
-// stage[S2_CH] float2, sown[S2_CH] u16 (owner of each staged slot), om[NH] u16, ooff/cnt/start/gpos [G] ints.
-__global__ void __launch_bounds__(S2_T) k_sp_part(ZView zv, const float* __restrict__ w, const unsigned* __restrict__ mm,
-                                                  int NH, int G, int ncx, int cpb, const uint16_t* __restrict__ om_g,
-                                                  const SpOwner* __restrict__ own, int* __restrict__ cursor,
-                                                  double* __restrict__ osum, float2* __restrict__ Xmb,
-                                                  float* __restrict__ Ymb, int* __restrict__ ypos) {
+// Warp-level partition by owner, no block barriers: a warp takes 256 consecutive elements of a slice part
+// (8 rounds of 32), ranks them per owner with shared-memory counters private to the warp, reserves one run
+// per (warp, owner) in the owner's mailbox region with one global atomic, and stores each element at
+// region + run + rank (runs of ~256/G consecutive slots).  For y it also records, in target order, the
+// mailbox slot (ypos) and the owner (yown).  No sums here: every owner sums its own x (k_sp_owner).
+constexpr int S2W_T = 256, S2W_WARPS = S2W_T / 32, S2W_PER = 8, S2W_WCH = 32 * S2W_PER;
+
+__global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __restrict__ w, const unsigned* __restrict__ mm,
+                                                   int NH, int G, int ncx, int wpc, const uint16_t* __restrict__ om_g,
+                                                   const SpOwner* __restrict__ own, int* __restrict__ cursor,
+                                                   float2* __restrict__ Xmb, float* __restrict__ Ymb,
+                                                   int* __restrict__ ypos, uint16_t* __restrict__ yown) {
   extern __shared__ __align__(16) unsigned char sh2[];
-  float2* stage = reinterpret_cast<float2*>(sh2);                       // [S2_CH]
-  int* ooff = reinterpret_cast<int*>(stage + S2_CH);                   // [G] region start of each owner
-  int* cnt = ooff + G;                                                  // [G]
-  int* start = cnt + G;                                                 // [G]
-  int* gpos = start + G;                                                // [G]
-  uint16_t* sown = reinterpret_cast<uint16_t*>(gpos + G);              // [S2_CH]
-  uint16_t* om = sown + S2_CH;                                          // [NH] (16-byte aligned: G, S2_CH even)
-  __shared__ int wbuf[S2_T / 32 + 1];
+  int* ooff = reinterpret_cast<int*>(sh2);                              // [G] region start of each owner
+  int* cntw = ooff + G;                                                 // [warps][G] per-warp counters / runs
+  uint16_t* om = reinterpret_cast<uint16_t*>(cntw + S2W_WARPS * G);    // [NH]
   const int p = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool isx = static_cast<int>(blockIdx.x) < ncx;
-  const int cb = isx ? blockIdx.x : blockIdx.x - ncx;   // chunk block
+  const int cb = isx ? blockIdx.x : blockIdx.x - ncx;
   const int n = static_cast<int>(isx ? zv.N : zv.M);
   const float* z = isx ? zv.zx + p * zv.ldx : zv.zy + p * zv.ldy;
   const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
   const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
   const float uoff = -xmin * hscale;
   {
-    const uint4* src = reinterpret_cast<const uint4*>(om_g + static_cast<int64_t>(p) * NH);   // NH % 8 == 0
-    uint4* dst = reinterpret_cast<uint4*>(om);
-    for (int b = tid; b < NH / 8; b += S2_T) dst[b] = __ldg(src + b);
+    const uint16_t* omp = om_g + static_cast<int64_t>(p) * NH;
+    for (int b = tid; b < NH; b += S2W_T) om[b] = omp[b];
     const SpOwner* ownp = own + static_cast<int64_t>(p) * G;
-    for (int o = tid; o < G; o += S2_T) ooff[o] = isx ? ownp[o].xoff : ownp[o].yoff;
+    for (int o = tid; o < G; o += S2W_T) ooff[o] = isx ? ownp[o].xoff : ownp[o].yoff;
   }
+  __syncthreads();
+  int* cw = cntw + wid * G;
   int* curp = cursor + static_cast<int64_t>(p) * 2 * G + (isx ? 0 : G);
-  double* osp = osum + static_cast<int64_t>(p) * G * 4;
-  for (int ch = 0; ch < cpb; ++ch) {
-    const int i0 = (cb * cpb + ch) * S2_CH;
-    if (i0 >= n) break;
-    for (int o = tid; o < G; o += S2_T) cnt[o] = 0;
-    float zz[S2_PER], ww[S2_PER];
+  float2* xdst = Xmb + static_cast<int64_t>(p) * zv.N;
+  float* ydst = Ymb + static_cast<int64_t>(p) * zv.M;
+  for (int it = 0; it < wpc; ++it) {
+    const int e0 = ((cb * wpc + it) * S2W_WARPS + wid) * S2W_WCH;   // this warp's 256 elements
+    if (e0 >= n) break;   // warp-uniform
+    for (int o = lane; o < G; o += 32) cw[o] = 0;
+    float zz[S2W_PER], ww[S2W_PER];
 #pragma unroll
-    for (int k = 0; k < S2_PER; ++k) {
-      const int i = i0 + tid + k * S2_T;
+    for (int k = 0; k < S2W_PER; ++k) {
+      const int i = e0 + 32 * k + lane;
       zz[k] = (i < n) ? __ldg(z + i) : 0.f;
       ww[k] = (isx && i < n) ? __ldg(w + i) : 0.f;
     }
-    __syncthreads();
-    int ow[S2_PER], rk[S2_PER];
+    __syncwarp();
+    int ow[S2W_PER], rk[S2W_PER];
 #pragma unroll
-    for (int k = 0; k < S2_PER; ++k) {
+    for (int k = 0; k < S2W_PER; ++k) {
       ow[k] = -1;
-      if (i0 + tid + k * S2_T < n) {
+      if (e0 + 32 * k + lane < n) {
         ow[k] = om[clamp_floor(ucoord(zz[k], uoff, hscale), NH)];
-        rk[k] = atomicAdd(&cnt[ow[k]], 1);
+        rk[k] = atomicAdd(&cw[ow[k]], 1);
       }
     }
-    __syncthreads();
-    {   // exclusive scan of cnt over the owners; reserve this chunk's run in every owner's region
-      const int per = (G + S2_T - 1) / S2_T;
-      const int o0 = min(G, tid * per), o1 = min(G, o0 + per);
-      int loc = 0;
-      for (int o = o0; o < o1; ++o) loc += cnt[o];
-      int total;
-      int r = block_excl_scan<S2_T>(loc, wbuf, &total);
-      for (int o = o0; o < o1; ++o) {
-        start[o] = r;
-        r += cnt[o];
-        gpos[o] = ooff[o] + (cnt[o] ? atomicAdd(curp + o, cnt[o]) : 0);
-      }
+    __syncwarp();
+    for (int o = lane; o < G; o += 32) {   // one run per (warp, owner): counter -> absolute slot of the run
+      const int c = cw[o];
+      cw[o] = c ? ooff[o] + atomicAdd(curp + o, c) : 0;
     }
-    __syncthreads();
+    __syncwarp();
 #pragma unroll
-    for (int k = 0; k < S2_PER; ++k) {
+    for (int k = 0; k < S2W_PER; ++k) {
       if (ow[k] < 0) continue;
-      const int s = start[ow[k]] + rk[k];
-      stage[s] = make_float2(zz[k], ww[k]);
-      sown[s] = static_cast<uint16_t>(ow[k]);
-      // the y's mailbox position, stored in target order (coalesced)
-      if (!isx) ypos[static_cast<int64_t>(p) * zv.M + i0 + tid + k * S2_T] = gpos[ow[k]] + rk[k];
-    }
-    __syncthreads();
-    const int nloc = min(S2_CH, n - i0);
-    for (int s = tid; s < nloc; s += S2_T) {   // staged slots are sorted by owner: runs, coalesced stores
-      const int o = sown[s];
-      const int dst = gpos[o] + (s - start[o]);
-      const float2 e = stage[s];
-      if (isx) Xmb[static_cast<int64_t>(p) * zv.N + dst] = e;
-      else Ymb[static_cast<int64_t>(p) * zv.M + dst] = e.x;
-    }
-    if (isx) {
-      // per-owner fp64 sums (w, w z, w z^2): warp q reduces the runs of owners q, q + 16, ... (coalesced)
-      for (int o = wid; o < G; o += S2_T / 32) {
-        const int c = cnt[o];
-        if (c == 0) continue;
-        double a = 0.0, b = 0.0, cc = 0.0;
-        for (int j = lane; j < c; j += 32) {
-          const float2 e = stage[start[o] + j];
-          const double wz = static_cast<double>(e.y) * e.x;
-          a += e.y;
-          b += wz;
-          cc += wz * e.x;
-        }
-        a = warp_sum_sp(a);
-        b = warp_sum_sp(b);
-        cc = warp_sum_sp(cc);
-        if (lane == 0) {
-          atomicAdd(osp + 4 * o, a);
-          atomicAdd(osp + 4 * o + 1, b);
-          atomicAdd(osp + 4 * o + 2, cc);
-        }
+      const int dst = cw[ow[k]] + rk[k];
+      const int i = e0 + 32 * k + lane;
+      if (isx) {
+        xdst[dst] = make_float2(zz[k], ww[k]);
+      } else {
+        ydst[dst] = zz[k];
+        ypos[static_cast<int64_t>(p) * zv.M + i] = dst;
+        yown[static_cast<int64_t>(p) * zv.M + i] = static_cast<uint16_t>(ow[k]);
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
@@ -345,7 +310,6 @@ struct __align__(16) OwnerShared {
   int start[SP_NBF + 1];      // bucket b holds xs[start[b], start[b+1])
   int wbuf[S3_T / 32 + 1];
   double2 dbuf[S3_T / 32 + 1];
-  double outer[4];            // Alo, Blo, Ahi, Bhi (other owners)
 };
 
 __device__ __forceinline__ double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -385,48 +349,22 @@ __device__ __forceinline__ double2 block_excl_scan_d2(double2 v, double2* wbuf, 
 }
 
 template <int SP_CAP, int SP_NBF, int MINB>
-__global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restrict__ own, const double* __restrict__ osum,
+__global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restrict__ own, double* __restrict__ otot,
                                                       const unsigned* __restrict__ mm, int NH, int G, int64_t N,
                                                       int64_t M, const float2* __restrict__ Xmb,
-                                                      const float* __restrict__ Ymb, double coef, float* __restrict__ R,
-                                                      SliceTot* __restrict__ tot) {
+                                                      const float* __restrict__ Ymb, double coef, float* __restrict__ R) {
   extern __shared__ __align__(16) unsigned char sh3[];
   constexpr int S3_PER = SP_CAP / S3_T;
   OwnerShared<SP_CAP, SP_NBF>& S = *reinterpret_cast<OwnerShared<SP_CAP, SP_NBF>*>(sh3);
   const int o = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
   const SpOwner r = own[static_cast<int64_t>(p) * G + o];
-  if (r.ycnt == 0 && o != 0) return;
+  // every owner publishes its x totals (sum w, sum w z, sum w z^2; fp64) for the other owners' targets
+  // (k_sp_outer), so an owner without targets still sums its x
+  __shared__ double own_tot[3];
+  if (tid < 3) own_tot[tid] = 0.0;
   const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
   const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
   const float uoff = -xmin * hscale;
-  // sums over the other owners: lo = owners < o, hi = owners > o (fp64, from the partition kernel)
-  {
-    const double* os = osum + static_cast<int64_t>(p) * G * 4;
-    double la = 0.0, lb = 0.0, ha = 0.0, hb = 0.0, tc = 0.0;
-    for (int q = tid; q < G; q += S3_T) {
-      const double a = os[4 * q], b = os[4 * q + 1];
-      if (q < o) { la += a; lb += b; }
-      if (q > o) { ha += a; hb += b; }
-      tc += os[4 * q + 2];
-    }
-    la = warp_sum_sp(la); lb = warp_sum_sp(lb); ha = warp_sum_sp(ha); hb = warp_sum_sp(hb); tc = warp_sum_sp(tc);
-    const int lane = tid & 31, wid = tid >> 5;
-    __shared__ double part[5][S3_T / 32];
-    if (lane == 0) { part[0][wid] = la; part[1][wid] = lb; part[2][wid] = ha; part[3][wid] = hb; part[4][wid] = tc; }
-    __syncthreads();
-    if (tid < 5) {
-      double s = 0.0;
-      for (int q = 0; q < S3_T / 32; ++q) s += part[tid][q];
-      if (tid < 4) S.outer[tid] = s;
-      else if (o == 0) {   // slice totals (Laplacian moment term): sum over all owners
-        double a = 0.0, b = 0.0;
-        for (int q = 0; q < S3_T / 32; ++q) { a += part[2][q]; b += part[3][q]; }
-        const double a0 = os[0], b0 = os[1];
-        tot[p] = SliceTot{a + a0, b + b0, s, 0.0};
-      }
-    }
-  }
-  if (r.ycnt == 0) return;   // owner 0 with no targets: only the slice totals
   const float2* xsrc = Xmb + static_cast<int64_t>(p) * N + r.xoff;
   const float* ysrc = Ymb + static_cast<int64_t>(p) * M + r.yoff;
   float* rdst = R + static_cast<int64_t>(p) * M + r.yoff;
@@ -485,12 +423,17 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
     for (int c0 = 0; c0 < SP_NBF; c0 += S3_T) {
       const int b = c0 + tid;
       double2 v = make_double2(0.0, 0.0);
+      double vc = 0.0;
       for (int i = S.start[b], e = S.start[b + 1]; i < e; ++i) {
         const float2 q = S.xs[i];
+        const double wz = static_cast<double>(q.y) * q.x;
         v.x += q.y;
-        v.y += static_cast<double>(q.y) * q.x;
+        v.y += wz;
+        vc += wz * q.x;
       }
       S.rec[b] = v;
+      vc = warp_sum_sp(vc);
+      if ((tid & 31) == 0) atomicAdd(&own_tot[2], vc);
     }
     __syncthreads();
     {
@@ -502,14 +445,17 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
       double2 run = block_excl_scan_d2(loc, S.dbuf, &tch);
 #pragma unroll
       for (int j = 0; j < PB; ++j) { S.rec[tid * PB + j] = run; run = run + v[j]; }
-      if (tid == 0) S.rec[SP_NBF] = tch;
+      if (tid == 0) {
+        S.rec[SP_NBF] = tch;
+        own_tot[0] += tch.x;
+        own_tot[1] += tch.y;
+      }
     }
     __syncthreads();
     // ---- targets of this owner, all lookups in shared memory:
     //   sum_n w|x - z| = z(2A_b - A) - 2B_b + B + 2 sum_{x in b, x < z} w (z - x) + [other owners]
-    const double dA = S.outer[0] - S.outer[2], dB = S.outer[3] - S.outer[1];   // z(Alo - Ahi) + (Bhi - Blo)
     const double2 Tp = S.rec[SP_NBF];
-    constexpr int YB = 8;   // targets per thread per batch; the next batch's loads are issued first
+    constexpr int YB = MINB >= 3 ? 4 : 8;   // targets per thread per batch (register budget); next batch loads first
     float zn[YB];
 #pragma unroll
     for (int k = 0; k < YB; ++k) {
@@ -545,8 +491,8 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
           s0 = fmaf(q.y, fmaxf(zf - q.x, 0.f), s0);
         }
         const double zd = zf;
-        double v = zd * (2.0 * rb.x - Tp.x) - 2.0 * rb.y + Tp.y + 2.0 * static_cast<double>(s0 + s1);
-        if (pass == 0) v += zd * dA + dB;
+        // this owner's part only; the other owners' part is added in k_sp_gather (k_sp_outer's table)
+        const double v = zd * (2.0 * rb.x - Tp.x) - 2.0 * rb.y + Tp.y + 2.0 * static_cast<double>(s0 + s1);
         const float t = static_cast<float>(-coef * v);
         if (pass == 0) rdst[i] = t;
         else rdst[i] += t;
@@ -554,36 +500,102 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
     }
     __syncthreads();
   }
+  if (tid == 0) {   // publish this owner's x totals (the last pass ended with a barrier)
+    double* ot = otot + (static_cast<int64_t>(p) * G + o) * 4;
+    ot[0] = own_tot[0];
+    ot[1] = own_tot[1];
+    ot[2] = own_tot[2];
+  }
 }
 
 // ---------------------------------------------------------------------------------------------- S4
-__global__ void __launch_bounds__(S4_T) k_sp_gather(int np, int64_t M, const int* __restrict__ ypos,
-                                                    const float* __restrict__ R, double* __restrict__ s64,
+// Per slice: the other owners' part of every target's sum.  For a target of owner o, the x of owners < o lie
+// below it and those of owners > o above it: sum w |x - z| over them = z (Alo - Ahi) + (Bhi - Blo).
+// dab[p][o] = (Alo - Ahi, Bhi - Blo) from the owners' fp64 totals; slice totals for the Laplacian moment term.
+constexpr int SO_T = 256;
+
+__global__ void __launch_bounds__(SO_T) k_sp_outer(const double* __restrict__ otot, int G, double2* __restrict__ dab,
+                                                   SliceTot* __restrict__ tot) {
+  __shared__ double wsc[3][SO_T / 32 + 1];
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double* ot = otot + static_cast<int64_t>(p) * G * 4;
+  double carryA = 0.0, carryB = 0.0, carryC = 0.0;
+  // totals first (two sweeps keep the code simple; G is small)
+  for (int o0 = 0; o0 < G; o0 += SO_T) {
+    const int o = o0 + tid;
+    double a = 0.0, b = 0.0, c = 0.0;
+    if (o < G) { a = ot[4 * o]; b = ot[4 * o + 1]; c = ot[4 * o + 2]; }
+    a = warp_sum_sp(a); b = warp_sum_sp(b); c = warp_sum_sp(c);
+    if (lane == 0) { wsc[0][wid] = a; wsc[1][wid] = b; wsc[2][wid] = c; }
+    __syncthreads();
+    if (tid == 0)
+      for (int q = 0; q < SO_T / 32; ++q) { carryA += wsc[0][q]; carryB += wsc[1][q]; carryC += wsc[2][q]; }
+    __syncthreads();
+  }
+  __shared__ double TA, TB;
+  if (tid == 0) { TA = carryA; TB = carryB; tot[p] = SliceTot{carryA, carryB, carryC, 0.0}; }
+  __syncthreads();
+  const double A = TA, B = TB;
+  double runA = 0.0, runB = 0.0;   // exclusive prefix over owner chunks
+  for (int o0 = 0; o0 < G; o0 += SO_T) {
+    const int o = o0 + tid;
+    double a = 0.0, b = 0.0;
+    if (o < G) { a = ot[4 * o]; b = ot[4 * o + 1]; }
+    double ia = warp_incl_scan_sp(a), ib = warp_incl_scan_sp(b);
+    if (lane == 31) { wsc[0][wid] = ia; wsc[1][wid] = ib; }
+    __syncthreads();
+    double wa = 0.0, wb = 0.0, ta = 0.0, tb = 0.0;
+    for (int q = 0; q < SO_T / 32; ++q) {
+      if (q < wid) { wa += wsc[0][q]; wb += wsc[1][q]; }
+      ta += wsc[0][q];
+      tb += wsc[1][q];
+    }
+    const double alo = runA + wa + ia - a, blo = runB + wb + ib - b;   // owners < o
+    if (o < G) dab[static_cast<int64_t>(p) * G + o] = make_double2(alo - (A - alo - a), (B - blo - b) - blo);
+    runA += ta;
+    runB += tb;
+    __syncthreads();
+  }
+}
+
+// Back to target order: t = R[ypos] (own owner) - coef (z dA + dB) (other owners), accumulated over a slice
+// group in fp64 registers, one coalesced atomic per target (or per-slice stores for sks_sum_1d).
+__global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, double coef, const int* __restrict__ ypos,
+                                                    const uint16_t* __restrict__ yown, const float* __restrict__ R,
+                                                    const double2* __restrict__ dab, double* __restrict__ s64,
                                                     float* __restrict__ per_slice_out) {
+  const int64_t M = zv.M;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * S4_CH + threadIdx.x;
   const int p0 = blockIdx.y * S4_SG, p1 = min(np, p0 + S4_SG);
   double acc[S4_PER];
 #pragma unroll
   for (int k = 0; k < S4_PER; ++k) acc[k] = 0.0;
   for (int p = p0; p < p1; ++p) {
-    int q[S4_PER];
+    int q[S4_PER], ow[S4_PER];
+    float z[S4_PER];
 #pragma unroll
     for (int k = 0; k < S4_PER; ++k) {
       const int64_t m = m0 + k * S4_T;
-      q[k] = (m < M) ? __ldcs(ypos + static_cast<int64_t>(p) * M + m) : 0;
+      const bool ok = m < M;
+      q[k] = ok ? __ldcs(ypos + static_cast<int64_t>(p) * M + m) : 0;
+      ow[k] = ok ? yown[static_cast<int64_t>(p) * M + m] : 0;
+      z[k] = ok ? __ldg(zv.zy + p * zv.ldy + m) : 0.f;
     }
     float t[S4_PER];
+    double2 d[S4_PER];
 #pragma unroll
     for (int k = 0; k < S4_PER; ++k) {
       const int64_t m = m0 + k * S4_T;
       t[k] = (m < M) ? __ldcs(R + static_cast<int64_t>(p) * M + q[k]) : 0.f;
+      d[k] = (m < M) ? __ldg(dab + static_cast<int64_t>(p) * G + ow[k]) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int k = 0; k < S4_PER; ++k) {
       const int64_t m = m0 + k * S4_T;
       if (m >= M) continue;
-      acc[k] += t[k];
-      if (per_slice_out) per_slice_out[static_cast<int64_t>(p) * M + m] = t[k];
+      const double tt = static_cast<double>(t[k]) - coef * (static_cast<double>(z[k]) * d[k].x + d[k].y);
+      acc[k] += tt;
+      if (per_slice_out) per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(tt);
     }
   }
   if (s64)
@@ -647,7 +659,9 @@ static size_t region_bytes(int64_t N, int64_t M, int np) {
   s += al(sizeof(int) * 2 * d.NH * static_cast<size_t>(np));          // H
   s += al(sizeof(int) * 2 * d.G * static_cast<size_t>(np));           // cursors
   s += al(sizeof(int) * static_cast<size_t>(np));                     // done tickets
-  s += al(sizeof(double) * 4 * d.G * static_cast<size_t>(np));        // owner sums
+  s += al(sizeof(double) * 4 * d.G * static_cast<size_t>(np));        // owner totals
+  s += al(sizeof(double2) * d.G * static_cast<size_t>(np));           // other-owner coefficients
+  s += al(sizeof(uint16_t) * M * static_cast<size_t>(np));            // y owners
   s += al(sizeof(uint16_t) * d.NH * static_cast<size_t>(np));         // owner map
   s += al(sizeof(SpOwner) * d.G * static_cast<size_t>(np));           // owners
   s += al(sizeof(float2) * N * static_cast<size_t>(np));              // x mailbox
@@ -710,8 +724,10 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
   int* H = reinterpret_cast<int*>(w);                 w += al(sizeof(int) * 2 * NH * static_cast<size_t>(gs));
   int* cursor = reinterpret_cast<int*>(w);            w += al(sizeof(int) * 2 * G * static_cast<size_t>(gs));
   int* done = reinterpret_cast<int*>(w);              w += al(sizeof(int) * static_cast<size_t>(gs));
-  double* osum = reinterpret_cast<double*>(w);        w += al(sizeof(double) * 4 * G * static_cast<size_t>(gs));
   const size_t zero_bytes = static_cast<size_t>(w - wbase);
+  double* otot = reinterpret_cast<double*>(w);        w += al(sizeof(double) * 4 * G * static_cast<size_t>(gs));
+  double2* dab = reinterpret_cast<double2*>(w);       w += al(sizeof(double2) * G * static_cast<size_t>(gs));
+  uint16_t* yown = reinterpret_cast<uint16_t*>(w);    w += al(sizeof(uint16_t) * M * static_cast<size_t>(gs));
   uint16_t* om = reinterpret_cast<uint16_t*>(w);      w += al(sizeof(uint16_t) * NH * static_cast<size_t>(gs));
   SpOwner* own = reinterpret_cast<SpOwner*>(w);       w += al(sizeof(SpOwner) * G * static_cast<size_t>(gs));
   float2* Xmb = reinterpret_cast<float2*>(w);         w += al(sizeof(float2) * N * static_cast<size_t>(gs));
@@ -733,11 +749,12 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
                          static_cast<int>(sizeof(OwnerShared<2048, 1024>)));
     attr = true;
   }
-  constexpr int cpb = 4;   // partition chunks per CTA
+  constexpr int wpc = 4;   // partition: 256-element rounds per warp
   const int ncx0 = static_cast<int>(cdiv(N, S0_CH)), ncy0 = static_cast<int>(cdiv(M, S0_CH));
-  const int ncx2 = static_cast<int>(cdiv(cdiv(N, S2_CH), cpb)), ncy2 = static_cast<int>(cdiv(cdiv(M, S2_CH), cpb));
+  const int64_t per_cta2 = int64_t(S2W_WARPS) * S2W_WCH * wpc;
+  const int ncx2 = static_cast<int>(cdiv(N, per_cta2)), ncy2 = static_cast<int>(cdiv(M, per_cta2));
   const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1);
-  const size_t sm2 = sizeof(float2) * S2_CH + sizeof(int) * 4 * G + sizeof(uint16_t) * (S2_CH + NH);
+  const size_t sm2 = sizeof(int) * (1 + S2W_WARPS) * G + sizeof(uint16_t) * NH;
   {
     const int np = std::min(gs, a.np - g0);
     ZView zv = a.zv;
@@ -753,14 +770,14 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
                                                          H, done, om, own);
     prof_end(pm);
     pm = prof_begin(PS_SP_PART, st);
-    k_sp_part<<<dim3(ncx2 + ncy2, np), S2_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, cpb, om, own, cursor, osum, Xmb,
-                                                         Ymb, ypos);
+    k_sp_part<<<dim3(ncx2 + ncy2, np), S2W_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, wpc, om, own, cursor, Xmb, Ymb,
+                                                          ypos, yown);
     prof_end(pm);
     pm = prof_begin(PS_SP_OWNER, st);
     switch (sp_variant()) {
 #define SP_OWNER_LAUNCH(C, B, MB)                                                                                  \
-  k_sp_owner<C, B, MB><<<dim3(G, np), S3_T, sizeof(OwnerShared<C, B>), st>>>(own, osum, mm, NH, G, N, M, Xmb, Ymb, \
-                                                                            a.coef, R, a.tot + g0)
+  k_sp_owner<C, B, MB><<<dim3(G, np), S3_T, sizeof(OwnerShared<C, B>), st>>>(own, otot, mm, NH, G, N, M, Xmb, Ymb, \
+                                                                            a.coef, R)
       case 1: SP_OWNER_LAUNCH(8192, 2048, 2); break;
       case 2: SP_OWNER_LAUNCH(4096, 2048, 3); break;
       case 3: SP_OWNER_LAUNCH(2048, 1024, 4); break;
@@ -769,8 +786,9 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
     }
     prof_end(pm);
     pm = prof_begin(PS_SP_GATHER, st);
+    k_sp_outer<<<np, SO_T, 0, st>>>(otot, G, dab, a.tot + g0);
     k_sp_gather<<<dim3(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG))), S4_T, 0, st>>>(
-        np, M, ypos, R, a.s64, pso);
+        zv, np, G, a.coef, ypos, yown, R, dab, a.s64, pso);
     prof_end(pm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
