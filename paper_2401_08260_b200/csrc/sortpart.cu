@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __rest
   extern __shared__ __align__(16) unsigned char sh2[];
   int* ooff = reinterpret_cast<int*>(sh2);                              // [G] region start of each owner
   int* cntw = ooff + G;                                                 // [warps][G] per-warp counters / runs
-  uint16_t* om = reinterpret_cast<uint16_t*>(cntw + S2W_WARPS * G);    // [NH]
+  uint16_t* om = reinterpret_cast<uint16_t*>(ooff + ((1 + S2W_WARPS) * G + 3) / 4 * 4);   // [NH], 16-B aligned
   const int p = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool isx = static_cast<int>(blockIdx.x) < ncx;
   const int cb = isx ? blockIdx.x : blockIdx.x - ncx;
@@ -248,8 +248,9 @@ __global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __rest
   const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
   const float uoff = -xmin * hscale;
   {
-    const uint16_t* omp = om_g + static_cast<int64_t>(p) * NH;
-    for (int b = tid; b < NH; b += S2W_T) om[b] = omp[b];
+    const uint4* src = reinterpret_cast<const uint4*>(om_g + static_cast<int64_t>(p) * NH);   // NH % 8 == 0
+    uint4* dst = reinterpret_cast<uint4*>(om);
+    for (int b = tid; b < NH / 8; b += S2W_T) dst[b] = __ldg(src + b);
     const SpOwner* ownp = own + static_cast<int64_t>(p) * G;
     for (int o = tid; o < G; o += S2W_T) ooff[o] = isx ? ownp[o].xoff : ownp[o].yoff;
   }
@@ -754,7 +755,7 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
   const int64_t per_cta2 = int64_t(S2W_WARPS) * S2W_WCH * wpc;
   const int ncx2 = static_cast<int>(cdiv(N, per_cta2)), ncy2 = static_cast<int>(cdiv(M, per_cta2));
   const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1);
-  const size_t sm2 = sizeof(int) * (1 + S2W_WARPS) * G + sizeof(uint16_t) * NH;
+  const size_t sm2 = sizeof(int) * (((1 + S2W_WARPS) * G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
   {
     const int np = std::min(gs, a.np - g0);
     ZView zv = a.zv;
