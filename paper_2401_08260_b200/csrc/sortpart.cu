@@ -40,19 +40,20 @@ namespace {
 
 constexpr int S0_T = 512, S0_CH = 16384;      // histogram: elements per CTA
 constexpr int S2_T = 512, S2_PER = 8, S2_CH = S2_T * S2_PER;   // partition: elements per CTA
-constexpr int S3_T = 512;   // owner kernel threads
-// owner kernel variants (x capacity, fine buckets, CTAs per SM): SKS_SP_VARIANT selects (measurement aid).
-// Measured on B200, cfg2 sp_owner: {4096,2048,3} 418 us, {8192,2048,2} 438, {4096,1024,3} 374, {2048,1024,4} 465.
+// owner kernel variants (x capacity, fine buckets, CTAs per SM, threads): SKS_SP_VARIANT selects (measurement
+// aid).  Measured on B200, cfg2 sp_owner (one stream): {4096,1024,3,512} 358 us (default), {8192,2048,2,512} 438,
+// {4096,1024,4,256} 389, {2048,1024,4,512} 465, {4096,1024,2,512} 401; finer buckets {4096,2048,3,512} 418.
 struct SpVar {
-  int cap, nbf, minb;
+  int cap, nbf, minb, nt;
 };
-constexpr SpVar kSpVars[] = {{4096, 1024, 3}, {8192, 2048, 2}, {4096, 2048, 3}, {2048, 1024, 4}};
+constexpr SpVar kSpVars[] = {{4096, 1024, 3, 512}, {8192, 2048, 2, 512}, {4096, 1024, 4, 256}, {2048, 1024, 4, 512},
+                             {4096, 1024, 2, 512}};
 int sp_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("SKS_SP_VARIANT");
     v = e ? std::atoi(e) : 0;
-    if (v < 0 || v > 3) v = 0;
+    if (v < 0 || v > 4) v = 0;
   }
   return v;
 }
@@ -304,13 +305,13 @@ __global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __rest
 }
 
 // ---------------------------------------------------------------------------------------------- S3
-template <int SP_CAP, int SP_NBF>
+template <int SP_CAP, int SP_NBF, int NT>
 struct __align__(16) OwnerShared {
   float2 xs[SP_CAP];          // the pass's x (z, w) in fine-bucket order
   double2 rec[SP_NBF + 1];    // exclusive prefix (sum w, sum w x) over the pass's buckets; [NBF] = pass totals
   int start[SP_NBF + 1];      // bucket b holds xs[start[b], start[b+1])
-  int wbuf[S3_T / 32 + 1];
-  double2 dbuf[S3_T / 32 + 1];
+  int wbuf[NT / 32 + 1];
+  double2 dbuf[NT / 32 + 1];
 };
 
 __device__ __forceinline__ double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -319,10 +320,11 @@ __device__ __forceinline__ double2 shfl_up_d2(double2 v, int d) {
   return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
 }
 
-// exclusive block scan of a double2 per thread (S3_T threads)
+// exclusive block scan of a double2 per thread (NT threads)
+template <int NT>
 __device__ __forceinline__ double2 block_excl_scan_d2(double2 v, double2* wbuf, double2* total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  constexpr int NW = S3_T / 32;
+  constexpr int NW = NT / 32;
   double2 inc = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -349,14 +351,14 @@ __device__ __forceinline__ double2 block_excl_scan_d2(double2 v, double2* wbuf, 
   return r;
 }
 
-template <int SP_CAP, int SP_NBF, int MINB>
+template <int SP_CAP, int SP_NBF, int MINB, int S3_T>
 __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restrict__ own, double* __restrict__ otot,
                                                       const unsigned* __restrict__ mm, int NH, int G, int64_t N,
                                                       int64_t M, const float2* __restrict__ Xmb,
                                                       const float* __restrict__ Ymb, double coef, float* __restrict__ R) {
   extern __shared__ __align__(16) unsigned char sh3[];
   constexpr int S3_PER = SP_CAP / S3_T;
-  OwnerShared<SP_CAP, SP_NBF>& S = *reinterpret_cast<OwnerShared<SP_CAP, SP_NBF>*>(sh3);
+  OwnerShared<SP_CAP, SP_NBF, S3_T>& S = *reinterpret_cast<OwnerShared<SP_CAP, SP_NBF, S3_T>*>(sh3);
   const int o = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
   const SpOwner r = own[static_cast<int64_t>(p) * G + o];
   // every owner publishes its x totals (sum w, sum w z, sum w z^2; fp64) for the other owners' targets
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
 #pragma unroll
       for (int j = 0; j < PB; ++j) { v[j] = S.rec[tid * PB + j]; loc = loc + v[j]; }
       double2 tch;
-      double2 run = block_excl_scan_d2(loc, S.dbuf, &tch);
+      double2 run = block_excl_scan_d2<S3_T>(loc, S.dbuf, &tch);
 #pragma unroll
       for (int j = 0; j < PB; ++j) { S.rec[tid * PB + j] = run; run = run + v[j]; }
       if (tid == 0) {
@@ -740,14 +742,15 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
   if (!attr) {
     cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sp_owner<4096, 2048, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(OwnerShared<4096, 2048>)));
-    cudaFuncSetAttribute(k_sp_owner<8192, 2048, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(OwnerShared<8192, 2048>)));
-    cudaFuncSetAttribute(k_sp_owner<4096, 1024, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(OwnerShared<4096, 1024>)));
-    cudaFuncSetAttribute(k_sp_owner<2048, 1024, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(OwnerShared<2048, 1024>)));
+#define SP_OWNER_ATTR(C, B, MB, T)                                                                              \
+  cudaFuncSetAttribute(k_sp_owner<C, B, MB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
+                       static_cast<int>(sizeof(OwnerShared<C, B, T>)))
+    SP_OWNER_ATTR(4096, 1024, 3, 512);
+    SP_OWNER_ATTR(8192, 2048, 2, 512);
+    SP_OWNER_ATTR(4096, 1024, 4, 256);
+    SP_OWNER_ATTR(2048, 1024, 4, 512);
+    SP_OWNER_ATTR(4096, 1024, 2, 512);
+#undef SP_OWNER_ATTR
     attr = true;
   }
   constexpr int wpc = 4;   // partition: 256-element rounds per warp
@@ -776,13 +779,14 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
     prof_end(pm);
     pm = prof_begin(PS_SP_OWNER, st);
     switch (sp_variant()) {
-#define SP_OWNER_LAUNCH(C, B, MB)                                                                                  \
-  k_sp_owner<C, B, MB><<<dim3(G, np), S3_T, sizeof(OwnerShared<C, B>), st>>>(own, otot, mm, NH, G, N, M, Xmb, Ymb, \
-                                                                            a.coef, R)
-      case 1: SP_OWNER_LAUNCH(8192, 2048, 2); break;
-      case 2: SP_OWNER_LAUNCH(4096, 2048, 3); break;
-      case 3: SP_OWNER_LAUNCH(2048, 1024, 4); break;
-      default: SP_OWNER_LAUNCH(4096, 1024, 3); break;
+#define SP_OWNER_LAUNCH(C, B, MB, T)                                                                            \
+  k_sp_owner<C, B, MB, T><<<dim3(G, np), T, sizeof(OwnerShared<C, B, T>), st>>>(own, otot, mm, NH, G, N, M, Xmb, \
+                                                                               Ymb, a.coef, R)
+      case 1: SP_OWNER_LAUNCH(8192, 2048, 2, 512); break;
+      case 2: SP_OWNER_LAUNCH(4096, 1024, 4, 256); break;
+      case 3: SP_OWNER_LAUNCH(2048, 1024, 4, 512); break;
+      case 4: SP_OWNER_LAUNCH(4096, 1024, 2, 512); break;
+      default: SP_OWNER_LAUNCH(4096, 1024, 3, 512); break;
 #undef SP_OWNER_LAUNCH
     }
     prof_end(pm);
