@@ -39,7 +39,6 @@ namespace sks {
 namespace {
 
 constexpr int S0_T = 512, S0_CH = 16384;      // histogram: elements per CTA
-constexpr int S2_T = 512, S2_PER = 8, S2_CH = S2_T * S2_PER;   // partition: elements per CTA
 // owner kernel variants (x capacity, fine buckets, CTAs per SM, threads): SKS_SP_VARIANT selects (measurement
 // aid).  Measured on B200, cfg2 sp_owner (one stream): {4096,1024,3,512} 358 us (default), {8192,2048,2,512} 438,
 // {4096,1024,4,256} 389, {2048,1024,4,512} 465, {4096,1024,2,512} 401; finer buckets {4096,2048,3,512} 418.
@@ -704,107 +703,131 @@ StreamPool& stream_pool() {   // per process (the library is used on one device 
 }
 }  // namespace
 
-cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
-  const int64_t N = a.zv.N, M = a.zv.M;
-  const SpDims d = sortpart_dims(N, M);
-  const int NH = d.NH, G = d.G;
-  const int gs = sortpart_group(N, M, a.np);
-  const int ns = active_streams(N, M, a.np);
-  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-  StreamPool& pool = stream_pool();
-  if (ns > 1 && !pool.ok) return cudaErrorInitializationError;
-  if (ns > 1) {   // fork: the helper streams start after everything already queued on the caller's stream
-    cudaError_t e = cudaEventRecord(pool.fork, st);
-    if (e != cudaSuccess) return e;
-    for (int i = 1; i < ns; ++i)
-      if ((e = cudaStreamWaitEvent(pool.s[i], pool.fork, 0)) != cudaSuccess) return e;
-  }
-  const size_t rb = region_bytes(N, M, gs);
-  for (int g0 = 0, gi = 0; g0 < a.np; g0 += gs, ++gi) {
-  char* w = static_cast<char*>(ws) + rb * (gi % ns);
-  char* const wbase = w;
-  cudaStream_t sst = (gi % ns) ? pool.s[gi % ns] : st;
-  int* H = reinterpret_cast<int*>(w);                 w += al(sizeof(int) * 2 * NH * static_cast<size_t>(gs));
-  int* cursor = reinterpret_cast<int*>(w);            w += al(sizeof(int) * 2 * G * static_cast<size_t>(gs));
-  int* done = reinterpret_cast<int*>(w);              w += al(sizeof(int) * static_cast<size_t>(gs));
-  const size_t zero_bytes = static_cast<size_t>(w - wbase);
-  double* otot = reinterpret_cast<double*>(w);        w += al(sizeof(double) * 4 * G * static_cast<size_t>(gs));
-  double2* dab = reinterpret_cast<double2*>(w);       w += al(sizeof(double2) * G * static_cast<size_t>(gs));
-  uint16_t* yown = reinterpret_cast<uint16_t*>(w);    w += al(sizeof(uint16_t) * M * static_cast<size_t>(gs));
-  uint16_t* om = reinterpret_cast<uint16_t*>(w);      w += al(sizeof(uint16_t) * NH * static_cast<size_t>(gs));
-  SpOwner* own = reinterpret_cast<SpOwner*>(w);       w += al(sizeof(SpOwner) * G * static_cast<size_t>(gs));
-  float2* Xmb = reinterpret_cast<float2*>(w);         w += al(sizeof(float2) * N * static_cast<size_t>(gs));
-  float* Ymb = reinterpret_cast<float*>(w);           w += al(sizeof(float) * M * static_cast<size_t>(gs));
-  float* R = reinterpret_cast<float*>(w);             w += al(sizeof(float) * M * static_cast<size_t>(gs));
-  int* ypos = reinterpret_cast<int*>(w);
+namespace {
+// scratch of one slice group (one region per stream; regions are reused by the groups of that stream)
+struct SpRegion {
+  int* H;           // [gs][2][NH] histograms           } zeroed per group
+  int* cursor;      // [gs][2][G] mailbox cursors       }
+  int* done;        // [gs] histogram tickets           }
+  size_t zero_bytes;
+  double* otot;     // [gs][G][4] owner totals (w, w z, w z^2)
+  double2* dab;     // [gs][G] other-owner coefficients
+  uint16_t* yown;   // [gs][M] owner of each target
+  uint16_t* om;     // [gs][NH] owner of each bin
+  SpOwner* own;     // [gs][G]
+  float2* Xmb;      // [gs][N] x mailbox (z, w)
+  float* Ymb;       // [gs][M] y mailbox (z)
+  float* R;         // [gs][M] own-owner part of t, mailbox order
+  int* ypos;        // [gs][M] mailbox slot of each target
+};
 
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+SpRegion carve_region(char* base, int64_t N, int64_t M, int NH, int G, int gs) {
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t g = static_cast<size_t>(gs);
+  SpRegion r;
+  char* w = base;
+  r.H = reinterpret_cast<int*>(w);            w += al(sizeof(int) * 2 * NH * g);
+  r.cursor = reinterpret_cast<int*>(w);       w += al(sizeof(int) * 2 * G * g);
+  r.done = reinterpret_cast<int*>(w);         w += al(sizeof(int) * g);
+  r.zero_bytes = static_cast<size_t>(w - base);
+  r.otot = reinterpret_cast<double*>(w);      w += al(sizeof(double) * 4 * G * g);
+  r.dab = reinterpret_cast<double2*>(w);      w += al(sizeof(double2) * G * g);
+  r.yown = reinterpret_cast<uint16_t*>(w);    w += al(sizeof(uint16_t) * M * g);
+  r.om = reinterpret_cast<uint16_t*>(w);      w += al(sizeof(uint16_t) * NH * g);
+  r.own = reinterpret_cast<SpOwner*>(w);      w += al(sizeof(SpOwner) * G * g);
+  r.Xmb = reinterpret_cast<float2*>(w);       w += al(sizeof(float2) * N * g);
+  r.Ymb = reinterpret_cast<float*>(w);        w += al(sizeof(float) * M * g);
+  r.R = reinterpret_cast<float*>(w);          w += al(sizeof(float) * M * g);
+  r.ypos = reinterpret_cast<int*>(w);
+  return r;
+}
+
+void set_attributes() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 #define SP_OWNER_ATTR(C, B, MB, T)                                                                              \
   cudaFuncSetAttribute(k_sp_owner<C, B, MB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
                        static_cast<int>(sizeof(OwnerShared<C, B, T>)))
-    SP_OWNER_ATTR(4096, 1024, 3, 512);
-    SP_OWNER_ATTR(8192, 2048, 2, 512);
-    SP_OWNER_ATTR(4096, 1024, 4, 256);
-    SP_OWNER_ATTR(2048, 1024, 4, 512);
-    SP_OWNER_ATTR(4096, 1024, 2, 512);
+  SP_OWNER_ATTR(4096, 1024, 3, 512);
+  SP_OWNER_ATTR(8192, 2048, 2, 512);
+  SP_OWNER_ATTR(4096, 1024, 4, 256);
+  SP_OWNER_ATTR(2048, 1024, 4, 512);
+  SP_OWNER_ATTR(4096, 1024, 2, 512);
 #undef SP_OWNER_ATTR
-    attr = true;
-  }
+  done = true;
+}
+
+// the five kernels of one slice group (slices [g0, g0 + np) of the call) on stream st
+cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int np, int NH, int G, cudaStream_t st) {
+  const int64_t N = a.zv.N, M = a.zv.M;
   constexpr int wpc = 4;   // partition: 256-element rounds per warp
   const int ncx0 = static_cast<int>(cdiv(N, S0_CH)), ncy0 = static_cast<int>(cdiv(M, S0_CH));
   const int64_t per_cta2 = int64_t(S2W_WARPS) * S2W_WCH * wpc;
   const int ncx2 = static_cast<int>(cdiv(N, per_cta2)), ncy2 = static_cast<int>(cdiv(M, per_cta2));
   const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1);
   const size_t sm2 = sizeof(int) * (((1 + S2W_WARPS) * G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
-  {
-    const int np = std::min(gs, a.np - g0);
-    ZView zv = a.zv;
-    zv.zx += g0 * zv.ldx;
-    zv.zy += g0 * zv.ldy;
-    const unsigned* mm = a.mm + 4 * g0;
-    float* pso = a.per_slice_out ? a.per_slice_out + static_cast<int64_t>(g0) * M : nullptr;
-    cudaStream_t st = sst;
-    cudaError_t e = cudaMemsetAsync(wbase, 0, zero_bytes, st);
-    if (e != cudaSuccess) return e;
-    ProfMark pm = prof_begin(PS_SP_HIST, st);
-    k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, kSpVars[sp_variant()].nbf,
-                                                         H, done, om, own);
-    prof_end(pm);
-    pm = prof_begin(PS_SP_PART, st);
-    k_sp_part<<<dim3(ncx2 + ncy2, np), S2W_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, wpc, om, own, cursor, Xmb, Ymb,
-                                                          ypos, yown);
-    prof_end(pm);
-    pm = prof_begin(PS_SP_OWNER, st);
-    switch (sp_variant()) {
+  ZView zv = a.zv;
+  zv.zx += g0 * zv.ldx;
+  zv.zy += g0 * zv.ldy;
+  const unsigned* mm = a.mm + 4 * g0;
+  float* pso = a.per_slice_out ? a.per_slice_out + static_cast<int64_t>(g0) * M : nullptr;
+  cudaError_t e = cudaMemsetAsync(r.H, 0, r.zero_bytes, st);
+  if (e != cudaSuccess) return e;
+  ProfMark pm = prof_begin(PS_SP_HIST, st);
+  k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, kSpVars[sp_variant()].nbf, r.H,
+                                                       r.done, r.om, r.own);
+  prof_end(pm);
+  pm = prof_begin(PS_SP_PART, st);
+  k_sp_part<<<dim3(ncx2 + ncy2, np), S2W_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, wpc, r.om, r.own, r.cursor, r.Xmb,
+                                                        r.Ymb, r.ypos, r.yown);
+  prof_end(pm);
+  pm = prof_begin(PS_SP_OWNER, st);
+  switch (sp_variant()) {
 #define SP_OWNER_LAUNCH(C, B, MB, T)                                                                            \
-  k_sp_owner<C, B, MB, T><<<dim3(G, np), T, sizeof(OwnerShared<C, B, T>), st>>>(own, otot, mm, NH, G, N, M, Xmb, \
-                                                                               Ymb, a.coef, R)
-      case 1: SP_OWNER_LAUNCH(8192, 2048, 2, 512); break;
-      case 2: SP_OWNER_LAUNCH(4096, 1024, 4, 256); break;
-      case 3: SP_OWNER_LAUNCH(2048, 1024, 4, 512); break;
-      case 4: SP_OWNER_LAUNCH(4096, 1024, 2, 512); break;
-      default: SP_OWNER_LAUNCH(4096, 1024, 3, 512); break;
+  k_sp_owner<C, B, MB, T><<<dim3(G, np), T, sizeof(OwnerShared<C, B, T>), st>>>(r.own, r.otot, mm, NH, G, N, M, \
+                                                                               r.Xmb, r.Ymb, a.coef, r.R)
+    case 1: SP_OWNER_LAUNCH(8192, 2048, 2, 512); break;
+    case 2: SP_OWNER_LAUNCH(4096, 1024, 4, 256); break;
+    case 3: SP_OWNER_LAUNCH(2048, 1024, 4, 512); break;
+    case 4: SP_OWNER_LAUNCH(4096, 1024, 2, 512); break;
+    default: SP_OWNER_LAUNCH(4096, 1024, 3, 512); break;
 #undef SP_OWNER_LAUNCH
-    }
-    prof_end(pm);
-    pm = prof_begin(PS_SP_GATHER, st);
-    k_sp_outer<<<np, SO_T, 0, st>>>(otot, G, dab, a.tot + g0);
-    k_sp_gather<<<dim3(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG))), S4_T, 0, st>>>(
-        zv, np, G, a.coef, ypos, yown, R, dab, a.s64, pso);
-    prof_end(pm);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
   }
+  prof_end(pm);
+  pm = prof_begin(PS_SP_GATHER, st);
+  k_sp_outer<<<np, SO_T, 0, st>>>(r.otot, G, r.dab, a.tot + g0);
+  k_sp_gather<<<dim3(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG))), S4_T, 0, st>>>(
+      zv, np, G, a.coef, r.ypos, r.yown, r.R, r.dab, a.s64, pso);
+  prof_end(pm);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
+  const int64_t N = a.zv.N, M = a.zv.M;
+  const SpDims d = sortpart_dims(N, M);
+  const int gs = sortpart_group(N, M, a.np);
+  const int ns = active_streams(N, M, a.np);
+  set_attributes();
+  StreamPool& pool = stream_pool();
+  if (ns > 1 && !pool.ok) return cudaErrorInitializationError;
+  cudaError_t e = cudaSuccess;
+  if (ns > 1) {   // fork: the helper streams start after everything already queued on the caller's stream
+    if ((e = cudaEventRecord(pool.fork, st)) != cudaSuccess) return e;
+    for (int i = 1; i < ns; ++i)
+      if ((e = cudaStreamWaitEvent(pool.s[i], pool.fork, 0)) != cudaSuccess) return e;
   }
-  if (ns > 1) {   // join
-    for (int i = 1; i < ns; ++i) {
-      cudaError_t e = cudaEventRecord(pool.join[i], pool.s[i]);
-      if (e != cudaSuccess) return e;
-      if ((e = cudaStreamWaitEvent(st, pool.join[i], 0)) != cudaSuccess) return e;
-    }
+  const size_t rb = region_bytes(N, M, gs);
+  for (int g0 = 0, gi = 0; g0 < a.np; g0 += gs, ++gi) {
+    const int si = gi % ns;
+    const SpRegion r = carve_region(static_cast<char*>(ws) + rb * si, N, M, d.NH, d.G, gs);
+    if ((e = launch_group(a, r, g0, std::min(gs, a.np - g0), d.NH, d.G, si ? pool.s[si] : st)) != cudaSuccess) return e;
+  }
+  for (int i = 1; i < ns; ++i) {   // join
+    if ((e = cudaEventRecord(pool.join[i], pool.s[i])) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, pool.join[i], 0)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
