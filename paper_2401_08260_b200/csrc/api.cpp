@@ -489,7 +489,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ProfScope ps(PS_MINMAX, st);
       SKS_CUDA(sks::launch_minmax(zv, nbat, mm, flag, st));
     }
-    launches += 2;
+    launches += 1 + (tc ? (nbat + 1023) / 1024 : 1);   // init_minmax + projection launch(es)
     int ndft_kw = 0;
     sks::EvalArgs ea{};
     ea.zv = zv;

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -456,16 +457,29 @@ cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, cons
                               cudaStream_t st) {
   const int dp = proj_tc_dpad(d);
   const int nk = dp / TC_BK;
-  const int BN = np > 128 ? 256 : (np > 64 ? 128 : 64);
-  CUtensorMap ta, tb;
+  CUtensorMap ta;
   if (!make_map(&ta, xs, static_cast<uint64_t>(L), static_cast<uint64_t>(3 * dp), TC_M)) return cudaErrorInvalidValue;
-  if (!make_map(&tb, g3, static_cast<uint64_t>(np), static_cast<uint64_t>(dp), static_cast<uint32_t>(BN)))
-    return cudaErrorInvalidValue;
   unsigned* pp = static_cast<unsigned*>(part);
-  if (np > 4096) return cudaErrorInvalidValue;   // range partials live in shared memory
-  if (BN == 256) return launch_tc<256, 2>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, pp, st);
-  if (BN == 128) return launch_tc<128, 3>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, pp, st);
-  return launch_tc<64, 3>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, pp, st);
+  // the per-CTA range partials of all its slices live in shared memory (20 B per slice): launches of at most
+  // kSliceChunk slices (the point tiles are re-read per launch, from L2 for moderate L)
+  constexpr int kSliceChunk = 1024;
+  for (int s0 = 0; s0 < np; s0 += kSliceChunk) {
+    const int ns = std::min(kSliceChunk, np - s0);
+    const int BN = ns > 128 ? 256 : (ns > 64 ? 128 : 64);
+    const void* g = static_cast<const uint16_t*>(g3) + static_cast<int64_t>(s0) * dp;
+    CUtensorMap tb;
+    if (!make_map(&tb, g, static_cast<uint64_t>(ns), static_cast<uint64_t>(dp), static_cast<uint32_t>(BN)))
+      return cudaErrorInvalidValue;
+    float* Zc = Z + static_cast<int64_t>(s0) * ldz;
+    unsigned* mmc = mm + 4 * s0;
+    const float* ic = inv_norm + s0;
+    cudaError_t e;
+    if (BN == 256) e = launch_tc<256, 2>(ta, tb, nk, L, Nx, ns, ic, Zc, ldz, mmc, flag, pp, st);
+    else if (BN == 128) e = launch_tc<128, 3>(ta, tb, nk, L, Nx, ns, ic, Zc, ldz, mmc, flag, pp, st);
+    else e = launch_tc<64, 3>(ta, tb, nk, L, Nx, ns, ic, Zc, ldz, mmc, flag, pp, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace sks

@@ -270,3 +270,30 @@ def test_cfg5_slice_subset_sampled():
         # the 2-slice partial is (1/P) * sum of 2 slices: compare on the per-slice-mean scale
         err = rel_err(s[tgt] * cfg.P / 2, ref * cfg.P / 2, w)
         assert err <= TOL["gaussian"], err
+
+
+# ---------------------------------------------------------------- the paper's error claims on the GPU path
+def test_slicing_error_decays_like_inverse_sqrt_P():
+    # Prop. 2.6 / Thm 2.7: the per-summand error of the GPU estimate against the exact sum
+    # (oracle (a)) decays like P^{-1/2}; the paper's Sec. 4.1 workload, Gaussian sigma = 1
+    cfg = I.scaled(I.CONFIGS["paper_gauss"], N=3000, M=3000)
+    x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
+    tgt = I.target_subset(cfg.M, 200)
+    exact = O.exact_sum("gaussian", 1.0, x, y[tgt], w)
+    sw = np.abs(w.astype(np.float64)).sum()
+    Ps = [16, 64, 256, 1024]
+    errs = []
+    for P in Ps:
+        s = S.sks_sum(dev(x), dev(y), dev(w), "gaussian", 1.0, P, cfg.dir_seed).cpu().numpy()
+        errs.append(np.abs(s[tgt] - exact).sum() / (len(tgt) * sw))
+    slope = np.polyfit(np.log(Ps), np.log(errs), 1)[0]
+    assert -0.75 < slope < -0.3, (slope, errs)
+
+
+def test_many_slices_projection_chunks():
+    # more slices than one projection launch takes (1024): chunked launches, same result as slice ranges
+    cfg = I.scaled(I.CONFIGS["paper_gauss"], N=600, M=300, P=2500)
+    s_all = run_cfg(cfg, n_tgt=50)[0].astype(np.float64)
+    s_a = run_cfg(cfg, n_tgt=50, p0=0, p1=1300)[0].astype(np.float64)
+    s_b = run_cfg(cfg, n_tgt=50, p0=1300, p1=2500)[0].astype(np.float64)
+    assert rel_err(s_a + s_b, s_all, I.weights(cfg)) <= 1e-6
