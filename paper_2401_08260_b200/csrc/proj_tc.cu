@@ -128,6 +128,40 @@ __device__ __forceinline__ void colrange16(uint32_t* kmn, uint32_t* kmx, int b4,
   *omx = max(kmx[0], __shfl_xor_sync(0xffffffffu, kmx[0], 1));
 }
 
+// the same on floats: min / max of the finite values (NaN / Inf are trapped separately)
+__device__ __forceinline__ void colrange16f(float* fmn, float* fmx, int b4, int b3, int b2, int b1, float* omn,
+                                            float* omx) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float smn = b4 ? fmn[k] : fmn[8 + k], smx = b4 ? fmx[k] : fmx[8 + k];
+    const float rmn = __shfl_xor_sync(0xffffffffu, smn, 16), rmx = __shfl_xor_sync(0xffffffffu, smx, 16);
+    fmn[k] = fminf(b4 ? fmn[8 + k] : fmn[k], rmn);
+    fmx[k] = fmaxf(b4 ? fmx[8 + k] : fmx[k], rmx);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float smn = b3 ? fmn[k] : fmn[4 + k], smx = b3 ? fmx[k] : fmx[4 + k];
+    const float rmn = __shfl_xor_sync(0xffffffffu, smn, 8), rmx = __shfl_xor_sync(0xffffffffu, smx, 8);
+    fmn[k] = fminf(b3 ? fmn[4 + k] : fmn[k], rmn);
+    fmx[k] = fmaxf(b3 ? fmx[4 + k] : fmx[k], rmx);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float smn = b2 ? fmn[k] : fmn[2 + k], smx = b2 ? fmx[k] : fmx[2 + k];
+    const float rmn = __shfl_xor_sync(0xffffffffu, smn, 4), rmx = __shfl_xor_sync(0xffffffffu, smx, 4);
+    fmn[k] = fminf(b2 ? fmn[2 + k] : fmn[k], rmn);
+    fmx[k] = fmaxf(b2 ? fmx[2 + k] : fmx[k], rmx);
+  }
+  {
+    const float smn = b1 ? fmn[0] : fmn[1], smx = b1 ? fmx[0] : fmx[1];
+    const float rmn = __shfl_xor_sync(0xffffffffu, smn, 2), rmx = __shfl_xor_sync(0xffffffffu, smx, 2);
+    fmn[0] = fminf(b1 ? fmn[1] : fmn[0], rmn);
+    fmx[0] = fmaxf(b1 ? fmx[1] : fmx[0], rmx);
+  }
+  *omn = fminf(fmn[0], __shfl_xor_sync(0xffffffffu, fmn[0], 1));
+  *omx = fmaxf(fmx[0], __shfl_xor_sync(0xffffffffu, fmx[0], 1));
+}
+
 // Persistent: grid = min(#tiles, #SMs) CTAs, tiles t = blockIdx.x + i*gridDim.x (slice tiles fastest, so the
 // CTAs that share a point tile run together and its TMA loads hit L2).  Two TMEM accumulators: the epilogue
 // of tile i overlaps the MMAs of tile i+1.  Per-slice ranges: per-CTA partials in smem -> global atomics.
@@ -238,7 +272,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr int HALF = BN / 2;
     const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
     const int my_col = 8 * b4 + 4 * b3 + 2 * b2 + b1;   // column of the chunk this lane pair ends up holding
-    bool bad = false;   // a non-finite projection (NaN / Inf in x, y or an overflow)
+    float trap = 0.f;   // becomes NaN if a projection is NaN / Inf (in x, y or an overflow)
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int b = it & 1;
@@ -248,7 +282,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int64_t w0 = m0 + 32 * q;
       const int64_t i = w0 + lane;
       const bool valid = i < L, isx = i < Nx;
-      const bool warp_any_x = (w0 < Nx), mixed = warp_any_x && (w0 + 32 > Nx);
+      const bool warp_any_x = (w0 < Nx), mixed = warp_any_x && (w0 + 32 > Nx), warp_full = (w0 + 32 <= L);
       const int ncols = min(HALF, np - n0);   // may be <= 0
       mbar_wait(&tfull[b], tph);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -277,7 +311,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
               : "r"(tbase + static_cast<uint32_t>(c0 + 16)));
         const int nc = min(16, ncols - c0);
-        if (emode == 1) { bad |= (cur[0] == 0x7fc00001u); continue; }   // measurement: TMEM drain only
+        if (emode == 1) { trap += (cur[0] == 0x7fc00001u) ? 1.f : 0.f; continue; }   // measurement: TMEM drain
         const float4* sv = reinterpret_cast<const float4*>(sinv + n0 + c0);
         float sc[16];
 #pragma unroll
@@ -285,44 +319,62 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const float4 f = sv[k];
           sc[4 * k] = f.x; sc[4 * k + 1] = f.y; sc[4 * k + 2] = f.z; sc[4 * k + 3] = f.w;
         }
-        uint32_t kmn[16], kmx[16];
+        // scale + store (running pointer along the slices) + NaN/Inf trap; ranges as floats.  Full chunks (all
+        // lanes valid, 16 columns) take a branch-free path.
+        float fmn[16], fmx[16];
+        float* zp = zrow + static_cast<int64_t>(c0) * ldz;
+        if (warp_full && nc == 16) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float z = __uint_as_float(cur[j]) * sc[j];
-          const bool ok = valid && j < nc;
-          if (ok) {
-            zrow[static_cast<int64_t>(c0 + j) * ldz] = z;
-            bad |= !isfinite(z);
+          for (int j = 0; j < 16; ++j) {
+            const float z = __uint_as_float(cur[j]) * sc[j];
+            *zp = z;
+            zp += ldz;
+            trap = fmaf(z, 0.f, trap);   // NaN / Inf -> NaN
+            fmn[j] = z;
+            fmx[j] = z;
           }
-          const uint32_t key = f2key_tc(z);
-          kmn[j] = ok ? key : 0xffffffffu;
-          kmx[j] = ok ? key : 0u;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float z = __uint_as_float(cur[j]) * sc[j];
+            const bool ok = valid && j < nc;
+            if (ok) {
+              *zp = z;
+              trap = fmaf(z, 0.f, trap);
+            }
+            zp += ldz;
+            fmn[j] = ok ? z : CUDART_INF_F;
+            fmx[j] = ok ? z : -CUDART_INF_F;
+          }
         }
-        if (emode == 2) { bad |= (kmn[0] == 1u); continue; }   // measurement: scale + store only
-        uint32_t amn, amx;
-        colrange16(kmn, kmx, b4, b3, b2, b1, &amn, &amx);
-        uint32_t xmn = amn, xmx = amx;
+        if (emode == 2) { trap += fmn[0] * 0.f; continue; }   // measurement: scale + store only
+        float amn, amx;
+        colrange16f(fmn, fmx, b4, b3, b2, b1, &amn, &amx);
+        float xmn = amn, xmx = amx;
         if (mixed) {   // the warp holding the x/y boundary: x-only ranges separately
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const uint32_t key = f2key_tc(__uint_as_float(cur[j]) * sc[j]);
+            const float z = __uint_as_float(cur[j]) * sc[j];
             const bool ok = valid && isx && j < nc;
-            kmn[j] = ok ? key : 0xffffffffu;
-            kmx[j] = ok ? key : 0u;
+            fmn[j] = ok ? z : CUDART_INF_F;
+            fmx[j] = ok ? z : -CUDART_INF_F;
           }
-          colrange16(kmn, kmx, b4, b3, b2, b1, &xmn, &xmx);
+          colrange16f(fmn, fmx, b4, b3, b2, b1, &xmn, &xmx);
         }
         if ((lane & 1) == 0 && my_col < nc) {
           const int s = n0 + c0 + my_col;
-          if (amn <= amx) { atomicMin(&rng[4 * s + 2], amn); atomicMax(&rng[4 * s + 3], amx); }
-          if (warp_any_x && xmn <= xmx) { atomicMin(&rng[4 * s + 0], xmn); atomicMax(&rng[4 * s + 1], xmx); }
+          if (amn <= amx) { atomicMin(&rng[4 * s + 2], f2key_tc(amn)); atomicMax(&rng[4 * s + 3], f2key_tc(amx)); }
+          if (warp_any_x && xmn <= xmx) {
+            atomicMin(&rng[4 * s + 0], f2key_tc(xmn));
+            atomicMax(&rng[4 * s + 1], f2key_tc(xmx));
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+    if (__any_sync(0xffffffffu, trap != 0.f) && lane == 0) atomicOr(flag, 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
