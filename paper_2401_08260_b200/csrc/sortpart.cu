@@ -230,6 +230,53 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
 // mailbox slot (ypos) and the owner (yown).  No sums here: every owner sums its own x (k_sp_owner).
 constexpr int S2W_T = 256, S2W_WARPS = S2W_T / 32, S2W_PER = 8, S2W_WCH = 32 * S2W_PER;
 
+// one round of one warp: 256 consecutive elements [e0, e0 + 256) of a slice part (FULL: all in range)
+template <bool IsX, bool FULL>
+__device__ __forceinline__ void part_round(int e0, int n, const float* __restrict__ z, const float* __restrict__ w,
+                                           float uoff, float hscale, int NH, int G, const uint16_t* om, const int* ooff,
+                                           int* cw, int* curp, float2* __restrict__ xdst, float* __restrict__ ydst,
+                                           int* __restrict__ yp, uint16_t* __restrict__ yo) {
+  const int lane = threadIdx.x & 31;
+  for (int o = lane; o < G; o += 32) cw[o] = 0;
+  float zz[S2W_PER], ww[S2W_PER];
+#pragma unroll
+  for (int k = 0; k < S2W_PER; ++k) {
+    const int i = e0 + 32 * k + lane;
+    zz[k] = (FULL || i < n) ? __ldg(z + i) : 0.f;
+    if (IsX) ww[k] = (FULL || i < n) ? __ldg(w + i) : 0.f;
+  }
+  __syncwarp();
+  int ow[S2W_PER], rk[S2W_PER];
+#pragma unroll
+  for (int k = 0; k < S2W_PER; ++k) {
+    ow[k] = -1;
+    if (FULL || e0 + 32 * k + lane < n) {
+      ow[k] = om[clamp_floor(ucoord(zz[k], uoff, hscale), NH)];
+      rk[k] = atomicAdd(&cw[ow[k]], 1);
+    }
+  }
+  __syncwarp();
+  for (int o = lane; o < G; o += 32) {   // one run per (warp, owner): counter -> absolute slot of the run
+    const int c = cw[o];
+    cw[o] = c ? ooff[o] + atomicAdd(curp + o, c) : 0;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < S2W_PER; ++k) {
+    if (!FULL && ow[k] < 0) continue;
+    const int dst = cw[ow[k]] + rk[k];
+    const int i = e0 + 32 * k + lane;
+    if (IsX) {
+      xdst[dst] = make_float2(zz[k], ww[k]);
+    } else {
+      ydst[dst] = zz[k];
+      yp[i] = dst;
+      yo[i] = static_cast<uint16_t>(ow[k]);
+    }
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __restrict__ w, const unsigned* __restrict__ mm,
                                                    int NH, int G, int ncx, int wpc, const uint16_t* __restrict__ om_g,
                                                    const SpOwner* __restrict__ own, int* __restrict__ cursor,
@@ -262,44 +309,16 @@ __global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __rest
   for (int it = 0; it < wpc; ++it) {
     const int e0 = ((cb * wpc + it) * S2W_WARPS + wid) * S2W_WCH;   // this warp's 256 elements
     if (e0 >= n) break;   // warp-uniform
-    for (int o = lane; o < G; o += 32) cw[o] = 0;
-    float zz[S2W_PER], ww[S2W_PER];
-#pragma unroll
-    for (int k = 0; k < S2W_PER; ++k) {
-      const int i = e0 + 32 * k + lane;
-      zz[k] = (i < n) ? __ldg(z + i) : 0.f;
-      ww[k] = (isx && i < n) ? __ldg(w + i) : 0.f;
+    const bool full = e0 + S2W_WCH <= n;   // warp-uniform: no per-element bounds in the common case
+    if (isx) {
+      if (full) part_round<true, true>(e0, n, z, w, uoff, hscale, NH, G, om, ooff, cw, curp, xdst, ydst, nullptr, nullptr);
+      else part_round<true, false>(e0, n, z, w, uoff, hscale, NH, G, om, ooff, cw, curp, xdst, ydst, nullptr, nullptr);
+    } else {
+      int* yp = ypos + static_cast<int64_t>(p) * zv.M;
+      uint16_t* yo = yown + static_cast<int64_t>(p) * zv.M;
+      if (full) part_round<false, true>(e0, n, z, w, uoff, hscale, NH, G, om, ooff, cw, curp, xdst, ydst, yp, yo);
+      else part_round<false, false>(e0, n, z, w, uoff, hscale, NH, G, om, ooff, cw, curp, xdst, ydst, yp, yo);
     }
-    __syncwarp();
-    int ow[S2W_PER], rk[S2W_PER];
-#pragma unroll
-    for (int k = 0; k < S2W_PER; ++k) {
-      ow[k] = -1;
-      if (e0 + 32 * k + lane < n) {
-        ow[k] = om[clamp_floor(ucoord(zz[k], uoff, hscale), NH)];
-        rk[k] = atomicAdd(&cw[ow[k]], 1);
-      }
-    }
-    __syncwarp();
-    for (int o = lane; o < G; o += 32) {   // one run per (warp, owner): counter -> absolute slot of the run
-      const int c = cw[o];
-      cw[o] = c ? ooff[o] + atomicAdd(curp + o, c) : 0;
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < S2W_PER; ++k) {
-      if (ow[k] < 0) continue;
-      const int dst = cw[ow[k]] + rk[k];
-      const int i = e0 + 32 * k + lane;
-      if (isx) {
-        xdst[dst] = make_float2(zz[k], ww[k]);
-      } else {
-        ydst[dst] = zz[k];
-        ypos[static_cast<int64_t>(p) * zv.M + i] = dst;
-        yown[static_cast<int64_t>(p) * zv.M + i] = static_cast<uint16_t>(ow[k]);
-      }
-    }
-    __syncwarp();
   }
 }
 
