@@ -286,32 +286,48 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
   }
 }
 
+// Wide footprints (W > 64 cells, e.g. the Laplacian's smooth part): one shared grid per CTA.  Shared-memory
+// float atomics are CAS loops on sm_100a, so the CTA accumulates in 32-bit fixed point with native integer
+// atomics: scale S = 2^30 / sum_{chunk} |w| bounds every partial cell sum by 2^30 (no overflow); the rounding
+// per contribution is <= sum_{chunk}|w| 2^-31, i.e. ~1e-9 of the chunk's weight, far below the fp32 grid.
 template <int WT>
 __global__ void __launch_bounds__(SP_THREADS) k_spread_shared(ZView zv, const float* __restrict__ w,
                                                               const FPar* __restrict__ fp, int n, PolyWin pw,
                                                               int64_t chunk, float* __restrict__ grid) {
-  extern __shared__ float sg[];   // [n]
+  extern __shared__ int sgi[];   // [n] fixed point
+  __shared__ float wred[SP_THREADS / 32];
   const int p = blockIdx.y, tid = threadIdx.x;
   const FPar f = fp[p];
-  for (int c = tid; c < n; c += SP_THREADS) sg[c] = 0.f;
-  __syncthreads();
-  const float nf = static_cast<float>(n), hw = 0.5f * pw.w;
+  for (int c = tid; c < n; c += SP_THREADS) sgi[c] = 0;
   const int64_t i0 = blockIdx.x * chunk, i1 = min(zv.N, i0 + chunk);
+  float aw = 0.f;
+  for (int64_t i = i0 + tid; i < i1; i += SP_THREADS) aw += fabsf(__ldg(w + i));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) aw += __shfl_xor_sync(0xffffffffu, aw, o);
+  if ((tid & 31) == 0) wred[tid >> 5] = aw;
+  __syncthreads();
+  float wsum = 0.f;
+#pragma unroll
+  for (int q = 0; q < SP_THREADS / 32; ++q) wsum += wred[q];
+  if (!(wsum > 0.f)) return;   // all weights zero in this chunk (uniform)
+  const float S = 1073741824.0f / (wsum * 1.0001f);   // 2^30 / sum|w| (margin for the fp32 sum)
+  const float nf = static_cast<float>(n), hw = 0.5f * pw.w;
   const float* zx = zv.zx + p * zv.ldx;
   for (int64_t i = i0 + tid; i < i1; i += SP_THREADS) {
     const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);
     const float a = __fsub_rn(v, hw), fl = floorf(a);
     const int l0 = static_cast<int>(fl) + 1;
-    const float wi = __ldg(w + i);
+    const float ws = __ldg(w + i) * S;
     float tw[WT];
     poly_taps<WT>(pw, a - fl, tw);
 #pragma unroll
-    for (int j = 0; j < WT; ++j) atomicAdd(&sg[(l0 + j) & (n - 1)], wi * tw[j]);
+    for (int j = 0; j < WT; ++j) atomicAdd(&sgi[(l0 + j) & (n - 1)], __float2int_rn(ws * tw[j]));
   }
   __syncthreads();
+  const float inv = 1.0f / S;
   for (int c = tid; c < n; c += SP_THREADS) {
-    const float s = sg[c];
-    if (s != 0.f) atomicAdd(&grid[static_cast<int64_t>(p) * n + c], s);
+    const int v = sgi[c];
+    if (v != 0) atomicAdd(&grid[static_cast<int64_t>(p) * n + c], static_cast<float>(v) * inv);
   }
 }
 
