@@ -66,8 +66,11 @@ def roofline_model(slot, cfg, P, plan):
     n = plan.get("n_grid", 0) or 0
     if slot == "split3":        # fp32 points -> 3 bf16 pieces
         return 4 * L * d + 6 * L * dp, 0
-    if slot == "project":       # Z = X G^T: read the pieces and G, write Z; 2 L d P fp32-accurate flops
-        return 6 * L * dp + 2 * P * dp + 4 * L * P, ("tensor", 2.0 * L * d * P)
+    if slot == "project":       # Z = X G^T, 2 L d P fp32-accurate flops.  d > 256 (BF16x3): read the 3 bf16
+        if d > 256:             # pieces and G, write Z; d <= 256 (TF32x2, split inside): read the fp32 points
+            return 6 * L * dp + 2 * P * dp + 4 * L * P, ("tensor", 2.0 * L * d * P)
+        dp32 = (d + 31) // 32 * 32
+        return 4 * L * d + 4 * P * dp32 + 4 * L * P, ("tensor", 2.0 * L * d * P)
     if slot == "sp_hist":       # read every projection
         return 4 * L * P, 0
     if slot == "sp_part":       # read projections and w, write x mailbox (z, w), y mailbox (z) + positions

@@ -165,13 +165,22 @@ bool use_sort_v1() {
   return v == 1;
 }
 
-bool use_tc_projection() {
-  static int v = -1;
-  if (v < 0) {
+// row a1 variant: 0 SIMT fp32 (measurement A/B), 1 BF16x3 (split kernel + three bf16 MMAs), 2 TF32x2 (split
+// inside the kernel, two tf32 MMAs).  TF32x2 reads the fp32 points once and needs no split buffer, at 4/3 of the
+// tensor work of BF16x3: the default for d <= 256, where the projection is HBM-bound; BF16x3 above.
+// SKS_PROJECTION = simt | bf16x3 | tf32x2 overrides.
+enum ProjMode { PM_SIMT = 0, PM_BF16X3 = 1, PM_TF32X2 = 2 };
+ProjMode proj_mode(int d) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = std::getenv("SKS_PROJECTION");
-    v = (e && std::strcmp(e, "simt") == 0) ? 0 : 1;   // A/B switch for measurements; tensor cores by default
+    v = -1;
+    if (e && std::strcmp(e, "simt") == 0) v = PM_SIMT;
+    if (e && std::strcmp(e, "bf16x3") == 0) v = PM_BF16X3;
+    if (e && std::strcmp(e, "tf32x2") == 0) v = PM_TF32X2;
   }
-  return v == 1;
+  if (v >= 0) return static_cast<ProjMode>(v);
+  return d <= 256 ? PM_TF32X2 : PM_BF16X3;
 }
 
 // leading dimension of the slice-major projections Z: a multiple of 4 floats (16-byte rows for TMA stores)
@@ -190,7 +199,7 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb,
   L.mm = take(sizeof(unsigned) * 4 * nbat);
   if (with_Z) {
     L.Z = take(sizeof(float) * zld(N, M) * nbat);
-    if (use_tc_projection()) {
+    if (proj_mode(d) == PM_BF16X3) {
       L.xs3 = take(sizeof(uint16_t) * 3 * static_cast<size_t>(sks::proj_tc_dpad(d)) * (N + M));
       L.part = take(sks::proj_tc_part_bytes(nbat));
     }
@@ -234,8 +243,10 @@ int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int nb, int
 struct DirEntry {
   float* g = nullptr;      // np x d
   float* inv = nullptr;    // np
-  void* g3 = nullptr;      // np x dp bf16: g zero padded (tensor-core projection operand)
+  void* g3 = nullptr;      // np x dp bf16: g zero padded (BF16x3 tensor-core operand)
   int K3 = 0;              // dp
+  float* g32 = nullptr;    // np x dp32 fp32: g zero padded to 32 (TF32x2 operand; bf16-exact, so tf32-exact)
+  int K32 = 0;             // dp32
 };
 std::mutex g_dir_mu;
 std::map<std::tuple<int, uint64_t, int, int, int, int>, DirEntry> g_dirs;
@@ -273,6 +284,12 @@ sks_status get_dirs(int P, int d, uint64_t seed, int p0, int p1, DirEntry* out) 
       }
     SKS_CUDA(cudaMalloc(&e.g3, sizeof(uint16_t) * g3.size()));
     SKS_CUDA(cudaMemcpy(e.g3, g3.data(), sizeof(uint16_t) * g3.size(), cudaMemcpyHostToDevice));
+    e.K32 = sks::proj_tf32_dpad(d);
+    std::vector<float> g32(static_cast<size_t>(np) * e.K32, 0.f);
+    for (int p = 0; p < np; ++p)
+      for (int j = 0; j < d; ++j) g32[static_cast<size_t>(p) * e.K32 + j] = g[static_cast<size_t>(p) * d + j];
+    SKS_CUDA(cudaMalloc(&e.g32, sizeof(float) * g32.size()));
+    SKS_CUDA(cudaMemcpy(e.g32, g32.data(), sizeof(float) * g32.size(), cudaMemcpyHostToDevice));
   }
   g_dirs[key] = e;
   *out = e;
@@ -455,7 +472,9 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     SKS_CUDA(sks::launch_zero(ws + L.s64, al(sizeof(double) * pr.M), st));
   }
   launches += s_out ? 2 : 1;
-  const bool tc = pr.with_Z && use_tc_projection();
+  const ProjMode pm = proj_mode(pr.d);
+  const bool tc = pr.with_Z && pm == PM_BF16X3;
+  const bool tf = pr.with_Z && pm == PM_TF32X2;
   if (tc) {
     ProfScope ps(PS_SPLIT, st);
     SKS_CUDA(sks::launch_split3(x, pr.N, y, pr.M, pr.d, ws + L.xs3, st));
@@ -479,6 +498,9 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
         SKS_CUDA(sks::launch_project_tc(ws + L.xs3, pr.N + pr.M, pr.N, pr.d,
                                         static_cast<const uint16_t*>(dirs->g3) + static_cast<int64_t>(b0) * dirs->K3,
                                         nbat, dirs->inv + b0, Z, ldz, mm, flag, ws + L.part, st));
+      else if (tf)
+        SKS_CUDA(sks::launch_project_tf32(x, pr.N, y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32,
+                                          nbat, dirs->inv + b0, Z, ldz, mm, flag, st));
       else
         SKS_CUDA(sks::launch_project(x, pr.N, y, pr.M, pr.d, dirs->g + static_cast<int64_t>(b0) * pr.d,
                                      dirs->inv + b0, nbat, Z, ldz, mm, flag, st));
@@ -489,7 +511,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ProfScope ps(PS_MINMAX, st);
       SKS_CUDA(sks::launch_minmax(zv, nbat, mm, flag, st));
     }
-    launches += 1 + (tc ? (nbat + 1023) / 1024 : 1);   // init_minmax + projection launch(es)
+    launches += 1 + ((tc || tf) ? (nbat + 1023) / 1024 : 1);   // init_minmax + projection launch(es)
     int ndft_kw = 0;
     sks::EvalArgs ea{};
     ea.zv = zv;
@@ -769,7 +791,8 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
   // first use, grown on demand; this entry point is a test/inspection aid, not the hot path)
   static thread_local unsigned* scratch = nullptr;
   static thread_local size_t scratch_bytes = 0;
-  const bool tc = use_tc_projection();
+  const ProjMode pm = proj_mode(d);
+  const bool tc = pm == PM_BF16X3;
   const size_t need = al(sizeof(unsigned) * 4 * np + 16) +
                       (tc ? al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n) + al(sks::proj_tc_part_bytes(np)) : 0);
   if (scratch_bytes < need) {
@@ -786,6 +809,8 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
     char* part = xs3 + al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n);
     SKS_CUDA(sks::launch_split3(pts, n, pts, 0, d, xs3, cs));
     SKS_CUDA(sks::launch_project_tc(xs3, n, n, d, dirs.g3, np, dirs.inv, z, n, mm, flag, part, cs));
+  } else if (pm == PM_TF32X2) {
+    SKS_CUDA(sks::launch_project_tf32(pts, n, pts, 0, d, dirs.g32, np, dirs.inv, z, n, mm, flag, cs));
   } else {
     SKS_CUDA(sks::launch_project(pts, n, pts, 0, d, dirs.g, dirs.inv, np, z, n, mm, flag, cs));
   }

@@ -64,6 +64,12 @@ size_t proj_tc_part_bytes(int np);   // scratch for per-CTA range partials
 cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, const void* g3, int np,
                               const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, void* part,
                               cudaStream_t st);
+// row a1 as TF32x2 with the split inside the kernel (small d: no split buffer, the fp32 points are read once):
+// hi = tf32_rn(x), lo = x - hi, two kind::tf32 MMAs against the fp32 (tf32-exact) directions g32 [np][dp32]
+int proj_tf32_dpad(int d);
+cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g32, int np,
+                                const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag,
+                                cudaStream_t st);
 // per-slice ranges of given projections (sks_sum_1d)
 cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_t st);
 cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st);

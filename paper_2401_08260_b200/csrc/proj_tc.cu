@@ -78,11 +78,22 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-template <int BN, int STAGES>
+// instruction descriptor kind::tf32: D f32, A/B tf32, both K-major, N, M
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Stage of the k-loop.  BF16x3 (TF32 = false): three bf16 pieces of 128 points x 64 dims (TMA from the split
+// buffer) + the direction tile.  TF32x2 (TF32 = true): hi / lo tf32 pieces of 128 points x 32 dims written by
+// the converter warps straight from the fp32 points + the fp32 direction tile (TMA).  Rows are 128 bytes,
+// 128-byte swizzled, in both cases.
+template <int BN, int STAGES, bool TF32 = false>
 struct TcSmem {
-  static constexpr int A_BYTES = TC_M * TC_BK * 2;          // one bf16 piece of 128 points x 64 dims
-  static constexpr int B_BYTES = BN * TC_BK * 2;            // BN directions x 64 dims
-  static constexpr int STAGE = 3 * A_BYTES + B_BYTES;       // hi, mid, lo pieces share one direction tile
+  static constexpr int NPIECE = TF32 ? 2 : 3;
+  static constexpr int A_BYTES = TC_M * 128;                // one piece: 128 points x 128 bytes
+  static constexpr int B_BYTES = BN * 128;                  // BN directions x 128 bytes
+  static constexpr int STAGE = NPIECE * A_BYTES + B_BYTES;  // the pieces share one direction tile
   static constexpr int BAR_OFF = STAGES * STAGE;
   static constexpr int RANGE_OFF = BAR_OFF + 8 * (2 * STAGES + 4) + 16;
   static constexpr int FIXED = RANGE_OFF + 1024;            // + per-CTA range partials [np_pad][4], 1/||g|| + slack
@@ -166,13 +177,20 @@ __device__ __forceinline__ void colrange16f(float* fmn, float* fmx, int b4, int 
 // CTAs that share a point tile run together and its TMA loads hit L2).  Two TMEM accumulators: the epilogue
 // of tile i overlaps the MMAs of tile i+1.  Per-slice ranges: per-CTA partials in smem -> global atomics.
 constexpr int TC_THREADS = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue (2 warpgroups)
+constexpr int TC_THREADS_TF32 = 512;   // + w12..w15: fp32 -> tf32 hi / lo converters
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// round to the nearest tf32 (10 explicit mantissa bits), kept in an fp32 container: exact tensor-core operand
+__device__ __forceinline__ float tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+
+template <int BN, int STAGES, bool TF32 = false>
+__global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nk, int64_t L,
               int64_t Nx, int np, const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz,
-              unsigned* __restrict__ mm, int* __restrict__ flag, int emode) {
-  using SM = TcSmem<BN, STAGES>;
+              unsigned* __restrict__ mm, int* __restrict__ flag, int emode, const float* __restrict__ px,
+              const float* __restrict__ py, int d) {
+  using SM = TcSmem<BN, STAGES, TF32>;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + SM::BAR_OFF);
@@ -191,7 +209,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     rng[4 * c + 0] = 0xffffffffu; rng[4 * c + 1] = 0u; rng[4 * c + 2] = 0xffffffffu; rng[4 * c + 3] = 0u;
   }
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], TF32 ? 5 : 1); mbar_init(&empty[s], TF32 ? 1 : 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -216,16 +234,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         unsigned char* sa = sm + stage * SM::STAGE;
-        mbar_expect_tx(&full[stage], SM::STAGE);
+        if (TF32) {   // the points are written by the converter warps; TMA brings the direction tile
+          mbar_expect_tx(&full[stage], SM::B_BYTES);
+          tma_load_2d(&tmB, &full[stage], sa + 2 * SM::A_BYTES, kb * 32, n0);
+        } else {
+          mbar_expect_tx(&full[stage], SM::STAGE);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) tma_load_2d(&tmA, &full[stage], sa + q * SM::A_BYTES, (q * nk + kb) * TC_BK, m0);
-        tma_load_2d(&tmB, &full[stage], sa + 3 * SM::A_BYTES, kb * TC_BK, n0);
+          for (int q = 0; q < 3; ++q) tma_load_2d(&tmA, &full[stage], sa + q * SM::A_BYTES, (q * nk + kb) * TC_BK, m0);
+          tma_load_2d(&tmB, &full[stage], sa + 3 * SM::A_BYTES, kb * TC_BK, n0);
+        }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (single thread)
-    constexpr uint32_t idesc = idesc_bf16(TC_M, BN);
+    constexpr uint32_t idesc = TF32 ? idesc_tf32(TC_M, BN) : idesc_bf16(TC_M, BN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -239,19 +262,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&full[stage], phase);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const unsigned char* sa = sm + stage * SM::STAGE;
-        const uint64_t db = umma_desc_sw128(sa + 3 * SM::A_BYTES);
+        const uint64_t db = umma_desc_sw128(sa + SM::NPIECE * SM::A_BYTES);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < SM::NPIECE; ++q) {
           const uint64_t da = umma_desc_sw128(sa + q * SM::A_BYTES);
 #pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k) {
+          for (int k = 0; k < 4; ++k) {   // 4 MMAs of K = 32 bytes (16 bf16 / 8 tf32) per 128-byte row
             const uint32_t acc = (kb > 0 || q > 0 || k > 0) ? 1u : 0u;
             const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);   // +32 B along K inside the swizzle row
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t"
-                "setp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-                "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+            if (TF32)
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\t"
+                  "setp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                  "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+            else
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\t"
+                  "setp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                  "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
           }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -263,7 +293,68 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                        smem_u32(&tfull[b]))
                    : "memory");
     }
-  } else if (warp >= 4) {
+  } else if (TF32 && warp >= 12) {
+    // ---- converters (TF32x2): the tile's points, fp32 -> hi = tf32_rn(x), lo = x - hi (exact in fp32; the MMA
+    //      reads it as tf32, so |x - hi - lo| <= 2^-21 |x|), written in the 128-byte swizzled K-major layout:
+    //      row r, 16-byte chunk c at r * 128 + ((c ^ (r % 8)) * 16).  Lane l: chunk l % 8 of rows 4 i + l / 8.
+    const int cw = warp - 12;   // 0..3: rows 32 cw .. 32 cw + 31
+    const int c = lane & 7, rsub = lane >> 3;
+    const bool vec = (d & 3) == 0;   // rows 16-byte aligned: one 16-byte load per chunk
+    // software pipeline: the 8 chunks of the next (tile, k-block) are loaded into registers while the current
+    // ones are converted and stored
+    auto load8 = [&](int64_t m0, int kb, float4* v) {
+      const int col = kb * 32 + 4 * c;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int64_t i = m0 + 32 * cw + 4 * it + rsub;
+        v[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < L && col < d) {
+          const float* row = (i < Nx) ? px + i * static_cast<int64_t>(d) : py + (i - Nx) * static_cast<int64_t>(d);
+          if (vec) v[it] = __ldg(reinterpret_cast<const float4*>(row + col));
+          else {
+            v[it].x = __ldg(row + col);
+            if (col + 1 < d) v[it].y = __ldg(row + col + 1);
+            if (col + 2 < d) v[it].z = __ldg(row + col + 2);
+            if (col + 3 < d) v[it].w = __ldg(row + col + 3);
+          }
+        }
+      }
+    };
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t t = blockIdx.x;
+    int kb = 0;
+    float4 cur[8];
+    if (t < ntiles) load8((t / ntn) * TC_M, 0, cur);
+    while (t < ntiles) {
+      // next (tile, k-block)
+      int64_t tn = t;
+      int kn = kb + 1;
+      if (kn == nk) { kn = 0; tn += gridDim.x; }
+      float4 nxt[8];
+      if (tn < ntiles) load8((tn / ntn) * TC_M, kn, nxt);
+      mbar_wait(&empty[stage], phase ^ 1);
+      unsigned char* sa = sm + stage * SM::STAGE;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int r = 32 * cw + 4 * it + rsub;
+        const float4 v = cur[it];
+        const float4 hi = make_float4(tf32_rn(v.x), tf32_rn(v.y), tf32_rn(v.z), tf32_rn(v.w));
+        const float4 lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+        const int off = r * 128 + ((c ^ (r & 7)) << 4);
+        *reinterpret_cast<float4*>(sa + off) = hi;
+        *reinterpret_cast<float4*>(sa + SM::A_BYTES + off) = lo;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+#pragma unroll
+      for (int it = 0; it < 8; ++it) cur[it] = nxt[it];
+      t = tn;
+      kb = kn;
+    }
+  } else if (warp >= 4 && warp < 12) {
     // ---- epilogue: warp w handles TMEM lane quadrant q = w % 4 (points m0 + 32q + lane) and the column half
     //      h = (w - 4) / 4 of the accumulator.  Per 16-column chunk: scale, store (coalesced along points),
     //      order-preserving keys, and the per-column min / max over the warp's 32 points by a butterfly that
@@ -469,29 +560,74 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_k, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool TF32 = false>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int64_t L, int64_t Nx, int np,
                       const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, unsigned* part,
-                      cudaStream_t st) {
-  using SM = TcSmem<BN, STAGES>;
+                      cudaStream_t st, const float* px = nullptr, const float* py = nullptr, int d = 0) {
+  using SM = TcSmem<BN, STAGES, TF32>;
   const int ntn = (np + BN - 1) / BN;
   const size_t smem = SM::FIXED + static_cast<size_t>(20) * ntn * BN;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_proj_tc<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_proj_tc<BN, STAGES, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int64_t ntiles = ((L + TC_M - 1) / TC_M) * ntn;
   const int grid = static_cast<int>(ntiles < kProjMaxCtas ? ntiles : kProjMaxCtas);
   static const int emode = std::getenv("SKS_PROJ_EMODE") ? std::atoi(std::getenv("SKS_PROJ_EMODE")) : 0;
-  k_proj_tc<BN, STAGES><<<grid, TC_THREADS, smem, st>>>(ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, emode);
+  k_proj_tc<BN, STAGES, TF32><<<grid, TF32 ? TC_THREADS_TF32 : TC_THREADS, smem, st>>>(
+      ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, emode, px, py, d);
   (void)part;
   return cudaGetLastError();
+}
+
+// direction tile of the TF32x2 path: fp32 [np][dp32] (values bf16-exact, hence tf32-exact), box 32 x rows
+bool make_map_f32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t gdim[2] = {cols, rows};
+  const cuuint64_t gstride[1] = {cols * 4};
+  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
 
 int proj_tc_dpad(int d) { return (d + TC_BK - 1) / TC_BK * TC_BK; }
+int proj_tf32_dpad(int d) { return (d + 31) / 32 * 32; }
+
+// Z = X G^T with the TF32x2 split done inside the kernel (converter warps read the fp32 points directly):
+// no split buffer; three k-blocks of 32 dims per 128-byte row pair... see k_proj_tc<.., true>
+cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64_t M, int d,
+                                const float* g32 /* fp32 [np][dp32] */, int np, const float* inv_norm, float* Z,
+                                int64_t ldz, unsigned* mm, int* flag, cudaStream_t st) {
+  const int dp = proj_tf32_dpad(d);
+  const int nk = dp / 32;
+  const int64_t L = N + M;
+  CUtensorMap ta;
+  std::memset(&ta, 0, sizeof(ta));   // unused by the TF32 path
+  constexpr int kSliceChunk = 1024;
+  for (int s0 = 0; s0 < np; s0 += kSliceChunk) {
+    const int ns = std::min(kSliceChunk, np - s0);
+    const int BN = ns > 128 ? 256 : (ns > 64 ? 128 : 64);
+    CUtensorMap tb;
+    if (!make_map_f32(&tb, g32 + static_cast<int64_t>(s0) * dp, static_cast<uint64_t>(ns), static_cast<uint64_t>(dp),
+                      static_cast<uint32_t>(BN)))
+      return cudaErrorInvalidValue;
+    float* Zc = Z + static_cast<int64_t>(s0) * ldz;
+    unsigned* mmc = mm + 4 * s0;
+    const float* ic = inv_norm + s0;
+    cudaError_t e;
+    if (BN == 256) e = launch_tc<256, 3, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d);
+    else if (BN == 128) e = launch_tc<128, 4, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d);
+    else e = launch_tc<64, 4, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
 
 cudaError_t launch_split3(const float* x, int64_t N, const float* y, int64_t M, int d, void* xs, cudaStream_t st) {
   const int dp = proj_tc_dpad(d);
