@@ -297,3 +297,28 @@ def test_many_slices_projection_chunks():
     s_a = run_cfg(cfg, n_tgt=50, p0=0, p1=1300)[0].astype(np.float64)
     s_b = run_cfg(cfg, n_tgt=50, p0=1300, p1=2500)[0].astype(np.float64)
     assert rel_err(s_a + s_b, s_all, I.weights(cfg)) <= 1e-6
+
+
+@pytest.mark.parametrize("mode", ["bf16x3", "tf32x2", "simt"])
+def test_projection_modes_subprocess(mode):
+    # every row-a1 variant (R2) against the fp64 projection, at small and large d (the variant is fixed per process)
+    import subprocess
+    import sys
+    import textwrap
+    code = textwrap.dedent(f"""
+        import sys, numpy as np, torch
+        sys.path.insert(0, {repr(str(__import__('pathlib').Path(__file__).resolve().parents[1]))})
+        import oracle as O, paper_2401_08260_b200 as S
+        for n, d, P in [(300, 3, 64), (1000, 50, 70), (257, 784, 33), (129, 3072, 17), (700, 100, 300)]:
+            pts = np.random.default_rng(n + d).uniform(-1, 1, (n, d)).astype(np.float32)
+            z = S.sks_project(torch.from_numpy(pts).cuda(), P, seed=7).cpu().numpy()
+            zo = O.project(pts, O.unit_directions(P, d, 7))
+            scale = np.linalg.norm(pts.astype(np.float64), axis=1).max()
+            err = np.max(np.abs(z - zo)) / scale
+            assert err <= 2e-6 * max(1.0, np.sqrt(d / 50)), (n, d, P, err)
+        print("ok")
+    """)
+    import os
+    env = dict(os.environ, SKS_PROJECTION=mode)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
