@@ -342,6 +342,24 @@ sks::PolyWin poly_win(const sks::FourierPlan& plan) {
   sks::PolyWin pw{};
   pw.w = plan.w;
   for (size_t i = 0; i < sizeof(pw.c) / sizeof(float); ++i) pw.c[i] = i < plan.poly.size() ? plan.poly[i] : 0.f;
+  // centered even / odd form of taps j < w/2 (fp64 binomial re-expansion of the power basis about f = 1/2)
+  constexpr int D = sks::PW_D;
+  static_assert(D == 7, "even/odd split assumes degree 7");
+  for (int j = 0; j < (plan.w + 1) / 2 && j < 6; ++j) {
+    double dm[D + 1] = {0};
+    for (int k = 0; k <= D; ++k) {
+      const double ck = (static_cast<size_t>(j) * (D + 1) + k < plan.poly.size()) ? plan.poly[j * (D + 1) + k] : 0.0;
+      double binom = 1.0;   // C(k, m) (1/2)^{k - m} u^m
+      for (int m = 0; m <= k; ++m) {
+        dm[m] += ck * binom * std::pow(0.5, k - m);
+        binom = binom * (k - m) / (m + 1);
+      }
+    }
+    for (int i = 0; i < 4; ++i) {
+      pw.eo[j][i] = static_cast<float>(dm[2 * i]);
+      pw.eo[j][4 + i] = static_cast<float>(dm[2 * i + 1]);
+    }
+  }
   return pw;
 }
 

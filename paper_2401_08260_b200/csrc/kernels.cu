@@ -56,6 +56,26 @@ __device__ __forceinline__ void poly_taps(const PolyWin& pw, float f, float* out
   }
 }
 
+// all w tap weights from the centered even / odd form: a pair of mirror taps costs 3 + 3 + 2 FMA (vs 2 x 7)
+template <int WT>
+__device__ __forceinline__ void poly_taps_eo(const PolyWin& pw, float f, float* out) {
+  const float u = f - 0.5f, u2 = u * u;
+#pragma unroll
+  for (int j = 0; j < WT / 2; ++j) {
+    const float* e = pw.eo[j];
+    const float E = fmaf(fmaf(fmaf(e[3], u2, e[2]), u2, e[1]), u2, e[0]);
+    const float O = fmaf(fmaf(fmaf(e[7], u2, e[6]), u2, e[5]), u2, e[4]);
+    out[j] = fmaf(u, O, E);
+    out[WT - 1 - j] = fmaf(-u, O, E);
+  }
+  if (WT & 1) {   // middle tap of an odd window
+    const float* e = pw.eo[WT / 2];
+    const float E = fmaf(fmaf(fmaf(e[3], u2, e[2]), u2, e[1]), u2, e[0]);
+    const float O = fmaf(fmaf(fmaf(e[7], u2, e[6]), u2, e[5]), u2, e[4]);
+    out[WT / 2] = fmaf(u, O, E);
+  }
+}
+
 // grid coordinate: identical fp32 op sequence on host (planner footprint) and device
 __device__ __forceinline__ float grid_coord(float z, float cen, float tau, float nf) {
   return __fmul_rn(__fmul_rn(__fsub_rn(z, cen), tau), nf);
@@ -261,15 +281,18 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
   for (int c = lane; c < W * 32; c += 32) mine[c] = 0.f;
   __syncwarp();
   const float nf = static_cast<float>(n), hw = 0.5f * pw.w;
-  const int64_t i0 = blockIdx.x * chunk, i1 = min(zv.N, i0 + chunk);
-  const float* zx = zv.zx + p * zv.ldx;
-  for (int64_t i = i0 + tid; i < i1; i += SP_THREADS) {
+  const int64_t i0 = blockIdx.x * chunk;
+  const int cnt = static_cast<int>(min(zv.N, i0 + chunk) - i0);   // 32-bit loop inside the chunk
+  const float* zx = zv.zx + p * zv.ldx + i0;
+  const float* wc = w + i0;
+  for (int i = tid; i < cnt; i += SP_THREADS) {
     const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);
     const float a = __fsub_rn(v, hw), fl = floorf(a);
     const int l0 = static_cast<int>(fl) + 1;
-    const float wi = __ldg(w + i);
+    const float wi = __ldg(wc + i);
     float tw[WT];
-    poly_taps<WT>(pw, a - fl, tw);
+    if (pw.w == WT) poly_taps_eo<WT>(pw, a - fl, tw);   // mirror pairs need the exact tap count (uniform branch)
+    else poly_taps<WT>(pw, a - fl, tw);                  // generic WT = 12 kernel for other widths
     float* cell = mine + (l0 - f.lmin) * 32 + lane;
 #pragma unroll
     for (int j = 0; j < WT; ++j) cell[j * 32] += wi * tw[j];

@@ -32,6 +32,9 @@ constexpr int PW_D = 7;   // == host kPolyDeg; 8 coefficients = two float4
 struct PolyWin {
   int w;
   float c[12 * (PW_D + 1)];
+  // centered form for spreading: with u = f - 1/2, tap j < w/2 has p_j = E_j(u^2) + u O_j(u^2) and the mirror tap
+  // p_{w-1-j}(f) := p_j(1 - f) = E_j(u^2) - u O_j(u^2)  (the ES window is even); eo[j] = {E_j[0..3], O_j[0..3]}
+  float eo[6][8];
 };
 
 // per-call constants of the closed-form torus coefficients (device planner, row a2)
