@@ -11,6 +11,7 @@
 #include <math_constants.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -285,17 +286,54 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
   const int cnt = static_cast<int>(min(zv.N, i0 + chunk) - i0);   // 32-bit loop inside the chunk
   const float* zx = zv.zx + p * zv.ldx + i0;
   const float* wc = w + i0;
-  for (int i = tid; i < cnt; i += SP_THREADS) {
-    const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);
-    const float a = __fsub_rn(v, hw), fl = floorf(a);
-    const int l0 = static_cast<int>(fl) + 1;
-    const float wi = __ldg(wc + i);
-    float tw[WT];
-    if (pw.w == WT) poly_taps_eo<WT>(pw, a - fl, tw);   // mirror pairs need the exact tap count (uniform branch)
-    else poly_taps<WT>(pw, a - fl, tw);                  // generic WT = 12 kernel for other widths
-    float* cell = mine + (l0 - f.lmin) * 32 + lane;
+  float* base = mine - f.lmin * 32 + lane;   // cell l of this lane's private grid: base[l * 32]
+  if (pw.w == WT && (WT & 1) == 0) {
+    // centered even/odd taps with the coefficients held in registers for the whole loop, two points per
+    // iteration.  The coefficients pass through shared memory: read from the constant bank, ptxas would
+    // re-load them (and move uniform registers into vector ones) inside the loop
+    __shared__ float eos[WT / 2][8];
+    if (tid < WT / 2 * 8) eos[tid / 8][tid % 8] = pw.eo[tid / 8][tid % 8];
+    __syncthreads();
+    float E[WT / 2][4], O[WT / 2][4];
 #pragma unroll
-    for (int j = 0; j < WT; ++j) cell[j * 32] += wi * tw[j];
+    for (int j = 0; j < WT / 2; ++j)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        E[j][k] = eos[j][k];
+        O[j][k] = eos[j][4 + k];
+      }
+    const float taun = f.tau * nf;   // nf = 2^k: ((z - cen) tau) nf == (z - cen) (tau nf) exactly (grid_coord)
+    auto one = [&](float z, float wi) {
+      const float a = __fsub_rn(__fmul_rn(__fsub_rn(z, f.cen), taun), hw), fl = floorf(a);
+      const float u = (a - fl) - 0.5f, u2 = u * u;
+      float* cell = base + (static_cast<int>(fl) + 1) * 32;
+#pragma unroll
+      for (int j = 0; j < WT / 2; ++j) {
+        const float Ej = fmaf(fmaf(fmaf(E[j][3], u2, E[j][2]), u2, E[j][1]), u2, E[j][0]);
+        const float Oj = fmaf(fmaf(fmaf(O[j][3], u2, O[j][2]), u2, O[j][1]), u2, O[j][0]);
+        cell[j * 32] = fmaf(wi, fmaf(u, Oj, Ej), cell[j * 32]);
+        cell[(WT - 1 - j) * 32] = fmaf(wi, fmaf(-u, Oj, Ej), cell[(WT - 1 - j) * 32]);
+      }
+    };
+    int i = tid;
+    for (; i + SP_THREADS < cnt; i += 2 * SP_THREADS) {
+      const float z0 = __ldg(zx + i), z1 = __ldg(zx + i + SP_THREADS);
+      const float w0 = __ldg(wc + i), w1 = __ldg(wc + i + SP_THREADS);
+      one(z0, w0);
+      one(z1, w1);
+    }
+    if (i < cnt) one(__ldg(zx + i), __ldg(wc + i));
+  } else {
+    for (int i = tid; i < cnt; i += SP_THREADS) {
+      const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);
+      const float a = __fsub_rn(v, hw), fl = floorf(a);
+      const float wi = __ldg(wc + i);
+      float tw[WT];
+      poly_taps<WT>(pw, a - fl, tw);                  // generic WT = 12 kernel for other widths
+      float* cell = base + (static_cast<int>(fl) + 1) * 32;
+#pragma unroll
+      for (int j = 0; j < WT; ++j) cell[j * 32] += wi * tw[j];
+    }
   }
   __syncthreads();
   // reduce: cell c -> sum over warps (registers) then lanes (shuffles)
@@ -357,11 +395,14 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_shared(ZView zv, const fl
 cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int n, const PolyWin& pw, int W,
                           float* grid, cudaStream_t st) {
   // chunking: enough CTAs to fill 148 SMs several times, >= 2048 points per CTA to amortise the flush
-  int64_t chunk = 8192;
-  while (chunk > 2048 && ((zv.N + chunk - 1) / chunk) * np < 4 * 148) chunk >>= 1;
+  // (private grids: up to 32768 points per CTA; the fixed-point shared grid keeps <= 8192, its rounding
+  // scales with the chunk's weight)
+  const bool priv = W <= SP_WMAX_PRIV;
+  int64_t chunk = priv ? 32768 : 8192;
+  while (chunk > 2048 && ((zv.N + chunk - 1) / chunk) * np < (priv ? 16 : 4) * 148) chunk >>= 1;
   const unsigned nchunk = static_cast<unsigned>((zv.N + chunk - 1) / chunk);
   if (nchunk == 0) return cudaSuccess;
-  if (W <= SP_WMAX_PRIV) {
+  if (priv) {
     const size_t smem = static_cast<size_t>(SP_WARPS) * W * 32 * sizeof(float);
     auto go = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP_WARPS * SP_WMAX_PRIV * 32 * 4);
@@ -475,6 +516,14 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, 
 // at a time work on the same slice group and its bucket records / grids stay in L2.
 constexpr int EV_THREADS = 256, EV_SG = 32;
 
+bool eval_fast() {   // SKS_EVAL_FAST=0: the generic kernel everywhere (A/B measurements)
+  static const bool v = [] {
+    const char* e = std::getenv("SKS_EVAL_FAST");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 __device__ __forceinline__ double eval_one(const EvalArgs& a, int p, float z, float nf, float hw, int64_t m,
                                            int64_t M) {
   const double zd = z;
@@ -536,10 +585,87 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
   if (a.s64) atomicAdd(a.s64 + m, acc);
 }
 
+// the common case (interpolation polynomials, fp64 target sums, no per-slice output): slice parameters staged
+// in shared memory, the cell's 8 coefficients by one 256-bit load, fp32 partial sums over 4 slices
+__device__ __forceinline__ void ld_q8(const float* q, float4& c0, float4& c1) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(c0.x), "=f"(c0.y), "=f"(c0.z), "=f"(c0.w), "=f"(c1.x), "=f"(c1.y), "=f"(c1.z), "=f"(c1.w)
+      : "l"(q));
+}
+
+template <bool MOMENT>
+__global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a) {
+  __shared__ float4 sp[EV_SG];   // (cen, tau n, Q offset of cell 0 (int bits), -)
+  __shared__ double4 st[MOMENT ? EV_SG : 1];   // (sum w, sum w z, sum w z^2, mom_coef tau) (fp64)
+  const int p0 = blockIdx.y * EV_SG, p1 = min(a.np, p0 + EV_SG);
+  const float nf = static_cast<float>(a.n), hw = 0.5f * a.pw.w;
+  for (int q = threadIdx.x; q < p1 - p0; q += EV_THREADS) {
+    const FPar f = a.fp[p0 + q];
+    // cell l0 = floor(v - w/2) + 1 of slice p reads Q[p][l0 - lminA]: float offset 8 (p WA + l0 - lminA)
+    const int qoff = 8 * ((p0 + q) * a.WA - f.lminA + 1);
+    sp[q] = make_float4(f.cen, f.tau * nf, __int_as_float(qoff), 0.f);
+    if (MOMENT) {
+      const SliceTot T = a.tot[p0 + q];
+      st[q] = make_double4(T.A, T.B, T.C, a.mom_coef * static_cast<double>(f.tau));
+    }
+  }
+  __syncthreads();
+  const int64_t m = blockIdx.x * static_cast<int64_t>(EV_THREADS) + threadIdx.x;
+  if (m >= a.zv.M) return;
+  const float* zy = a.zv.zy + m;
+  auto one = [&](int q, float z) {
+    const float4 c = sp[q];
+    const float av = __fsub_rn(__fmul_rn(__fsub_rn(z, c.x), c.y), hw), fl = floorf(av);
+    const float fr = av - fl;
+    float4 c0, c1;
+    ld_q8(a.Q + (__float_as_int(c.z) + 8 * static_cast<int>(fl)), c0, c1);
+    float t = fmaf(c1.w, fr, c1.z);
+    t = fmaf(t, fr, c1.y);
+    t = fmaf(t, fr, c1.x);
+    t = fmaf(t, fr, c0.w);
+    t = fmaf(t, fr, c0.z);
+    t = fmaf(t, fr, c0.y);
+    return fmaf(t, fr, c0.x);
+  };
+  double acc = 0.0;
+  int p = p0;
+  for (; p + 4 <= p1; p += 4) {   // 4 independent slices in flight per target
+    float z[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) z[k] = __ldg(zy + (p + k) * a.zv.ldy);
+    float part = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) part += one(p - p0 + k, z[k]);
+    acc += part;
+    if (MOMENT)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double zd = z[k];
+        const double4 T = st[p - p0 + k];
+        acc += T.w * (T.z - 2.0 * zd * T.y + zd * zd * T.x);
+      }
+  }
+  for (; p < p1; ++p) {
+    const float z = __ldg(zy + p * a.zv.ldy);
+    acc += one(p - p0, z);
+    if (MOMENT) {
+      const double zd = z;
+      const double4 T = st[p - p0];
+      acc += T.w * (T.z - 2.0 * zd * T.y + zd * zd * T.x);
+    }
+  }
+  atomicAdd(a.s64 + m, acc);
+}
+
 cudaError_t launch_eval(const EvalArgs& a, cudaStream_t st) {
   const unsigned bx = static_cast<unsigned>((a.zv.M + EV_THREADS - 1) / EV_THREADS);
   const unsigned by = static_cast<unsigned>((a.np + EV_SG - 1) / EV_SG);
-  k_eval<<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
+  if (a.fourier && a.Q && a.s64 && !a.per_slice_out && eval_fast()) {
+    if (a.moment) k_eval_q<true><<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
+    else k_eval_q<false><<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
+  } else {
+    k_eval<<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 
