@@ -95,7 +95,7 @@ struct TcSmem {
   static constexpr int B_BYTES = BN * 128;                  // BN directions x 128 bytes
   static constexpr int STAGE = NPIECE * A_BYTES + B_BYTES;  // the pieces share one direction tile
   static constexpr int BAR_OFF = STAGES * STAGE;
-  static constexpr int RANGE_OFF = BAR_OFF + 8 * (2 * STAGES + 4) + 16;
+  static constexpr int RANGE_OFF = (BAR_OFF + 8 * (3 * STAGES + 4) + 16 + 63) / 64 * 64;   // float4-aligned
   static constexpr int FIXED = RANGE_OFF + 1024;            // + per-CTA range partials [np_pad][4], 1/||g|| + slack
 };
 
@@ -103,74 +103,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// min / max of 16 columns (kmn[j] / kmx[j] = this lane's key of column j) over the 32 lanes of a warp: five
-// butterfly stages, each halving the columns a lane keeps; afterwards lanes 2c and 2c + 1 hold column
-// c = 8 b4 + 4 b3 + 2 b2 + b1 (b_k = bit k of the lane).  Destroys kmn / kmx.
-__device__ __forceinline__ void colrange16(uint32_t* kmn, uint32_t* kmx, int b4, int b3, int b2, int b1, uint32_t* omn,
-                                           uint32_t* omx) {
+// min / max of 16 columns (fmn[j] / fmx[j] = this lane's value of column j) over the 32 lanes of a warp by warp
+// reductions (redux.sync f32, sm_100a): lane j (< 16) gets column j's bounds (finite inputs; NaN / Inf are trapped
+// separately)
+__device__ __forceinline__ void colrange16r(const float* fmn, const float* fmx, int lane, float* omn, float* omx) {
+  float mn = CUDART_INF_F, mx = -CUDART_INF_F;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {   // offset 16: keep columns 8 b4 + k
-    const uint32_t smn = b4 ? kmn[k] : kmn[8 + k], smx = b4 ? kmx[k] : kmx[8 + k];
-    const uint32_t rmn = __shfl_xor_sync(0xffffffffu, smn, 16), rmx = __shfl_xor_sync(0xffffffffu, smx, 16);
-    kmn[k] = min(b4 ? kmn[8 + k] : kmn[k], rmn);
-    kmx[k] = max(b4 ? kmx[8 + k] : kmx[k], rmx);
+  for (int j = 0; j < 16; ++j) {
+    float a, b;
+    asm("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(a) : "f"(fmn[j]));
+    asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(b) : "f"(fmx[j]));
+    mn = lane == j ? a : mn;
+    mx = lane == j ? b : mx;
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {   // offset 8
-    const uint32_t smn = b3 ? kmn[k] : kmn[4 + k], smx = b3 ? kmx[k] : kmx[4 + k];
-    const uint32_t rmn = __shfl_xor_sync(0xffffffffu, smn, 8), rmx = __shfl_xor_sync(0xffffffffu, smx, 8);
-    kmn[k] = min(b3 ? kmn[4 + k] : kmn[k], rmn);
-    kmx[k] = max(b3 ? kmx[4 + k] : kmx[k], rmx);
-  }
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {   // offset 4
-    const uint32_t smn = b2 ? kmn[k] : kmn[2 + k], smx = b2 ? kmx[k] : kmx[2 + k];
-    const uint32_t rmn = __shfl_xor_sync(0xffffffffu, smn, 4), rmx = __shfl_xor_sync(0xffffffffu, smx, 4);
-    kmn[k] = min(b2 ? kmn[2 + k] : kmn[k], rmn);
-    kmx[k] = max(b2 ? kmx[2 + k] : kmx[k], rmx);
-  }
-  {   // offset 2
-    const uint32_t smn = b1 ? kmn[0] : kmn[1], smx = b1 ? kmx[0] : kmx[1];
-    const uint32_t rmn = __shfl_xor_sync(0xffffffffu, smn, 2), rmx = __shfl_xor_sync(0xffffffffu, smx, 2);
-    kmn[0] = min(b1 ? kmn[1] : kmn[0], rmn);
-    kmx[0] = max(b1 ? kmx[1] : kmx[0], rmx);
-  }
-  *omn = min(kmn[0], __shfl_xor_sync(0xffffffffu, kmn[0], 1));   // offset 1: both lanes of the pair
-  *omx = max(kmx[0], __shfl_xor_sync(0xffffffffu, kmx[0], 1));
-}
-
-// the same on floats: min / max of the finite values (NaN / Inf are trapped separately)
-__device__ __forceinline__ void colrange16f(float* fmn, float* fmx, int b4, int b3, int b2, int b1, float* omn,
-                                            float* omx) {
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float smn = b4 ? fmn[k] : fmn[8 + k], smx = b4 ? fmx[k] : fmx[8 + k];
-    const float rmn = __shfl_xor_sync(0xffffffffu, smn, 16), rmx = __shfl_xor_sync(0xffffffffu, smx, 16);
-    fmn[k] = fminf(b4 ? fmn[8 + k] : fmn[k], rmn);
-    fmx[k] = fmaxf(b4 ? fmx[8 + k] : fmx[k], rmx);
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float smn = b3 ? fmn[k] : fmn[4 + k], smx = b3 ? fmx[k] : fmx[4 + k];
-    const float rmn = __shfl_xor_sync(0xffffffffu, smn, 8), rmx = __shfl_xor_sync(0xffffffffu, smx, 8);
-    fmn[k] = fminf(b3 ? fmn[4 + k] : fmn[k], rmn);
-    fmx[k] = fmaxf(b3 ? fmx[4 + k] : fmx[k], rmx);
-  }
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const float smn = b2 ? fmn[k] : fmn[2 + k], smx = b2 ? fmx[k] : fmx[2 + k];
-    const float rmn = __shfl_xor_sync(0xffffffffu, smn, 4), rmx = __shfl_xor_sync(0xffffffffu, smx, 4);
-    fmn[k] = fminf(b2 ? fmn[2 + k] : fmn[k], rmn);
-    fmx[k] = fmaxf(b2 ? fmx[2 + k] : fmx[k], rmx);
-  }
-  {
-    const float smn = b1 ? fmn[0] : fmn[1], smx = b1 ? fmx[0] : fmx[1];
-    const float rmn = __shfl_xor_sync(0xffffffffu, smn, 2), rmx = __shfl_xor_sync(0xffffffffu, smx, 2);
-    fmn[0] = fminf(b1 ? fmn[1] : fmn[0], rmn);
-    fmx[0] = fmaxf(b1 ? fmx[1] : fmx[0], rmx);
-  }
-  *omn = fminf(fmn[0], __shfl_xor_sync(0xffffffffu, fmn[0], 1));
-  *omx = fmaxf(fmx[0], __shfl_xor_sync(0xffffffffu, fmx[0], 1));
+  *omn = mn;
+  *omx = mx;
 }
 
 // Persistent: grid = min(#tiles, #SMs) CTAs, tiles t = blockIdx.x + i*gridDim.x (slice tiles fastest, so the
@@ -189,7 +136,8 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nk, int64_t L,
               int64_t Nx, int np, const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz,
               unsigned* __restrict__ mm, int* __restrict__ flag, int emode, const float* __restrict__ px,
-              const float* __restrict__ py, int d) {
+              const float* __restrict__ py, int d, const __grid_constant__ CUtensorMap tmX,
+              const __grid_constant__ CUtensorMap tmY, int xtma) {
   using SM = TcSmem<BN, STAGES, TF32>;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -197,7 +145,8 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;     // [2]
   uint64_t* tempty = tfull + 2;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xfull = tempty + 2;         // [STAGES] TF32x2 with TMA points: the raw fp32 tile (hi piece) landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + STAGES);
   unsigned* rng = reinterpret_cast<unsigned*>(sm + SM::RANGE_OFF);   // [np_pad][4] keys
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntn = (np + BN - 1) / BN;
@@ -209,11 +158,19 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
     rng[4 * c + 0] = 0xffffffffu; rng[4 * c + 1] = 0u; rng[4 * c + 2] = 0xffffffffu; rng[4 * c + 3] = 0u;
   }
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], TF32 ? 5 : 1); mbar_init(&empty[s], TF32 ? 1 : 1); }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], TF32 ? 5 : 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&xfull[s], 1);
+    }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (TF32 && xtma) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
+    }
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -234,7 +191,15 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         unsigned char* sa = sm + stage * SM::STAGE;
-        if (TF32) {   // the points are written by the converter warps; TMA brings the direction tile
+        if (TF32) {   // TMA brings the direction tile (and, with xtma, the raw fp32 points = the hi piece)
+          if (xtma) {
+            // rows m0 .. m0 + 127 of the concatenated points: x rows from tmX, y rows from tmY (rows outside a
+            // map are zero-filled); a tile straddling x / y lands its y rows in the lo slot, merged by the converters
+            const bool hasx = m0 < Nx, hasy = m0 + TC_M > Nx && L > Nx;
+            mbar_expect_tx(&xfull[stage], (hasx && hasy ? 2 : 1) * SM::A_BYTES);
+            if (hasx) tma_load_2d(&tmX, &xfull[stage], sa, kb * 32, m0);
+            if (hasy) tma_load_2d(&tmY, &xfull[stage], hasx ? sa + SM::A_BYTES : sa, kb * 32, static_cast<int>(m0 - Nx));
+          }
           mbar_expect_tx(&full[stage], SM::B_BYTES);
           tma_load_2d(&tmB, &full[stage], sa + 2 * SM::A_BYTES, kb * 32, n0);
         } else {
@@ -299,6 +264,41 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
     //      row r, 16-byte chunk c at r * 128 + ((c ^ (r % 8)) * 16).  Lane l: chunk l % 8 of rows 4 i + l / 8.
     const int cw = warp - 12;   // 0..3: rows 32 cw .. 32 cw + 31
     const int c = lane & 7, rsub = lane >> 3;
+    if (xtma) {
+      // the raw fp32 tile is the hi operand as it stands: kind::tf32 reads the top 19 bits of each 32-bit
+      // container (truncation), so lo = x - trunc_tf32(x) completes it exactly in fp32
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t m0 = (t / ntn) * TC_M;
+        const int split = (m0 < Nx && m0 + TC_M > Nx) ? static_cast<int>(Nx - m0) : TC_M;   // y rows >= split
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&xfull[stage], phase);
+          unsigned char* sa = sm + stage * SM::STAGE;
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int r = 32 * cw + 4 * it + rsub;
+            const int off = r * 128 + ((c ^ (r & 7)) << 4);
+            float4 v;
+            if (r < split) {
+              v = *reinterpret_cast<const float4*>(sa + off);
+            } else {   // straddling tile: the y rows were loaded into the lo slot
+              v = *reinterpret_cast<const float4*>(sa + SM::A_BYTES + off);
+              *reinterpret_cast<float4*>(sa + off) = v;
+            }
+            const float4 lo = make_float4(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u),
+                                          v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u),
+                                          v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u),
+                                          v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
+            *reinterpret_cast<float4*>(sa + SM::A_BYTES + off) = lo;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    } else {
     const bool vec = (d & 3) == 0;   // rows 16-byte aligned: one 16-byte load per chunk
     // software pipeline: the 8 chunks of the next (tile, k-block) are loaded into registers while the current
     // ones are converted and stored
@@ -354,15 +354,13 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
       t = tn;
       kb = kn;
     }
+    }
   } else if (warp >= 4 && warp < 12) {
     // ---- epilogue: warp w handles TMEM lane quadrant q = w % 4 (points m0 + 32q + lane) and the column half
-    //      h = (w - 4) / 4 of the accumulator.  Per 16-column chunk: scale, store (coalesced along points),
-    //      order-preserving keys, and the per-column min / max over the warp's 32 points by a butterfly that
-    //      halves the columns at every shuffle stage (16 columns -> one column per lane pair in 5 stages).
+    //      h = (w - 4) / 4 of the accumulator.  Per 16-column chunk: scale, store (coalesced along points), and
+    //      the per-column min / max over the warp's 32 points by warp reductions (colrange16r).
     const int q = warp & 3, h = (warp - 4) >> 2;
     constexpr int HALF = BN / 2;
-    const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
-    const int my_col = 8 * b4 + 4 * b3 + 2 * b2 + b1;   // column of the chunk this lane pair ends up holding
     float trap = 0.f;   // becomes NaN if a projection is NaN / Inf (in x, y or an overflow)
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -439,8 +437,10 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
           }
         }
         if (emode == 2) { trap += fmn[0] * 0.f; continue; }   // measurement: scale + store only
+        // per-column min / max over the warp's 32 points: one warp reduction per column and bound (redux.sync
+        // f32, sm_100a), lane j keeps column j
         float amn, amx;
-        colrange16f(fmn, fmx, b4, b3, b2, b1, &amn, &amx);
+        colrange16r(fmn, fmx, lane, &amn, &amx);
         float xmn = amn, xmx = amx;
         if (mixed) {   // the warp holding the x/y boundary: x-only ranges separately
 #pragma unroll
@@ -450,10 +450,10 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
             fmn[j] = ok ? z : CUDART_INF_F;
             fmx[j] = ok ? z : -CUDART_INF_F;
           }
-          colrange16f(fmn, fmx, b4, b3, b2, b1, &xmn, &xmx);
+          colrange16r(fmn, fmx, lane, &xmn, &xmx);
         }
-        if ((lane & 1) == 0 && my_col < nc) {
-          const int s = n0 + c0 + my_col;
+        if (lane < nc) {
+          const int s = n0 + c0 + lane;
           if (amn <= amx) { atomicMin(&rng[4 * s + 2], f2key_tc(amn)); atomicMax(&rng[4 * s + 3], f2key_tc(amx)); }
           if (warp_any_x && xmn <= xmx) {
             atomicMin(&rng[4 * s + 0], f2key_tc(xmn));
@@ -563,7 +563,8 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_k, 
 template <int BN, int STAGES, bool TF32 = false>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int64_t L, int64_t Nx, int np,
                       const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, unsigned* part,
-                      cudaStream_t st, const float* px = nullptr, const float* py = nullptr, int d = 0) {
+                      cudaStream_t st, const float* px = nullptr, const float* py = nullptr, int d = 0,
+                      const CUtensorMap* tx = nullptr, const CUtensorMap* ty = nullptr) {
   using SM = TcSmem<BN, STAGES, TF32>;
   const int ntn = (np + BN - 1) / BN;
   const size_t smem = SM::FIXED + static_cast<size_t>(20) * ntn * BN;
@@ -575,8 +576,9 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int6
   const int64_t ntiles = ((L + TC_M - 1) / TC_M) * ntn;
   const int grid = static_cast<int>(ntiles < kProjMaxCtas ? ntiles : kProjMaxCtas);
   static const int emode = std::getenv("SKS_PROJ_EMODE") ? std::atoi(std::getenv("SKS_PROJ_EMODE")) : 0;
+  const int xtma = tx != nullptr;
   k_proj_tc<BN, STAGES, TF32><<<grid, TF32 ? TC_THREADS_TF32 : TC_THREADS, smem, st>>>(
-      ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, emode, px, py, d);
+      ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, emode, px, py, d, xtma ? *tx : ta, xtma ? *ty : ta, xtma);
   (void)part;
   return cudaGetLastError();
 }
@@ -590,6 +592,20 @@ bool make_map_f32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
   const cuuint32_t box[2] = {32, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// raw fp32 points [rows][d] for the TF32x2 path: box 32 dims x 128 rows, 128-byte swizzle (the hi operand layout);
+// dims >= d and rows outside [0, rows) are zero-filled
+bool make_map_pts(CUtensorMap* m, const float* base, uint64_t rows, uint64_t d) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t gdim[2] = {d, rows};
+  const cuuint64_t gstride[1] = {d * 4};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(TC_M)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -609,6 +625,19 @@ cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64
   const int64_t L = N + M;
   CUtensorMap ta;
   std::memset(&ta, 0, sizeof(ta));   // unused by the TF32 path
+  // raw points by TMA (fp32 rows of d floats, box 32 dims x 128 rows, 128-byte swizzle): needs 16-byte row
+  // strides and bases; otherwise the converter warps load them
+  static const bool xtma_env = !std::getenv("SKS_PROJ_XTMA") || std::atoi(std::getenv("SKS_PROJ_XTMA")) != 0;
+  CUtensorMap tx, ty;
+  const bool aligned = (d % 4) == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0 &&
+                       (M == 0 || (reinterpret_cast<uintptr_t>(y) % 16) == 0);
+  bool xtma = xtma_env && aligned && N > 0;
+  if (xtma) {
+    xtma = make_map_pts(&tx, x, static_cast<uint64_t>(N), static_cast<uint64_t>(d)) &&
+           (M == 0 ? (ty = tx, true) : make_map_pts(&ty, y, static_cast<uint64_t>(M), static_cast<uint64_t>(d)));
+  }
+  const CUtensorMap* ptx = xtma ? &tx : nullptr;
+  const CUtensorMap* pty = xtma ? &ty : nullptr;
   constexpr int kSliceChunk = 1024;
   for (int s0 = 0; s0 < np; s0 += kSliceChunk) {
     const int ns = std::min(kSliceChunk, np - s0);
@@ -621,9 +650,9 @@ cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64
     unsigned* mmc = mm + 4 * s0;
     const float* ic = inv_norm + s0;
     cudaError_t e;
-    if (BN == 256) e = launch_tc<256, 3, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d);
-    else if (BN == 128) e = launch_tc<128, 4, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d);
-    else e = launch_tc<64, 4, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d);
+    if (BN == 256) e = launch_tc<256, 3, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
+    else if (BN == 128) e = launch_tc<128, 4, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
+    else e = launch_tc<64, 4, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
