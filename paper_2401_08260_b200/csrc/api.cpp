@@ -167,9 +167,13 @@ bool use_sort_v1() {
 
 // row a1 variant: 0 SIMT fp32 (measurement A/B), 1 BF16x3 (split kernel + three bf16 MMAs), 2 TF32x2 (split
 // inside the kernel, two tf32 MMAs).  TF32x2 reads the fp32 points once and needs no split buffer, at 4/3 of the
-// tensor work of BF16x3: the default for d <= 256, where the projection is HBM-bound; BF16x3 above.
-// SKS_PROJECTION = simt | bf16x3 | tf32x2 overrides.
+// tensor work of BF16x3.  With the points read by TMA (the raw fp32 tile is the hi operand) it is the faster one
+// at every d (cfg3 0.56 vs 0.59 ms, cfg4 1.64 vs 1.79 ms including the split pass); without (unaligned points,
+// d % 4 != 0) its converter warps load the points and BF16x3 wins above d = 256.  proj_mode(d) sizes the
+// workspace (the split buffer above d = 256); use_tf32(...) decides per call.  SKS_PROJECTION = simt | bf16x3 |
+// tf32x2 overrides.
 enum ProjMode { PM_SIMT = 0, PM_BF16X3 = 1, PM_TF32X2 = 2 };
+bool proj_forced() { return std::getenv("SKS_PROJECTION") != nullptr; }
 ProjMode proj_mode(int d) {
   static int v = -2;
   if (v == -2) {
@@ -490,7 +494,8 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     SKS_CUDA(sks::launch_zero(ws + L.s64, al(sizeof(double) * pr.M), st));
   }
   launches += s_out ? 2 : 1;
-  const ProjMode pm = proj_mode(pr.d);
+  ProjMode pm = proj_mode(pr.d);
+  if (pm == PM_BF16X3 && !proj_forced() && sks::proj_tf32_tma_ok(x, pr.N, y, pr.M, pr.d)) pm = PM_TF32X2;
   const bool tc = pr.with_Z && pm == PM_BF16X3;
   const bool tf = pr.with_Z && pm == PM_TF32X2;
   if (tc) {
@@ -809,7 +814,8 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
   // first use, grown on demand; this entry point is a test/inspection aid, not the hot path)
   static thread_local unsigned* scratch = nullptr;
   static thread_local size_t scratch_bytes = 0;
-  const ProjMode pm = proj_mode(d);
+  ProjMode pm = proj_mode(d);
+  if (pm == PM_BF16X3 && !proj_forced() && sks::proj_tf32_tma_ok(pts, n, pts, 0, d)) pm = PM_TF32X2;
   const bool tc = pm == PM_BF16X3;
   const size_t need = al(sizeof(unsigned) * 4 * np + 16) +
                       (tc ? al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n) + al(sks::proj_tc_part_bytes(np)) : 0);

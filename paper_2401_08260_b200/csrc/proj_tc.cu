@@ -613,6 +613,12 @@ bool make_map_pts(CUtensorMap* m, const float* base, uint64_t rows, uint64_t d) 
 }  // namespace
 
 int proj_tc_dpad(int d) { return (d + TC_BK - 1) / TC_BK * TC_BK; }
+
+bool proj_tf32_tma_ok(const float* x, int64_t N, const float* y, int64_t M, int d) {
+  static const bool env = !std::getenv("SKS_PROJ_XTMA") || std::atoi(std::getenv("SKS_PROJ_XTMA")) != 0;
+  return env && (d % 4) == 0 && N > 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0 &&
+         (M == 0 || (reinterpret_cast<uintptr_t>(y) % 16) == 0);
+}
 int proj_tf32_dpad(int d) { return (d + 31) / 32 * 32; }
 
 // Z = X G^T with the TF32x2 split done inside the kernel (converter warps read the fp32 points directly):
@@ -627,11 +633,8 @@ cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64
   std::memset(&ta, 0, sizeof(ta));   // unused by the TF32 path
   // raw points by TMA (fp32 rows of d floats, box 32 dims x 128 rows, 128-byte swizzle): needs 16-byte row
   // strides and bases; otherwise the converter warps load them
-  static const bool xtma_env = !std::getenv("SKS_PROJ_XTMA") || std::atoi(std::getenv("SKS_PROJ_XTMA")) != 0;
   CUtensorMap tx, ty;
-  const bool aligned = (d % 4) == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0 &&
-                       (M == 0 || (reinterpret_cast<uintptr_t>(y) % 16) == 0);
-  bool xtma = xtma_env && aligned && N > 0;
+  bool xtma = proj_tf32_tma_ok(x, N, y, M, d);
   if (xtma) {
     xtma = make_map_pts(&tx, x, static_cast<uint64_t>(N), static_cast<uint64_t>(d)) &&
            (M == 0 ? (ty = tx, true) : make_map_pts(&ty, y, static_cast<uint64_t>(M), static_cast<uint64_t>(d)));
