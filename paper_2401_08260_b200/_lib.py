@@ -29,7 +29,8 @@ class sks_plan_info(ctypes.Structure):
                 ("band_lo_min", ctypes.c_int32), ("window_w", ctypes.c_int32), ("spread_cells", ctypes.c_int32),
                 ("n_buckets", ctypes.c_int32), ("slice_batch", ctypes.c_int32), ("n_batches", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("tau_min", ctypes.c_double), ("tau_max", ctypes.c_double),
-                ("engine", ctypes.c_int32), ("band_width", ctypes.c_int32)]
+                ("engine", ctypes.c_int32), ("band_width", ctypes.c_int32),
+                ("proj_mode", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

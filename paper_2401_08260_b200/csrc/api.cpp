@@ -665,6 +665,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
   info.slice_batch = batch;
   info.n_batches = nbatches;
   info.launches = launches;
+  info.proj_mode = !pr.with_Z ? 0 : tc ? 2 : tf ? 3 : 1;
   if (!pt.fourier) info.tau_min = 0;
   g_plan = info;
   return SKS_OK;
