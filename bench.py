@@ -137,6 +137,19 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def rows(self):
+        try:
+            return sum(1 for r in open(self.path) if r.strip())
+        except OSError:
+            return 0
+
+    def wait_rows(self, n, timeout_s):
+        """block until the sampler has written at least n rows (short timed regions: nvidia-smi needs ~0.1-1 s
+        to start, so the region is bracketed by samples taken just before and just after it)"""
+        t0 = time.perf_counter()
+        while self.proc is not None and self.rows() < n and time.perf_counter() - t0 < timeout_s:
+            time.sleep(0.02)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -275,6 +288,8 @@ def main():
     S.sks_profile_enable(True)
     S.sks_profile_read()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks.wait_rows(1, 5.0)
+    r0 = clocks.rows()
     if G > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -286,6 +301,7 @@ def main():
     torch.cuda.synchronize()
     if G > 1:
         dist.barrier()
+    clocks.wait_rows(r0 + 1, 1.0)
     clk = clocks.stop()
     prof = S.sks_profile_read()
     S.sks_profile_enable(False)

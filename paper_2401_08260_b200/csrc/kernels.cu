@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
   const float* wc = w + i0;
   float* base = mine - f.lmin * 32 + lane;   // cell l of this lane's private grid: base[l * 32]
   if (pw.w == WT && (WT & 1) == 0) {
-    // centered even/odd taps with the coefficients held in registers for the whole loop, two points per
+    // centered even/odd taps with the coefficients held in registers for the whole loop, four points per
     // iteration.  The coefficients pass through shared memory: read from the constant bank, ptxas would
     // re-load them (and move uniform registers into vector ones) inside the loop
     __shared__ float eos[WT / 2][8];
@@ -315,14 +315,19 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
         cell[(WT - 1 - j) * 32] = fmaf(wi, fmaf(-u, Oj, Ej), cell[(WT - 1 - j) * 32]);
       }
     };
-    int i = tid;
-    for (; i + SP_THREADS < cnt; i += 2 * SP_THREADS) {
-      const float z0 = __ldg(zx + i), z1 = __ldg(zx + i + SP_THREADS);
-      const float w0 = __ldg(wc + i), w1 = __ldg(wc + i + SP_THREADS);
-      one(z0, w0);
-      one(z1, w1);
+    int i0 = 0;
+    if (((reinterpret_cast<uintptr_t>(zx) | reinterpret_cast<uintptr_t>(wc)) & 15) == 0) {
+      // four consecutive points per thread by 16-byte loads (coalesced, all four in flight)
+      for (; i0 + 4 * SP_THREADS <= cnt; i0 += 4 * SP_THREADS) {
+        const float4 z = __ldg(reinterpret_cast<const float4*>(zx + i0) + tid);
+        const float4 ww = __ldg(reinterpret_cast<const float4*>(wc + i0) + tid);
+        one(z.x, ww.x);
+        one(z.y, ww.y);
+        one(z.z, ww.z);
+        one(z.w, ww.w);
+      }
     }
-    if (i < cnt) one(__ldg(zx + i), __ldg(wc + i));
+    for (int i = i0 + tid; i < cnt; i += SP_THREADS) one(__ldg(zx + i), __ldg(wc + i));
   } else {
     for (int i = tid; i < cnt; i += SP_THREADS) {
       const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);

@@ -470,8 +470,11 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  // this CTA's per-slice ranges into the global ranges (one atomic per slice and bound; ~148-way contention)
-  for (int e = threadIdx.x; e < 4 * np; e += blockDim.x) {
+  // this CTA's per-slice ranges into the global ranges (one atomic per slice and bound it touched); each CTA
+  // starts at a different slice so that the CTAs finishing together do not queue on the same addresses
+  const int ne = 4 * np, e0 = static_cast<int>((static_cast<int64_t>(blockIdx.x) * 4 * 61) % ne);
+  for (int k = threadIdx.x; k < ne; k += blockDim.x) {
+    const int e = (e0 + k) % ne;
     const unsigned v = rng[e];
     if ((e & 1) == 0) {
       if (v != 0xffffffffu) atomicMin(mm + e, v);

@@ -17,4 +17,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   python bench.py --config cfg3 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $out/${tag}_launches_cfg3.csv 2> /dev/null
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_sp_(owner|part|hist)" -c 3 \
   -o $out/${tag}_sort_full python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_proj_tc|k_spread|k_eval" -c 3 \
+  -o $out/${tag}_cfg3_full python bench.py --config cfg3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 ls -la $out | grep $tag
