@@ -591,7 +591,8 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
 }
 
 // the common case (interpolation polynomials, fp64 target sums, no per-slice output): slice parameters staged
-// in shared memory, the cell's 8 coefficients by one 256-bit load, fp32 partial sums over 4 slices
+// in shared memory, the cell's 8 coefficients by one 256-bit load, fp32 partial sums over EV_U slices
+constexpr int EV_U = 8;
 __device__ __forceinline__ void ld_q8(const float* q, float4& c0, float4& c1) {
   asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=f"(c0.x), "=f"(c0.y), "=f"(c0.z), "=f"(c0.w), "=f"(c1.x), "=f"(c1.y), "=f"(c1.z), "=f"(c1.w)
@@ -634,17 +635,26 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a) {
   };
   double acc = 0.0;
   int p = p0;
-  for (; p + 4 <= p1; p += 4) {   // 4 independent slices in flight per target
-    float z[4];
+  // EV_U independent slices in flight per target; the projections of the next EV_U slices are loaded before the
+  // current ones are evaluated (the kernel is bound by the latency of the z -> coefficient load chain)
+  float zn[EV_U];
+  if (p + EV_U <= p1)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) z[k] = __ldg(zy + (p + k) * a.zv.ldy);
+    for (int k = 0; k < EV_U; ++k) zn[k] = __ldg(zy + (p + k) * a.zv.ldy);
+  for (; p + EV_U <= p1; p += EV_U) {
+    float z[EV_U];
+#pragma unroll
+    for (int k = 0; k < EV_U; ++k) z[k] = zn[k];
+    if (p + 2 * EV_U <= p1)
+#pragma unroll
+      for (int k = 0; k < EV_U; ++k) zn[k] = __ldg(zy + (p + EV_U + k) * a.zv.ldy);
     float part = 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) part += one(p - p0 + k, z[k]);
+    for (int k = 0; k < EV_U; ++k) part += one(p - p0 + k, z[k]);
     acc += part;
     if (MOMENT)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < EV_U; ++k) {
         const double zd = z[k];
         const double4 T = st[p - p0 + k];
         acc += T.w * (T.z - 2.0 * zd * T.y + zd * zd * T.x);
