@@ -11,7 +11,8 @@
 // B200 design (measured, scratch/ubench_scatter.cu): a scattered 4-8 byte global or DSMEM access costs
 // 1-3 SM cycles per element, a random local shared-memory access 0.2.  So every random access of the
 // method is kept in the local shared memory of one CTA, and data moves between CTAs only in coalesced runs:
-//   S0 k_sp_hist   per slice: histogram of the x and y projections over NH equal bins of [xmin, xmax]
+//   S0 k_sp_hist   per chunk: histogram of the x and y projections over NH equal bins of [xmin, xmax] into the
+//                  chunk's own slot (no global atomics); the last chunk of a slice sums them
 //                  (+ slice totals sum w, sum w x, sum w x^2 in fp64 for the Laplacian moment term)
 //   S1 k_sp_plan   per slice: bins -> G owners balanced by x count (owner = contiguous bin range, so the
 //                  key k = (owner, fine bucket) stays monotone); region offsets of every owner
@@ -129,7 +130,7 @@ __device__ __forceinline__ T block_excl_scan(T v, T* wbuf, T* total) {
 // (ticket counter per slice): owner of bin b = floor(cx[b] G / Nx) with cx the exclusive prefix x count, so
 // the owners are contiguous bin ranges (monotone) holding <= Nx/G + (largest bin) x each.
 __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __restrict__ mm, int NH, int G,
-                                                  int ncx, int nchunks, int NBF, int* __restrict__ H,
+                                                  int ncx, int nchunks, int chx, int chy, int NBF, int* __restrict__ H,
                                                   int* __restrict__ done, uint16_t* __restrict__ om,
                                                   SpOwner* __restrict__ own) {
   extern __shared__ int hs[];   // [NH] histogram; in the plan: cx[NH + 1], cy[NH + 1], blo[G + 1]
@@ -140,7 +141,8 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
   const int c = isx ? blockIdx.x : blockIdx.x - ncx;
   const int n = static_cast<int>(isx ? zv.N : zv.M);
   const float* z = isx ? zv.zx + p * zv.ldx : zv.zy + p * zv.ldy;
-  const int i0 = c * S0_CH, i1 = min(n, i0 + S0_CH);
+  const int ch = isx ? chx : chy;
+  const int i0 = c * ch, i1 = min(n, i0 + ch);
   const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
   const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
   const float uoff = -xmin * hscale;
@@ -170,9 +172,9 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
       }
   }
   __syncthreads();
-  int* Hp = H + (static_cast<int64_t>(p) * 2 + (isx ? 0 : 1)) * NH;
-  for (int b = tid; b < NH; b += S0_T)
-    if (hs[b]) atomicAdd(Hp + b, hs[b]);
+  // the chunk's histogram into its own slot (plain coalesced stores; the plan sums the chunks)
+  int* Hp = H + (static_cast<int64_t>(p) * nchunks + blockIdx.x) * NH;
+  for (int b = tid; b < NH; b += S0_T) __stcg(Hp + b, hs[b]);
   __threadfence();
   __syncthreads();
   if (tid == 0) last = (atomicAdd(done + p, 1) == nchunks - 1);
@@ -183,18 +185,27 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
   int* cx = hs;
   int* cy = cx + NH + 1;
   int* blo = cy + NH + 1;
-  const int* hx = H + static_cast<int64_t>(p) * 2 * NH;
-  const int* hy = hx + NH;
+  const int* hp = H + static_cast<int64_t>(p) * nchunks * NH;
+  // per bin: x and y counts summed over the chunks (into cx / cy, then scanned in place)
+  for (int b = tid; b < NH; b += S0_T) {
+    int sx = 0, sy = 0;
+    for (int q = 0; q < ncx; ++q) sx += __ldcg(hp + static_cast<int64_t>(q) * NH + b);
+    for (int q = ncx; q < nchunks; ++q) sy += __ldcg(hp + static_cast<int64_t>(q) * NH + b);
+    cx[b] = sx;
+    cy[b] = sy;
+  }
+  __syncthreads();
   const int per = (NH + S0_T - 1) / S0_T;
   const int b0 = min(NH, tid * per), b1 = min(NH, b0 + per);
   int lx = 0, ly = 0;
-  for (int b = b0; b < b1; ++b) { lx += __ldcg(hx + b); ly += __ldcg(hy + b); }
+  for (int b = b0; b < b1; ++b) { lx += cx[b]; ly += cy[b]; }
   int tx, ty;
   int rx = block_excl_scan<S0_T>(lx, wbuf, &tx);
   int ry = block_excl_scan<S0_T>(ly, wbuf, &ty);
   for (int b = b0; b < b1; ++b) {
+    const int vx = cx[b], vy = cy[b];
     cx[b] = rx; cy[b] = ry;
-    rx += __ldcg(hx + b); ry += __ldcg(hy + b);
+    rx += vx; ry += vy;
   }
   if (tid == 0) { cx[NH] = tx; cy[NH] = ty; }
   for (int o = tid; o <= G; o += S0_T) blo[o] = (o == 0) ? 0 : NH;
@@ -426,7 +437,6 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
       if (tid == 0) S.start[SP_NBF] = total;
     }
     __syncthreads();
-#pragma unroll
     constexpr int XB = S3_PER < 8 ? S3_PER : 8;
 #pragma unroll
     for (int h = 0; h < S3_PER; h += XB) {   // second read of the pass's x (L2), XB in flight per thread
@@ -629,13 +639,19 @@ __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, dou
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// histogram chunks of a slice part: S0_CH elements each, at most S0_MAXC chunks (then longer chunks)
+constexpr int S0_MAXC = 8;
+inline int hist_chunks(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(S0_MAXC, cdiv(n, S0_CH)))); }
+inline int hist_chunk_len(int64_t n) { return static_cast<int>(std::max<int64_t>(1, cdiv(n, hist_chunks(n)))); }
+
 }  // namespace
 
 SpDims sortpart_dims(int64_t N, int64_t M) {
   SpDims d;
-  // histogram bins: ~16 x per bin on average, at least 2048, at most 16384 (u16 owner map in shared memory)
+  // histogram bins: ~64 x per bin on average (owners of ~3000 x balance to a bin), at least 2048, at most 16384
+  // (u16 owner map in shared memory)
   int nh = 2048;
-  while (nh < 16384 && nh * 16 < N) nh *= 2;
+  while (nh < 16384 && nh * 64 < N) nh *= 2;
   d.NH = nh;
   // owners: 3/4 of the owner capacity each (room for the bin granularity of the balance)
   int64_t g = cdiv(N, kSpVars[sp_variant()].cap * 3 / 4);
@@ -677,7 +693,7 @@ static size_t region_bytes(int64_t N, int64_t M, int np) {
   const SpDims d = sortpart_dims(N, M);
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   size_t s = 0;
-  s += al(sizeof(int) * 2 * d.NH * static_cast<size_t>(np));          // H
+  s += al(sizeof(int) * (hist_chunks(N) + hist_chunks(M)) * d.NH * static_cast<size_t>(np));   // H (per chunk)
   s += al(sizeof(int) * 2 * d.G * static_cast<size_t>(np));           // cursors
   s += al(sizeof(int) * static_cast<size_t>(np));                     // done tickets
   s += al(sizeof(double) * 4 * d.G * static_cast<size_t>(np));        // owner totals
@@ -725,10 +741,10 @@ StreamPool& stream_pool() {   // per process (the library is used on one device 
 namespace {
 // scratch of one slice group (one region per stream; regions are reused by the groups of that stream)
 struct SpRegion {
-  int* H;           // [gs][2][NH] histograms           } zeroed per group
-  int* cursor;      // [gs][2][G] mailbox cursors       }
+  int* cursor;      // [gs][2][G] mailbox cursors       } zeroed per group
   int* done;        // [gs] histogram tickets           }
   size_t zero_bytes;
+  int* H;           // [gs][chunks][NH] chunk histograms
   double* otot;     // [gs][G][4] owner totals (w, w z, w z^2)
   double2* dab;     // [gs][G] other-owner coefficients
   uint16_t* yown;   // [gs][M] owner of each target
@@ -745,10 +761,10 @@ SpRegion carve_region(char* base, int64_t N, int64_t M, int NH, int G, int gs) {
   const size_t g = static_cast<size_t>(gs);
   SpRegion r;
   char* w = base;
-  r.H = reinterpret_cast<int*>(w);            w += al(sizeof(int) * 2 * NH * g);
   r.cursor = reinterpret_cast<int*>(w);       w += al(sizeof(int) * 2 * G * g);
   r.done = reinterpret_cast<int*>(w);         w += al(sizeof(int) * g);
   r.zero_bytes = static_cast<size_t>(w - base);
+  r.H = reinterpret_cast<int*>(w);            w += al(sizeof(int) * (hist_chunks(N) + hist_chunks(M)) * NH * g);
   r.otot = reinterpret_cast<double*>(w);      w += al(sizeof(double) * 4 * G * g);
   r.dab = reinterpret_cast<double2*>(w);      w += al(sizeof(double2) * G * g);
   r.yown = reinterpret_cast<uint16_t*>(w);    w += al(sizeof(uint16_t) * M * g);
@@ -782,7 +798,7 @@ void set_attributes() {
 cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int np, int NH, int G, cudaStream_t st) {
   const int64_t N = a.zv.N, M = a.zv.M;
   constexpr int wpc = 4;   // partition: 256-element rounds per warp
-  const int ncx0 = static_cast<int>(cdiv(N, S0_CH)), ncy0 = static_cast<int>(cdiv(M, S0_CH));
+  const int ncx0 = hist_chunks(N), ncy0 = hist_chunks(M);
   const int64_t per_cta2 = int64_t(S2W_WARPS) * S2W_WCH * wpc;
   const int ncx2 = static_cast<int>(cdiv(N, per_cta2)), ncy2 = static_cast<int>(cdiv(M, per_cta2));
   const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1);
@@ -792,11 +808,12 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   zv.zy += g0 * zv.ldy;
   const unsigned* mm = a.mm + 4 * g0;
   float* pso = a.per_slice_out ? a.per_slice_out + static_cast<int64_t>(g0) * M : nullptr;
-  cudaError_t e = cudaMemsetAsync(r.H, 0, r.zero_bytes, st);
+  cudaError_t e = cudaMemsetAsync(r.cursor, 0, r.zero_bytes, st);
   if (e != cudaSuccess) return e;
   ProfMark pm = prof_begin(PS_SP_HIST, st);
-  k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, kSpVars[sp_variant()].nbf, r.H,
-                                                       r.done, r.om, r.own);
+  k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, hist_chunk_len(N),
+                                                       hist_chunk_len(M), kSpVars[sp_variant()].nbf, r.H, r.done, r.om,
+                                                       r.own);
   prof_end(pm);
   pm = prof_begin(PS_SP_PART, st);
   k_sp_part<<<dim3(ncx2 + ncy2, np), S2W_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, wpc, r.om, r.own, r.cursor, r.Xmb,
