@@ -393,6 +393,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
   // every owner publishes its x totals (sum w, sum w z, sum w z^2; fp64) for the other owners' targets
   // (k_sp_outer), so an owner without targets still sums its x
   __shared__ double own_tot[3];
+  __shared__ double wvc[S3_T / 32];   // per-warp sum w z^2 of the pass (shared fp64 atomics are CAS loops)
   if (tid < 3) own_tot[tid] = 0.0;
   const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
   const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
@@ -450,11 +451,11 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
     __syncthreads();
     // ---- fp64 bucket sums (thread t: buckets t, t + S3_T, ...: neighbouring lanes read neighbouring buckets)
     //      into rec[], then one blocked exclusive scan (thread t: buckets 4t .. 4t+3)
+    double vc = 0.0;   // sum w z^2 of this thread's buckets (per-warp partials, summed by thread 0 below)
 #pragma unroll
     for (int c0 = 0; c0 < SP_NBF; c0 += S3_T) {
       const int b = c0 + tid;
       double2 v = make_double2(0.0, 0.0);
-      double vc = 0.0;
       for (int i = S.start[b], e = S.start[b + 1]; i < e; ++i) {
         const float2 q = S.xs[i];
         const double wz = static_cast<double>(q.y) * q.x;
@@ -463,9 +464,9 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
         vc += wz * q.x;
       }
       S.rec[b] = v;
-      vc = warp_sum_sp(vc);
-      if ((tid & 31) == 0) atomicAdd(&own_tot[2], vc);
     }
+    vc = warp_sum_sp(vc);
+    if ((tid & 31) == 0) wvc[tid >> 5] = vc;
     __syncthreads();
     {
       constexpr int PB = SP_NBF / S3_T;
@@ -480,6 +481,10 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
         S.rec[SP_NBF] = tch;
         own_tot[0] += tch.x;
         own_tot[1] += tch.y;
+        double c2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < S3_T / 32; ++q) c2 += wvc[q];
+        own_tot[2] += c2;
       }
     }
     __syncthreads();
