@@ -67,7 +67,7 @@ def roofline_model(slot, cfg, P, plan):
     if slot == "split3":        # fp32 points -> 3 bf16 pieces
         return 4 * L * d + 6 * L * dp, 0
     if slot == "project":       # Z = X G^T, 2 L d P fp32-accurate flops.  BF16x3 (plan proj_mode 2): read the 3
-        if plan.get("proj_mode") == 2:   # bf16 pieces and G, write Z; TF32x2 (3): read the fp32 points
+        if plan.get("proj_mode") == 2:   # bf16 pieces and G, write Z; TF32x2 (3) / FP16x2 (4): the fp32 points
             return 6 * L * dp + 2 * P * dp + 4 * L * P, ("tensor", 2.0 * L * d * P)
         dp32 = (d + 31) // 32 * 32
         return 4 * L * d + 4 * P * dp32 + 4 * L * P, ("tensor", 2.0 * L * d * P)
@@ -101,11 +101,14 @@ def roofline(slot, cfg, P, plan, ms_per_launch, pk, traffic):
     by, fl = roofline_model(slot, cfg, P, plan)
     kind, fl = fl if fl else (None, 0.0)
     t = ms_per_launch * 1e-3
-    tf32 = plan.get("proj_mode") == 3
-    peaks_tf = {"tensor": pk["bf16_tflops"] / (4.0 if tf32 else 3.0),
+    pmode = plan.get("proj_mode")
+    tdiv = {3: 4.0, 4: 2.0}.get(pmode, 3.0)   # MMA-equivalents per fp32-accurate product (bf16-rate units)
+    peaks_tf = {"tensor": pk["bf16_tflops"] / tdiv,
                 "alu": 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12}
-    srcs = {"tensor": ("MEASURED_PEAKS.json bf16_tflops / 4 (TF32x2 fp32 emulation: two tf32 MMAs per product, "
-                       "tf32 = bf16 / 2 nominal)") if tf32 else "MEASURED_PEAKS.json bf16_tflops / 3 (BF16x3 fp32 emulation)",
+    srcs = {"tensor": {3: "MEASURED_PEAKS.json bf16_tflops / 4 (TF32x2 fp32 emulation: two tf32 MMAs per product, "
+                          "tf32 = bf16 / 2 nominal)",
+                       4: "MEASURED_PEAKS.json bf16_tflops / 2 (FP16x2 fp32 emulation: two fp16 MMAs per product, "
+                          "fp16 = bf16 rate)"}.get(pmode, "MEASURED_PEAKS.json bf16_tflops / 3 (BF16x3 fp32 emulation)"),
             "alu": "148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (MEASURED_PEAKS.json; B200_PROFILING unit counts)"}
     if fl and fl / (peaks_tf[kind] * 1e12) > by / (pk["hbm_gbs"] * 1e9):
         r = {"kernel": slot, "bound": kind, "achieved": fl / t / 1e12, "peak": peaks_tf[kind], "unit": "TFLOP/s",

@@ -94,7 +94,8 @@ typedef struct {
   int32_t engine;        /* Fourier engine used: 0 none, 1 NFFT, 2 NDFT                                  */
   int32_t band_width;    /* widest kept band k_hi - k_lo + 1 over the slices                             */
   int32_t proj_mode;     /* projection arithmetic: 0 none (given projections), 1 SIMT fp32, 2 BF16x3 (three bf16
-                            MMAs per product), 3 TF32x2 (two tf32 MMAs per product); reading R2                   */
+                            MMAs per product), 3 TF32x2 (two tf32 MMAs per product), 4 FP16x2 (two fp16 MMAs per
+                            product on 2^e-scaled points); reading R2                                             */
 } sks_plan_info;
 
 /* Bytes of DEVICE workspace sks_sum needs for this problem (slice range [p_begin, p_end) of P).

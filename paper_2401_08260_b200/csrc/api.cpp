@@ -165,6 +165,24 @@ bool use_sort_v1() {
   return v == 1;
 }
 
+// fp32 -> IEEE binary16, round to nearest even (host; |v| < 65504 here)
+uint16_t to_half_rne(float v) {
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+  const uint32_t sign = (u >> 16) & 0x8000u;
+  const float a = std::fabs(v);
+  if (a >= 65520.0f) return static_cast<uint16_t>(sign | 0x7c00u);
+  if (a < 6.103515625e-05f) {   // subnormal: multiple of 2^-24, rounded to nearest even
+    const float q = a * 16777216.0f;
+    return static_cast<uint16_t>(sign | static_cast<uint32_t>(std::nearbyint(q)));
+  }
+  uint32_t au;
+  std::memcpy(&au, &a, 4);
+  const uint32_t r = au + 0xfffu + ((au >> 13) & 1u);   // round the low 13 mantissa bits to nearest even
+  const uint32_t e = (r >> 23) - 127 + 15, m = (r >> 13) & 0x3ffu;
+  return static_cast<uint16_t>(sign | (e << 10) | m);
+}
+
 // row a1 variant: 0 SIMT fp32 (measurement A/B), 1 BF16x3 (split kernel + three bf16 MMAs), 2 TF32x2 (split
 // inside the kernel, two tf32 MMAs).  TF32x2 reads the fp32 points once and needs no split buffer, at 4/3 of the
 // tensor work of BF16x3.  With the points read by TMA (the raw fp32 tile is the hi operand) it is the faster one
@@ -172,7 +190,7 @@ bool use_sort_v1() {
 // d % 4 != 0) its converter warps load the points and BF16x3 wins above d = 256.  proj_mode(d) sizes the
 // workspace (the split buffer above d = 256); use_tf32(...) decides per call.  SKS_PROJECTION = simt | bf16x3 |
 // tf32x2 overrides.
-enum ProjMode { PM_SIMT = 0, PM_BF16X3 = 1, PM_TF32X2 = 2 };
+enum ProjMode { PM_SIMT = 0, PM_BF16X3 = 1, PM_TF32X2 = 2, PM_FP16X2 = 3 };
 bool proj_forced() { return std::getenv("SKS_PROJECTION") != nullptr; }
 ProjMode proj_mode(int d) {
   static int v = -2;
@@ -182,10 +200,23 @@ ProjMode proj_mode(int d) {
     if (e && std::strcmp(e, "simt") == 0) v = PM_SIMT;
     if (e && std::strcmp(e, "bf16x3") == 0) v = PM_BF16X3;
     if (e && std::strcmp(e, "tf32x2") == 0) v = PM_TF32X2;
+    if (e && std::strcmp(e, "fp16x2") == 0) v = PM_FP16X2;
   }
   if (v >= 0) return static_cast<ProjMode>(v);
   return d <= 256 ? PM_TF32X2 : PM_BF16X3;
 }
+
+// per call: the TMA-fed paths when the points allow (d % 4 == 0, aligned): FP16x2 where the GEMM is compute-
+// bound (d >= 256; twice the tf32 MMA rate at the same 22-bit precision), TF32x2 below (store-bound: no sample
+// pass); allow_f16 = false after a point fell outside the fp16 range (the call is rerun)
+ProjMode proj_mode_call(int d, const float* x, int64_t N, const float* y, int64_t M, bool allow_f16) {
+  ProjMode pm = proj_mode(d);
+  const bool tma = sks::proj_tf32_tma_ok(x, N, y, M, d);
+  if (pm == PM_FP16X2 && (!tma || !allow_f16)) pm = PM_TF32X2;
+  if (!proj_forced() && tma) pm = (d >= 256 && allow_f16) ? PM_FP16X2 : PM_TF32X2;
+  return pm;
+}
+constexpr sks_status kRetryTF32 = static_cast<sks_status>(100);   // internal: rerun without FP16x2
 
 // leading dimension of the slice-major projections Z: a multiple of 4 floats (16-byte rows for TMA stores)
 inline int64_t zld(int64_t N, int64_t M) { return (N + M + 3) / 4 * 4; }
@@ -250,6 +281,7 @@ struct DirEntry {
   void* g3 = nullptr;      // np x dp bf16: g zero padded (BF16x3 tensor-core operand)
   int K3 = 0;              // dp
   float* g32 = nullptr;    // np x dp32 fp32: g zero padded to 32 (TF32x2 operand; bf16-exact, so tf32-exact)
+  void* g16 = nullptr;     // np x K3 fp16: 2^8 g (FP16x2 operand; exact but for |g| < 2^-22)
   int K32 = 0;             // dp32
 };
 std::mutex g_dir_mu;
@@ -294,6 +326,11 @@ sks_status get_dirs(int P, int d, uint64_t seed, int p0, int p1, DirEntry* out) 
       for (int j = 0; j < d; ++j) g32[static_cast<size_t>(p) * e.K32 + j] = g[static_cast<size_t>(p) * d + j];
     SKS_CUDA(cudaMalloc(&e.g32, sizeof(float) * g32.size()));
     SKS_CUDA(cudaMemcpy(e.g32, g32.data(), sizeof(float) * g32.size(), cudaMemcpyHostToDevice));
+    std::vector<uint16_t> g16(static_cast<size_t>(np) * e.K3, 0);
+    for (int p = 0; p < np; ++p)
+      for (int j = 0; j < d; ++j) g16[static_cast<size_t>(p) * e.K3 + j] = to_half_rne(256.0f * g[static_cast<size_t>(p) * d + j]);
+    SKS_CUDA(cudaMalloc(&e.g16, sizeof(uint16_t) * g16.size()));
+    SKS_CUDA(cudaMemcpy(e.g16, g16.data(), sizeof(uint16_t) * g16.size(), cudaMemcpyHostToDevice));
   }
   g_dirs[key] = e;
   *out = e;
@@ -381,6 +418,7 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
   SKS_CUDA(cudaMemcpyAsync(hmm, ws + L.mm, sizeof(unsigned) * 4 * nbat, cudaMemcpyDeviceToHost, st));
   SKS_CUDA(cudaMemcpyAsync(hflag, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   SKS_CUDA(cudaStreamSynchronize(st));
+  if (*hflag & 2) return kRetryTF32;
   if (*hflag) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
   std::vector<float> r(4 * nbat);
   sks::decode_minmax(hmm, r.data(), 4 * nbat);
@@ -471,7 +509,7 @@ struct Problem {
 
 sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const float* y, const float* w,
                        const DirEntry* dirs, const float* zx_in, const float* zy_in, float* s_out, float* t_out,
-                       double inv_P, void* workspace, size_t ws_bytes, cudaStream_t st) {
+                       double inv_P, void* workspace, size_t ws_bytes, cudaStream_t st, bool allow_f16 = true) {
   const Path pt = path_of(pr.k.kind);
   const int nb = (pt.sort || pt.moment) ? buckets_for(pr.N) : 0;
   const int batch = choose_batch(pr.N, pr.M, pt, pr.nslices, pr.with_Z, nb, o.batch, pr.d);
@@ -494,10 +532,10 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     SKS_CUDA(sks::launch_zero(ws + L.s64, al(sizeof(double) * pr.M), st));
   }
   launches += s_out ? 2 : 1;
-  ProjMode pm = proj_mode(pr.d);
-  if (pm == PM_BF16X3 && !proj_forced() && sks::proj_tf32_tma_ok(x, pr.N, y, pr.M, pr.d)) pm = PM_TF32X2;
+  const ProjMode pm = pr.with_Z ? proj_mode_call(pr.d, x, pr.N, y, pr.M, allow_f16) : PM_SIMT;
   const bool tc = pr.with_Z && pm == PM_BF16X3;
   const bool tf = pr.with_Z && pm == PM_TF32X2;
+  const bool th = pr.with_Z && pm == PM_FP16X2;
   if (tc) {
     ProfScope ps(PS_SPLIT, st);
     SKS_CUDA(sks::launch_split3(x, pr.N, y, pr.M, pr.d, ws + L.xs3, st));
@@ -524,6 +562,11 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       else if (tf)
         SKS_CUDA(sks::launch_project_tf32(x, pr.N, y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32,
                                           nbat, dirs->inv + b0, Z, ldz, mm, flag, st));
+      else if (th)
+        SKS_CUDA(sks::launch_project_f16(x, pr.N, y, pr.M, pr.d,
+                                         static_cast<const uint16_t*>(dirs->g16) + static_cast<int64_t>(b0) * dirs->K3,
+                                         nbat, dirs->inv + b0, Z, ldz, mm, flag,
+                                         reinterpret_cast<unsigned*>(flag) + 1, st));
       else
         SKS_CUDA(sks::launch_project(x, pr.N, y, pr.M, pr.d, dirs->g + static_cast<int64_t>(b0) * pr.d,
                                      dirs->inv + b0, nbat, Z, ldz, mm, flag, st));
@@ -534,7 +577,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ProfScope ps(PS_MINMAX, st);
       SKS_CUDA(sks::launch_minmax(zv, nbat, mm, flag, st));
     }
-    launches += 1 + ((tc || tf) ? (nbat + 1023) / 1024 : 1);   // init_minmax + projection launch(es)
+    launches += 1 + ((tc || tf) ? (nbat + 1023) / 1024 : th ? 1 + (nbat + 1023) / 1024 : 1);   // init_minmax + projection
     int ndft_kw = 0;
     sks::EvalArgs ea{};
     ea.zv = zv;
@@ -656,6 +699,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     if (s != SKS_OK) return s;
     SKS_CUDA(cudaMemcpyAsync(hb, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     SKS_CUDA(cudaStreamSynchronize(st));
+    if (*static_cast<int*>(hb) & 2) return kRetryTF32;
     if (*static_cast<int*>(hb)) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
   }
   info.path = pt.fourier ? (pt.sort ? 2 : 0) : 1;
@@ -665,7 +709,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
   info.slice_batch = batch;
   info.n_batches = nbatches;
   info.launches = launches;
-  info.proj_mode = !pr.with_Z ? 0 : tc ? 2 : tf ? 3 : 1;
+  info.proj_mode = !pr.with_Z ? 0 : tc ? 2 : tf ? 3 : th ? 4 : 1;
   if (!pt.fourier) info.tau_min = 0;
   g_plan = info;
   return SKS_OK;
@@ -763,8 +807,12 @@ sks_status sks_sum(const float* x, int64_t N, const float* y, int64_t M, int32_t
   DirEntry dirs;
   if ((st = get_dirs(P, d, seed, p_begin, p_end, &dirs)) != SKS_OK) return st;
   Problem pr{N, M, d, kernel, p_end - p_begin, true};
-  return run_batches(pr, o, x, y, w, &dirs, nullptr, nullptr, s, nullptr, 1.0 / P, workspace, workspace_bytes,
-                     static_cast<cudaStream_t>(stream));
+  st = run_batches(pr, o, x, y, w, &dirs, nullptr, nullptr, s, nullptr, 1.0 / P, workspace, workspace_bytes,
+                   static_cast<cudaStream_t>(stream));
+  if (st == kRetryTF32)   // a point outside the FP16x2 range: the same call on TF32x2
+    st = run_batches(pr, o, x, y, w, &dirs, nullptr, nullptr, s, nullptr, 1.0 / P, workspace, workspace_bytes,
+                     static_cast<cudaStream_t>(stream), false);
+  return st;
 }
 
 sks_status sks_workspace_size_host(int64_t N, int64_t M, int32_t d, sks_kernel kernel, int32_t P, int32_t p_begin,
@@ -828,13 +876,17 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
   }
   unsigned* mm = scratch;
   int* flag = reinterpret_cast<int*>(scratch + 4 * np);
+  SKS_CUDA(cudaMemsetAsync(flag, 0, 16, cs));   // flag and the FP16x2 sampled max
   SKS_CUDA(sks::launch_init_minmax(mm, np, cs));
   if (tc) {
     char* xs3 = reinterpret_cast<char*>(scratch) + al(sizeof(unsigned) * 4 * np + 16);
     char* part = xs3 + al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n);
     SKS_CUDA(sks::launch_split3(pts, n, pts, 0, d, xs3, cs));
     SKS_CUDA(sks::launch_project_tc(xs3, n, n, d, dirs.g3, np, dirs.inv, z, n, mm, flag, part, cs));
-  } else if (pm == PM_TF32X2) {
+  } else if (pm == PM_FP16X2 && sks::proj_tf32_tma_ok(pts, n, pts, 0, d)) {
+    SKS_CUDA(sks::launch_project_f16(pts, n, pts, 0, d, dirs.g16, np, dirs.inv, z, n, mm, flag,
+                                     reinterpret_cast<unsigned*>(flag) + 1, cs));
+  } else if (pm == PM_TF32X2 || pm == PM_FP16X2) {
     SKS_CUDA(sks::launch_project_tf32(pts, n, pts, 0, d, dirs.g32, np, dirs.inv, z, n, mm, flag, cs));
   } else {
     SKS_CUDA(sks::launch_project(pts, n, pts, 0, d, dirs.g, dirs.inv, np, z, n, mm, flag, cs));

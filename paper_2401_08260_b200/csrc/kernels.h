@@ -70,6 +70,12 @@ cudaError_t launch_project_tc(const void* xs, int64_t L, int64_t Nx, int d, cons
 // row a1 as TF32x2 with the split inside the kernel (small d: no split buffer, the fp32 points are read once):
 // hi = tf32_rn(x), lo = x - hi, two kind::tf32 MMAs against the fp32 (tf32-exact) directions g32 [np][dp32]
 int proj_tf32_dpad(int d);
+// row a1 as FP16x2: s x = hi + lo in fp16 (s = 2^e from a sampled max |x|), directions as fp16(2^8 g), two
+// kind::f16 MMAs (twice the tf32 rate, the precision of TF32x2).  Needs proj_tf32_tma_ok; f16max = 4 zeroed
+// scratch bytes; flag bit 1 = a point outside the fp16 range (rerun with TF32x2)
+cudaError_t launch_project_f16(const float* x, int64_t N, const float* y, int64_t M, int d, const void* g16, int np,
+                               const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag,
+                               unsigned* f16max, cudaStream_t st);
 // the points can be read by TMA (d % 4 == 0, 16-byte aligned arrays): the raw fp32 tile is the hi operand
 bool proj_tf32_tma_ok(const float* x, int64_t N, const float* y, int64_t M, int d);
 cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g32, int np,

@@ -11,6 +11,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -78,6 +79,36 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+// FP16x2 point scale s = 2^(14 - e), max|x| = m 2^e (m in [0.5, 1)): s max|x| < 2^14 (1 if max|x| = 0)
+__device__ __forceinline__ float f16_scale(unsigned maxbits) {
+  const float m = __uint_as_float(maxbits);
+  if (!(m > 0.f) || !(m < 3.0e38f)) return 1.0f;
+  int e;
+  frexpf(m, &e);
+  return ldexpf(1.0f, 14 - e);
+}
+
+// max |x| over a sample of the points (rows k L / S, k < S) into *out (float bits; positive floats order as
+// unsigned ints), for the FP16x2 scale; out zeroed by the caller
+__global__ void k_absmax_sample(const float* __restrict__ x, int64_t N, const float* __restrict__ y, int64_t M, int d,
+                                int S, unsigned* __restrict__ out) {
+  const int64_t L = N + M;
+  float m = 0.f;
+  for (int k = blockIdx.x; k < S; k += gridDim.x) {
+    const int64_t i = static_cast<int64_t>(k) * L / S;
+    const float* row = (i < N) ? x + i * d : y + (i - N) * d;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) m = fmaxf(m, fabsf(__ldg(row + j)));
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
+// instruction descriptor kind::f16 with fp16 A / B (format 0): D f32, both K-major, N, M
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
 // instruction descriptor kind::tf32: D f32, A/B tf32, both K-major, N, M
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
@@ -88,9 +119,13 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
 // buffer) + the direction tile.  TF32x2 (TF32 = true): hi / lo tf32 pieces of 128 points x 32 dims written by
 // the converter warps straight from the fp32 points + the fp32 direction tile (TMA).  Rows are 128 bytes,
 // 128-byte swizzled, in both cases.
-template <int BN, int STAGES, bool TF32 = false>
+// MODE 0: BF16x3 from the pre-split buffer (TMA); 1: TF32x2 (raw fp32 points = hi operand, converters form
+// lo); 3: FP16x2 (raw fp32 points by TMA into the hi / lo slots, converters write fp16 hi / lo of the scaled
+// points in place; directions as fp16 x 2^8)
+template <int BN, int STAGES, int MODE = 0>
 struct TcSmem {
-  static constexpr int NPIECE = TF32 ? 2 : 3;
+  static constexpr bool TF32 = MODE == 1;
+  static constexpr int NPIECE = MODE == 0 ? 3 : 2;
   static constexpr int A_BYTES = TC_M * 128;                // one piece: 128 points x 128 bytes
   static constexpr int B_BYTES = BN * 128;                  // BN directions x 128 bytes
   static constexpr int STAGE = NPIECE * A_BYTES + B_BYTES;  // the pieces share one direction tile
@@ -131,14 +166,15 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
-template <int BN, int STAGES, bool TF32 = false>
-__global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
+template <int BN, int STAGES, int MODE = 0>
+__global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nk, int64_t L,
               int64_t Nx, int np, const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz,
               unsigned* __restrict__ mm, int* __restrict__ flag, int emode, const float* __restrict__ px,
               const float* __restrict__ py, int d, const __grid_constant__ CUtensorMap tmX,
-              const __grid_constant__ CUtensorMap tmY, int xtma) {
-  using SM = TcSmem<BN, STAGES, TF32>;
+              const __grid_constant__ CUtensorMap tmY, int xtma, const unsigned* __restrict__ f16max) {
+  using SM = TcSmem<BN, STAGES, MODE>;
+  constexpr bool TF32 = MODE == 1, CONV = MODE != 0, F16 = MODE == 3;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + SM::BAR_OFF);
@@ -151,7 +187,9 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntn = (np + BN - 1) / BN;
   float* sinv = reinterpret_cast<float*>(rng + 4 * ntn * BN);          // [np_pad] 1/||g_p||
-  for (int c = threadIdx.x; c < ntn * BN; c += blockDim.x) sinv[c] = (c < np) ? inv_norm[c] : 0.f;
+  // FP16x2: D accumulates (2^8 g) . (s x); the epilogue scale takes 1 / (2^8 s) with the 1 / ||g||
+  const float zs = F16 ? 1.0f / (256.0f * f16_scale(__ldg(f16max))) : 1.0f;
+  for (int c = threadIdx.x; c < ntn * BN; c += blockDim.x) sinv[c] = (c < np) ? inv_norm[c] * zs : 0.f;
   const int64_t ntm = (L + TC_M - 1) / TC_M;
   const int64_t ntiles = ntm * ntn;
   for (int c = threadIdx.x; c < ntn * BN; c += blockDim.x) {
@@ -159,7 +197,7 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], TF32 ? 5 : 1);
+      mbar_init(&full[s], CONV ? 5 : 1);
       mbar_init(&empty[s], 1);
       mbar_init(&xfull[s], 1);
     }
@@ -167,7 +205,7 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    if (TF32 && xtma) {
+    if (CONV && xtma) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
     }
@@ -191,7 +229,17 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         unsigned char* sa = sm + stage * SM::STAGE;
-        if (TF32) {   // TMA brings the direction tile (and, with xtma, the raw fp32 points = the hi piece)
+        if (F16) {   // raw fp32 points (two boxes of 32 dims) into the hi / lo slots + the fp16 direction tile
+          const bool hasx = m0 < Nx;
+          mbar_expect_tx(&xfull[stage], 2 * SM::A_BYTES);
+          // a tile straddling x / y: the x rows by TMA (the rest zero-filled), the y rows by the converters
+          const CUtensorMap* mp = hasx ? &tmX : &tmY;
+          const int row = hasx ? static_cast<int>(m0) : static_cast<int>(m0 - Nx);
+          tma_load_2d(mp, &xfull[stage], sa, kb * 64, row);
+          tma_load_2d(mp, &xfull[stage], sa + SM::A_BYTES, kb * 64 + 32, row);
+          mbar_expect_tx(&full[stage], SM::B_BYTES);
+          tma_load_2d(&tmB, &full[stage], sa + 2 * SM::A_BYTES, kb * TC_BK, n0);
+        } else if (TF32) {   // TMA brings the direction tile (and, with xtma, the raw fp32 points = the hi piece)
           if (xtma) {
             // rows m0 .. m0 + 127 of the concatenated points: x rows from tmX, y rows from tmY (rows outside a
             // map are zero-filled); a tile straddling x / y lands its y rows in the lo slot, merged by the converters
@@ -213,7 +261,7 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (single thread)
-    constexpr uint32_t idesc = TF32 ? idesc_tf32(TC_M, BN) : idesc_bf16(TC_M, BN);
+    constexpr uint32_t idesc = TF32 ? idesc_tf32(TC_M, BN) : F16 ? idesc_f16(TC_M, BN) : idesc_bf16(TC_M, BN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -258,6 +306,86 @@ __global__ void __launch_bounds__(TF32 ? TC_THREADS_TF32 : TC_THREADS, 1)
                        smem_u32(&tfull[b]))
                    : "memory");
     }
+  } else if (F16 && warp >= 12) {
+    // ---- converters (FP16x2): the raw fp32 rows of a k-block (64 dims) sit in the hi / lo slots (128-byte
+    //      swizzled fp32 boxes of 32 dims).  Lane c of a 4-row group reads dims 8c .. 8c + 7 of its row (two
+    //      16-byte fp32 chunks), the warp syncs, then writes fp16 chunk c of hi = f16(s x) and lo = f16(s x - hi)
+    //      for that row (|s x - hi - lo| <= 2^-22 |s x| + 2^-25: the 22-bit precision of TF32x2).  s = 2^e puts
+    //      the largest sampled |x| near 2^14; a larger value (|s x| >= 2^15) sets flag bit 1 (the caller reruns
+    //      the call with TF32x2).  Rows are private to a warp.
+    const int cw = warp - 12;
+    const int c = lane & 7, rsub = lane >> 3;
+    const float xs = f16_scale(__ldg(f16max));
+    float amax = 0.f;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t m0 = (t / ntn) * TC_M;
+      const int split = (m0 < Nx && m0 + TC_M > Nx) ? static_cast<int>(Nx - m0) : TC_M;   // y rows >= split
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&xfull[stage], phase);
+        unsigned char* sa = sm + stage * SM::STAGE;
+        // two halves of 4 row groups: all 4 groups' raw chunks are read before the warp syncs and overwrites them
+#pragma unroll
+        for (int hb = 0; hb < 8; hb += 4) {
+          float v[4][8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = 32 * cw + 4 * (hb + q) + rsub;
+            const int box = c >> 2, j0 = 2 * (c & 3);   // fp32 box (0: hi slot, 1: lo slot), chunks j0, j0 + 1
+            const unsigned char* rb = sa + box * SM::A_BYTES + r * 128;
+            if (r < split) {
+              const float4 a4 = *reinterpret_cast<const float4*>(rb + ((j0 ^ (r & 7)) << 4));
+              const float4 b4 = *reinterpret_cast<const float4*>(rb + (((j0 + 1) ^ (r & 7)) << 4));
+              v[q][0] = a4.x; v[q][1] = a4.y; v[q][2] = a4.z; v[q][3] = a4.w;
+              v[q][4] = b4.x; v[q][5] = b4.y; v[q][6] = b4.z; v[q][7] = b4.w;
+            } else {   // straddling tile: y rows from global memory
+              const int64_t i = m0 + r;
+              const int col = kb * 64 + 8 * c;
+#pragma unroll
+              for (int u = 0; u < 8; ++u) v[q][u] = 0.f;
+              if (i < L) {
+                const float* row = py + (i - Nx) * static_cast<int64_t>(d);
+                if (col < d) {
+                  const float4 a4 = __ldg(reinterpret_cast<const float4*>(row + col));
+                  v[q][0] = a4.x; v[q][1] = a4.y; v[q][2] = a4.z; v[q][3] = a4.w;
+                }
+                if (col + 4 < d) {
+                  const float4 b4 = __ldg(reinterpret_cast<const float4*>(row + col + 4));
+                  v[q][4] = b4.x; v[q][5] = b4.y; v[q][6] = b4.z; v[q][7] = b4.w;
+                }
+              }
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = 32 * cw + 4 * (hb + q) + rsub;
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float a = v[q][2 * k] * xs, b = v[q][2 * k + 1] * xs;
+              amax = fmaxf(amax, fmaxf(fabsf(a), fabsf(b)));
+              const __half2 h = __floats2half2_rn(a, b);
+              const float2 hf = __half22float2(h);
+              const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+              hi[k] = *reinterpret_cast<const uint32_t*>(&h);
+              lo[k] = *reinterpret_cast<const uint32_t*>(&l);
+            }
+            const int off = r * 128 + ((c ^ (r & 7)) << 4);
+            *reinterpret_cast<uint4*>(sa + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(sa + SM::A_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
+          __syncwarp();   // the second half's raw rows are read only after the first half's writes
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    // NaN compares false: a NaN input is caught by the epilogue's trap instead
+    if (__any_sync(0xffffffffu, !(amax < 32768.f) && amax == amax) && lane == 0) atomicOr(flag, 2);
   } else if (TF32 && warp >= 12) {
     // ---- converters (TF32x2): the tile's points, fp32 -> hi = tf32_rn(x), lo = x - hi (exact in fp32; the MMA
     //      reads it as tf32, so |x - hi - lo| <= 2^-21 |x|), written in the 128-byte swizzled K-major layout:
@@ -563,25 +691,27 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_k, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int STAGES, bool TF32 = false>
+template <int BN, int STAGES, int MODE = 0>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int64_t L, int64_t Nx, int np,
                       const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, unsigned* part,
                       cudaStream_t st, const float* px = nullptr, const float* py = nullptr, int d = 0,
-                      const CUtensorMap* tx = nullptr, const CUtensorMap* ty = nullptr) {
-  using SM = TcSmem<BN, STAGES, TF32>;
+                      const CUtensorMap* tx = nullptr, const CUtensorMap* ty = nullptr,
+                      const unsigned* f16max = nullptr) {
+  using SM = TcSmem<BN, STAGES, MODE>;
   const int ntn = (np + BN - 1) / BN;
   const size_t smem = SM::FIXED + static_cast<size_t>(20) * ntn * BN;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_proj_tc<BN, STAGES, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_proj_tc<BN, STAGES, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int64_t ntiles = ((L + TC_M - 1) / TC_M) * ntn;
   const int grid = static_cast<int>(ntiles < kProjMaxCtas ? ntiles : kProjMaxCtas);
   static const int emode = std::getenv("SKS_PROJ_EMODE") ? std::atoi(std::getenv("SKS_PROJ_EMODE")) : 0;
   const int xtma = tx != nullptr;
-  k_proj_tc<BN, STAGES, TF32><<<grid, TF32 ? TC_THREADS_TF32 : TC_THREADS, smem, st>>>(
-      ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, emode, px, py, d, xtma ? *tx : ta, xtma ? *ty : ta, xtma);
+  k_proj_tc<BN, STAGES, MODE><<<grid, MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, smem, st>>>(
+      ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, emode, px, py, d, xtma ? *tx : ta, xtma ? *ty : ta, xtma,
+      f16max);
   (void)part;
   return cudaGetLastError();
 }
@@ -656,12 +786,46 @@ cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64
     unsigned* mmc = mm + 4 * s0;
     const float* ic = inv_norm + s0;
     cudaError_t e;
-    if (BN == 256) e = launch_tc<256, 3, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
-    else if (BN == 128) e = launch_tc<128, 4, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
-    else e = launch_tc<64, 4, true>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
+    if (BN == 256) e = launch_tc<256, 3, 1>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
+    else if (BN == 128) e = launch_tc<128, 4, 1>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
+    else e = launch_tc<64, 4, 1>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// FP16x2 (MODE 3): points by TMA (needs proj_tf32_tma_ok), directions g16 = fp16(2^8 g) [np][dp] (dp = 64-padded);
+// f16max: 4 zeroed bytes of scratch for the sampled max |x|; a point with |s x| >= 2^15 sets flag bit 1
+cudaError_t launch_project_f16(const float* x, int64_t N, const float* y, int64_t M, int d, const void* g16, int np,
+                               const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag,
+                               unsigned* f16max, cudaStream_t st) {
+  const int dp = proj_tc_dpad(d);
+  const int nk = dp / TC_BK;
+  const int64_t L = N + M;
+  CUtensorMap tx, ty;
+  if (!make_map_pts(&tx, x, static_cast<uint64_t>(N), static_cast<uint64_t>(d))) return cudaErrorInvalidValue;
+  if (M == 0) ty = tx;
+  else if (!make_map_pts(&ty, y, static_cast<uint64_t>(M), static_cast<uint64_t>(d))) return cudaErrorInvalidValue;
+  const int S = static_cast<int>(std::min<int64_t>(L, 2048));
+  k_absmax_sample<<<256, 256, 0, st>>>(x, N, y, M, d, S, f16max);
+  constexpr int kSliceChunk = 1024;
+  for (int s0 = 0; s0 < np; s0 += kSliceChunk) {
+    const int ns = std::min(kSliceChunk, np - s0);
+    const int BN = ns > 128 ? 256 : (ns > 64 ? 128 : 64);
+    const void* g = static_cast<const uint16_t*>(g16) + static_cast<int64_t>(s0) * dp;
+    CUtensorMap tb;
+    if (!make_map(&tb, g, static_cast<uint64_t>(ns), static_cast<uint64_t>(dp), static_cast<uint32_t>(BN)))
+      return cudaErrorInvalidValue;
+    float* Zc = Z + static_cast<int64_t>(s0) * ldz;
+    unsigned* mmc = mm + 4 * s0;
+    const float* ic = inv_norm + s0;
+    cudaError_t e;
+    if (BN == 256) e = launch_tc<256, 3, 3>(tb, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, &tx, &ty, f16max);
+    else if (BN == 128) e = launch_tc<128, 4, 3>(tb, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, &tx, &ty, f16max);
+    else e = launch_tc<64, 4, 3>(tb, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, &tx, &ty, f16max);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_split3(const float* x, int64_t N, const float* y, int64_t M, int d, void* xs, cudaStream_t st) {

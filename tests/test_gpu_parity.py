@@ -299,7 +299,7 @@ def test_many_slices_projection_chunks():
     assert rel_err(s_a + s_b, s_all, I.weights(cfg)) <= 1e-6
 
 
-@pytest.mark.parametrize("mode", ["bf16x3", "tf32x2", "simt"])
+@pytest.mark.parametrize("mode", ["bf16x3", "tf32x2", "fp16x2", "simt"])
 def test_projection_modes_subprocess(mode):
     # every row-a1 variant (R2) against the fp64 projection, at small and large d (the variant is fixed per process)
     import subprocess
@@ -322,3 +322,27 @@ def test_projection_modes_subprocess(mode):
     env = dict(os.environ, SKS_PROJECTION=mode)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_fp16x2_default_scaling_and_range_fallback():
+    # d >= 256 runs FP16x2 (proj_mode 4): points scaled by a power of two from a row sample; data far from 1 in
+    # magnitude must keep fp32-accurate projections (the sums match oracle (b) exactly for negdist), and a row
+    # outside the sampled range (|s x| >= 2^15: row 1 is not among the sampled rows k L / 2048) makes the call
+    # rerun on TF32x2 (proj_mode 3) with the same result
+    rng = np.random.default_rng(5)
+    N, M, d, P = 5000, 400, 256, 6
+    base_x = rng.normal(size=(N, d)).astype(np.float32)
+    base_y = rng.normal(size=(M, d)).astype(np.float32)
+    w = rng.uniform(0, 1, N).astype(np.float32)
+    tgt = np.arange(0, M, 7)
+    for mag, spike, mode in [(1e-5, False, 4), (1.0, False, 4), (3e4, False, 4), (1.0, True, 3)]:
+        x = base_x * np.float32(mag)
+        y = base_y * np.float32(mag)
+        if spike:
+            x[1] *= np.float32(1e5)
+        s = S.sks_sum(dev(x), dev(y), dev(w), "negdist", 1.0, P, 11).cpu().numpy()
+        assert S.sks_last_plan()["proj_mode"] == mode, (mag, spike, S.sks_last_plan())
+        ref = O.sliced_sum("negdist", 0.0, x, y, w, P, 11, targets=tgt)
+        # negdist is homogeneous of degree 1: compare relative to mag (and to the spike's scale)
+        err = np.max(np.abs(s[tgt].astype(np.float64) - ref)) / np.abs(ref).max()
+        assert err <= 2e-6, (mag, spike, err)
