@@ -409,7 +409,7 @@ sks::PolyWin poly_win(const sks::FourierPlan& plan) {
 // ndft.cu; evaluation is then launch_ndft_eval), 0 for the NFFT (spread + FFT filter here, k_eval later).
 sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView zv, const float* w, int nbat,
                          char* ws, const Layout& L, cudaStream_t st, sks::FourierPlan* plan, int* launches,
-                         int* ndft_kw) {
+                         int* ndft_kw, bool f16_ran) {
   void* hbuf = nullptr;
   sks_status s = stage(sizeof(unsigned) * 4 * nbat + 16 + sizeof(sks::FPar) * nbat + sizeof(float) * (kNmax / 2 + 1), &hbuf);
   if (s != SKS_OK) return s;
@@ -418,7 +418,7 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
   SKS_CUDA(cudaMemcpyAsync(hmm, ws + L.mm, sizeof(unsigned) * 4 * nbat, cudaMemcpyDeviceToHost, st));
   SKS_CUDA(cudaMemcpyAsync(hflag, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   SKS_CUDA(cudaStreamSynchronize(st));
-  if (*hflag & 2) return kRetryTF32;
+  if (*hflag && f16_ran) return kRetryTF32;   // FP16x2 range exceeded (or a NaN / Inf input: TF32x2 reports it)
   if (*hflag) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
   std::vector<float> r(4 * nbat);
   sks::decode_minmax(hmm, r.data(), 4 * nbat);
@@ -649,7 +649,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ea.tot = sa.tot;
     }
     if (pt.fourier) {
-      sks_status s = fourier_batch(pr.k, pr.d, o, zv, w, nbat, ws, L, st, &plan, &launches, &ndft_kw);
+      sks_status s = fourier_batch(pr.k, pr.d, o, zv, w, nbat, ws, L, st, &plan, &launches, &ndft_kw, th);
       if (s != SKS_OK) return s;
       info.engine = ndft_kw ? 2 : 1;
       info.band_width = 0;
@@ -699,7 +699,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     if (s != SKS_OK) return s;
     SKS_CUDA(cudaMemcpyAsync(hb, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     SKS_CUDA(cudaStreamSynchronize(st));
-    if (*static_cast<int*>(hb) & 2) return kRetryTF32;
+    if (*static_cast<int*>(hb) && th) return kRetryTF32;   // FP16x2 range exceeded, or NaN / Inf input
     if (*static_cast<int*>(hb)) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
   }
   info.path = pt.fourier ? (pt.sort ? 2 : 0) : 1;

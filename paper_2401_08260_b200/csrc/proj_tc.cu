@@ -311,12 +311,12 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
     //      swizzled fp32 boxes of 32 dims).  Lane c of a 4-row group reads dims 8c .. 8c + 7 of its row (two
     //      16-byte fp32 chunks), the warp syncs, then writes fp16 chunk c of hi = f16(s x) and lo = f16(s x - hi)
     //      for that row (|s x - hi - lo| <= 2^-22 |s x| + 2^-25: the 22-bit precision of TF32x2).  s = 2^e puts
-    //      the largest sampled |x| near 2^14; a larger value (|s x| >= 2^15) sets flag bit 1 (the caller reruns
-    //      the call with TF32x2).  Rows are private to a warp.
+    //      the largest sampled |x| near 2^14; a value beyond the fp16 range (|s x| >= 65520, outside the sample)
+    //      becomes Inf and trips the epilogue's non-finite trap: the caller reruns the call with TF32x2, which
+    //      reports genuine NaN / Inf inputs.  Rows are private to a warp.
     const int cw = warp - 12;
     const int c = lane & 7, rsub = lane >> 3;
     const float xs = f16_scale(__ldg(f16max));
-    float amax = 0.f;
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -365,7 +365,6 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const float a = v[q][2 * k] * xs, b = v[q][2 * k + 1] * xs;
-              amax = fmaxf(amax, fmaxf(fabsf(a), fabsf(b)));
               const __half2 h = __floats2half2_rn(a, b);
               const float2 hf = __half22float2(h);
               const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
@@ -384,8 +383,6 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-    // NaN compares false: a NaN input is caught by the epilogue's trap instead
-    if (__any_sync(0xffffffffu, !(amax < 32768.f) && amax == amax) && lane == 0) atomicOr(flag, 2);
   } else if (TF32 && warp >= 12) {
     // ---- converters (TF32x2): the tile's points, fp32 -> hi = tf32_rn(x), lo = x - hi (exact in fp32; the MMA
     //      reads it as tf32, so |x - hi - lo| <= 2^-21 |x|), written in the 128-byte swizzled K-major layout:
