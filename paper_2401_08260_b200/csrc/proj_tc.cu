@@ -175,6 +175,10 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
               const __grid_constant__ CUtensorMap tmY, int xtma, const unsigned* __restrict__ f16max) {
   using SM = TcSmem<BN, STAGES, MODE>;
   constexpr bool TF32 = MODE == 1, CONV = MODE != 0, F16 = MODE == 3;
+  // warp roles: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle; epilogue warps 4 .. 4 + NEPI - 1; converters CW0 .. 15.
+  // FP16x2 (tensor-bound, d >= 256) trades epilogue warps for converters: 4 epilogue warps (all columns of a
+  // lane quadrant each) and 8 converter warps (16 rows each)
+  constexpr int NEPI = F16 ? 4 : 8, CW0 = F16 ? 8 : 12, NCONV = 16 - CW0, RPW = TC_M / NCONV;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + SM::BAR_OFF);
@@ -197,11 +201,11 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], CONV ? 5 : 1);
+      mbar_init(&full[s], CONV ? NCONV + 1 : 1);
       mbar_init(&empty[s], 1);
       mbar_init(&xfull[s], 1);
     }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], NEPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -306,15 +310,15 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
                        smem_u32(&tfull[b]))
                    : "memory");
     }
-  } else if (F16 && warp >= 12) {
+  } else if (F16 && warp >= CW0) {
     // ---- converters (FP16x2): the raw fp32 rows of a k-block (64 dims) sit in the hi / lo slots (128-byte
     //      swizzled fp32 boxes of 32 dims).  Lane c of a 4-row group reads dims 8c .. 8c + 7 of its row (two
     //      16-byte fp32 chunks), the warp syncs, then writes fp16 chunk c of hi = f16(s x) and lo = f16(s x - hi)
     //      for that row (|s x - hi - lo| <= 2^-22 |s x| + 2^-25: the 22-bit precision of TF32x2).  s = 2^e puts
     //      the largest sampled |x| near 2^14; a value beyond the fp16 range (|s x| >= 65520, outside the sample)
     //      becomes Inf and trips the epilogue's non-finite trap: the caller reruns the call with TF32x2, which
-    //      reports genuine NaN / Inf inputs.  Rows are private to a warp.
-    const int cw = warp - 12;
+    //      reports genuine NaN / Inf inputs.  Rows are private to a warp (RPW = 16 rows per converter warp).
+    const int cw = warp - CW0;
     const int c = lane & 7, rsub = lane >> 3;
     const float xs = f16_scale(__ldg(f16max));
     int stage = 0;
@@ -327,11 +331,11 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
         unsigned char* sa = sm + stage * SM::STAGE;
         // two halves of 4 row groups: all 4 groups' raw chunks are read before the warp syncs and overwrites them
 #pragma unroll
-        for (int hb = 0; hb < 8; hb += 4) {
+        for (int hb = 0; hb < (emode == 7 ? 0 : RPW / 4); hb += 4) {
           float v[4][8];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int r = 32 * cw + 4 * (hb + q) + rsub;
+            const int r = RPW * cw + 4 * (hb + q) + rsub;
             const int box = c >> 2, j0 = 2 * (c & 3);   // fp32 box (0: hi slot, 1: lo slot), chunks j0, j0 + 1
             const unsigned char* rb = sa + box * SM::A_BYTES + r * 128;
             if (r < split) {
@@ -360,7 +364,7 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
           __syncwarp();
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int r = 32 * cw + 4 * (hb + q) + rsub;
+            const int r = RPW * cw + 4 * (hb + q) + rsub;
             uint32_t hi[4], lo[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -480,12 +484,13 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
       kb = kn;
     }
     }
-  } else if (warp >= 4 && warp < 12) {
-    // ---- epilogue: warp w handles TMEM lane quadrant q = w % 4 (points m0 + 32q + lane) and the column half
-    //      h = (w - 4) / 4 of the accumulator.  Per 16-column chunk: scale, store (coalesced along points), and
-    //      the per-column min / max over the warp's 32 points by warp reductions (colrange16r).
+  } else if (warp >= 4 && warp < 4 + NEPI) {
+    // ---- epilogue: warp w handles TMEM lane quadrant q = w % 4 (points m0 + 32q + lane) and the column part
+    //      h = (w - 4) / 4 of the accumulator (two halves; FP16x2: all columns).  Per 16-column chunk: scale,
+    //      store (coalesced along points), and the per-column min / max over the warp's 32 points by warp
+    //      reductions (colrange16r).
     const int q = warp & 3, h = (warp - 4) >> 2;
-    constexpr int HALF = BN / 2;
+    constexpr int HALF = BN / (NEPI / 4);
     float trap = 0.f;   // becomes NaN if a projection is NaN / Inf (in x, y or an overflow)
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -525,7 +530,7 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
               : "r"(tbase + static_cast<uint32_t>(c0 + 16)));
         const int nc = min(16, ncols - c0);
-        if (emode == 1) { trap += (cur[0] == 0x7fc00001u) ? 1.f : 0.f; continue; }   // measurement: TMEM drain
+        if (emode == 1 || emode == 7) { trap += (cur[0] == 0x7fc00001u) ? 1.f : 0.f; continue; }   // measurement: TMEM drain
         const float4* sv = reinterpret_cast<const float4*>(sinv + n0 + c0);
         float sc[16];
 #pragma unroll
