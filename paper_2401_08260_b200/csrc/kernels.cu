@@ -438,14 +438,19 @@ cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int 
 // ------------------------------------------------------------------ a6: FFT -> x D -> inverse FFT (one CTA per slice)
 constexpr int FF_THREADS = 512;
 
+// radix-2 stages.  PS: tw holds one contiguous twiddle table per stage (stage s: e^{-2 pi i pos / 2^s} at
+// tw[2^(s-1) - 1 + pos], n - 1 entries), so consecutive lanes read consecutive twiddles (no bank conflicts);
+// otherwise (n = 16384, shared memory) the n/2 twiddles of the last stage, read with stride n / 2^s
+template <bool PS>
 __device__ __forceinline__ void fft_stages(float2* buf, const float2* tw, int n, int logn) {
   for (int s = 1; s <= logn; ++s) {
     const int half = 1 << (s - 1);
-    const int tstride = n >> s;
+    const float2* tws = PS ? tw + (half - 1) : tw;
+    const int tstride = PS ? 1 : (n >> s);
     for (int b = threadIdx.x; b < n / 2; b += FF_THREADS) {
       const int grp = b >> (s - 1), pos = b & (half - 1);
       const int i = grp * 2 * half + pos, j = i + half;
-      const float2 t = tw[pos * tstride];
+      const float2 t = tws[pos * tstride];
       const float2 a = buf[i], c = buf[j];
       const float2 bt = make_float2(c.x * t.x - c.y * t.y, c.x * t.y + c.y * t.x);
       buf[i] = make_float2(a.x + bt.x, a.y + bt.y);
@@ -461,18 +466,29 @@ __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restri
                                                            float* __restrict__ Q) {
   extern __shared__ float2 sm[];
   float2* buf = sm;          // [n]
-  float2* tw = sm + n;       // [n/2] forward twiddles e^{-2 pi i j / n}
+  float2* tw = sm + n;       // per-stage forward twiddles (fft_stages)
   const int p = blockIdx.x;
   const int nh = n / 2 + 1;
-  for (int j = threadIdx.x; j < n / 2; j += FF_THREADS) {
-    float sv, cv;
-    sincospif(2.0f * static_cast<float>(j) / static_cast<float>(n), &sv, &cv);
-    tw[j] = make_float2(cv, -sv);
+  const bool ps = n <= 8192;
+  if (ps) {
+    for (int j = threadIdx.x; j < n - 1; j += FF_THREADS) {
+      const int half = 1 << (31 - __clz(j + 1)), pos = j + 1 - half;   // stage with 2^(s-1) = half
+      float sv, cv;
+      sincospif(static_cast<float>(pos) / static_cast<float>(half), &sv, &cv);   // angle 2 pi pos / (2 half)
+      tw[j] = make_float2(cv, -sv);
+    }
+  } else {
+    for (int j = threadIdx.x; j < n / 2; j += FF_THREADS) {
+      float sv, cv;
+      sincospif(2.0f * static_cast<float>(j) / static_cast<float>(n), &sv, &cv);
+      tw[j] = make_float2(cv, -sv);
+    }
   }
   const float* gp = grid + static_cast<int64_t>(p) * n;
   for (int l = threadIdx.x; l < n; l += FF_THREADS) buf[__brev(l) >> (32 - logn)] = make_float2(gp[l], 0.f);
   __syncthreads();
-  fft_stages(buf, tw, n, logn);                     // G_k = sum_l g_l e^{-2 pi i k l / n}
+  if (ps) fft_stages<true>(buf, tw, n, logn);      // G_k = sum_l g_l e^{-2 pi i k l / n}
+  else fft_stages<false>(buf, tw, n, logn);
   const float* Dp = D + static_cast<int64_t>(p) * nh;
   for (int k = threadIdx.x; k < n; k += FF_THREADS) {
     const float dk = Dp[k <= n / 2 ? k : n - k];
@@ -485,7 +501,8 @@ __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restri
     if (l < r) { const float2 t = buf[l]; buf[l] = buf[r]; buf[r] = t; }
   }
   __syncthreads();
-  fft_stages(buf, tw, n, logn);                     // h_l = conj(FFT(conj X))_l; real part
+  if (ps) fft_stages<true>(buf, tw, n, logn);      // h_l = conj(FFT(conj X))_l; real part
+  else fft_stages<false>(buf, tw, n, logn);
   float* hp = h + static_cast<int64_t>(p) * n;
   for (int l = threadIdx.x; l < n; l += FF_THREADS) hp[l] = buf[l].x;
   if (Q) {   // interpolation polynomials of the footprint cells: Q[c][k] = sum_j h[l + j] coef_j[k]
@@ -504,11 +521,10 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, 
                               const PolyWin& pw, int WA, float* Q, cudaStream_t st) {
   int logn = 0;
   while ((1 << logn) < n) ++logn;
-  const size_t smem = static_cast<size_t>(n) * sizeof(float2) + static_cast<size_t>(n / 2) * sizeof(float2);
+  const size_t smem = static_cast<size_t>(n) * sizeof(float2) + static_cast<size_t>(n <= 8192 ? n : n / 2) * sizeof(float2);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_fft_filter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         16384 * 8 + 8192 * 8);
+    cudaFuncSetAttribute(k_fft_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8 + 8192 * 8);
     attr = true;
   }
   k_fft_filter<<<np, FF_THREADS, smem, st>>>(grid, D, n, logn, h, fp, pw, WA, Q);
