@@ -88,16 +88,19 @@ __device__ __forceinline__ float f16_scale(unsigned maxbits) {
   return ldexpf(1.0f, 14 - e);
 }
 
-// max |x| over a sample of the points (rows k L / S, k < S) into *out (float bits; positive floats order as
+// max |x| over a sample of the points (rows k L / S, k < S; d % 4 == 0, 16-byte aligned rows) into *out (float bits; positive floats order as
 // unsigned ints), for the FP16x2 scale; out zeroed by the caller
 __global__ void k_absmax_sample(const float* __restrict__ x, int64_t N, const float* __restrict__ y, int64_t M, int d,
                                 int S, unsigned* __restrict__ out) {
   const int64_t L = N + M;
   float m = 0.f;
-  for (int k = blockIdx.x; k < S; k += gridDim.x) {
+  for (int k = blockIdx.x; k < S; k += gridDim.x) {   // one row per CTA and step, 16-byte loads (d % 4 == 0)
     const int64_t i = static_cast<int64_t>(k) * L / S;
-    const float* row = (i < N) ? x + i * d : y + (i - N) * d;
-    for (int j = threadIdx.x; j < d; j += blockDim.x) m = fmaxf(m, fabsf(__ldg(row + j)));
+    const float4* row = reinterpret_cast<const float4*>((i < N) ? x + i * d : y + (i - N) * d);
+    for (int j = threadIdx.x; j < d / 4; j += blockDim.x) {
+      const float4 v = __ldg(row + j);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -808,8 +811,8 @@ cudaError_t launch_project_f16(const float* x, int64_t N, const float* y, int64_
   if (!make_map_pts(&tx, x, static_cast<uint64_t>(N), static_cast<uint64_t>(d))) return cudaErrorInvalidValue;
   if (M == 0) ty = tx;
   else if (!make_map_pts(&ty, y, static_cast<uint64_t>(M), static_cast<uint64_t>(d))) return cudaErrorInvalidValue;
-  const int S = static_cast<int>(std::min<int64_t>(L, 2048));
-  k_absmax_sample<<<256, 256, 0, st>>>(x, N, y, M, d, S, f16max);
+  const int S = static_cast<int>(std::min<int64_t>(L, 1024));
+  k_absmax_sample<<<S, 256, 0, st>>>(x, N, y, M, d, S, f16max);
   constexpr int kSliceChunk = 1024;
   for (int s0 = 0; s0 < np; s0 += kSliceChunk) {
     const int ns = std::min(kSliceChunk, np - s0);

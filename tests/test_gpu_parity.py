@@ -327,7 +327,7 @@ def test_projection_modes_subprocess(mode):
 def test_fp16x2_default_scaling_and_range_fallback():
     # d >= 256 runs FP16x2 (proj_mode 4): points scaled by a power of two from a row sample; data far from 1 in
     # magnitude must keep fp32-accurate projections (the sums match oracle (b) exactly for negdist), and a row
-    # outside the sampled range (|s x| >= 2^15: row 1 is not among the sampled rows k L / 2048) makes the call
+    # outside the sampled range (beyond the fp16 range; row 1 is not among the sampled rows k L / 1024) makes the call
     # rerun on TF32x2 (proj_mode 3) with the same result
     rng = np.random.default_rng(5)
     N, M, d, P = 5000, 400, 256, 6
