@@ -39,7 +39,7 @@ namespace sks {
 
 namespace {
 
-constexpr int S0_T = 512, S0_CH = 16384;      // histogram: elements per CTA
+constexpr int S0_T = 512;      // histogram threads
 // owner kernel variants (x capacity, fine buckets, CTAs per SM, threads): SKS_SP_VARIANT selects (measurement
 // aid).  Measured on B200, cfg2 sp_owner (one stream): {4096,1024,3,512} 358 us (default), {8192,2048,2,512} 438,
 // {4096,1024,4,256} 389, {2048,1024,4,512} 465, {4096,1024,2,512} 401; finer buckets {4096,2048,3,512} 418.
@@ -57,7 +57,9 @@ int sp_variant() {
   }
   return v;
 }
-constexpr int S4_T = 256, S4_PER = 4, S4_CH = S4_T * S4_PER, S4_SG = 8;    // gather
+constexpr int S4_T = 256, S4_PER = 4, S4_CH = S4_T * S4_PER;    // gather
+constexpr int S4_SG = 8;   // slices per gather thread (measured 4 / 8 / 16 / 32: 8 best)
+constexpr int S0_CH = 32768;   // histogram: elements per CTA (measured 8192 / 16384 / 32768: the largest best)
 
 __device__ __forceinline__ float key2f_sp(unsigned k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
