@@ -22,7 +22,8 @@
 //   S3 k_sp_owner  per (owner, slice): the owner's x into NBF fine buckets in shared memory (counting sort),
 //                  fp64 exclusive bucket prefix sums, then every y of the owner evaluated from shared memory
 //                  only; t (fp32) written at the y's mailbox position (coalesced)
-//   S4 k_sp_gather per (target chunk, slice group): t gathered back to target order through the recorded
+//   S4 k_sp_gather per (target chunk, slice group): the other owners' contribution table from the owners'
+//                  fp64 totals (in shared memory), t gathered back to target order through the recorded
 //                  positions, accumulated over slices in fp64 registers, one coalesced atomic per target
 // An owner whose x exceed the shared-memory capacity (degenerate data: one bin holding > SP_CAP points) is
 // processed in several passes over subsets of its x (the identity is additive over the sources).
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
   const int o = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
   const SpOwner r = own[static_cast<int64_t>(p) * G + o];
   // every owner publishes its x totals (sum w, sum w z, sum w z^2; fp64) for the other owners' targets
-  // (k_sp_outer), so an owner without targets still sums its x
+  // (k_sp_gather's other-owner table), so an owner without targets still sums its x
   __shared__ double own_tot[3];
   __shared__ double wvc[S3_T / 32];   // per-warp sum w z^2 of the pass (shared fp64 atomics are CAS loops)
   if (tid < 3) own_tot[tid] = 0.0;
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
           s0 = fmaf(q.y, fmaxf(zf - q.x, 0.f), s0);
         }
         const double zd = zf;
-        // this owner's part only; the other owners' part is added in k_sp_gather (k_sp_outer's table)
+        // this owner's part only; the other owners' part is added in k_sp_gather (its other-owner table)
         const double v = zd * (2.0 * rb.x - Tp.x) - 2.0 * rb.y + Tp.y + 2.0 * static_cast<double>(s0 + s1);
         const float t = static_cast<float>(-coef * v);
         if (pass == 0) rdst[i] = t;
@@ -547,64 +548,40 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
 }
 
 // ---------------------------------------------------------------------------------------------- S4
-// Per slice: the other owners' part of every target's sum.  For a target of owner o, the x of owners < o lie
-// below it and those of owners > o above it: sum w |x - z| over them = z (Alo - Ahi) + (Bhi - Blo).
-// dab[p][o] = (Alo - Ahi, Bhi - Blo) from the owners' fp64 totals; slice totals for the Laplacian moment term.
-constexpr int SO_T = 256;
+static_assert(S4_SG == S4_T / 32, "one warp per slice of the gather's slice group builds its other-owner table");
 
-__global__ void __launch_bounds__(SO_T) k_sp_outer(const double* __restrict__ otot, int G, double2* __restrict__ dab,
-                                                   SliceTot* __restrict__ tot) {
-  __shared__ double wsc[3][SO_T / 32 + 1];
-  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const double* ot = otot + static_cast<int64_t>(p) * G * 4;
-  double carryA = 0.0, carryB = 0.0, carryC = 0.0;
-  // totals first (two sweeps keep the code simple; G is small)
-  for (int o0 = 0; o0 < G; o0 += SO_T) {
-    const int o = o0 + tid;
-    double a = 0.0, b = 0.0, c = 0.0;
-    if (o < G) { a = ot[4 * o]; b = ot[4 * o + 1]; c = ot[4 * o + 2]; }
-    a = warp_sum_sp(a); b = warp_sum_sp(b); c = warp_sum_sp(c);
-    if (lane == 0) { wsc[0][wid] = a; wsc[1][wid] = b; wsc[2][wid] = c; }
-    __syncthreads();
-    if (tid == 0)
-      for (int q = 0; q < SO_T / 32; ++q) { carryA += wsc[0][q]; carryB += wsc[1][q]; carryC += wsc[2][q]; }
-    __syncthreads();
-  }
-  __shared__ double TA, TB;
-  if (tid == 0) { TA = carryA; TB = carryB; tot[p] = SliceTot{carryA, carryB, carryC, 0.0}; }
-  __syncthreads();
-  const double A = TA, B = TB;
-  double runA = 0.0, runB = 0.0;   // exclusive prefix over owner chunks
-  for (int o0 = 0; o0 < G; o0 += SO_T) {
-    const int o = o0 + tid;
-    double a = 0.0, b = 0.0;
-    if (o < G) { a = ot[4 * o]; b = ot[4 * o + 1]; }
-    double ia = warp_incl_scan_sp(a), ib = warp_incl_scan_sp(b);
-    if (lane == 31) { wsc[0][wid] = ia; wsc[1][wid] = ib; }
-    __syncthreads();
-    double wa = 0.0, wb = 0.0, ta = 0.0, tb = 0.0;
-    for (int q = 0; q < SO_T / 32; ++q) {
-      if (q < wid) { wa += wsc[0][q]; wb += wsc[1][q]; }
-      ta += wsc[0][q];
-      tb += wsc[1][q];
-    }
-    const double alo = runA + wa + ia - a, blo = runB + wb + ib - b;   // owners < o
-    if (o < G) dab[static_cast<int64_t>(p) * G + o] = make_double2(alo - (A - alo - a), (B - blo - b) - blo);
-    runA += ta;
-    runB += tb;
-    __syncthreads();
-  }
-}
-
-// Back to target order: t = R[ypos] (own owner) - coef (z dA + dB) (other owners), accumulated over a slice
-// group in fp64 registers, one coalesced atomic per target (or per-slice stores for sks_sum_1d).
 __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, double coef, const int* __restrict__ ypos,
                                                     const uint16_t* __restrict__ yown, const float* __restrict__ R,
-                                                    const double2* __restrict__ dab, double* __restrict__ s64,
-                                                    float* __restrict__ per_slice_out) {
+                                                    const double* __restrict__ otot, SliceTot* __restrict__ tot,
+                                                    double* __restrict__ s64, float* __restrict__ per_slice_out) {
+  extern __shared__ double2 sdab[];   // [S4_SG][G] other-owner coefficients of the group's slices
   const int64_t M = zv.M;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * S4_CH + threadIdx.x;
   const int p0 = blockIdx.y * S4_SG, p1 = min(np, p0 + S4_SG);
+  {
+    // warp w: slice p0 + w.  For a target of owner o, the x of owners < o lie below it and those of owners > o
+    // above it: sum w |x - z| over them = z (Alo - Ahi) + (Bhi - Blo), from the owners' fp64 totals (fused here:
+    // every CTA of the slice group rebuilds the small table; the first target block also writes the slice totals)
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, p = p0 + wid;
+    if (p < p1) {
+      const double* ot = otot + static_cast<int64_t>(p) * G * 4;
+      double A = 0.0, B = 0.0, C = 0.0;
+      for (int o = lane; o < G; o += 32) { A += ot[4 * o]; B += ot[4 * o + 1]; C += ot[4 * o + 2]; }
+      A = warp_sum_sp(A); B = warp_sum_sp(B); C = warp_sum_sp(C);
+      if (blockIdx.x == 0 && lane == 0) tot[p] = SliceTot{A, B, C, 0.0};
+      double runA = 0.0, runB = 0.0;
+      for (int o0 = 0; o0 < G; o0 += 32) {
+        const int o = o0 + lane;
+        const double a = o < G ? ot[4 * o] : 0.0, b = o < G ? ot[4 * o + 1] : 0.0;
+        const double ia = warp_incl_scan_sp(a), ib = warp_incl_scan_sp(b);
+        const double alo = runA + ia - a, blo = runB + ib - b;   // owners < o
+        if (o < G) sdab[wid * G + o] = make_double2(alo - (A - alo - a), (B - blo - b) - blo);
+        runA += __shfl_sync(0xffffffffu, ia, 31);
+        runB += __shfl_sync(0xffffffffu, ib, 31);
+      }
+    }
+    __syncthreads();
+  }
   double acc[S4_PER];
 #pragma unroll
   for (int k = 0; k < S4_PER; ++k) acc[k] = 0.0;
@@ -625,7 +602,7 @@ __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, dou
     for (int k = 0; k < S4_PER; ++k) {
       const int64_t m = m0 + k * S4_T;
       t[k] = (m < M) ? __ldcs(R + static_cast<int64_t>(p) * M + q[k]) : 0.f;
-      d[k] = (m < M) ? __ldg(dab + static_cast<int64_t>(p) * G + ow[k]) : make_double2(0.0, 0.0);
+      d[k] = (m < M) ? sdab[(p - p0) * G + ow[k]] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int k = 0; k < S4_PER; ++k) {
@@ -704,7 +681,6 @@ static size_t region_bytes(int64_t N, int64_t M, int np) {
   s += al(sizeof(int) * 2 * d.G * static_cast<size_t>(np));           // cursors
   s += al(sizeof(int) * static_cast<size_t>(np));                     // done tickets
   s += al(sizeof(double) * 4 * d.G * static_cast<size_t>(np));        // owner totals
-  s += al(sizeof(double2) * d.G * static_cast<size_t>(np));           // other-owner coefficients
   s += al(sizeof(uint16_t) * M * static_cast<size_t>(np));            // y owners
   s += al(sizeof(uint16_t) * d.NH * static_cast<size_t>(np));         // owner map
   s += al(sizeof(SpOwner) * d.G * static_cast<size_t>(np));           // owners
@@ -753,7 +729,6 @@ struct SpRegion {
   size_t zero_bytes;
   int* H;           // [gs][chunks][NH] chunk histograms
   double* otot;     // [gs][G][4] owner totals (w, w z, w z^2)
-  double2* dab;     // [gs][G] other-owner coefficients
   uint16_t* yown;   // [gs][M] owner of each target
   uint16_t* om;     // [gs][NH] owner of each bin
   SpOwner* own;     // [gs][G]
@@ -773,7 +748,6 @@ SpRegion carve_region(char* base, int64_t N, int64_t M, int NH, int G, int gs) {
   r.zero_bytes = static_cast<size_t>(w - base);
   r.H = reinterpret_cast<int*>(w);            w += al(sizeof(int) * (hist_chunks(N) + hist_chunks(M)) * NH * g);
   r.otot = reinterpret_cast<double*>(w);      w += al(sizeof(double) * 4 * G * g);
-  r.dab = reinterpret_cast<double2*>(w);      w += al(sizeof(double2) * G * g);
   r.yown = reinterpret_cast<uint16_t*>(w);    w += al(sizeof(uint16_t) * M * g);
   r.om = reinterpret_cast<uint16_t*>(w);      w += al(sizeof(uint16_t) * NH * g);
   r.own = reinterpret_cast<SpOwner*>(w);      w += al(sizeof(SpOwner) * G * g);
@@ -789,6 +763,7 @@ void set_attributes() {
   if (done) return;
   cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_sp_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
 #define SP_OWNER_ATTR(C, B, MB, T)                                                                              \
   cudaFuncSetAttribute(k_sp_owner<C, B, MB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
                        static_cast<int>(sizeof(OwnerShared<C, B, T>)))
@@ -840,9 +815,8 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   }
   prof_end(pm);
   pm = prof_begin(PS_SP_GATHER, st);
-  k_sp_outer<<<np, SO_T, 0, st>>>(r.otot, G, r.dab, a.tot + g0);
-  k_sp_gather<<<dim3(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG))), S4_T, 0, st>>>(
-      zv, np, G, a.coef, r.ypos, r.yown, r.R, r.dab, a.s64, pso);
+  k_sp_gather<<<dim3(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG))), S4_T,
+                sizeof(double2) * S4_SG * G, st>>>(zv, np, G, a.coef, r.ypos, r.yown, r.R, r.otot, a.tot + g0, a.s64, pso);
   prof_end(pm);
   return cudaGetLastError();
 }
