@@ -523,15 +523,12 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
   sks::FourierPlan plan;
   sks_plan_info info{};
   info.tau_min = 1e300;
-  {
+  {   // flag words, fp64 target sums and the first batch's ranges in one launch
     ProfScope ps(PS_AUX, st);
-    SKS_CUDA(sks::launch_zero(ws + L.flag, al(16), st));
+    SKS_CUDA(sks::launch_prologue(ws + L.flag, s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr, pr.M,
+                                  reinterpret_cast<unsigned*>(ws + L.mm), std::min(batch, pr.nslices), st));
   }
-  if (s_out) {
-    ProfScope ps(PS_AUX, st);
-    SKS_CUDA(sks::launch_zero(ws + L.s64, al(sizeof(double) * pr.M), st));
-  }
-  launches += s_out ? 2 : 1;
+  launches += 1;
   const ProjMode pm = pr.with_Z ? proj_mode_call(pr.d, x, pr.N, y, pr.M, allow_f16) : PM_SIMT;
   const bool tc = pr.with_Z && pm == PM_BF16X3;
   const bool tf = pr.with_Z && pm == PM_TF32X2;
@@ -546,7 +543,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     ++nbatches;
     unsigned* mm = reinterpret_cast<unsigned*>(ws + L.mm);
     int* flag = reinterpret_cast<int*>(ws + L.flag);
-    {
+    if (b0 > 0) {   // (the first batch's ranges are initialised by the prologue)
       ProfScope ps(PS_AUX, st);
       SKS_CUDA(sks::launch_init_minmax(mm, nbat, st));
     }
@@ -577,7 +574,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ProfScope ps(PS_MINMAX, st);
       SKS_CUDA(sks::launch_minmax(zv, nbat, mm, flag, st));
     }
-    launches += 1 + ((tc || tf) ? (nbat + 1023) / 1024 : th ? 1 + (nbat + 1023) / 1024 : 1);   // init_minmax + projection
+    launches += (b0 > 0) + ((tc || tf) ? (nbat + 1023) / 1024 : th ? 1 + (nbat + 1023) / 1024 : 1);   // init_minmax + projection
     int ndft_kw = 0;
     sks::EvalArgs ea{};
     ea.zv = zv;

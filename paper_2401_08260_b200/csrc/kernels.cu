@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -196,6 +197,23 @@ __global__ void k_minmax(ZView zv, unsigned* mm, int* flag) {
     if (xmn <= xmx) { atomicMin(&mm[p * 4 + 0], f2key(xmn)); atomicMax(&mm[p * 4 + 1], f2key(xmx)); }
     if (amn <= amx) { atomicMin(&mm[p * 4 + 2], f2key(amn)); atomicMax(&mm[p * 4 + 3], f2key(amx)); }
   }
+}
+
+// call prologue in one launch: zero the flag words, zero the fp64 target sums, initialise the first batch's ranges
+__global__ void k_prologue(uint4* flag16, double* s64, int64_t M, unsigned* mm, int np) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t == 0) *flag16 = make_uint4(0, 0, 0, 0);
+  if (t < np) { mm[t * 4 + 0] = 0xffffffffu; mm[t * 4 + 1] = 0u; mm[t * 4 + 2] = 0xffffffffu; mm[t * 4 + 3] = 0u; }
+  if (s64)
+    for (int64_t m = t; m < M; m += static_cast<int64_t>(gridDim.x) * blockDim.x) s64[m] = 0.0;
+}
+
+cudaError_t launch_prologue(void* flag16, double* s64, int64_t M, unsigned* mm, int np, cudaStream_t st) {
+  int64_t blocks = (std::max<int64_t>(s64 ? M : 0, np) + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  k_prologue<<<static_cast<unsigned>(blocks), 256, 0, st>>>(static_cast<uint4*>(flag16), s64, M, mm, np);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st) {

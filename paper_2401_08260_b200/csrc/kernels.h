@@ -84,6 +84,8 @@ cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64
 // per-slice ranges of given projections (sks_sum_1d)
 cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_t st);
 cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st);
+// call prologue (one launch): flag16 (16 bytes) and s64 [M] (nullptr: none) zeroed, mm [np][4] initialised
+cudaError_t launch_prologue(void* flag16, double* s64, int64_t M, unsigned* mm, int np, cudaStream_t st);
 void decode_minmax(const unsigned* enc, float* dec, int n);
 
 // rows a3 + a4 (sortpath.cu): per slice, one 4-CTA cluster counting-sorts the x and y projections into
