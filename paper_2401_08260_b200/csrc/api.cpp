@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -417,7 +418,10 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
   int* hflag = reinterpret_cast<int*>(hmm + 4 * nbat);
   SKS_CUDA(cudaMemcpyAsync(hmm, ws + L.mm, sizeof(unsigned) * 4 * nbat, cudaMemcpyDeviceToHost, st));
   SKS_CUDA(cudaMemcpyAsync(hflag, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  static const bool htime = std::getenv("SKS_HOST_TIMING") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   SKS_CUDA(cudaStreamSynchronize(st));
+  const auto t1 = std::chrono::steady_clock::now();
   if (*hflag && f16_ran) return kRetryTF32;   // FP16x2 range exceeded (or a NaN / Inf input: TF32x2 reports it)
   if (*hflag) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
   std::vector<float> r(4 * nbat);
@@ -434,6 +438,11 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
   std::string err;
   if (!sks::build_fourier_plan(km, o.eps, o.w, o.os, nbat, xmn.data(), xmx.data(), amn.data(), amx.data(), *plan, &err))
     return fail(err.rfind("non-finite", 0) == 0 ? SKS_ERR_NONFINITE : SKS_ERR_UNSUPPORTED, err);
+  const auto t2 = std::chrono::steady_clock::now();
+  if (htime)
+    std::fprintf(stderr, "[sks host] sync wait %.1f us, plan %.1f us\n",
+                 std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                 std::chrono::duration<double, std::micro>(t2 - t1).count());
   const int n = plan->n;
   sks::FPar* hfp = reinterpret_cast<sks::FPar*>(hflag + 4);
   int kband = 0;

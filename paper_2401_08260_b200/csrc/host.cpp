@@ -254,7 +254,26 @@ bool fit_window_poly(int w, double beta, float* coef, double* max_err) {
 }
 
 // ------------------------------------------------------------------ band selection (R5)
+static void select_band_uncached(const KernelModel& k, double tau, double eps, int kcap, int* klo, int* khi);
+
+// band per (kernel, tau, eps): cached, repeated calls on the same data re-plan with identical taus
 static void select_band(const KernelModel& k, double tau, double eps, int kcap, int* klo, int* khi) {
+  using Key = std::tuple<int, int, double, int, double, double, int>;
+  static std::mutex mu;
+  static std::map<Key, std::pair<int, int>> cache;
+  const Key key{k.kind, k.matern_p, k.scale, k.d, tau, eps, kcap};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) { *klo = it->second.first; *khi = it->second.second; return; }
+  }
+  select_band_uncached(k, tau, eps, kcap, klo, khi);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() > 4096) cache.clear();   // bounded
+  cache.emplace(key, std::make_pair(*klo, *khi));
+}
+
+static void select_band_uncached(const KernelModel& k, double tau, double eps, int kcap, int* klo, int* khi) {
   // c_k for k >= 0; c_{-k} = c_k.  Keep the smallest band [klo,khi] (|k| in band) with dropped mass <= eps.
   std::vector<double> c;
   c.reserve(1024);
@@ -392,7 +411,25 @@ bool build_fourier_plan(const KernelModel& k, double eps, int w, int oversample,
   out.W = W;
   out.WA = WA;
   out.poly.assign(static_cast<size_t>(w) * (kPolyDeg + 1), 0.f);
-  if (!fit_window_poly(w, out.beta, out.poly.data(), &out.poly_err)) {
+  // the fit depends on (w, beta) only: cached (it costs ~w x 400 exp evaluations per call otherwise)
+  bool fit_ok;
+  {
+    static std::mutex mu;
+    static std::map<std::pair<int, float>, std::pair<std::vector<float>, double>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(w, out.beta);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      std::vector<float> c(out.poly.size());
+      double e = 0.0;
+      fit_window_poly(w, out.beta, c.data(), &e);
+      it = cache.emplace(key, std::make_pair(std::move(c), e)).first;
+    }
+    out.poly = it->second.first;
+    out.poly_err = it->second.second;
+    fit_ok = out.poly_err < 1e-4;
+  }
+  if (!fit_ok) {
     if (err) *err = "window polynomial fit failed (error " + std::to_string(out.poly_err) + ")";
     return false;
   }
