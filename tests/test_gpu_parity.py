@@ -346,3 +346,25 @@ def test_fp16x2_default_scaling_and_range_fallback():
         # negdist is homogeneous of degree 1: compare relative to mag (and to the spike's scale)
         err = np.max(np.abs(s[tgt].astype(np.float64) - ref)) / np.abs(ref).max()
         assert err <= 2e-6, (mag, spike, err)
+
+
+@pytest.mark.parametrize("N,M,d,kind", [(100, 50, 784, "negdist"), (130, 7, 256, "gaussian"), (3, 2, 300, "negdist"),
+                                        (1000, 500, 258, "negdist"), (129, 129, 512, "laplacian")])
+def test_projection_paths_small_shapes(N, M, d, kind):
+    # the projection variants at awkward sizes: a single straddling point tile (N < 128), d = 256 (FP16x2 from
+    # d >= 256), d % 4 != 0 above 256 (BF16x3 with the split pass), tiny N / M
+    rng = np.random.default_rng(N * 7 + d)
+    x = rng.normal(size=(N, d)).astype(np.float32)
+    y = rng.normal(size=(M, d)).astype(np.float32)
+    w = rng.uniform(-1, 1, N).astype(np.float32)
+    P, scale = 8, 25.0
+    s = S.sks_sum(dev(x), dev(y), dev(w), kind, scale, P, 3).cpu().numpy()
+    ref = O.sliced_sum(kind, scale if kind != "negdist" else 0.0, x, y, w, P, 3)
+    err = rel_err(s, ref, w)
+    tol = TOL[kind]
+    if kind == "negdist":
+        # exact up to the projections' rounding (R2: |dz| <= 2e-6 ||pt||): |dt| <= c_d sum|w| 2 * 2e-6 max||pt||
+        import math
+        cd = math.sqrt(math.pi) * math.exp(math.lgamma((d + 1) / 2) - math.lgamma(d / 2))
+        tol = max(tol, 4e-6 * cd * max(np.linalg.norm(x, axis=1).max(), np.linalg.norm(y, axis=1).max()))
+    assert err <= tol, (N, M, d, kind, err, tol, S.sks_last_plan())
