@@ -342,6 +342,7 @@ struct __align__(16) OwnerShared {
   float2 xs[SP_CAP];          // the pass's x (z, w) in fine-bucket order
   double2 rec[SP_NBF + 1];    // exclusive prefix (sum w, sum w x) over the pass's buckets; [NBF] = pass totals
   int start[SP_NBF + 1];      // bucket b holds xs[start[b], start[b+1])
+  int2 se[SP_NBF];            // (start[b], start[b+1]) in one 8-byte word for the lookups
   int wbuf[NT / 32 + 1];
   double2 dbuf[NT / 32 + 1];
 };
@@ -437,7 +438,11 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
       int total;
       int run = block_excl_scan<S3_T>(loc, S.wbuf, &total);
 #pragma unroll
-      for (int j = 0; j < PB; ++j) { S.start[tid * PB + j] = run; run += c[j]; }
+      for (int j = 0; j < PB; ++j) {
+        S.start[tid * PB + j] = run;
+        S.se[tid * PB + j] = make_int2(run, run + c[j]);
+        run += c[j];
+      }
       if (tid == 0) S.start[SP_NBF] = total;
     }
     __syncthreads();
@@ -459,7 +464,8 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
     for (int c0 = 0; c0 < SP_NBF; c0 += S3_T) {
       const int b = c0 + tid;
       double2 v = make_double2(0.0, 0.0);
-      for (int i = S.start[b], e = S.start[b + 1]; i < e; ++i) {
+      const int2 br = S.se[b];
+      for (int i = br.x, e = br.y; i < e; ++i) {
         const float2 q = S.xs[i];
         const double wz = static_cast<double>(q.y) * q.x;
         v.x += q.y;
@@ -517,7 +523,8 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
         const float zf = zy[k];
         const int b = fine_of<SP_NBF>(ucoord(zf, uoff, hscale), r.blo, r.fmul);
         const double2 rb = S.rec[b];
-        const int j0 = S.start[b], j1 = S.start[b + 1];
+        const int2 jr = S.se[b];
+        const int j0 = jr.x, j1 = jr.y;
         float s0 = 0.f, s1 = 0.f;
         int j = j0;
         for (; j + 2 <= j1; j += 2) {
