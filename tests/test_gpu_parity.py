@@ -239,6 +239,17 @@ def test_errors_fail_loudly():
     with pytest.raises(S.SKSError) as e:
         S.sks_sum(torch.randn(100, 4, device="cuda"), y, w, "negdist", 1.0, 8, 1, workspace=ws)
     assert e.value.status == 4
+    # d >= 256 (FP16x2): an Inf / NaN input trips the trap, the call reruns on TF32x2, which reports it
+    xb = torch.randn(300, 256, device="cuda")
+    yb = torch.randn(40, 256, device="cuda")
+    wb = torch.rand(300, device="cuda")
+    for bad in (float("inf"), float("nan")):
+        xb2 = xb.clone()
+        xb2[7, 3] = bad
+        for kind in ("negdist", "gaussian"):
+            with pytest.raises(S.SKSError) as e:
+                S.sks_sum(xb2, yb, wb, kind, 20.0, 8, 1)
+            assert e.value.status == 5, (bad, kind)
 
 
 # ---------------------------------------------------------------- BASELINE.json full sizes, sampled targets
