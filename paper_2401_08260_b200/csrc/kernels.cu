@@ -674,14 +674,14 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a) {
   float zn[EV_U];
   if (p + EV_U <= p1)
 #pragma unroll
-    for (int k = 0; k < EV_U; ++k) zn[k] = __ldg(zy + (p + k) * a.zv.ldy);
+    for (int k = 0; k < EV_U; ++k) zn[k] = __ldcs(zy + (p + k) * a.zv.ldy);
   for (; p + EV_U <= p1; p += EV_U) {
     float z[EV_U];
 #pragma unroll
     for (int k = 0; k < EV_U; ++k) z[k] = zn[k];
     if (p + 2 * EV_U <= p1)
 #pragma unroll
-      for (int k = 0; k < EV_U; ++k) zn[k] = __ldg(zy + (p + EV_U + k) * a.zv.ldy);
+      for (int k = 0; k < EV_U; ++k) zn[k] = __ldcs(zy + (p + EV_U + k) * a.zv.ldy);
     float part = 0.f;
 #pragma unroll
     for (int k = 0; k < EV_U; ++k) part += one(p - p0 + k, z[k]);
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a) {
       }
   }
   for (; p < p1; ++p) {
-    const float z = __ldg(zy + p * a.zv.ldy);
+    const float z = __ldcs(zy + p * a.zv.ldy);
     acc += one(p - p0, z);
     if (MOMENT) {
       const double zd = z;
