@@ -413,18 +413,18 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
     __syncthreads();
     // ---- fine-bucket counting sort of this pass's x into shared memory
     int fr[S3_PER];   // (fine bucket << 13) | rank inside the bucket, -1: none
+    float2 xw[S3_PER];   // the pass's (z, w), read once and kept in registers until the scatter
     {
-      float zx[S3_PER];   // all loads in flight before the first use
 #pragma unroll
-      for (int k = 0; k < S3_PER; ++k) {
+      for (int k = 0; k < S3_PER; ++k) {   // all loads in flight before the first use
         const int i = tid + k * S3_T;
-        zx[k] = (i < nk) ? ldg_cg(&xp[i].x) : 0.f;
+        xw[k] = (i < nk) ? ldg_cg2(xp + i) : make_float2(0.f, 0.f);
       }
 #pragma unroll
       for (int k = 0; k < S3_PER; ++k) {
         fr[k] = -1;
         if (tid + k * S3_T < nk) {
-          const int b = fine_of<SP_NBF>(ucoord(zx[k], uoff, hscale), r.blo, r.fmul);
+          const int b = fine_of<SP_NBF>(ucoord(xw[k].x, uoff, hscale), r.blo, r.fmul);
           fr[k] = (b << 13) | atomicAdd(&S.start[b], 1);   // rank < SP_CAP <= 8192
         }
       }
@@ -446,16 +446,9 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
       if (tid == 0) S.start[SP_NBF] = total;
     }
     __syncthreads();
-    constexpr int XB = S3_PER < 8 ? S3_PER : 8;
 #pragma unroll
-    for (int h = 0; h < S3_PER; h += XB) {   // second read of the pass's x (L2), XB in flight per thread
-      float2 e8[XB];
-#pragma unroll
-      for (int k = 0; k < XB; ++k) e8[k] = (fr[h + k] >= 0) ? ldg_cg2(xp + tid + (h + k) * S3_T) : make_float2(0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < XB; ++k)
-        if (fr[h + k] >= 0) S.xs[S.start[fr[h + k] >> 13] + (fr[h + k] & 8191)] = e8[k];
-    }
+    for (int k = 0; k < S3_PER; ++k)
+      if (fr[k] >= 0) S.xs[S.start[fr[k] >> 13] + (fr[k] & 8191)] = xw[k];
     __syncthreads();
     // ---- fp64 bucket sums (thread t: buckets t, t + S3_T, ...: neighbouring lanes read neighbouring buckets)
     //      into rec[], then one blocked exclusive scan (thread t: buckets 4t .. 4t+3)
