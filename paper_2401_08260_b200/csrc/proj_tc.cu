@@ -162,7 +162,7 @@ __device__ __forceinline__ void colrange16r(const float* fmn, const float* fmx, 
 // CTAs that share a point tile run together and its TMA loads hit L2).  Two TMEM accumulators: the epilogue
 // of tile i overlaps the MMAs of tile i+1.  Per-slice ranges: per-CTA partials in smem -> global atomics.
 constexpr int TC_THREADS = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue (2 warpgroups)
-constexpr int TC_THREADS_TF32 = 512;   // + w12..w15: fp32 -> tf32 hi / lo converters
+constexpr int TC_THREADS_TF32 = 512;   // + converter warps (TF32x2: w12..w15; FP16x2: w8..w15, 4 epilogue warps)
 
 // round to the nearest tf32 (10 explicit mantissa bits), kept in an fp32 container: exact tensor-core operand
 __device__ __forceinline__ float tf32_rn(float x) {
