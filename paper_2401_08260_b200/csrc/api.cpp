@@ -605,7 +605,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
         ProfScope ps(PS_SORT, st);   // the whole sort stage (fork .. join); its kernels also time themselves
         SKS_CUDA(sks::launch_sortpart(sa, ws + L.sp, st));
       }
-      launches += 4 * sks::sortpart_groups(pr.N, pr.M, nbat);   // hist, part, owner, gather per group
+      launches += sks::sortpart_launches_per_group(pr.N, pr.M) * sks::sortpart_groups(pr.N, pr.M, nbat);
       ea.tot = sa.tot;
     } else if (pt.sort) {
       // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)

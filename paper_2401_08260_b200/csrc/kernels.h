@@ -147,6 +147,7 @@ struct SortPartArgs {
 SpDims sortpart_dims(int64_t N, int64_t M);
 size_t sortpart_bytes(int64_t N, int64_t M, int np);   // scratch of launch_sortpart
 int sortpart_group(int64_t N, int64_t M, int np);      // slices per L2-resident group
+int sortpart_launches_per_group(int64_t N, int64_t M);   // kernels per group (4, or 5 with many owners)
 inline int sortpart_groups(int64_t N, int64_t M, int np) {
   const int g = sortpart_group(N, M, np);
   return (np + g - 1) / g;

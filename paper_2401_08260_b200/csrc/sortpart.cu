@@ -60,6 +60,7 @@ int sp_variant() {
 }
 constexpr int S4_T = 256, S4_PER = 4, S4_CH = S4_T * S4_PER;    // gather
 constexpr int S4_SG = 8;   // slices per gather thread (measured 4 / 8 / 16 / 32: 8 best)
+constexpr int kSmemDabMax = 128;   // owners per slice up to which the gather builds the other-owner table itself
 constexpr int S0_CH = 32768;   // histogram: elements per CTA (measured 8192 / 16384 / 32768: the largest best)
 
 __device__ __forceinline__ float key2f_sp(unsigned k) {
@@ -548,13 +549,63 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
 }
 
 // ---------------------------------------------------------------------------------------------- S4
+// Many owners (G > kSmemDabMax): the other-owner table once per slice in global memory (k_sp_outer) instead of
+// being rebuilt in every gather CTA's shared memory.
+constexpr int SO_T = 256;
+
+__global__ void __launch_bounds__(SO_T) k_sp_outer(const double* __restrict__ otot, int G, double2* __restrict__ dab,
+                                                   SliceTot* __restrict__ tot) {
+  __shared__ double wsc[3][SO_T / 32 + 1];
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double* ot = otot + static_cast<int64_t>(p) * G * 4;
+  double carryA = 0.0, carryB = 0.0, carryC = 0.0;
+  // totals first (two sweeps keep the code simple; G is small)
+  for (int o0 = 0; o0 < G; o0 += SO_T) {
+    const int o = o0 + tid;
+    double a = 0.0, b = 0.0, c = 0.0;
+    if (o < G) { a = ot[4 * o]; b = ot[4 * o + 1]; c = ot[4 * o + 2]; }
+    a = warp_sum_sp(a); b = warp_sum_sp(b); c = warp_sum_sp(c);
+    if (lane == 0) { wsc[0][wid] = a; wsc[1][wid] = b; wsc[2][wid] = c; }
+    __syncthreads();
+    if (tid == 0)
+      for (int q = 0; q < SO_T / 32; ++q) { carryA += wsc[0][q]; carryB += wsc[1][q]; carryC += wsc[2][q]; }
+    __syncthreads();
+  }
+  __shared__ double TA, TB;
+  if (tid == 0) { TA = carryA; TB = carryB; tot[p] = SliceTot{carryA, carryB, carryC, 0.0}; }
+  __syncthreads();
+  const double A = TA, B = TB;
+  double runA = 0.0, runB = 0.0;   // exclusive prefix over owner chunks
+  for (int o0 = 0; o0 < G; o0 += SO_T) {
+    const int o = o0 + tid;
+    double a = 0.0, b = 0.0;
+    if (o < G) { a = ot[4 * o]; b = ot[4 * o + 1]; }
+    double ia = warp_incl_scan_sp(a), ib = warp_incl_scan_sp(b);
+    if (lane == 31) { wsc[0][wid] = ia; wsc[1][wid] = ib; }
+    __syncthreads();
+    double wa = 0.0, wb = 0.0, ta = 0.0, tb = 0.0;
+    for (int q = 0; q < SO_T / 32; ++q) {
+      if (q < wid) { wa += wsc[0][q]; wb += wsc[1][q]; }
+      ta += wsc[0][q];
+      tb += wsc[1][q];
+    }
+    const double alo = runA + wa + ia - a, blo = runB + wb + ib - b;   // owners < o
+    if (o < G) dab[static_cast<int64_t>(p) * G + o] = make_double2(alo - (A - alo - a), (B - blo - b) - blo);
+    runA += ta;
+    runB += tb;
+    __syncthreads();
+  }
+}
+
 static_assert(S4_SG == S4_T / 32, "one warp per slice of the gather's slice group builds its other-owner table");
 
+template <bool GDAB>
 __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, double coef, const int* __restrict__ ypos,
                                                     const uint16_t* __restrict__ yown, const float* __restrict__ R,
                                                     const double* __restrict__ otot, SliceTot* __restrict__ tot,
-                                                    double* __restrict__ s64, float* __restrict__ per_slice_out) {
-  extern __shared__ double2 sdab[];   // [S4_SG][G] other-owner coefficients of the group's slices
+                                                    const double2* __restrict__ gdab, double* __restrict__ s64,
+                                                    float* __restrict__ per_slice_out) {
+  extern __shared__ double2 sdab[];   // [S4_SG][G] other-owner coefficients of the group's slices (gdab == null)
   const int64_t M = zv.M;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * S4_CH + threadIdx.x;
   const int p0 = blockIdx.y * S4_SG, p1 = min(np, p0 + S4_SG);
@@ -563,7 +614,7 @@ __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, dou
     // above it: sum w |x - z| over them = z (Alo - Ahi) + (Bhi - Blo), from the owners' fp64 totals (fused here:
     // every CTA of the slice group rebuilds the small table; the first target block also writes the slice totals)
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, p = p0 + wid;
-    if (p < p1) {
+    if (p < p1 && !GDAB) {
       const double* ot = otot + static_cast<int64_t>(p) * G * 4;
       double A = 0.0, B = 0.0, C = 0.0;
       for (int o = lane; o < G; o += 32) { A += ot[4 * o]; B += ot[4 * o + 1]; C += ot[4 * o + 2]; }
@@ -602,7 +653,8 @@ __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, dou
     for (int k = 0; k < S4_PER; ++k) {
       const int64_t m = m0 + k * S4_T;
       t[k] = (m < M) ? __ldcs(R + static_cast<int64_t>(p) * M + q[k]) : 0.f;
-      d[k] = (m < M) ? sdab[(p - p0) * G + ow[k]] : make_double2(0.0, 0.0);
+      d[k] = (m < M) ? (GDAB ? __ldg(gdab + static_cast<int64_t>(p) * G + ow[k]) : sdab[(p - p0) * G + ow[k]])
+                     : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int k = 0; k < S4_PER; ++k) {
@@ -681,6 +733,7 @@ static size_t region_bytes(int64_t N, int64_t M, int np) {
   s += al(sizeof(int) * 2 * d.G * static_cast<size_t>(np));           // cursors
   s += al(sizeof(int) * static_cast<size_t>(np));                     // done tickets
   s += al(sizeof(double) * 4 * d.G * static_cast<size_t>(np));        // owner totals
+  s += al(sizeof(double2) * d.G * static_cast<size_t>(np));           // other-owner coefficients (large G)
   s += al(sizeof(uint16_t) * M * static_cast<size_t>(np));            // y owners
   s += al(sizeof(uint16_t) * d.NH * static_cast<size_t>(np));         // owner map
   s += al(sizeof(SpOwner) * d.G * static_cast<size_t>(np));           // owners
@@ -695,6 +748,8 @@ static int active_streams(int64_t N, int64_t M, int np) {
   const int gs = sortpart_group(N, M, np);
   return std::min(sortpart_streams(), (np + gs - 1) / gs);
 }
+
+int sortpart_launches_per_group(int64_t N, int64_t M) { return sortpart_dims(N, M).G > kSmemDabMax ? 5 : 4; }
 
 size_t sortpart_bytes(int64_t N, int64_t M, int np) {
   return region_bytes(N, M, sortpart_group(N, M, np)) * active_streams(N, M, np);
@@ -729,6 +784,7 @@ struct SpRegion {
   size_t zero_bytes;
   int* H;           // [gs][chunks][NH] chunk histograms
   double* otot;     // [gs][G][4] owner totals (w, w z, w z^2)
+  double2* dab;     // [gs][G] other-owner coefficients (G > kSmemDabMax only)
   uint16_t* yown;   // [gs][M] owner of each target
   uint16_t* om;     // [gs][NH] owner of each bin
   SpOwner* own;     // [gs][G]
@@ -748,6 +804,7 @@ SpRegion carve_region(char* base, int64_t N, int64_t M, int NH, int G, int gs) {
   r.zero_bytes = static_cast<size_t>(w - base);
   r.H = reinterpret_cast<int*>(w);            w += al(sizeof(int) * (hist_chunks(N) + hist_chunks(M)) * NH * g);
   r.otot = reinterpret_cast<double*>(w);      w += al(sizeof(double) * 4 * G * g);
+  r.dab = reinterpret_cast<double2*>(w);      w += al(sizeof(double2) * G * g);
   r.yown = reinterpret_cast<uint16_t*>(w);    w += al(sizeof(uint16_t) * M * g);
   r.om = reinterpret_cast<uint16_t*>(w);      w += al(sizeof(uint16_t) * NH * g);
   r.own = reinterpret_cast<SpOwner*>(w);      w += al(sizeof(SpOwner) * G * g);
@@ -763,7 +820,7 @@ void set_attributes() {
   if (done) return;
   cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_sp_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  cudaFuncSetAttribute(k_sp_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
 #define SP_OWNER_ATTR(C, B, MB, T)                                                                              \
   cudaFuncSetAttribute(k_sp_owner<C, B, MB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
                        static_cast<int>(sizeof(OwnerShared<C, B, T>)))
@@ -815,8 +872,15 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   }
   prof_end(pm);
   pm = prof_begin(PS_SP_GATHER, st);
-  k_sp_gather<<<dim3(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG))), S4_T,
-                sizeof(double2) * S4_SG * G, st>>>(zv, np, G, a.coef, r.ypos, r.yown, r.R, r.otot, a.tot + g0, a.s64, pso);
+  const bool smem_dab = G <= kSmemDabMax;   // few owners: each gather CTA builds its slices' table in shared memory
+  if (!smem_dab) k_sp_outer<<<np, SO_T, 0, st>>>(r.otot, G, r.dab, a.tot + g0);
+  const dim3 ggrid(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG)));
+  if (smem_dab)
+    k_sp_gather<false><<<ggrid, S4_T, sizeof(double2) * S4_SG * G, st>>>(zv, np, G, a.coef, r.ypos, r.yown, r.R, r.otot,
+                                                                        a.tot + g0, nullptr, a.s64, pso);
+  else
+    k_sp_gather<true><<<ggrid, S4_T, 0, st>>>(zv, np, G, a.coef, r.ypos, r.yown, r.R, r.otot, a.tot + g0, r.dab,
+                                              a.s64, pso);
   prof_end(pm);
   return cudaGetLastError();
 }
