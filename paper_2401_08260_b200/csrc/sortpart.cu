@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -136,7 +137,7 @@ __device__ __forceinline__ T block_excl_scan(T v, T* wbuf, T* total) {
 __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __restrict__ mm, int NH, int G,
                                                   int ncx, int nchunks, int chx, int chy, int NBF, int* __restrict__ H,
                                                   int* __restrict__ done, uint16_t* __restrict__ om,
-                                                  SpOwner* __restrict__ own) {
+                                                  SpOwner* __restrict__ own, int* __restrict__ base) {
   extern __shared__ int hs[];   // [NH] histogram; in the plan: cx[NH + 1], cy[NH + 1], blo[G + 1]
   __shared__ int wbuf[S0_T / 32 + 1];
   __shared__ int last;
@@ -234,6 +235,28 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
     r.fmul = (hi > lo) ? static_cast<float>(NBF) / static_cast<float>(hi - lo) : 0.f;
     r.pad0 = r.pad1 = 0;
     own[static_cast<int64_t>(p) * G + o] = r;
+  }
+  if (base == nullptr) return;
+  // many owners: the first mailbox slot of every (chunk, owner) -- the owner's region start plus its counts in
+  // the earlier chunks of the same part -- so that the partition needs no run reservations (k_sp_part_big)
+  __syncthreads();
+  int* cnt = blo + G + 1;   // [nchunks][G]
+  for (int e = tid; e < nchunks * G; e += S0_T) cnt[e] = 0;
+  __syncthreads();
+  for (int b = tid; b < NH; b += S0_T) {
+    const int oo = min(G - 1, static_cast<int>((static_cast<int64_t>(cx[b]) * G) / Nx));
+    for (int q = 0; q < nchunks; ++q) {
+      const int v = __ldcg(hp + static_cast<int64_t>(q) * NH + b);
+      if (v) atomicAdd(&cnt[q * G + oo], v);
+    }
+  }
+  __syncthreads();
+  for (int o = tid; o < G; o += S0_T) {
+    const int lo = blo[o];
+    int rx = cx[lo], ry = cy[lo];
+    int* bp = base + static_cast<int64_t>(p) * nchunks * G + o;
+    for (int q = 0; q < ncx; ++q) { bp[q * G] = rx; rx += cnt[q * G + o]; }
+    for (int q = ncx; q < nchunks; ++q) { bp[q * G] = ry; ry += cnt[q * G + o]; }
   }
 }
 
@@ -333,6 +356,67 @@ __global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __rest
       uint16_t* yo = yown + static_cast<int64_t>(p) * zv.M;
       if (full) part_round<false, true>(e0, n, z, w, uoff, hscale, NH, G, om, ooff, cw, curp, xdst, ydst, yp, yo);
       else part_round<false, false>(e0, n, z, w, uoff, hscale, NH, G, om, ooff, cw, curp, xdst, ydst, yp, yo);
+    }
+  }
+}
+
+// Many owners (G > kSmemDabMax): one CTA per histogram chunk, each element's slot = its (chunk, owner) base from the
+// plan + its rank among the chunk's elements of that owner (a shared-memory counter per owner; with many owners
+// the counters see little contention).  No global atomics: with the per-warp-round reservations above, a round of
+// 256 elements over ~1000 owners costs about one global atomic per element.
+constexpr int S2B_U = 4;   // elements in flight per thread
+
+__global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __restrict__ w, const unsigned* __restrict__ mm,
+                                                      int NH, int G, int ncx, int nchunks, int chx, int chy,
+                                                      const uint16_t* __restrict__ om_g, const int* __restrict__ base,
+                                                      float2* __restrict__ Xmb, float* __restrict__ Ymb,
+                                                      int* __restrict__ ypos, uint16_t* __restrict__ yown) {
+  extern __shared__ __align__(16) unsigned char shb[];
+  int* cnt = reinterpret_cast<int*>(shb);                               // [G] next slot per owner
+  uint16_t* om = reinterpret_cast<uint16_t*>(cnt + (G + 3) / 4 * 4);   // [NH], 16-B aligned
+  const int p = blockIdx.y, tid = threadIdx.x;
+  const bool isx = static_cast<int>(blockIdx.x) < ncx;
+  const int c = isx ? blockIdx.x : blockIdx.x - ncx;
+  const int n = static_cast<int>(isx ? zv.N : zv.M);
+  const int ch = isx ? chx : chy;
+  const float* z = isx ? zv.zx + p * zv.ldx : zv.zy + p * zv.ldy;
+  const float xmin = key2f_sp(mm[p * 4 + 0]), xmax = key2f_sp(mm[p * 4 + 1]);
+  const float hscale = (xmax > xmin) ? static_cast<float>(NH) / (xmax - xmin) : 0.f;
+  const float uoff = -xmin * hscale;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(om_g + static_cast<int64_t>(p) * NH);   // NH % 8 == 0
+    uint4* dst = reinterpret_cast<uint4*>(om);
+    for (int b = tid; b < NH / 8; b += S0_T) dst[b] = __ldg(src + b);
+    const int* bp = base + (static_cast<int64_t>(p) * nchunks + blockIdx.x) * G;
+    for (int o = tid; o < G; o += S0_T) cnt[o] = __ldg(bp + o);
+  }
+  __syncthreads();
+  const int i0 = c * ch, i1 = min(n, i0 + ch);
+  float2* xdst = Xmb + static_cast<int64_t>(p) * zv.N;
+  float* ydst = Ymb + static_cast<int64_t>(p) * zv.M;
+  int* yp = ypos + static_cast<int64_t>(p) * zv.M;
+  uint16_t* yo = yown + static_cast<int64_t>(p) * zv.M;
+  for (int e = i0 + tid; e < i1; e += S2B_U * S0_T) {
+    float zz[S2B_U], ww[S2B_U];
+#pragma unroll
+    for (int k = 0; k < S2B_U; ++k) {
+      const int i = e + k * S0_T;
+      zz[k] = i < i1 ? __ldg(z + i) : 0.f;
+      if (isx) ww[k] = i < i1 ? __ldg(w + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < S2B_U; ++k) {
+      const int i = e + k * S0_T;
+      if (i >= i1) continue;
+      const int o = om[clamp_floor(ucoord(zz[k], uoff, hscale), NH)];
+      const int dst = atomicAdd(&cnt[o], 1);
+      if (isx) {
+        xdst[dst] = make_float2(zz[k], ww[k]);
+      } else {
+        ydst[dst] = zz[k];
+        yp[i] = dst;
+        yo[i] = static_cast<uint16_t>(o);
+      }
     }
   }
 }
@@ -734,6 +818,7 @@ static size_t region_bytes(int64_t N, int64_t M, int np) {
   s += al(sizeof(int) * static_cast<size_t>(np));                     // done tickets
   s += al(sizeof(double) * 4 * d.G * static_cast<size_t>(np));        // owner totals
   s += al(sizeof(double2) * d.G * static_cast<size_t>(np));           // other-owner coefficients (large G)
+  s += al(sizeof(int) * (hist_chunks(N) + hist_chunks(M)) * d.G * static_cast<size_t>(np));   // (chunk, owner) bases
   s += al(sizeof(uint16_t) * M * static_cast<size_t>(np));            // y owners
   s += al(sizeof(uint16_t) * d.NH * static_cast<size_t>(np));         // owner map
   s += al(sizeof(SpOwner) * d.G * static_cast<size_t>(np));           // owners
@@ -785,6 +870,7 @@ struct SpRegion {
   int* H;           // [gs][chunks][NH] chunk histograms
   double* otot;     // [gs][G][4] owner totals (w, w z, w z^2)
   double2* dab;     // [gs][G] other-owner coefficients (G > kSmemDabMax only)
+  int* base;        // [gs][chunks][G] first mailbox slot of every (chunk, owner) (G > kSmemDabMax only)
   uint16_t* yown;   // [gs][M] owner of each target
   uint16_t* om;     // [gs][NH] owner of each bin
   SpOwner* own;     // [gs][G]
@@ -805,6 +891,7 @@ SpRegion carve_region(char* base, int64_t N, int64_t M, int NH, int G, int gs) {
   r.H = reinterpret_cast<int*>(w);            w += al(sizeof(int) * (hist_chunks(N) + hist_chunks(M)) * NH * g);
   r.otot = reinterpret_cast<double*>(w);      w += al(sizeof(double) * 4 * G * g);
   r.dab = reinterpret_cast<double2*>(w);      w += al(sizeof(double2) * G * g);
+  r.base = reinterpret_cast<int*>(w);         w += al(sizeof(int) * (hist_chunks(N) + hist_chunks(M)) * G * g);
   r.yown = reinterpret_cast<uint16_t*>(w);    w += al(sizeof(uint16_t) * M * g);
   r.om = reinterpret_cast<uint16_t*>(w);      w += al(sizeof(uint16_t) * NH * g);
   r.own = reinterpret_cast<SpOwner*>(w);      w += al(sizeof(SpOwner) * G * g);
@@ -818,8 +905,9 @@ SpRegion carve_region(char* base, int64_t N, int64_t M, int NH, int G, int gs) {
 void set_attributes() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);   // (+ static shared)
   cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_sp_part_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_sp_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
 #define SP_OWNER_ATTR(C, B, MB, T)                                                                              \
   cudaFuncSetAttribute(k_sp_owner<C, B, MB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
@@ -840,8 +928,11 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   const int ncx0 = hist_chunks(N), ncy0 = hist_chunks(M);
   const int64_t per_cta2 = int64_t(S2W_WARPS) * S2W_WCH * wpc;
   const int ncx2 = static_cast<int>(cdiv(N, per_cta2)), ncy2 = static_cast<int>(cdiv(M, per_cta2));
-  const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1);
+  const bool big = G > kSmemDabMax;   // many owners: plan bases + atomic-free partition (k_sp_part_big)
+  const int nch = ncx0 + ncy0;
+  const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1 + (big ? static_cast<size_t>(nch) * G : 0));
   const size_t sm2 = sizeof(int) * (((1 + S2W_WARPS) * G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
+  const size_t sm2b = sizeof(int) * ((G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
   ZView zv = a.zv;
   zv.zx += g0 * zv.ldx;
   zv.zy += g0 * zv.ldy;
@@ -852,11 +943,17 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   ProfMark pm = prof_begin(PS_SP_HIST, st);
   k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, hist_chunk_len(N),
                                                        hist_chunk_len(M), kSpVars[sp_variant()].nbf, r.H, r.done, r.om,
-                                                       r.own);
+                                                       r.own, big ? r.base : nullptr);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_end(pm);
   pm = prof_begin(PS_SP_PART, st);
-  k_sp_part<<<dim3(ncx2 + ncy2, np), S2W_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, wpc, r.om, r.own, r.cursor, r.Xmb,
-                                                        r.Ymb, r.ypos, r.yown);
+  if (big)
+    k_sp_part_big<<<dim3(nch, np), S0_T, sm2b, st>>>(zv, a.w, mm, NH, G, ncx0, nch, hist_chunk_len(N), hist_chunk_len(M),
+                                                     r.om, r.base, r.Xmb, r.Ymb, r.ypos, r.yown);
+  else
+    k_sp_part<<<dim3(ncx2 + ncy2, np), S2W_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, wpc, r.om, r.own, r.cursor, r.Xmb,
+                                                          r.Ymb, r.ypos, r.yown);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_end(pm);
   pm = prof_begin(PS_SP_OWNER, st);
   switch (sp_variant()) {
