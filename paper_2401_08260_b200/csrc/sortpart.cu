@@ -360,11 +360,12 @@ __global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __rest
   }
 }
 
-// Many owners (G > kSmemDabMax): one CTA per histogram chunk, each element's slot = its (chunk, owner) base from the
-// plan + its rank among the chunk's elements of that owner (a shared-memory counter per owner; with many owners
-// the counters see little contention).  No global atomics: with the per-warp-round reservations above, a round of
-// 256 elements over ~1000 owners costs about one global atomic per element.
-constexpr int S2B_U = 4;   // elements in flight per thread
+// Many owners (G > kSmemDabMax): one CTA per histogram chunk; the plan gave every (chunk, owner) its first mailbox
+// slot, so no global atomics are needed (with the per-warp-round reservations above, a round of 256 elements over
+// ~1000 owners costs about one global atomic per element).  The chunk is processed in sub-chunks of SB elements,
+// each counting-sorted by owner in shared memory before it is written, so that an owner's elements of the
+// sub-chunk leave as one contiguous run (the mailbox writes are otherwise 8-byte scatters over ~1000 regions).
+constexpr int SB_PER = 8, SB = S0_T * SB_PER;   // elements per sub-chunk
 
 __global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __restrict__ w, const unsigned* __restrict__ mm,
                                                       int NH, int G, int ncx, int nchunks, int chx, int chy,
@@ -372,8 +373,13 @@ __global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __r
                                                       float2* __restrict__ Xmb, float* __restrict__ Ymb,
                                                       int* __restrict__ ypos, uint16_t* __restrict__ yown) {
   extern __shared__ __align__(16) unsigned char shb[];
-  int* cnt = reinterpret_cast<int*>(shb);                               // [G] next slot per owner
-  uint16_t* om = reinterpret_cast<uint16_t*>(cnt + (G + 3) / 4 * 4);   // [NH], 16-B aligned
+  const int G4 = (G + 3) / 4 * 4;
+  int* gnext = reinterpret_cast<int*>(shb);               // [G] next mailbox slot of each owner (this chunk)
+  int* lcnt = gnext + G4;                                 // [G] sub-chunk counts, then exclusive starts
+  float2* stg = reinterpret_cast<float2*>(lcnt + G4);     // [SB] sub-chunk elements in owner order
+  uint16_t* sow = reinterpret_cast<uint16_t*>(stg + SB);  // [SB] owner of each staged element
+  uint16_t* om = sow + SB;                                // [NH]
+  __shared__ int wbuf[S0_T / 32 + 1];
   const int p = blockIdx.y, tid = threadIdx.x;
   const bool isx = static_cast<int>(blockIdx.x) < ncx;
   const int c = isx ? blockIdx.x : blockIdx.x - ncx;
@@ -388,36 +394,68 @@ __global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __r
     uint4* dst = reinterpret_cast<uint4*>(om);
     for (int b = tid; b < NH / 8; b += S0_T) dst[b] = __ldg(src + b);
     const int* bp = base + (static_cast<int64_t>(p) * nchunks + blockIdx.x) * G;
-    for (int o = tid; o < G; o += S0_T) cnt[o] = __ldg(bp + o);
+    for (int o = tid; o < G; o += S0_T) gnext[o] = __ldg(bp + o);
   }
-  __syncthreads();
   const int i0 = c * ch, i1 = min(n, i0 + ch);
   float2* xdst = Xmb + static_cast<int64_t>(p) * zv.N;
   float* ydst = Ymb + static_cast<int64_t>(p) * zv.M;
   int* yp = ypos + static_cast<int64_t>(p) * zv.M;
   uint16_t* yo = yown + static_cast<int64_t>(p) * zv.M;
-  for (int e = i0 + tid; e < i1; e += S2B_U * S0_T) {
-    float zz[S2B_U], ww[S2B_U];
+  for (int e0 = i0; e0 < i1; e0 += SB) {
+    for (int o = tid; o < G; o += S0_T) lcnt[o] = 0;
+    __syncthreads();
+    float zz[SB_PER], ww[SB_PER];
+    int ow[SB_PER], rk[SB_PER];
 #pragma unroll
-    for (int k = 0; k < S2B_U; ++k) {
-      const int i = e + k * S0_T;
+    for (int k = 0; k < SB_PER; ++k) {
+      const int i = e0 + k * S0_T + tid;
       zz[k] = i < i1 ? __ldg(z + i) : 0.f;
-      if (isx) ww[k] = i < i1 ? __ldg(w + i) : 0.f;
+      ww[k] = (isx && i < i1) ? __ldg(w + i) : 0.f;
     }
 #pragma unroll
-    for (int k = 0; k < S2B_U; ++k) {
-      const int i = e + k * S0_T;
-      if (i >= i1) continue;
-      const int o = om[clamp_floor(ucoord(zz[k], uoff, hscale), NH)];
-      const int dst = atomicAdd(&cnt[o], 1);
-      if (isx) {
-        xdst[dst] = make_float2(zz[k], ww[k]);
-      } else {
-        ydst[dst] = zz[k];
-        yp[i] = dst;
-        yo[i] = static_cast<uint16_t>(o);
+    for (int k = 0; k < SB_PER; ++k) {
+      ow[k] = -1;
+      if (e0 + k * S0_T + tid < i1) {
+        ow[k] = om[clamp_floor(ucoord(zz[k], uoff, hscale), NH)];
+        rk[k] = atomicAdd(&lcnt[ow[k]], 1);
       }
     }
+    __syncthreads();
+    // exclusive starts of the owners in the sub-chunk (blocked: thread t scans owners [t * per, (t+1) * per))
+    const int per = (G + S0_T - 1) / S0_T;
+    const int o0 = min(G, tid * per), o1 = min(G, o0 + per);
+    int loc = 0;
+    for (int o = o0; o < o1; ++o) loc += lcnt[o];
+    int tot;
+    int run = block_excl_scan<S0_T>(loc, wbuf, &tot);
+    for (int o = o0; o < o1; ++o) { const int v = lcnt[o]; lcnt[o] = run; run += v; }
+    __syncthreads();
+    // stage in owner order; y: positions / owners straight to target order
+#pragma unroll
+    for (int k = 0; k < SB_PER; ++k) {
+      if (ow[k] < 0) continue;
+      const int sidx = lcnt[ow[k]] + rk[k];
+      stg[sidx] = make_float2(zz[k], ww[k]);
+      sow[sidx] = static_cast<uint16_t>(ow[k]);
+      if (!isx) {
+        const int i = e0 + k * S0_T + tid;
+        yp[i] = gnext[ow[k]] + rk[k];
+        yo[i] = static_cast<uint16_t>(ow[k]);
+      }
+    }
+    __syncthreads();
+    // write out in owner order: consecutive staging slots of an owner -> consecutive mailbox slots
+    for (int sidx = tid; sidx < tot; sidx += S0_T) {
+      const int o = sow[sidx];
+      const int dst = gnext[o] + (sidx - lcnt[o]);
+      const float2 v = stg[sidx];
+      if (isx) xdst[dst] = v;
+      else ydst[dst] = v.x;
+    }
+    __syncthreads();
+    // advance the owners' next slots by their sub-chunk counts (counts = next start - start)
+    for (int o = o0; o < o1; ++o) gnext[o] += ((o + 1 < G) ? lcnt[o + 1] : tot) - lcnt[o];
+    __syncthreads();
   }
 }
 
@@ -932,7 +970,8 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   const int nch = ncx0 + ncy0;
   const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1 + (big ? static_cast<size_t>(nch) * G : 0));
   const size_t sm2 = sizeof(int) * (((1 + S2W_WARPS) * G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
-  const size_t sm2b = sizeof(int) * ((G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
+  const size_t sm2b = sizeof(int) * 2 * ((G + 3) / 4 * 4) + (sizeof(float2) + sizeof(uint16_t)) * SB +
+                      sizeof(uint16_t) * NH;
   ZView zv = a.zv;
   zv.zx += g0 * zv.ldx;
   zv.zy += g0 * zv.ldy;
