@@ -966,7 +966,9 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   const int ncx0 = hist_chunks(N), ncy0 = hist_chunks(M);
   const int64_t per_cta2 = int64_t(S2W_WARPS) * S2W_WCH * wpc;
   const int ncx2 = static_cast<int>(cdiv(N, per_cta2)), ncy2 = static_cast<int>(cdiv(M, per_cta2));
-  const bool big = G > kSmemDabMax;   // many owners: plan bases + atomic-free partition (k_sp_part_big)
+  // many owners: plan bases + atomic-free partition (k_sp_part_big); with few (cfg2: 29) the warp rounds win
+  // (measured with the big path forced at G = 29: cfg2 0.817 -> 0.846 ms)
+  const bool big = G > kSmemDabMax;
   const int nch = ncx0 + ncy0;
   const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1 + (big ? static_cast<size_t>(nch) * G : 0));
   const size_t sm2 = sizeof(int) * (((1 + S2W_WARPS) * G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
