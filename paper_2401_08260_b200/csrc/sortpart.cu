@@ -240,23 +240,21 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
   // many owners: the first mailbox slot of every (chunk, owner) -- the owner's region start plus its counts in
   // the earlier chunks of the same part -- so that the partition needs no run reservations (k_sp_part_big)
   __syncthreads();
-  int* cnt = blo + G + 1;   // [nchunks][G]
-  for (int e = tid; e < nchunks * G; e += S0_T) cnt[e] = 0;
-  __syncthreads();
-  for (int b = tid; b < NH; b += S0_T) {
-    const int oo = min(G - 1, static_cast<int>((static_cast<int64_t>(cx[b]) * G) / Nx));
-    for (int q = 0; q < nchunks; ++q) {
+  int* cnt = blo + G + 1;   // [G] the current chunk's count per owner
+  int* run = cnt + G;       // [G] running slot per owner (the x part, then the y part)
+  for (int q = 0; q < nchunks; ++q) {
+    if (q == 0 || q == ncx)
+      for (int o = tid; o < G; o += S0_T) run[o] = (q == 0) ? cx[blo[o]] : cy[blo[o]];
+    for (int o = tid; o < G; o += S0_T) cnt[o] = 0;
+    __syncthreads();
+    for (int b = tid; b < NH; b += S0_T) {
       const int v = __ldcg(hp + static_cast<int64_t>(q) * NH + b);
-      if (v) atomicAdd(&cnt[q * G + oo], v);
+      if (v) atomicAdd(&cnt[min(G - 1, static_cast<int>((static_cast<int64_t>(cx[b]) * G) / Nx))], v);
     }
-  }
-  __syncthreads();
-  for (int o = tid; o < G; o += S0_T) {
-    const int lo = blo[o];
-    int rx = cx[lo], ry = cy[lo];
-    int* bp = base + static_cast<int64_t>(p) * nchunks * G + o;
-    for (int q = 0; q < ncx; ++q) { bp[q * G] = rx; rx += cnt[q * G + o]; }
-    for (int q = ncx; q < nchunks; ++q) { bp[q * G] = ry; ry += cnt[q * G + o]; }
+    __syncthreads();
+    int* bp = base + (static_cast<int64_t>(p) * nchunks + q) * G;
+    for (int o = tid; o < G; o += S0_T) { bp[o] = run[o]; run[o] += cnt[o]; }
+    __syncthreads();
   }
 }
 
@@ -365,13 +363,13 @@ __global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __rest
 // ~1000 owners costs about one global atomic per element).  The chunk is processed in sub-chunks of SB elements,
 // each counting-sorted by owner in shared memory before it is written, so that an owner's elements of the
 // sub-chunk leave as one contiguous run (the mailbox writes are otherwise 8-byte scatters over ~1000 regions).
-constexpr int SB_PER = 8, SB = S0_T * SB_PER;   // elements per sub-chunk
-
+template <int SB_PER>
 __global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __restrict__ w, const unsigned* __restrict__ mm,
                                                       int NH, int G, int ncx, int nchunks, int chx, int chy,
                                                       const uint16_t* __restrict__ om_g, const int* __restrict__ base,
                                                       float2* __restrict__ Xmb, float* __restrict__ Ymb,
                                                       int* __restrict__ ypos, uint16_t* __restrict__ yown) {
+  constexpr int SB = S0_T * SB_PER;   // elements per sub-chunk
   extern __shared__ __align__(16) unsigned char shb[];
   const int G4 = (G + 3) / 4 * 4;
   int* gnext = reinterpret_cast<int*>(shb);               // [G] next mailbox slot of each owner (this chunk)
@@ -814,7 +812,12 @@ SpDims sortpart_dims(int64_t N, int64_t M) {
   // owners: 85% of the owner capacity each (room for the bin granularity of the balance)
   int64_t g = cdiv(N, kSpVars[sp_variant()].cap * 85 / 100);   // (60 / 75 / 85 / 95% measured: 85-95 best, 85 leaves room)
   if (g < 1) g = 1;
-  if (g > 1024) g = 1024;   // beyond: owners take several passes
+  static int gmax = -1;
+  if (gmax < 0) {
+    const char* e = std::getenv("SKS_SP_GMAX");
+    gmax = e ? std::max(129, std::min(4096, std::atoi(e))) : 4096;
+  }
+  if (g > gmax) g = gmax;   // beyond: owners take several passes
   d.G = static_cast<int>(g);
   (void)M;
   return d;
@@ -945,7 +948,8 @@ void set_attributes() {
   if (done) return;
   cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);   // (+ static shared)
   cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_sp_part_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_sp_part_big<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_sp_part_big<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_sp_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
 #define SP_OWNER_ATTR(C, B, MB, T)                                                                              \
   cudaFuncSetAttribute(k_sp_owner<C, B, MB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
@@ -959,6 +963,20 @@ void set_attributes() {
   done = true;
 }
 
+// elements per thread of a k_sp_partbig sub-chunk (SKS_SP_SBPER = 8 | 16)
+int part_sbper(int G) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SKS_SP_SBPER");
+    v = e ? std::atoi(e) : 0;
+  }
+  if (v == 8 || v == 16) return v;
+  // measured N = 1e7, P = 100 sort stage (ms, {G cap, SB_PER}): {1024, 8} 51.3, {4096, 8} 58.2, {4096, 16} 49.1,
+  // {2048, 16} 49.4; N = 3e6 (G = 862): 8 -> 10.89, 16 -> 11.02.  More owners shorten the owner passes and the
+  // gather (26.9 -> 17.4 ms) but cut the mailbox runs per sub-chunk, so the sub-chunk grows with G.
+  return G > 1024 ? 16 : 8;
+}
+
 // the five kernels of one slice group (slices [g0, g0 + np) of the call) on stream st
 cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int np, int NH, int G, cudaStream_t st) {
   const int64_t N = a.zv.N, M = a.zv.M;
@@ -970,9 +988,10 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   // (measured with the big path forced at G = 29: cfg2 0.817 -> 0.846 ms)
   const bool big = G > kSmemDabMax;
   const int nch = ncx0 + ncy0;
-  const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1 + (big ? static_cast<size_t>(nch) * G : 0));
+  const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1 + (big ? 2 * static_cast<size_t>(G) : 0));
   const size_t sm2 = sizeof(int) * (((1 + S2W_WARPS) * G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
-  const size_t sm2b = sizeof(int) * 2 * ((G + 3) / 4 * 4) + (sizeof(float2) + sizeof(uint16_t)) * SB +
+  const int sbper = part_sbper(G);
+  const size_t sm2b = sizeof(int) * 2 * ((G + 3) / 4 * 4) + (sizeof(float2) + sizeof(uint16_t)) * S0_T * sbper +
                       sizeof(uint16_t) * NH;
   ZView zv = a.zv;
   zv.zx += g0 * zv.ldx;
@@ -989,8 +1008,8 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   prof_end(pm);
   pm = prof_begin(PS_SP_PART, st);
   if (big)
-    k_sp_part_big<<<dim3(nch, np), S0_T, sm2b, st>>>(zv, a.w, mm, NH, G, ncx0, nch, hist_chunk_len(N), hist_chunk_len(M),
-                                                     r.om, r.base, r.Xmb, r.Ymb, r.ypos, r.yown);
+    (sbper == 16 ? k_sp_part_big<16> : k_sp_part_big<8>)<<<dim3(nch, np), S0_T, sm2b, st>>>(
+        zv, a.w, mm, NH, G, ncx0, nch, hist_chunk_len(N), hist_chunk_len(M), r.om, r.base, r.Xmb, r.Ymb, r.ypos, r.yown);
   else
     k_sp_part<<<dim3(ncx2 + ncy2, np), S2W_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, wpc, r.om, r.own, r.cursor, r.Xmb,
                                                           r.Ymb, r.ypos, r.yown);

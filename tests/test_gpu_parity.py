@@ -54,6 +54,7 @@ CASES_1D = [
     ("negdist", 0.0, 3, 70000, 333, 2),
     ("negdist", 0.0, 50, 200000, 400, 2),   # ~58 owners per slice (sortpart.cu)
     ("negdist", 0.0, 50, 600000, 200, 2),   # > 128 owners: plan bases, atomic-free partition, global owner table
+    ("negdist", 0.0, 50, 5000000, 300, 1),  # > 1024 owners (sortpart_dims): sequential per-chunk plan bases
     ("gaussian", 1.0, 3, 2003, 1001, 4),
     ("gaussian", 11.0, 784, 4097, 515, 3),
     ("gaussian", 30.0, 100, 5000, 700, 3),
