@@ -137,7 +137,7 @@ __device__ __forceinline__ T block_excl_scan(T v, T* wbuf, T* total) {
 __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __restrict__ mm, int NH, int G,
                                                   int ncx, int nchunks, int chx, int chy, int NBF, int* __restrict__ H,
                                                   int* __restrict__ done, uint16_t* __restrict__ om,
-                                                  SpOwner* __restrict__ own, int* __restrict__ base) {
+                                                  SpOwner* __restrict__ own, int* __restrict__ base, int base_par) {
   extern __shared__ int hs[];   // [NH] histogram; in the plan: cx[NH + 1], cy[NH + 1], blo[G + 1]
   __shared__ int wbuf[S0_T / 32 + 1];
   __shared__ int last;
@@ -240,19 +240,45 @@ __global__ void __launch_bounds__(S0_T) k_sp_hist(ZView zv, const unsigned* __re
   // many owners: the first mailbox slot of every (chunk, owner) -- the owner's region start plus its counts in
   // the earlier chunks of the same part -- so that the partition needs no run reservations (k_sp_part_big)
   __syncthreads();
+  if (base_par) {   // all chunks at once: cnt[nchunks][G] fits in shared memory
+    int* cnt = blo + G + 1;
+    for (int e = tid; e < nchunks * G; e += S0_T) cnt[e] = 0;
+    __syncthreads();
+    for (int b = tid; b < NH; b += S0_T) {
+      const int oo = min(G - 1, static_cast<int>((static_cast<int64_t>(cx[b]) * G) / Nx));
+      for (int q = 0; q < nchunks; ++q) {
+        const int v = __ldcg(hp + static_cast<int64_t>(q) * NH + b);
+        if (v) atomicAdd(&cnt[q * G + oo], v);
+      }
+    }
+    __syncthreads();
+    for (int o = tid; o < G; o += S0_T) {
+      const int lo = blo[o];
+      int rx = cx[lo], ry = cy[lo];
+      int* bp = base + static_cast<int64_t>(p) * nchunks * G + o;
+      for (int q = 0; q < ncx; ++q) { bp[q * G] = rx; rx += cnt[q * G + o]; }
+      for (int q = ncx; q < nchunks; ++q) { bp[q * G] = ry; ry += cnt[q * G + o]; }
+    }
+    return;
+  }
+  // else one chunk at a time (shared memory O(G))
   int* cnt = blo + G + 1;   // [G] the current chunk's count per owner
-  int* run = cnt + G;       // [G] running slot per owner (the x part, then the y part)
+  int* runx = cnt + G;      // [G] running x slot per owner
+  int* runy = runx + G;     // [G] running y slot per owner
+  for (int o = tid; o < G; o += S0_T) { runx[o] = cx[blo[o]]; runy[o] = cy[blo[o]]; }
+  __syncthreads();
+  int* bown = cy;           // cy is spent: the owner of each bin (one division per bin, not one per chunk)
+  for (int b = tid; b < NH; b += S0_T) bown[b] = min(G - 1, static_cast<int>((static_cast<int64_t>(cx[b]) * G) / Nx));
   for (int q = 0; q < nchunks; ++q) {
-    if (q == 0 || q == ncx)
-      for (int o = tid; o < G; o += S0_T) run[o] = (q == 0) ? cx[blo[o]] : cy[blo[o]];
     for (int o = tid; o < G; o += S0_T) cnt[o] = 0;
     __syncthreads();
     for (int b = tid; b < NH; b += S0_T) {
       const int v = __ldcg(hp + static_cast<int64_t>(q) * NH + b);
-      if (v) atomicAdd(&cnt[min(G - 1, static_cast<int>((static_cast<int64_t>(cx[b]) * G) / Nx))], v);
+      if (v) atomicAdd(&cnt[bown[b]], v);
     }
     __syncthreads();
     int* bp = base + (static_cast<int64_t>(p) * nchunks + q) * G;
+    int* run = q < ncx ? runx : runy;
     for (int o = tid; o < G; o += S0_T) { bp[o] = run[o]; run[o] += cnt[o]; }
     __syncthreads();
   }
@@ -988,7 +1014,12 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   // (measured with the big path forced at G = 29: cfg2 0.817 -> 0.846 ms)
   const bool big = G > kSmemDabMax;
   const int nch = ncx0 + ncy0;
-  const size_t sm0 = sizeof(int) * std::max<size_t>(NH, 2 * (NH + 1) + G + 1 + (big ? 2 * static_cast<size_t>(G) : 0));
+  // plan bases: every chunk at once while cnt[nch][G] fits (measured N = 1e6, G = 288: one chunk at a time is
+  // 2% slower), else one chunk at a time
+  const size_t plan_ints = 2 * (NH + 1) + G + 1;
+  const int base_par = big && plan_ints + static_cast<size_t>(nch) * G <= 200 * 1024 / sizeof(int);
+  const size_t sm0 = sizeof(int) * std::max<size_t>(
+      NH, plan_ints + (big ? (base_par ? static_cast<size_t>(nch) * G : 3 * static_cast<size_t>(G)) : 0));
   const size_t sm2 = sizeof(int) * (((1 + S2W_WARPS) * G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
   const int sbper = part_sbper(G);
   const size_t sm2b = sizeof(int) * 2 * ((G + 3) / 4 * 4) + (sizeof(float2) + sizeof(uint16_t)) * S0_T * sbper +
@@ -1003,7 +1034,7 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   ProfMark pm = prof_begin(PS_SP_HIST, st);
   k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, hist_chunk_len(N),
                                                        hist_chunk_len(M), kSpVars[sp_variant()].nbf, r.H, r.done, r.om,
-                                                       r.own, big ? r.base : nullptr);
+                                                       r.own, big ? r.base : nullptr, base_par);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_end(pm);
   pm = prof_begin(PS_SP_PART, st);
