@@ -59,7 +59,9 @@ def main():
                     recs.append({"kernel": kind, "engine": engine, "N": N, "P": P, "error": str(e)})
                     print(json.dumps(recs[-1]), flush=True)
                     continue
-                reps = 1 if N * P >= 1e9 else 3
+                reps = max(1, min(20, int(2e9 // (N * P))))   # short calls: more repetitions
+                for _ in range(min(reps, 3)):   # warm-up (clocks, caches) before the timed calls
+                    f()
                 torch.cuda.synchronize()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
