@@ -989,7 +989,7 @@ void set_attributes() {
   done = true;
 }
 
-// elements per thread of a k_sp_partbig sub-chunk (SKS_SP_SBPER = 8 | 16)
+// elements per thread of a k_sp_part_big sub-chunk (SKS_SP_SBPER = 8 | 16)
 int part_sbper(int G) {
   static int v = -1;
   if (v < 0) {
