@@ -389,13 +389,13 @@ __global__ void __launch_bounds__(S2W_T) k_sp_part(ZView zv, const float* __rest
 // ~1000 owners costs about one global atomic per element).  The chunk is processed in sub-chunks of SB elements,
 // each counting-sorted by owner in shared memory before it is written, so that an owner's elements of the
 // sub-chunk leave as one contiguous run (the mailbox writes are otherwise 8-byte scatters over ~1000 regions).
-template <int SB_PER>
-__global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __restrict__ w, const unsigned* __restrict__ mm,
+template <int NT, int SB_PER>
+__global__ void __launch_bounds__(NT) k_sp_part_big(ZView zv, const float* __restrict__ w, const unsigned* __restrict__ mm,
                                                       int NH, int G, int ncx, int nchunks, int chx, int chy,
                                                       const uint16_t* __restrict__ om_g, const int* __restrict__ base,
                                                       float2* __restrict__ Xmb, float* __restrict__ Ymb,
                                                       int* __restrict__ ypos, uint16_t* __restrict__ yown) {
-  constexpr int SB = S0_T * SB_PER;   // elements per sub-chunk
+  constexpr int SB = NT * SB_PER;   // elements per sub-chunk
   extern __shared__ __align__(16) unsigned char shb[];
   const int G4 = (G + 3) / 4 * 4;
   int* gnext = reinterpret_cast<int*>(shb);               // [G] next mailbox slot of each owner (this chunk)
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __r
   float2* stg = reinterpret_cast<float2*>(lcnt + G4);     // [SB] sub-chunk elements in owner order
   uint16_t* sow = reinterpret_cast<uint16_t*>(stg + SB);  // [SB] owner of each staged element
   uint16_t* om = sow + SB;                                // [NH]
-  __shared__ int wbuf[S0_T / 32 + 1];
+  __shared__ int wbuf[NT / 32 + 1];
   const int p = blockIdx.y, tid = threadIdx.x;
   const bool isx = static_cast<int>(blockIdx.x) < ncx;
   const int c = isx ? blockIdx.x : blockIdx.x - ncx;
@@ -416,9 +416,9 @@ __global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __r
   {
     const uint4* src = reinterpret_cast<const uint4*>(om_g + static_cast<int64_t>(p) * NH);   // NH % 8 == 0
     uint4* dst = reinterpret_cast<uint4*>(om);
-    for (int b = tid; b < NH / 8; b += S0_T) dst[b] = __ldg(src + b);
+    for (int b = tid; b < NH / 8; b += NT) dst[b] = __ldg(src + b);
     const int* bp = base + (static_cast<int64_t>(p) * nchunks + blockIdx.x) * G;
-    for (int o = tid; o < G; o += S0_T) gnext[o] = __ldg(bp + o);
+    for (int o = tid; o < G; o += NT) gnext[o] = __ldg(bp + o);
   }
   const int i0 = c * ch, i1 = min(n, i0 + ch);
   float2* xdst = Xmb + static_cast<int64_t>(p) * zv.N;
@@ -426,32 +426,32 @@ __global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __r
   int* yp = ypos + static_cast<int64_t>(p) * zv.M;
   uint16_t* yo = yown + static_cast<int64_t>(p) * zv.M;
   for (int e0 = i0; e0 < i1; e0 += SB) {
-    for (int o = tid; o < G; o += S0_T) lcnt[o] = 0;
+    for (int o = tid; o < G; o += NT) lcnt[o] = 0;
     __syncthreads();
     float zz[SB_PER], ww[SB_PER];
     int ow[SB_PER], rk[SB_PER];
 #pragma unroll
     for (int k = 0; k < SB_PER; ++k) {
-      const int i = e0 + k * S0_T + tid;
+      const int i = e0 + k * NT + tid;
       zz[k] = i < i1 ? __ldg(z + i) : 0.f;
       ww[k] = (isx && i < i1) ? __ldg(w + i) : 0.f;
     }
 #pragma unroll
     for (int k = 0; k < SB_PER; ++k) {
       ow[k] = -1;
-      if (e0 + k * S0_T + tid < i1) {
+      if (e0 + k * NT + tid < i1) {
         ow[k] = om[clamp_floor(ucoord(zz[k], uoff, hscale), NH)];
         rk[k] = atomicAdd(&lcnt[ow[k]], 1);
       }
     }
     __syncthreads();
     // exclusive starts of the owners in the sub-chunk (blocked: thread t scans owners [t * per, (t+1) * per))
-    const int per = (G + S0_T - 1) / S0_T;
+    const int per = (G + NT - 1) / NT;
     const int o0 = min(G, tid * per), o1 = min(G, o0 + per);
     int loc = 0;
     for (int o = o0; o < o1; ++o) loc += lcnt[o];
     int tot;
-    int run = block_excl_scan<S0_T>(loc, wbuf, &tot);
+    int run = block_excl_scan<NT>(loc, wbuf, &tot);
     for (int o = o0; o < o1; ++o) { const int v = lcnt[o]; lcnt[o] = run; run += v; }
     __syncthreads();
     // stage in owner order; y: positions / owners straight to target order
@@ -462,14 +462,14 @@ __global__ void __launch_bounds__(S0_T) k_sp_part_big(ZView zv, const float* __r
       stg[sidx] = make_float2(zz[k], ww[k]);
       sow[sidx] = static_cast<uint16_t>(ow[k]);
       if (!isx) {
-        const int i = e0 + k * S0_T + tid;
+        const int i = e0 + k * NT + tid;
         yp[i] = gnext[ow[k]] + rk[k];
         yo[i] = static_cast<uint16_t>(ow[k]);
       }
     }
     __syncthreads();
     // write out in owner order: consecutive staging slots of an owner -> consecutive mailbox slots
-    for (int sidx = tid; sidx < tot; sidx += S0_T) {
+    for (int sidx = tid; sidx < tot; sidx += NT) {
       const int o = sow[sidx];
       const int dst = gnext[o] + (sidx - lcnt[o]);
       const float2 v = stg[sidx];
@@ -984,8 +984,9 @@ void set_attributes() {
   if (done) return;
   cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);   // (+ static shared)
   cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_sp_part_big<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_sp_part_big<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_sp_part_big<S0_T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_sp_part_big<S0_T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_sp_part_big<1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_sp_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
 #define SP_OWNER_ATTR(C, B, MB, T)                                                                              \
   cudaFuncSetAttribute(k_sp_owner<C, B, MB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
@@ -1013,6 +1014,20 @@ int part_sbper(int G) {
   return G > 1024 ? 16 : 8;
 }
 
+// threads of a k_sp_part_big CTA (SKS_SP_PBT = 512 | 1024; 1024: 8 elements per thread, the same 8192-element
+// sub-chunk as 512 x 16 at twice the warps per SM -- the kernel is latency bound at one CTA per SM, ncu: 25% of
+// the warp slots active).  Measured N = 1e7, P = 100 / 1000: 512 x 16 53.4 / 529 ms, 1024 x 8 49.4 / 489;
+// N = 1e6 (288 owners, 512 x 8): no difference.
+int part_big_threads(int G) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SKS_SP_PBT");
+    v = e ? std::atoi(e) : 0;
+  }
+  if (v == 512 || v == 1024) return v;
+  return G > 1024 ? 1024 : S0_T;
+}
+
 // the five kernels of one slice group (slices [g0, g0 + np) of the call) on stream st
 cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int np, int NH, int G, cudaStream_t st) {
   const int64_t N = a.zv.N, M = a.zv.M;
@@ -1032,7 +1047,8 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
       NH, plan_ints + (big ? (base_par ? static_cast<size_t>(nch) * G : 3 * static_cast<size_t>(G)) : 0));
   const size_t sm2 = sizeof(int) * (((1 + S2W_WARPS) * G + 3) / 4 * 4) + sizeof(uint16_t) * NH;
   const int sbper = part_sbper(G);
-  const size_t sm2b = sizeof(int) * 2 * ((G + 3) / 4 * 4) + (sizeof(float2) + sizeof(uint16_t)) * S0_T * sbper +
+  const int sbelems = part_big_threads(G) == 1024 ? 1024 * 8 : S0_T * sbper;
+  const size_t sm2b = sizeof(int) * 2 * ((G + 3) / 4 * 4) + (sizeof(float2) + sizeof(uint16_t)) * sbelems +
                       sizeof(uint16_t) * NH;
   ZView zv = a.zv;
   zv.zx += g0 * zv.ldx;
@@ -1049,8 +1065,12 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   prof_end(pm);
   pm = prof_begin(PS_SP_PART, st);
   if (big)
-    (sbper == 16 ? k_sp_part_big<16> : k_sp_part_big<8>)<<<dim3(nch, np), S0_T, sm2b, st>>>(
-        zv, a.w, mm, NH, G, ncx0, nch, hist_chunk_len(N), hist_chunk_len(M), r.om, r.base, r.Xmb, r.Ymb, r.ypos, r.yown);
+  {
+    const int pbt = part_big_threads(G);
+    auto kern = pbt == 1024 ? k_sp_part_big<1024, 8> : (sbper == 16 ? k_sp_part_big<S0_T, 16> : k_sp_part_big<S0_T, 8>);
+    kern<<<dim3(nch, np), pbt, sm2b, st>>>(zv, a.w, mm, NH, G, ncx0, nch, hist_chunk_len(N), hist_chunk_len(M), r.om,
+                                           r.base, r.Xmb, r.Ymb, r.ypos, r.yown);
+  }
   else
     k_sp_part<<<dim3(ncx2 + ncy2, np), S2W_T, sm2, st>>>(zv, a.w, mm, NH, G, ncx2, wpc, r.om, r.own, r.cursor, r.Xmb,
                                                           r.Ymb, r.ypos, r.yown);
