@@ -60,7 +60,8 @@ int sp_variant() {
   return v;
 }
 constexpr int S4_T = 256, S4_PER = 4, S4_CH = S4_T * S4_PER;    // gather
-constexpr int S4_SG = 8;   // slices per gather thread (measured 4 / 8 / 16 / 32: 8 best)
+constexpr int S4_SG = 8;   // slices per gather thread (measured 4 / 8 / 16 / 32: 8 best; also on the global-table
+                           // path at N = 1e7, P = 1000: 8 / 16 / 32 -> 489 / 494 / 507 ms, scratch/gsg.sh)
 constexpr int kSmemDabMax = 128;   // owners per slice up to which the gather builds the other-owner table itself
 constexpr int S0_CH = 32768;   // histogram: elements per CTA (measured 8192 / 16384 / 32768: the largest best)
 
