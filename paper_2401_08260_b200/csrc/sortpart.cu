@@ -45,6 +45,8 @@ constexpr int S0_T = 512;      // histogram threads
 // owner kernel variants (x capacity, fine buckets, CTAs per SM, threads): SKS_SP_VARIANT selects (measurement
 // aid).  Measured on B200, cfg2 sp_owner (one stream): {4096,1024,3,512} 358 us (default), {8192,2048,2,512} 438,
 // {4096,1024,4,256} 389, {2048,1024,4,512} 465, {4096,1024,2,512} 401; finer buckets {4096,2048,3,512} 418.
+// At d = 100, P = 1000 (scratch/variant.sh), N = 1e6 / 1e7 ms: variant 0 34.5 / 489, 1 37.9 / 485, 2 36.1 / 504,
+// 3 40.2 / 588, 4 36.3 / 510.
 struct SpVar {
   int cap, nbf, minb, nt;
 };
