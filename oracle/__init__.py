@@ -49,6 +49,7 @@ def lib() -> ctypes.CDLL:
             "or_F": (d, [i, d, i, d]),
             "or_f": (d, [i, d, i, i, d]),
             "or_f_vec": (None, [i, d, i, i, vp, vp, i64]),
+            "or_f_series_vec": (None, [i, d, i, i, vp, vp, i64]),
             "or_F_vec": (None, [i, d, i, vp, vp, i64]),
             "or_splitmix64": (u64, [u64]),
             "or_round_bf16": (d, [d]),
@@ -112,10 +113,21 @@ def F(kind: str, param: float, r, matern_p: int = 1) -> np.ndarray:
 
 
 def f(kind: str, param: float, d: int, r, matern_p: int = 1) -> np.ndarray:
-    """1D counterpart f of F (Table 1, App. C), series in fp64."""
+    """1D counterpart f of F (Table 1, App. C), series in fp64; at d = 3 the closed form
+    f = F + t F' of Cor 2.4 for the smooth kernels."""
     r = np.ascontiguousarray(np.atleast_1d(r), dtype=np.float64)
     out = np.empty_like(r)
     lib().or_f_vec(KIND[kind], float(param), int(matern_p), int(d), _ptr(r), _ptr(out), r.size)
+    _check()
+    return out
+
+
+def f_series(kind: str, param: float, d: int, r, matern_p: int = 1) -> np.ndarray:
+    """f by its defining series (Table 1 / App. C) at any d, bypassing the d = 3 closed form of Cor 2.4
+     that ``f`` uses; for the pins comparing the two."""
+    r = np.ascontiguousarray(np.atleast_1d(r), dtype=np.float64)
+    out = np.empty_like(r)
+    lib().or_f_series_vec(KIND[kind], float(param), int(matern_p), int(d), _ptr(r), _ptr(out), r.size)
     _check()
     return out
 

@@ -14,7 +14,8 @@
  *   (b) or_sliced_sum  s_m = (1/P) sum_p sum_n w_n f(|<xi_p,x_n> - <xi_p,y_m>|) P:454, Alg.1
  *       with the 1D sums done directly (definition) instead of a fast engine.
  *   f = the 1D counterpart of F from Table 1 / Appendix C,
- *   evaluated from its defining power series (Thm 2.2).
+ *   evaluated from its defining power series (Thm 2.2); at d = 3 from the closed form
+ *   f(t) = F(t) + t F'(t) of Cor 2.4, which needs no series.
  *   directions: DESIGN.md R1 (the paper only says "Draw P random directions").
  *
  * Pins (tests/test_oracle_*.py, -m "not gpu"): brute force on tiny inputs with hand values,
@@ -169,7 +170,53 @@ double or_f_matern(double r, double beta, int p, int d) {
 /* negative distance: f(r) = -c_d r  (Table 1) */
 double or_f_negdist(double r, int d) { return -or_cd(d) * r; }
 
+/* d = 3: Cor 2.4 gives the counterpart in closed form, f(t) = F(t) + t F'(t), for any
+ * differentiable F.  Written out for the three smooth kernels (F from Table 1 P:200-204 / P:1163):
+ *   Gaussian  F = exp(-t^2/(2 s^2)):      t F' = -(t^2/s^2) F
+ *   Laplacian F = exp(-t/ell):            t F' = -(t/ell) F
+ *   Matern    F = C e^{-q} S(q), q = sqrt(2p+1) t/beta, S(q) = sum_n a_n (2q)^{p-n}:
+ *             t F' = q dF/dq = C e^{-q} q (S'(q) - S(q)),  S'(q) = sum_{n<p} a_n 2 (p-n) (2q)^{p-n-1}.
+ * These are exact (no series), so the oracle stays conditioned at any t for d = 3. */
+static double f_d3(int kind, double param, int mp, double t) {
+  switch (kind) {
+    case OR_GAUSSIAN: {
+      double u = t * t / (param * param);
+      return (1.0 - u) * exp(-0.5 * u);
+    }
+    case OR_LAPLACIAN: {
+      double u = t / param;
+      return (1.0 - u) * exp(-u);
+    }
+    case OR_MATERN: {
+      int p = mp;
+      double q = sqrt(2.0 * p + 1.0) * t / param;
+      double C = tgamma(p + 1.0) / tgamma(2.0 * p + 1.0);
+      double S = 0.0, dS = 0.0;
+      for (int n = 0; n <= p; ++n) {
+        double a = tgamma(p + n + 1.0) / (tgamma(n + 1.0) * tgamma(p - n + 1.0));
+        S += a * pow(2.0 * q, p - n);
+        if (p - n >= 1) dS += a * 2.0 * (p - n) * pow(2.0 * q, p - n - 1);
+      }
+      return C * exp(-q) * (S + q * (dS - S));
+    }
+  }
+  return NAN;
+}
+
+/* f by its defining series (Table 1 / App. C) at any d, bypassing the d = 3 closed form; used by the
+ * pins that compare the two where the series is well conditioned. */
+double or_f_series(int kind, double param, int mp, int d, double r) {
+  switch (kind) {
+    case OR_GAUSSIAN: return or_f_gauss(r, param, d);
+    case OR_NEGDIST: return or_f_negdist(r, d);
+    case OR_LAPLACIAN: return or_f_laplace(r, 1.0 / param, d);
+    case OR_MATERN: return or_f_matern(r, param, mp, d);
+  }
+  return NAN;
+}
+
 double or_f(int kind, double param, int mp, int d, double r) {
+  if (d == 3 && kind != OR_NEGDIST) return f_d3(kind, param, mp, r);
   switch (kind) {
     case OR_GAUSSIAN: return or_f_gauss(r, param, d);
     case OR_NEGDIST: return or_f_negdist(r, d);
@@ -181,6 +228,9 @@ double or_f(int kind, double param, int mp, int d, double r) {
 
 void or_f_vec(int kind, double param, int mp, int d, const double* r, double* out, int64_t n) {
   for (int64_t i = 0; i < n; ++i) out[i] = or_f(kind, param, mp, d, r[i]);
+}
+void or_f_series_vec(int kind, double param, int mp, int d, const double* r, double* out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) out[i] = or_f_series(kind, param, mp, d, r[i]);
 }
 void or_F_vec(int kind, double param, int mp, const double* r, double* out, int64_t n) {
   for (int64_t i = 0; i < n; ++i) out[i] = or_F(kind, param, mp, r[i]);

@@ -48,18 +48,35 @@ def test_d1_counterpart_equals_F():
 
 
 def test_d3_cor24():
-    # Cor 2.4: d=3 -> f(t) = F(t) + t F'(t)
+    # Cor 2.4: d=3 -> f(t) = F(t) + t F'(t).  The oracle evaluates this closed form at d = 3; pin it
+    # against the defining series of Table 1 / App. C where the plain series is well
+    # conditioned, and against the hand-differentiated forms
     s = 1.0
     np.testing.assert_allclose(O.f("gaussian", s, 3, R), (1 - R**2 / s**2) * np.exp(-R**2 / (2 * s**2)), atol=1e-12)
     a = 0.5
     np.testing.assert_allclose(O.f("laplacian", 1 / a, 3, R), (1 - a * R) * np.exp(-a * R), atol=1e-12)
     b, s3 = 1.0, math.sqrt(3)
-    Rm = R[R <= 4.0]   # beyond, the plain alternating 1F2 series loses digits and the oracle refuses
-    np.testing.assert_allclose(O.f("matern", b, 3, Rm, matern_p=1),
-                               (1 + s3 * Rm / b - 3 * Rm**2 / b**2) * np.exp(-s3 * Rm / b), atol=1e-9)
+    np.testing.assert_allclose(O.f("matern", b, 3, R, matern_p=1),
+                               (1 + s3 * R / b - 3 * R**2 / b**2) * np.exp(-s3 * R / b), atol=1e-12)
+    Rm = R[R <= 4.0]   # beyond, the plain alternating 1F2 series loses digits and the oracle's series refuses
+    for kind, par, mp in [("gaussian", 1.0, 1), ("laplacian", 2.0, 1), ("matern", 1.0, 1), ("matern", 1.5, 2),
+                          ("matern", 2.0, 0)]:
+        np.testing.assert_allclose(O.f(kind, par, 3, Rm, matern_p=mp), O.f_series(kind, par, 3, Rm, matern_p=mp),
+                                   atol=1e-9, err_msg=f"{kind} p={mp}")
     with pytest.raises(O.OracleConditioningError):
-        O.f("matern", b, 3, [12.0], matern_p=1)
+        O.f_series("matern", b, 3, [12.0], matern_p=1)
     np.testing.assert_allclose(O.f("negdist", 0, 3, R), -2 * R, atol=1e-14)
+
+
+@pytest.mark.parametrize("kind,par,mp", [("gaussian", 1.0, 1), ("laplacian", 1.0, 1), ("matern", 1.0, 1),
+                                         ("matern", 1.0, 2), ("matern", 0.7, 0)])
+def test_d3_closed_form_by_S3_quadrature(kind, par, mp):
+    # Prop 2.3 at d = 3: the weight (1-t^2)^0 and the constant 2 Gamma(3/2)/(sqrt(pi) Gamma(1)) = 1, so
+    # F(s) = int_0^1 f(ts) dt.  Checked far beyond the series' conditioned range (s up to 20 beta)
+    for s in (0.5, 2.0, 6.0, 12.0, 20.0):
+        val, _ = integrate.quad(lambda t: float(O.f(kind, par, 3, [t * s], matern_p=mp)[0]), 0.0, 1.0, limit=400,
+                                epsabs=1e-14, epsrel=1e-13)
+        assert val == pytest.approx(float(O.F(kind, par, [s], matern_p=mp)[0]), abs=1e-12), (kind, mp, s)
 
 
 def _Sd(fun, d, s):
@@ -68,6 +85,35 @@ def _Sd(fun, d, s):
     val, _ = integrate.quad(lambda t: fun(t * s) * (1 - t * t) ** ((d - 3) / 2), 0.0, 1.0, limit=400,
                             epsabs=1e-13, epsrel=1e-12)
     return c * val
+
+
+def _Sd_highd(fun, d, s):
+    """Prop 2.3 for large d: the weight (1-t^2)^((d-3)/2) <= exp(-40) beyond t = sqrt(80/(d-3)), so the
+    integral is taken over [0, sqrt(80/(d-3))] with breakpoints at k/sqrt(d) (its width scale)."""
+    c = 2 * math.exp(math.lgamma(d / 2) - math.lgamma((d - 1) / 2)) / math.sqrt(math.pi)
+    t1 = math.sqrt(80.0 / (d - 3))
+    pts = [k / math.sqrt(d) for k in range(1, int(t1 * math.sqrt(d)) + 1) if k / math.sqrt(d) < t1]
+    val, _ = integrate.quad(lambda t: fun(t * s) * math.exp((d - 3) / 2 * math.log1p(-t * t)), 0.0, t1,
+                            points=pts, limit=800, epsabs=1e-15, epsrel=1e-13)
+    return c * val
+
+
+# the BASELINE configs' own (kind, dimension, parameter): cfg5 Gaussian d=100, cfg3 Gaussian d=784 (sigma = median
+# pairwise distance, R10/R11), cfg4 Laplacian d=3072 (ell = median pairwise distance); s spans the data's distances
+HIGHD = [("gaussian", 100, 30.65994192636891, (5.0, 20.0, 30.0, 45.0, 60.0)),
+         ("gaussian", 784, 11.025468358570834, (2.0, 5.0, 8.0, 11.0, 16.0)),
+         ("laplacian", 3072, 22.62531764763029, (4.0, 15.0, 22.6, 30.0, 40.0))]
+
+
+@pytest.mark.parametrize("kind,d,par,svals", HIGHD, ids=["cfg5", "cfg3", "cfg4"])
+def test_Sd_quadrature_config_dimensions(kind, d, par, svals):
+    # S_d f = F (Prop 2.3) at the dimensions and parameters the GPU parity tests run: pins the oracle's series for f
+    # where a dropped term or a wrong index would show (d in 100 ... 3072)
+    for s in svals:
+        fs = lambda r: float(O.f(kind, par, d, [r])[0])
+        # (the Laplacian's f has a |r| kink at 0 that the quadrature resolves to ~1e-12)
+        tol = 2e-12 if kind == "laplacian" else 1e-12
+        assert _Sd_highd(fs, d, s) == pytest.approx(float(O.F(kind, par, [s])[0]), abs=tol), (kind, d, s)
 
 
 @pytest.mark.parametrize("d", [2, 5, 10, 50])
