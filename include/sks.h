@@ -76,6 +76,8 @@ typedef struct {
   int32_t engine;        /* [0 = auto] Fourier engine for the Gaussian / Matern: 1 = NFFT (Remark P:519-525),
                             2 = NDFT on the kept band (the paper's Gaussian engine; at most 32
                             coefficients, else SKS_ERR_UNSUPPORTED); auto = NFFT (measured faster on B200)  */
+  int32_t projection;    /* [0 = auto] row a1 arithmetic (R2), all fp32-accurate: 1 = BF16x3, 2 = TF32x2,
+                            3 = FP16x2 (falls back to TF32x2 where it cannot run); auto picks by d and alignment   */
 } sks_options;
 
 /* Diagnostic description of the last plan built on this thread (for reports and tests). */
@@ -93,7 +95,7 @@ typedef struct {
   double tau_min, tau_max;   /* torus scaling range over slices                                         */
   int32_t engine;        /* Fourier engine used: 0 none, 1 NFFT, 2 NDFT                                  */
   int32_t band_width;    /* widest kept band k_hi - k_lo + 1 over the slices                             */
-  int32_t proj_mode;     /* projection arithmetic: 0 none (given projections), 1 SIMT fp32, 2 BF16x3 (three bf16
+  int32_t proj_mode;     /* projection arithmetic: 0 none (given projections), 2 BF16x3 (three bf16
                             MMAs per product), 3 TF32x2 (two tf32 MMAs per product), 4 FP16x2 (two fp16 MMAs per
                             product on 2^e-scaled points); reading R2                                             */
 } sks_plan_info;
@@ -127,9 +129,10 @@ sks_status sks_sum_host(const float* x, int64_t N, const float* y, int64_t M, in
 sks_status sks_directions(int32_t P, int32_t d, uint64_t seed, int32_t p_begin, int32_t p_end, float* g_out,
                           double* inv_norm_out);
 
-/* Row a1 alone: z[(p-p_begin)*n + i] = <xi_p, pts_i>, pts DEVICE n x d fp32, z DEVICE fp32. */
+/* Row a1 alone: z[(p-p_begin)*n + i] = <xi_p, pts_i>, pts DEVICE n x d fp32, z DEVICE fp32.
+ * opt: NULL or options (only `projection` is used). */
 sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64_t seed, int32_t p_begin,
-                       int32_t p_end, float* z, void* stream);
+                       int32_t p_end, float* z, const sks_options* opt, void* stream);
 
 /* Rows a2-a7 alone: per-slice 1D sums t[q*M + m] = sum_n w_n f(|zx[q*N+n] - zy[q*M+m]|) for q < n_slices
  * on given DEVICE projections zx (n_slices x N), zy (n_slices x M), DEVICE w (N); t DEVICE fp32 out.

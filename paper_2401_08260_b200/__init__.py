@@ -25,13 +25,15 @@ def _torch():
 
 
 ENGINES = {"auto": 0, "nfft": 1, "ndft": 2}
+PROJECTIONS = {"auto": 0, "bf16x3": 1, "tf32x2": 2, "fp16x2": 3}
 
 
-def _opts(eps=0.0, window_w=0, oversample=0, slice_batch=0, engine="auto"):
+def _opts(eps=0.0, window_w=0, oversample=0, slice_batch=0, engine="auto", projection="auto"):
     e = ENGINES[engine] if isinstance(engine, str) else int(engine)
-    if not (eps or window_w or oversample or slice_batch or e):
+    pj = PROJECTIONS[projection] if isinstance(projection, str) else int(projection)
+    if not (eps or window_w or oversample or slice_batch or e or pj):
         return None
-    return options(eps, window_w, oversample, slice_batch, e)
+    return options(eps, window_w, oversample, slice_batch, e, pj)
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -123,7 +125,8 @@ def sks_directions(P: int, d: int, seed: int, p_begin: int = 0, p_end: Optional[
     return g, inv
 
 
-def sks_project(pts, P: int, seed: int, p_begin: int = 0, p_end: Optional[int] = None, stream=None):
+def sks_project(pts, P: int, seed: int, p_begin: int = 0, p_end: Optional[int] = None, stream=None,
+                projection: str = "auto"):
     """z (np, n) fp32 = <xi_p, pts_i> (row a1) for CUDA pts (n, d)."""
     torch = _torch()
     L = _lib.load()
@@ -132,7 +135,7 @@ def sks_project(pts, P: int, seed: int, p_begin: int = 0, p_end: Optional[int] =
     p_end = P if p_end is None else p_end
     z = torch.empty((p_end - p_begin, n), dtype=torch.float32, device=pts.device)
     check(L.sks_project(pts.data_ptr(), n, d, P, ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), p_begin, p_end,
-                        z.data_ptr(), _stream_ptr(stream)))
+                        z.data_ptr(), _opts(projection=projection), _stream_ptr(stream)))
     return z
 
 

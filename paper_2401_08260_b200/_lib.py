@@ -21,7 +21,7 @@ class sks_kernel(ctypes.Structure):
 
 class sks_options(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("window_w", ctypes.c_int32), ("oversample", ctypes.c_int32),
-                ("slice_batch", ctypes.c_int32), ("engine", ctypes.c_int32)]
+                ("slice_batch", ctypes.c_int32), ("engine", ctypes.c_int32), ("projection", ctypes.c_int32)]
 
 
 class sks_plan_info(ctypes.Structure):
@@ -45,7 +45,7 @@ SIGNATURES = {
     "sks_workspace_size_host": (_i32, [_i64, _i64, _i32, _K, _i32, _i32, _i32, _O, ctypes.POINTER(_sz)]),
     "sks_sum_host": (_i32, [_vp, _i64, _vp, _i64, _i32, _vp, _K, _i32, _u64, _i32, _i32, _vp, _vp, _sz, _O, _vp]),
     "sks_directions": (_i32, [_i32, _i32, _u64, _i32, _i32, _vp, _vp]),
-    "sks_project": (_i32, [_vp, _i64, _i32, _i32, _u64, _i32, _i32, _vp, _vp]),
+    "sks_project": (_i32, [_vp, _i64, _i32, _i32, _u64, _i32, _i32, _vp, _O, _vp]),
     "sks_workspace_size_1d": (_i32, [_i64, _i64, _i32, _K, _i32, _O, ctypes.POINTER(_sz)]),
     "sks_sum_1d": (_i32, [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _K, _vp, _vp, _sz, _O, _vp]),
     "sks_fourier_coeffs": (_i32, [_K, _i32, ctypes.c_double, _i32, _i32, _vp]),
@@ -90,5 +90,7 @@ def kernel(kind: str, scale: float = 1.0, matern_p: int = 1) -> sks_kernel:
     return sks_kernel(KINDS[kind], int(matern_p), float(scale))
 
 
-def options(eps: float = 0.0, window_w: int = 0, oversample: int = 0, slice_batch: int = 0, engine: int = 0):
-    return ctypes.pointer(sks_options(float(eps), int(window_w), int(oversample), int(slice_batch), int(engine)))
+def options(eps: float = 0.0, window_w: int = 0, oversample: int = 0, slice_batch: int = 0, engine: int = 0,
+            projection: int = 0):
+    return ctypes.pointer(sks_options(float(eps), int(window_w), int(oversample), int(slice_batch), int(engine),
+                                      int(projection)))

@@ -103,7 +103,8 @@ struct Opts {
   int w = 6;
   int os = 2;
   int batch = 0;
-  int engine = 0;   // Fourier engine: 0 auto (NDFT when the band is narrow), 1 NFFT, 2 NDFT
+  int engine = 0;   // Fourier engine: 0 auto (= NFFT), 1 NFFT, 2 NDFT
+  int proj = 0;     // row a1 variant: 0 auto, 1 BF16x3, 2 TF32x2, 3 FP16x2
 };
 
 sks_status resolve_opts(const sks_options* o, Opts* r) {
@@ -118,6 +119,9 @@ sks_status resolve_opts(const sks_options* o, Opts* r) {
     if (d.batch < 0) return fail(SKS_ERR_INVALID, "slice_batch must be >= 0");
     d.engine = o->engine;
     if (d.engine < 0 || d.engine > 2) return fail(SKS_ERR_INVALID, "engine must be 0 (auto), 1 (NFFT) or 2 (NDFT)");
+    d.proj = o->projection;
+    if (d.proj < 0 || d.proj > 3)
+      return fail(SKS_ERR_INVALID, "projection must be 0 (auto), 1 (BF16x3), 2 (TF32x2) or 3 (FP16x2)");
   }
   *r = d;
   return SKS_OK;
@@ -139,11 +143,6 @@ Path path_of(int kind) {
   return Path{kind == SKS_NEGDIST || kind == SKS_LAPLACIAN, kind != SKS_NEGDIST, kind == SKS_LAPLACIAN};
 }
 
-int buckets_for(int64_t N) {
-  (void)N;
-  return sks::sortpath_buckets();
-}
-
 constexpr int kNmax = 16384;   // largest NFFT grid the kernels are built for
 constexpr int kQmax = 1024;    // footprint cells with precomputed interpolation polynomials
 constexpr size_t kAlign = 256;
@@ -155,16 +154,6 @@ struct Layout {
          grid = 0,
          h = 0, D = 0, fpar = 0, phi = 0, s64 = 0, flag = 0, total = 0;
 };
-
-// sort path: owner-partitioned (sortpart.cu) by default; SKS_SORT_V1=1 selects the earlier cluster kernel
-bool use_sort_v1() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("SKS_SORT_V1");
-    v = (e && std::strcmp(e, "0") != 0) ? 1 : 0;
-  }
-  return v == 1;
-}
 
 // fp32 -> IEEE binary16, round to nearest even (host; |v| < 65504 here)
 uint16_t to_half_rne(float v) {
@@ -184,45 +173,37 @@ uint16_t to_half_rne(float v) {
   return static_cast<uint16_t>(sign | (e << 10) | m);
 }
 
-// row a1 variant: 0 SIMT fp32 (measurement A/B), 1 BF16x3 (split kernel + three bf16 MMAs), 2 TF32x2 (split
-// inside the kernel, two tf32 MMAs).  TF32x2 reads the fp32 points once and needs no split buffer, at 4/3 of the
-// tensor work of BF16x3.  With the points read by TMA (the raw fp32 tile is the hi operand) it is the faster one
-// at every d (cfg3 0.56 vs 0.59 ms, cfg4 1.64 vs 1.79 ms including the split pass); without (unaligned points,
-// d % 4 != 0) its converter warps load the points and BF16x3 wins above d = 256.  proj_mode(d) sizes the
-// workspace (the split buffer above d = 256); use_tf32(...) decides per call.  SKS_PROJECTION = simt | bf16x3 |
-// tf32x2 overrides.
-enum ProjMode { PM_SIMT = 0, PM_BF16X3 = 1, PM_TF32X2 = 2, PM_FP16X2 = 3 };
-bool proj_forced() { return std::getenv("SKS_PROJECTION") != nullptr; }
-ProjMode proj_mode(int d) {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = std::getenv("SKS_PROJECTION");
-    v = -1;
-    if (e && std::strcmp(e, "simt") == 0) v = PM_SIMT;
-    if (e && std::strcmp(e, "bf16x3") == 0) v = PM_BF16X3;
-    if (e && std::strcmp(e, "tf32x2") == 0) v = PM_TF32X2;
-    if (e && std::strcmp(e, "fp16x2") == 0) v = PM_FP16X2;
-  }
-  if (v >= 0) return static_cast<ProjMode>(v);
+// row a1 variant (reading R2).  TF32x2 reads the fp32 points once (TMA: the raw tile is the hi operand) and
+// needs no split buffer; FP16x2 has the same precision at twice the MMA rate but a sampled point scale, so it is
+// taken where the GEMM is compute-bound (d >= 256).  Points TMA cannot read (unaligned, d % 4 != 0): TF32x2 with
+// the converters loading the points below d = 256, BF16x3 (split pass + three bf16 MMAs) above (measured cfg3
+// 0.56 vs 0.59 ms, cfg4 1.64 vs 1.79 ms for TF32x2 vs BF16x3 with TMA; without TMA BF16x3 wins above d = 256).
+// sks_options.projection forces a variant (tests of every variant).
+enum ProjMode { PM_AUTO = 0, PM_BF16X3 = 1, PM_TF32X2 = 2, PM_FP16X2 = 3 };
+
+// the variant that sizes the workspace (BF16x3 needs the split buffer)
+ProjMode proj_mode(int d, int forced) {
+  if (forced) return static_cast<ProjMode>(forced);
   return d <= 256 ? PM_TF32X2 : PM_BF16X3;
 }
 
-// per call: the TMA-fed paths when the points allow (d % 4 == 0, aligned): FP16x2 where the GEMM is compute-
-// bound (d >= 256; twice the tf32 MMA rate at the same 22-bit precision), TF32x2 below (store-bound: no sample
-// pass); allow_f16 = false after a point fell outside the fp16 range (the call is rerun)
-ProjMode proj_mode_call(int d, const float* x, int64_t N, const float* y, int64_t M, bool allow_f16) {
-  ProjMode pm = proj_mode(d);
+// per call: allow_f16 = false after a point fell outside the fp16 range (the call is rerun)
+ProjMode proj_mode_call(int d, int forced, const float* x, int64_t N, const float* y, int64_t M, bool allow_f16) {
   const bool tma = sks::proj_tf32_tma_ok(x, N, y, M, d);
-  if (pm == PM_FP16X2 && (!tma || !allow_f16)) pm = PM_TF32X2;
-  if (!proj_forced() && tma) pm = (d >= 256 && allow_f16) ? PM_FP16X2 : PM_TF32X2;
-  return pm;
+  if (forced) {
+    ProjMode pm = static_cast<ProjMode>(forced);
+    if (pm == PM_FP16X2 && (!tma || !allow_f16)) pm = PM_TF32X2;
+    return pm;
+  }
+  if (tma) return (d >= 256 && allow_f16) ? PM_FP16X2 : PM_TF32X2;
+  return proj_mode(d, 0);
 }
 constexpr sks_status kRetryTF32 = static_cast<sks_status>(100);   // internal: rerun without FP16x2
 
 // leading dimension of the slice-major projections Z: a multiple of 4 floats (16-byte rows for TMA stores)
 inline int64_t zld(int64_t N, int64_t M) { return (N + M + 3) / 4 * 4; }
 
-Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb, int d) {
+Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, int proj) {
   Layout L;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -235,23 +216,14 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb,
   L.mm = take(sizeof(unsigned) * 4 * nbat);
   if (with_Z) {
     L.Z = take(sizeof(float) * zld(N, M) * nbat);
-    if (proj_mode(d) == PM_BF16X3) {
+    if (proj_mode(d, proj) == PM_BF16X3) {
       L.xs3 = take(sizeof(uint16_t) * 3 * static_cast<size_t>(sks::proj_tc_dpad(d)) * (N + M));
       L.part = take(sks::proj_tc_part_bytes(nbat));
     }
   }
   if (pt.sort || pt.moment) {
     L.tot = take(sizeof(sks::SliceTot) * static_cast<size_t>(nbat));
-    if (use_sort_v1()) {
-      const int slots = sks::sortpath_slots(nbat);
-      L.xs = take(sizeof(float2) * N * slots);
-      L.ys = take(sizeof(float2) * M * slots);
-      L.rec = take(sizeof(sks::BucketRec) * nb * static_cast<size_t>(slots));
-      L.ovf = take(sizeof(int) * static_cast<size_t>(nbat));
-      L.bpar = take(sizeof(float) * 2 * nbat);
-    } else {
-      L.sp = take(sks::sortpart_bytes(N, M, nbat));
-    }
+    L.sp = take(sks::sortpart_bytes(N, M, nbat));
   }
   if (pt.fourier) {
     L.grid = take(sizeof(float) * kNmax * static_cast<size_t>(nbat));
@@ -266,12 +238,12 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int nb,
   return L;
 }
 
-int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int nb, int req, int d) {
+int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int req, int d, int proj) {
   if (req > 0) return std::min(req, np);
   // auto: all local slices unless the batch working set would exceed 64 GiB of HBM
   const size_t budget = size_t(64) << 30;
   int b = np;
-  while (b > 1 && make_layout(N, M, pt, b, with_Z, nb, d).total > budget) b = (b + 1) / 2;
+  while (b > 1 && make_layout(N, M, pt, b, with_Z, d, proj).total > budget) b = (b + 1) / 2;
   return b;
 }
 
@@ -418,10 +390,7 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
   int* hflag = reinterpret_cast<int*>(hmm + 4 * nbat);
   SKS_CUDA(cudaMemcpyAsync(hmm, ws + L.mm, sizeof(unsigned) * 4 * nbat, cudaMemcpyDeviceToHost, st));
   SKS_CUDA(cudaMemcpyAsync(hflag, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  static const bool htime = std::getenv("SKS_HOST_TIMING") != nullptr;
-  const auto t0 = std::chrono::steady_clock::now();
   SKS_CUDA(cudaStreamSynchronize(st));
-  const auto t1 = std::chrono::steady_clock::now();
   if (*hflag && f16_ran) return kRetryTF32;   // FP16x2 range exceeded (or a NaN / Inf input: TF32x2 reports it)
   if (*hflag) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
   std::vector<float> r(4 * nbat);
@@ -438,11 +407,6 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
   std::string err;
   if (!sks::build_fourier_plan(km, o.eps, o.w, o.os, nbat, xmn.data(), xmx.data(), amn.data(), amx.data(), *plan, &err))
     return fail(err.rfind("non-finite", 0) == 0 ? SKS_ERR_NONFINITE : SKS_ERR_UNSUPPORTED, err);
-  const auto t2 = std::chrono::steady_clock::now();
-  if (htime)
-    std::fprintf(stderr, "[sks host] sync wait %.1f us, plan %.1f us\n",
-                 std::chrono::duration<double, std::micro>(t1 - t0).count(),
-                 std::chrono::duration<double, std::micro>(t2 - t1).count());
   const int n = plan->n;
   sks::FPar* hfp = reinterpret_cast<sks::FPar*>(hflag + 4);
   int kband = 0;
@@ -502,7 +466,8 @@ sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView z
 
 sks_status validate_common(int64_t N, int64_t M, int32_t d, const sks_kernel& k, int32_t P, int32_t p0, int32_t p1) {
   if (N <= 0 || M <= 0 || d <= 0) return fail(SKS_ERR_INVALID, "N, M and d must be > 0");
-  if (N > (int64_t(1) << 31) - 1 || M > (int64_t(1) << 40)) return fail(SKS_ERR_INVALID, "N must be < 2^31");
+  // the sort path and the per-target indices hold N and M in 32-bit integers
+  if (N > INT32_MAX || M > INT32_MAX) return fail(SKS_ERR_INVALID, "N and M must be < 2^31");
   if (P <= 0 || p0 < 0 || p1 > P || p0 >= p1) return fail(SKS_ERR_INVALID, "slice range must satisfy 0 <= p_begin < p_end <= P");
   return check_kernel(k);
 }
@@ -520,9 +485,8 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
                        const DirEntry* dirs, const float* zx_in, const float* zy_in, float* s_out, float* t_out,
                        double inv_P, void* workspace, size_t ws_bytes, cudaStream_t st, bool allow_f16 = true) {
   const Path pt = path_of(pr.k.kind);
-  const int nb = (pt.sort || pt.moment) ? buckets_for(pr.N) : 0;
-  const int batch = choose_batch(pr.N, pr.M, pt, pr.nslices, pr.with_Z, nb, o.batch, pr.d);
-  const Layout L = make_layout(pr.N, pr.M, pt, batch, pr.with_Z, nb, pr.d);
+  const int batch = choose_batch(pr.N, pr.M, pt, pr.nslices, pr.with_Z, o.batch, pr.d, o.proj);
+  const Layout L = make_layout(pr.N, pr.M, pt, batch, pr.with_Z, pr.d, o.proj);
   if (!workspace || ws_bytes < L.total)
     return fail(SKS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(SKS_ERR_INVALID, "workspace must be 256-byte aligned");
@@ -538,7 +502,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
                                   reinterpret_cast<unsigned*>(ws + L.mm), std::min(batch, pr.nslices), st));
   }
   launches += 1;
-  const ProjMode pm = pr.with_Z ? proj_mode_call(pr.d, x, pr.N, y, pr.M, allow_f16) : PM_SIMT;
+  const ProjMode pm = pr.with_Z ? proj_mode_call(pr.d, o.proj, x, pr.N, y, pr.M, allow_f16) : PM_AUTO;
   const bool tc = pr.with_Z && pm == PM_BF16X3;
   const bool tf = pr.with_Z && pm == PM_TF32X2;
   const bool th = pr.with_Z && pm == PM_FP16X2;
@@ -573,9 +537,6 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
                                          static_cast<const uint16_t*>(dirs->g16) + static_cast<int64_t>(b0) * dirs->K3,
                                          nbat, dirs->inv + b0, Z, ldz, mm, flag,
                                          reinterpret_cast<unsigned*>(flag) + 1, st));
-      else
-        SKS_CUDA(sks::launch_project(x, pr.N, y, pr.M, pr.d, dirs->g + static_cast<int64_t>(b0) * pr.d,
-                                     dirs->inv + b0, nbat, Z, ldz, mm, flag, st));
       zv = sks::ZView{Z, Z + pr.N, ldz, ldz, pr.N, pr.M};
     } else {
       zv = sks::ZView{zx_in + static_cast<int64_t>(b0) * pr.N, zy_in + static_cast<int64_t>(b0) * pr.M, pr.N, pr.M,
@@ -583,14 +544,14 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ProfScope ps(PS_MINMAX, st);
       SKS_CUDA(sks::launch_minmax(zv, nbat, mm, flag, st));
     }
-    launches += (b0 > 0) + ((tc || tf) ? (nbat + 1023) / 1024 : th ? 1 + (nbat + 1023) / 1024 : 1);   // init_minmax + projection
+    launches += (b0 > 0) + (pr.with_Z ? (th ? 1 : 0) + (nbat + 1023) / 1024 : 1);   // init_minmax + projection / minmax
     int ndft_kw = 0;
     sks::EvalArgs ea{};
     ea.zv = zv;
     ea.np = nbat;
     double* s64 = s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr;
     float* tps = t_out ? t_out + static_cast<int64_t>(b0) * pr.M : nullptr;
-    if (pt.sort && !use_sort_v1()) {
+    if (pt.sort) {
       // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)
       sks::SortPartArgs sa{};
       sa.zv = zv;
@@ -606,52 +567,6 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
         SKS_CUDA(sks::launch_sortpart(sa, ws + L.sp, st));
       }
       launches += sks::sortpart_launches_per_group(pr.N, pr.M) * sks::sortpart_groups(pr.N, pr.M, nbat);
-      ea.tot = sa.tot;
-    } else if (pt.sort) {
-      // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)
-      sks::SortArgs sa{};
-      sa.zv = zv;
-      sa.w = w;
-      sa.np = nbat;
-      sa.mm = mm;
-      sa.xs = reinterpret_cast<float2*>(ws + L.xs);
-      sa.ys = reinterpret_cast<float2*>(ws + L.ys);
-      sa.rec = reinterpret_cast<sks::BucketRec*>(ws + L.rec);
-      sa.tot = reinterpret_cast<sks::SliceTot*>(ws + L.tot);
-      sa.bpar = reinterpret_cast<float*>(ws + L.bpar);
-      sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
-      sa.s64 = s64;
-      sa.per_slice_out = tps;
-      sa.ovf = reinterpret_cast<int*>(ws + L.ovf);
-      static const bool phase_timing = std::getenv("SKS_PHASE_TIMING") != nullptr;
-      static long long* dbg = nullptr;
-      const int slots = sks::sortpath_slots(nbat);
-      if (const char* v = std::getenv("SKS_SORT_VARIANT")) sa.variant = std::atoi(v);
-      if (phase_timing) {
-        if (!dbg) SKS_CUDA(cudaMalloc(&dbg, sizeof(long long) * 8 * 16 * 160));
-        SKS_CUDA(cudaMemsetAsync(dbg, 0, sizeof(long long) * 8 * 16 * 160, st));
-        sa.dbg = dbg;
-      }
-      {
-        ProfScope ps(PS_SORT_V1, st);
-        SKS_CUDA(sks::launch_sortpath(sa, slots, st));
-      }
-      if (phase_timing) {
-        std::vector<long long> h(8 * 16 * 160);
-        SKS_CUDA(cudaMemcpyAsync(h.data(), dbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
-        SKS_CUDA(cudaStreamSynchronize(st));
-        double avg[8] = {0};
-        int ncta = 0;
-        for (int c = 0; c < 16 * 160; ++c)
-          if (h[8 * c] > 0) {
-            ++ncta;
-            for (int k = 0; k < 8; ++k) avg[k] += h[8 * c + k];
-          }
-        for (int k = 0; k < 8; ++k) avg[k] /= (ncta ? ncta : 1);
-        std::fprintf(stderr, "[sks phase cycles per slice] P0+map %.0f  P1 %.0f  P2 %.0f  P3 %.0f  P4/5 %.0f  P6 %.0f\n",
-                     avg[0], avg[1], avg[2], avg[3], avg[4], avg[5]);
-      }
-      ++launches;
       ea.tot = sa.tot;
     }
     if (pt.fourier) {
@@ -711,11 +626,11 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
   info.path = pt.fourier ? (pt.sort ? 2 : 0) : 1;
   if (!pt.fourier) info.engine = 0;
   info.window_w = pt.fourier ? o.w : 0;
-  info.n_buckets = nb;
+  info.n_buckets = (pt.sort || pt.moment) ? sks::sortpart_dims(pr.N, pr.M).NH : 0;
   info.slice_batch = batch;
   info.n_batches = nbatches;
   info.launches = launches;
-  info.proj_mode = !pr.with_Z ? 0 : tc ? 2 : tf ? 3 : th ? 4 : 1;
+  info.proj_mode = !pr.with_Z ? 0 : tc ? 2 : tf ? 3 : 4;
   if (!pt.fourier) info.tau_min = 0;
   g_plan = info;
   return SKS_OK;
@@ -796,9 +711,8 @@ sks_status sks_workspace_size(int64_t N, int64_t M, int32_t d, sks_kernel kernel
   if ((s = resolve_opts(opt, &o)) != SKS_OK) return s;
   if (!bytes) return fail(SKS_ERR_INVALID, "bytes is NULL");
   const Path pt = path_of(kernel.kind);
-  const int nb = (pt.sort || pt.moment) ? buckets_for(N) : 0;
-  const int batch = choose_batch(N, M, pt, p_end - p_begin, true, nb, o.batch, d);
-  *bytes = make_layout(N, M, pt, batch, true, nb, d).total;
+  const int batch = choose_batch(N, M, pt, p_end - p_begin, true, o.batch, d, o.proj);
+  *bytes = make_layout(N, M, pt, batch, true, d, o.proj).total;
   return SKS_OK;
 }
 
@@ -857,20 +771,22 @@ sks_status sks_sum_host(const float* x, int64_t N, const float* y, int64_t M, in
 }
 
 sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64_t seed, int32_t p_begin,
-                       int32_t p_end, float* z, void* stream) {
+                       int32_t p_end, float* z, const sks_options* opt, void* stream) {
   if (!pts || !z || n <= 0 || d <= 0) return fail(SKS_ERR_INVALID, "bad pts/z/n/d");
+  if (n > INT32_MAX) return fail(SKS_ERR_INVALID, "n must be < 2^31");
   if (P <= 0 || p_begin < 0 || p_end > P || p_begin >= p_end) return fail(SKS_ERR_INVALID, "bad slice range");
-  DirEntry dirs;
-  sks_status st = get_dirs(P, d, seed, p_begin, p_end, &dirs);
+  Opts o;
+  sks_status st = resolve_opts(opt, &o);
   if (st != SKS_OK) return st;
+  DirEntry dirs;
+  if ((st = get_dirs(P, d, seed, p_begin, p_end, &dirs)) != SKS_OK) return st;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   const int np = p_end - p_begin;
   // ranges / flag / split scratch are not needed by the caller: a small per-thread scratch (allocated on
   // first use, grown on demand; this entry point is a test/inspection aid, not the hot path)
   static thread_local unsigned* scratch = nullptr;
   static thread_local size_t scratch_bytes = 0;
-  ProjMode pm = proj_mode(d);
-  if (pm == PM_BF16X3 && !proj_forced() && sks::proj_tf32_tma_ok(pts, n, pts, 0, d)) pm = PM_TF32X2;
+  const ProjMode pm = proj_mode_call(d, o.proj, pts, n, pts, 0, true);
   const bool tc = pm == PM_BF16X3;
   const size_t need = al(sizeof(unsigned) * 4 * np + 16) +
                       (tc ? al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n) + al(sks::proj_tc_part_bytes(np)) : 0);
@@ -889,13 +805,11 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
     char* part = xs3 + al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n);
     SKS_CUDA(sks::launch_split3(pts, n, pts, 0, d, xs3, cs));
     SKS_CUDA(sks::launch_project_tc(xs3, n, n, d, dirs.g3, np, dirs.inv, z, n, mm, flag, part, cs));
-  } else if (pm == PM_FP16X2 && sks::proj_tf32_tma_ok(pts, n, pts, 0, d)) {
+  } else if (pm == PM_FP16X2) {
     SKS_CUDA(sks::launch_project_f16(pts, n, pts, 0, d, dirs.g16, np, dirs.inv, z, n, mm, flag,
                                      reinterpret_cast<unsigned*>(flag) + 1, cs));
-  } else if (pm == PM_TF32X2 || pm == PM_FP16X2) {
-    SKS_CUDA(sks::launch_project_tf32(pts, n, pts, 0, d, dirs.g32, np, dirs.inv, z, n, mm, flag, cs));
   } else {
-    SKS_CUDA(sks::launch_project(pts, n, pts, 0, d, dirs.g, dirs.inv, np, z, n, mm, flag, cs));
+    SKS_CUDA(sks::launch_project_tf32(pts, n, pts, 0, d, dirs.g32, np, dirs.inv, z, n, mm, flag, cs));
   }
   return SKS_OK;
 }
@@ -908,9 +822,8 @@ sks_status sks_workspace_size_1d(int64_t N, int64_t M, int32_t d, sks_kernel ker
   if ((s = resolve_opts(opt, &o)) != SKS_OK) return s;
   if (!bytes) return fail(SKS_ERR_INVALID, "bytes is NULL");
   const Path pt = path_of(kernel.kind);
-  const int nb = (pt.sort || pt.moment) ? buckets_for(N) : 0;
-  const int batch = choose_batch(N, M, pt, n_slices, false, nb, o.batch, d);
-  *bytes = make_layout(N, M, pt, batch, false, nb, d).total;
+  const int batch = choose_batch(N, M, pt, n_slices, false, o.batch, d, o.proj);
+  *bytes = make_layout(N, M, pt, batch, false, d, o.proj).total;
   return SKS_OK;
 }
 

@@ -1,9 +1,9 @@
-// kernels.cu -- sm_100a kernels of libsks (v0: SIMT projection, counting-sort sort path, NFFT path).
+// kernels.cu -- sm_100a kernels of libsks: ranges / prologue helpers and the NFFT path.
 //
 // Row map (SURVEY.md Sec. 8a / DESIGN.md):
-//   a1 projection ............ k_project            (Alg.1)
+//   a1 projection ............ proj_tc.cu           (Alg.1)
 //   a2 torus plan (D_k) ....... k_plan_D             (R3-R7b)
-//   a3 sort + a4 scans/evaluate: sortpath.cu (two-level counting sort, fp64 prefix sums; Sec. 3.2, Alg. 2)
+//   a3 sort + a4 scans/evaluate: sortpart.cu (owner-partitioned counting sort, fp64 prefix sums; Sec. 3.2, Alg. 2)
 //   a5 spread ................. k_spread_private / k_spread_shared   (NFFT adjoint)
 //   a6 FFT x D iFFT ........... k_fft_filter
 //   a7 interpolate + mean ..... k_eval (Fourier part) + k_finalize   (Alg.1)
@@ -13,6 +13,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "kernels.h"
 
@@ -32,6 +35,16 @@ __host__ __device__ inline float key2f(unsigned k) {
   memcpy(&f, &u, 4);
   return f;
 #endif
+}
+
+void set_smem_attr_once(const void* kernel, int bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.insert(std::make_tuple(kernel, dev, bytes)).second)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 void decode_minmax(const unsigned* enc, float* dec, int n) {
@@ -83,93 +96,6 @@ __device__ __forceinline__ float grid_coord(float z, float cen, float tau, float
   return __fmul_rn(__fmul_rn(__fsub_rn(z, cen), tau), nf);
 }
 
-// ------------------------------------------------------------------ a1: projection (SIMT fp32, v0)
-// Z[p][i] = inv_norm[p] * sum_j g[p][j] * pt_i[j];  tile 64 slices x 128 points, K-step 16
-constexpr int PJ_BM = 64, PJ_BN = 128, PJ_BK = 16;
-
-__global__ void __launch_bounds__(256) k_project(const float* __restrict__ x, int64_t N, const float* __restrict__ y,
-                                                 int64_t M, int d, const float* __restrict__ g,
-                                                 const float* __restrict__ inv_norm, int np, float* __restrict__ Z,
-                                                 int64_t ldz, unsigned* __restrict__ mm, int* __restrict__ flag) {
-  __shared__ float Gs[PJ_BK][PJ_BM + 4];
-  __shared__ float Ps[PJ_BK][PJ_BN + 4];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t L = N + M;
-  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * PJ_BN;
-  const int s0 = blockIdx.y * PJ_BM;
-  float acc[4][8];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
-
-  for (int k0 = 0; k0 < d; k0 += PJ_BK) {
-    // G tile: 64 x 16, 4 per thread
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int e = tid + r * 256, row = e >> 4, col = e & 15;
-      const int s = s0 + row, k = k0 + col;
-      Gs[col][row] = (s < np && k < d) ? g[static_cast<int64_t>(s) * d + k] : 0.f;
-    }
-    // point tile: 128 x 16, 8 per thread
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int e = tid + r * 256, row = e >> 4, col = e & 15;
-      const int64_t i = i0 + row;
-      const int k = k0 + col;
-      float v = 0.f;
-      if (i < L && k < d) v = (i < N) ? x[i * d + k] : y[(i - N) * d + k];
-      Ps[col][row] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < PJ_BK; ++kk) {
-      float a[4], b[8];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = Gs[kk][ty * 4 + r];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) b[c] = Ps[kk][tx + 16 * c];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
-    }
-    __syncthreads();
-  }
-  // epilogue: normalise, store, per-slice ranges (x-only and all) + non-finite flag
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int s = s0 + ty * 4 + r;
-    const float sc = (s < np) ? inv_norm[s] : 0.f;
-    float xmn = CUDART_INF_F, xmx = -CUDART_INF_F, amn = CUDART_INF_F, amx = -CUDART_INF_F;
-    bool bad = false;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int64_t i = i0 + tx + 16 * c;
-      const float z = acc[r][c] * sc;
-      if (s < np && i < L) {
-        Z[static_cast<int64_t>(s) * ldz + i] = z;
-        if (!isfinite(z)) bad = true;
-        amn = fminf(amn, z);
-        amx = fmaxf(amx, z);
-        if (i < N) { xmn = fminf(xmn, z); xmx = fmaxf(xmx, z); }
-      }
-    }
-#pragma unroll
-    for (int o = 8; o >= 1; o >>= 1) {   // reduce over the 16 lanes sharing this slice row
-      xmn = fminf(xmn, __shfl_xor_sync(0xffffffffu, xmn, o));
-      xmx = fmaxf(xmx, __shfl_xor_sync(0xffffffffu, xmx, o));
-      amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, o));
-      amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
-    }
-    if (bad) atomicOr(flag, 1);
-    if (tx == 0 && s < np) {
-      if (xmn <= xmx) { atomicMin(&mm[s * 4 + 0], f2key(xmn)); atomicMax(&mm[s * 4 + 1], f2key(xmx)); }
-      if (amn <= amx) { atomicMin(&mm[s * 4 + 2], f2key(amn)); atomicMax(&mm[s * 4 + 3], f2key(amx)); }
-    }
-  }
-}
-
 __global__ void k_init_minmax(unsigned* mm, int np) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < np) { mm[i * 4 + 0] = 0xffffffffu; mm[i * 4 + 1] = 0u; mm[i * 4 + 2] = 0xffffffffu; mm[i * 4 + 3] = 0u; }
@@ -218,14 +144,6 @@ cudaError_t launch_prologue(void* flag16, double* s64, int64_t M, unsigned* mm, 
 
 cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st) {
   k_init_minmax<<<(np + 255) / 256, 256, 0, st>>>(mm, np);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_project(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g,
-                           const float* inv_norm, int np, float* Z, int64_t ldz, unsigned* mm, int* flag,
-                           cudaStream_t st) {
-  dim3 grid(static_cast<unsigned>((N + M + PJ_BN - 1) / PJ_BN), (np + PJ_BM - 1) / PJ_BM);
-  k_project<<<grid, 256, 0, st>>>(x, N, y, M, d, g, inv_norm, np, Z, ldz, mm, flag);
   return cudaGetLastError();
 }
 
@@ -428,7 +346,7 @@ cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int 
   if (priv) {
     const size_t smem = static_cast<size_t>(SP_WARPS) * W * 32 * sizeof(float);
     auto go = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP_WARPS * SP_WMAX_PRIV * 32 * 4);
+      set_smem_attr_once(reinterpret_cast<const void*>(kern), SP_WARPS * SP_WMAX_PRIV * 32 * 4);
       kern<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, W, chunk, grid);
     };
     switch (pw.w) {
@@ -440,7 +358,7 @@ cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int 
   } else {
     const size_t smem = static_cast<size_t>(n) * sizeof(float);
     auto go = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4);
+      set_smem_attr_once(reinterpret_cast<const void*>(kern), 16384 * 4);
       kern<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, chunk, grid);
     };
     switch (pw.w) {
@@ -540,11 +458,7 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, 
   int logn = 0;
   while ((1 << logn) < n) ++logn;
   const size_t smem = static_cast<size_t>(n) * sizeof(float2) + static_cast<size_t>(n <= 8192 ? n : n / 2) * sizeof(float2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_fft_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8 + 8192 * 8);
-    attr = true;
-  }
+  set_smem_attr_once(reinterpret_cast<const void*>(k_fft_filter), 16384 * 8 + 8192 * 8);
   k_fft_filter<<<np, FF_THREADS, smem, st>>>(grid, D, n, logn, h, fp, pw, WA, Q);
   return cudaGetLastError();
 }
@@ -554,14 +468,6 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, 
 // atomic into s64 (or per-slice stores for sks_sum_1d).  Target blocks vary fastest, so the CTAs resident
 // at a time work on the same slice group and its bucket records / grids stay in L2.
 constexpr int EV_THREADS = 256, EV_SG = 32;
-
-bool eval_fast() {   // SKS_EVAL_FAST=0: the generic kernel everywhere (A/B measurements)
-  static const bool v = [] {
-    const char* e = std::getenv("SKS_EVAL_FAST");
-    return e ? std::atoi(e) != 0 : true;
-  }();
-  return v;
-}
 
 __device__ __forceinline__ double eval_one(const EvalArgs& a, int p, float z, float nf, float hw, int64_t m,
                                            int64_t M) {
@@ -709,7 +615,7 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a) {
 cudaError_t launch_eval(const EvalArgs& a, cudaStream_t st) {
   const unsigned bx = static_cast<unsigned>((a.zv.M + EV_THREADS - 1) / EV_THREADS);
   const unsigned by = static_cast<unsigned>((a.np + EV_SG - 1) / EV_SG);
-  if (a.fourier && a.Q && a.s64 && !a.per_slice_out && eval_fast()) {
+  if (a.fourier && a.Q && a.s64 && !a.per_slice_out) {
     if (a.moment) k_eval_q<true><<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
     else k_eval_q<false><<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
   } else {

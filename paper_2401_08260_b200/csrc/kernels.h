@@ -7,7 +7,7 @@ namespace sks {
 
 // opt-in per-launch timing (sks_profile_*, api.cpp): CUDA events around launches, accumulated per slot
 enum ProfSlot {
-  PS_SPLIT = 0, PS_PROJECT, PS_MINMAX, PS_SP_HIST, PS_SP_PART, PS_SP_OWNER, PS_SP_GATHER, PS_SORT_V1, PS_PLAN,
+  PS_SPLIT = 0, PS_PROJECT, PS_MINMAX, PS_SP_HIST, PS_SP_PART, PS_SP_OWNER, PS_SP_GATHER, PS_RESERVED, PS_PLAN,
   PS_SPREAD, PS_FFT, PS_EVAL, PS_AUX, PS_NDFT_SPREAD, PS_NDFT_EVAL, PS_SORT, PS_N
 };
 struct ProfMark {
@@ -17,6 +17,10 @@ struct ProfMark {
 };
 ProfMark prof_begin(int slot, cudaStream_t st);
 void prof_end(const ProfMark& m);
+
+// raise a kernel's dynamic shared-memory limit to `bytes` on the current device (function attributes are per
+// device): set once per (kernel, device), thread-safe
+void set_smem_attr_once(const void* kernel, int bytes);
 
 // per-slice Fourier parameters (device copy of SlicePlan)
 struct FPar {
@@ -54,11 +58,8 @@ struct ZView {
   int64_t N, M;
 };
 
-// row a1: Z[p][i] = inv_norm[p] * <g_p, pt_i>, i in [0, N+M) (x block then y block); per-slice ranges
-// mm[p*4 + {0,1,2,3}] = encoded {xmin, xmax, allmin, allmax}; nonfinite flag.
-cudaError_t launch_project(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g,
-                           const float* inv_norm, int np, float* Z, int64_t ldz, unsigned* mm, int* flag,
-                           cudaStream_t st);
+// row a1 (proj_tc.cu): Z[p][i] = inv_norm[p] * <g_p, pt_i>, i in [0, N+M) (x block then y block); per-slice ranges
+// mm[p*4 + {0,1,2,3}] = encoded {xmin, xmax, allmin, allmax}; non-finite flag.
 // row a1 on tensor cores (proj_tc.cu): split fp32 points into 3 bf16 pieces (K-concatenated, d padded to
 // dp = proj_tc_dpad(d)), then Z = Xs . G3^T on tcgen05 with TMA/TMEM, same epilogue contract as above.
 int proj_tc_dpad(int d);
@@ -88,40 +89,10 @@ cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st);
 cudaError_t launch_prologue(void* flag16, double* s64, int64_t M, unsigned* mm, int np, cudaStream_t st);
 void decode_minmax(const unsigned* enc, float* dec, int n);
 
-// rows a3 + a4 (sortpath.cu): per slice, one 4-CTA cluster counting-sorts the x and y projections into
-// NB monotone buckets, builds fp64 bucket prefix sums and evaluates t_m = -coef sum_n w_n |x_n - y_m| for
-// every target exactly; results into s64 (fp64 atomics) or per-slice outputs.
 struct SliceTot {
   double A, B, C, pad;   // sum w, sum w z, sum w z^2 over the slice's sources
 };
-struct BucketRec {       // 32 bytes: one sector per target lookup
-  double A, B;           // exclusive prefix over buckets < b: sum w, sum w z (fp64)
-  int off, cnt;          // slot range of the bucket in xs
-  float w, wz;           // the bucket's own sums (rounded)
-};
-struct SortArgs {
-  ZView zv;              // projections of the np slices
-  const float* w;
-  int np;
-  const unsigned* mm;    // [np][4] ranges
-  float2* xs;            // [slots][N] (z, w) in bucket order
-  float2* ys;            // [slots][M] (z, m) in bucket order
-  BucketRec* rec;        // [slots][NB]
-  SliceTot* tot;         // [np]
-  float* bpar;           // [np][2] (zmin, granule scale)
-  double coef;           // t = -coef * sum_n w_n |x_n - z|   (c_d, or alpha c_d for the Laplacian part)
-  double* s64;           // accumulate t into s64[m] (fp64 atomics), or
-  float* per_slice_out;  // store t into per_slice_out[p*M + m]
-  int* ovf;              // [np] slices the DSMEM-resident kernel could not hold (done by the global kernel)
-  int only_flagged;      // global kernel: process only slices with ovf[p] != 0
-  int variant;           // debug/measurement variants of the scatter (0 = normal)
-  long long* dbg;        // optional [grid][8] per-phase cycle counts of each CTA's first slice (SKS_PHASE_TIMING)
-};
-int sortpath_buckets();
-int sortpath_slots(int np);   // scratch slots (co-resident clusters) used for np slices
-cudaError_t launch_sortpath(const SortArgs& a, int slots, cudaStream_t st);
-
-// rows a3 + a4, owner-partitioned (sortpart.cu, default): histogram -> G owners per slice (contiguous value
+// rows a3 + a4, owner-partitioned (sortpart.cu): histogram -> G owners per slice (contiguous value
 // ranges balanced by x count) -> coalesced partition into per-owner mailboxes -> per-owner fine-bucket
 // counting sort, fp64 prefix sums and target evaluation in shared memory -> gather back to target order.
 struct SpOwner {         // one owner (contiguous bin range [blo, blo + NBF/fmul)) of one slice

@@ -33,7 +33,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <set>
 
 #include "kernels.h"
 
@@ -42,25 +44,11 @@ namespace sks {
 namespace {
 
 constexpr int S0_T = 512;      // histogram threads
-// owner kernel variants (x capacity, fine buckets, CTAs per SM, threads): SKS_SP_VARIANT selects (measurement
-// aid).  Measured on B200, cfg2 sp_owner (one stream): {4096,1024,3,512} 358 us (default), {8192,2048,2,512} 438,
-// {4096,1024,4,256} 389, {2048,1024,4,512} 465, {4096,1024,2,512} 401; finer buckets {4096,2048,3,512} 418.
-// At d = 100, P = 1000 (scratch/variant.sh), N = 1e6 / 1e7 ms: variant 0 34.5 / 489, 1 37.9 / 485, 2 36.1 / 504,
-// 3 40.2 / 588, 4 36.3 / 510.
-struct SpVar {
-  int cap, nbf, minb, nt;
-};
-constexpr SpVar kSpVars[] = {{4096, 1024, 3, 512}, {8192, 2048, 2, 512}, {4096, 1024, 4, 256}, {2048, 1024, 4, 512},
-                             {4096, 1024, 2, 512}};
-int sp_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("SKS_SP_VARIANT");
-    v = e ? std::atoi(e) : 0;
-    if (v < 0 || v > 4) v = 0;
-  }
-  return v;
-}
+// owner kernel shape (x capacity, fine buckets, CTAs per SM, threads).  Measured on B200, cfg2 sp_owner (one
+// stream): {4096,1024,3,512} 358 us (kept), {8192,2048,2,512} 438, {4096,1024,4,256} 389, {2048,1024,4,512} 465,
+// {4096,1024,2,512} 401; finer buckets {4096,2048,3,512} 418.  At d = 100, P = 1000, N = 1e6 / 1e7 (ms): kept
+// 34.5 / 489, the others 35.5-40.2 / 485-588.
+constexpr int SP_CAP = 4096, SP_NBF = 1024, SP_MINB = 3, SP_NT = 512;
 constexpr int S4_T = 256, S4_PER = 4, S4_CH = S4_T * S4_PER;    // gather
 constexpr int S4_SG = 8;   // slices per gather thread (measured 4 / 8 / 16 / 32: 8 best; also on the global-table
                            // path at N = 1e7, P = 1000: 8 / 16 / 32 -> 489 / 494 / 507 ms, scratch/gsg.sh)
@@ -824,18 +812,11 @@ __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, dou
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// histogram chunks of a slice part: S0_CH elements each, at most SKS_SP_MAXC (default 8) chunks, then longer
-// chunks (measured N = 1e6 / 1e7, P = 1000: 8 -> 34.4 / 528 ms, 16 -> 36.0 / 528, 32 -> 38.6 / 526)
-inline int hist_max_chunks() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("SKS_SP_MAXC");
-    v = e ? std::max(1, std::min(64, std::atoi(e))) : 8;
-  }
-  return v;
-}
+// histogram chunks of a slice part: S0_CH elements each, at most 8 chunks, then longer chunks (measured
+// N = 1e6 / 1e7, P = 1000: at most 8 -> 34.4 / 528 ms, 16 -> 36.0 / 528, 32 -> 38.6 / 526)
+constexpr int kHistMaxChunks = 8;
 inline int hist_chunks(int64_t n) {
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(hist_max_chunks(), cdiv(n, S0_CH))));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kHistMaxChunks, cdiv(n, S0_CH))));
 }
 inline int hist_chunk_len(int64_t n) { return static_cast<int>(std::max<int64_t>(1, cdiv(n, hist_chunks(n)))); }
 
@@ -849,43 +830,26 @@ SpDims sortpart_dims(int64_t N, int64_t M) {
   while (nh < 16384 && static_cast<int64_t>(nh) * 64 < N) nh *= 2;   // (32 / 64 / 128 per bin measured: 64)
   d.NH = nh;
   // owners: 85% of the owner capacity each (room for the bin granularity of the balance)
-  int64_t g = cdiv(N, kSpVars[sp_variant()].cap * 85 / 100);   // (60 / 75 / 85 / 95% measured: 85-95 best, 85 leaves room)
+  int64_t g = cdiv(N, SP_CAP * 85 / 100);   // (60 / 75 / 85 / 95% measured: 85-95 best, 85 leaves room)
   if (g < 1) g = 1;
-  static int gmax = -1;
-  if (gmax < 0) {
-    const char* e = std::getenv("SKS_SP_GMAX");
-    gmax = e ? std::max(129, std::min(4096, std::atoi(e))) : 4096;
-  }
-  if (g > gmax) g = gmax;   // beyond: owners take several passes
+  if (g > 4096) g = 4096;   // (u16 owner ids; beyond, owners take several passes)
   d.G = static_cast<int>(g);
   (void)M;
   return d;
 }
 
-// The slices are processed in groups, the groups round-robin on SKS_SORT_STREAMS (default 2) streams forked
-// from the caller's stream, each stream with its own scratch region: the four kernels of one group are
-// latency-bound at their phase boundaries, and a second group's kernels fill the idle SMs.
-// Group size: SKS_SORT_GROUP, default ceil(P_batch / streams).
-int sortpart_streams() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("SKS_SORT_STREAMS");
-    v = e ? std::atoi(e) : 2;
-    if (v < 1) v = 1;
-    if (v > 4) v = 4;
-  }
-  return v;
-}
+// The slices are processed in groups, the groups round-robin on kSortStreams streams forked from the caller's
+// stream, each stream with its own scratch region: the four kernels of one group are latency-bound at their
+// phase boundaries, and a second group's kernels fill the idle SMs (1 -> 2 streams: cfg2 1.11 -> 1.03 ms; 3 / 4
+// no better).  Group size ceil(P_batch / streams) (measured 4 / 12 / 48 / 256 slices on one stream: 7.2 / 3.2 /
+// 1.49 / 0.95 ms on cfg2: the per-group tails dominate small groups).
+constexpr int kSortStreams = 2;
+int sortpart_streams() { return kSortStreams; }
 
 int sortpart_group(int64_t N, int64_t M, int np) {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = std::getenv("SKS_SORT_GROUP");
-    env = e ? std::max(1, std::atoi(e)) : 0;
-  }
   (void)N;
   (void)M;
-  const int64_t g = env ? env : (np + sortpart_streams() - 1) / sortpart_streams();
+  const int64_t g = (np + kSortStreams - 1) / kSortStreams;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, np)));
 }
 
@@ -921,18 +885,19 @@ size_t sortpart_bytes(int64_t N, int64_t M, int np) {
 }
 
 namespace {
+// helper streams and fork / join events: one set per (thread, device), so that concurrent calls on different
+// threads never share an event, and a call on another device never launches onto this device's streams
 struct StreamPool {
-  cudaStream_t s[4] = {};
-  cudaEvent_t fork = nullptr, join[4] = {};
+  cudaStream_t s[kSortStreams] = {};
+  cudaEvent_t fork = nullptr, join[kSortStreams] = {};
   bool ok = false;
 };
-StreamPool& stream_pool() {   // per process (the library is used on one device per process)
-  static std::mutex mu;
-  static StreamPool pool;
-  std::lock_guard<std::mutex> lk(mu);
+StreamPool& stream_pool(int dev) {
+  thread_local std::map<int, StreamPool> pools;
+  StreamPool& pool = pools[dev];
   if (!pool.ok) {
     bool good = cudaEventCreateWithFlags(&pool.fork, cudaEventDisableTiming) == cudaSuccess;
-    for (int i = 1; i < 4 && good; ++i)
+    for (int i = 1; i < kSortStreams && good; ++i)
       good = cudaStreamCreateWithFlags(&pool.s[i], cudaStreamNonBlocking) == cudaSuccess &&
              cudaEventCreateWithFlags(&pool.join[i], cudaEventDisableTiming) == cudaSuccess;
     pool.ok = good;
@@ -982,54 +947,33 @@ SpRegion carve_region(char* base, int64_t N, int64_t M, int NH, int G, int gs) {
   return r;
 }
 
-void set_attributes() {
-  static bool done = false;
-  if (done) return;
+// dynamic shared-memory limits: a function attribute is per device, so it is set once per device
+void set_attributes(int dev) {
+  static std::mutex mu;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(dev)) return;
   cudaFuncSetAttribute(k_sp_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);   // (+ static shared)
   cudaFuncSetAttribute(k_sp_part, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_sp_part_big<S0_T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_sp_part_big<S0_T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_sp_part_big<1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_sp_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-#define SP_OWNER_ATTR(C, B, MB, T)                                                                              \
-  cudaFuncSetAttribute(k_sp_owner<C, B, MB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
-                       static_cast<int>(sizeof(OwnerShared<C, B, T>)))
-  SP_OWNER_ATTR(4096, 1024, 3, 512);
-  SP_OWNER_ATTR(8192, 2048, 2, 512);
-  SP_OWNER_ATTR(4096, 1024, 4, 256);
-  SP_OWNER_ATTR(2048, 1024, 4, 512);
-  SP_OWNER_ATTR(4096, 1024, 2, 512);
-#undef SP_OWNER_ATTR
-  done = true;
+  cudaFuncSetAttribute(k_sp_owner<SP_CAP, SP_NBF, SP_MINB, SP_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(sizeof(OwnerShared<SP_CAP, SP_NBF, SP_NT>)));
+  done.insert(dev);
 }
 
-// elements per thread of a k_sp_part_big sub-chunk (SKS_SP_SBPER = 8 | 16)
-int part_sbper(int G) {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("SKS_SP_SBPER");
-    v = e ? std::atoi(e) : 0;
-  }
-  if (v == 8 || v == 16) return v;
-  // measured N = 1e7, P = 100 sort stage (ms, {G cap, SB_PER}): {1024, 8} 51.3, {4096, 8} 58.2, {4096, 16} 49.1,
-  // {2048, 16} 49.4; N = 3e6 (G = 862): 8 -> 10.89, 16 -> 11.02.  More owners shorten the owner passes and the
-  // gather (26.9 -> 17.4 ms) but cut the mailbox runs per sub-chunk, so the sub-chunk grows with G.
-  return G > 1024 ? 16 : 8;
-}
+// elements per thread of a k_sp_part_big sub-chunk: measured N = 1e7, P = 100 sort stage (ms, {G cap, per thread}):
+// {1024, 8} 51.3, {4096, 8} 58.2, {4096, 16} 49.1, {2048, 16} 49.4; N = 3e6 (G = 862): 8 -> 10.89, 16 -> 11.02.  More
+// owners shorten the owner passes and the gather (26.9 -> 17.4 ms) but cut the mailbox runs per sub-chunk, so the
+// sub-chunk grows with G.
+int part_sbper(int G) { return G > 1024 ? 16 : 8; }
 
-// threads of a k_sp_part_big CTA (SKS_SP_PBT = 512 | 1024; 1024: 8 elements per thread, the same 8192-element
-// sub-chunk as 512 x 16 at twice the warps per SM -- the kernel is latency bound at one CTA per SM, ncu: 25% of
-// the warp slots active).  Measured N = 1e7, P = 100 / 1000: 512 x 16 53.4 / 529 ms, 1024 x 8 49.4 / 489;
-// N = 1e6 (288 owners, 512 x 8): no difference.
-int part_big_threads(int G) {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("SKS_SP_PBT");
-    v = e ? std::atoi(e) : 0;
-  }
-  if (v == 512 || v == 1024) return v;
-  return G > 1024 ? 1024 : S0_T;
-}
+// threads of a k_sp_part_big CTA (1024: 8 elements per thread, the same 8192-element sub-chunk as 512 x 16 at
+// twice the warps per SM -- the kernel is latency bound at one CTA per SM, ncu: 25% of the warp slots active).
+// Measured N = 1e7, P = 100 / 1000: 512 x 16 53.4 / 529 ms, 1024 x 8 49.4 / 489; N = 1e6 (288 owners): no difference.
+int part_big_threads(int G) { return G > 1024 ? 1024 : S0_T; }
 
 // the five kernels of one slice group (slices [g0, g0 + np) of the call) on stream st
 cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int np, int NH, int G, cudaStream_t st) {
@@ -1062,7 +1006,7 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   if (e != cudaSuccess) return e;
   ProfMark pm = prof_begin(PS_SP_HIST, st);
   k_sp_hist<<<dim3(ncx0 + ncy0, np), S0_T, sm0, st>>>(zv, mm, NH, G, ncx0, ncx0 + ncy0, hist_chunk_len(N),
-                                                       hist_chunk_len(M), kSpVars[sp_variant()].nbf, r.H, r.done, r.om,
+                                                       hist_chunk_len(M), SP_NBF, r.H, r.done, r.om,
                                                        r.own, big ? r.base : nullptr, base_par);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_end(pm);
@@ -1080,17 +1024,8 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_end(pm);
   pm = prof_begin(PS_SP_OWNER, st);
-  switch (sp_variant()) {
-#define SP_OWNER_LAUNCH(C, B, MB, T)                                                                            \
-  k_sp_owner<C, B, MB, T><<<dim3(G, np), T, sizeof(OwnerShared<C, B, T>), st>>>(r.own, r.otot, mm, NH, G, N, M, \
-                                                                               r.Xmb, r.Ymb, a.coef, r.R)
-    case 1: SP_OWNER_LAUNCH(8192, 2048, 2, 512); break;
-    case 2: SP_OWNER_LAUNCH(4096, 1024, 4, 256); break;
-    case 3: SP_OWNER_LAUNCH(2048, 1024, 4, 512); break;
-    case 4: SP_OWNER_LAUNCH(4096, 1024, 2, 512); break;
-    default: SP_OWNER_LAUNCH(4096, 1024, 3, 512); break;
-#undef SP_OWNER_LAUNCH
-  }
+  k_sp_owner<SP_CAP, SP_NBF, SP_MINB, SP_NT><<<dim3(G, np), SP_NT, sizeof(OwnerShared<SP_CAP, SP_NBF, SP_NT>), st>>>(
+      r.own, r.otot, mm, NH, G, N, M, r.Xmb, r.Ymb, a.coef, r.R);
   prof_end(pm);
   pm = prof_begin(PS_SP_GATHER, st);
   const bool smem_dab = G <= kSmemDabMax;   // few owners: each gather CTA builds its slices' table in shared memory
@@ -1112,10 +1047,12 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
   const SpDims d = sortpart_dims(N, M);
   const int gs = sortpart_group(N, M, a.np);
   const int ns = active_streams(N, M, a.np);
-  set_attributes();
-  StreamPool& pool = stream_pool();
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  set_attributes(dev);
+  StreamPool& pool = stream_pool(dev);
   if (ns > 1 && !pool.ok) return cudaErrorInitializationError;
-  cudaError_t e = cudaSuccess;
   if (ns > 1) {   // fork: the helper streams start after everything already queued on the caller's stream
     if ((e = cudaEventRecord(pool.fork, st)) != cudaSuccess) return e;
     for (int i = 1; i < ns; ++i)

@@ -18,6 +18,11 @@ pytestmark = pytest.mark.gpu
 import paper_2401_08260_b200 as S  # noqa: E402
 
 TOL = {"negdist": 1e-5, "gaussian": 1e-4, "matern": 1e-4, "laplacian": 1e-4}
+# row a1 (reading R2): max |z_gpu - z_fp64| <= 5e-7 max ||pt||.  Every variant leaves a per-
+# coordinate residual of at most 2^-22 |x_j| (TF32x2 with the lo piece rounded to nearest, FP16x2) or 2^-24 |x_j|
+# (BF16x3), so |dz| <= 2^-22 sum_j |x_j xi_j| <= 2^-22 ||pt|| (Cauchy-Schwarz, ||xi|| = 1) = 2.4e-7 ||pt||, plus the
+# fp32 accumulation and the fp32 1/||g|| scale (a few 2^-24 |z| <= 6e-8 ||pt|| each)
+PROJ_TOL = 5e-7
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -43,7 +48,7 @@ def test_projection_parity(n, d, P):
     z = S.sks_project(dev(pts), P, seed=7).cpu().numpy()
     zo = O.project(pts, O.unit_directions(P, d, 7))
     scale = np.linalg.norm(pts.astype(np.float64), axis=1).max()
-    assert np.max(np.abs(z - zo)) <= 2e-6 * scale * max(1.0, np.sqrt(d / 50)), np.max(np.abs(z - zo))
+    assert np.max(np.abs(z - zo)) <= PROJ_TOL * scale, np.max(np.abs(z - zo)) / scale
 
 
 # ---------------------------------------------------------------- a2-a7: the 1D engines on given projections
@@ -54,15 +59,17 @@ CASES_1D = [
     ("negdist", 0.0, 3, 70000, 333, 2),
     ("negdist", 0.0, 50, 200000, 400, 2),   # ~58 owners per slice (sortpart.cu)
     ("negdist", 0.0, 50, 600000, 200, 2),   # > 128 owners: plan bases, atomic-free partition, global owner table
-    ("negdist", 0.0, 50, 5000000, 300, 1),  # > 1024 owners (sortpart_dims): sequential per-chunk plan bases
+    ("negdist", 0.0, 50, 5000000, 300, 1),  # > 1024 owners (1437): the many-owner partition with 1024-thread CTAs
     ("gaussian", 1.0, 3, 2003, 1001, 4),
     ("gaussian", 11.0, 784, 4097, 515, 3),
     ("gaussian", 30.0, 100, 5000, 700, 3),
     ("laplacian", 22.6, 3072, 3001, 517, 3),
     ("laplacian", 2.0, 50, 2500, 600, 3),
     ("matern", 8.0, 50, 3000, 600, 3),    # beta large enough that the oracle's 1F2 series stays well
-    ("matern", 3.0, 3, 1500, 400, 2),     # conditioned over the test's |dz| range
-    ("matern", 5.0, 10, 2000, 300, 2),
+    ("matern", 5.0, 10, 2000, 300, 2),    # conditioned over the test's |dz| range
+    ("matern", 1.0, 3, 1500, 400, 2),     # d = 3: the oracle's closed form (Cor 2.4), any beta (the paper's beta = 1)
+    ("laplacian", 0.5, 3, 2000, 500, 2),  # d = 3 closed form (Cor 2.4) far beyond the series' range (|dz| / ell ~ 12)
+    ("gaussian", 0.3, 3, 2000, 500, 2),
 ]
 
 
@@ -149,6 +156,22 @@ def test_sum_1d_owner_overflow_multipass():
             ref = O.sum_1d(kind, scale if kind != "negdist" else 0.0, 50, zx[q].astype(np.float64),
                            w.astype(np.float64), zy[q].astype(np.float64))
             assert rel_err(t[q], ref, w) <= TOL[kind], (kind, q)
+
+
+@pytest.mark.slow
+def test_sum_1d_sequential_plan_bases():
+    # k_sp_hist's one-chunk-at-a-time plan bases (base_par = 0): > 128 owners and 2 (NH + 1) + G + 1 + chunks * G
+    # beyond the shared-memory plan budget.  N = 4e6 (G = 1150 owners, NH = 16384) with M = 262144 targets (8 + 8
+    # histogram chunks): 32770 + 1151 + 16 * 1150 = 52321 > 51200 ints.  Checked on a target subset
+    rng = np.random.default_rng(13)
+    N, M = 4_000_000, 262_144
+    zx = rng.standard_normal((1, N)).astype(np.float32)
+    zy = (1.3 * rng.standard_normal((1, M))).astype(np.float32)
+    w = rng.uniform(0, 1, N).astype(np.float32)
+    t = S.sks_sum_1d(dev(zx), dev(zy), dev(w), 50, "negdist", 1.0).cpu().numpy()
+    sub = np.linspace(0, M - 1, 300).astype(np.int64)
+    ref = O.sum_1d("negdist", 0.0, 50, zx[0].astype(np.float64), w.astype(np.float64), zy[0, sub].astype(np.float64))
+    assert rel_err(t[0, sub], ref, w) <= TOL["negdist"]
 
 
 def test_sum_1d_targets_outside_source_range():
@@ -255,7 +278,7 @@ def test_errors_fail_loudly():
 
 
 # ---------------------------------------------------------------- BASELINE.json full sizes, sampled targets
-FULL = [("cfg2", 48), ("cfg3", 12), ("cfg4", 10)]
+FULL = [("cfg2", 256), ("cfg3", 256), ("cfg4", 256)]
 
 
 @pytest.mark.slow
@@ -270,19 +293,22 @@ def test_full_size_sampled(name, n_tgt):
 
 @pytest.mark.slow
 def test_cfg5_slice_subset_sampled():
-    # cfg5 at full N=M=1e7 on one GPU for a 2-slice sub-range of each of the 8 ranks' ranges
+    # cfg5 at full N = M = 1e7 on one GPU: a 2-slice sub-range at the start of each of the 8 ranks' ranges (16 slices
+    # spanning all 8 rank ranges, in the launch configuration of a rank: p_begin/p_end), 32 sampled targets each
+    from paper_2401_08260_b200.parallel import slice_range
     cfg = I.CONFIGS["cfg5"]
     x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
     param = I.kernel_param(cfg)
     xd, yd, wd = dev(x), dev(y), dev(w)
-    tgt = I.target_subset(cfg.M, 8)
-    for rank in (0, 7):
-        p0 = rank * cfg.P // 8
+    tgt = I.target_subset(cfg.M, 32)
+    for rank in range(8):
+        p0 = slice_range(rank, 8, cfg.P)[0]
         s = S.sks_sum(xd, yd, wd, "gaussian", param, cfg.P, cfg.dir_seed, p_begin=p0, p_end=p0 + 2).cpu().numpy()
         ref = O.sliced_sum("gaussian", param, x, y, w, cfg.P, cfg.dir_seed, targets=tgt, p0=p0, p1=p0 + 2)
         # the 2-slice partial is (1/P) * sum of 2 slices: compare on the per-slice-mean scale
         err = rel_err(s[tgt] * cfg.P / 2, ref * cfg.P / 2, w)
-        assert err <= TOL["gaussian"], err
+        print(f"cfg5 rank {rank} slices [{p0}, {p0 + 2}): max|ds|/sum|w| = {err:.3e}")
+        assert err <= TOL["gaussian"], (rank, err)
 
 
 # ---------------------------------------------------------------- the paper's error claims on the GPU path
@@ -312,29 +338,20 @@ def test_many_slices_projection_chunks():
     assert rel_err(s_a + s_b, s_all, I.weights(cfg)) <= 1e-6
 
 
-@pytest.mark.parametrize("mode", ["bf16x3", "tf32x2", "fp16x2", "simt"])
-def test_projection_modes_subprocess(mode):
-    # every row-a1 variant (R2) against the fp64 projection, at small and large d (the variant is fixed per process)
-    import subprocess
-    import sys
-    import textwrap
-    code = textwrap.dedent(f"""
-        import sys, numpy as np, torch
-        sys.path.insert(0, {repr(str(__import__('pathlib').Path(__file__).resolve().parents[1]))})
-        import oracle as O, paper_2401_08260_b200 as S
-        for n, d, P in [(300, 3, 64), (1000, 50, 70), (257, 784, 33), (129, 3072, 17), (700, 100, 300)]:
-            pts = np.random.default_rng(n + d).uniform(-1, 1, (n, d)).astype(np.float32)
-            z = S.sks_project(torch.from_numpy(pts).cuda(), P, seed=7).cpu().numpy()
-            zo = O.project(pts, O.unit_directions(P, d, 7))
-            scale = np.linalg.norm(pts.astype(np.float64), axis=1).max()
-            err = np.max(np.abs(z - zo)) / scale
-            assert err <= 2e-6 * max(1.0, np.sqrt(d / 50)), (n, d, P, err)
-        print("ok")
-    """)
-    import os
-    env = dict(os.environ, SKS_PROJECTION=mode)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+@pytest.mark.parametrize("mode", ["bf16x3", "tf32x2", "fp16x2"])
+def test_projection_modes(mode):
+    # every row-a1 variant (R2) against the fp64 projection, at small and large d (sks_options.projection)
+    for n, d, P in [(300, 3, 64), (1000, 50, 70), (257, 784, 33), (129, 3072, 17), (700, 100, 300), (333, 52, 9)]:
+        pts = np.random.default_rng(n + d).uniform(-1, 1, (n, d)).astype(np.float32)
+        z = S.sks_project(dev(pts), P, seed=7, projection=mode).cpu().numpy()
+        zo = O.project(pts, O.unit_directions(P, d, 7))
+        scale = np.linalg.norm(pts.astype(np.float64), axis=1).max()
+        err = np.max(np.abs(z - zo)) / scale
+        assert err <= PROJ_TOL, (mode, n, d, P, err)
+    # the end-to-end sum on a forced variant
+    cfg = I.scaled(I.CONFIGS["cfg2"], N=3000, M=500, P=8)
+    _, got, ref, w, _ = run_cfg(cfg, n_tgt=100, projection=mode)
+    assert rel_err(got, ref, w) <= TOL["negdist"]
 
 
 def test_fp16x2_default_scaling_and_range_fallback():
@@ -376,8 +393,8 @@ def test_projection_paths_small_shapes(N, M, d, kind):
     err = rel_err(s, ref, w)
     tol = TOL[kind]
     if kind == "negdist":
-        # exact up to the projections' rounding (R2: |dz| <= 2e-6 ||pt||): |dt| <= c_d sum|w| 2 * 2e-6 max||pt||
+        # exact up to the projections' rounding (R2: |dz| <= PROJ_TOL ||pt||): |dt| <= c_d sum|w| 2 PROJ_TOL max||pt||
         import math
         cd = math.sqrt(math.pi) * math.exp(math.lgamma((d + 1) / 2) - math.lgamma(d / 2))
-        tol = max(tol, 4e-6 * cd * max(np.linalg.norm(x, axis=1).max(), np.linalg.norm(y, axis=1).max()))
+        tol = max(tol, 2 * PROJ_TOL * cd * max(np.linalg.norm(x, axis=1).max(), np.linalg.norm(y, axis=1).max()))
     assert err <= tol, (N, M, d, kind, err, tol, S.sks_last_plan())
