@@ -4,8 +4,11 @@
 Metric (BASELINE.json): slice-points/s = (N+M)*P / t and ms per kernel sum.  A "step" is one full
 kernel sum (all Sec. 8a rows: projection, sort/Fourier 1D engines, slice mean, and for N>1 GPUs the
 NCCL all-reduce of the M-length partial sums) over one batch of seeded synthetic inputs already
-resident in HBM.  Default workload: BASELINE.json configs[1] ("cfg2", negative distance, d=50,
-N=M=1e5, P=256).  Slices are partitioned over ranks ([rP/G, (r+1)P/G)), scaling is strong.
+resident in HBM.  Default workload: BASELINE.json configs[4] ("cfg5", Gaussian, d=100, N=M=1e7, P=512), the
+largest configuration that fits one GPU (all 512 slices on one GPU at N=1; 64 per GPU at N=8) and the one the
+1 -> 8 GPU target is defined on.  Slices are partitioned over ranks ([rP/G, (r+1)P/G)) by
+parallel.distributed_sliced_sum, whose one NCCL all-reduce combines the partial sums; scaling is strong (the
+total work is fixed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfgX] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
@@ -40,7 +43,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=sorted(I.CONFIGS))
+    ap.add_argument("--config", default="cfg5", choices=sorted(I.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -55,69 +58,79 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
 
 
-# ------------------------------------------------------------------ roofline model per kernel (DESIGN.md Sec. 6)
+# ------------------------------------------------------------------ roofline model per kernel (SURVEY.md Sec. 8(d))
+# Algorithmic work per SLICE-POINT (one point of L = N + M on one slice), SURVEY.md Sec. 8(d) / DESIGN.md Sec. 6:
+#   projection  2 d fp32-accurate flops + 4 B projection store (+ 4 d / P_local B of input)
+#   sort path   84 B: 4 B projection store (counted in the projection) + 80 B for the sort stage (4 LSD passes x
+#               (4 B key + 4 B payload) x read/write = 64 B, 4 B histogram, 8 B scan read, ~4 B output)
+#   Fourier     4 B projection load (+ 2m window taps of arithmetic; spread over the x, interpolation over the y)
+# The "compulsory" figures are this build's own minimum traffic (each input read once, each output written
+# once: the owner-partitioned sort moves 28 B per slice-point, not 80), reported beside the Sec. 8(d) fraction.
+SORT_B_PER_SP = 80.0
+
+
 def roofline_model(slot, cfg, P, plan):
-    """(algorithmic HBM bytes, algorithmic flops) of ONE launch of each kernel slot over P slices: compulsory
-    traffic (each input read once, each output written once) and the method's own arithmetic; the per-unit
-    figures and their derivation are in DESIGN.md Sec. 6."""
+    """(Sec. 8(d) bytes, compulsory bytes, (bound kind, algorithmic flops)) of ONE launch of a kernel slot over P
+    slices."""
     N, M, d = cfg.N, cfg.M, cfg.d
     L = N + M
-    dp = (d + 63) // 64 * 64
     n = plan.get("n_grid", 0) or 0
-    if slot == "split3":        # fp32 points -> 3 bf16 pieces
-        return 4 * L * d + 6 * L * dp, 0
-    if slot == "project":       # Z = X G^T, 2 L d P fp32-accurate flops.  BF16x3 (plan proj_mode 2): read the 3
-        if plan.get("proj_mode") == 2:   # bf16 pieces and G, write Z; TF32x2 (3) / FP16x2 (4): the fp32 points
-            return 6 * L * dp + 2 * P * dp + 4 * L * P, ("tensor", 2.0 * L * d * P)
-        dp32 = (d + 31) // 32 * 32
-        return 4 * L * d + 4 * P * dp32 + 4 * L * P, ("tensor", 2.0 * L * d * P)
-    if slot == "sp_hist":       # read every projection
-        return 4 * L * P, 0
-    if slot == "sp_part":       # read projections and w, write x mailbox (z, w), y mailbox (z) + positions
-        return 4 * L * P + 4 * N + (8 * N + 8 * M) * P, 0
-    if slot == "sp_owner":      # read the mailboxes, write t per (slice, target)
-        return (8 * N + 8 * M) * P, 0
-    if slot == "sp_gather":     # read positions and t, accumulate s (fp64)
-        return 8 * M * P + 16 * M, 0
-    if slot == "sortsum":       # the sort stage as a whole: the sum of its four kernels' compulsory traffic
-        return sum(roofline_model(k, cfg, P, plan)[0] for k in ("sp_hist", "sp_part", "sp_owner", "sp_gather")), 0
-    if slot == "sortsum_v1":
-        return 4 * L * P + 4 * N + 16 * M, 0
-    if slot == "spread":        # per point and slice: w window taps, each a degree-7 Horner (7 FMA) and one FMA
-        w = plan.get("window_w", 6) or 6
-        return 4 * N * P + 4 * N + 4 * n * P, ("alu", 2.0 * N * P * w * 8)
+    w = plan.get("window_w", 6) or 6
+    if slot == "project":
+        by = 4 * L * d + 4 * L * P
+        return by, by, ("tensor", 2.0 * L * d * P)
+    if slot == "split3":
+        return 4 * L * d, 4 * L * d + 6 * L * ((d + 63) // 64 * 64), None
+    comp = {"sp_hist": 4 * L * P, "sp_part": 4 * L * P + 4 * N + (8 * N + 8 * M) * P,
+            "sp_owner": (8 * N + 8 * M) * P, "sp_gather": 8 * M * P + 16 * M}
+    if slot in comp:
+        return comp[slot], comp[slot], None
+    if slot == "sortsum":   # the sort stage (fork .. join of its kernels on two streams)
+        return SORT_B_PER_SP * L * P, sum(comp.values()), None
+    if slot == "spread":    # per x slice-point: w taps, each a degree-7 window polynomial (even/odd form: 4 FMA
+        #                     per tap) and one FMA into the grid
+        return 4 * N * P, 4 * N * P + 4 * N + 4 * n * P, ("alu", 2.0 * N * P * w * 5)
+    if slot == "eval":      # per y slice-point: one degree-7 Horner (7 FMA) on the cell's interpolation polynomial
+        return 4 * M * P, 4 * M * P + 16 * M + 4 * n * P, ("alu", 2.0 * M * P * 7)
     if slot == "fft_filter":
-        return 4 * n * P + 4 * (n // 2 + 1) * P + 4 * n * P, 0
+        return 8 * n * P, 8 * n * P + 4 * (n // 2 + 1) * P, None
     if slot == "plan_D":
-        return 4 * (n // 2 + 1) * P, 0
-    if slot == "eval":          # Fourier interpolation: one degree-7 Horner per target and slice (+ moment term)
-        return 4 * M * P + 16 * M + 4 * n * P, ("alu", 2.0 * M * P * 7)
-    return 0, 0
+        return 4 * (n // 2 + 1) * P, 4 * (n // 2 + 1) * P, None
+    return 0, 0, None
+
+
+def tensor_peak(pk, pmode):
+    """fp32-accurate flops/s of the projection (reading R2): TF32x2 = two tf32 MMAs per product at half the bf16
+    rate (the guide's nominal tf32:bf16 ratio), FP16x2 = two fp16 MMAs at the bf16 rate, BF16x3 = three."""
+    div = {3: 4.0, 4: 2.0}.get(pmode, 3.0)
+    src = {3: "MEASURED_PEAKS.json bf16_tflops / 4 (TF32x2: 2 tf32 MMAs per fp32 product, tf32 = bf16 / 2 nominal)",
+           4: "MEASURED_PEAKS.json bf16_tflops / 2 (FP16x2: 2 fp16 MMAs per fp32 product, fp16 = bf16 rate)"}
+    return pk["bf16_tflops"] / div, src.get(pmode, "MEASURED_PEAKS.json bf16_tflops / 3 (BF16x3)")
 
 
 def roofline(slot, cfg, P, plan, ms_per_launch, pk, traffic):
-    """achieved / peak of one kernel: bound = the larger of its HBM time and its arithmetic time at peak
-    (tensor: fp32-accurate TF32x2 / BF16x3 = two tf32 / three bf16 MMAs per fp32 product, R2; alu: FP32 FMA)."""
-    by, fl = roofline_model(slot, cfg, P, plan)
+    """achieved / peak of one kernel, Sec. 8(d) units: the bound is the larger of the HBM time of its Sec. 8(d)
+    bytes and the time of its algorithmic arithmetic at peak (tensor for the projection, FP32 FMA for the
+    spread / interpolation).  Also the compulsory-traffic fraction (this build's own minimum bytes)."""
+    by, comp, fl = roofline_model(slot, cfg, P, plan)
     kind, fl = fl if fl else (None, 0.0)
     t = ms_per_launch * 1e-3
-    pmode = plan.get("proj_mode")
-    tdiv = {3: 4.0, 4: 2.0}.get(pmode, 3.0)   # MMA-equivalents per fp32-accurate product (bf16-rate units)
-    peaks_tf = {"tensor": pk["bf16_tflops"] / tdiv,
-                "alu": 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12}
-    srcs = {"tensor": {3: "MEASURED_PEAKS.json bf16_tflops / 4 (TF32x2 fp32 emulation: two tf32 MMAs per product, "
-                          "tf32 = bf16 / 2 nominal)",
-                       4: "MEASURED_PEAKS.json bf16_tflops / 2 (FP16x2 fp32 emulation: two fp16 MMAs per product, "
-                          "fp16 = bf16 rate)"}.get(pmode, "MEASURED_PEAKS.json bf16_tflops / 3 (BF16x3 fp32 emulation)"),
-            "alu": "148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (MEASURED_PEAKS.json; B200_PROFILING unit counts)"}
-    if fl and fl / (peaks_tf[kind] * 1e12) > by / (pk["hbm_gbs"] * 1e9):
-        r = {"kernel": slot, "bound": kind, "achieved": fl / t / 1e12, "peak": peaks_tf[kind], "unit": "TFLOP/s",
-             "peak_source": srcs[kind], "algorithmic_flops_per_launch": fl}
+    alu = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    peaks_tf = {"tensor": tensor_peak(pk, plan.get("proj_mode")),
+                "alu": (alu, "148 SMs x 128 FP32 lanes x 2 flop/FMA x sm_max_mhz (MEASURED_PEAKS.json; B200_PROFILING "
+                             "unit counts)")}
+    hbm = pk["hbm_gbs"]
+    if fl and fl / (peaks_tf[kind][0] * 1e12) > by / (hbm * 1e9):
+        r = {"kernel": slot, "bound": kind, "achieved": fl / t / 1e12, "peak": peaks_tf[kind][0], "unit": "TFLOP/s",
+             "peak_source": peaks_tf[kind][1], "algorithmic_flops_per_launch": fl}
     else:
-        r = {"kernel": slot, "bound": "hbm", "achieved": by / t / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
-             "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else ""),
-             "algorithmic_bytes_per_launch": by}
+        r = {"kernel": slot, "bound": "hbm", "achieved": by / t / 1e9, "peak": hbm, "unit": "GB/s",
+             "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else "")}
     r["frac"] = r["achieved"] / r["peak"]
+    r["model"] = "SURVEY.md Sec. 8(d) per-slice-point work x slice-points per launch"
+    r["algorithmic_bytes_per_launch"] = by
+    r["compulsory_bytes_per_launch"] = comp
+    r["compulsory_frac"] = comp / t / 1e9 / hbm
     r["traffic"] = traffic
     return r
 
@@ -253,6 +266,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     G = world
     if world > 1:
+        # NCCL init logging (stderr): the communicator lines show nranks / the NVLink(S) transport
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -276,10 +292,11 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
-        S.sks_sum(xd, yd, wd, cfg.kind, scale, cfg.P, cfg.dir_seed, p0, p1, cfg.matern_p, out=s, workspace=ws)
-        if G > 1:
-            dist.all_reduce(s)
+    from paper_2401_08260_b200.parallel import distributed_sliced_sum
+
+    def step():   # this rank's slice range through the C-ABI, then the one all-reduce (SUM) of the partials
+        distributed_sliced_sum(lambda a, b: S.sks_sum(xd, yd, wd, cfg.kind, scale, cfg.P, cfg.dir_seed, a, b,
+                                                      cfg.matern_p, out=s, workspace=ws), cfg.P)
 
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
