@@ -23,14 +23,18 @@
  *     faster for the _host variant).
  *   - The library allocates no memory on the hot path.  It keeps a small immutable per-process cache
  *     of device copies of the directions, keyed by (seed, P, d, p_begin, p_end), created on first use.
- *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All work is enqueued
- *     on `stream`; the call returns after the stream has executed it (v0 synchronises twice: the Fourier
- *     planner reads back the per-slice projection ranges once per slice batch, and every call reads back
- *     the non-finite flag at its end so that SKS_ERR_NONFINITE is reported by the call itself).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All work is enqueued on
+ *     `stream` with no host synchronisation inside: the per-slice torus plan (row a2) is computed on the device
+ *     from the projection epilogue's ranges, and the FP16x2 -> TF32x2 projection rerun is a device-predicated
+ *     launch.  The device status of the call (non-finite projection, a plan beyond the built grid) sits in the
+ *     first 48 bytes of the workspace.  By default the call ends with ONE synchronisation of `stream` that reads
+ *     it back, so errors are returned by the call itself; with sks_options.async = 1 the call returns right after
+ *     enqueueing and sks_sync_status(workspace, stream) reports the status later.
  *   - Return value: SKS_OK or an error status; sks_last_error() then returns a thread-local message.
  *     On error the contents of output buffers are unspecified.
- *   - Thread safety: calls on different streams / threads may run concurrently; the direction cache
- *     is internally locked.
+ *   - Thread safety: calls on different threads may run concurrently (each thread uses its own helper streams
+ *     and events; the direction / planner / graph caches are internally locked), also on different devices of
+ *     one process.  Two calls must not share a workspace while either is in flight.
  */
 #ifndef SKS_H_
 #define SKS_H_
@@ -49,7 +53,7 @@ typedef enum {
                                exceeds the built limits (grid n > 16384)                                 */
   SKS_ERR_CUDA = 3,         /* CUDA runtime error (incl. no device / missing sm_100a support)            */
   SKS_ERR_WORKSPACE = 4,    /* workspace NULL or smaller than sks_workspace_size()                       */
-  SKS_ERR_NONFINITE = 5     /* a projection was NaN/Inf (checked by the planner / at the end of the call) */
+  SKS_ERR_NONFINITE = 5     /* a projection was NaN/Inf (device flag, read at the call's synchronisation)  */
 } sks_status;
 
 typedef enum {
@@ -78,16 +82,22 @@ typedef struct {
                             coefficients, else SKS_ERR_UNSUPPORTED); auto = NFFT (measured faster on B200)  */
   int32_t projection;    /* [0 = auto] row a1 arithmetic (R2), all fp32-accurate: 1 = BF16x3, 2 = TF32x2,
                             3 = FP16x2 (falls back to TF32x2 where it cannot run); auto picks by d and alignment   */
+  int32_t async;         /* [0] 1: return right after enqueueing (no synchronisation); the device status is read by
+                            sks_sync_status(workspace, stream)                                                     */
+  int32_t graph;         /* [0] 1: replay the call as a CUDA graph (implies async).  The first call with a given set
+                            of arguments (pointers, sizes, kernel, P, seed, range, options, stream) runs eagerly and
+                            captures its launches; later identical calls launch the instantiated graph (one
+                            cudaGraphLaunch): for launch-latency-bound problems (hard part 9)        */
 } sks_options;
 
 /* Diagnostic description of the last plan built on this thread (for reports and tests). */
 typedef struct {
   int32_t path;          /* 0 = Fourier only, 1 = sort only, 2 = sort + Fourier                        */
-  int32_t n_grid;        /* NFFT grid length n (power of two), 0 if no Fourier part                     */
+  int32_t n_grid;        /* largest per-slice NFFT grid length n_p (power of two), 0 if no Fourier part */
   int32_t k_max;         /* largest |k| kept over the slices                                            */
   int32_t band_lo_min;   /* smallest lower band edge over the slices (Gaussian bands exclude 0..lo-1)   */
   int32_t window_w;      /* taps per point                                                              */
-  int32_t spread_cells;  /* widest per-slice grid footprint W (cells)                                   */
+  int32_t spread_cells;  /* widest per-slice footprint W of the x points (cells)                        */
   int32_t n_buckets;     /* buckets of the counting sort (sort part), 0 if none                         */
   int32_t slice_batch;   /* slices per batch                                                            */
   int32_t n_batches;     /* batches in the call                                                         */
@@ -98,6 +108,8 @@ typedef struct {
   int32_t proj_mode;     /* projection arithmetic: 0 none (given projections), 2 BF16x3 (three bf16
                             MMAs per product), 3 TF32x2 (two tf32 MMAs per product), 4 FP16x2 (two fp16 MMAs per
                             product on 2^e-scaled points); reading R2                                             */
+  int32_t fused;         /* 1: the sources' projections were spread from the tensor-core accumulators (rows a1 + a5
+                            fused, never stored), 0: projections stored and re-read            */
 } sks_plan_info;
 
 /* Bytes of DEVICE workspace sks_sum needs for this problem (slice range [p_begin, p_end) of P).
@@ -148,8 +160,15 @@ sks_status sks_sum_1d(const float* zx, const float* zy, const float* w, int64_t 
  * R7 / R7b closed forms for LAPLACIAN (smooth part of the Sec. 3.3 decomposition) and MATERN). */
 sks_status sks_fourier_coeffs(sks_kernel kernel, int32_t d, double tau, int32_t k0, int32_t k1, double* out);
 
-/* Plan of the last sks_sum / sks_sum_1d call on this thread. */
+/* Plan of the last sks_sum / sks_sum_1d call on this thread.  The device-planned fields (n_grid, k_max,
+ * band_lo_min, spread_cells, band_width, tau_min/max) are filled when the call's status was read back (the
+ * default synchronous call, or sks_sync_status after an async one). */
 sks_status sks_last_plan(sks_plan_info* info);
+
+/* Synchronise `stream` and return the device status of the last call that used `workspace` (DEVICE pointer
+ * passed to sks_sum / sks_sum_1d): SKS_OK, SKS_ERR_NONFINITE or SKS_ERR_UNSUPPORTED (a plan needing a grid
+ * beyond the built limit, or an NDFT band wider than 32).  Also completes sks_last_plan's device fields. */
+sks_status sks_sync_status(void* workspace, void* stream);
 
 /* Opt-in measurement support (bench.py): while enabled, every kernel launch of sks_sum / sks_sum_1d is
  * bracketed by CUDA events recorded on the launch stream (negligible overhead, no synchronisation). */

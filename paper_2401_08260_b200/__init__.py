@@ -15,7 +15,7 @@ from . import _lib
 from ._lib import SKSError, check, kernel, options  # noqa: F401
 
 __all__ = ["sks_workspace_size", "sks_sum", "sks_sum_host", "sks_workspace_size_host", "sks_directions",
-           "sks_project", "sks_sum_1d", "sks_workspace_size_1d", "sks_fourier_coeffs", "sks_last_plan",
+           "sks_project", "sks_sum_1d", "sks_workspace_size_1d", "sks_fourier_coeffs", "sks_last_plan", "sks_sync_status",
            "sks_version", "sks_profile_enable", "sks_profile_read", "SKSError"]
 
 
@@ -28,12 +28,13 @@ ENGINES = {"auto": 0, "nfft": 1, "ndft": 2}
 PROJECTIONS = {"auto": 0, "bf16x3": 1, "tf32x2": 2, "fp16x2": 3}
 
 
-def _opts(eps=0.0, window_w=0, oversample=0, slice_batch=0, engine="auto", projection="auto"):
+def _opts(eps=0.0, window_w=0, oversample=0, slice_batch=0, engine="auto", projection="auto", async_=False,
+          graph=False):
     e = ENGINES[engine] if isinstance(engine, str) else int(engine)
     pj = PROJECTIONS[projection] if isinstance(projection, str) else int(projection)
-    if not (eps or window_w or oversample or slice_batch or e or pj):
+    if not (eps or window_w or oversample or slice_batch or e or pj or async_ or graph):
         return None
-    return options(eps, window_w, oversample, slice_batch, e, pj)
+    return options(eps, window_w, oversample, slice_batch, e, pj, int(bool(async_)), int(bool(graph)))
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -182,6 +183,11 @@ def sks_profile_read() -> dict:
     check(L.sks_profile_read(ms.ctypes.data, cnt.ctypes.data, 16))
     names = L.sks_profile_names().decode().split(",")
     return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(names)}
+
+
+def sks_sync_status(workspace, stream=None) -> None:
+    """Synchronise the stream and raise SKSError if the last call on `workspace` (async / graph) failed."""
+    check(_lib.load().sks_sync_status(workspace.data_ptr(), _stream_ptr(stream)))
 
 
 def sks_last_plan() -> dict:

@@ -21,7 +21,8 @@ class sks_kernel(ctypes.Structure):
 
 class sks_options(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("window_w", ctypes.c_int32), ("oversample", ctypes.c_int32),
-                ("slice_batch", ctypes.c_int32), ("engine", ctypes.c_int32), ("projection", ctypes.c_int32)]
+                ("slice_batch", ctypes.c_int32), ("engine", ctypes.c_int32), ("projection", ctypes.c_int32),
+                ("async_", ctypes.c_int32), ("graph", ctypes.c_int32)]
 
 
 class sks_plan_info(ctypes.Structure):
@@ -30,7 +31,7 @@ class sks_plan_info(ctypes.Structure):
                 ("n_buckets", ctypes.c_int32), ("slice_batch", ctypes.c_int32), ("n_batches", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("tau_min", ctypes.c_double), ("tau_max", ctypes.c_double),
                 ("engine", ctypes.c_int32), ("band_width", ctypes.c_int32),
-                ("proj_mode", ctypes.c_int32)]
+                ("proj_mode", ctypes.c_int32), ("fused", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -50,6 +51,7 @@ SIGNATURES = {
     "sks_sum_1d": (_i32, [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _K, _vp, _vp, _sz, _O, _vp]),
     "sks_fourier_coeffs": (_i32, [_K, _i32, ctypes.c_double, _i32, _i32, _vp]),
     "sks_last_plan": (_i32, [ctypes.POINTER(sks_plan_info)]),
+    "sks_sync_status": (_i32, [_vp, _vp]),
     "sks_profile_enable": (_i32, [_i32]),
     "sks_profile_read": (_i32, [_vp, _vp, _i32]),
     "sks_profile_names": (ctypes.c_char_p, []),
@@ -91,6 +93,6 @@ def kernel(kind: str, scale: float = 1.0, matern_p: int = 1) -> sks_kernel:
 
 
 def options(eps: float = 0.0, window_w: int = 0, oversample: int = 0, slice_batch: int = 0, engine: int = 0,
-            projection: int = 0):
+            projection: int = 0, async_: int = 0, graph: int = 0):
     return ctypes.pointer(sks_options(float(eps), int(window_w), int(oversample), int(slice_batch), int(engine),
-                                      int(projection)))
+                                      int(projection), int(async_), int(graph)))

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsks.so")
-SOURCES = ["kernels.cu", "sortpart.cu", "ndft.cu", "proj_tc.cu", "api.cpp", "host.cpp"]
+SOURCES = ["kernels.cu", "plan.cu", "sortpart.cu", "ndft.cu", "proj_tc.cu", "fused.cu", "api.cpp", "host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -31,6 +31,11 @@ struct Prof {
   int64_t cnt[PS_N] = {};
 } g_prof;
 
+bool capturing(cudaStream_t st) {   // no timing events inside a CUDA-graph capture
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
 cudaEvent_t prof_event() {
   if (!g_prof.pool.empty()) {
     cudaEvent_t e = g_prof.pool.back();
@@ -48,7 +53,7 @@ struct ProfScope {   // brackets one launch with events on its stream when profi
   cudaEvent_t a = nullptr;
   ProfScope(int s, cudaStream_t stream) : slot(s), st(stream) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
-    if (!g_prof.on) return;
+    if (!g_prof.on || capturing(st)) return;
     a = prof_event();
     cudaEventRecord(a, st);
   }
@@ -68,7 +73,7 @@ namespace sks {
 ProfMark prof_begin(int slot, cudaStream_t st) {
   ProfMark m{slot, st, nullptr};
   std::lock_guard<std::mutex> lk(g_prof.mu);
-  if (!g_prof.on) return m;
+  if (!g_prof.on || capturing(st)) return m;
   m.a = prof_event();
   cudaEventRecord(m.a, st);
   return m;
@@ -105,6 +110,8 @@ struct Opts {
   int batch = 0;
   int engine = 0;   // Fourier engine: 0 auto (= NFFT), 1 NFFT, 2 NDFT
   int proj = 0;     // row a1 variant: 0 auto, 1 BF16x3, 2 TF32x2, 3 FP16x2
+  int async = 0;    // 1: enqueue only (status through sks_sync_status)
+  int graph = 0;    // 1: replay a captured CUDA graph of the call (implies async)
 };
 
 sks_status resolve_opts(const sks_options* o, Opts* r) {
@@ -122,6 +129,8 @@ sks_status resolve_opts(const sks_options* o, Opts* r) {
     d.proj = o->projection;
     if (d.proj < 0 || d.proj > 3)
       return fail(SKS_ERR_INVALID, "projection must be 0 (auto), 1 (BF16x3), 2 (TF32x2) or 3 (FP16x2)");
+    d.graph = o->graph ? 1 : 0;
+    d.async = (o->async || d.graph) ? 1 : 0;
   }
   *r = d;
   return SKS_OK;
@@ -143,17 +152,27 @@ Path path_of(int kind) {
   return Path{kind == SKS_NEGDIST || kind == SKS_LAPLACIAN, kind != SKS_NEGDIST, kind == SKS_LAPLACIAN};
 }
 
-constexpr int kNmax = 16384;   // largest NFFT grid the kernels are built for
-constexpr int kQmax = 1024;    // footprint cells with precomputed interpolation polynomials
+constexpr int kNcapLog = 14;
+constexpr int kNcap = 1 << kNcapLog;   // largest NFFT grid the kernels are built for (n_cap)
 constexpr size_t kAlign = 256;
 inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
+// the call's status area at the start of the workspace: flag16 [4] (kernels.h), plan summary [8], + slack
+constexpr size_t kStatusBytes = 64;
+
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
-  size_t Z = 0, xs3 = 0, part = 0, mm = 0, xs = 0, ys = 0, rec = 0, tot = 0, bpar = 0, ovf = 0, sp = 0, Q = 0, what = 0,
-         grid = 0,
-         h = 0, D = 0, fpar = 0, phi = 0, s64 = 0, flag = 0, total = 0;
+  size_t status = 0, s64 = 0, mm = 0, Z = 0, xs3 = 0, part = 0, tot = 0, sp = 0, grid = 0, D = 0, fpar = 0, Q = 0,
+         what = 0, bound = 0, total = 0;
 };
+
+// rows a1 + a5 fused (fused.cu) for the Fourier-only kernels when the sources are many: their projections are
+// spread from the tensor-core accumulators and never stored; only the targets' projections go through HBM.  The
+// decision depends on the problem's shape only (never on data), so the workspace size is known up front.
+constexpr int64_t kFusedMinN = 1 << 18;
+bool fused_shape(int64_t N, int d, Path pt, bool with_Z, int w) {
+  return with_Z && pt.fourier && !pt.sort && N >= kFusedMinN && d <= 128 && d % 4 == 0 && (w % 2) == 0 && w >= 4;
+}
 
 // fp32 -> IEEE binary16, round to nearest even (host; |v| < 65504 here)
 uint16_t to_half_rne(float v) {
@@ -187,23 +206,21 @@ ProjMode proj_mode(int d, int forced) {
   return d <= 256 ? PM_TF32X2 : PM_BF16X3;
 }
 
-// per call: allow_f16 = false after a point fell outside the fp16 range (the call is rerun)
-ProjMode proj_mode_call(int d, int forced, const float* x, int64_t N, const float* y, int64_t M, bool allow_f16) {
+ProjMode proj_mode_call(int d, int forced, const float* x, int64_t N, const float* y, int64_t M) {
   const bool tma = sks::proj_tf32_tma_ok(x, N, y, M, d);
   if (forced) {
     ProjMode pm = static_cast<ProjMode>(forced);
-    if (pm == PM_FP16X2 && (!tma || !allow_f16)) pm = PM_TF32X2;
+    if (pm == PM_FP16X2 && !tma) pm = PM_TF32X2;
     return pm;
   }
-  if (tma) return (d >= 256 && allow_f16) ? PM_FP16X2 : PM_TF32X2;
+  if (tma) return d >= 256 ? PM_FP16X2 : PM_TF32X2;
   return proj_mode(d, 0);
 }
-constexpr sks_status kRetryTF32 = static_cast<sks_status>(100);   // internal: rerun without FP16x2
 
 // leading dimension of the slice-major projections Z: a multiple of 4 floats (16-byte rows for TMA stores)
 inline int64_t zld(int64_t N, int64_t M) { return (N + M + 3) / 4 * 4; }
 
-Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, int proj) {
+Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, int proj, bool fused) {
   Layout L;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -211,11 +228,11 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, 
     o += al(bytes);
     return at;
   };
-  L.flag = take(16);
+  L.status = take(kStatusBytes);
   L.s64 = take(sizeof(double) * M);
   L.mm = take(sizeof(unsigned) * 4 * nbat);
   if (with_Z) {
-    L.Z = take(sizeof(float) * zld(N, M) * nbat);
+    L.Z = take(sizeof(float) * (fused ? zld(0, M) : zld(N, M)) * nbat);   // fused: the targets' block only
     if (proj_mode(d, proj) == PM_BF16X3) {
       L.xs3 = take(sizeof(uint16_t) * 3 * static_cast<size_t>(sks::proj_tc_dpad(d)) * (N + M));
       L.part = take(sks::proj_tc_part_bytes(nbat));
@@ -226,30 +243,28 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, 
     L.sp = take(sks::sortpart_bytes(N, M, nbat));
   }
   if (pt.fourier) {
-    L.grid = take(sizeof(float) * kNmax * static_cast<size_t>(nbat));
-    L.h = take(sizeof(float) * kNmax * static_cast<size_t>(nbat));
-    L.D = take(sizeof(float) * (kNmax / 2 + 1) * static_cast<size_t>(nbat));
+    L.grid = take(sizeof(float) * kNcap * static_cast<size_t>(nbat));
+    L.D = take(sizeof(float) * (kNcap / 2 + 1) * static_cast<size_t>(nbat));
     L.fpar = take(sizeof(sks::FPar) * nbat);
-    L.phi = take(sizeof(float) * (kNmax / 2 + 1));
-    L.Q = take(sizeof(float) * kQmax * (sks::PW_D + 1) * static_cast<size_t>(nbat));
-    L.what = take(sizeof(double) * 2 * 32 * static_cast<size_t>(nbat));
+    L.Q = take(sizeof(float) * sks::q_stride(kNcap) * static_cast<size_t>(nbat));
+    L.what = take(sizeof(double) * 2 * sks::kNdftWidth * static_cast<size_t>(nbat));
+    if (fused) L.bound = take(sks::source_bound_bytes(d));
   }
   L.total = o;
   return L;
 }
 
-int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int req, int d, int proj) {
+int choose_batch(int64_t N, int64_t M, Path pt, int np, bool with_Z, int req, int d, int proj, bool fused) {
   if (req > 0) return std::min(req, np);
   // auto: all local slices unless the batch working set would exceed 64 GiB of HBM
   const size_t budget = size_t(64) << 30;
   int b = np;
-  while (b > 1 && make_layout(N, M, pt, b, with_Z, d, proj).total > budget) b = (b + 1) / 2;
+  while (b > 1 && make_layout(N, M, pt, b, with_Z, d, proj, fused).total > budget) b = (b + 1) / 2;
   return b;
 }
 
 // ---- direction cache (device copies; immutable once created)
 struct DirEntry {
-  float* g = nullptr;      // np x d
   float* inv = nullptr;    // np
   void* g3 = nullptr;      // np x dp bf16: g zero padded (BF16x3 tensor-core operand)
   int K3 = 0;              // dp
@@ -277,60 +292,43 @@ sks_status get_dirs(int P, int d, uint64_t seed, int p0, int p1, DirEntry* out) 
   std::vector<float> invf(np);
   for (int i = 0; i < np; ++i) invf[i] = static_cast<float>(inv[i]);
   DirEntry e;
-  SKS_CUDA(cudaMalloc(&e.g, sizeof(float) * g.size()));
   SKS_CUDA(cudaMalloc(&e.inv, sizeof(float) * np));
-  SKS_CUDA(cudaMemcpy(e.g, g.data(), sizeof(float) * g.size(), cudaMemcpyHostToDevice));
   SKS_CUDA(cudaMemcpy(e.inv, invf.data(), sizeof(float) * np, cudaMemcpyHostToDevice));
-  {
-    const int dp = sks::proj_tc_dpad(d);
-    e.K3 = dp;
-    std::vector<uint16_t> g3(static_cast<size_t>(np) * e.K3, 0);
-    for (int p = 0; p < np; ++p)
-      for (int j = 0; j < d; ++j) {
-        uint32_t u;
-        std::memcpy(&u, &g[static_cast<size_t>(p) * d + j], 4);
-        g3[static_cast<size_t>(p) * e.K3 + j] = static_cast<uint16_t>(u >> 16);   // exact: g is bf16 (R1)
-      }
-    SKS_CUDA(cudaMalloc(&e.g3, sizeof(uint16_t) * g3.size()));
-    SKS_CUDA(cudaMemcpy(e.g3, g3.data(), sizeof(uint16_t) * g3.size(), cudaMemcpyHostToDevice));
-    e.K32 = sks::proj_tf32_dpad(d);
-    std::vector<float> g32(static_cast<size_t>(np) * e.K32, 0.f);
-    for (int p = 0; p < np; ++p)
-      for (int j = 0; j < d; ++j) g32[static_cast<size_t>(p) * e.K32 + j] = g[static_cast<size_t>(p) * d + j];
-    SKS_CUDA(cudaMalloc(&e.g32, sizeof(float) * g32.size()));
-    SKS_CUDA(cudaMemcpy(e.g32, g32.data(), sizeof(float) * g32.size(), cudaMemcpyHostToDevice));
-    std::vector<uint16_t> g16(static_cast<size_t>(np) * e.K3, 0);
-    for (int p = 0; p < np; ++p)
-      for (int j = 0; j < d; ++j) g16[static_cast<size_t>(p) * e.K3 + j] = to_half_rne(256.0f * g[static_cast<size_t>(p) * d + j]);
-    SKS_CUDA(cudaMalloc(&e.g16, sizeof(uint16_t) * g16.size()));
-    SKS_CUDA(cudaMemcpy(e.g16, g16.data(), sizeof(uint16_t) * g16.size(), cudaMemcpyHostToDevice));
-  }
+  const int dp = sks::proj_tc_dpad(d);
+  e.K3 = dp;
+  std::vector<uint16_t> g3(static_cast<size_t>(np) * e.K3, 0);
+  for (int p = 0; p < np; ++p)
+    for (int j = 0; j < d; ++j) {
+      uint32_t u;
+      std::memcpy(&u, &g[static_cast<size_t>(p) * d + j], 4);
+      g3[static_cast<size_t>(p) * e.K3 + j] = static_cast<uint16_t>(u >> 16);   // exact: g is bf16 (R1)
+    }
+  SKS_CUDA(cudaMalloc(&e.g3, sizeof(uint16_t) * g3.size()));
+  SKS_CUDA(cudaMemcpy(e.g3, g3.data(), sizeof(uint16_t) * g3.size(), cudaMemcpyHostToDevice));
+  e.K32 = sks::proj_tf32_dpad(d);
+  std::vector<float> g32(static_cast<size_t>(np) * e.K32, 0.f);
+  for (int p = 0; p < np; ++p)
+    for (int j = 0; j < d; ++j) g32[static_cast<size_t>(p) * e.K32 + j] = g[static_cast<size_t>(p) * d + j];
+  SKS_CUDA(cudaMalloc(&e.g32, sizeof(float) * g32.size()));
+  SKS_CUDA(cudaMemcpy(e.g32, g32.data(), sizeof(float) * g32.size(), cudaMemcpyHostToDevice));
+  std::vector<uint16_t> g16(static_cast<size_t>(np) * e.K3, 0);
+  for (int p = 0; p < np; ++p)
+    for (int j = 0; j < d; ++j) g16[static_cast<size_t>(p) * e.K3 + j] = to_half_rne(256.0f * g[static_cast<size_t>(p) * d + j]);
+  SKS_CUDA(cudaMalloc(&e.g16, sizeof(uint16_t) * g16.size()));
+  SKS_CUDA(cudaMemcpy(e.g16, g16.data(), sizeof(uint16_t) * g16.size(), cudaMemcpyHostToDevice));
   g_dirs[key] = e;
   *out = e;
   return SKS_OK;
 }
 
-// ---- pinned host staging (per thread, grows)
-struct Staging {
-  void* p = nullptr;
-  size_t cap = 0;
-  ~Staging() {
-    if (p) cudaFreeHost(p);
-  }
+// ---- planner constants: data-independent, cached per device (host fp64 + one upload of the window table)
+struct PlanEntry {
+  sks::PlanConst pc{};
+  sks::PolyWin pw{};
+  float* phi2inv = nullptr;   // device [kNcap / 2 + 1]
 };
-thread_local Staging g_stage;
-
-sks_status stage(size_t bytes, void** out) {
-  if (g_stage.cap < bytes) {
-    if (g_stage.p) cudaFreeHost(g_stage.p);
-    g_stage.p = nullptr;
-    g_stage.cap = 0;
-    SKS_CUDA(cudaHostAlloc(&g_stage.p, bytes, cudaHostAllocDefault));
-    g_stage.cap = bytes;
-  }
-  *out = g_stage.p;
-  return SKS_OK;
-}
+std::mutex g_plan_mu;
+std::map<std::tuple<int, int, int, double, int, double, int, int>, PlanEntry> g_plans;
 
 sks::CoeffConst coeff_const(const sks_kernel& k, int d) {
   sks::CoeffConst c{};
@@ -352,17 +350,17 @@ sks::CoeffConst coeff_const(const sks_kernel& k, int d) {
   return c;
 }
 
-sks::PolyWin poly_win(const sks::FourierPlan& plan) {
+sks::PolyWin poly_win(const sks::WindowTables& wt) {
   sks::PolyWin pw{};
-  pw.w = plan.w;
-  for (size_t i = 0; i < sizeof(pw.c) / sizeof(float); ++i) pw.c[i] = i < plan.poly.size() ? plan.poly[i] : 0.f;
+  pw.w = wt.w;
+  for (size_t i = 0; i < sizeof(pw.c) / sizeof(float); ++i) pw.c[i] = i < wt.poly.size() ? wt.poly[i] : 0.f;
   // centered even / odd form of taps j < w/2 (fp64 binomial re-expansion of the power basis about f = 1/2)
   constexpr int D = sks::PW_D;
   static_assert(D == 7, "even/odd split assumes degree 7");
-  for (int j = 0; j < (plan.w + 1) / 2 && j < 6; ++j) {
+  for (int j = 0; j < (wt.w + 1) / 2 && j < 6; ++j) {
     double dm[D + 1] = {0};
     for (int k = 0; k <= D; ++k) {
-      const double ck = (static_cast<size_t>(j) * (D + 1) + k < plan.poly.size()) ? plan.poly[j * (D + 1) + k] : 0.0;
+      const double ck = (static_cast<size_t>(j) * (D + 1) + k < wt.poly.size()) ? wt.poly[j * (D + 1) + k] : 0.0;
       double binom = 1.0;   // C(k, m) (1/2)^{k - m} u^m
       for (int m = 0; m <= k; ++m) {
         dm[m] += ck * binom * std::pow(0.5, k - m);
@@ -377,92 +375,42 @@ sks::PolyWin poly_win(const sks::FourierPlan& plan) {
   return pw;
 }
 
-// Fourier part of one batch: planner (one readback of the ranges), device D_k, spread, FFT filter.
-// Fourier part of one batch.  *ndft_kw = padded band width when the NDFT engine was chosen (rows a5 + a7 by
-// ndft.cu; evaluation is then launch_ndft_eval), 0 for the NFFT (spread + FFT filter here, k_eval later).
-sks_status fourier_batch(const sks_kernel& k, int d, const Opts& o, sks::ZView zv, const float* w, int nbat,
-                         char* ws, const Layout& L, cudaStream_t st, sks::FourierPlan* plan, int* launches,
-                         int* ndft_kw, bool f16_ran) {
-  void* hbuf = nullptr;
-  sks_status s = stage(sizeof(unsigned) * 4 * nbat + 16 + sizeof(sks::FPar) * nbat + sizeof(float) * (kNmax / 2 + 1), &hbuf);
-  if (s != SKS_OK) return s;
-  unsigned* hmm = static_cast<unsigned*>(hbuf);
-  int* hflag = reinterpret_cast<int*>(hmm + 4 * nbat);
-  SKS_CUDA(cudaMemcpyAsync(hmm, ws + L.mm, sizeof(unsigned) * 4 * nbat, cudaMemcpyDeviceToHost, st));
-  SKS_CUDA(cudaMemcpyAsync(hflag, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  SKS_CUDA(cudaStreamSynchronize(st));
-  if (*hflag && f16_ran) return kRetryTF32;   // FP16x2 range exceeded (or a NaN / Inf input: TF32x2 reports it)
-  if (*hflag) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
-  std::vector<float> r(4 * nbat);
-  sks::decode_minmax(hmm, r.data(), 4 * nbat);
-  std::vector<float> xmn(nbat), xmx(nbat), amn(nbat), amx(nbat);
-  for (int p = 0; p < nbat; ++p) {
-    xmn[p] = r[4 * p];
-    xmx[p] = r[4 * p + 1];
-    amn[p] = r[4 * p + 2];
-    amx[p] = r[4 * p + 3];
-    if (zv.N == 0) { xmn[p] = amn[p]; xmx[p] = amx[p]; }
+sks_status get_plan(const sks_kernel& k, int d, const Opts& o, bool ndft, PlanEntry* out) {
+  int dev = 0;
+  SKS_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(dev, k.kind, k.kind == SKS_MATERN ? k.matern_p : 0, k.scale, d, o.eps, o.w, o.os);
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto it = g_plans.find(key);
+  if (it == g_plans.end()) {
+    PlanEntry e;
+    const sks::KernelModel km{k.kind, k.matern_p, k.scale, d};
+    e.pc.cc = coeff_const(k, d);
+    e.pc.reps = sks::decay_radius(km, o.eps);
+    e.pc.eps = o.eps;
+    e.pc.os = o.os;
+    e.pc.w = o.w;
+    e.pc.ncap_log = kNcapLog;
+    const sks::WindowTables& wt = sks::window_tables(o.w, o.os, kNcap);
+    if (!(wt.poly_err < 1e-4))
+      return fail(SKS_ERR_UNSUPPORTED, "window polynomial fit failed (error " + std::to_string(wt.poly_err) + ")");
+    e.pw = poly_win(wt);
+    SKS_CUDA(cudaMalloc(&e.phi2inv, sizeof(float) * wt.phi2inv.size()));
+    SKS_CUDA(cudaMemcpy(e.phi2inv, wt.phi2inv.data(), sizeof(float) * wt.phi2inv.size(), cudaMemcpyHostToDevice));
+    it = g_plans.emplace(key, e).first;
   }
-  sks::KernelModel km{k.kind, k.matern_p, k.scale, d};
-  std::string err;
-  if (!sks::build_fourier_plan(km, o.eps, o.w, o.os, nbat, xmn.data(), xmx.data(), amn.data(), amx.data(), *plan, &err))
-    return fail(err.rfind("non-finite", 0) == 0 ? SKS_ERR_NONFINITE : SKS_ERR_UNSUPPORTED, err);
-  const int n = plan->n;
-  sks::FPar* hfp = reinterpret_cast<sks::FPar*>(hflag + 4);
-  int kband = 0;
-  for (int p = 0; p < nbat; ++p) {
-    const sks::SlicePlan& sp = plan->slices[p];
-    hfp[p] = sks::FPar{sp.tau, sp.cen, sp.lmin, (sp.klo << 16) | sp.khi, sp.lminA, 0};
-    kband = std::max(kband, sp.khi - sp.klo + 1);
-  }
-  // engine (R6): the NFFT by default; the NDFT on the kept band (the paper's Gaussian engine) on request, for
-  // Gaussian / Matern bands of at most 32 coefficients.  Measured on B200, BJ cfg3 (band of 9): NDFT spread /
-  // eval 389 / 398 us vs NFFT spread / eval 250 / 231 us, so auto keeps the NFFT.
-  const bool smooth = k.kind == SKS_GAUSSIAN || k.kind == SKS_MATERN;
-  int kw = sks::ndft_width(kband);
-  if (o.engine == 2 && (!smooth || kw == 0))
-    return fail(SKS_ERR_UNSUPPORTED, "NDFT engine: Gaussian / Matern with at most 32 kept coefficients only");
-  if (o.engine != 2) kw = 0;
-  *ndft_kw = kw;
-  float* hphi = reinterpret_cast<float*>(hfp + nbat);
-  for (int kk = 0; kk <= n / 2; ++kk) hphi[kk] = kw ? 1.0f : plan->phi2inv[kk];   // NDFT: no window to undo
-  SKS_CUDA(cudaMemcpyAsync(ws + L.fpar, hfp, sizeof(sks::FPar) * nbat, cudaMemcpyHostToDevice, st));
-  SKS_CUDA(cudaMemcpyAsync(ws + L.phi, hphi, sizeof(float) * (n / 2 + 1), cudaMemcpyHostToDevice, st));
-  const sks::FPar* dfp = reinterpret_cast<const sks::FPar*>(ws + L.fpar);
-  {
-    ProfScope ps(PS_PLAN, st);
-    SKS_CUDA(sks::launch_plan_D(dfp, nbat, coeff_const(k, d), reinterpret_cast<const float*>(ws + L.phi), n,
-                                reinterpret_cast<float*>(ws + L.D), st));
-  }
-  if (kw) {
-    {
-      ProfScope ps(PS_AUX, st);
-      SKS_CUDA(sks::launch_zero(ws + L.what, al(sizeof(double) * 2 * 32 * static_cast<size_t>(nbat)), st));
-    }
-    {
-      ProfScope ps(PS_NDFT_SPREAD, st);
-      SKS_CUDA(sks::launch_ndft_spread(zv, w, nbat, dfp, kw, reinterpret_cast<double*>(ws + L.what), st));
-    }
-    *launches += 3;
-    return SKS_OK;
-  }
-  {
-    ProfScope ps(PS_AUX, st);
-    SKS_CUDA(sks::launch_zero(ws + L.grid, al(sizeof(float) * static_cast<size_t>(n) * nbat), st));
-  }
-  {
-    ProfScope ps(PS_SPREAD, st);
-    SKS_CUDA(sks::launch_spread(zv, w, nbat, dfp, n, poly_win(*plan), plan->W, reinterpret_cast<float*>(ws + L.grid), st));
-  }
-  {
-    ProfScope ps(PS_FFT, st);
-    SKS_CUDA(sks::launch_fft_filter(reinterpret_cast<const float*>(ws + L.grid), reinterpret_cast<const float*>(ws + L.D),
-                                    nbat, n, reinterpret_cast<float*>(ws + L.h), dfp, poly_win(*plan), plan->WA,
-                                    plan->WA <= kQmax ? reinterpret_cast<float*>(ws + L.Q) : nullptr, st));
-  }
-  *launches += 4;
+  *out = it->second;
+  out->pc.ndft = ndft ? 1 : 0;
   return SKS_OK;
 }
+
+// ---- pinned host staging for the status readback (per thread)
+struct Staging {
+  void* p = nullptr;
+  ~Staging() {
+    if (p) cudaFreeHost(p);
+  }
+};
+thread_local Staging g_stage;
 
 sks_status validate_common(int64_t N, int64_t M, int32_t d, const sks_kernel& k, int32_t P, int32_t p0, int32_t p1) {
   if (N <= 0 || M <= 0 || d <= 0) return fail(SKS_ERR_INVALID, "N, M and d must be > 0");
@@ -472,7 +420,9 @@ sks_status validate_common(int64_t N, int64_t M, int32_t d, const sks_kernel& k,
   return check_kernel(k);
 }
 
-// the batched pipeline shared by sks_sum and sks_sum_1d
+// the batched pipeline shared by sks_sum and sks_sum_1d: enqueues every kernel of the call on `st` with no host
+// synchronisation (the device planner takes the projection ranges straight from the epilogue); the status words
+// at the start of the workspace are read back by finish_call / sks_sync_status
 struct Problem {
   int64_t N, M;
   int d;
@@ -481,28 +431,39 @@ struct Problem {
   bool with_Z;
 };
 
-sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const float* y, const float* w,
-                       const DirEntry* dirs, const float* zx_in, const float* zy_in, float* s_out, float* t_out,
-                       double inv_P, void* workspace, size_t ws_bytes, cudaStream_t st, bool allow_f16 = true) {
+sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const float* y, const float* w,
+                        const DirEntry* dirs, const float* zx_in, const float* zy_in, float* s_out, float* t_out,
+                        double inv_P, void* workspace, size_t ws_bytes, cudaStream_t st, sks_plan_info* info_out) {
   const Path pt = path_of(pr.k.kind);
-  const int batch = choose_batch(pr.N, pr.M, pt, pr.nslices, pr.with_Z, o.batch, pr.d, o.proj);
-  const Layout L = make_layout(pr.N, pr.M, pt, batch, pr.with_Z, pr.d, o.proj);
+  const bool fshape = fused_shape(pr.N, pr.d, pt, pr.with_Z, o.w) && o.engine != 2;
+  const int batch = choose_batch(pr.N, pr.M, pt, pr.nslices, pr.with_Z, o.batch, pr.d, o.proj, fshape);
+  const Layout L = make_layout(pr.N, pr.M, pt, batch, pr.with_Z, pr.d, o.proj, fshape);
   if (!workspace || ws_bytes < L.total)
     return fail(SKS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(SKS_ERR_INVALID, "workspace must be 256-byte aligned");
   char* ws = static_cast<char*>(workspace);
   const double cdd = sks::cd(pr.d);
+  const bool ndft = pt.fourier && o.engine == 2 && (pr.k.kind == SKS_GAUSSIAN || pr.k.kind == SKS_MATERN);
+  if (o.engine == 2 && !ndft)
+    return fail(SKS_ERR_UNSUPPORTED, "NDFT engine: Gaussian / Matern with at most 32 kept coefficients only");
+  PlanEntry plan;
+  if (pt.fourier) {
+    sks_status s = get_plan(pr.k, pr.d, o, ndft, &plan);
+    if (s != SKS_OK) return s;
+  }
+  unsigned* flag16 = reinterpret_cast<unsigned*>(ws + L.status);
+  unsigned* summary = flag16 + 4;
   int launches = 0, nbatches = 0;
-  sks::FourierPlan plan;
-  sks_plan_info info{};
-  info.tau_min = 1e300;
   {   // flag words, fp64 target sums and the first batch's ranges in one launch
     ProfScope ps(PS_AUX, st);
-    SKS_CUDA(sks::launch_prologue(ws + L.flag, s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr, pr.M,
+    SKS_CUDA(sks::launch_prologue(flag16, s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr, pr.M,
                                   reinterpret_cast<unsigned*>(ws + L.mm), std::min(batch, pr.nslices), st));
   }
   launches += 1;
-  const ProjMode pm = pr.with_Z ? proj_mode_call(pr.d, o.proj, x, pr.N, y, pr.M, allow_f16) : PM_AUTO;
+  const ProjMode pm = pr.with_Z ? proj_mode_call(pr.d, o.proj, x, pr.N, y, pr.M) : PM_AUTO;
+  // fused path: the shape qualifies, the points are TMA-readable, and the projection is TF32x2 (the variant the
+  // fused kernel computes; d <= 128)
+  const bool fused = fshape && pm == PM_TF32X2 && sks::fused_spread_ok(pr.d, x) && sks::proj_tf32_tma_ok(y, pr.M, y, 0, pr.d);
   const bool tc = pr.with_Z && pm == PM_BF16X3;
   const bool tf = pr.with_Z && pm == PM_TF32X2;
   const bool th = pr.with_Z && pm == PM_FP16X2;
@@ -515,42 +476,58 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     const int nbat = std::min(batch, pr.nslices - b0);
     ++nbatches;
     unsigned* mm = reinterpret_cast<unsigned*>(ws + L.mm);
-    int* flag = reinterpret_cast<int*>(ws + L.flag);
+    int* flag = reinterpret_cast<int*>(flag16);
     if (b0 > 0) {   // (the first batch's ranges are initialised by the prologue)
       ProfScope ps(PS_AUX, st);
       SKS_CUDA(sks::launch_init_minmax(mm, nbat, st));
+      ++launches;
     }
     sks::ZView zv;
-    if (pr.with_Z) {
+    if (fused) {   // the targets' projections (and their exact ranges) only; the sources are projected below
+      float* Z = reinterpret_cast<float*>(ws + L.Z);
+      const int64_t ldz = zld(0, pr.M);
+      ProfScope ps(PS_PROJECT, st);
+      SKS_CUDA(sks::launch_project_tf32(y, pr.M, y, 0, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, nbat,
+                                        dirs->inv + b0, Z, ldz, mm, flag, nullptr, st));
+      launches += (nbat + 1023) / 1024;
+      zv = sks::ZView{nullptr, Z, 0, ldz, pr.N, pr.M};
+    } else if (pr.with_Z) {
       float* Z = reinterpret_cast<float*>(ws + L.Z);
       const int64_t ldz = zld(pr.N, pr.M);
       ProfScope ps(PS_PROJECT, st);
-      if (tc)
+      const int chunks = (nbat + 1023) / 1024;
+      if (tc) {
         SKS_CUDA(sks::launch_project_tc(ws + L.xs3, pr.N + pr.M, pr.N, pr.d,
                                         static_cast<const uint16_t*>(dirs->g3) + static_cast<int64_t>(b0) * dirs->K3,
                                         nbat, dirs->inv + b0, Z, ldz, mm, flag, ws + L.part, st));
-      else if (tf)
+        launches += chunks;
+      } else if (tf) {
         SKS_CUDA(sks::launch_project_tf32(x, pr.N, y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32,
-                                          nbat, dirs->inv + b0, Z, ldz, mm, flag, st));
-      else if (th)
+                                          nbat, dirs->inv + b0, Z, ldz, mm, flag, nullptr, st));
+        launches += chunks;
+      } else {   // FP16x2, then -- only if a point fell outside the fp16 range (flag) -- the same batch on TF32x2
         SKS_CUDA(sks::launch_project_f16(x, pr.N, y, pr.M, pr.d,
                                          static_cast<const uint16_t*>(dirs->g16) + static_cast<int64_t>(b0) * dirs->K3,
-                                         nbat, dirs->inv + b0, Z, ldz, mm, flag,
-                                         reinterpret_cast<unsigned*>(flag) + 1, st));
+                                         nbat, dirs->inv + b0, Z, ldz, mm, flag, flag16 + 1, st));
+        SKS_CUDA(sks::launch_rerun_prep(flag16, mm, nbat, st));
+        SKS_CUDA(sks::launch_project_tf32(x, pr.N, y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32,
+                                          nbat, dirs->inv + b0, Z, ldz, mm, flag, flag16 + 3, st));
+        launches += 2 + 2 * chunks;
+      }
       zv = sks::ZView{Z, Z + pr.N, ldz, ldz, pr.N, pr.M};
     } else {
       zv = sks::ZView{zx_in + static_cast<int64_t>(b0) * pr.N, zy_in + static_cast<int64_t>(b0) * pr.M, pr.N, pr.M,
                       pr.N, pr.M};
       ProfScope ps(PS_MINMAX, st);
       SKS_CUDA(sks::launch_minmax(zv, nbat, mm, flag, st));
+      ++launches;
     }
-    launches += (b0 > 0) + (pr.with_Z ? (th ? 1 : 0) + (nbat + 1023) / 1024 : 1);   // init_minmax + projection / minmax
-    int ndft_kw = 0;
+    double* s64 = s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr;
+    float* tps = t_out ? t_out + static_cast<int64_t>(b0) * pr.M : nullptr;
     sks::EvalArgs ea{};
     ea.zv = zv;
     ea.np = nbat;
-    double* s64 = s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr;
-    float* tps = t_out ? t_out + static_cast<int64_t>(b0) * pr.M : nullptr;
+    ea.flag16 = flag16;
     if (pt.sort) {
       // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)
       sks::SortPartArgs sa{};
@@ -570,24 +547,60 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
       ea.tot = sa.tot;
     }
     if (pt.fourier) {
-      sks_status s = fourier_batch(pr.k, pr.d, o, zv, w, nbat, ws, L, st, &plan, &launches, &ndft_kw, th);
-      if (s != SKS_OK) return s;
-      info.engine = ndft_kw ? 2 : 1;
-      info.band_width = 0;
-      for (const auto& sp : plan.slices) info.band_width = std::max(info.band_width, sp.khi - sp.klo + 1);
+      sks::FPar* fp = reinterpret_cast<sks::FPar*>(ws + L.fpar);
+      float* grid = reinterpret_cast<float*>(ws + L.grid);
+      if (fused) {   // the sources' range bound in place of their exact ranges (fused.cu)
+        ProfScope ps(PS_MINMAX, st);
+        double* mu = reinterpret_cast<double*>(ws + L.bound);
+        SKS_CUDA(sks::launch_source_bound(x, pr.N, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
+                                          dirs->inv + b0, nbat, mu,
+                                          reinterpret_cast<unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 16),
+                                          mm, flag16, st));
+        launches += 3;
+      }
+      {
+        ProfScope ps(PS_PLAN, st);
+        SKS_CUDA(sks::launch_plan(mm, nbat, plan.pc, plan.phi2inv, fp, reinterpret_cast<float*>(ws + L.D), grid, flag16,
+                                  summary, st));
+        launches += 1;
+      }
+      if (ndft) {
+        double* what = reinterpret_cast<double*>(ws + L.what);
+        {
+          ProfScope ps(PS_AUX, st);
+          SKS_CUDA(sks::launch_zero(what, al(sizeof(double) * 2 * sks::kNdftWidth * static_cast<size_t>(nbat)), st));
+        }
+        {
+          ProfScope ps(PS_NDFT_SPREAD, st);
+          SKS_CUDA(sks::launch_ndft_spread(zv, w, nbat, fp, what, flag16, st));
+        }
+        {
+          ProfScope ps(PS_NDFT_EVAL, st);
+          SKS_CUDA(sks::launch_ndft_eval(zv, nbat, fp, reinterpret_cast<const float*>(ws + L.D), kNcap / 2 + 1, what,
+                                         s64, tps, pt.sort, flag16, st));
+        }
+        launches += 3;
+        continue;
+      }
+      if (fused) {
+        ProfScope ps(PS_SPREAD, st);
+        SKS_CUDA(sks::launch_proj_spread(x, pr.N, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
+                                         dirs->inv + b0, nbat, w, fp, plan.pw, kNcap, grid, flag16, st));
+      } else {
+        ProfScope ps(PS_SPREAD, st);
+        SKS_CUDA(sks::launch_spread(zv, w, nbat, fp, kNcap, plan.pw, pr.k.kind == SKS_LAPLACIAN, grid, flag16, st));
+      }
+      {
+        ProfScope ps(PS_FFT, st);
+        SKS_CUDA(sks::launch_fft_filter(grid, reinterpret_cast<const float*>(ws + L.D), nbat, kNcap, fp, plan.pw,
+                                        reinterpret_cast<float*>(ws + L.Q), flag16, st));
+      }
+      launches += 2;
       ea.fourier = true;
-      ea.fp = reinterpret_cast<const sks::FPar*>(ws + L.fpar);
-      ea.h = reinterpret_cast<const float*>(ws + L.h);
-      ea.n = plan.n;
-      ea.pw = poly_win(plan);
-      ea.WA = plan.WA;
-      ea.Q = plan.WA <= kQmax ? reinterpret_cast<const float*>(ws + L.Q) : nullptr;
-      info.n_grid = plan.n;
-      info.k_max = std::max(info.k_max, plan.k_max);
-      info.band_lo_min = plan.band_lo_min;
-      info.spread_cells = std::max(info.spread_cells, plan.W);
-      info.tau_min = std::min(info.tau_min, plan.tau_min);
-      info.tau_max = std::max(info.tau_max, plan.tau_max);
+      ea.fp = fp;
+      ea.Q = reinterpret_cast<const float*>(ws + L.Q);
+      ea.ncap = kNcap;
+      ea.w = o.w;
     }
     if (pt.moment) {
       ea.moment = true;
@@ -596,13 +609,7 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     ea.s64 = s64;
     ea.per_slice_out = tps;
     ea.accumulate_out = pt.sort;
-    if (ndft_kw) {   // Gaussian / Matern on the NDFT engine (no moment term)
-      ProfScope ps(PS_NDFT_EVAL, st);
-      SKS_CUDA(sks::launch_ndft_eval(zv, nbat, reinterpret_cast<const sks::FPar*>(ws + L.fpar),
-                                     reinterpret_cast<const float*>(ws + L.D), plan.n / 2 + 1, ndft_kw,
-                                     reinterpret_cast<const double*>(ws + L.what), s64, tps, pt.sort, st));
-      ++launches;
-    } else if (pt.fourier || pt.moment) {
+    if (pt.fourier || pt.moment) {
       ProfScope ps(PS_EVAL, st);
       SKS_CUDA(sks::launch_eval(ea, st));
       ++launches;
@@ -613,34 +620,73 @@ sks_status run_batches(const Problem& pr, const Opts& o, const float* x, const f
     SKS_CUDA(sks::launch_finalize(reinterpret_cast<const double*>(ws + L.s64), pr.M, inv_P, s_out, st));
     ++launches;
   }
-  // fail loudly on non-finite projections (one readback at the end of the call)
-  {
-    void* hb = nullptr;
-    sks_status s = stage(16, &hb);
-    if (s != SKS_OK) return s;
-    SKS_CUDA(cudaMemcpyAsync(hb, ws + L.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-    SKS_CUDA(cudaStreamSynchronize(st));
-    if (*static_cast<int*>(hb) && th) return kRetryTF32;   // FP16x2 range exceeded, or NaN / Inf input
-    if (*static_cast<int*>(hb)) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
-  }
+  sks_plan_info info{};
   info.path = pt.fourier ? (pt.sort ? 2 : 0) : 1;
-  if (!pt.fourier) info.engine = 0;
+  info.engine = pt.fourier ? (ndft ? 2 : 1) : 0;
   info.window_w = pt.fourier ? o.w : 0;
   info.n_buckets = (pt.sort || pt.moment) ? sks::sortpart_dims(pr.N, pr.M).NH : 0;
   info.slice_batch = batch;
   info.n_batches = nbatches;
   info.launches = launches;
   info.proj_mode = !pr.with_Z ? 0 : tc ? 2 : tf ? 3 : 4;
-  if (!pt.fourier) info.tau_min = 0;
-  g_plan = info;
+  info.fused = fused ? 1 : 0;
+  *info_out = info;
   return SKS_OK;
+}
+
+// read the call's status words (one 48-byte readback and a stream synchronisation) into a status and the plan
+// summary; `info` holds the host-side fields of the call
+sks_status read_status(const void* workspace, cudaStream_t st, sks_plan_info* info) {
+  if (!g_stage.p) SKS_CUDA(cudaHostAlloc(&g_stage.p, kStatusBytes, cudaHostAllocDefault));
+  unsigned* h = static_cast<unsigned*>(g_stage.p);
+  SKS_CUDA(cudaMemcpyAsync(h, workspace, 48, cudaMemcpyDeviceToHost, st));
+  SKS_CUDA(cudaStreamSynchronize(st));
+  if (info && info->path != 1) {   // Fourier plan summary (plan.cu)
+    const unsigned* sm = h + 4;
+    float tmn, tmx;
+    std::memcpy(&tmn, sm + 5, 4);
+    std::memcpy(&tmx, sm + 6, 4);
+    info->n_grid = static_cast<int>(sm[0]);
+    info->k_max = static_cast<int>(sm[1]);
+    info->band_lo_min = static_cast<int>(sm[2]);
+    info->spread_cells = static_cast<int>(sm[3]);
+    info->band_width = static_cast<int>(sm[4]);
+    info->tau_min = tmn;
+    info->tau_max = tmx;
+  }
+  if (info && h[3]) info->proj_mode = 3;   // FP16x2 range exceeded: the projection ran on TF32x2
+  if (h[0]) return fail(SKS_ERR_NONFINITE, "non-finite projection (NaN/Inf in x, y or an overflow)");
+  if (h[2] & 1u)
+    return fail(SKS_ERR_UNSUPPORTED, "NFFT grid beyond the built limit n = " + std::to_string(kNcap) +
+                                         " (the kernel's spectrum is too wide for the data's range)");
+  if (h[2] & 2u) return fail(SKS_ERR_UNSUPPORTED, "NDFT engine: Gaussian / Matern with at most 32 kept coefficients only");
+  return SKS_OK;
+}
+
+// ---- CUDA-graph replay of whole calls (sks_options.graph): keyed by every argument of the call
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  sks_plan_info info{};
+};
+std::mutex g_graph_mu;
+std::map<std::string, GraphEntry> g_graphs;
+
+std::string graph_key(int dev, const void* a, const void* b, const void* c, const void* dd, const void* ws, size_t wsb,
+                      int64_t N, int64_t M, int d, const sks_kernel& k, int P, uint64_t seed, int p0, int p1,
+                      const Opts& o, cudaStream_t st) {
+  char buf[512];
+  std::snprintf(buf, sizeof(buf), "%d|%p|%p|%p|%p|%p|%zu|%lld|%lld|%d|%d|%d|%.17g|%d|%llu|%d|%d|%.17g|%d|%d|%d|%d|%d|%p",
+                dev, a, b, c, dd, ws, wsb, static_cast<long long>(N), static_cast<long long>(M), d, k.kind, k.matern_p,
+                k.scale, P, static_cast<unsigned long long>(seed), p0, p1, o.eps, o.w, o.os, o.batch, o.engine, o.proj,
+                static_cast<void*>(st));
+  return buf;
 }
 
 }  // namespace
 
 extern "C" {
 
-const char* sks_version(void) { return "sks 0.1 (sm_100a)"; }
+const char* sks_version(void) { return "sks 0.2 (sm_100a)"; }
 
 const char* sks_last_error(void) { return g_err.c_str(); }
 
@@ -675,7 +721,7 @@ sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots) {
 }
 
 const char* sks_profile_names(void) {
-  return "split3,project,minmax,sp_hist,sp_part,sp_owner,sp_gather,sortsum_v1,plan_D,spread,fft_filter,eval,aux,"
+  return "split3,project,minmax,sp_hist,sp_part,sp_owner,sp_gather,reserved,plan,spread,fft_filter,eval,aux,"
          "ndft_spread,ndft_eval,sortsum";
 }
 
@@ -683,6 +729,11 @@ sks_status sks_last_plan(sks_plan_info* info) {
   if (!info) return fail(SKS_ERR_INVALID, "info is NULL");
   *info = g_plan;
   return SKS_OK;
+}
+
+sks_status sks_sync_status(void* workspace, void* stream) {
+  if (!workspace) return fail(SKS_ERR_INVALID, "workspace is NULL");
+  return read_status(workspace, static_cast<cudaStream_t>(stream), &g_plan);
 }
 
 sks_status sks_directions(int32_t P, int32_t d, uint64_t seed, int32_t p_begin, int32_t p_end, float* g_out,
@@ -711,8 +762,9 @@ sks_status sks_workspace_size(int64_t N, int64_t M, int32_t d, sks_kernel kernel
   if ((s = resolve_opts(opt, &o)) != SKS_OK) return s;
   if (!bytes) return fail(SKS_ERR_INVALID, "bytes is NULL");
   const Path pt = path_of(kernel.kind);
-  const int batch = choose_batch(N, M, pt, p_end - p_begin, true, o.batch, d, o.proj);
-  *bytes = make_layout(N, M, pt, batch, true, d, o.proj).total;
+  const bool fshape = fused_shape(N, d, pt, true, o.w) && o.engine != 2;
+  const int batch = choose_batch(N, M, pt, p_end - p_begin, true, o.batch, d, o.proj, fshape);
+  *bytes = make_layout(N, M, pt, batch, true, d, o.proj, fshape).total;
   return SKS_OK;
 }
 
@@ -726,13 +778,55 @@ sks_status sks_sum(const float* x, int64_t N, const float* y, int64_t M, int32_t
   if ((st = resolve_opts(opt, &o)) != SKS_OK) return st;
   DirEntry dirs;
   if ((st = get_dirs(P, d, seed, p_begin, p_end, &dirs)) != SKS_OK) return st;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
   Problem pr{N, M, d, kernel, p_end - p_begin, true};
-  st = run_batches(pr, o, x, y, w, &dirs, nullptr, nullptr, s, nullptr, 1.0 / P, workspace, workspace_bytes,
-                   static_cast<cudaStream_t>(stream));
-  if (st == kRetryTF32)   // a point outside the FP16x2 range: the same call on TF32x2
-    st = run_batches(pr, o, x, y, w, &dirs, nullptr, nullptr, s, nullptr, 1.0 / P, workspace, workspace_bytes,
-                     static_cast<cudaStream_t>(stream), false);
-  return st;
+  if (o.graph) {
+    int dev = 0;
+    SKS_CUDA(cudaGetDevice(&dev));
+    const std::string key = graph_key(dev, x, y, w, s, workspace, workspace_bytes, N, M, d, kernel, P, seed, p_begin,
+                                      p_end, o, cs);
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    auto it = g_graphs.find(key);
+    if (it == g_graphs.end()) {
+      // first call with these arguments: run it eagerly (fills every cache and sets the kernels' attributes, so
+      // the capture contains launches only), then capture the same launch sequence into a graph
+      sks_plan_info info{};
+      st = enqueue_call(pr, o, x, y, w, &dirs, nullptr, nullptr, s, nullptr, 1.0 / P, workspace, workspace_bytes, cs,
+                        &info);
+      if (st != SKS_OK) return st;
+      g_plan = info;
+      // capture on a private stream (the legacy default stream cannot be captured); replays go to `cs`
+      cudaStream_t cap = nullptr;
+      SKS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      cudaGraph_t graph = nullptr;
+      SKS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      sks_plan_info info2{};
+      const sks_status cst = enqueue_call(pr, o, x, y, w, &dirs, nullptr, nullptr, s, nullptr, 1.0 / P, workspace,
+                                          workspace_bytes, cap, &info2);
+      const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+      cudaStreamDestroy(cap);
+      if (cst != SKS_OK) return cst;
+      if (ce != cudaSuccess) return fail(SKS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+      GraphEntry ge;
+      ge.info = info2;
+      SKS_CUDA(cudaGraphInstantiate(&ge.exec, graph, 0));
+      cudaGraphDestroy(graph);
+      if (g_graphs.size() >= 64) {   // bounded: drop the whole cache (graphs are cheap to rebuild)
+        for (auto& kv : g_graphs) cudaGraphExecDestroy(kv.second.exec);
+        g_graphs.clear();
+      }
+      g_graphs.emplace(key, ge);
+      return SKS_OK;
+    }
+    g_plan = it->second.info;
+    SKS_CUDA(cudaGraphLaunch(it->second.exec, cs));
+    return SKS_OK;
+  }
+  sks_plan_info info{};
+  st = enqueue_call(pr, o, x, y, w, &dirs, nullptr, nullptr, s, nullptr, 1.0 / P, workspace, workspace_bytes, cs, &info);
+  g_plan = info;
+  if (st != SKS_OK || o.async) return st;
+  return read_status(workspace, cs, &g_plan);
 }
 
 sks_status sks_workspace_size_host(int64_t N, int64_t M, int32_t d, sks_kernel kernel, int32_t P, int32_t p_begin,
@@ -753,21 +847,25 @@ sks_status sks_sum_host(const float* x, int64_t N, const float* y, int64_t M, in
   if (!workspace || workspace_bytes < need) return fail(SKS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(SKS_ERR_INVALID, "workspace must be 256-byte aligned");
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  // the compute workspace first (its status words at offset 0), then the device copies of x, y, w, s
+  size_t inner = 0;
+  if ((st = sks_workspace_size(N, M, d, kernel, P, p_begin, p_end, opt, &inner)) != SKS_OK) return st;
   char* ws = static_cast<char*>(workspace);
-  float* dx = reinterpret_cast<float*>(ws);
-  float* dy = reinterpret_cast<float*>(ws + al(sizeof(float) * N * d));
+  float* dx = reinterpret_cast<float*>(ws + al(inner));
+  float* dy = reinterpret_cast<float*>(reinterpret_cast<char*>(dx) + al(sizeof(float) * N * d));
   float* dw = reinterpret_cast<float*>(reinterpret_cast<char*>(dy) + al(sizeof(float) * M * d));
   float* ds = reinterpret_cast<float*>(reinterpret_cast<char*>(dw) + al(sizeof(float) * N));
-  char* rest = reinterpret_cast<char*>(ds) + al(sizeof(float) * M);
-  const size_t used = static_cast<size_t>(rest - ws);
   SKS_CUDA(cudaMemcpyAsync(dx, x, sizeof(float) * N * d, cudaMemcpyHostToDevice, cs));
   SKS_CUDA(cudaMemcpyAsync(dy, y, sizeof(float) * M * d, cudaMemcpyHostToDevice, cs));
   SKS_CUDA(cudaMemcpyAsync(dw, w, sizeof(float) * N, cudaMemcpyHostToDevice, cs));
-  st = sks_sum(dx, N, dy, M, d, dw, kernel, P, seed, p_begin, p_end, ds, rest, workspace_bytes - used, opt, stream);
+  sks_options o{};
+  if (opt) o = *opt;
+  o.async = 1;   // one synchronisation below covers the result copy and the status
+  o.graph = 0;
+  st = sks_sum(dx, N, dy, M, d, dw, kernel, P, seed, p_begin, p_end, ds, ws, inner, &o, stream);
   if (st != SKS_OK) return st;
   SKS_CUDA(cudaMemcpyAsync(s, ds, sizeof(float) * M, cudaMemcpyDeviceToHost, cs));
-  SKS_CUDA(cudaStreamSynchronize(cs));
-  return SKS_OK;
+  return read_status(ws, cs, &g_plan);
 }
 
 sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64_t seed, int32_t p_begin,
@@ -786,7 +884,7 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
   // first use, grown on demand; this entry point is a test/inspection aid, not the hot path)
   static thread_local unsigned* scratch = nullptr;
   static thread_local size_t scratch_bytes = 0;
-  const ProjMode pm = proj_mode_call(d, o.proj, pts, n, pts, 0, true);
+  const ProjMode pm = proj_mode_call(d, o.proj, pts, n, pts, 0);
   const bool tc = pm == PM_BF16X3;
   const size_t need = al(sizeof(unsigned) * 4 * np + 16) +
                       (tc ? al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n) + al(sks::proj_tc_part_bytes(np)) : 0);
@@ -805,11 +903,13 @@ sks_status sks_project(const float* pts, int64_t n, int32_t d, int32_t P, uint64
     char* part = xs3 + al(sizeof(uint16_t) * 3 * sks::proj_tc_dpad(d) * n);
     SKS_CUDA(sks::launch_split3(pts, n, pts, 0, d, xs3, cs));
     SKS_CUDA(sks::launch_project_tc(xs3, n, n, d, dirs.g3, np, dirs.inv, z, n, mm, flag, part, cs));
-  } else if (pm == PM_FP16X2) {
-    SKS_CUDA(sks::launch_project_f16(pts, n, pts, 0, d, dirs.g16, np, dirs.inv, z, n, mm, flag,
-                                     reinterpret_cast<unsigned*>(flag) + 1, cs));
+  } else if (pm == PM_FP16X2) {   // (+ the TF32x2 rerun, predicated on a point outside the fp16 range)
+    unsigned* f16 = reinterpret_cast<unsigned*>(flag);
+    SKS_CUDA(sks::launch_project_f16(pts, n, pts, 0, d, dirs.g16, np, dirs.inv, z, n, mm, flag, f16 + 1, cs));
+    SKS_CUDA(sks::launch_rerun_prep(f16, mm, np, cs));
+    SKS_CUDA(sks::launch_project_tf32(pts, n, pts, 0, d, dirs.g32, np, dirs.inv, z, n, mm, flag, f16 + 3, cs));
   } else {
-    SKS_CUDA(sks::launch_project_tf32(pts, n, pts, 0, d, dirs.g32, np, dirs.inv, z, n, mm, flag, cs));
+    SKS_CUDA(sks::launch_project_tf32(pts, n, pts, 0, d, dirs.g32, np, dirs.inv, z, n, mm, flag, nullptr, cs));
   }
   return SKS_OK;
 }
@@ -822,8 +922,8 @@ sks_status sks_workspace_size_1d(int64_t N, int64_t M, int32_t d, sks_kernel ker
   if ((s = resolve_opts(opt, &o)) != SKS_OK) return s;
   if (!bytes) return fail(SKS_ERR_INVALID, "bytes is NULL");
   const Path pt = path_of(kernel.kind);
-  const int batch = choose_batch(N, M, pt, n_slices, false, o.batch, d, o.proj);
-  *bytes = make_layout(N, M, pt, batch, false, d, o.proj).total;
+  const int batch = choose_batch(N, M, pt, n_slices, false, o.batch, d, o.proj, false);
+  *bytes = make_layout(N, M, pt, batch, false, d, o.proj, false).total;
   return SKS_OK;
 }
 
@@ -836,8 +936,12 @@ sks_status sks_sum_1d(const float* zx, const float* zy, const float* w, int64_t 
   Opts o;
   if ((st = resolve_opts(opt, &o)) != SKS_OK) return st;
   Problem pr{N, M, d, kernel, n_slices, false};
-  return run_batches(pr, o, nullptr, nullptr, w, nullptr, zx, zy, nullptr, t, 1.0, workspace, workspace_bytes,
-                     static_cast<cudaStream_t>(stream));
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  sks_plan_info info{};
+  st = enqueue_call(pr, o, nullptr, nullptr, w, nullptr, zx, zy, nullptr, t, 1.0, workspace, workspace_bytes, cs, &info);
+  g_plan = info;
+  if (st != SKS_OK || o.async) return st;
+  return read_status(workspace, cs, &g_plan);
 }
 
 }  // extern "C"

@@ -1,0 +1,464 @@
+// fused.cu -- rows a1 + a5 fused for the Fourier kernels at large N (the memory remark
+// P:973-979): the projections of the SOURCES are spread into the slices' NFFT grids straight from the tensor-core
+// accumulators, so they never reach HBM (cfg5 on one GPU: 20 GB of projection stores and as many loads saved).
+//
+//   k_sample_mean   mu = mean of a strided sample of the sources (fp64; any mu is valid, a central one is tight)
+//   k_norm_bound    rho = max_n ||x_n - mu||, nmax = max_n ||x_n|| over all sources (one pass over X)
+//   k_bound_ranges  per slice p: c_p = <xi_p, mu>; every source projection lies in [c_p - rho', c_p + rho']
+//                   (Cauchy-Schwarz, ||xi_p|| = 1; rho' adds the projection's fp32 error bound), combined with
+//                   the targets' exact ranges from their projection epilogue into the planner's ranges (R3: the
+//                   torus must hold every point; a range bound instead of the exact x range only widens 1/tau)
+//   k_proj_spread   persistent, one CTA per (slice tile of 128, range of 128-point source tiles):
+//                   A = the tile's directions (resident in shared memory), B = the point tile (TMA, the raw fp32
+//                   tile is the tf32 hi piece, converter warps form lo = rn_tf32(x - hi): TF32x2, reading R2),
+//                   tcgen05.mma M = 128 slices x N = 128 points into double-buffered TMEM; epilogue warps own one
+//                   slice each (TMEM lane = slice) and spread w_n phi(v - l) into the slice's private grid column
+//                   in shared memory ([half][cell][slice]: conflict-free read-modify-writes, no atomics), flushed
+//                   once per CTA with global atomics
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "kernels.h"
+#include "tc_util.h"
+
+namespace sks {
+
+namespace {
+
+using namespace tc;
+
+// ------------------------------------------------------------------ range bound of the sources
+constexpr int MEAN_ROWS = 2048, MEAN_PARTS = 32;   // sampled rows k N / MEAN_ROWS, summed in MEAN_PARTS groups
+
+// part[g][j] = sum of dimension j over the sampled rows k = g, g + MEAN_PARTS, ... (fp64)
+__global__ void __launch_bounds__(128) k_sample_mean_part(const float* __restrict__ x, int64_t N, int d,
+                                                          double* __restrict__ part) {
+  const int S = static_cast<int>(N < MEAN_ROWS ? N : MEAN_ROWS);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double s = 0.0;
+    for (int k = blockIdx.x; k < S; k += MEAN_PARTS)
+      s += static_cast<double>(__ldg(x + (static_cast<int64_t>(k) * N / S) * d + j));
+    part[static_cast<int64_t>(blockIdx.x) * d + j] = s;
+  }
+}
+
+// mu[j] = (sum over the parts, in order) / S; also zeroes the norm-bound words nb[0..3]
+__global__ void k_sample_mean_fin(int64_t N, int d, const double* __restrict__ part, double* __restrict__ mu,
+                                  unsigned* __restrict__ nb) {
+  const int S = static_cast<int>(N < MEAN_ROWS ? N : MEAN_ROWS);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double s = 0.0;
+    for (int g = 0; g < MEAN_PARTS; ++g) s += part[static_cast<int64_t>(g) * d + j];
+    mu[j] = s / S;
+  }
+  if (threadIdx.x < 4) nb[threadIdx.x] = 0u;
+}
+
+// one warp per row (d <= 128: one float4 per lane), fp32 sums of squares, maxima as float bits (non-negative
+// floats order as unsigned ints); out[0] = max ||x - mu||^2, out[1] = max ||x||^2, out[2] = non-finite seen
+__global__ void __launch_bounds__(256) k_norm_bound(const float* __restrict__ x, int64_t N, int d,
+                                                    const double* __restrict__ mu, unsigned* __restrict__ out) {
+  __shared__ float smu[128];
+  for (int j = threadIdx.x; j < 128; j += blockDim.x) smu[j] = j < d ? static_cast<float>(mu[j]) : 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool on = 4 * lane < d;
+  const float4 m4 = on ? make_float4(smu[4 * lane], smu[4 * lane + 1], smu[4 * lane + 2], smu[4 * lane + 3])
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+  float r2max = 0.f, n2max = 0.f;
+  bool bad = false;
+  constexpr int U = 4;   // rows per warp and iteration, all loads in flight first
+  for (int64_t i0 = w0 * U; i0 < N; i0 += nw * U) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (on && i0 + u < N) v[u] = __ldcs(reinterpret_cast<const float4*>(x + (i0 + u) * d) + lane);   // streamed once
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float a = v[u].x - m4.x, b = v[u].y - m4.y, c = v[u].z - m4.z, e = v[u].w - m4.w;
+      float r2 = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
+      float n2 = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, v[u].w * v[u].w)));
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+      }
+      bad |= !isfinite(n2);
+      r2max = fmaxf(r2max, r2);
+      n2max = fmaxf(n2max, n2);
+    }
+  }
+  if (lane == 0) {
+    if (r2max > 0.f) atomicMax(out + 0, __float_as_uint(r2max));
+    if (n2max > 0.f) atomicMax(out + 1, __float_as_uint(n2max));
+    if (bad) atomicOr(out + 2, 1u);
+  }
+}
+
+__device__ __forceinline__ unsigned f2key_fu(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f_fu(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// one warp per slice: c_p = <g_p, mu> inv_p (fp64), rho' = rho (1 + 2^-10) + 2^-19 nmax: the fp32 sums of squares
+// (relative error <= d 2^-24 <= 2^-17 for d <= 128, halved by the root) and the projection's error (<= 2^-21 ||x||,
+// DESIGN.md R2) are far inside these margins.  mm[p] = {xmin, xmax, allmin, allmax}: x from the bound, all =
+// x bound and the targets' exact range (their projection epilogue wrote it into mm[p][2..3])
+__global__ void k_bound_ranges(const float* __restrict__ g32, int dp32, int d, const float* __restrict__ inv_norm,
+                               int np, const double* __restrict__ mu, const unsigned* __restrict__ nb,
+                               unsigned* __restrict__ mm, unsigned* __restrict__ flag16) {
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (p >= np) return;
+  double s = 0.0;
+  for (int j = lane; j < d; j += 32) s += static_cast<double>(g32[static_cast<int64_t>(p) * dp32 + j]) * mu[j];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane) return;
+  if (nb[2]) {
+    atomicOr(flag16, 1u);
+    return;
+  }
+  const double c = s * static_cast<double>(inv_norm[p]);
+  const double rho = sqrt(static_cast<double>(__uint_as_float(nb[0]))) * (1.0 + 0x1p-10) +
+                     sqrt(static_cast<double>(__uint_as_float(nb[1]))) * 0x1p-19;
+  const float lo = static_cast<float>(c - rho), hi = static_cast<float>(c + rho);
+  const float xlo = nextafterf(lo, -CUDART_INF_F), xhi = nextafterf(hi, CUDART_INF_F);
+  const float ymn = key2f_fu(mm[4 * p + 2]), ymx = key2f_fu(mm[4 * p + 3]);
+  mm[4 * p + 0] = f2key_fu(xlo);
+  mm[4 * p + 1] = f2key_fu(xhi);
+  mm[4 * p + 2] = f2key_fu(fminf(xlo, ymn));
+  mm[4 * p + 3] = f2key_fu(fmaxf(xhi, ymx));
+}
+
+// ------------------------------------------------------------------ the fused projection + spread
+constexpr int FS_S = 128;          // slices per tile (UMMA M = TMEM lanes)
+constexpr int FS_P = 128;          // points per tile (UMMA N)
+constexpr int FS_STAGES = 2;
+constexpr int FS_KBMAX = 4;        // k-blocks of 32 dims: d <= 128
+constexpr int FS_WCAP = 40;        // private grid cells per slice (wider footprints: global atomics)
+constexpr int FS_EPI = 16;         // epilogue warps: 4 per TMEM lane quadrant, 32 points of the tile each
+constexpr int FS_THREADS = 32 * (8 + FS_EPI);   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 -, w4..w7 converters, epilogue
+constexpr int FS_PIECE = FS_P * 128;                      // one k-block of 128 points: 16 KB
+constexpr int FS_A = FS_S * 128;                          // one k-block of the directions: 16 KB
+constexpr int FS_OFF_STAGE = FS_KBMAX * FS_A;             // 64 KB of resident directions
+constexpr int FS_OFF_GRID = FS_OFF_STAGE + FS_STAGES * 2 * FS_PIECE;
+constexpr int FS_OFF_BAR = FS_OFF_GRID + (FS_EPI / 4) * FS_WCAP * FS_S * 4;
+constexpr int FS_SMEM = FS_OFF_BAR + 256 + 1024;          // + barriers, TMEM slot, alignment slack
+
+template <int WT>
+__global__ void __launch_bounds__(FS_THREADS, 1)
+    k_proj_spread(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int nk, int64_t N,
+                  int np, int ranges, const float* __restrict__ inv_norm, const float* __restrict__ w,
+                  const FPar* __restrict__ fp, PolyWin pw, int ncap, float* __restrict__ grid,
+                  const unsigned* __restrict__ flag16) {
+  if (call_failed(flag16)) return;
+  extern __shared__ unsigned char fsraw[];
+  // aligned by pointer arithmetic on the __shared__ array: the compiler keeps the shared state space (LDS / STS,
+  // not generic LD / ST)
+  unsigned char* sm = fsraw + ((1024u - (smem_u32(fsraw) & 1023u)) & 1023u);
+  float* priv = reinterpret_cast<float*>(sm + FS_OFF_GRID);   // [FS_EPI / 4][FS_WCAP][FS_S]
+  uint64_t* afull = reinterpret_cast<uint64_t*>(sm + FS_OFF_BAR);
+  uint64_t* xfull = afull + 1;                 // [FS_STAGES] raw tile landed
+  uint64_t* full = xfull + FS_STAGES;          // [FS_STAGES] lo written (converters)
+  uint64_t* empty = full + FS_STAGES;          // [FS_STAGES] consumed by the MMAs
+  uint64_t* tfull = empty + FS_STAGES;         // [2]
+  uint64_t* tempty = tfull + 2;                // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int st_idx = blockIdx.x % ((np + FS_S - 1) / FS_S), r = blockIdx.x / ((np + FS_S - 1) / FS_S);
+  const int64_t ntp = (N + FS_P - 1) / FS_P;
+  const int64_t t0 = r * ntp / ranges, t1 = (r + 1) * ntp / ranges;   // this CTA's point tiles
+  const int s0 = st_idx * FS_S;
+
+  for (int e = threadIdx.x; e < (FS_EPI / 4) * FS_WCAP * FS_S; e += FS_THREADS) priv[e] = 0.f;
+  if (warp == 0 && lane == 0) {
+    mbar_init(afull, 1);
+    for (int s = 0; s < FS_STAGES; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&full[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], FS_EPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * FS_P));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer: the tile's directions once, then the raw fp32 point tiles (the hi piece)
+    mbar_expect_tx(afull, nk * FS_A);
+    for (int kb = 0; kb < nk; ++kb) tma_load_2d(&tmA, afull, sm + kb * FS_A, kb * 32, s0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = t0; t < t1; ++t)
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char* sa = sm + FS_OFF_STAGE + stage * 2 * FS_PIECE;
+        mbar_expect_tx(&xfull[stage], FS_PIECE);
+        tma_load_2d(&tmX, &xfull[stage], sa, kb * 32, static_cast<int>(t * FS_P));
+        if (++stage == FS_STAGES) { stage = 0; phase ^= 1; }
+      }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer: D[slice][point] += A (directions, tf32-exact) . B (hi, then lo)
+    constexpr uint32_t idesc = idesc_tf32(FS_S, FS_P);
+    mbar_wait(afull, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      const int b = it & 1;
+      mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(b * FS_P);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const unsigned char* sb = sm + FS_OFF_STAGE + stage * 2 * FS_PIECE;
+        const uint64_t da = umma_desc_sw128(sm + kb * FS_A);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint64_t db = umma_desc_sw128(sb + q * FS_PIECE);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {   // 4 MMAs of K = 8 tf32 (32 bytes) per 128-byte row
+            const uint32_t acc = (kb > 0 || q > 0 || k > 0) ? 1u : 0u;
+            const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[stage]))
+                     : "memory");
+        if (++stage == FS_STAGES) { stage = 0; phase ^= 1; }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&tfull[b]))
+                   : "memory");
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---- converters: lo = rn_tf32(x - trunc_tf32(x)) of every element of the raw tile (the hi operand as it
+    //      stands: kind::tf32 reads the top 19 bits).  Lane l: 16-byte chunk l % 8 of rows 4 i + l / 8
+    const int cw = warp - 4, c = lane & 7, rsub = lane >> 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = t0; t < t1; ++t)
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&xfull[stage], phase);
+        unsigned char* sa = sm + FS_OFF_STAGE + stage * 2 * FS_PIECE;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = 32 * cw + 4 * i + rsub;
+          const int off = row * 128 + ((c ^ (row & 7)) << 4);
+          const float4 v = *reinterpret_cast<const float4*>(sa + off);
+          const float4 lo = make_float4(tf32_cvt_rn(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u)),
+                                        tf32_cvt_rn(v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u)),
+                                        tf32_cvt_rn(v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u)),
+                                        tf32_cvt_rn(v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u)));
+          *reinterpret_cast<float4*>(sa + FS_PIECE + off) = lo;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == FS_STAGES) { stage = 0; phase ^= 1; }
+      }
+  } else if (warp >= 8) {
+    // ---- epilogue: warp w owns TMEM lane quadrant q = w % 4 (slices s0 + 32 q + lane) and the 32 points
+    //      h = (w - 8) / 4 of the tile; per point: the grid coordinate a = acc (tau_p n_p / ||g_p||) - (cen_p tau_p
+    //      n_p + w/2) (one FMA; the planner's footprint has a cell of margin either side and the cell index is
+    //      clamped to the private column), WT taps of the window polynomial (centred even / odd form), w_n-weighted
+    //      into the slice's private column (cell-major: bank = lane, conflict-free)
+    const int q = warp & 3, h = (warp - 8) >> 2;
+    const int p = s0 + 32 * q + lane;
+    const bool live = p < np;
+    FPar f{};
+    float inv = 0.f;
+    if (live) {
+      f = fp[p];
+      inv = inv_norm[p];
+    }
+    const int n = 1 << f.logn;
+    const float taun = f.tau * static_cast<float>(n);
+    const float ga = inv * taun, gb = -fmaf(f.cen, taun, 0.5f * pw.w);
+    const int W = f.W;
+    const bool wide = W > FS_WCAP;   // (footprint beyond the private column: global atomics for this slice)
+    float* col = priv + (h * FS_WCAP) * FS_S + 32 * q + lane;   // cell c at col[c * FS_S]
+    float* gp = grid + static_cast<int64_t>(live ? p : 0) * ncap;
+    float E[WT / 2][4], O[WT / 2][4];
+#pragma unroll
+    for (int j = 0; j < WT / 2; ++j)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        E[j][k] = pw.eo[j][k];
+        O[j][k] = pw.eo[j][4 + k];
+      }
+    const int cmax = W - WT;   // last admissible first-tap cell (relative to lmin)
+    // the weights of the warp's 32 points, one per lane, loaded one tile ahead (software pipelined: a global load's
+    // latency would otherwise stall the epilogue warps at every tile)
+    auto wload = [&](int64_t t) {
+      const int64_t i = t * FS_P + h * 32 + lane;
+      return (t < t1 && i < N) ? __ldg(w + i) : 0.f;
+    };
+    float wnext = wload(t0);
+    int it = 0;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      const int b = it & 1;
+      const int c0 = h * 32;
+      const int64_t i0 = t * FS_P + c0;
+      const float wv = wnext;
+      wnext = wload(t + 1);
+      mbar_wait(&tfull[b], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      uint32_t v[32];
+      const uint32_t taddr = tmem_base + static_cast<uint32_t>(b * FS_P + c0) + (static_cast<uint32_t>(32 * q) << 16);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+          "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // the accumulator is in registers: release it to the MMAs of tile t + 2 before spreading
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+      const int nj = (N - i0 < 32) ? static_cast<int>(N - i0) : 32;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float wi = __shfl_sync(0xffffffffu, wv, j);
+        if (j < nj && live) {
+          const float a = fmaf(__uint_as_float(v[j]), ga, gb), fl = floorf(a);
+          const float u = (a - fl) - 0.5f, u2 = u * u;
+          int cl = static_cast<int>(fl) + 1 - f.lmin;
+          cl = cl < 0 ? 0 : (cl > cmax ? cmax : cl);   // (a valid bound never clamps; memory safety only)
+          float tw[WT];
+#pragma unroll
+          for (int m = 0; m < WT / 2; ++m) {
+            const float Em = fmaf(fmaf(fmaf(E[m][3], u2, E[m][2]), u2, E[m][1]), u2, E[m][0]);
+            const float Om = fmaf(fmaf(fmaf(O[m][3], u2, O[m][2]), u2, O[m][1]), u2, O[m][0]);
+            tw[m] = fmaf(u, Om, Em);
+            tw[WT - 1 - m] = fmaf(-u, Om, Em);
+          }
+          if (!wide) {
+            float* cell = col + cl * FS_S;
+#pragma unroll
+            for (int m = 0; m < WT; ++m) cell[m * FS_S] = fmaf(wi, tw[m], cell[m * FS_S]);
+          } else {
+#pragma unroll
+            for (int m = 0; m < WT; ++m) atomicAdd(&gp[(f.lmin + cl + m) & (n - 1)], wi * tw[m]);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp >= 8 && warp < 12) {   // flush: the FS_EPI / 4 private columns of each slice, one atomic per cell
+    const int q = warp & 3, p = s0 + 32 * q + lane;
+    if (p < np) {
+      const FPar f = fp[p];
+      const int n = 1 << f.logn;
+      if (f.W <= FS_WCAP) {
+        float* gp = grid + static_cast<int64_t>(p) * ncap;
+        const float* c0 = priv + 32 * q + lane;
+        for (int c = 0; c < f.W; ++c) {
+          float s = 0.f;
+#pragma unroll
+          for (int g = 0; g < FS_EPI / 4; ++g) s += c0[(g * FS_WCAP + c) * FS_S];
+          if (s != 0.f) atomicAdd(&gp[(f.lmin + c) & (n - 1)], s);
+        }
+      }
+    }
+  }
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * FS_P));
+}
+
+bool encode_f32_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+                    uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t gdim[2] = {cols, rows};
+  const cuuint64_t gstride[1] = {row_stride_elems * 4};
+  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+size_t source_bound_bytes(int d) { return sizeof(double) * static_cast<size_t>(d) * (1 + MEAN_PARTS) + 16; }
+
+bool fused_spread_ok(int d, const float* x) {
+  return d <= 32 * FS_KBMAX && d % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+}
+
+cudaError_t launch_source_bound(const float* x, int64_t N, int d, const float* g32, int dp32, const float* inv_norm,
+                                int np, double* mu, unsigned* nb, unsigned* mm, unsigned* flag16, cudaStream_t st) {
+  double* part = mu + d;   // [MEAN_PARTS][d] scratch after mu (source_bound_bytes)
+  k_sample_mean_part<<<MEAN_PARTS, 128, 0, st>>>(x, N, d, part);
+  k_sample_mean_fin<<<1, 128, 0, st>>>(N, d, part, mu, nb);
+  int64_t blocks = (N * 32 / 4 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_norm_bound<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, N, d, mu, nb);
+  k_bound_ranges<<<(np + 7) / 8, 256, 0, st>>>(g32, dp32, d, inv_norm, np, mu, nb, mm, flag16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_proj_spread(const float* x, int64_t N, int d, const float* g32, int dp32, const float* inv_norm,
+                               int np, const float* w, const FPar* fp, const PolyWin& pw, int ncap, float* grid,
+                               const unsigned* flag16, cudaStream_t st) {
+  CUtensorMap tmA, tmX;
+  const int nk = dp32 / 32;
+  if (!encode_f32_map(&tmA, g32, static_cast<uint64_t>(np), static_cast<uint64_t>(dp32), static_cast<uint64_t>(dp32),
+                      FS_S) ||
+      !encode_f32_map(&tmX, x, static_cast<uint64_t>(N), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FS_P))
+    return cudaErrorInvalidValue;
+  const int ntiles_s = (np + FS_S - 1) / FS_S;
+  const int64_t ntp = (N + FS_P - 1) / FS_P;
+  int ranges = 148 / ntiles_s;
+  if (ranges < 1) ranges = 1;
+  if (ranges > ntp) ranges = static_cast<int>(ntp);
+  auto go = [&](auto kern) {
+    set_smem_attr_once(reinterpret_cast<const void*>(kern), FS_SMEM);
+    kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, nk, N, np, ranges, inv_norm, w, fp, pw, ncap, grid,
+                                                         flag16);
+  };
+  switch (pw.w) {
+    case 4: go(k_proj_spread<4>); break;
+    case 6: go(k_proj_spread<6>); break;
+    case 8: go(k_proj_spread<8>); break;
+    case 10: go(k_proj_spread<10>); break;
+    case 12: go(k_proj_spread<12>); break;
+    default: return cudaErrorInvalidValue;   // (odd widths: the unfused path)
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace sks

@@ -253,187 +253,31 @@ bool fit_window_poly(int w, double beta, float* coef, double* max_err) {
   return worst < 1e-4;
 }
 
-// ------------------------------------------------------------------ band selection (R5)
-static void select_band_uncached(const KernelModel& k, double tau, double eps, int kcap, int* klo, int* khi);
-
-// band per (kernel, tau, eps): cached, repeated calls on the same data re-plan with identical taus
-static void select_band(const KernelModel& k, double tau, double eps, int kcap, int* klo, int* khi) {
-  using Key = std::tuple<int, int, double, int, double, double, int>;
+// ------------------------------------------------------------------ data-independent window tables (R6)
+// ES shape for the requested oversampling (Barnett et al. 2019 choice beta = 0.97 pi (1 - 1/(2 os)) w, os capped at
+// 8); a slice's actual grid oversampling n_p / (2 (k_hi + 1)) is >= os (n_p is a power of two), where this window
+// is only more accurate.  Phi is tabulated on j / n_cap (j <= n_cap / 2): the planner reads Phi(k / n_p) at
+// j = k n_cap / n_p.  Cached per (w, os, n_cap).
+const WindowTables& window_tables(int w, int os, int ncap) {
   static std::mutex mu;
-  static std::map<Key, std::pair<int, int>> cache;
-  const Key key{k.kind, k.matern_p, k.scale, k.d, tau, eps, kcap};
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) { *klo = it->second.first; *khi = it->second.second; return; }
-  }
-  select_band_uncached(k, tau, eps, kcap, klo, khi);
+  static std::map<std::tuple<int, int, int>, WindowTables> cache;
   std::lock_guard<std::mutex> lk(mu);
-  if (cache.size() > 4096) cache.clear();   // bounded
-  cache.emplace(key, std::make_pair(*klo, *khi));
-}
-
-static void select_band_uncached(const KernelModel& k, double tau, double eps, int kcap, int* klo, int* khi) {
-  // c_k for k >= 0; c_{-k} = c_k.  Keep the smallest band [klo,khi] (|k| in band) with dropped mass <= eps.
-  std::vector<double> c;
-  c.reserve(1024);
-  double peak = 0.0;
-  int kpk = 0;
-  for (int kk = 0; kk <= kcap; ++kk) {
-    const double v = std::fabs(torus_coeff(k, tau, kk));
-    c.push_back(v);
-    if (v > peak) { peak = v; kpk = kk; }
-    if (kk > kpk + 8 && kk > 16) {
-      const double tail_est = (k.kind == 0) ? v : v * kk / 3.0;   // algebraic (k^-4) tails: sum ~ v k/3
-      if (v < 1e-3 * eps && tail_est < 0.25 * eps) break;
-    }
+  const auto key = std::make_tuple(w, os, ncap);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  WindowTables t;
+  t.w = w;
+  t.beta = static_cast<float>(0.97 * kPi * (1.0 - 1.0 / (2.0 * std::min(os, 8))) * w);
+  t.poly.assign(static_cast<size_t>(w) * (kPolyDeg + 1), 0.f);
+  fit_window_poly(w, t.beta, t.poly.data(), &t.poly_err);
+  std::vector<double> gx, gw;
+  gauss_legendre(128, gx, gw);
+  t.phi2inv.assign(ncap / 2 + 1, 0.f);
+  for (int j = 0; j <= ncap / 2; ++j) {
+    const double ph = window_ft(static_cast<double>(j) / ncap, w, t.beta, gx, gw);
+    t.phi2inv[j] = static_cast<float>(1.0 / (ph * ph));
   }
-  const int K = static_cast<int>(c.size()) - 1;
-  // upper edge: drop from the top while the dropped mass (x2 for +-k) stays <= eps/2 (+ analytic tail)
-  const double far_tail = (k.kind == 0) ? 0.0 : c[K] * K / 3.0;
-  double dropped = 2.0 * far_tail;
-  int hi = K;
-  while (hi > 0 && dropped + 2.0 * c[hi] <= 0.5 * eps) { dropped += 2.0 * c[hi]; --hi; }
-  int lo = 0;
-  if (k.kind == 0) {  // Gaussian bands sit on a bump away from 0 for d > 1
-    double dl = 0.0;
-    while (lo < hi && dl + (lo == 0 ? 1.0 : 2.0) * c[lo] <= 0.5 * eps) { dl += (lo == 0 ? 1.0 : 2.0) * c[lo]; ++lo; }
-  }
-  *klo = lo;
-  *khi = hi;
-}
-
-static int ceil_pow2(int64_t v) {
-  int n = 1;
-  while (n < v) n <<= 1;
-  return n;
-}
-
-bool build_fourier_plan(const KernelModel& k, double eps, int w, int oversample, int ns, const float* xmin,
-                        const float* xmax, const float* amin, const float* amax, FourierPlan& out,
-                        std::string* err) {
-  const double reps = decay_radius(k, eps);
-  out.slices.assign(ns, SlicePlan{});
-  out.w = w;
-  int kmax = 0, lomin = 1 << 30;
-  double tmin = 1e300, tmax = 0.0;
-  for (int p = 0; p < ns; ++p) {
-    if (!std::isfinite(amin[p]) || !std::isfinite(amax[p]) || !std::isfinite(xmin[p]) || !std::isfinite(xmax[p])) {
-      if (err) *err = "non-finite projection in slice " + std::to_string(p);
-      return false;
-    }
-    const double R = static_cast<double>(amax[p]) - static_cast<double>(amin[p]);
-    double inv_tau = R + reps;                                   // aliases at distance >= 1/tau - R = r_eps (R3)
-    if (k.kind == 2) inv_tau = std::max(inv_tau, 2.0 * R * (1.0 + 1e-6) + 1e-30);   // |du| <= 1/2 for h (R7)
-    const double tau = 1.0 / inv_tau;
-    SlicePlan& sp = out.slices[p];
-    sp.tau = static_cast<float>(tau);
-    sp.cen = static_cast<float>(0.5 * (static_cast<double>(amin[p]) + static_cast<double>(amax[p])));
-    tmin = std::min(tmin, tau);
-    tmax = std::max(tmax, tau);
-  }
-  // Band edges move monotonically with tau (c_k = tau fhat(tau k) [+ companion]: the spectrum stretches as
-  // 1/tau), so the union of the bands at the extreme tau covers every slice; a wider band than a slice
-  // strictly needs only adds (tiny) coefficients.
-  {
-    int lo1, hi1, lo2, hi2;
-    select_band(k, static_cast<double>(static_cast<float>(tmin)), eps, 1 << 16, &lo1, &hi1);
-    select_band(k, static_cast<double>(static_cast<float>(tmax)), eps, 1 << 16, &lo2, &hi2);
-    lomin = std::min(lo1, lo2);
-    kmax = std::max(hi1, hi2);
-    for (int p = 0; p < ns; ++p) {
-      out.slices[p].klo = lomin;
-      out.slices[p].khi = kmax;
-    }
-  }
-  const int n = std::max(16, ceil_pow2(static_cast<int64_t>(oversample) * 2 * (kmax + 1)));
-  if (n > 16384) {
-    if (err) *err = "NFFT grid n=" + std::to_string(n) + " exceeds the built limit 16384 (k_max=" + std::to_string(kmax) + ")";
-    return false;
-  }
-  out.n = n;
-  out.k_max = kmax;
-  out.band_lo_min = lomin;
-  out.tau_min = tmin;
-  out.tau_max = tmax;
-  // ES shape for the actual oversampling (Barnett et al. 2019 choice beta = 0.97 pi (1 - 1/(2 os)) w)
-  const double os = static_cast<double>(n) / (2.0 * (kmax + 1));
-  out.beta = static_cast<float>(0.97 * kPi * (1.0 - 1.0 / (2.0 * std::min(os, 8.0))) * w);
-  const int nh = n / 2 + 1;
-  std::vector<double> Phi;
-  {
-    static std::mutex mu;
-    static std::map<std::tuple<int, int, float>, std::vector<double>> cache;
-    std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(n, w, out.beta);
-    auto it = cache.find(key);
-    if (it == cache.end()) {
-      std::vector<double> gx, gw;
-      gauss_legendre(128, gx, gw);
-      std::vector<double> ph(nh);
-      for (int kk = 0; kk < nh; ++kk) ph[kk] = window_ft(static_cast<double>(kk) / n, w, out.beta, gx, gw);
-      it = cache.emplace(key, std::move(ph)).first;
-    }
-    Phi = it->second;
-  }
-  out.phi2inv.assign(nh, 0.0f);
-  for (int kk = 0; kk < nh; ++kk) out.phi2inv[kk] = static_cast<float>(1.0 / (Phi[kk] * Phi[kk]));
-  int W = 0, WA = 0;
-  for (int p = 0; p < ns; ++p) {
-    SlicePlan& sp = out.slices[p];
-    // footprint of the x points in grid cells: identical fp32 operations to the device (no contraction)
-    volatile float t = sp.tau, c = sp.cen, nf = static_cast<float>(n), hw = 0.5f * w;
-    volatile float u0 = xmin[p] - c;
-    volatile float u1 = xmax[p] - c;
-    volatile float v0 = u0 * t;
-    volatile float v1 = u1 * t;
-    volatile float g0 = v0 * nf;
-    volatile float g1 = v1 * nf;
-    volatile float a0 = g0 - hw;
-    volatile float a1 = g1 - hw;
-    const int l0 = static_cast<int>(std::floor(a0)) + 1 - 1;   // one cell of margin
-    const int l1 = static_cast<int>(std::floor(a1)) + w + 1;
-    sp.lmin = l0;
-    W = std::max(W, l1 - l0 + 1);
-    volatile float ua0 = amin[p] - c;
-    volatile float ua1 = amax[p] - c;
-    volatile float va0 = ua0 * t;
-    volatile float va1 = ua1 * t;
-    volatile float ga0 = va0 * nf;
-    volatile float ga1 = va1 * nf;
-    volatile float aa0 = ga0 - hw;
-    volatile float aa1 = ga1 - hw;
-    const int la0 = static_cast<int>(std::floor(aa0)) + 1 - 1;
-    const int la1 = static_cast<int>(std::floor(aa1)) + 1 + 1;   // cells l0 (not l0+w): interpolation polynomials
-    sp.lminA = la0;
-    WA = std::max(WA, la1 - la0 + 1);
-  }
-  out.W = W;
-  out.WA = WA;
-  out.poly.assign(static_cast<size_t>(w) * (kPolyDeg + 1), 0.f);
-  // the fit depends on (w, beta) only: cached (it costs ~w x 400 exp evaluations per call otherwise)
-  bool fit_ok;
-  {
-    static std::mutex mu;
-    static std::map<std::pair<int, float>, std::pair<std::vector<float>, double>> cache;
-    std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_pair(w, out.beta);
-    auto it = cache.find(key);
-    if (it == cache.end()) {
-      std::vector<float> c(out.poly.size());
-      double e = 0.0;
-      fit_window_poly(w, out.beta, c.data(), &e);
-      it = cache.emplace(key, std::make_pair(std::move(c), e)).first;
-    }
-    out.poly = it->second.first;
-    out.poly_err = it->second.second;
-    fit_ok = out.poly_err < 1e-4;
-  }
-  if (!fit_ok) {
-    if (err) *err = "window polynomial fit failed (error " + std::to_string(out.poly_err) + ")";
-    return false;
-  }
-  return true;
+  return cache.emplace(key, std::move(t)).first->second;
 }
 
 }  // namespace sks

@@ -31,14 +31,6 @@ double torus_coeff(const KernelModel& k, double tau, int64_t kk);
 // decay radius (in x units) beyond which |f(x)| <= eps  (reading R3): numeric Fourier integral, cached
 double decay_radius(const KernelModel& k, double eps);
 
-// ---- per-call Fourier plan
-struct SlicePlan {
-  float tau, cen;   // u = tau (z - cen) in [-1/2, 1/2)
-  int lmin;         // first grid cell of the x footprint (unwrapped)
-  int lminA;        // first grid cell of the footprint of all points (x and y)
-  int klo, khi;     // kept band: klo <= |k| <= khi
-};
-
 // Piecewise-polynomial form of the window (R6): for a point with fractional offset f in [0,1), tap j of w
 // has weight p_j(f) = sum_k coef[j*(deg+1) + k] f^k ~= ES((f + w/2 - 1 - j) * 2/w).
 // degree 7: the fit error is set by the ES window's edge kink, not by the degree (w = 6, os = 2: 6.7e-7 at
@@ -46,25 +38,15 @@ struct SlicePlan {
 constexpr int kPolyDeg = 7;
 bool fit_window_poly(int w, double beta, float* coef /* w*(kPolyDeg+1) */, double* max_err);
 
-struct FourierPlan {
-  int n = 0;            // grid length (power of two)
-  int w = 0;            // window taps
-  float beta = 0.f;     // ES window shape
-  int k_max = 0, band_lo_min = 0;
-  int W = 0;            // widest per-slice footprint of the x points (cells)
-  int WA = 0;           // widest per-slice footprint of all points (cells)
-  std::vector<float> poly;   // w * (kPolyDeg + 1) window polynomial coefficients
+// data-independent window data of the device planner (R6): ES shape, its piecewise-polynomial fit, and
+// 1 / Phi(j / ncap)^2 for j = 0 .. ncap / 2 (window deconvolution, folded into D_k by the planner)
+struct WindowTables {
+  int w = 0;
+  float beta = 0.f;
+  std::vector<float> poly;      // w * (kPolyDeg + 1)
   double poly_err = 0.0;
-  double tau_min = 0, tau_max = 0;
-  std::vector<SlicePlan> slices;
-  std::vector<float> phi2inv;   // [n/2 + 1]  1 / Phi(k/n)^2 (window deconvolution, folded into D_k on device)
+  std::vector<float> phi2inv;   // [ncap / 2 + 1]
 };
-
-// Build the plan for `ns` slices from per-slice projection ranges.
-//   xmin/xmax: range of the x (source) projections, amin/amax: range over x and y.
-// Returns false with a message on failure (unsupported size / non-finite range).
-bool build_fourier_plan(const KernelModel& k, double eps, int w, int oversample, int ns, const float* xmin,
-                        const float* xmax, const float* amin, const float* amax, FourierPlan& out,
-                        std::string* err);
+const WindowTables& window_tables(int w, int os, int ncap);
 
 }  // namespace sks

@@ -125,10 +125,14 @@ __global__ void k_minmax(ZView zv, unsigned* mm, int* flag) {
   }
 }
 
-// call prologue in one launch: zero the flag words, zero the fp64 target sums, initialise the first batch's ranges
+// call prologue in one launch: zero the flag words, initialise the plan summary, zero the fp64 target sums and
+// initialise the first batch's ranges
 __global__ void k_prologue(uint4* flag16, double* s64, int64_t M, unsigned* mm, int np) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (t == 0) *flag16 = make_uint4(0, 0, 0, 0);
+  // the device planner's summary words (flag16 + 4): maxima from 0, minima (k_lo, tau) from all ones
+  if (t < kPlanSummaryWords)
+    reinterpret_cast<unsigned*>(flag16)[4 + t] = (t == 2 || t == 5) ? 0xffffffffu : 0u;
   if (t < np) { mm[t * 4 + 0] = 0xffffffffu; mm[t * 4 + 1] = 0u; mm[t * 4 + 2] = 0xffffffffu; mm[t * 4 + 3] = 0u; }
   if (s64)
     for (int64_t m = t; m < M; m += static_cast<int64_t>(gridDim.x) * blockDim.x) s64[m] = 0.0;
@@ -139,6 +143,23 @@ cudaError_t launch_prologue(void* flag16, double* s64, int64_t M, unsigned* mm, 
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
   k_prologue<<<static_cast<unsigned>(blocks), 256, 0, st>>>(static_cast<uint4*>(flag16), s64, M, mm, np);
+  return cudaGetLastError();
+}
+
+__global__ void k_rerun_prep(unsigned* flag16, unsigned* mm, int np) {
+  if (flag16[0] == 0) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    mm[i * 4 + 0] = 0xffffffffu; mm[i * 4 + 1] = 0u; mm[i * 4 + 2] = 0xffffffffu; mm[i * 4 + 3] = 0u;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    flag16[3] = 1u;
+    flag16[0] = 0u;
+  }
+}
+
+cudaError_t launch_rerun_prep(unsigned* flag16, unsigned* mm, int np, cudaStream_t st) {
+  k_rerun_prep<<<1, 256, 0, st>>>(flag16, mm, np);   // one CTA: its flag reset follows its range resets
   return cudaGetLastError();
 }
 
@@ -155,73 +176,27 @@ cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ a2: device planner D_k = c_k / Phi_k^2
-__device__ double torus_coeff_dev(const CoeffConst& c, double tau, int k) {
-  const double PI = 3.14159265358979323846;
-  const double rho = c.scale * tau * static_cast<double>(k);
-  double fh = 0.0;
-  if (c.kind == 0) {
-    if (rho == 0.0) fh = (c.d == 1) ? sqrt(2.0 * PI) : 0.0;
-    else {
-      const double a = 2.0 * PI * PI * rho * rho;
-      fh = exp(c.logpref - a + 0.5 * (c.d - 1) * log(a));
-    }
-  } else if (c.kind == 2) {
-    const double s = 2.0 * PI * rho;
-    if (s == 0.0) fh = (c.d == 1) ? 2.0 : 0.0;
-    else fh = exp(c.logpref + (c.d - 1) * log(s) - 0.5 * (c.d + 1) * log1p(s * s));
-  } else if (c.kind == 3) {
-    const double lr = (c.d == 1) ? 0.0 : ((rho == 0.0) ? -INFINITY : (c.d - 1) * log(rho));
-    fh = exp(c.logpref + lr - (c.nu + 0.5 * c.d) * log(2.0 * c.nu + 4.0 * PI * PI * rho * rho));
-  }
-  double v = tau * c.scale * fh;
-  if (c.kind == 2) {
-    const double A = c.lap_A / tau;
-    v += (k == 0) ? A / 6.0 : -A / (2.0 * PI * PI * static_cast<double>(k) * static_cast<double>(k));
-  }
-  return v;
-}
-
-__global__ void k_plan_D(const FPar* __restrict__ fp, CoeffConst cc, const float* __restrict__ phi2inv, int n,
-                         float* __restrict__ D) {
-  const int p = blockIdx.y;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nh = n / 2 + 1;
-  if (k >= nh) return;
-  const FPar f = fp[p];
-  const int klo = f.klo_khi >> 16, khi = f.klo_khi & 0xffff;
-  float v = 0.f;
-  if (k >= klo && k <= khi) v = static_cast<float>(torus_coeff_dev(cc, static_cast<double>(f.tau), k) * phi2inv[k]);
-  D[static_cast<int64_t>(p) * nh + k] = v;
-}
-
-cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* phi2inv, int n, float* D,
-                          cudaStream_t st) {
-  const int nh = n / 2 + 1;
-  k_plan_D<<<dim3((nh + 255) / 256, np), 256, 0, st>>>(fp, cc, phi2inv, n, D);
-  return cudaGetLastError();
-}
-
 // ------------------------------------------------------------------ a5: spreading (adjoint NFFT gridding)
-// Per-lane private sub-grids [warp][cell][lane] (conflict-free RMW, no atomics) over the slice's footprint
-// of W cells; one CTA = (chunk of points, slice).  Fallback for wide footprints: CTA grid + smem atomics.
-constexpr int SP_THREADS = 256, SP_WARPS = SP_THREADS / 32, SP_WMAX_PRIV = 64;
+// One kernel, the path chosen per slice (uniform per CTA) from the plan's footprint W_p:
+//  * W_p <= SP_WMAX_PRIV: per-lane private sub-grids [warp][cell][lane] over the slice's footprint (conflict-free
+//    read-modify-writes, no atomics), reduced over warps and lanes at the end;
+//  * wider (e.g. the Laplacian's smooth part): one shared grid of n_p cells per CTA.  Shared-memory float atomics
+//    are CAS loops on sm_100a, so the CTA accumulates in 32-bit fixed point with native integer atomics, in sub-
+//    chunks of SP_SUB points: scale S = 2^30 / sum_{sub-chunk} |w| bounds every partial cell sum by 2^30; the
+//    rounding per contribution is <= sum_{sub-chunk} |w| 2^-31, ~1e-9 of the sub-chunk's weight.
+// One CTA = (chunk of points, slice).
+constexpr int SP_THREADS = 256, SP_WARPS = SP_THREADS / 32, SP_WMAX_PRIV = 64, SP_SUB = 8192;
+constexpr int SP_SMEM = SP_WARPS * SP_WMAX_PRIV * 32 * 4;   // = 16384 * 4: also the widest shared grid
+static_assert(SP_SMEM >= 16384 * 4, "the shared-grid path needs n_cap floats");
 
 template <int WT>
-__global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const float* __restrict__ w,
-                                                               const FPar* __restrict__ fp, int n, PolyWin pw,
-                                                               int W, int64_t chunk, float* __restrict__ grid) {
-  extern __shared__ float priv[];   // [SP_WARPS][W][32]
-  const int p = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const FPar f = fp[p];
+__device__ __forceinline__ void spread_private(const FPar& f, const float* zx, const float* wc, int cnt, int W,
+                                               float nf, const PolyWin& pw, float* priv, float* gp, int n) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   float* mine = priv + static_cast<int64_t>(wid) * W * 32;
   for (int c = lane; c < W * 32; c += 32) mine[c] = 0.f;
   __syncwarp();
-  const float nf = static_cast<float>(n), hw = 0.5f * pw.w;
-  const int64_t i0 = blockIdx.x * chunk;
-  const int cnt = static_cast<int>(min(zv.N, i0 + chunk) - i0);   // 32-bit loop inside the chunk
-  const float* zx = zv.zx + p * zv.ldx + i0;
-  const float* wc = w + i0;
+  const float hw = 0.5f * pw.w;
   float* base = mine - f.lmin * 32 + lane;   // cell l of this lane's private grid: base[l * 32]
   if (pw.w == WT && (WT & 1) == 0) {
     // centered even/odd taps with the coefficients held in registers for the whole loop, four points per
@@ -284,89 +259,88 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread_private(ZView zv, const f
     for (int q = 0; q < SP_WARPS; ++q) s += priv[(static_cast<int64_t>(q) * W + c) * 32 + lane];
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0 && s != 0.f) atomicAdd(&grid[static_cast<int64_t>(p) * n + ((f.lmin + c) & (n - 1))], s);
+    if (lane == 0 && s != 0.f) atomicAdd(&gp[(f.lmin + c) & (n - 1)], s);
   }
 }
 
-// Wide footprints (W > 64 cells, e.g. the Laplacian's smooth part): one shared grid per CTA.  Shared-memory
-// float atomics are CAS loops on sm_100a, so the CTA accumulates in 32-bit fixed point with native integer
-// atomics: scale S = 2^30 / sum_{chunk} |w| bounds every partial cell sum by 2^30 (no overflow); the rounding
-// per contribution is <= sum_{chunk}|w| 2^-31, i.e. ~1e-9 of the chunk's weight, far below the fp32 grid.
 template <int WT>
-__global__ void __launch_bounds__(SP_THREADS) k_spread_shared(ZView zv, const float* __restrict__ w,
-                                                              const FPar* __restrict__ fp, int n, PolyWin pw,
-                                                              int64_t chunk, float* __restrict__ grid) {
-  extern __shared__ int sgi[];   // [n] fixed point
+__device__ __forceinline__ void spread_shared(const FPar& f, const float* zx, const float* wc, int cnt, float nf,
+                                              const PolyWin& pw, int* sgi, float* gp, int n) {
   __shared__ float wred[SP_THREADS / 32];
-  const int p = blockIdx.y, tid = threadIdx.x;
-  const FPar f = fp[p];
-  for (int c = tid; c < n; c += SP_THREADS) sgi[c] = 0;
-  const int64_t i0 = blockIdx.x * chunk, i1 = min(zv.N, i0 + chunk);
-  float aw = 0.f;
-  for (int64_t i = i0 + tid; i < i1; i += SP_THREADS) aw += fabsf(__ldg(w + i));
+  const int tid = threadIdx.x;
+  const float hw = 0.5f * pw.w;
+  for (int s0 = 0; s0 < cnt; s0 += SP_SUB) {
+    const int s1 = min(cnt, s0 + SP_SUB);
+    for (int c = tid; c < n; c += SP_THREADS) sgi[c] = 0;
+    float aw = 0.f;
+    for (int i = s0 + tid; i < s1; i += SP_THREADS) aw += fabsf(__ldg(wc + i));
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) aw += __shfl_xor_sync(0xffffffffu, aw, o);
-  if ((tid & 31) == 0) wred[tid >> 5] = aw;
-  __syncthreads();
-  float wsum = 0.f;
+    for (int o = 16; o >= 1; o >>= 1) aw += __shfl_xor_sync(0xffffffffu, aw, o);
+    if ((tid & 31) == 0) wred[tid >> 5] = aw;
+    __syncthreads();
+    float wsum = 0.f;
 #pragma unroll
-  for (int q = 0; q < SP_THREADS / 32; ++q) wsum += wred[q];
-  if (!(wsum > 0.f)) return;   // all weights zero in this chunk (uniform)
-  const float S = 1073741824.0f / (wsum * 1.0001f);   // 2^30 / sum|w| (margin for the fp32 sum)
-  const float nf = static_cast<float>(n), hw = 0.5f * pw.w;
-  const float* zx = zv.zx + p * zv.ldx;
-  for (int64_t i = i0 + tid; i < i1; i += SP_THREADS) {
-    const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);
-    const float a = __fsub_rn(v, hw), fl = floorf(a);
-    const int l0 = static_cast<int>(fl) + 1;
-    const float ws = __ldg(w + i) * S;
-    float tw[WT];
-    poly_taps<WT>(pw, a - fl, tw);
+    for (int q = 0; q < SP_THREADS / 32; ++q) wsum += wred[q];
+    if (wsum > 0.f) {   // (uniform: all weights of this sub-chunk zero otherwise)
+      const float S = 1073741824.0f / (wsum * 1.0001f);   // 2^30 / sum|w| (margin for the fp32 sum)
+      for (int i = s0 + tid; i < s1; i += SP_THREADS) {
+        const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);
+        const float a = __fsub_rn(v, hw), fl = floorf(a);
+        const int l0 = static_cast<int>(fl) + 1;
+        const float ws = __ldg(wc + i) * S;
+        float tw[WT];
+        poly_taps<WT>(pw, a - fl, tw);
 #pragma unroll
-    for (int j = 0; j < WT; ++j) atomicAdd(&sgi[(l0 + j) & (n - 1)], __float2int_rn(ws * tw[j]));
-  }
-  __syncthreads();
-  const float inv = 1.0f / S;
-  for (int c = tid; c < n; c += SP_THREADS) {
-    const int v = sgi[c];
-    if (v != 0) atomicAdd(&grid[static_cast<int64_t>(p) * n + c], static_cast<float>(v) * inv);
+        for (int j = 0; j < WT; ++j) atomicAdd(&sgi[(l0 + j) & (n - 1)], __float2int_rn(ws * tw[j]));
+      }
+      __syncthreads();
+      const float inv = 1.0f / S;
+      for (int c = tid; c < n; c += SP_THREADS) {
+        const int v = sgi[c];
+        if (v != 0) atomicAdd(&gp[c], static_cast<float>(v) * inv);
+      }
+    }
+    __syncthreads();
   }
 }
 
-cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int n, const PolyWin& pw, int W,
-                          float* grid, cudaStream_t st) {
-  // chunking: enough CTAs to fill 148 SMs several times, >= 2048 points per CTA to amortise the flush
-  // (private grids: up to 32768 points per CTA; the fixed-point shared grid keeps <= 8192, its rounding
-  // scales with the chunk's weight)
-  const bool priv = W <= SP_WMAX_PRIV;
-  int64_t chunk = priv ? 32768 : 8192;
-  while (chunk > 2048 && ((zv.N + chunk - 1) / chunk) * np < (priv ? 16 : 4) * 148) chunk >>= 1;
+template <int WT>
+__global__ void __launch_bounds__(SP_THREADS) k_spread(ZView zv, const float* __restrict__ w,
+                                                       const FPar* __restrict__ fp, int ncap, PolyWin pw,
+                                                       int64_t chunk, float* __restrict__ grid,
+                                                       const unsigned* __restrict__ flag16) {
+  extern __shared__ float spsm[];
+  if (call_failed(flag16)) return;
+  const int p = blockIdx.y;
+  const FPar f = fp[p];
+  const int n = 1 << f.logn;
+  const float nf = static_cast<float>(n);
+  const int64_t i0 = blockIdx.x * chunk;
+  const int cnt = static_cast<int>(min(zv.N, i0 + chunk) - i0);   // 32-bit loop inside the chunk
+  const float* zx = zv.zx + p * zv.ldx + i0;
+  const float* wc = w + i0;
+  float* gp = grid + static_cast<int64_t>(p) * ncap;
+  if (f.W <= SP_WMAX_PRIV) spread_private<WT>(f, zx, wc, cnt, f.W, nf, pw, spsm, gp, n);
+  else spread_shared<WT>(f, zx, wc, cnt, nf, pw, reinterpret_cast<int*>(spsm), gp, n);
+}
+
+cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int ncap, const PolyWin& pw,
+                          bool wide_likely, float* grid, const unsigned* flag16, cudaStream_t st) {
+  // chunking: enough CTAs to fill 148 SMs several times, >= 2048 points per CTA to amortise the flush (narrow
+  // footprints: up to 32768 points per CTA; wide ones (the Laplacian) flush n_p cells per 8192-point sub-chunk)
+  int64_t chunk = wide_likely ? 8192 : 32768;
+  while (chunk > 2048 && ((zv.N + chunk - 1) / chunk) * np < (wide_likely ? 4 : 16) * 148) chunk >>= 1;
   const unsigned nchunk = static_cast<unsigned>((zv.N + chunk - 1) / chunk);
   if (nchunk == 0) return cudaSuccess;
-  if (priv) {
-    const size_t smem = static_cast<size_t>(SP_WARPS) * W * 32 * sizeof(float);
-    auto go = [&](auto kern) {
-      set_smem_attr_once(reinterpret_cast<const void*>(kern), SP_WARPS * SP_WMAX_PRIV * 32 * 4);
-      kern<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, W, chunk, grid);
-    };
-    switch (pw.w) {
-      case 4: go(k_spread_private<4>); break;
-      case 6: go(k_spread_private<6>); break;
-      case 8: go(k_spread_private<8>); break;
-      default: go(k_spread_private<12>); break;   // taps beyond w have zero coefficients
-    }
-  } else {
-    const size_t smem = static_cast<size_t>(n) * sizeof(float);
-    auto go = [&](auto kern) {
-      set_smem_attr_once(reinterpret_cast<const void*>(kern), 16384 * 4);
-      kern<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, n, pw, chunk, grid);
-    };
-    switch (pw.w) {
-      case 4: go(k_spread_shared<4>); break;
-      case 6: go(k_spread_shared<6>); break;
-      case 8: go(k_spread_shared<8>); break;
-      default: go(k_spread_shared<12>); break;
-    }
+  auto go = [&](auto kern) {
+    set_smem_attr_once(reinterpret_cast<const void*>(kern), SP_SMEM);
+    kern<<<dim3(nchunk, np), SP_THREADS, SP_SMEM, st>>>(zv, w, fp, ncap, pw, chunk, grid, flag16);
+  };
+  switch (pw.w) {
+    case 4: go(k_spread<4>); break;
+    case 6: go(k_spread<6>); break;
+    case 8: go(k_spread<8>); break;
+    default: go(k_spread<12>); break;   // taps beyond w have zero coefficients
   }
   return cudaGetLastError();
 }
@@ -397,14 +371,15 @@ __device__ __forceinline__ void fft_stages(float2* buf, const float2* tw, int n,
 }
 
 __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restrict__ grid, const float* __restrict__ D,
-                                                           int n, int logn, float* __restrict__ h,
-                                                           const FPar* __restrict__ fp, PolyWin pw, int WA,
-                                                           float* __restrict__ Q) {
+                                                           int ncap, const FPar* __restrict__ fp, PolyWin pw,
+                                                           float* __restrict__ Q, const unsigned* __restrict__ flag16) {
   extern __shared__ float2 sm[];
-  float2* buf = sm;          // [n]
-  float2* tw = sm + n;       // per-stage forward twiddles (fft_stages)
+  if (call_failed(flag16)) return;
   const int p = blockIdx.x;
-  const int nh = n / 2 + 1;
+  const FPar f = fp[p];
+  const int logn = f.logn, n = 1 << logn;
+  float2* buf = sm;          // [n]
+  float2* tw = sm + ncap;    // per-stage forward twiddles (fft_stages)
   const bool ps = n <= 8192;
   if (ps) {
     for (int j = threadIdx.x; j < n - 1; j += FF_THREADS) {
@@ -420,12 +395,12 @@ __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restri
       tw[j] = make_float2(cv, -sv);
     }
   }
-  const float* gp = grid + static_cast<int64_t>(p) * n;
+  const float* gp = grid + static_cast<int64_t>(p) * ncap;
   for (int l = threadIdx.x; l < n; l += FF_THREADS) buf[__brev(l) >> (32 - logn)] = make_float2(gp[l], 0.f);
   __syncthreads();
   if (ps) fft_stages<true>(buf, tw, n, logn);      // G_k = sum_l g_l e^{-2 pi i k l / n}
   else fft_stages<false>(buf, tw, n, logn);
-  const float* Dp = D + static_cast<int64_t>(p) * nh;
+  const float* Dp = D + static_cast<int64_t>(p) * (ncap / 2 + 1);
   for (int k = threadIdx.x; k < n; k += FF_THREADS) {
     const float dk = Dp[k <= n / 2 ? k : n - k];
     const float2 v = buf[k];
@@ -439,70 +414,58 @@ __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restri
   __syncthreads();
   if (ps) fft_stages<true>(buf, tw, n, logn);      // h_l = conj(FFT(conj X))_l; real part
   else fft_stages<false>(buf, tw, n, logn);
-  float* hp = h + static_cast<int64_t>(p) * n;
-  for (int l = threadIdx.x; l < n; l += FF_THREADS) hp[l] = buf[l].x;
-  if (Q) {   // interpolation polynomials of the footprint cells: Q[c][k] = sum_j h[l + j] coef_j[k]
-    const int l00 = fp[p].lminA;
-    float* qp = Q + static_cast<int64_t>(p) * WA * (PW_D + 1);
-    for (int e = threadIdx.x; e < WA * (PW_D + 1); e += FF_THREADS) {
-      const int c = e / (PW_D + 1), k = e - c * (PW_D + 1);
-      float acc = 0.f;
-      for (int j = 0; j < pw.w; ++j) acc = fmaf(buf[(l00 + c + j) & (n - 1)].x, pw.c[j * (PW_D + 1) + k], acc);
-      qp[e] = acc;
-    }
+  // interpolation polynomials of the footprint cells: Q[c][k] = sum_j h[lminA + c + j] coef_j[k]
+  const int l00 = f.lminA, WA = f.WA;
+  float* qp = Q + static_cast<int64_t>(p) * q_stride(ncap);
+  for (int e = threadIdx.x; e < WA * (PW_D + 1); e += FF_THREADS) {
+    const int c = e / (PW_D + 1), k = e - c * (PW_D + 1);
+    float acc = 0.f;
+    for (int j = 0; j < pw.w; ++j) acc = fmaf(buf[(l00 + c + j) & (n - 1)].x, pw.c[j * (PW_D + 1) + k], acc);
+    qp[e] = acc;
   }
 }
 
-cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, const FPar* fp,
-                              const PolyWin& pw, int WA, float* Q, cudaStream_t st) {
-  int logn = 0;
-  while ((1 << logn) < n) ++logn;
-  const size_t smem = static_cast<size_t>(n) * sizeof(float2) + static_cast<size_t>(n <= 8192 ? n : n / 2) * sizeof(float2);
-  set_smem_attr_once(reinterpret_cast<const void*>(k_fft_filter), 16384 * 8 + 8192 * 8);
-  k_fft_filter<<<np, FF_THREADS, smem, st>>>(grid, D, n, logn, h, fp, pw, WA, Q);
+cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int ncap, const FPar* fp, const PolyWin& pw,
+                              float* Q, const unsigned* flag16, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(ncap) * sizeof(float2) + static_cast<size_t>(8192) * sizeof(float2);
+  set_smem_attr_once(reinterpret_cast<const void*>(k_fft_filter), static_cast<int>(smem));
+  k_fft_filter<<<np, FF_THREADS, smem, st>>>(grid, D, ncap, fp, pw, Q, flag16);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ a7: interpolation at the targets
 // grid (target blocks, slice groups): each thread handles one target over EV_SG slices, then one fp64
 // atomic into s64 (or per-slice stores for sks_sum_1d).  Target blocks vary fastest, so the CTAs resident
-// at a time work on the same slice group and its bucket records / grids stay in L2.
+// at a time work on the same slice group and its polynomials stay in L2.  A target's value on slice p is one
+// degree-7 Horner on the interpolation polynomial of its cell (Q, written by k_fft_filter).
 constexpr int EV_THREADS = 256, EV_SG = 32;
 
-__device__ __forceinline__ double eval_one(const EvalArgs& a, int p, float z, float nf, float hw, int64_t m,
-                                           int64_t M) {
+__device__ __forceinline__ float horner8(float4 c0, float4 c1, float fr) {
+  float t = fmaf(c1.w, fr, c1.z);
+  t = fmaf(t, fr, c1.y);
+  t = fmaf(t, fr, c1.x);
+  t = fmaf(t, fr, c0.w);
+  t = fmaf(t, fr, c0.z);
+  t = fmaf(t, fr, c0.y);
+  return fmaf(t, fr, c0.x);
+}
+
+__device__ __forceinline__ double eval_one(const EvalArgs& a, int p, float z, float hw, int64_t m, int64_t M) {
   const double zd = z;
   double t = 0.0;
+  const FPar f = a.fp[p];
   if (a.moment) {
     const SliceTot T = a.tot[p];
-    t += a.mom_coef * static_cast<double>(a.fp[p].tau) * (T.C - 2.0 * zd * T.B + zd * zd * T.A);
+    t += a.mom_coef * static_cast<double>(f.tau) * (T.C - 2.0 * zd * T.B + zd * zd * T.A);
   }
   if (a.fourier) {
-    const FPar f = a.fp[p];
-    const float v = grid_coord(z, f.cen, f.tau, nf);
+    const float v = grid_coord(z, f.cen, f.tau, static_cast<float>(1 << f.logn));
     const float av = __fsub_rn(v, hw), fl = floorf(av);
     const int l0 = static_cast<int>(fl) + 1;
-    const float fr = av - fl;
-    float tf = 0.f;
-    if (a.Q) {   // one Horner per target on the cell's interpolation polynomial
-      static_assert(PW_D == 7, "interpolation polynomials are read as two float4");
-      const float4* q = reinterpret_cast<const float4*>(a.Q + (static_cast<int64_t>(p) * a.WA + (l0 - f.lminA)) * 8);
-      const float4 c0 = __ldg(q), c1 = __ldg(q + 1);
-      float acc2 = fmaf(c1.w, fr, c1.z);
-      acc2 = fmaf(acc2, fr, c1.y);
-      acc2 = fmaf(acc2, fr, c1.x);
-      acc2 = fmaf(acc2, fr, c0.w);
-      acc2 = fmaf(acc2, fr, c0.z);
-      acc2 = fmaf(acc2, fr, c0.y);
-      tf = fmaf(acc2, fr, c0.x);
-    } else {
-      const float* hp = a.h + static_cast<int64_t>(p) * a.n;
-      float tw[12];
-      poly_taps<12>(a.pw, fr, tw);   // taps beyond w have zero coefficients
-#pragma unroll
-      for (int j = 0; j < 12; ++j) tf = fmaf(__ldg(hp + ((l0 + j) & (a.n - 1))), tw[j], tf);
-    }
-    t += tf;
+    static_assert(PW_D == 7, "interpolation polynomials are read as two float4");
+    const float4* q = reinterpret_cast<const float4*>(a.Q + static_cast<int64_t>(p) * q_stride(a.ncap) +
+                                                      (l0 - f.lminA) * 8);
+    t += horner8(__ldg(q), __ldg(q + 1), av - fl);
   }
   if (a.per_slice_out) {
     float* o = a.per_slice_out + static_cast<int64_t>(p) * M + m;
@@ -512,11 +475,12 @@ __device__ __forceinline__ double eval_one(const EvalArgs& a, int p, float z, fl
 }
 
 __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
+  if (call_failed(a.flag16)) return;
   const int64_t M = a.zv.M;
   const int64_t m = blockIdx.x * static_cast<int64_t>(EV_THREADS) + threadIdx.x;
   if (m >= M) return;
   const int p0 = blockIdx.y * EV_SG, p1 = min(a.np, p0 + EV_SG);
-  const float nf = static_cast<float>(a.n), hw = 0.5f * a.pw.w;
+  const float hw = 0.5f * a.w;
   double acc = 0.0;
   int p = p0;
   for (; p + 4 <= p1; p += 4) {   // 4 independent slices in flight per target
@@ -524,14 +488,14 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) z[k] = __ldg(a.zv.zy + (p + k) * a.zv.ldy + m);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) acc += eval_one(a, p + k, z[k], nf, hw, m, M);
+    for (int k = 0; k < 4; ++k) acc += eval_one(a, p + k, z[k], hw, m, M);
   }
-  for (; p < p1; ++p) acc += eval_one(a, p, __ldg(a.zv.zy + p * a.zv.ldy + m), nf, hw, m, M);
+  for (; p < p1; ++p) acc += eval_one(a, p, __ldg(a.zv.zy + p * a.zv.ldy + m), hw, m, M);
   if (a.s64) atomicAdd(a.s64 + m, acc);
 }
 
-// the common case (interpolation polynomials, fp64 target sums, no per-slice output): slice parameters staged
-// in shared memory, the cell's 8 coefficients by one 256-bit load, fp32 partial sums over EV_U slices
+// the common case (fp64 target sums, no per-slice output): slice parameters staged in shared memory, the cell's 8
+// coefficients by one 256-bit load, fp32 partial sums over EV_U slices
 constexpr int EV_U = 8;
 __device__ __forceinline__ void ld_q8(const float* q, float4& c0, float4& c1) {
   asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -540,16 +504,18 @@ __device__ __forceinline__ void ld_q8(const float* q, float4& c0, float4& c1) {
 }
 
 template <bool MOMENT>
-__global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a) {
-  __shared__ float4 sp[EV_SG];   // (cen, tau n, Q offset of cell 0 (int bits), -)
+__global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a, int sg) {
+  __shared__ float4 sp[EV_SG];   // (cen, tau n_p, Q offset of cell 0 (int bits), -)
   __shared__ double4 st[MOMENT ? EV_SG : 1];   // (sum w, sum w z, sum w z^2, mom_coef tau) (fp64)
-  const int p0 = blockIdx.y * EV_SG, p1 = min(a.np, p0 + EV_SG);
-  const float nf = static_cast<float>(a.n), hw = 0.5f * a.pw.w;
+  if (call_failed(a.flag16)) return;
+  const int p0 = blockIdx.y * sg, p1 = min(a.np, p0 + sg);
+  const float hw = 0.5f * a.w;
+  const int64_t qs = q_stride(a.ncap);
   for (int q = threadIdx.x; q < p1 - p0; q += EV_THREADS) {
     const FPar f = a.fp[p0 + q];
-    // cell l0 = floor(v - w/2) + 1 of slice p reads Q[p][l0 - lminA]: float offset 8 (p WA + l0 - lminA)
-    const int qoff = 8 * ((p0 + q) * a.WA - f.lminA + 1);
-    sp[q] = make_float4(f.cen, f.tau * nf, __int_as_float(qoff), 0.f);
+    // cell l0 = floor(v - w/2) + 1 of slice p reads Q[p][l0 - lminA]: float offset qs (p - p0) + 8 (l0 - lminA)
+    const int qoff = static_cast<int>(qs * q) + 8 * (1 - f.lminA);
+    sp[q] = make_float4(f.cen, f.tau * static_cast<float>(1 << f.logn), __int_as_float(qoff), 0.f);
     if (MOMENT) {
       const SliceTot T = a.tot[p0 + q];
       st[q] = make_double4(T.A, T.B, T.C, a.mom_coef * static_cast<double>(f.tau));
@@ -559,19 +525,13 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a) {
   const int64_t m = blockIdx.x * static_cast<int64_t>(EV_THREADS) + threadIdx.x;
   if (m >= a.zv.M) return;
   const float* zy = a.zv.zy + m;
+  const float* Qg = a.Q + qs * p0;
   auto one = [&](int q, float z) {
     const float4 c = sp[q];
     const float av = __fsub_rn(__fmul_rn(__fsub_rn(z, c.x), c.y), hw), fl = floorf(av);
-    const float fr = av - fl;
     float4 c0, c1;
-    ld_q8(a.Q + (__float_as_int(c.z) + 8 * static_cast<int>(fl)), c0, c1);
-    float t = fmaf(c1.w, fr, c1.z);
-    t = fmaf(t, fr, c1.y);
-    t = fmaf(t, fr, c1.x);
-    t = fmaf(t, fr, c0.w);
-    t = fmaf(t, fr, c0.z);
-    t = fmaf(t, fr, c0.y);
-    return fmaf(t, fr, c0.x);
+    ld_q8(Qg + (__float_as_int(c.z) + 8 * static_cast<int>(fl)), c0, c1);
+    return horner8(c0, c1, av - fl);
   };
   double acc = 0.0;
   int p = p0;
@@ -614,11 +574,16 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a) {
 
 cudaError_t launch_eval(const EvalArgs& a, cudaStream_t st) {
   const unsigned bx = static_cast<unsigned>((a.zv.M + EV_THREADS - 1) / EV_THREADS);
-  const unsigned by = static_cast<unsigned>((a.np + EV_SG - 1) / EV_SG);
-  if (a.fourier && a.Q && a.s64 && !a.per_slice_out) {
-    if (a.moment) k_eval_q<true><<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
-    else k_eval_q<false><<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
+  if (a.fourier && a.s64 && !a.per_slice_out) {
+    // slices per CTA: EV_SG, or fewer (down to EV_U) when the targets alone give too few CTAs (small, latency-bound
+    // problems such as BJ cfg1: more CTAs in flight at the cost of one more fp64 atomic per target and group)
+    int sg = EV_SG;
+    while (sg > EV_U && static_cast<int64_t>(bx) * ((a.np + sg - 1) / sg) < 2 * 148) sg >>= 1;
+    const unsigned by = static_cast<unsigned>((a.np + sg - 1) / sg);
+    if (a.moment) k_eval_q<true><<<dim3(bx, by), EV_THREADS, 0, st>>>(a, sg);
+    else k_eval_q<false><<<dim3(bx, by), EV_THREADS, 0, st>>>(a, sg);
   } else {
+    const unsigned by = static_cast<unsigned>((a.np + EV_SG - 1) / EV_SG);
     k_eval<<<dim3(bx, by), EV_THREADS, 0, st>>>(a);
   }
   return cudaGetLastError();

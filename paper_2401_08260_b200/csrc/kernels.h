@@ -22,14 +22,21 @@ void prof_end(const ProfMark& m);
 // device): set once per (kernel, device), thread-safe
 void set_smem_attr_once(const void* kernel, int bytes);
 
-// per-slice Fourier parameters (device copy of SlicePlan)
+// per-slice Fourier plan (row a2), written by the device planner k_plan (plan.cu)
 struct FPar {
-  float tau, cen;
-  int lmin;     // first cell of the x footprint (spreading)
-  int klo_khi;  // (klo << 16) | khi
-  int lminA;    // first cell of the all-points footprint (interpolation polynomials)
-  int pad;
+  float tau, cen;   // u = tau (z - cen)
+  int lmin;         // first cell of the x footprint (spreading)
+  int klo, khi;     // kept band klo <= |k| <= khi
+  int lminA;        // first cell of the all-points footprint (interpolation polynomials)
+  int logn;         // grid n = 2^logn
+  int W, WA;        // widths (cells) of the x / all-points footprints
+  int pad[3];
 };
+
+// flag words of a call (16 bytes in the workspace): [0] non-finite projection, [1] FP16x2 sampled max |x|,
+// [2] plan failure bits (1: grid beyond n_cap, 2: band too wide for the NDFT), [3] FP16x2 range exceeded (the
+// projection was redone on TF32x2).  Kernels after the planner exit at once if [0] or [2] is set.
+__device__ __forceinline__ bool call_failed(const unsigned* flag16) { return (flag16[0] | flag16[2]) != 0; }
 
 // window polynomials: tap j weight p_j(f) = sum_k c[j*(PW_D+1)+k] f^k, f = frac(v - w/2)  (R6)
 constexpr int PW_D = 7;   // == host kPolyDeg; 8 coefficients = two float4
@@ -49,6 +56,17 @@ struct CoeffConst {
   double nu;        // Matern nu
   double lap_A;     // Laplacian: c_d / scale  (alpha c_d), multiplied by 1/tau per slice
 };
+
+// data-independent inputs of the device planner (host, cached per (kernel, d, eps, w, os))
+struct PlanConst {
+  CoeffConst cc;
+  double reps;      // decay radius r_eps of the counterpart (x units, reading R3)
+  double eps;       // dropped-coefficient budget (R5)
+  int os, w;        // oversampling, window taps
+  int ncap_log;     // log2 of the largest grid (n_cap)
+  int ndft;         // 1: the NDFT engine (band <= 32, no window deconvolution)
+};
+constexpr int kPlanSummaryWords = 8;   // max n, max k_hi, min k_lo, max W, max band, tau min / max bits, max WA
 
 // views of the projected points of a slice batch: x-part zx[p*ldx + i], y-part zy[p*ldy + m]
 struct ZView {
@@ -79,13 +97,19 @@ cudaError_t launch_project_f16(const float* x, int64_t N, const float* y, int64_
                                unsigned* f16max, cudaStream_t st);
 // the points can be read by TMA (d % 4 == 0, 16-byte aligned arrays): the raw fp32 tile is the hi operand
 bool proj_tf32_tma_ok(const float* x, int64_t N, const float* y, int64_t M, int d);
+// pred: nullptr, or a device word; the launch does nothing unless *pred != 0 (the FP16x2 -> TF32x2 rerun)
 cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g32, int np,
                                 const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag,
-                                cudaStream_t st);
+                                const unsigned* pred, cudaStream_t st);
+// after an FP16x2 projection: if it flagged a non-finite value (a point beyond the fp16 range, or a NaN / Inf input),
+// move the flag to flag16[3] (rerun) and reset the ranges mm [np][4], so that the predicated TF32x2 launch redoes the
+// batch (and flags genuine NaN / Inf inputs again)
+cudaError_t launch_rerun_prep(unsigned* flag16, unsigned* mm, int np, cudaStream_t st);
 // per-slice ranges of given projections (sks_sum_1d)
 cudaError_t launch_minmax(ZView zv, int np, unsigned* mm, int* flag, cudaStream_t st);
 cudaError_t launch_init_minmax(unsigned* mm, int np, cudaStream_t st);
-// call prologue (one launch): flag16 (16 bytes) and s64 [M] (nullptr: none) zeroed, mm [np][4] initialised
+// call prologue (one launch): flag16 (16 bytes) zeroed, the plan summary at flag16 + 16 bytes initialised, s64 [M]
+// (nullptr: none) zeroed, mm [np][4] initialised
 cudaError_t launch_prologue(void* flag16, double* s64, int64_t M, unsigned* mm, int np, cudaStream_t st);
 void decode_minmax(const unsigned* enc, float* dec, int n);
 
@@ -125,25 +149,41 @@ inline int sortpart_groups(int64_t N, int64_t M, int np) {
 }
 cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st);
 
-// row a2: D[p][k] = c_k(tau_p) / Phi_k^2 on the band of slice p, else 0  (k = 0..n/2)
-cudaError_t launch_plan_D(const FPar* fp, int np, CoeffConst cc, const float* phi2inv, int n, float* D,
-                          cudaStream_t st);
-// row a5: g[p][l] = sum_n w_n phi_win(v_n - l) over the x projections (ES window, w taps)
-cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int n, const PolyWin& pw, int W,
-                          float* grid, cudaStream_t st);
-// row a6: h[p] = IFFT_n(D[p] * FFT_n(g[p]))   (unnormalised, one CTA per slice, smem radix-2)
+// row a2 (plan.cu): per slice, from the ranges mm [np][4]: FPar fp[p], D[p][k] (stride n_cap/2 + 1) =
+// c_k(tau_p) / Phi(k / n_p)^2 on the band (phi2inv_cap[j] = 1 / Phi(j / n_cap)^2), grid[p][0, n_p) zeroed (stride
+// n_cap); failures set flag16 bits; summary [kPlanSummaryWords] (initialised by the prologue)
+cudaError_t launch_plan(const unsigned* mm, int np, const PlanConst& pc, const float* phi2inv_cap, FPar* fp, float* D,
+                        float* grid, unsigned* flag16, unsigned* summary, cudaStream_t st);
+// rows a1 + a5 fused (fused.cu; sources only, Fourier kernels at large N): the sources' projections are spread into
+// the grids from the tensor-core accumulators, never stored.  fused_spread_ok: d <= 128, d % 4 == 0, 16-byte
+// aligned x.  launch_source_bound: the sources' per-slice range bound (c_p +- rho') into mm[p][0..1] and combined
+// with the targets' exact range mm[p][2..3] (mu: source_bound_bytes(d) of scratch, nb: its last 16 bytes); then launch_plan,
+// then launch_proj_spread in place of the projection of x + launch_spread
+bool fused_spread_ok(int d, const float* x);
+size_t source_bound_bytes(int d);   // scratch of launch_source_bound: mu, partial sums, nb
+cudaError_t launch_source_bound(const float* x, int64_t N, int d, const float* g32, int dp32, const float* inv_norm,
+                                int np, double* mu, unsigned* nb, unsigned* mm, unsigned* flag16, cudaStream_t st);
+cudaError_t launch_proj_spread(const float* x, int64_t N, int d, const float* g32, int dp32, const float* inv_norm,
+                               int np, const float* w, const FPar* fp, const PolyWin& pw, int ncap, float* grid,
+                               const unsigned* flag16, cudaStream_t st);
+// row a5: g[p][l] = sum_n w_n phi_win(v_n - l) over the x projections (ES window, w taps); grid stride n_cap
+cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int ncap, const PolyWin& pw,
+                          bool wide_likely, float* grid, const unsigned* flag16, cudaStream_t st);
+// row a6: h[p] = IFFT_n(D[p] * FFT_n(g[p]))   (unnormalised, one CTA per slice, smem radix-2, n = n_p)
 // also writes the per-cell interpolation polynomials Q[p][c][k] = sum_j h[lminA + c + j] coef[j][k] for the
-// WA cells of the all-points footprint (Q == nullptr: skipped)
-cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int n, float* h, const FPar* fp,
-                              const PolyWin& pw, int WA, float* Q, cudaStream_t st);
+// WA cells of the all-points footprint (Q stride kQStride(n_cap) floats per slice)
+__host__ __device__ inline int64_t q_stride(int ncap) { return static_cast<int64_t>(ncap + 16) * (PW_D + 1); }
+cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int ncap, const FPar* fp, const PolyWin& pw,
+                              float* Q, const unsigned* flag16, cudaStream_t st);
 
 // rows a5 + a7 by the NDFT on the kept band (ndft.cu; the paper's Gaussian engine): KW = padded band
 // width (8, 16 or 32; ndft_width(K) = 0: too wide), what [np][2 KW] fp64 (zeroed by the caller)
-int ndft_width(int K);
-cudaError_t launch_ndft_spread(ZView zv, const float* w, int np, const FPar* fp, int KW, double* what,
+constexpr int kNdftWidth = 32;
+cudaError_t launch_ndft_spread(ZView zv, const float* w, int np, const FPar* fp, double* what, const unsigned* flag16,
                                cudaStream_t st);
-cudaError_t launch_ndft_eval(ZView zv, int np, const FPar* fp, const float* D, int nh, int KW, const double* what,
-                             double* s64, float* per_slice_out, bool accumulate_out, cudaStream_t st);
+cudaError_t launch_ndft_eval(ZView zv, int np, const FPar* fp, const float* D, int dstride, const double* what,
+                             double* s64, float* per_slice_out, bool accumulate_out, const unsigned* flag16,
+                             cudaStream_t st);
 
 // row a7 (+ Laplacian moment term) + slice accumulation:
 //   per y_m: acc = sum_p [ Fourier interp + mom_coef * tau_p * S_moment ]
@@ -155,11 +195,10 @@ struct EvalArgs {
   // Fourier part
   bool fourier;
   const FPar* fp;
-  const float* h;
-  const float* Q;       // [np][WA][PW_D+1] interpolation polynomials (nullptr: per-tap window on h)
-  int WA;
-  PolyWin pw;
-  int n;
+  const float* Q;       // [np][q_stride(ncap)] per-cell interpolation polynomials (launch_fft_filter)
+  int ncap;
+  int w;                // window taps
+  const unsigned* flag16;
   // Laplacian moment part: t += mom_coef * tau_p * sum_n w_n (z_n - z_m)^2
   bool moment;
   double mom_coef;

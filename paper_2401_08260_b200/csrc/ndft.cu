@@ -22,11 +22,13 @@ constexpr int ND_T = 256;
 
 template <int KW>
 __global__ void __launch_bounds__(ND_T) k_ndft_spread(ZView zv, const float* __restrict__ w, const FPar* __restrict__ fp,
-                                                      int64_t chunk, double* __restrict__ what) {
+                                                      int64_t chunk, double* __restrict__ what,
+                                                      const unsigned* __restrict__ flag16) {
   __shared__ float red[ND_T / 32][2 * KW];
+  if (call_failed(flag16)) return;
   const int p = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const FPar f = fp[p];
-  const int klo = f.klo_khi >> 16;
+  const int klo = f.klo;
   const float* zx = zv.zx + p * zv.ldx;
   const int64_t i0 = blockIdx.x * chunk, i1 = min(zv.N, i0 + chunk);
   float are[KW], aim[KW];
@@ -75,22 +77,24 @@ constexpr int NE_T = 256, NE_SG = 32;
 
 template <int KW>
 __global__ void __launch_bounds__(NE_T) k_ndft_eval(ZView zv, int np, const FPar* __restrict__ fp,
-                                                    const float* __restrict__ D, int nh,
+                                                    const float* __restrict__ D, int dstride,
                                                     const double* __restrict__ what, double* __restrict__ s64,
-                                                    float* __restrict__ per_slice_out, bool accumulate_out) {
+                                                    float* __restrict__ per_slice_out, bool accumulate_out,
+                                                    const unsigned* __restrict__ flag16) {
   __shared__ float2 ch[NE_SG][KW];   // (2 - [k = 0]) c_k what_k
   __shared__ float2 pc[NE_SG];       // (tau, cen)
   __shared__ int plo[NE_SG];
+  if (call_failed(flag16)) return;
   const int p0 = blockIdx.y * NE_SG, p1 = min(np, p0 + NE_SG);
   for (int e = threadIdx.x; e < (p1 - p0) * KW; e += NE_T) {
     const int q = e / KW, k = e - q * KW;
     const int p = p0 + q;
     const FPar f = fp[p];
-    const int klo = f.klo_khi >> 16, khi = f.klo_khi & 0xffff;
+    const int klo = f.klo, khi = f.khi;
     const int kk = klo + k;
     float2 v = make_float2(0.f, 0.f);
-    if (kk <= khi && kk < nh) {
-      const double c = static_cast<double>(D[static_cast<int64_t>(p) * nh + kk]) * (kk == 0 ? 1.0 : 2.0);
+    if (kk <= khi) {
+      const double c = static_cast<double>(D[static_cast<int64_t>(p) * dstride + kk]) * (kk == 0 ? 1.0 : 2.0);
       const double* wp = what + static_cast<int64_t>(p) * 2 * KW + 2 * k;
       v = make_float2(static_cast<float>(c * wp[0]), static_cast<float>(c * wp[1]));
     }
@@ -131,47 +135,26 @@ __global__ void __launch_bounds__(NE_T) k_ndft_eval(ZView zv, int np, const FPar
   if (s64) atomicAdd(s64 + m, acc);
 }
 
-template <int KW>
-cudaError_t spread_kw(ZView zv, const float* w, int np, const FPar* fp, double* what, cudaStream_t st) {
+}  // namespace
+
+cudaError_t launch_ndft_spread(ZView zv, const float* w, int np, const FPar* fp, double* what, const unsigned* flag16,
+                               cudaStream_t st) {
+  if (zv.N == 0) return cudaSuccess;
   int64_t chunk = 16384;
   while (chunk > 1024 && ((zv.N + chunk - 1) / chunk) * np < 4 * 148) chunk >>= 1;
   const unsigned nchunk = static_cast<unsigned>((zv.N + chunk - 1) / chunk);
-  k_ndft_spread<KW><<<dim3(nchunk, np), ND_T, 0, st>>>(zv, w, fp, chunk, what);
+  k_ndft_spread<kNdftWidth><<<dim3(nchunk, np), ND_T, 0, st>>>(zv, w, fp, chunk, what, flag16);
   return cudaGetLastError();
 }
 
-template <int KW>
-cudaError_t eval_kw(ZView zv, int np, const FPar* fp, const float* D, int nh, const double* what, double* s64,
-                    float* pso, bool acc, cudaStream_t st) {
+cudaError_t launch_ndft_eval(ZView zv, int np, const FPar* fp, const float* D, int dstride, const double* what,
+                             double* s64, float* per_slice_out, bool accumulate_out, const unsigned* flag16,
+                             cudaStream_t st) {
   const unsigned bx = static_cast<unsigned>((zv.M + NE_T - 1) / NE_T);
   const unsigned by = static_cast<unsigned>((np + NE_SG - 1) / NE_SG);
-  k_ndft_eval<KW><<<dim3(bx, by), NE_T, 0, st>>>(zv, np, fp, D, nh, what, s64, pso, acc);
+  k_ndft_eval<kNdftWidth><<<dim3(bx, by), NE_T, 0, st>>>(zv, np, fp, D, dstride, what, s64, per_slice_out,
+                                                         accumulate_out, flag16);
   return cudaGetLastError();
-}
-
-}  // namespace
-
-int ndft_width(int K) { return K <= 8 ? 8 : (K <= 16 ? 16 : (K <= 32 ? 32 : 0)); }
-
-cudaError_t launch_ndft_spread(ZView zv, const float* w, int np, const FPar* fp, int KW, double* what,
-                               cudaStream_t st) {
-  if (zv.N == 0) return cudaSuccess;
-  switch (KW) {
-    case 8: return spread_kw<8>(zv, w, np, fp, what, st);
-    case 16: return spread_kw<16>(zv, w, np, fp, what, st);
-    case 32: return spread_kw<32>(zv, w, np, fp, what, st);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-cudaError_t launch_ndft_eval(ZView zv, int np, const FPar* fp, const float* D, int nh, int KW, const double* what,
-                             double* s64, float* per_slice_out, bool accumulate_out, cudaStream_t st) {
-  switch (KW) {
-    case 8: return eval_kw<8>(zv, np, fp, D, nh, what, s64, per_slice_out, accumulate_out, st);
-    case 16: return eval_kw<16>(zv, np, fp, D, nh, what, s64, per_slice_out, accumulate_out, st);
-    case 32: return eval_kw<32>(zv, np, fp, D, nh, what, s64, per_slice_out, accumulate_out, st);
-    default: return cudaErrorInvalidValue;
-  }
 }
 
 }  // namespace sks

@@ -21,10 +21,13 @@
 #include <cstring>
 
 #include "kernels.h"
+#include "tc_util.h"
 
 namespace sks {
 
 namespace {
+
+using namespace tc;
 
 constexpr int TC_M = 128;   // points per tile (UMMA M)
 constexpr int TC_BK = 64;   // bf16 elements per k-block = 128 bytes (one swizzle row)
@@ -33,50 +36,6 @@ constexpr int kProjMaxCtas = 148;   // persistent grid: one CTA per SM
 __device__ __forceinline__ unsigned f2key_tc(float f) {
   const unsigned u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-// UMMA shared-memory descriptor, K-major, 128-byte swizzle: SBO = 1024 B (8 rows x 128 B), LBO = 16 B
-// (ignored for swizzled K-major), version 1, layout type 2 (SWIZZLE_128B).
-__device__ __forceinline__ uint64_t umma_desc_sw128(const void* p) {
-  const uint64_t addr = smem_u32(p);
-  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) |
-         (2ull << 61);
-}
-
-// instruction descriptor kind::f16: D f32, A/B bf16, both K-major, N, M
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-         (static_cast<uint32_t>(M >> 4) << 24);
 }
 
 // FP16x2 point scale s = 2^(14 - e), max|x| = m 2^e (m in [0.5, 1)): s max|x| < 2^14 (1 if max|x| = 0)
@@ -107,17 +66,6 @@ __global__ void k_absmax_sample(const float* __restrict__ x, int64_t N, const fl
   if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
 }
 
-// instruction descriptor kind::f16 with fp16 A / B (format 0): D f32, both K-major, N, M
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
-  return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
-}
-
-// instruction descriptor kind::tf32: D f32, A/B tf32, both K-major, N, M
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-         (static_cast<uint32_t>(M >> 4) << 24);
-}
-
 // Stage of the k-loop.  BF16x3 (TF32 = false): three bf16 pieces of 128 points x 64 dims (TMA from the split
 // buffer) + the direction tile.  TF32x2 (TF32 = true): hi / lo tf32 pieces of 128 points x 32 dims written by
 // the converter warps straight from the fp32 points + the fp32 direction tile (TMA).  Rows are 128 bytes,
@@ -136,10 +84,6 @@ struct TcSmem {
   static constexpr int RANGE_OFF = (BAR_OFF + 8 * (3 * STAGES + 4) + 16 + 63) / 64 * 64;   // float4-aligned
   static constexpr int FIXED = RANGE_OFF + 1024;            // + per-CTA range partials [np_pad][4], 1/||g|| + slack
 };
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // min / max of 16 columns (fmn[j] / fmx[j] = this lane's value of column j) over the 32 lanes of a warp by warp
 // reductions (redux.sync f32, sm_100a): lane j (< 16) gets column j's bounds (finite inputs; NaN / Inf are trapped
@@ -169,23 +113,15 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
-// lo piece of TF32x2, rounded to the nearest tf32 (ties to even) instead of being truncated by the tensor core's
-// operand read: the residual |x - hi - lo| <= 2^-11 ulp_tf32(x - hi) is then unbiased.  Truncating lo as well left a
-// one-signed error ~2^-22 |<xi, x>| per projection, i.e. a uniform scale error that the homogeneous negative distance
-// sum turns into ~2^-22 |t| (cfg2: 2.4e-6 of sum |w| at |t| ~ 10)
-__device__ __forceinline__ float tf32_cvt_rn(float x) {
-  uint32_t r;
-  asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
 template <int BN, int STAGES, int MODE = 0>
 __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
     k_proj_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nk, int64_t L,
               int64_t Nx, int np, const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz,
               unsigned* __restrict__ mm, int* __restrict__ flag, const float* __restrict__ px,
               const float* __restrict__ py, int d, const __grid_constant__ CUtensorMap tmX,
-              const __grid_constant__ CUtensorMap tmY, int xtma, const unsigned* __restrict__ f16max) {
+              const __grid_constant__ CUtensorMap tmY, int xtma, const unsigned* __restrict__ f16max,
+              const unsigned* __restrict__ pred) {
+  if (pred && *pred == 0) return;   // predicated launch (the FP16x2 -> TF32x2 rerun): nothing to redo
   using SM = TcSmem<BN, STAGES, MODE>;
   constexpr bool TF32 = MODE == 1, CONV = MODE != 0, F16 = MODE == 3;
   // warp roles: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle; epilogue warps 4 .. 4 + NEPI - 1; converters CW0 .. 15.
@@ -193,7 +129,9 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
   // lane quadrant each) and 8 converter warps (16 rows each)
   constexpr int NEPI = F16 ? 4 : 8, CW0 = F16 ? 8 : 12, NCONV = 16 - CW0, RPW = TC_M / NCONV;
   extern __shared__ unsigned char smraw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  // aligned by pointer arithmetic on the __shared__ array: the compiler keeps the shared state space (LDS / STS,
+  // not generic LD / ST)
+  unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + SM::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;     // [2]
@@ -681,18 +619,6 @@ __global__ void k_split3(const float* __restrict__ x, int64_t N, const float* __
   }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
 bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_k, uint32_t box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
@@ -710,7 +636,7 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int6
                       const float* inv_norm, float* Z, int64_t ldz, unsigned* mm, int* flag, unsigned* part,
                       cudaStream_t st, const float* px = nullptr, const float* py = nullptr, int d = 0,
                       const CUtensorMap* tx = nullptr, const CUtensorMap* ty = nullptr,
-                      const unsigned* f16max = nullptr) {
+                      const unsigned* f16max = nullptr, const unsigned* pred = nullptr) {
   using SM = TcSmem<BN, STAGES, MODE>;
   const int ntn = (np + BN - 1) / BN;
   const size_t smem = SM::FIXED + static_cast<size_t>(20) * ntn * BN;
@@ -720,7 +646,7 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int nk, int6
   const int xtma = tx != nullptr;
   k_proj_tc<BN, STAGES, MODE><<<grid, MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, smem, st>>>(
       ta, tb, nk, L, Nx, np, inv_norm, Z, ldz, mm, flag, px, py, d, xtma ? *tx : ta, xtma ? *ty : ta, xtma,
-      f16max);
+      f16max, pred);
   (void)part;
   return cudaGetLastError();
 }
@@ -766,7 +692,7 @@ int proj_tf32_dpad(int d) { return (d + 31) / 32 * 32; }
 // no split buffer; three k-blocks of 32 dims per 128-byte row pair... see k_proj_tc<.., true>
 cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64_t M, int d,
                                 const float* g32 /* fp32 [np][dp32] */, int np, const float* inv_norm, float* Z,
-                                int64_t ldz, unsigned* mm, int* flag, cudaStream_t st) {
+                                int64_t ldz, unsigned* mm, int* flag, const unsigned* pred, cudaStream_t st) {
   const int dp = proj_tf32_dpad(d);
   const int nk = dp / 32;
   const int64_t L = N + M;
@@ -794,9 +720,9 @@ cudaError_t launch_project_tf32(const float* x, int64_t N, const float* y, int64
     unsigned* mmc = mm + 4 * s0;
     const float* ic = inv_norm + s0;
     cudaError_t e;
-    if (BN == 256) e = launch_tc<256, 3, 1>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
-    else if (BN == 128) e = launch_tc<128, 4, 1>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
-    else e = launch_tc<64, 4, 1>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty);
+    if (BN == 256) e = launch_tc<256, 3, 1>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty, nullptr, pred);
+    else if (BN == 128) e = launch_tc<128, 4, 1>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty, nullptr, pred);
+    else e = launch_tc<64, 4, 1>(ta, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, ptx, pty, nullptr, pred);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -478,7 +478,7 @@ def test_async_status_reports_errors():
 
 # ---------------------------------------------------------------- rows a1 + a5 fused (large N, Fourier kernels)
 @pytest.mark.parametrize("kind,scale,d,N,M,P", [("gaussian", 30.0, 100, 300_001, 3000, 150),
-                                                ("matern", 6.0, 52, 262_144 + 77, 1500, 33),
+                                                ("matern", 20.0, 52, 262_144 + 77, 1500, 33),
                                                 ("gaussian", 2.0, 8, 400_000, 2000, 20)])
 def test_fused_projection_spread(kind, scale, d, N, M, P):
     # N >= 2^18, d <= 128, d % 4 == 0: the sources' projections are spread from the tensor-core accumulators
