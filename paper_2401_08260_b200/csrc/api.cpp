@@ -166,9 +166,11 @@ struct Layout {
          what = 0, bound = 0, total = 0;
 };
 
-// rows a1 + a5 fused (fused.cu) for the Fourier-only kernels when the sources are many: their projections are
-// spread from the tensor-core accumulators and never stored; only the targets' projections go through HBM.  The
-// decision depends on the problem's shape only (never on data), so the workspace size is known up front.
+// rows a1 + a5 and a1 + a7 fused (fused.cu) for the Fourier-only kernels when the points are many: the sources'
+// projections are spread and the targets' interpolated straight from the tensor-core accumulators; no projection
+// is stored.  The decision depends on the problem's shape only (never on data), so the workspace size is known up
+// front (the run-time conditions -- TMA-readable points -- fall back to the stored-projection path, whose
+// workspace the layout then also holds).
 constexpr int64_t kFusedMinN = 1 << 18;
 bool fused_shape(int64_t N, int d, Path pt, bool with_Z, int w) {
   return with_Z && pt.fourier && !pt.sort && N >= kFusedMinN && d <= 128 && d % 4 == 0 && (w % 2) == 0 && w >= 4;
@@ -232,7 +234,7 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, 
   L.s64 = take(sizeof(double) * M);
   L.mm = take(sizeof(unsigned) * 4 * nbat);
   if (with_Z) {
-    L.Z = take(sizeof(float) * (fused ? zld(0, M) : zld(N, M)) * nbat);   // fused: the targets' block only
+    L.Z = take(sizeof(float) * zld(N, M) * nbat);   // (fused calls do not touch it unless they fall back)
     if (proj_mode(d, proj) == PM_BF16X3) {
       L.xs3 = take(sizeof(uint16_t) * 3 * static_cast<size_t>(sks::proj_tc_dpad(d)) * (N + M));
       L.part = take(sks::proj_tc_part_bytes(nbat));
@@ -463,7 +465,7 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
   const ProjMode pm = pr.with_Z ? proj_mode_call(pr.d, o.proj, x, pr.N, y, pr.M) : PM_AUTO;
   // fused path: the shape qualifies, the points are TMA-readable, and the projection is TF32x2 (the variant the
   // fused kernel computes; d <= 128)
-  const bool fused = fshape && pm == PM_TF32X2 && sks::fused_spread_ok(pr.d, x) && sks::proj_tf32_tma_ok(y, pr.M, y, 0, pr.d);
+  const bool fused = fshape && pm == PM_TF32X2 && s_out && sks::fused_spread_ok(pr.d, x) && sks::fused_spread_ok(pr.d, y);
   const bool tc = pr.with_Z && pm == PM_BF16X3;
   const bool tf = pr.with_Z && pm == PM_TF32X2;
   const bool th = pr.with_Z && pm == PM_FP16X2;
@@ -483,14 +485,8 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
       ++launches;
     }
     sks::ZView zv;
-    if (fused) {   // the targets' projections (and their exact ranges) only; the sources are projected below
-      float* Z = reinterpret_cast<float*>(ws + L.Z);
-      const int64_t ldz = zld(0, pr.M);
-      ProfScope ps(PS_PROJECT, st);
-      SKS_CUDA(sks::launch_project_tf32(y, pr.M, y, 0, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, nbat,
-                                        dirs->inv + b0, Z, ldz, mm, flag, nullptr, st));
-      launches += (nbat + 1023) / 1024;
-      zv = sks::ZView{nullptr, Z, 0, ldz, pr.N, pr.M};
+    if (fused) {   // nothing stored: both point sets are projected inside the fused kernels below
+      zv = sks::ZView{nullptr, nullptr, 0, 0, pr.N, pr.M};
     } else if (pr.with_Z) {
       float* Z = reinterpret_cast<float*>(ws + L.Z);
       const int64_t ldz = zld(pr.N, pr.M);
@@ -552,11 +548,11 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
       if (fused) {   // the sources' range bound in place of their exact ranges (fused.cu)
         ProfScope ps(PS_MINMAX, st);
         double* mu = reinterpret_cast<double*>(ws + L.bound);
-        SKS_CUDA(sks::launch_source_bound(x, pr.N, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
-                                          dirs->inv + b0, nbat, mu,
-                                          reinterpret_cast<unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 16),
+        SKS_CUDA(sks::launch_source_bound(x, pr.N, y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32,
+                                          dirs->K32, dirs->inv + b0, nbat, mu,
+                                          reinterpret_cast<unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32),
                                           mm, flag16, st));
-        launches += 3;
+        launches += 5;
       }
       {
         ProfScope ps(PS_PLAN, st);
@@ -609,7 +605,12 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
     ea.s64 = s64;
     ea.per_slice_out = tps;
     ea.accumulate_out = pt.sort;
-    if (pt.fourier || pt.moment) {
+    if (fused) {
+      ProfScope ps(PS_EVAL, st);
+      SKS_CUDA(sks::launch_proj_eval(y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
+                                     dirs->inv + b0, nbat, ea.fp, ea.Q, kNcap, o.w, s64, flag16, st));
+      ++launches;
+    } else if (pt.fourier || pt.moment) {
       ProfScope ps(PS_EVAL, st);
       SKS_CUDA(sks::launch_eval(ea, st));
       ++launches;

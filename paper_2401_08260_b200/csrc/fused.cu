@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(128) k_sample_mean_part(const float* __restric
   }
 }
 
-// mu[j] = (sum over the parts, in order) / S; also zeroes the norm-bound words nb[0..3]
+// mu[j] = (sum over the parts, in order) / S; also zeroes the norm-bound words nb[0..7]
 __global__ void k_sample_mean_fin(int64_t N, int d, const double* __restrict__ part, double* __restrict__ mu,
                                   unsigned* __restrict__ nb) {
   const int S = static_cast<int>(N < MEAN_ROWS ? N : MEAN_ROWS);
@@ -54,7 +54,7 @@ __global__ void k_sample_mean_fin(int64_t N, int d, const double* __restrict__ p
     for (int g = 0; g < MEAN_PARTS; ++g) s += part[static_cast<int64_t>(g) * d + j];
     mu[j] = s / S;
   }
-  if (threadIdx.x < 4) nb[threadIdx.x] = 0u;
+  if (threadIdx.x < 8) nb[threadIdx.x] = 0u;
 }
 
 // one warp per row (d <= 128: one float4 per lane), fp32 sums of squares, maxima as float bits (non-negative
@@ -110,12 +110,20 @@ __device__ __forceinline__ float key2f_fu(unsigned k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-// one warp per slice: c_p = <g_p, mu> inv_p (fp64), rho' = rho (1 + 2^-10) + 2^-19 nmax: the fp32 sums of squares
-// (relative error <= d 2^-24 <= 2^-17 for d <= 128, halved by the root) and the projection's error (<= 2^-21 ||x||,
-// DESIGN.md R2) are far inside these margins.  mm[p] = {xmin, xmax, allmin, allmax}: x from the bound, all =
-// x bound and the targets' exact range (their projection epilogue wrote it into mm[p][2..3])
+// rho' = rho (1 + 2^-10) + 2^-19 nmax from the norm words {max ||z - mu||^2, max ||z||^2}: the fp32 sums of squares
+// (relative error <= d 2^-24 <= 2^-17 for d <= 128, halved by the root) and the projection's error (<= 2^-21 ||z||,
+// DESIGN.md R2) are far inside these margins
+__device__ __forceinline__ double bound_radius(const unsigned* nb) {
+  return sqrt(static_cast<double>(__uint_as_float(nb[0]))) * (1.0 + 0x1p-10) +
+         sqrt(static_cast<double>(__uint_as_float(nb[1]))) * 0x1p-19;
+}
+
+// one warp per slice: c_p = <g_p, mu> inv_p (fp64); every projection of the bounded set lies in [c_p - rho',
+// c_p + rho'] (Cauchy-Schwarz, ||xi_p|| = 1).  mm[p] = {xmin, xmax, allmin, allmax}: x from its bound (nb[0..2]);
+// all = the hull of the x bound and either the targets' bound (ybound: nb[4..6]) or their exact range (their
+// projection epilogue wrote it into mm[p][2..3])
 __global__ void k_bound_ranges(const float* __restrict__ g32, int dp32, int d, const float* __restrict__ inv_norm,
-                               int np, const double* __restrict__ mu, const unsigned* __restrict__ nb,
+                               int np, const double* __restrict__ mu, const unsigned* __restrict__ nb, int ybound,
                                unsigned* __restrict__ mm, unsigned* __restrict__ flag16) {
   const int lane = threadIdx.x & 31;
   const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -125,16 +133,23 @@ __global__ void k_bound_ranges(const float* __restrict__ g32, int dp32, int d, c
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane) return;
-  if (nb[2]) {
+  if (nb[2] || (ybound && nb[6])) {
     atomicOr(flag16, 1u);
     return;
   }
   const double c = s * static_cast<double>(inv_norm[p]);
-  const double rho = sqrt(static_cast<double>(__uint_as_float(nb[0]))) * (1.0 + 0x1p-10) +
-                     sqrt(static_cast<double>(__uint_as_float(nb[1]))) * 0x1p-19;
-  const float lo = static_cast<float>(c - rho), hi = static_cast<float>(c + rho);
-  const float xlo = nextafterf(lo, -CUDART_INF_F), xhi = nextafterf(hi, CUDART_INF_F);
-  const float ymn = key2f_fu(mm[4 * p + 2]), ymx = key2f_fu(mm[4 * p + 3]);
+  const double rx = bound_radius(nb);
+  const float xlo = nextafterf(static_cast<float>(c - rx), -CUDART_INF_F);
+  const float xhi = nextafterf(static_cast<float>(c + rx), CUDART_INF_F);
+  float ymn, ymx;
+  if (ybound) {
+    const double ry = bound_radius(nb + 4);
+    ymn = nextafterf(static_cast<float>(c - ry), -CUDART_INF_F);
+    ymx = nextafterf(static_cast<float>(c + ry), CUDART_INF_F);
+  } else {
+    ymn = key2f_fu(mm[4 * p + 2]);
+    ymx = key2f_fu(mm[4 * p + 3]);
+  }
   mm[4 * p + 0] = f2key_fu(xlo);
   mm[4 * p + 1] = f2key_fu(xhi);
   mm[4 * p + 2] = f2key_fu(fminf(xlo, ymn));
@@ -144,9 +159,9 @@ __global__ void k_bound_ranges(const float* __restrict__ g32, int dp32, int d, c
 // ------------------------------------------------------------------ the fused projection + spread
 constexpr int FS_S = 128;          // slices per tile (UMMA M = TMEM lanes)
 constexpr int FS_P = 128;          // points per tile (UMMA N)
-constexpr int FS_STAGES = 2;
+constexpr int FS_STAGES = 3;
 constexpr int FS_KBMAX = 4;        // k-blocks of 32 dims: d <= 128
-constexpr int FS_WCAP = 40;        // private grid cells per slice (wider footprints: global atomics)
+constexpr int FS_WCAP = 32;        // private grid cells per slice (wider footprints: global atomics)
 constexpr int FS_EPI = 16;         // epilogue warps: 4 per TMEM lane quadrant, 32 points of the tile each
 constexpr int FS_THREADS = 32 * (8 + FS_EPI);   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 -, w4..w7 converters, epilogue
 constexpr int FS_PIECE = FS_P * 128;                      // one k-block of 128 points: 16 KB
@@ -155,6 +170,7 @@ constexpr int FS_OFF_STAGE = FS_KBMAX * FS_A;             // 64 KB of resident d
 constexpr int FS_OFF_GRID = FS_OFF_STAGE + FS_STAGES * 2 * FS_PIECE;
 constexpr int FS_OFF_BAR = FS_OFF_GRID + (FS_EPI / 4) * FS_WCAP * FS_S * 4;
 constexpr int FS_SMEM = FS_OFF_BAR + 256 + 1024;          // + barriers, TMEM slot, alignment slack
+static_assert(FS_SMEM <= 227 * 1024, "k_proj_spread shared memory");
 
 template <int WT>
 __global__ void __launch_bounds__(FS_THREADS, 1)
@@ -306,15 +322,21 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     const bool wide = W > FS_WCAP;   // (footprint beyond the private column: global atomics for this slice)
     float* col = priv + (h * FS_WCAP) * FS_S + 32 * q + lane;   // cell c at col[c * FS_S]
     float* gp = grid + static_cast<int64_t>(live ? p : 0) * ncap;
+    // window coefficients through shared memory into registers (read from the parameter bank, ptxas would
+    // re-load them inside the loop)
+    float* eos = reinterpret_cast<float*>(sm + FS_OFF_BAR + 128);   // [WT / 2][8]
+    if (warp == 8 && lane < WT / 2 * 8) eos[lane] = pw.eo[lane / 8][lane % 8];
+    asm volatile("bar.sync 1, %0;" ::"r"(FS_EPI * 32) : "memory");
     float E[WT / 2][4], O[WT / 2][4];
 #pragma unroll
     for (int j = 0; j < WT / 2; ++j)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        E[j][k] = pw.eo[j][k];
-        O[j][k] = pw.eo[j][4 + k];
+        E[j][k] = eos[8 * j + k];
+        O[j][k] = eos[8 * j + 4 + k];
       }
     const int cmax = W - WT;   // last admissible first-tap cell (relative to lmin)
+    const bool fast = live && !wide;   // (dead lanes of the last slice tile and wide footprints: the slow loop)
     // the weights of the warp's 32 points, one per lane, loaded one tile ahead (software pipelined: a global load's
     // latency would otherwise stall the epilogue warps at every tile)
     auto wload = [&](int64_t t) {
@@ -331,48 +353,59 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
       wnext = wload(t + 1);
       mbar_wait(&tfull[b], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      uint32_t v[32];
       const uint32_t taddr = tmem_base + static_cast<uint32_t>(b * FS_P + c0) + (static_cast<uint32_t>(32 * q) << 16);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-          "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      // the accumulator is in registers: release it to the MMAs of tile t + 2 before spreading
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
       const int nj = (N - i0 < 32) ? static_cast<int>(N - i0) : 32;
+#pragma unroll 1
+      for (int j0 = 0; j0 < 32; j0 += 8) {   // 8 columns (points) per TMEM load: few registers held
+        uint32_t v[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "r"(taddr + j0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float w8[8];   // the 8 points' weights (shuffled by the whole warp before any lane-dependent branch)
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float wi = __shfl_sync(0xffffffffu, wv, j);
-        if (j < nj && live) {
-          const float a = fmaf(__uint_as_float(v[j]), ga, gb), fl = floorf(a);
-          const float u = (a - fl) - 0.5f, u2 = u * u;
-          int cl = static_cast<int>(fl) + 1 - f.lmin;
-          cl = cl < 0 ? 0 : (cl > cmax ? cmax : cl);   // (a valid bound never clamps; memory safety only)
-          float tw[WT];
+        for (int jj = 0; jj < 8; ++jj) {
+          const float t = __shfl_sync(0xffffffffu, wv, j0 + jj);
+          w8[jj] = j0 + jj < nj ? t : 0.f;
+        }
+        if (fast) {
+          // branch-free: points beyond N carry weight 0 (their rows are zero-filled by TMA; the clamp keeps their
+          // cell in range)
 #pragma unroll
-          for (int m = 0; m < WT / 2; ++m) {
-            const float Em = fmaf(fmaf(fmaf(E[m][3], u2, E[m][2]), u2, E[m][1]), u2, E[m][0]);
-            const float Om = fmaf(fmaf(fmaf(O[m][3], u2, O[m][2]), u2, O[m][1]), u2, O[m][0]);
-            tw[m] = fmaf(u, Om, Em);
-            tw[WT - 1 - m] = fmaf(-u, Om, Em);
-          }
-          if (!wide) {
+          for (int jj = 0; jj < 8; ++jj) {
+            const float wi = w8[jj];
+            const float a = fmaf(__uint_as_float(v[jj]), ga, gb), fl = floorf(a);
+            const float u = (a - fl) - 0.5f, u2 = u * u;
+            const int cl = min(max(static_cast<int>(fl) + 1 - f.lmin, 0), cmax);   // (memory safety only)
             float* cell = col + cl * FS_S;
 #pragma unroll
-            for (int m = 0; m < WT; ++m) cell[m * FS_S] = fmaf(wi, tw[m], cell[m * FS_S]);
-          } else {
-#pragma unroll
-            for (int m = 0; m < WT; ++m) atomicAdd(&gp[(f.lmin + cl + m) & (n - 1)], wi * tw[m]);
+            for (int m = 0; m < WT / 2; ++m) {
+              const float Em = fmaf(fmaf(fmaf(E[m][3], u2, E[m][2]), u2, E[m][1]), u2, E[m][0]);
+              const float Om = fmaf(fmaf(fmaf(O[m][3], u2, O[m][2]), u2, O[m][1]), u2, O[m][0]);
+              cell[m * FS_S] = fmaf(wi, fmaf(u, Om, Em), cell[m * FS_S]);
+              cell[(WT - 1 - m) * FS_S] = fmaf(wi, fmaf(-u, Om, Em), cell[(WT - 1 - m) * FS_S]);
+            }
+          }
+        } else if (live) {   // footprint wider than the private column: global atomics for this slice
+          for (int jj = 0; jj < 8; ++jj) {
+            const float wi = w8[jj];
+            if (j0 + jj >= nj) continue;
+            const float a = fmaf(__uint_as_float(v[jj]), ga, gb), fl = floorf(a);
+            const float u = (a - fl) - 0.5f, u2 = u * u;
+            const int cl = min(max(static_cast<int>(fl) + 1 - f.lmin, 0), cmax);
+            for (int m = 0; m < WT / 2; ++m) {
+              const float Em = fmaf(fmaf(fmaf(E[m][3], u2, E[m][2]), u2, E[m][1]), u2, E[m][0]);
+              const float Om = fmaf(fmaf(fmaf(O[m][3], u2, O[m][2]), u2, O[m][1]), u2, O[m][0]);
+              atomicAdd(&gp[(f.lmin + cl + m) & (n - 1)], wi * fmaf(u, Om, Em));
+              atomicAdd(&gp[(f.lmin + cl + WT - 1 - m) & (n - 1)], wi * fmaf(-u, Om, Em));
+            }
           }
         }
       }
+      // the accumulator is read: release it to the MMAs of tile t + 2
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -398,6 +431,248 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * FS_P));
 }
 
+// ------------------------------------------------------------------ the fused projection + interpolation
+// Rows a1 + a7 for the TARGETS: persistent, one CTA per (slice group of 64, range of 128-point target tiles);
+// A = the target tile (TMA, TF32x2 as above), B = the group's directions (resident), tcgen05.mma M = 128 targets x
+// N = 64 slices into double-buffered TMEM (TMEM lane = target).  The group's interpolation polynomials Q (written by
+// k_fft_filter) are staged in shared memory once; an epilogue thread owns one target and 16 of the group's slices:
+// per slice one FMA for the grid coordinate, one 32-byte polynomial lookup (the lanes of a warp read the same
+// slice's table: broadcasts), one degree-7 Horner.  The four partial sums of a target (16 slices each) are added
+// in shared memory and the group's sum goes to the target's fp64 accumulator with one atomic.
+constexpr int FE_T = 128;          // targets per tile (UMMA M)
+constexpr int FE_S = 64;           // slices per group (UMMA N)
+constexpr int FE_STAGES = 3;
+constexpr int FE_QCAP = 40;        // cells of interpolation polynomials staged per slice (wider: read from global)
+constexpr int FE_EPI = 16;         // epilogue warps: 4 per TMEM lane quadrant, 16 slices each
+constexpr int FE_THREADS = 32 * (8 + FE_EPI);
+constexpr int FE_PIECE = FE_T * 128;                      // one k-block of 128 targets: 16 KB
+constexpr int FE_B = FE_S * 128;                          // one k-block of the group's directions: 8 KB
+constexpr int FE_OFF_STAGE = FS_KBMAX * FE_B;             // 32 KB of resident directions
+constexpr int FE_OFF_Q = FE_OFF_STAGE + FE_STAGES * 2 * FE_PIECE;
+constexpr int FE_OFF_SP = FE_OFF_Q + FE_S * FE_QCAP * 32;            // per-slice constants float4 [FE_S]
+constexpr int FE_OFF_RED = FE_OFF_SP + FE_S * 16;                    // partial sums [2][4][FE_T] fp32
+constexpr int FE_OFF_BAR = FE_OFF_RED + 2 * 4 * FE_T * 4;
+constexpr int FE_SMEM = FE_OFF_BAR + 256 + 1024;
+static_assert(FE_SMEM <= 227 * 1024, "k_proj_eval shared memory");
+
+// position of cell c in a slice's staged table: 16-byte entries, cells 8a + b stored at 8a + (b ^ (a & 7)), so that
+// the cells of a contiguous range fall into different 4-bank groups (a plain layout puts c and c + 8 in the same one)
+__device__ __forceinline__ int qswz(int c) { return c ^ ((c >> 3) & 7); }
+
+__global__ void __launch_bounds__(FE_THREADS, 1)
+    k_proj_eval(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY, int nk, int64_t M,
+                int np, int ranges, const float* __restrict__ inv_norm, const FPar* __restrict__ fp,
+                const float* __restrict__ Q, int ncap, int w, double* __restrict__ s64,
+                const unsigned* __restrict__ flag16) {
+  if (call_failed(flag16)) return;
+  extern __shared__ unsigned char feraw[];
+  // aligned by pointer arithmetic on the __shared__ array (shared state space kept: LDS / STS)
+  unsigned char* sm = feraw + ((1024u - (smem_u32(feraw) & 1023u)) & 1023u);
+  float4* sq = reinterpret_cast<float4*>(sm + FE_OFF_Q);   // [2][FE_S][FE_QCAP]: coefficients 0-3 | 4-7 of a cell
+  float4* sp = reinterpret_cast<float4*>(sm + FE_OFF_SP);  // (ga, gb, -, -) per slice; .z = int bits of lminA, .w = WQ
+  float* red = reinterpret_cast<float*>(sm + FE_OFF_RED);  // [2][4][FE_T]
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(sm + FE_OFF_BAR);
+  uint64_t* xfull = bfull + 1;
+  uint64_t* full = xfull + FE_STAGES;
+  uint64_t* empty = full + FE_STAGES;
+  uint64_t* tfull = empty + FE_STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ngroups = (np + FE_S - 1) / FE_S;
+  const int g = blockIdx.x % ngroups, r = blockIdx.x / ngroups;
+  const int s0 = g * FE_S;
+  const int64_t ntt = (M + FE_T - 1) / FE_T;
+  const int64_t t0 = r * ntt / ranges, t1 = (r + 1) * ntt / ranges;
+  const int64_t qs = q_stride(ncap);
+
+  // the group's per-slice constants and interpolation polynomials (all threads)
+  for (int ls = threadIdx.x; ls < FE_S; ls += FE_THREADS) {
+    const int p = s0 + ls;
+    float4 c = make_float4(0.f, 0.f, __int_as_float(0), __int_as_float(0));
+    if (p < np) {
+      const FPar f = fp[p];
+      const float taun = f.tau * static_cast<float>(1 << f.logn);
+      c = make_float4(inv_norm[p] * taun, -fmaf(f.cen, taun, 0.5f * w), __int_as_float(f.lminA), __int_as_float(f.WA));
+    }
+    sp[ls] = c;
+  }
+  // (two planes: the lanes of a warp read one slice's table at ~16 distinct cells, 16-byte cell stride per plane:
+  // at most two lanes' cells share a bank group, half the wavefronts of the 32-byte interleaved layout)
+  for (int e = threadIdx.x; e < FE_S * FE_QCAP * 2; e += FE_THREADS) {
+    const int ls = e / (FE_QCAP * 2), rem = e - ls * FE_QCAP * 2, cell = rem >> 1, half = rem & 1;
+    const int p = s0 + ls;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p < np && cell < fp[p].WA) v = __ldg(reinterpret_cast<const float4*>(Q + p * qs + cell * 8) + half);
+    sq[(half * FE_S + ls) * FE_QCAP + qswz(cell)] = v;
+  }
+  if (warp == 0 && lane == 0) {
+    mbar_init(bfull, 1);
+    for (int s = 0; s < FE_STAGES; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&full[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], FE_EPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * FE_S));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer: the group's directions once, then the raw fp32 target tiles (the hi piece)
+    mbar_expect_tx(bfull, nk * FE_B);
+    for (int kb = 0; kb < nk; ++kb) tma_load_2d(&tmB, bfull, sm + kb * FE_B, kb * 32, s0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = t0; t < t1; ++t)
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char* sa = sm + FE_OFF_STAGE + stage * 2 * FE_PIECE;
+        mbar_expect_tx(&xfull[stage], FE_PIECE);
+        tma_load_2d(&tmY, &xfull[stage], sa, kb * 32, static_cast<int>(t * FE_T));
+        if (++stage == FE_STAGES) { stage = 0; phase ^= 1; }
+      }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer: D[target][slice] += A (hi, then lo) . B (directions, tf32-exact)
+    constexpr uint32_t idesc = idesc_tf32(FE_T, FE_S);
+    mbar_wait(bfull, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      const int b = it & 1;
+      mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(b * FE_S);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const unsigned char* sa = sm + FE_OFF_STAGE + stage * 2 * FE_PIECE;
+        const uint64_t db = umma_desc_sw128(sm + kb * FE_B);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint64_t da = umma_desc_sw128(sa + q * FE_PIECE);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t acc = (kb > 0 || q > 0 || k > 0) ? 1u : 0u;
+            const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[stage]))
+                     : "memory");
+        if (++stage == FE_STAGES) { stage = 0; phase ^= 1; }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&tfull[b]))
+                   : "memory");
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---- converters: lo = rn_tf32(x - trunc_tf32(x)) (as in k_proj_spread)
+    const int cw = warp - 4, c = lane & 7, rsub = lane >> 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = t0; t < t1; ++t)
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&xfull[stage], phase);
+        unsigned char* sa = sm + FE_OFF_STAGE + stage * 2 * FE_PIECE;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = 32 * cw + 4 * i + rsub;
+          const int off = row * 128 + ((c ^ (row & 7)) << 4);
+          const float4 v = *reinterpret_cast<const float4*>(sa + off);
+          const float4 lo = make_float4(tf32_cvt_rn(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u)),
+                                        tf32_cvt_rn(v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u)),
+                                        tf32_cvt_rn(v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u)),
+                                        tf32_cvt_rn(v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u)));
+          *reinterpret_cast<float4*>(sa + FE_PIECE + off) = lo;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == FE_STAGES) { stage = 0; phase ^= 1; }
+      }
+  } else if (warp >= 8) {
+    // ---- epilogue: warp w owns TMEM lane quadrant q = w % 4 (targets 32 q + lane of the tile) and the 16 slices
+    //      h = (w - 8) / 4 of the group
+    const int q = warp & 3, h = (warp - 8) >> 2;
+    int it = 0;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      const int b = it & 1;
+      mbar_wait(&tfull[b], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      uint32_t v[16];
+      const uint32_t taddr = tmem_base + static_cast<uint32_t>(b * FE_S + 16 * h) + (static_cast<uint32_t>(32 * q) << 16);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+          "%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int ls = 16 * h + j;
+        const float4 c = sp[ls];   // broadcast
+        const float a = fmaf(__uint_as_float(v[j]), c.x, c.y), fl = floorf(a);
+        int cl = static_cast<int>(fl) + 1 - __float_as_int(c.z);
+        const int wq = __float_as_int(c.w);
+        cl = cl < 0 ? 0 : (cl >= wq ? wq - 1 : cl);   // (a valid bound never clamps; memory safety only)
+        float4 c0, c1;
+        if (wq <= FE_QCAP) {
+          c0 = sq[ls * FE_QCAP + qswz(cl)];
+          c1 = sq[(FE_S + ls) * FE_QCAP + qswz(cl)];
+        } else {   // footprint wider than the staged table: the polynomial from global memory
+          const float4* qp = reinterpret_cast<const float4*>(Q + (s0 + ls) * qs + cl * 8);
+          c0 = __ldg(qp);
+          c1 = __ldg(qp + 1);
+        }
+        const float fr = a - fl;
+        float tv = fmaf(c1.w, fr, c1.z);
+        tv = fmaf(tv, fr, c1.y);
+        tv = fmaf(tv, fr, c1.x);
+        tv = fmaf(tv, fr, c0.w);
+        tv = fmaf(tv, fr, c0.z);
+        tv = fmaf(tv, fr, c0.y);
+        tv = fmaf(tv, fr, c0.x);
+        acc += (s0 + ls < np) ? tv : 0.f;
+      }
+      float* rb = red + (b * 4) * FE_T;
+      rb[h * FE_T + 32 * q + lane] = acc;
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");   // the quadrant's four partial sums of the tile
+      if (h == 0) {
+        const int64_t m = t * FE_T + 32 * q + lane;
+        const double sum = static_cast<double>(rb[32 * q + lane]) + rb[FE_T + 32 * q + lane] +
+                           rb[2 * FE_T + 32 * q + lane] + rb[3 * FE_T + 32 * q + lane];
+        if (m < M) atomicAdd(s64 + m, sum);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * FE_S));
+}
+
 bool encode_f32_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                     uint32_t box_rows) {
   auto enc = get_encode();
@@ -413,21 +688,26 @@ bool encode_f32_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t co
 
 }  // namespace
 
-size_t source_bound_bytes(int d) { return sizeof(double) * static_cast<size_t>(d) * (1 + MEAN_PARTS) + 16; }
+size_t source_bound_bytes(int d) { return sizeof(double) * static_cast<size_t>(d) * (1 + MEAN_PARTS) + 32; }
 
 bool fused_spread_ok(int d, const float* x) {
   return d <= 32 * FS_KBMAX && d % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
 }
 
-cudaError_t launch_source_bound(const float* x, int64_t N, int d, const float* g32, int dp32, const float* inv_norm,
-                                int np, double* mu, unsigned* nb, unsigned* mm, unsigned* flag16, cudaStream_t st) {
+cudaError_t launch_source_bound(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g32, int dp32,
+                                const float* inv_norm, int np, double* mu, unsigned* nb, unsigned* mm, unsigned* flag16,
+                                cudaStream_t st) {
   double* part = mu + d;   // [MEAN_PARTS][d] scratch after mu (source_bound_bytes)
   k_sample_mean_part<<<MEAN_PARTS, 128, 0, st>>>(x, N, d, part);
   k_sample_mean_fin<<<1, 128, 0, st>>>(N, d, part, mu, nb);
-  int64_t blocks = (N * 32 / 4 + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  k_norm_bound<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, N, d, mu, nb);
-  k_bound_ranges<<<(np + 7) / 8, 256, 0, st>>>(g32, dp32, d, inv_norm, np, mu, nb, mm, flag16);
+  auto norms = [&](const float* z, int64_t n, unsigned* out) {
+    int64_t blocks = (n * 32 / 4 + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_norm_bound<<<static_cast<unsigned>(blocks), 256, 0, st>>>(z, n, d, mu, out);
+  };
+  norms(x, N, nb);
+  if (y) norms(y, M, nb + 4);
+  k_bound_ranges<<<(np + 7) / 8, 256, 0, st>>>(g32, dp32, d, inv_norm, np, mu, nb, y ? 1 : 0, mm, flag16);
   return cudaGetLastError();
 }
 
@@ -458,6 +738,30 @@ cudaError_t launch_proj_spread(const float* x, int64_t N, int d, const float* g3
     case 12: go(k_proj_spread<12>); break;
     default: return cudaErrorInvalidValue;   // (odd widths: the unfused path)
   }
+  return cudaGetLastError();
+}
+
+}  // namespace sks
+
+namespace sks {
+
+cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32, int dp32, const float* inv_norm, int np,
+                             const FPar* fp, const float* Q, int ncap, int w, double* s64, const unsigned* flag16,
+                             cudaStream_t st) {
+  CUtensorMap tmB, tmY;
+  const int nk = dp32 / 32;
+  if (!encode_f32_map(&tmB, g32, static_cast<uint64_t>(np), static_cast<uint64_t>(dp32), static_cast<uint64_t>(dp32),
+                      FE_S) ||
+      !encode_f32_map(&tmY, y, static_cast<uint64_t>(M), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FE_T))
+    return cudaErrorInvalidValue;
+  const int ngroups = (np + FE_S - 1) / FE_S;
+  const int64_t ntt = (M + FE_T - 1) / FE_T;
+  int ranges = 148 / ngroups;
+  if (ranges < 1) ranges = 1;
+  if (ranges > ntt) ranges = static_cast<int>(ntt);
+  set_smem_attr_once(reinterpret_cast<const void*>(k_proj_eval), FE_SMEM);
+  k_proj_eval<<<ngroups * ranges, FE_THREADS, FE_SMEM, st>>>(tmB, tmY, nk, M, np, ranges, inv_norm, fp, Q, ncap, w, s64,
+                                                            flag16);
   return cudaGetLastError();
 }
 

@@ -160,12 +160,18 @@ cudaError_t launch_plan(const unsigned* mm, int np, const PlanConst& pc, const f
 // with the targets' exact range mm[p][2..3] (mu: source_bound_bytes(d) of scratch, nb: its last 16 bytes); then launch_plan,
 // then launch_proj_spread in place of the projection of x + launch_spread
 bool fused_spread_ok(int d, const float* x);
-size_t source_bound_bytes(int d);   // scratch of launch_source_bound: mu, partial sums, nb
-cudaError_t launch_source_bound(const float* x, int64_t N, int d, const float* g32, int dp32, const float* inv_norm,
-                                int np, double* mu, unsigned* nb, unsigned* mm, unsigned* flag16, cudaStream_t st);
+size_t source_bound_bytes(int d);   // scratch of launch_source_bound: mu, partial sums, nb (32 bytes, at the end)
+cudaError_t launch_source_bound(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g32, int dp32,
+                                const float* inv_norm, int np, double* mu, unsigned* nb, unsigned* mm, unsigned* flag16,
+                                cudaStream_t st);
 cudaError_t launch_proj_spread(const float* x, int64_t N, int d, const float* g32, int dp32, const float* inv_norm,
                                int np, const float* w, const FPar* fp, const PolyWin& pw, int ncap, float* grid,
                                const unsigned* flag16, cudaStream_t st);
+// rows a1 + a7 fused for the targets (fused.cu): projections of y interpolated from the tensor-core accumulators,
+// s64[m] += sum over the slices of t_{m,p} (after launch_fft_filter wrote Q)
+cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32, int dp32, const float* inv_norm, int np,
+                             const FPar* fp, const float* Q, int ncap, int w, double* s64, const unsigned* flag16,
+                             cudaStream_t st);
 // row a5: g[p][l] = sum_n w_n phi_win(v_n - l) over the x projections (ES window, w taps); grid stride n_cap
 cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int ncap, const PolyWin& pw,
                           bool wide_likely, float* grid, const unsigned* flag16, cudaStream_t st);
