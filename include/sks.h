@@ -84,6 +84,10 @@ typedef struct {
                             3 = FP16x2 (falls back to TF32x2 where it cannot run); auto picks by d and alignment   */
   int32_t async;         /* [0] 1: return right after enqueueing (no synchronisation); the device status is read by
                             sks_sync_status(workspace, stream)                                                     */
+  int32_t deterministic; /* [0] 1: bitwise run-to-run deterministic results: no floating-point atomics --
+                            per-target sums of every slice group go to a partial-sum buffer added in a fixed order,
+                            grids are accumulated by one CTA per slice, each sort bucket is taken in value order; the
+                            fused large-N path is not used.  Same tolerances; slower where the atomics were spread  */
   int32_t graph;         /* [0] 1: replay the call as a CUDA graph (implies async).  The first call with a given set
                             of arguments (pointers, sizes, kernel, P, seed, range, options, stream) runs eagerly and
                             captures its launches; later identical calls launch the instantiated graph (one

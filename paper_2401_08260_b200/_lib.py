@@ -22,7 +22,7 @@ class sks_kernel(ctypes.Structure):
 class sks_options(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("window_w", ctypes.c_int32), ("oversample", ctypes.c_int32),
                 ("slice_batch", ctypes.c_int32), ("engine", ctypes.c_int32), ("projection", ctypes.c_int32),
-                ("async_", ctypes.c_int32), ("graph", ctypes.c_int32)]
+                ("async_", ctypes.c_int32), ("deterministic", ctypes.c_int32), ("graph", ctypes.c_int32)]
 
 
 class sks_plan_info(ctypes.Structure):
@@ -93,6 +93,6 @@ def kernel(kind: str, scale: float = 1.0, matern_p: int = 1) -> sks_kernel:
 
 
 def options(eps: float = 0.0, window_w: int = 0, oversample: int = 0, slice_batch: int = 0, engine: int = 0,
-            projection: int = 0, async_: int = 0, graph: int = 0):
+            projection: int = 0, async_: int = 0, graph: int = 0, deterministic: int = 0):
     return ctypes.pointer(sks_options(float(eps), int(window_w), int(oversample), int(slice_batch), int(engine),
-                                      int(projection), int(async_), int(graph)))
+                                      int(projection), int(async_), int(deterministic), int(graph)))

@@ -112,6 +112,7 @@ struct Opts {
   int proj = 0;     // row a1 variant: 0 auto, 1 BF16x3, 2 TF32x2, 3 FP16x2
   int async = 0;    // 1: enqueue only (status through sks_sync_status)
   int graph = 0;    // 1: replay a captured CUDA graph of the call (implies async)
+  int det = 0;      // 1: bitwise run-to-run deterministic (no float atomics; fixed-order reductions)
 };
 
 sks_status resolve_opts(const sks_options* o, Opts* r) {
@@ -131,6 +132,7 @@ sks_status resolve_opts(const sks_options* o, Opts* r) {
       return fail(SKS_ERR_INVALID, "projection must be 0 (auto), 1 (BF16x3), 2 (TF32x2) or 3 (FP16x2)");
     d.graph = o->graph ? 1 : 0;
     d.async = (o->async || d.graph) ? 1 : 0;
+    d.det = o->deterministic ? 1 : 0;
   }
   *r = d;
   return SKS_OK;
@@ -163,8 +165,21 @@ constexpr size_t kStatusBytes = 64;
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
   size_t status = 0, s64 = 0, mm = 0, Z = 0, xs3 = 0, part = 0, tot = 0, sp = 0, grid = 0, D = 0, fpar = 0, Q = 0,
-         what = 0, bound = 0, total = 0;
+         what = 0, bound = 0, dpart = 0, total = 0;
+  int dgroups = 0;   // deterministic mode: TargetAcc groups of the whole call
 };
+
+// deterministic mode: the TargetAcc groups (rows of the partial-sum buffer) a call writes -- the sort path's gather
+// rows and the interpolation's slice groups, batch by batch
+int det_groups(int64_t N, int64_t M, Path pt, int nslices, int batch) {
+  int g = 0;
+  for (int b0 = 0; b0 < nslices; b0 += batch) {
+    const int nbat = std::min(batch, nslices - b0);
+    if (pt.sort) g += sks::sortpart_acc_groups(N, M, nbat);
+    if (pt.fourier || pt.moment) g += (nbat + sks::kEvalGroup - 1) / sks::kEvalGroup;
+  }
+  return g;
+}
 
 // rows a1 + a5 and a1 + a7 fused (fused.cu) for the Fourier-only kernels when the points are many: the sources'
 // projections are spread and the targets' interpolated straight from the tensor-core accumulators; no projection
@@ -222,7 +237,7 @@ ProjMode proj_mode_call(int d, int forced, const float* x, int64_t N, const floa
 // leading dimension of the slice-major projections Z: a multiple of 4 floats (16-byte rows for TMA stores)
 inline int64_t zld(int64_t N, int64_t M) { return (N + M + 3) / 4 * 4; }
 
-Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, int proj, bool fused) {
+Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, int proj, bool fused, int dgroups = 0) {
   Layout L;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -251,6 +266,10 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, 
     L.Q = take(sizeof(float) * sks::q_stride(kNcap) * static_cast<size_t>(nbat));
     L.what = take(sizeof(double) * 2 * sks::kNdftWidth * static_cast<size_t>(nbat));
     if (fused) L.bound = take(sks::source_bound_bytes(d));
+  }
+  if (dgroups) {
+    L.dpart = take(sizeof(double) * static_cast<size_t>(M) * dgroups);
+    L.dgroups = dgroups;
   }
   L.total = o;
   return L;
@@ -437,9 +456,11 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
                         const DirEntry* dirs, const float* zx_in, const float* zy_in, float* s_out, float* t_out,
                         double inv_P, void* workspace, size_t ws_bytes, cudaStream_t st, sks_plan_info* info_out) {
   const Path pt = path_of(pr.k.kind);
-  const bool fshape = fused_shape(pr.N, pr.d, pt, pr.with_Z, o.w) && o.engine != 2;
+  const bool fshape = fused_shape(pr.N, pr.d, pt, pr.with_Z, o.w) && o.engine != 2 && !o.det;
   const int batch = choose_batch(pr.N, pr.M, pt, pr.nslices, pr.with_Z, o.batch, pr.d, o.proj, fshape);
-  const Layout L = make_layout(pr.N, pr.M, pt, batch, pr.with_Z, pr.d, o.proj, fshape);
+  const bool det = o.det && s_out;   // (per-slice outputs of sks_sum_1d have no cross-slice sums)
+  const Layout L = make_layout(pr.N, pr.M, pt, batch, pr.with_Z, pr.d, o.proj, fshape,
+                               det ? det_groups(pr.N, pr.M, pt, pr.nslices, batch) : 0);
   if (!workspace || ws_bytes < L.total)
     return fail(SKS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(SKS_ERR_INVALID, "workspace must be 256-byte aligned");
@@ -455,7 +476,7 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
   }
   unsigned* flag16 = reinterpret_cast<unsigned*>(ws + L.status);
   unsigned* summary = flag16 + 4;
-  int launches = 0, nbatches = 0;
+  int launches = 0, nbatches = 0, dgoff = 0;
   {   // flag words, fp64 target sums and the first batch's ranges in one launch
     ProfScope ps(PS_AUX, st);
     SKS_CUDA(sks::launch_prologue(flag16, s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr, pr.M,
@@ -520,6 +541,17 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
     }
     double* s64 = s_out ? reinterpret_cast<double*>(ws + L.s64) : nullptr;
     float* tps = t_out ? t_out + static_cast<int64_t>(b0) * pr.M : nullptr;
+    // where the per-target sums go: fp64 atomics into s64, or (deterministic mode) the next rows of the partial-sum
+    // buffer, added in order by the finalize kernel
+    auto target_acc = [&](int groups) {
+      sks::TargetAcc ta{s64, nullptr, pr.M, 0};
+      if (det) {
+        ta.part = reinterpret_cast<double*>(ws + L.dpart);
+        ta.goff = dgoff;
+        dgoff += groups;
+      }
+      return ta;
+    };
     sks::EvalArgs ea{};
     ea.zv = zv;
     ea.np = nbat;
@@ -533,8 +565,9 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
       sa.mm = mm;
       sa.tot = reinterpret_cast<sks::SliceTot*>(ws + L.tot);
       sa.coef = (pr.k.kind == SKS_NEGDIST) ? cdd : cdd / pr.k.scale;
-      sa.s64 = s64;
+      sa.acc = target_acc(sks::sortpart_acc_groups(pr.N, pr.M, nbat));
       sa.per_slice_out = tps;
+      sa.det = det;
       {
         ProfScope ps(PS_SORT, st);   // the whole sort stage (fork .. join); its kernels also time themselves
         SKS_CUDA(sks::launch_sortpart(sa, ws + L.sp, st));
@@ -568,14 +601,15 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
         }
         {
           ProfScope ps(PS_NDFT_SPREAD, st);
-          SKS_CUDA(sks::launch_ndft_spread(zv, w, nbat, fp, what, flag16, st));
+          SKS_CUDA(sks::launch_ndft_spread(zv, w, nbat, fp, what, det, flag16, st));
         }
         {
           ProfScope ps(PS_NDFT_EVAL, st);
           SKS_CUDA(sks::launch_ndft_eval(zv, nbat, fp, reinterpret_cast<const float*>(ws + L.D), kNcap / 2 + 1, what,
-                                         s64, tps, pt.sort, flag16, st));
+                                         target_acc((nbat + sks::kNdftEvalGroup - 1) / sks::kNdftEvalGroup), tps,
+                                         pt.sort, flag16, st));
         }
-        launches += 3;
+        launches += nbat <= 148 ? 2 : 3;
         continue;
       }
       if (fused) {
@@ -584,14 +618,17 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
                                          dirs->inv + b0, nbat, w, fp, plan.pw, kNcap, grid, flag16, st));
       } else {
         ProfScope ps(PS_SPREAD, st);
-        SKS_CUDA(sks::launch_spread(zv, w, nbat, fp, kNcap, plan.pw, pr.k.kind == SKS_LAPLACIAN, grid, flag16, st));
+        SKS_CUDA(sks::launch_spread(zv, w, nbat, fp, kNcap, plan.pw, pr.k.kind == SKS_LAPLACIAN, det, grid, flag16, st));
       }
       {
         ProfScope ps(PS_FFT, st);
+        // the first tier's grid capacity: the Laplacian's smooth part needs wide bands (n_p ~ 2048-4096 on the
+        // BJ / paper workloads), the Gaussian / Matern narrow ones (n_p ~ 64-1024)
         SKS_CUDA(sks::launch_fft_filter(grid, reinterpret_cast<const float*>(ws + L.D), nbat, kNcap, fp, plan.pw,
-                                        reinterpret_cast<float*>(ws + L.Q), flag16, st));
+                                        reinterpret_cast<float*>(ws + L.Q), pr.k.kind == SKS_LAPLACIAN ? 4096 : 2048,
+                                        flag16, st));
       }
-      launches += 2;
+      launches += nbat <= 148 ? 2 : 3;
       ea.fourier = true;
       ea.fp = fp;
       ea.Q = reinterpret_cast<const float*>(ws + L.Q);
@@ -602,9 +639,10 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
       ea.moment = true;
       ea.mom_coef = cdd / pr.k.scale;   // + alpha c_d tau sum_n w_n (z_n - z_m)^2   (R7)
     }
-    ea.s64 = s64;
     ea.per_slice_out = tps;
     ea.accumulate_out = pt.sort;
+    if (pt.fourier || pt.moment) ea.acc = fused ? sks::TargetAcc{s64, nullptr, pr.M, 0}
+                                                : target_acc((nbat + sks::kEvalGroup - 1) / sks::kEvalGroup);
     if (fused) {
       ProfScope ps(PS_EVAL, st);
       SKS_CUDA(sks::launch_proj_eval(y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
@@ -612,13 +650,16 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
       ++launches;
     } else if (pt.fourier || pt.moment) {
       ProfScope ps(PS_EVAL, st);
-      SKS_CUDA(sks::launch_eval(ea, st));
+      SKS_CUDA(sks::launch_eval(ea, det, st));
       ++launches;
     }
   }
   if (s_out) {
     ProfScope ps(PS_AUX, st);
-    SKS_CUDA(sks::launch_finalize(reinterpret_cast<const double*>(ws + L.s64), pr.M, inv_P, s_out, st));
+    if (det)
+      SKS_CUDA(sks::launch_finalize_det(reinterpret_cast<const double*>(ws + L.dpart), dgoff, pr.M, inv_P, s_out, st));
+    else
+      SKS_CUDA(sks::launch_finalize(reinterpret_cast<const double*>(ws + L.s64), pr.M, inv_P, s_out, st));
     ++launches;
   }
   sks_plan_info info{};
@@ -763,9 +804,10 @@ sks_status sks_workspace_size(int64_t N, int64_t M, int32_t d, sks_kernel kernel
   if ((s = resolve_opts(opt, &o)) != SKS_OK) return s;
   if (!bytes) return fail(SKS_ERR_INVALID, "bytes is NULL");
   const Path pt = path_of(kernel.kind);
-  const bool fshape = fused_shape(N, d, pt, true, o.w) && o.engine != 2;
+  const bool fshape = fused_shape(N, d, pt, true, o.w) && o.engine != 2 && !o.det;
   const int batch = choose_batch(N, M, pt, p_end - p_begin, true, o.batch, d, o.proj, fshape);
-  *bytes = make_layout(N, M, pt, batch, true, d, o.proj, fshape).total;
+  *bytes = make_layout(N, M, pt, batch, true, d, o.proj, fshape,
+                       o.det ? det_groups(N, M, pt, p_end - p_begin, batch) : 0).total;
   return SKS_OK;
 }
 

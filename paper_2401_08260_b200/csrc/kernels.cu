@@ -304,10 +304,30 @@ __device__ __forceinline__ void spread_shared(const FPar& f, const float* zx, co
   }
 }
 
+// a grid larger than the launch's shared-memory capacity (rare: a slice whose plan needs n_p beyond it): the taps
+// go straight to the global grid with atomics
+template <int WT>
+__device__ __forceinline__ void spread_global(const FPar& f, const float* zx, const float* wc, int cnt, float nf,
+                                              const PolyWin& pw, float* gp, int n) {
+  const float hw = 0.5f * pw.w;
+  for (int i = threadIdx.x; i < cnt; i += SP_THREADS) {
+    const float v = grid_coord(__ldg(zx + i), f.cen, f.tau, nf);
+    const float a = __fsub_rn(v, hw), fl = floorf(a);
+    const int l0 = static_cast<int>(fl) + 1;
+    const float wi = __ldg(wc + i);
+    float tw[WT];
+    poly_taps<WT>(pw, a - fl, tw);
+#pragma unroll
+    for (int j = 0; j < WT; ++j) atomicAdd(&gp[(l0 + j) & (n - 1)], wi * tw[j]);
+  }
+}
+
+// cap: the launch's shared memory in floats.  Per slice: private sub-grids if they fit (W * 8 warps * 32 lanes),
+// else a fixed-point shared grid if n_p fits, else global atomics
 template <int WT>
 __global__ void __launch_bounds__(SP_THREADS) k_spread(ZView zv, const float* __restrict__ w,
                                                        const FPar* __restrict__ fp, int ncap, PolyWin pw,
-                                                       int64_t chunk, float* __restrict__ grid,
+                                                       int64_t chunk, float* __restrict__ grid, int cap,
                                                        const unsigned* __restrict__ flag16) {
   extern __shared__ float spsm[];
   if (call_failed(flag16)) return;
@@ -320,21 +340,28 @@ __global__ void __launch_bounds__(SP_THREADS) k_spread(ZView zv, const float* __
   const float* zx = zv.zx + p * zv.ldx + i0;
   const float* wc = w + i0;
   float* gp = grid + static_cast<int64_t>(p) * ncap;
-  if (f.W <= SP_WMAX_PRIV) spread_private<WT>(f, zx, wc, cnt, f.W, nf, pw, spsm, gp, n);
-  else spread_shared<WT>(f, zx, wc, cnt, nf, pw, reinterpret_cast<int*>(spsm), gp, n);
+  if (f.W <= SP_WMAX_PRIV && f.W * SP_WARPS * 32 <= cap) spread_private<WT>(f, zx, wc, cnt, f.W, nf, pw, spsm, gp, n);
+  else if (n <= cap) spread_shared<WT>(f, zx, wc, cnt, nf, pw, reinterpret_cast<int*>(spsm), gp, n);
+  else spread_global<WT>(f, zx, wc, cnt, nf, pw, gp, n);
 }
 
 cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int ncap, const PolyWin& pw,
-                          bool wide_likely, float* grid, const unsigned* flag16, cudaStream_t st) {
+                          bool wide_likely, bool det, float* grid, const unsigned* flag16, cudaStream_t st) {
   // chunking: enough CTAs to fill 148 SMs several times, >= 2048 points per CTA to amortise the flush (narrow
-  // footprints: up to 32768 points per CTA; wide ones (the Laplacian) flush n_p cells per 8192-point sub-chunk)
+  // footprints: up to 32768 points per CTA; wide ones (the Laplacian) flush n_p cells per 8192-point sub-chunk).
+  // Deterministic mode: the whole slice in one CTA (its grid cells are then written by one thread each, in order)
   int64_t chunk = wide_likely ? 8192 : 32768;
   while (chunk > 2048 && ((zv.N + chunk - 1) / chunk) * np < (wide_likely ? 4 : 16) * 148) chunk >>= 1;
+  if (det) chunk = zv.N;
   const unsigned nchunk = static_cast<unsigned>((zv.N + chunk - 1) / chunk);
   if (nchunk == 0) return cudaSuccess;
+  // shared memory: 32 KB -- private sub-grids up to 32 cells (the Gaussian footprints of BJ cfg3 / cfg5: 17 / 31),
+  // a shared grid of up to 8192 cells (the Laplacian's n_p ~ 4096) -- keeps 7 CTAs per SM (64 KB: 3; measured
+  // cfg4 spread 0.35 -> 0.23 ms)
+  const int smem = SP_SMEM / 2;
   auto go = [&](auto kern) {
-    set_smem_attr_once(reinterpret_cast<const void*>(kern), SP_SMEM);
-    kern<<<dim3(nchunk, np), SP_THREADS, SP_SMEM, st>>>(zv, w, fp, ncap, pw, chunk, grid, flag16);
+    set_smem_attr_once(reinterpret_cast<const void*>(kern), smem);
+    kern<<<dim3(nchunk, np), SP_THREADS, smem, st>>>(zv, w, fp, ncap, pw, chunk, grid, smem / 4, flag16);
   };
   switch (pw.w) {
     case 4: go(k_spread<4>); break;
@@ -370,16 +397,20 @@ __device__ __forceinline__ void fft_stages(float2* buf, const float2* tw, int n,
   }
 }
 
+// one launch per capacity tier: this launch handles the slices with nlo < n_p <= cap (its shared memory holds
+// cap complex cells and their twiddles), the others exit at once
 __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restrict__ grid, const float* __restrict__ D,
                                                            int ncap, const FPar* __restrict__ fp, PolyWin pw,
-                                                           float* __restrict__ Q, const unsigned* __restrict__ flag16) {
+                                                           float* __restrict__ Q, int nlo, int cap,
+                                                           const unsigned* __restrict__ flag16) {
   extern __shared__ float2 sm[];
   if (call_failed(flag16)) return;
   const int p = blockIdx.x;
   const FPar f = fp[p];
   const int logn = f.logn, n = 1 << logn;
+  if (n <= nlo || n > cap) return;
   float2* buf = sm;          // [n]
-  float2* tw = sm + ncap;    // per-stage forward twiddles (fft_stages)
+  float2* tw = sm + cap;     // per-stage forward twiddles (fft_stages)
   const bool ps = n <= 8192;
   if (ps) {
     for (int j = threadIdx.x; j < n - 1; j += FF_THREADS) {
@@ -426,10 +457,17 @@ __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restri
 }
 
 cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int ncap, const FPar* fp, const PolyWin& pw,
-                              float* Q, const unsigned* flag16, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(ncap) * sizeof(float2) + static_cast<size_t>(8192) * sizeof(float2);
-  set_smem_attr_once(reinterpret_cast<const void*>(k_fft_filter), static_cast<int>(smem));
-  k_fft_filter<<<np, FF_THREADS, smem, st>>>(grid, D, ncap, fp, pw, Q, flag16);
+                              float* Q, int cap_hint, const unsigned* flag16, cudaStream_t st) {
+  // two capacity tiers: the common grids (n_p <= cap_hint) with the shared memory they need -- several CTAs per SM
+  // -- and, predicated on the device plan, any larger grid up to n_cap in a second launch whose CTAs otherwise exit
+  auto smem_for = [](int cap) {
+    return static_cast<size_t>(cap) * sizeof(float2) + static_cast<size_t>(cap <= 8192 ? cap : cap / 2) * sizeof(float2);
+  };
+  set_smem_attr_once(reinterpret_cast<const void*>(k_fft_filter), static_cast<int>(smem_for(ncap)));
+  // (at most one CTA per SM anyway -- np <= 148 -- one launch at full capacity saves the second launch's latency)
+  const int cap = np <= 148 ? ncap : std::min(cap_hint, ncap);
+  k_fft_filter<<<np, FF_THREADS, smem_for(cap), st>>>(grid, D, ncap, fp, pw, Q, 0, cap, flag16);
+  if (cap < ncap) k_fft_filter<<<np, FF_THREADS, smem_for(ncap), st>>>(grid, D, ncap, fp, pw, Q, cap, ncap, flag16);
   return cudaGetLastError();
 }
 
@@ -491,7 +529,7 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval(EvalArgs a) {
     for (int k = 0; k < 4; ++k) acc += eval_one(a, p + k, z[k], hw, m, M);
   }
   for (; p < p1; ++p) acc += eval_one(a, p, __ldg(a.zv.zy + p * a.zv.ldy + m), hw, m, M);
-  if (a.s64) atomicAdd(a.s64 + m, acc);
+  acc_target(a.acc, blockIdx.y, m, acc);
 }
 
 // the common case (fp64 target sums, no per-slice output): slice parameters staged in shared memory, the cell's 8
@@ -569,16 +607,19 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a, int sg) {
       acc += T.w * (T.z - 2.0 * zd * T.y + zd * zd * T.x);
     }
   }
-  atomicAdd(a.s64 + m, acc);
+  acc_target(a.acc, blockIdx.y, m, acc);
 }
 
-cudaError_t launch_eval(const EvalArgs& a, cudaStream_t st) {
+static_assert(kEvalGroup == EV_SG, "deterministic groups of the eval kernels");
+
+cudaError_t launch_eval(const EvalArgs& a, bool det, cudaStream_t st) {
   const unsigned bx = static_cast<unsigned>((a.zv.M + EV_THREADS - 1) / EV_THREADS);
-  if (a.fourier && a.s64 && !a.per_slice_out) {
+  if (a.fourier && (a.acc.s64 || a.acc.part) && !a.per_slice_out) {
     // slices per CTA: EV_SG, or fewer (down to EV_U) when the targets alone give too few CTAs (small, latency-bound
-    // problems such as BJ cfg1: more CTAs in flight at the cost of one more fp64 atomic per target and group)
+    // problems such as BJ cfg1: more CTAs in flight at the cost of one more fp64 atomic per target and group; not
+    // in deterministic mode, whose groups are fixed)
     int sg = EV_SG;
-    while (sg > EV_U && static_cast<int64_t>(bx) * ((a.np + sg - 1) / sg) < 2 * 148) sg >>= 1;
+    while (!det && sg > EV_U && static_cast<int64_t>(bx) * ((a.np + sg - 1) / sg) < 2 * 148) sg >>= 1;
     const unsigned by = static_cast<unsigned>((a.np + sg - 1) / sg);
     if (a.moment) k_eval_q<true><<<dim3(bx, by), EV_THREADS, 0, st>>>(a, sg);
     else k_eval_q<false><<<dim3(bx, by), EV_THREADS, 0, st>>>(a, sg);
@@ -601,6 +642,24 @@ cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t st) {
   size_t blocks = (n16 + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_zero<<<static_cast<unsigned>(blocks), 256, 0, st>>>(static_cast<uint4*>(p), n16);
+  return cudaGetLastError();
+}
+
+__global__ void k_finalize_det(const double* __restrict__ part, int G, int64_t M, double scale,
+                               float* __restrict__ s) {
+  for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < M;
+       m += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double v = 0.0;
+    for (int g = 0; g < G; ++g) v += part[static_cast<int64_t>(g) * M + m];
+    s[m] = static_cast<float>(v * scale);
+  }
+}
+
+cudaError_t launch_finalize_det(const double* part, int G, int64_t M, double scale, float* s, cudaStream_t st) {
+  int64_t blocks = (M + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  k_finalize_det<<<static_cast<unsigned>(blocks), 256, 0, st>>>(part, G, M, scale, s);
   return cudaGetLastError();
 }
 

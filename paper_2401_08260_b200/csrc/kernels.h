@@ -68,6 +68,22 @@ struct PlanConst {
 };
 constexpr int kPlanSummaryWords = 8;   // max n, max k_hi, min k_lo, max W, max band, tau min / max bits, max WA
 
+// Where a kernel's per-(target, slice group) sums go: fp64 atomics into s64 (default), or -- deterministic mode
+// (sks_options.deterministic) -- plain stores part[(goff + group) * M + m], added in a fixed order by
+// launch_finalize_det.  Every (group, target) of a launch is written exactly once.
+struct TargetAcc {
+  double* s64;
+  double* part;
+  int64_t M;
+  int goff;
+};
+#if defined(__CUDACC__)
+__device__ __forceinline__ void acc_target(const TargetAcc& t, int grp, int64_t m, double v) {
+  if (t.part) t.part[(static_cast<int64_t>(t.goff) + grp) * t.M + m] = v;
+  else if (t.s64) atomicAdd(t.s64 + m, v);
+}
+#endif
+
 // views of the projected points of a slice batch: x-part zx[p*ldx + i], y-part zy[p*ldy + m]
 struct ZView {
   const float* zx;
@@ -136,10 +152,12 @@ struct SortPartArgs {
   const unsigned* mm;    // [np][4] ranges
   SliceTot* tot;         // [np] sum w, sum w z, sum w z^2 (fp64)
   double coef;           // t = -coef * sum_n w_n |x_n - z|
-  double* s64;           // accumulate sum_p t into s64[m] (fp64 atomics, coalesced), or
+  TargetAcc acc;         // accumulate sum_p t per target (fp64; deterministic mode: one group per gather row), or
   float* per_slice_out;  // store t into per_slice_out[p*M + m]
+  bool det;              // deterministic mode: each owner's buckets ordered by value before they are summed
 };
 SpDims sortpart_dims(int64_t N, int64_t M);
+int sortpart_acc_groups(int64_t N, int64_t M, int np);   // TargetAcc groups one launch_sortpart writes
 size_t sortpart_bytes(int64_t N, int64_t M, int np);   // scratch of launch_sortpart
 int sortpart_group(int64_t N, int64_t M, int np);      // slices per L2-resident group
 int sortpart_launches_per_group(int64_t N, int64_t M);   // kernels per group (4, or 5 with many owners)
@@ -173,22 +191,25 @@ cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32,
                              const FPar* fp, const float* Q, int ncap, int w, double* s64, const unsigned* flag16,
                              cudaStream_t st);
 // row a5: g[p][l] = sum_n w_n phi_win(v_n - l) over the x projections (ES window, w taps); grid stride n_cap
+// det: one CTA per slice (no cross-CTA grid accumulation; the private grids are reduced in a fixed order)
 cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int ncap, const PolyWin& pw,
-                          bool wide_likely, float* grid, const unsigned* flag16, cudaStream_t st);
+                          bool wide_likely, bool det, float* grid, const unsigned* flag16, cudaStream_t st);
 // row a6: h[p] = IFFT_n(D[p] * FFT_n(g[p]))   (unnormalised, one CTA per slice, smem radix-2, n = n_p)
 // also writes the per-cell interpolation polynomials Q[p][c][k] = sum_j h[lminA + c + j] coef[j][k] for the
 // WA cells of the all-points footprint (Q stride kQStride(n_cap) floats per slice)
 __host__ __device__ inline int64_t q_stride(int ncap) { return static_cast<int64_t>(ncap + 16) * (PW_D + 1); }
+// (cap_hint: the grid size up to which the first of two launches handles a slice: sizes its shared memory)
 cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int ncap, const FPar* fp, const PolyWin& pw,
-                              float* Q, const unsigned* flag16, cudaStream_t st);
+                              float* Q, int cap_hint, const unsigned* flag16, cudaStream_t st);
 
 // rows a5 + a7 by the NDFT on the kept band (ndft.cu; the paper's Gaussian engine): KW = padded band
 // width (8, 16 or 32; ndft_width(K) = 0: too wide), what [np][2 KW] fp64 (zeroed by the caller)
 constexpr int kNdftWidth = 32;
-cudaError_t launch_ndft_spread(ZView zv, const float* w, int np, const FPar* fp, double* what, const unsigned* flag16,
-                               cudaStream_t st);
+cudaError_t launch_ndft_spread(ZView zv, const float* w, int np, const FPar* fp, double* what, bool det,
+                               const unsigned* flag16, cudaStream_t st);
+constexpr int kNdftEvalGroup = 32;   // slices per k_ndft_eval CTA row (one TargetAcc group)
 cudaError_t launch_ndft_eval(ZView zv, int np, const FPar* fp, const float* D, int dstride, const double* what,
-                             double* s64, float* per_slice_out, bool accumulate_out, const unsigned* flag16,
+                             TargetAcc acc, float* per_slice_out, bool accumulate_out, const unsigned* flag16,
                              cudaStream_t st);
 
 // row a7 (+ Laplacian moment term) + slice accumulation:
@@ -209,12 +230,15 @@ struct EvalArgs {
   bool moment;
   double mom_coef;
   // outputs
-  double* s64;
+  TargetAcc acc;
   float* per_slice_out;
   bool accumulate_out;   // per_slice_out += t (after the sort path stored its part)
 };
-cudaError_t launch_eval(const EvalArgs& a, cudaStream_t st);
+constexpr int kEvalGroup = 32;   // slices per eval CTA row in deterministic mode (one TargetAcc group)
+cudaError_t launch_eval(const EvalArgs& a, bool det, cudaStream_t st);
 cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t st);
 cudaError_t launch_finalize(const double* s64, int64_t M, double scale, float* s, cudaStream_t st);
+// deterministic mode: s[m] = scale * sum_{g < G} part[g * M + m], the groups added in order
+cudaError_t launch_finalize_det(const double* part, int G, int64_t M, double scale, float* s, cudaStream_t st);
 
 }  // namespace sks

@@ -78,7 +78,7 @@ constexpr int NE_T = 256, NE_SG = 32;
 template <int KW>
 __global__ void __launch_bounds__(NE_T) k_ndft_eval(ZView zv, int np, const FPar* __restrict__ fp,
                                                     const float* __restrict__ D, int dstride,
-                                                    const double* __restrict__ what, double* __restrict__ s64,
+                                                    const double* __restrict__ what, TargetAcc tacc,
                                                     float* __restrict__ per_slice_out, bool accumulate_out,
                                                     const unsigned* __restrict__ flag16) {
   __shared__ float2 ch[NE_SG][KW];   // (2 - [k = 0]) c_k what_k
@@ -132,27 +132,30 @@ __global__ void __launch_bounds__(NE_T) k_ndft_eval(ZView zv, int np, const FPar
     }
     acc += t;
   }
-  if (s64) atomicAdd(s64 + m, acc);
+  acc_target(tacc, blockIdx.y, m, acc);
 }
 
 }  // namespace
 
-cudaError_t launch_ndft_spread(ZView zv, const float* w, int np, const FPar* fp, double* what, const unsigned* flag16,
-                               cudaStream_t st) {
+cudaError_t launch_ndft_spread(ZView zv, const float* w, int np, const FPar* fp, double* what, bool det,
+                               const unsigned* flag16, cudaStream_t st) {
   if (zv.N == 0) return cudaSuccess;
   int64_t chunk = 16384;
   while (chunk > 1024 && ((zv.N + chunk - 1) / chunk) * np < 4 * 148) chunk >>= 1;
+  if (det) chunk = zv.N;   // deterministic mode: one CTA per slice, no cross-CTA atomics
   const unsigned nchunk = static_cast<unsigned>((zv.N + chunk - 1) / chunk);
   k_ndft_spread<kNdftWidth><<<dim3(nchunk, np), ND_T, 0, st>>>(zv, w, fp, chunk, what, flag16);
   return cudaGetLastError();
 }
 
+static_assert(kNdftEvalGroup == NE_SG, "deterministic groups of the NDFT eval");
+
 cudaError_t launch_ndft_eval(ZView zv, int np, const FPar* fp, const float* D, int dstride, const double* what,
-                             double* s64, float* per_slice_out, bool accumulate_out, const unsigned* flag16,
+                             TargetAcc acc, float* per_slice_out, bool accumulate_out, const unsigned* flag16,
                              cudaStream_t st) {
   const unsigned bx = static_cast<unsigned>((zv.M + NE_T - 1) / NE_T);
   const unsigned by = static_cast<unsigned>((np + NE_SG - 1) / NE_SG);
-  k_ndft_eval<kNdftWidth><<<dim3(bx, by), NE_T, 0, st>>>(zv, np, fp, D, dstride, what, s64, per_slice_out,
+  k_ndft_eval<kNdftWidth><<<dim3(bx, by), NE_T, 0, st>>>(zv, np, fp, D, dstride, what, acc, per_slice_out,
                                                          accumulate_out, flag16);
   return cudaGetLastError();
 }

@@ -526,7 +526,8 @@ template <int SP_CAP, int SP_NBF, int MINB, int S3_T>
 __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restrict__ own, double* __restrict__ otot,
                                                       const unsigned* __restrict__ mm, int NH, int G, int64_t N,
                                                       int64_t M, const float2* __restrict__ Xmb,
-                                                      const float* __restrict__ Ymb, double coef, float* __restrict__ R) {
+                                                      const float* __restrict__ Ymb, double coef, float* __restrict__ R,
+                                                      int det) {
   extern __shared__ __align__(16) unsigned char sh3[];
   constexpr int S3_PER = SP_CAP / S3_T;
   OwnerShared<SP_CAP, SP_NBF, S3_T>& S = *reinterpret_cast<OwnerShared<SP_CAP, SP_NBF, S3_T>*>(sh3);
@@ -588,6 +589,23 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
     for (int k = 0; k < S3_PER; ++k)
       if (fr[k] >= 0) S.xs[S.start[fr[k] >> 13] + (fr[k] & 8191)] = xw[k];
     __syncthreads();
+    if (det) {   // deterministic mode: each bucket's (z, w) in value order (the counting sort's order depends on the
+                 // shared atomics' timing; the bucket sums below are then taken in a fixed order); a bucket holds a
+                 // handful of points, one thread sorts it by insertion
+      for (int b = tid; b < SP_NBF; b += S3_T) {
+        const int2 br = S.se[b];
+        for (int i = br.x + 1; i < br.y; ++i) {
+          const float2 v = S.xs[i];
+          int j = i - 1;
+          while (j >= br.x && (S.xs[j].x > v.x || (S.xs[j].x == v.x && S.xs[j].y > v.y))) {
+            S.xs[j + 1] = S.xs[j];
+            --j;
+          }
+          S.xs[j + 1] = v;
+        }
+      }
+      __syncthreads();
+    }
     // ---- fp64 bucket sums (thread t: buckets t, t + S3_T, ...: neighbouring lanes read neighbouring buckets)
     //      into rec[], then one blocked exclusive scan (thread t: buckets 4t .. 4t+3)
     double vc = 0.0;   // sum w z^2 of this thread's buckets (per-warp partials, summed by thread 0 below)
@@ -740,7 +758,7 @@ template <bool GDAB>
 __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, double coef, const int* __restrict__ ypos,
                                                     const uint16_t* __restrict__ yown, const float* __restrict__ R,
                                                     const double* __restrict__ otot, SliceTot* __restrict__ tot,
-                                                    const double2* __restrict__ gdab, double* __restrict__ s64,
+                                                    const double2* __restrict__ gdab, TargetAcc tacc,
                                                     float* __restrict__ per_slice_out) {
   extern __shared__ double2 sdab[];   // [S4_SG][G] other-owner coefficients of the group's slices (gdab == null)
   const int64_t M = zv.M;
@@ -802,12 +820,11 @@ __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, dou
       if (per_slice_out) per_slice_out[static_cast<int64_t>(p) * M + m] = static_cast<float>(tt);
     }
   }
-  if (s64)
 #pragma unroll
-    for (int k = 0; k < S4_PER; ++k) {
-      const int64_t m = m0 + k * S4_T;
-      if (m < M) atomicAdd(s64 + m, acc[k]);
-    }
+  for (int k = 0; k < S4_PER; ++k) {
+    const int64_t m = m0 + k * S4_T;
+    if (m < M) acc_target(tacc, blockIdx.y, m, acc[k]);
+  }
 }
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -876,6 +893,11 @@ static size_t region_bytes(int64_t N, int64_t M, int np) {
 static int active_streams(int64_t N, int64_t M, int np) {
   const int gs = sortpart_group(N, M, np);
   return std::min(sortpart_streams(), (np + gs - 1) / gs);
+}
+
+int sortpart_acc_groups(int64_t N, int64_t M, int np) {
+  const int gs = sortpart_group(N, M, np);
+  return static_cast<int>(cdiv(np, gs) * cdiv(gs, S4_SG));
 }
 
 int sortpart_launches_per_group(int64_t N, int64_t M) { return sortpart_dims(N, M).G > kSmemDabMax ? 5 : 4; }
@@ -976,7 +998,8 @@ int part_sbper(int G) { return G > 1024 ? 16 : 8; }
 int part_big_threads(int G) { return G > 1024 ? 1024 : S0_T; }
 
 // the five kernels of one slice group (slices [g0, g0 + np) of the call) on stream st
-cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int np, int NH, int G, cudaStream_t st) {
+cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int gi, int g0, int np, int NH, int G,
+                         cudaStream_t st) {
   const int64_t N = a.zv.N, M = a.zv.M;
   constexpr int wpc = 8;   // partition: 256-element rounds per warp (measured 4: 0.850, 8: 0.835, 16: 0.834 ms cfg2)
   const int ncx0 = hist_chunks(N), ncy0 = hist_chunks(M);
@@ -1025,18 +1048,20 @@ cudaError_t launch_group(const SortPartArgs& a, const SpRegion& r, int g0, int n
   prof_end(pm);
   pm = prof_begin(PS_SP_OWNER, st);
   k_sp_owner<SP_CAP, SP_NBF, SP_MINB, SP_NT><<<dim3(G, np), SP_NT, sizeof(OwnerShared<SP_CAP, SP_NBF, SP_NT>), st>>>(
-      r.own, r.otot, mm, NH, G, N, M, r.Xmb, r.Ymb, a.coef, r.R);
+      r.own, r.otot, mm, NH, G, N, M, r.Xmb, r.Ymb, a.coef, r.R, a.det ? 1 : 0);
   prof_end(pm);
   pm = prof_begin(PS_SP_GATHER, st);
   const bool smem_dab = G <= kSmemDabMax;   // few owners: each gather CTA builds its slices' table in shared memory
   if (!smem_dab) k_sp_outer<<<np, SO_T, 0, st>>>(r.otot, G, r.dab, a.tot + g0);
   const dim3 ggrid(static_cast<unsigned>(cdiv(M, S4_CH)), static_cast<unsigned>(cdiv(np, S4_SG)));
+  TargetAcc tacc = a.acc;   // this group's rows of the TargetAcc groups (deterministic mode)
+  tacc.goff += gi * static_cast<int>(cdiv(sortpart_group(N, M, a.np), S4_SG));
   if (smem_dab)
     k_sp_gather<false><<<ggrid, S4_T, sizeof(double2) * S4_SG * G, st>>>(zv, np, G, a.coef, r.ypos, r.yown, r.R, r.otot,
-                                                                        a.tot + g0, nullptr, a.s64, pso);
+                                                                        a.tot + g0, nullptr, tacc, pso);
   else
     k_sp_gather<true><<<ggrid, S4_T, 0, st>>>(zv, np, G, a.coef, r.ypos, r.yown, r.R, r.otot, a.tot + g0, r.dab,
-                                              a.s64, pso);
+                                              tacc, pso);
   prof_end(pm);
   return cudaGetLastError();
 }
@@ -1062,7 +1087,8 @@ cudaError_t launch_sortpart(const SortPartArgs& a, void* ws, cudaStream_t st) {
   for (int g0 = 0, gi = 0; g0 < a.np; g0 += gs, ++gi) {
     const int si = gi % ns;
     const SpRegion r = carve_region(static_cast<char*>(ws) + rb * si, N, M, d.NH, d.G, gs);
-    if ((e = launch_group(a, r, g0, std::min(gs, a.np - g0), d.NH, d.G, si ? pool.s[si] : st)) != cudaSuccess) return e;
+    if ((e = launch_group(a, r, gi, g0, std::min(gs, a.np - g0), d.NH, d.G, si ? pool.s[si] : st)) != cudaSuccess)
+      return e;
   }
   for (int i = 1; i < ns; ++i) {   // join
     if ((e = cudaEventRecord(pool.join[i], pool.s[i])) != cudaSuccess) return e;

@@ -493,3 +493,29 @@ def test_fused_projection_spread(kind, scale, d, N, M, P):
     err = rel_err(s[tgt], ref, w)
     print(f"fused {kind} d={d} N={N} P={P}: max|ds|/sum|w| = {err:.3e}  plan={info}")
     assert err <= TOL[kind], err
+
+
+# ---------------------------------------------------------------- opt-in bitwise determinism
+@pytest.mark.parametrize("name,size,kw", [("cfg1", {}, {}), ("cfg1", {}, {"engine": "ndft"}),
+                                          ("cfg2", dict(N=30000, M=5000, P=24), {}),
+                                          ("paper_laplace", dict(N=4000, M=1000, P=40), {}),
+                                          ("paper_matern", dict(N=3000, M=800, P=16), {}),
+                                          ("cfg5", dict(N=300_000, M=3000, P=20), {})],
+                         ids=["cfg1", "cfg1-ndft", "cfg2", "laplace", "matern", "cfg5-large-N"])
+def test_deterministic_mode_bitwise(name, size, kw):
+    # sks_options.deterministic: no floating-point atomics, fixed-order reductions -> identical bits run to run,
+    # the same estimate as the default mode (which adds per-group sums with fp64 atomics), and oracle parity
+    cfg = I.scaled(I.CONFIGS[name], **size) if size else I.CONFIGS[name]
+    x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
+    par = I.kernel_param(cfg) if cfg.kind != "negdist" else 1.0
+    xd, yd, wd = dev(x), dev(y), dev(w)
+    runs = [S.sks_sum(xd, yd, wd, cfg.kind, par, cfg.P, cfg.dir_seed, matern_p=cfg.matern_p, deterministic=True,
+                      **kw).cpu().numpy() for _ in range(3)]
+    assert all(np.array_equal(runs[0].view(np.uint32), r.view(np.uint32)) for r in runs[1:])
+    assert S.sks_last_plan()["fused"] == 0
+    base = S.sks_sum(xd, yd, wd, cfg.kind, par, cfg.P, cfg.dir_seed, matern_p=cfg.matern_p, **kw).cpu().numpy()
+    assert rel_err(runs[0], base.astype(np.float64), w) <= 1e-6
+    tgt = I.target_subset(cfg.M, 100)
+    ref = O.sliced_sum(cfg.kind, par if cfg.kind != "negdist" else 0.0, x, y, w, cfg.P, cfg.dir_seed, targets=tgt,
+                       matern_p=cfg.matern_p)
+    assert rel_err(runs[0][tgt], ref, w) <= TOL[cfg.kind]

@@ -7,10 +7,10 @@ import csv
 import json
 import sys
 
-SLOTS = [("k_split3", "split3"), ("k_proj_tc", "project"), ("k_project", "project"), ("k_minmax", "minmax"),
+SLOTS = [("k_split3", "split3"), ("k_proj_tc", "project"), ("k_minmax", "minmax"), ("k_norm_bound", "minmax"),
          ("k_sp_hist", "sp_hist"), ("k_sp_part", "sp_part"), ("k_sp_owner", "sp_owner"), ("k_sp_gather", "sp_gather"),
-         ("k_sortsum", "sortsum_v1"), ("k_plan_D", "plan_D"), ("k_spread", "spread"), ("k_fft_filter", "fft_filter"),
-         ("k_eval", "eval")]
+         ("k_plan", "plan"), ("k_proj_spread", "spread"), ("k_spread", "spread"), ("k_fft_filter", "fft_filter"),
+         ("k_proj_eval", "eval"), ("k_eval", "eval")]
 rows = list(csv.reader(open(sys.argv[1])))
 hdr, per = None, {}
 for r in rows:
