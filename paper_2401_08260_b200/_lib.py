@@ -7,7 +7,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsks.so")
+# SKS_LIB selects another build of the same library (the bounds-checked libsks_checked.so of build.py --checked)
+LIB_PATH = os.environ.get("SKS_LIB") or os.path.join(HERE, "libsks.so")
 
 SKS_OK, SKS_ERR_INVALID, SKS_ERR_UNSUPPORTED, SKS_ERR_CUDA, SKS_ERR_WORKSPACE, SKS_ERR_NONFINITE = range(6)
 STATUS_NAMES = {0: "SKS_OK", 1: "SKS_ERR_INVALID", 2: "SKS_ERR_UNSUPPORTED", 3: "SKS_ERR_CUDA",

@@ -165,7 +165,7 @@ constexpr size_t kStatusBytes = 64;
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
   size_t status = 0, s64 = 0, mm = 0, Z = 0, xs3 = 0, part = 0, tot = 0, sp = 0, grid = 0, D = 0, fpar = 0, Q = 0,
-         what = 0, bound = 0, dpart = 0, total = 0;
+         what = 0, bound = 0, ylo = 0, dpart = 0, total = 0;
   int dgroups = 0;   // deterministic mode: TargetAcc groups of the whole call
 };
 
@@ -265,7 +265,10 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, 
     L.fpar = take(sizeof(sks::FPar) * nbat);
     L.Q = take(sizeof(float) * sks::q_stride(kNcap) * static_cast<size_t>(nbat));
     L.what = take(sizeof(double) * 2 * sks::kNdftWidth * static_cast<size_t>(nbat));
-    if (fused) L.bound = take(sks::source_bound_bytes(d));
+    if (fused) {
+      L.bound = take(sks::source_bound_bytes(d));
+      L.ylo = take(sizeof(float) * static_cast<size_t>(M) * d);   // the targets' pre-split lo piece (fused eval)
+    }
   }
   if (dgroups) {
     L.dpart = take(sizeof(double) * static_cast<size_t>(M) * dgroups);
@@ -646,8 +649,9 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
     if (fused) {
       ProfScope ps(PS_EVAL, st);
       SKS_CUDA(sks::launch_proj_eval(y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
-                                     dirs->inv + b0, nbat, ea.fp, ea.Q, kNcap, o.w, s64, flag16, st));
-      ++launches;
+                                     dirs->inv + b0, nbat, ea.fp, ea.Q, kNcap, o.w, s64,
+                                     reinterpret_cast<float*>(ws + L.ylo), flag16, st));
+      launches += 2;
     } else if (pt.fourier || pt.moment) {
       ProfScope ps(PS_EVAL, st);
       SKS_CUDA(sks::launch_eval(ea, det, st));

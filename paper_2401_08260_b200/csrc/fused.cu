@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     uint32_t phase = 0;
     for (int64_t t = t0; t < t1; ++t)
       for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&xfull[stage], phase);
+        mbar_wait_sleep(&xfull[stage], phase);
         unsigned char* sa = sm + FS_OFF_STAGE + stage * 2 * FS_PIECE;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
       const int64_t i0 = t * FS_P + c0;
       const float wv = wnext;
       wnext = wload(t + 1);
-      mbar_wait(&tfull[b], (it >> 1) & 1);
+      mbar_wait_sleep(&tfull[b], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t taddr = tmem_base + static_cast<uint32_t>(b * FS_P + c0) + (static_cast<uint32_t>(32 * q) << 16);
       const int nj = (N - i0 < 32) ? static_cast<int>(N - i0) : 32;
@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
             const float a = fmaf(__uint_as_float(v[jj]), ga, gb), fl = floorf(a);
             const float u = (a - fl) - 0.5f, u2 = u * u;
             const int cl = min(max(static_cast<int>(fl) + 1 - f.lmin, 0), cmax);   // (memory safety only)
+            SKS_CHECK(wi == 0.f || cl == static_cast<int>(fl) + 1 - f.lmin);   // the bound holds: no clamping
             float* cell = col + cl * FS_S;
 #pragma unroll
             for (int m = 0; m < WT / 2; ++m) {
@@ -460,7 +461,8 @@ static_assert(FE_SMEM <= 227 * 1024, "k_proj_eval shared memory");
 __device__ __forceinline__ int qswz(int c) { return c ^ ((c >> 3) & 7); }
 
 __global__ void __launch_bounds__(FE_THREADS, 1)
-    k_proj_eval(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY, int nk, int64_t M,
+    k_proj_eval(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY,
+                const __grid_constant__ CUtensorMap tmYlo, int nk, int64_t M,
                 int np, int ranges, const float* __restrict__ inv_norm, const FPar* __restrict__ fp,
                 const float* __restrict__ Q, int ncap, int w, double* __restrict__ s64,
                 const unsigned* __restrict__ flag16) {
@@ -516,7 +518,8 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], FE_EPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmYlo)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -538,8 +541,10 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         unsigned char* sa = sm + FE_OFF_STAGE + stage * 2 * FE_PIECE;
-        mbar_expect_tx(&xfull[stage], FE_PIECE);
+        // the raw fp32 tile (the hi piece) and the pre-split lo piece (k_split_lo): no conversion in the CTA
+        mbar_expect_tx(&xfull[stage], 2 * FE_PIECE);
         tma_load_2d(&tmY, &xfull[stage], sa, kb * 32, static_cast<int>(t * FE_T));
+        tma_load_2d(&tmYlo, &xfull[stage], sa + FE_PIECE, kb * 32, static_cast<int>(t * FE_T));
         if (++stage == FE_STAGES) { stage = 0; phase ^= 1; }
       }
   } else if (warp == 1 && lane == 0) {
@@ -555,7 +560,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(b * FE_S);
       for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait(&xfull[stage], phase);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const unsigned char* sa = sm + FE_OFF_STAGE + stage * 2 * FE_PIECE;
         const uint64_t db = umma_desc_sw128(sm + kb * FE_B);
@@ -582,31 +587,6 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
                        smem_u32(&tfull[b]))
                    : "memory");
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ---- converters: lo = rn_tf32(x - trunc_tf32(x)) (as in k_proj_spread)
-    const int cw = warp - 4, c = lane & 7, rsub = lane >> 3;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int64_t t = t0; t < t1; ++t)
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&xfull[stage], phase);
-        unsigned char* sa = sm + FE_OFF_STAGE + stage * 2 * FE_PIECE;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row = 32 * cw + 4 * i + rsub;
-          const int off = row * 128 + ((c ^ (row & 7)) << 4);
-          const float4 v = *reinterpret_cast<const float4*>(sa + off);
-          const float4 lo = make_float4(tf32_cvt_rn(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u)),
-                                        tf32_cvt_rn(v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u)),
-                                        tf32_cvt_rn(v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u)),
-                                        tf32_cvt_rn(v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u)));
-          *reinterpret_cast<float4*>(sa + FE_PIECE + off) = lo;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[stage]);
-        if (++stage == FE_STAGES) { stage = 0; phase ^= 1; }
-      }
   } else if (warp >= 8) {
     // ---- epilogue: warp w owns TMEM lane quadrant q = w % 4 (targets 32 q + lane of the tile) and the 16 slices
     //      h = (w - 8) / 4 of the group
@@ -614,7 +594,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
     int it = 0;
     for (int64_t t = t0; t < t1; ++t, ++it) {
       const int b = it & 1;
-      mbar_wait(&tfull[b], (it >> 1) & 1);
+      mbar_wait_sleep(&tfull[b], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       uint32_t v[16];
       const uint32_t taddr = tmem_base + static_cast<uint32_t>(b * FE_S + 16 * h) + (static_cast<uint32_t>(32 * q) << 16);
@@ -636,6 +616,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
         const float a = fmaf(__uint_as_float(v[j]), c.x, c.y), fl = floorf(a);
         int cl = static_cast<int>(fl) + 1 - __float_as_int(c.z);
         const int wq = __float_as_int(c.w);
+        SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < wq));   // the bound holds
         cl = cl < 0 ? 0 : (cl >= wq ? wq - 1 : cl);   // (a valid bound never clamps; memory safety only)
         float4 c0, c1;
         if (wq <= FE_QCAP) {
@@ -745,14 +726,35 @@ cudaError_t launch_proj_spread(const float* x, int64_t N, int d, const float* g3
 
 namespace sks {
 
+// the TF32x2 lo piece of every coordinate, once (the eval CTAs of all slice groups load it by TMA instead of each
+// converting the same tile): lo = rn_tf32(y - trunc_tf32(y)), the kind::tf32 operand read of y being the hi piece
+__global__ void k_split_lo(const float4* __restrict__ y, int64_t n4, float4* __restrict__ lo) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 v = __ldcs(y + i);
+    __stcs(lo + i, make_float4(tf32_cvt_rn(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u)),
+                               tf32_cvt_rn(v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u)),
+                               tf32_cvt_rn(v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u)),
+                               tf32_cvt_rn(v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u))));
+  }
+}
+
 cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32, int dp32, const float* inv_norm, int np,
-                             const FPar* fp, const float* Q, int ncap, int w, double* s64, const unsigned* flag16,
-                             cudaStream_t st) {
-  CUtensorMap tmB, tmY;
+                             const FPar* fp, const float* Q, int ncap, int w, double* s64, float* ylo,
+                             const unsigned* flag16, cudaStream_t st) {
+  {
+    const int64_t n4 = M * d / 4;   // (d % 4 == 0 on the fused path)
+    int64_t blocks = (n4 + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_split_lo<<<static_cast<unsigned>(blocks), 256, 0, st>>>(reinterpret_cast<const float4*>(y), n4,
+                                                              reinterpret_cast<float4*>(ylo));
+  }
+  CUtensorMap tmB, tmY, tmYlo;
   const int nk = dp32 / 32;
   if (!encode_f32_map(&tmB, g32, static_cast<uint64_t>(np), static_cast<uint64_t>(dp32), static_cast<uint64_t>(dp32),
                       FE_S) ||
-      !encode_f32_map(&tmY, y, static_cast<uint64_t>(M), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FE_T))
+      !encode_f32_map(&tmY, y, static_cast<uint64_t>(M), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FE_T) ||
+      !encode_f32_map(&tmYlo, ylo, static_cast<uint64_t>(M), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FE_T))
     return cudaErrorInvalidValue;
   const int ngroups = (np + FE_S - 1) / FE_S;
   const int64_t ntt = (M + FE_T - 1) / FE_T;
@@ -760,7 +762,7 @@ cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32,
   if (ranges < 1) ranges = 1;
   if (ranges > ntt) ranges = static_cast<int>(ntt);
   set_smem_attr_once(reinterpret_cast<const void*>(k_proj_eval), FE_SMEM);
-  k_proj_eval<<<ngroups * ranges, FE_THREADS, FE_SMEM, st>>>(tmB, tmY, nk, M, np, ranges, inv_norm, fp, Q, ncap, w, s64,
+  k_proj_eval<<<ngroups * ranges, FE_THREADS, FE_SMEM, st>>>(tmB, tmY, tmYlo, nk, M, np, ranges, inv_norm, fp, Q, ncap, w, s64,
                                                             flag16);
   return cudaGetLastError();
 }

@@ -217,6 +217,7 @@ __device__ __forceinline__ void spread_private(const FPar& f, const float* zx, c
     auto one = [&](float z, float wi) {
       const float a = __fsub_rn(__fmul_rn(__fsub_rn(z, f.cen), taun), hw), fl = floorf(a);
       const float u = (a - fl) - 0.5f, u2 = u * u;
+      SKS_CHECK(static_cast<int>(fl) + 1 - f.lmin >= 0 && static_cast<int>(fl) + 1 - f.lmin + WT <= W);
       float* cell = base + (static_cast<int>(fl) + 1) * 32;
 #pragma unroll
       for (int j = 0; j < WT / 2; ++j) {
@@ -246,6 +247,7 @@ __device__ __forceinline__ void spread_private(const FPar& f, const float* zx, c
       const float wi = __ldg(wc + i);
       float tw[WT];
       poly_taps<WT>(pw, a - fl, tw);                  // generic WT = 12 kernel for other widths
+      SKS_CHECK(static_cast<int>(fl) + 1 - f.lmin >= 0 && static_cast<int>(fl) + 1 - f.lmin + pw.w <= W);
       float* cell = base + (static_cast<int>(fl) + 1) * 32;
 #pragma unroll
       for (int j = 0; j < WT; ++j) cell[j * 32] += wi * tw[j];
@@ -501,6 +503,7 @@ __device__ __forceinline__ double eval_one(const EvalArgs& a, int p, float z, fl
     const float av = __fsub_rn(v, hw), fl = floorf(av);
     const int l0 = static_cast<int>(fl) + 1;
     static_assert(PW_D == 7, "interpolation polynomials are read as two float4");
+    SKS_CHECK(l0 - f.lminA >= 0 && l0 - f.lminA < f.WA);
     const float4* q = reinterpret_cast<const float4*>(a.Q + static_cast<int64_t>(p) * q_stride(a.ncap) +
                                                       (l0 - f.lminA) * 8);
     t += horner8(__ldg(q), __ldg(q + 1), av - fl);
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a, int sg) {
     const FPar f = a.fp[p0 + q];
     // cell l0 = floor(v - w/2) + 1 of slice p reads Q[p][l0 - lminA]: float offset qs (p - p0) + 8 (l0 - lminA)
     const int qoff = static_cast<int>(qs * q) + 8 * (1 - f.lminA);
-    sp[q] = make_float4(f.cen, f.tau * static_cast<float>(1 << f.logn), __int_as_float(qoff), 0.f);
+    sp[q] = make_float4(f.cen, f.tau * static_cast<float>(1 << f.logn), __int_as_float(qoff), __int_as_float(f.WA));
     if (MOMENT) {
       const SliceTot T = a.tot[p0 + q];
       st[q] = make_double4(T.A, T.B, T.C, a.mom_coef * static_cast<double>(f.tau));
@@ -568,6 +571,8 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_q(EvalArgs a, int sg) {
     const float4 c = sp[q];
     const float av = __fsub_rn(__fmul_rn(__fsub_rn(z, c.x), c.y), hw), fl = floorf(av);
     float4 c0, c1;
+    SKS_CHECK(__float_as_int(c.z) + 8 * static_cast<int>(fl) >= static_cast<int>(qs) * q &&
+              __float_as_int(c.z) + 8 * static_cast<int>(fl) < static_cast<int>(qs) * q + 8 * __float_as_int(c.w));
     ld_q8(Qg + (__float_as_int(c.z) + 8 * static_cast<int>(fl)), c0, c1);
     return horner8(c0, c1, av - fl);
   };

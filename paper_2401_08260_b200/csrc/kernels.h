@@ -3,6 +3,25 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+// Checked builds (-DSKS_CHECKS, build.py --checked -> libsks_checked.so): device-side bounds checks on every data-
+// dependent index (grid cells, polynomial tables, mailbox slots, sort ranks) that trap with a message.  They stand in
+// for compute-sanitizer, which this pool does not run; tests/test_checked_build.py drives every kernel through them.
+#if defined(SKS_CHECKS) && defined(__CUDACC__)
+#include <cstdio>
+#define SKS_CHECK(c)                                                                          \
+  do {                                                                                        \
+    if (!(c)) {                                                                               \
+      printf("SKS_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,           \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x), #c);                 \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define SKS_CHECK(c) \
+  do {               \
+  } while (0)
+#endif
+
 namespace sks {
 
 // opt-in per-launch timing (sks_profile_*, api.cpp): CUDA events around launches, accumulated per slot
@@ -187,9 +206,10 @@ cudaError_t launch_proj_spread(const float* x, int64_t N, int d, const float* g3
                                const unsigned* flag16, cudaStream_t st);
 // rows a1 + a7 fused for the targets (fused.cu): projections of y interpolated from the tensor-core accumulators,
 // s64[m] += sum over the slices of t_{m,p} (after launch_fft_filter wrote Q)
+// (ylo: M x d fp32 scratch for the pre-split lo piece of y)
 cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32, int dp32, const float* inv_norm, int np,
-                             const FPar* fp, const float* Q, int ncap, int w, double* s64, const unsigned* flag16,
-                             cudaStream_t st);
+                             const FPar* fp, const float* Q, int ncap, int w, double* s64, float* ylo,
+                             const unsigned* flag16, cudaStream_t st);
 // row a5: g[p][l] = sum_n w_n phi_win(v_n - l) over the x projections (ES window, w taps); grid stride n_cap
 // det: one CTA per slice (no cross-CTA grid accumulation; the private grids are reduced in a fixed order)
 cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int ncap, const PolyWin& pw,

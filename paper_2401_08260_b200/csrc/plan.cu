@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(PL_T) k_plan(const unsigned* __restrict__ mm, 
   auto cell = [&](float z) { return floorf(__fsub_rn(__fmul_rn(__fsub_rn(z, cen), taun), hw)); };
   const int l0 = static_cast<int>(cell(xmn)), l1 = static_cast<int>(cell(xmx)) + pc.w + 1;   // one cell of margin
   const int la0 = static_cast<int>(cell(amn)), la1 = static_cast<int>(cell(amx)) + 2;
+  SKS_CHECK(l1 - l0 + 1 >= pc.w + 2 && la1 - la0 + 1 >= 3 && la1 - la0 + 1 <= ncap + 16 && khi <= KC && klo <= khi);
   // diagonal: D[k] = c_k / Phi(k/n)^2 on the band (the NDFT has no window to undo)
   const int nh = n / 2 + 1, shift = pc.ncap_log - logn;
   float* Dp = D + static_cast<int64_t>(p) * (ncap / 2 + 1);

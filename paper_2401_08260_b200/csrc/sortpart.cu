@@ -319,6 +319,7 @@ __device__ __forceinline__ void part_round(int e0, int n, const float* __restric
     if (!FULL && ow[k] < 0) continue;
     const int dst = cw[ow[k]] + rk[k];
     const int i = e0 + 32 * k + lane;
+    SKS_CHECK(dst >= 0 && dst < n && ow[k] < G);
     if (IsX) {
       xdst[dst] = make_float2(zz[k], ww[k]);
     } else {
@@ -587,7 +588,10 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < S3_PER; ++k)
-      if (fr[k] >= 0) S.xs[S.start[fr[k] >> 13] + (fr[k] & 8191)] = xw[k];
+      if (fr[k] >= 0) {
+        SKS_CHECK(S.start[fr[k] >> 13] + (fr[k] & 8191) < nk);
+        S.xs[S.start[fr[k] >> 13] + (fr[k] & 8191)] = xw[k];
+      }
     __syncthreads();
     if (det) {   // deterministic mode: each bucket's (z, w) in value order (the counting sort's order depends on the
                  // shared atomics' timing; the bucket sums below are then taken in a fixed order); a bucket holds a
