@@ -165,7 +165,7 @@ constexpr size_t kStatusBytes = 64;
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
   size_t status = 0, s64 = 0, mm = 0, Z = 0, xs3 = 0, part = 0, tot = 0, sp = 0, grid = 0, D = 0, fpar = 0, Q = 0,
-         what = 0, bound = 0, ylo = 0, dpart = 0, total = 0;
+         what = 0, bound = 0, xlo = 0, ylo = 0, dpart = 0, total = 0;
   int dgroups = 0;   // deterministic mode: TargetAcc groups of the whole call
 };
 
@@ -267,7 +267,8 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, 
     L.what = take(sizeof(double) * 2 * sks::kNdftWidth * static_cast<size_t>(nbat));
     if (fused) {
       L.bound = take(sks::source_bound_bytes(d));
-      L.ylo = take(sizeof(float) * static_cast<size_t>(M) * d);   // the targets' pre-split lo piece (fused eval)
+      L.xlo = take(sizeof(float) * static_cast<size_t>(N) * d);   // the TF32x2 lo pieces of the sources and the
+      L.ylo = take(sizeof(float) * static_cast<size_t>(M) * d);   // targets (written by the bound pass, fused path)
     }
   }
   if (dgroups) {
@@ -498,6 +499,13 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
     SKS_CUDA(sks::launch_split3(x, pr.N, y, pr.M, pr.d, ws + L.xs3, st));
     ++launches;
   }
+  if (fused) {   // direction-independent: the sources' centre and radius, the targets' radius, both lo pieces
+    ProfScope ps(PS_MINMAX, st);
+    SKS_CUDA(sks::launch_source_prep(x, pr.N, y, pr.M, pr.d, reinterpret_cast<double*>(ws + L.bound),
+                                     reinterpret_cast<unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32),
+                                     reinterpret_cast<float*>(ws + L.xlo), reinterpret_cast<float*>(ws + L.ylo), st));
+    launches += 4;
+  }
   for (int b0 = 0; b0 < pr.nslices; b0 += batch) {
     const int nbat = std::min(batch, pr.nslices - b0);
     ++nbatches;
@@ -581,14 +589,13 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
     if (pt.fourier) {
       sks::FPar* fp = reinterpret_cast<sks::FPar*>(ws + L.fpar);
       float* grid = reinterpret_cast<float*>(ws + L.grid);
-      if (fused) {   // the sources' range bound in place of their exact ranges (fused.cu)
+      if (fused) {   // both point sets' range bounds in place of their exact ranges (fused.cu)
         ProfScope ps(PS_MINMAX, st);
-        double* mu = reinterpret_cast<double*>(ws + L.bound);
-        SKS_CUDA(sks::launch_source_bound(x, pr.N, y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32,
-                                          dirs->K32, dirs->inv + b0, nbat, mu,
-                                          reinterpret_cast<unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32),
+        SKS_CUDA(sks::launch_bound_ranges(dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32, pr.d,
+                                          dirs->inv + b0, nbat, reinterpret_cast<const double*>(ws + L.bound),
+                                          reinterpret_cast<const unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32),
                                           mm, flag16, st));
-        launches += 5;
+        launches += 1;
       }
       {
         ProfScope ps(PS_PLAN, st);
@@ -617,7 +624,7 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
       }
       if (fused) {
         ProfScope ps(PS_SPREAD, st);
-        SKS_CUDA(sks::launch_proj_spread(x, pr.N, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
+        SKS_CUDA(sks::launch_proj_spread(x, reinterpret_cast<const float*>(ws + L.xlo), pr.N, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
                                          dirs->inv + b0, nbat, w, fp, plan.pw, kNcap, grid, flag16, st));
       } else {
         ProfScope ps(PS_SPREAD, st);
@@ -650,8 +657,8 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
       ProfScope ps(PS_EVAL, st);
       SKS_CUDA(sks::launch_proj_eval(y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
                                      dirs->inv + b0, nbat, ea.fp, ea.Q, kNcap, o.w, s64,
-                                     reinterpret_cast<float*>(ws + L.ylo), flag16, st));
-      launches += 2;
+                                     reinterpret_cast<const float*>(ws + L.ylo), flag16, st));
+      launches += 1;
     } else if (pt.fourier || pt.moment) {
       ProfScope ps(PS_EVAL, st);
       SKS_CUDA(sks::launch_eval(ea, det, st));

@@ -57,10 +57,20 @@ __global__ void k_sample_mean_fin(int64_t N, int d, const double* __restrict__ p
   if (threadIdx.x < 8) nb[threadIdx.x] = 0u;
 }
 
+__device__ __forceinline__ float tf32_lo(float v) {
+  return tf32_cvt_rn(v - __uint_as_float(__float_as_uint(v) & 0xffffe000u));
+}
+__device__ __forceinline__ float4 tf32_lo4(float4 v) {
+  return make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+}
+
 // one warp per row (d <= 128: one float4 per lane), fp32 sums of squares, maxima as float bits (non-negative
-// floats order as unsigned ints); out[0] = max ||x - mu||^2, out[1] = max ||x||^2, out[2] = non-finite seen
+// floats order as unsigned ints); out[0] = max ||x - mu||^2, out[1] = max ||x||^2, out[2] = non-finite seen.
+// The same pass writes the TF32x2 lo piece of every element, lo = rn_tf32(x - trunc_tf32(x)) (reading R2; the
+// fused kernels read the raw tile as the hi piece and this array as the lo piece)
 __global__ void __launch_bounds__(256) k_norm_bound(const float* __restrict__ x, int64_t N, int d,
-                                                    const double* __restrict__ mu, unsigned* __restrict__ out) {
+                                                    const double* __restrict__ mu, unsigned* __restrict__ out,
+                                                    float* __restrict__ lo) {
   __shared__ float smu[128];
   for (int j = threadIdx.x; j < 128; j += blockDim.x) smu[j] = j < d ? static_cast<float>(mu[j]) : 0.f;
   __syncthreads();
@@ -82,6 +92,7 @@ __global__ void __launch_bounds__(256) k_norm_bound(const float* __restrict__ x,
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      if (on && i0 + u < N) __stcg(reinterpret_cast<float4*>(lo + (i0 + u) * d) + lane, tf32_lo4(v[u]));
       const float a = v[u].x - m4.x, b = v[u].y - m4.y, c = v[u].z - m4.z, e = v[u].w - m4.w;
       float r2 = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
       float n2 = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, v[u].w * v[u].w)));
@@ -163,7 +174,7 @@ constexpr int FS_STAGES = 3;
 constexpr int FS_KBMAX = 4;        // k-blocks of 32 dims: d <= 128
 constexpr int FS_WCAP = 32;        // private grid cells per slice (wider footprints: global atomics)
 constexpr int FS_EPI = 16;         // epilogue warps: 4 per TMEM lane quadrant, 32 points of the tile each
-constexpr int FS_THREADS = 32 * (8 + FS_EPI);   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 -, w4..w7 converters, epilogue
+constexpr int FS_THREADS = 32 * (4 + FS_EPI);   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 -, w4.. epilogue
 constexpr int FS_PIECE = FS_P * 128;                      // one k-block of 128 points: 16 KB
 constexpr int FS_A = FS_S * 128;                          // one k-block of the directions: 16 KB
 constexpr int FS_OFF_STAGE = FS_KBMAX * FS_A;             // 64 KB of resident directions
@@ -174,7 +185,8 @@ static_assert(FS_SMEM <= 227 * 1024, "k_proj_spread shared memory");
 
 template <int WT>
 __global__ void __launch_bounds__(FS_THREADS, 1)
-    k_proj_spread(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int nk, int64_t N,
+    k_proj_spread(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
+                  const __grid_constant__ CUtensorMap tmXlo, int nk, int64_t N,
                   int np, int ranges, const float* __restrict__ inv_norm, const float* __restrict__ w,
                   const FPar* __restrict__ fp, PolyWin pw, int ncap, float* __restrict__ grid,
                   const unsigned* __restrict__ flag16) {
@@ -185,9 +197,8 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   unsigned char* sm = fsraw + ((1024u - (smem_u32(fsraw) & 1023u)) & 1023u);
   float* priv = reinterpret_cast<float*>(sm + FS_OFF_GRID);   // [FS_EPI / 4][FS_WCAP][FS_S]
   uint64_t* afull = reinterpret_cast<uint64_t*>(sm + FS_OFF_BAR);
-  uint64_t* xfull = afull + 1;                 // [FS_STAGES] raw tile landed
-  uint64_t* full = xfull + FS_STAGES;          // [FS_STAGES] lo written (converters)
-  uint64_t* empty = full + FS_STAGES;          // [FS_STAGES] consumed by the MMAs
+  uint64_t* xfull = afull + 1;                 // [FS_STAGES] raw tile (hi) and lo piece landed
+  uint64_t* empty = xfull + FS_STAGES;         // [FS_STAGES] consumed by the MMAs
   uint64_t* tfull = empty + FS_STAGES;         // [2]
   uint64_t* tempty = tfull + 2;                // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
@@ -202,13 +213,13 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     mbar_init(afull, 1);
     for (int s = 0; s < FS_STAGES; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&full[s], 4);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], FS_EPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmXlo)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -221,7 +232,8 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // ---- TMA producer: the tile's directions once, then the raw fp32 point tiles (the hi piece)
+    // ---- TMA producer: the tile's directions once, then the raw fp32 point tiles (the hi piece) and their lo
+    //      pieces (written by the k_norm_bound pass)
     mbar_expect_tx(afull, nk * FS_A);
     for (int kb = 0; kb < nk; ++kb) tma_load_2d(&tmA, afull, sm + kb * FS_A, kb * 32, s0);
     int stage = 0;
@@ -230,8 +242,9 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         unsigned char* sa = sm + FS_OFF_STAGE + stage * 2 * FS_PIECE;
-        mbar_expect_tx(&xfull[stage], FS_PIECE);
+        mbar_expect_tx(&xfull[stage], 2 * FS_PIECE);
         tma_load_2d(&tmX, &xfull[stage], sa, kb * 32, static_cast<int>(t * FS_P));
+        tma_load_2d(&tmXlo, &xfull[stage], sa + FS_PIECE, kb * 32, static_cast<int>(t * FS_P));
         if (++stage == FS_STAGES) { stage = 0; phase ^= 1; }
       }
   } else if (warp == 1 && lane == 0) {
@@ -247,7 +260,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(b * FS_P);
       for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait(&xfull[stage], phase);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const unsigned char* sb = sm + FS_OFF_STAGE + stage * 2 * FS_PIECE;
         const uint64_t da = umma_desc_sw128(sm + kb * FS_A);
@@ -274,39 +287,13 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
                        smem_u32(&tfull[b]))
                    : "memory");
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ---- converters: lo = rn_tf32(x - trunc_tf32(x)) of every element of the raw tile (the hi operand as it
-    //      stands: kind::tf32 reads the top 19 bits).  Lane l: 16-byte chunk l % 8 of rows 4 i + l / 8
-    const int cw = warp - 4, c = lane & 7, rsub = lane >> 3;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int64_t t = t0; t < t1; ++t)
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait_sleep(&xfull[stage], phase);
-        unsigned char* sa = sm + FS_OFF_STAGE + stage * 2 * FS_PIECE;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row = 32 * cw + 4 * i + rsub;
-          const int off = row * 128 + ((c ^ (row & 7)) << 4);
-          const float4 v = *reinterpret_cast<const float4*>(sa + off);
-          const float4 lo = make_float4(tf32_cvt_rn(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u)),
-                                        tf32_cvt_rn(v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u)),
-                                        tf32_cvt_rn(v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u)),
-                                        tf32_cvt_rn(v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u)));
-          *reinterpret_cast<float4*>(sa + FS_PIECE + off) = lo;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[stage]);
-        if (++stage == FS_STAGES) { stage = 0; phase ^= 1; }
-      }
-  } else if (warp >= 8) {
+  } else if (warp >= 4) {
     // ---- epilogue: warp w owns TMEM lane quadrant q = w % 4 (slices s0 + 32 q + lane) and the 32 points
     //      h = (w - 8) / 4 of the tile; per point: the grid coordinate a = acc (tau_p n_p / ||g_p||) - (cen_p tau_p
     //      n_p + w/2) (one FMA; the planner's footprint has a cell of margin either side and the cell index is
     //      clamped to the private column), WT taps of the window polynomial (centred even / odd form), w_n-weighted
     //      into the slice's private column (cell-major: bank = lane, conflict-free)
-    const int q = warp & 3, h = (warp - 8) >> 2;
+    const int q = warp & 3, h = (warp - 4) >> 2;
     const int p = s0 + 32 * q + lane;
     const bool live = p < np;
     FPar f{};
@@ -325,7 +312,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     // window coefficients through shared memory into registers (read from the parameter bank, ptxas would
     // re-load them inside the loop)
     float* eos = reinterpret_cast<float*>(sm + FS_OFF_BAR + 128);   // [WT / 2][8]
-    if (warp == 8 && lane < WT / 2 * 8) eos[lane] = pw.eo[lane / 8][lane % 8];
+    if (warp == 4 && lane < WT / 2 * 8) eos[lane] = pw.eo[lane / 8][lane % 8];
     asm volatile("bar.sync 1, %0;" ::"r"(FS_EPI * 32) : "memory");
     float E[WT / 2][4], O[WT / 2][4];
 #pragma unroll
@@ -412,7 +399,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp >= 8 && warp < 12) {   // flush: the FS_EPI / 4 private columns of each slice, one atomic per cell
+  if (warp >= 4 && warp < 8) {   // flush: the FS_EPI / 4 private columns of each slice, one atomic per cell
     const int q = warp & 3, p = s0 + 32 * q + lane;
     if (p < np) {
       const FPar f = fp[p];
@@ -445,7 +432,7 @@ constexpr int FE_S = 64;           // slices per group (UMMA N)
 constexpr int FE_STAGES = 3;
 constexpr int FE_QCAP = 40;        // cells of interpolation polynomials staged per slice (wider: read from global)
 constexpr int FE_EPI = 16;         // epilogue warps: 4 per TMEM lane quadrant, 16 slices each
-constexpr int FE_THREADS = 32 * (8 + FE_EPI);
+constexpr int FE_THREADS = 32 * (4 + FE_EPI);
 constexpr int FE_PIECE = FE_T * 128;                      // one k-block of 128 targets: 16 KB
 constexpr int FE_B = FE_S * 128;                          // one k-block of the group's directions: 8 KB
 constexpr int FE_OFF_STAGE = FS_KBMAX * FE_B;             // 32 KB of resident directions
@@ -475,8 +462,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
   float* red = reinterpret_cast<float*>(sm + FE_OFF_RED);  // [2][4][FE_T]
   uint64_t* bfull = reinterpret_cast<uint64_t*>(sm + FE_OFF_BAR);
   uint64_t* xfull = bfull + 1;
-  uint64_t* full = xfull + FE_STAGES;
-  uint64_t* empty = full + FE_STAGES;
+  uint64_t* empty = xfull + FE_STAGES;
   uint64_t* tfull = empty + FE_STAGES;   // [2]
   uint64_t* tempty = tfull + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
@@ -512,13 +498,12 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
     mbar_init(bfull, 1);
     for (int s = 0; s < FE_STAGES; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&full[s], 4);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], FE_EPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmYlo)) : "memory");
   }
   if (warp == 2) {
@@ -587,10 +572,10 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
                        smem_u32(&tfull[b]))
                    : "memory");
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 4) {
     // ---- epilogue: warp w owns TMEM lane quadrant q = w % 4 (targets 32 q + lane of the tile) and the 16 slices
-    //      h = (w - 8) / 4 of the group
-    const int q = warp & 3, h = (warp - 8) >> 2;
+    //      h = (w - 4) / 4 of the group
+    const int q = warp & 3, h = (warp - 4) >> 2;
     int it = 0;
     for (int64_t t = t0; t < t1; ++t, ++it) {
       const int b = it & 1;
@@ -675,31 +660,36 @@ bool fused_spread_ok(int d, const float* x) {
   return d <= 32 * FS_KBMAX && d % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
 }
 
-cudaError_t launch_source_bound(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g32, int dp32,
-                                const float* inv_norm, int np, double* mu, unsigned* nb, unsigned* mm, unsigned* flag16,
-                                cudaStream_t st) {
+cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_t M, int d, double* mu, unsigned* nb,
+                               float* xlo, float* ylo, cudaStream_t st) {
   double* part = mu + d;   // [MEAN_PARTS][d] scratch after mu (source_bound_bytes)
   k_sample_mean_part<<<MEAN_PARTS, 128, 0, st>>>(x, N, d, part);
   k_sample_mean_fin<<<1, 128, 0, st>>>(N, d, part, mu, nb);
-  auto norms = [&](const float* z, int64_t n, unsigned* out) {
+  auto norms = [&](const float* z, int64_t n, unsigned* out, float* lo) {
     int64_t blocks = (n * 32 / 4 + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    k_norm_bound<<<static_cast<unsigned>(blocks), 256, 0, st>>>(z, n, d, mu, out);
+    k_norm_bound<<<static_cast<unsigned>(blocks), 256, 0, st>>>(z, n, d, mu, out, lo);
   };
-  norms(x, N, nb);
-  if (y) norms(y, M, nb + 4);
-  k_bound_ranges<<<(np + 7) / 8, 256, 0, st>>>(g32, dp32, d, inv_norm, np, mu, nb, y ? 1 : 0, mm, flag16);
+  norms(x, N, nb, xlo);
+  norms(y, M, nb + 4, ylo);
   return cudaGetLastError();
 }
 
-cudaError_t launch_proj_spread(const float* x, int64_t N, int d, const float* g32, int dp32, const float* inv_norm,
-                               int np, const float* w, const FPar* fp, const PolyWin& pw, int ncap, float* grid,
-                               const unsigned* flag16, cudaStream_t st) {
-  CUtensorMap tmA, tmX;
+cudaError_t launch_bound_ranges(const float* g32, int dp32, int d, const float* inv_norm, int np, const double* mu,
+                                const unsigned* nb, unsigned* mm, unsigned* flag16, cudaStream_t st) {
+  k_bound_ranges<<<(np + 7) / 8, 256, 0, st>>>(g32, dp32, d, inv_norm, np, mu, nb, 1, mm, flag16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_proj_spread(const float* x, const float* xlo, int64_t N, int d, const float* g32, int dp32,
+                               const float* inv_norm, int np, const float* w, const FPar* fp, const PolyWin& pw,
+                               int ncap, float* grid, const unsigned* flag16, cudaStream_t st) {
+  CUtensorMap tmA, tmX, tmXlo;
   const int nk = dp32 / 32;
   if (!encode_f32_map(&tmA, g32, static_cast<uint64_t>(np), static_cast<uint64_t>(dp32), static_cast<uint64_t>(dp32),
                       FS_S) ||
-      !encode_f32_map(&tmX, x, static_cast<uint64_t>(N), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FS_P))
+      !encode_f32_map(&tmX, x, static_cast<uint64_t>(N), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FS_P) ||
+      !encode_f32_map(&tmXlo, xlo, static_cast<uint64_t>(N), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FS_P))
     return cudaErrorInvalidValue;
   const int ntiles_s = (np + FS_S - 1) / FS_S;
   const int64_t ntp = (N + FS_P - 1) / FS_P;
@@ -708,7 +698,7 @@ cudaError_t launch_proj_spread(const float* x, int64_t N, int d, const float* g3
   if (ranges > ntp) ranges = static_cast<int>(ntp);
   auto go = [&](auto kern) {
     set_smem_attr_once(reinterpret_cast<const void*>(kern), FS_SMEM);
-    kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, nk, N, np, ranges, inv_norm, w, fp, pw, ncap, grid,
+    kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, tmXlo, nk, N, np, ranges, inv_norm, w, fp, pw, ncap, grid,
                                                          flag16);
   };
   switch (pw.w) {
@@ -728,27 +718,9 @@ namespace sks {
 
 // the TF32x2 lo piece of every coordinate, once (the eval CTAs of all slice groups load it by TMA instead of each
 // converting the same tile): lo = rn_tf32(y - trunc_tf32(y)), the kind::tf32 operand read of y being the hi piece
-__global__ void k_split_lo(const float4* __restrict__ y, int64_t n4, float4* __restrict__ lo) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float4 v = __ldcs(y + i);
-    __stcs(lo + i, make_float4(tf32_cvt_rn(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u)),
-                               tf32_cvt_rn(v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u)),
-                               tf32_cvt_rn(v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u)),
-                               tf32_cvt_rn(v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u))));
-  }
-}
-
 cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32, int dp32, const float* inv_norm, int np,
-                             const FPar* fp, const float* Q, int ncap, int w, double* s64, float* ylo,
+                             const FPar* fp, const float* Q, int ncap, int w, double* s64, const float* ylo,
                              const unsigned* flag16, cudaStream_t st) {
-  {
-    const int64_t n4 = M * d / 4;   // (d % 4 == 0 on the fused path)
-    int64_t blocks = (n4 + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    k_split_lo<<<static_cast<unsigned>(blocks), 256, 0, st>>>(reinterpret_cast<const float4*>(y), n4,
-                                                              reinterpret_cast<float4*>(ylo));
-  }
   CUtensorMap tmB, tmY, tmYlo;
   const int nk = dp32 / 32;
   if (!encode_f32_map(&tmB, g32, static_cast<uint64_t>(np), static_cast<uint64_t>(dp32), static_cast<uint64_t>(dp32),

@@ -193,22 +193,26 @@ cudaError_t launch_plan(const unsigned* mm, int np, const PlanConst& pc, const f
                         float* grid, unsigned* flag16, unsigned* summary, cudaStream_t st);
 // rows a1 + a5 fused (fused.cu; sources only, Fourier kernels at large N): the sources' projections are spread into
 // the grids from the tensor-core accumulators, never stored.  fused_spread_ok: d <= 128, d % 4 == 0, 16-byte
-// aligned x.  launch_source_bound: the sources' per-slice range bound (c_p +- rho') into mm[p][0..1] and combined
-// with the targets' exact range mm[p][2..3] (mu: source_bound_bytes(d) of scratch, nb: its last 16 bytes); then launch_plan,
-// then launch_proj_spread in place of the projection of x + launch_spread
+// aligned x.  launch_source_prep, then per batch launch_bound_ranges (mu: source_bound_bytes(d) of scratch, nb: its
+// last 32 bytes), launch_plan, launch_proj_spread in place of the projection of x + launch_spread
 bool fused_spread_ok(int d, const float* x);
-size_t source_bound_bytes(int d);   // scratch of launch_source_bound: mu, partial sums, nb (32 bytes, at the end)
-cudaError_t launch_source_bound(const float* x, int64_t N, const float* y, int64_t M, int d, const float* g32, int dp32,
-                                const float* inv_norm, int np, double* mu, unsigned* nb, unsigned* mm, unsigned* flag16,
-                                cudaStream_t st);
-cudaError_t launch_proj_spread(const float* x, int64_t N, int d, const float* g32, int dp32, const float* inv_norm,
-                               int np, const float* w, const FPar* fp, const PolyWin& pw, int ncap, float* grid,
-                               const unsigned* flag16, cudaStream_t st);
+size_t source_bound_bytes(int d);   // scratch of launch_source_prep: mu, partial sums, nb (32 bytes, at the end)
+// launch_source_prep (once per call, direction-independent): mu, the norm words nb (max ||z - mu||^2, max ||z||^2,
+// non-finite) of x (nb[0..2]) and y (nb[4..6]), and the TF32x2 lo pieces of both point sets (xlo: N d floats, ylo:
+// M d floats, row-major like x / y) in the same pass.  launch_bound_ranges (per slice batch): every slice's range
+// bound c_p +- rho' of both sets into mm[p]
+cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_t M, int d, double* mu, unsigned* nb,
+                               float* xlo, float* ylo, cudaStream_t st);
+cudaError_t launch_bound_ranges(const float* g32, int dp32, int d, const float* inv_norm, int np, const double* mu,
+                                const unsigned* nb, unsigned* mm, unsigned* flag16, cudaStream_t st);
+cudaError_t launch_proj_spread(const float* x, const float* xlo, int64_t N, int d, const float* g32, int dp32,
+                               const float* inv_norm, int np, const float* w, const FPar* fp, const PolyWin& pw,
+                               int ncap, float* grid, const unsigned* flag16, cudaStream_t st);
 // rows a1 + a7 fused for the targets (fused.cu): projections of y interpolated from the tensor-core accumulators,
 // s64[m] += sum over the slices of t_{m,p} (after launch_fft_filter wrote Q)
 // (ylo: M x d fp32 scratch for the pre-split lo piece of y)
 cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32, int dp32, const float* inv_norm, int np,
-                             const FPar* fp, const float* Q, int ncap, int w, double* s64, float* ylo,
+                             const FPar* fp, const float* Q, int ncap, int w, double* s64, const float* ylo,
                              const unsigned* flag16, cudaStream_t st);
 // row a5: g[p][l] = sum_n w_n phi_win(v_n - l) over the x projections (ES window, w taps); grid stride n_cap
 // det: one CTA per slice (no cross-CTA grid accumulation; the private grids are reduced in a fixed order)
