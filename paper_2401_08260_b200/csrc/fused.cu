@@ -186,7 +186,7 @@ static_assert(FS_SMEM <= 227 * 1024, "k_proj_spread shared memory");
 template <int WT>
 __global__ void __launch_bounds__(FS_THREADS, 1)
     k_proj_spread(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
-                  const __grid_constant__ CUtensorMap tmXlo, int nk, int64_t N,
+                  const __grid_constant__ CUtensorMap tmXlo, int nk, int klast, int64_t N,
                   int np, int ranges, const float* __restrict__ inv_norm, const float* __restrict__ w,
                   const FPar* __restrict__ fp, PolyWin pw, int ncap, float* __restrict__ grid,
                   const unsigned* __restrict__ flag16) {
@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
           const uint64_t db = umma_desc_sw128(sb + q * FS_PIECE);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {   // 4 MMAs of K = 8 tf32 (32 bytes) per 128-byte row
+            if (kb == nk - 1 && k >= klast) break;   // (k-steps wholly in the zero padding beyond d)
             const uint32_t acc = (kb > 0 || q > 0 || k > 0) ? 1u : 0u;
             const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
             asm volatile(
@@ -357,21 +358,45 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
         }
         if (fast) {
           // branch-free: points beyond N carry weight 0 (their rows are zero-filled by TMA; the clamp keeps their
-          // cell in range)
+          // cell in range).  Two points per step: the grid coordinate and the window polynomials of both in packed
+          // fp32x2 FMAs (FFMA2, the same operations and rounding as the scalar form), then the two points'
+          // read-modify-writes one after the other (their cells may coincide)
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const float wi = w8[jj];
-            const float a = fmaf(__uint_as_float(v[jj]), ga, gb), fl = floorf(a);
-            const float u = (a - fl) - 0.5f, u2 = u * u;
-            const int cl = min(max(static_cast<int>(fl) + 1 - f.lmin, 0), cmax);   // (memory safety only)
-            SKS_CHECK(wi == 0.f || cl == static_cast<int>(fl) + 1 - f.lmin);   // the bound holds: no clamping
-            float* cell = col + cl * FS_S;
+          for (int jj = 0; jj < 8; jj += 2) {
+            const float2 a = __ffma2_rn(make_float2(__uint_as_float(v[jj]), __uint_as_float(v[jj + 1])),
+                                        make_float2(ga, ga), make_float2(gb, gb));
+            const float2 fl = make_float2(floorf(a.x), floorf(a.y));
+            const float2 u = __fadd2_rn(__fadd2_rn(a, make_float2(-fl.x, -fl.y)), make_float2(-0.5f, -0.5f));
+            const float2 u2 = __fmul2_rn(u, u);
+            const int cl0 = min(max(static_cast<int>(fl.x) + 1 - f.lmin, 0), cmax);   // (memory safety only)
+            const int cl1 = min(max(static_cast<int>(fl.y) + 1 - f.lmin, 0), cmax);
+            SKS_CHECK(w8[jj] == 0.f || cl0 == static_cast<int>(fl.x) + 1 - f.lmin);   // the bound holds: no clamping
+            SKS_CHECK(w8[jj + 1] == 0.f || cl1 == static_cast<int>(fl.y) + 1 - f.lmin);
+            float2 tl[WT / 2], th[WT / 2];   // taps m and WT - 1 - m of both points
 #pragma unroll
             for (int m = 0; m < WT / 2; ++m) {
-              const float Em = fmaf(fmaf(fmaf(E[m][3], u2, E[m][2]), u2, E[m][1]), u2, E[m][0]);
-              const float Om = fmaf(fmaf(fmaf(O[m][3], u2, O[m][2]), u2, O[m][1]), u2, O[m][0]);
-              cell[m * FS_S] = fmaf(wi, fmaf(u, Om, Em), cell[m * FS_S]);
-              cell[(WT - 1 - m) * FS_S] = fmaf(wi, fmaf(-u, Om, Em), cell[(WT - 1 - m) * FS_S]);
+              const float2 Em = __ffma2_rn(
+                  __ffma2_rn(__ffma2_rn(make_float2(E[m][3], E[m][3]), u2, make_float2(E[m][2], E[m][2])), u2,
+                             make_float2(E[m][1], E[m][1])),
+                  u2, make_float2(E[m][0], E[m][0]));
+              const float2 Om = __ffma2_rn(
+                  __ffma2_rn(__ffma2_rn(make_float2(O[m][3], O[m][3]), u2, make_float2(O[m][2], O[m][2])), u2,
+                             make_float2(O[m][1], O[m][1])),
+                  u2, make_float2(O[m][0], O[m][0]));
+              tl[m] = __ffma2_rn(u, Om, Em);
+              th[m] = __ffma2_rn(make_float2(-u.x, -u.y), Om, Em);
+            }
+            float* cell = col + cl0 * FS_S;
+#pragma unroll
+            for (int m = 0; m < WT / 2; ++m) {
+              cell[m * FS_S] = fmaf(w8[jj], tl[m].x, cell[m * FS_S]);
+              cell[(WT - 1 - m) * FS_S] = fmaf(w8[jj], th[m].x, cell[(WT - 1 - m) * FS_S]);
+            }
+            cell = col + cl1 * FS_S;
+#pragma unroll
+            for (int m = 0; m < WT / 2; ++m) {
+              cell[m * FS_S] = fmaf(w8[jj + 1], tl[m].y, cell[m * FS_S]);
+              cell[(WT - 1 - m) * FS_S] = fmaf(w8[jj + 1], th[m].y, cell[(WT - 1 - m) * FS_S]);
             }
           }
         } else if (live) {   // footprint wider than the private column: global atomics for this slice
@@ -449,7 +474,7 @@ __device__ __forceinline__ int qswz(int c) { return c ^ ((c >> 3) & 7); }
 
 __global__ void __launch_bounds__(FE_THREADS, 1)
     k_proj_eval(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY,
-                const __grid_constant__ CUtensorMap tmYlo, int nk, int64_t M,
+                const __grid_constant__ CUtensorMap tmYlo, int nk, int klast, int64_t M,
                 int np, int ranges, const float* __restrict__ inv_norm, const FPar* __restrict__ fp,
                 const float* __restrict__ Q, int ncap, int w, double* __restrict__ s64,
                 const unsigned* __restrict__ flag16) {
@@ -477,7 +502,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
   // the group's per-slice constants and interpolation polynomials (all threads)
   for (int ls = threadIdx.x; ls < FE_S; ls += FE_THREADS) {
     const int p = s0 + ls;
-    float4 c = make_float4(0.f, 0.f, __int_as_float(0), __int_as_float(0));
+    float4 c = make_float4(0.f, 0.f, __int_as_float(0), __int_as_float(1));   // (dead slice: cell 0 of a zero table)
     if (p < np) {
       const FPar f = fp[p];
       const float taun = f.tau * static_cast<float>(1 << f.logn);
@@ -554,6 +579,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
           const uint64_t da = umma_desc_sw128(sa + q * FE_PIECE);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
+            if (kb == nk - 1 && k >= klast) break;   // (k-steps wholly in the zero padding beyond d)
             const uint32_t acc = (kb > 0 || q > 0 || k > 0) ? 1u : 0u;
             const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
             asm volatile(
@@ -576,6 +602,8 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
     // ---- epilogue: warp w owns TMEM lane quadrant q = w % 4 (targets 32 q + lane of the tile) and the 16 slices
     //      h = (w - 4) / 4 of the group
     const int q = warp & 3, h = (warp - 4) >> 2;
+    bool fits = true;   // (warp-uniform) every table of the warp's slices is staged in shared memory
+    for (int j = 0; j < 16; ++j) fits &= __float_as_int(sp[16 * h + j].w) <= FE_QCAP;
     int it = 0;
     for (int64_t t = t0; t < t1; ++t, ++it) {
       const int b = it & 1;
@@ -594,6 +622,40 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
       float acc = 0.f;
+      if (fits) {
+        // every table of the warp's 16 slices is staged: 4 slices at a time, their cells and both table loads
+        // first, then the 4 Horner chains (independent: latency hidden by ILP).  Dead slices (p >= np) have a zero
+        // table and WA = 1: they add exactly 0
+#pragma unroll
+        for (int j0 = 0; j0 < 16; j0 += 4) {
+          float fr[4];
+          float4 c0[4], c1[4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int ls = 16 * h + j0 + jj;
+            const float4 c = sp[ls];   // broadcast
+            const float a = fmaf(__uint_as_float(v[j0 + jj]), c.x, c.y), fl = floorf(a);
+            fr[jj] = a - fl;
+            // (fl is an integer of magnitude < 2^22: its int value from the 1.5 2^23 shift, no F2I)
+            int cl = (__float_as_int(fl + 12582912.f) - 0x4B400000) + 1 - __float_as_int(c.z);
+            const int wq = __float_as_int(c.w);
+            SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < wq));
+            cl = cl < 0 ? 0 : (cl >= wq ? wq - 1 : cl);   // (memory safety only)
+            c0[jj] = sq[ls * FE_QCAP + qswz(cl)];
+            c1[jj] = sq[(FE_S + ls) * FE_QCAP + qswz(cl)];
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            float tv = fmaf(c1[jj].w, fr[jj], c1[jj].z);
+            tv = fmaf(tv, fr[jj], c1[jj].y);
+            tv = fmaf(tv, fr[jj], c1[jj].x);
+            tv = fmaf(tv, fr[jj], c0[jj].w);
+            tv = fmaf(tv, fr[jj], c0[jj].z);
+            tv = fmaf(tv, fr[jj], c0[jj].y);
+            acc += fmaf(tv, fr[jj], c0[jj].x);
+          }
+        }
+      } else {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int ls = 16 * h + j;
@@ -621,6 +683,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
         tv = fmaf(tv, fr, c0.y);
         tv = fmaf(tv, fr, c0.x);
         acc += (s0 + ls < np) ? tv : 0.f;
+      }
       }
       float* rb = red + (b * 4) * FE_T;
       rb[h * FE_T + 32 * q + lane] = acc;
@@ -698,7 +761,7 @@ cudaError_t launch_proj_spread(const float* x, const float* xlo, int64_t N, int 
   if (ranges > ntp) ranges = static_cast<int>(ntp);
   auto go = [&](auto kern) {
     set_smem_attr_once(reinterpret_cast<const void*>(kern), FS_SMEM);
-    kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, tmXlo, nk, N, np, ranges, inv_norm, w, fp, pw, ncap, grid,
+    kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, tmXlo, nk, (d - 32 * (nk - 1) + 7) / 8, N, np, ranges, inv_norm, w, fp, pw, ncap, grid,
                                                          flag16);
   };
   switch (pw.w) {
@@ -734,7 +797,7 @@ cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32,
   if (ranges < 1) ranges = 1;
   if (ranges > ntt) ranges = static_cast<int>(ntt);
   set_smem_attr_once(reinterpret_cast<const void*>(k_proj_eval), FE_SMEM);
-  k_proj_eval<<<ngroups * ranges, FE_THREADS, FE_SMEM, st>>>(tmB, tmY, tmYlo, nk, M, np, ranges, inv_norm, fp, Q, ncap, w, s64,
+  k_proj_eval<<<ngroups * ranges, FE_THREADS, FE_SMEM, st>>>(tmB, tmY, tmYlo, nk, (d - 32 * (nk - 1) + 7) / 8, M, np, ranges, inv_norm, fp, Q, ncap, w, s64,
                                                             flag16);
   return cudaGetLastError();
 }
