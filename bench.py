@@ -87,6 +87,16 @@ def roofline_model(slot, cfg, P, plan):
         return comp[slot], comp[slot], None
     if slot == "sortsum":   # the sort stage (fork .. join of its kernels on two streams)
         return SORT_B_PER_SP * L * P, sum(comp.values()), None
+    if plan.get("fused"):   # the fused large-N path (fused.cu): projection + spread / projection + interpolation
+        if slot == "minmax":   # source prep: one pass over x and y (norm bounds) writing their TF32x2 lo pieces
+            by = 4 * (N + M) * d * 2
+            return by, by, None
+        if slot == "spread":   # per x slice-point: 2 d projection flops (tensor) + w taps (FP32); x and its lo piece
+            by = 8 * N * d + 4 * N + 4 * n * P
+            return by, by, ("tensor", 2.0 * N * d * P), ("alu", 2.0 * N * P * w * 5)
+        if slot == "eval":     # per y slice-point: 2 d projection flops (tensor) + one degree-7 Horner (FP32)
+            by = 8 * M * d + 8 * M + 4 * n * P
+            return by, by, ("tensor", 2.0 * M * d * P), ("alu", 2.0 * M * P * 7)
     if slot == "spread":    # per x slice-point: w taps, each a degree-7 window polynomial (even/odd form: 4 FMA
         #                     per tap) and one FMA into the grid
         return 4 * N * P, 4 * N * P + 4 * N + 4 * n * P, ("alu", 2.0 * N * P * w * 5)
@@ -112,14 +122,16 @@ def roofline(slot, cfg, P, plan, ms_per_launch, pk, traffic):
     """achieved / peak of one kernel, Sec. 8(d) units: the bound is the larger of the HBM time of its Sec. 8(d)
     bytes and the time of its algorithmic arithmetic at peak (tensor for the projection, FP32 FMA for the
     spread / interpolation).  Also the compulsory-traffic fraction (this build's own minimum bytes)."""
-    by, comp, fl = roofline_model(slot, cfg, P, plan)
-    kind, fl = fl if fl else (None, 0.0)
+    by, comp, *work = roofline_model(slot, cfg, P, plan)
+    work = [x for x in work if x]
     t = ms_per_launch * 1e-3
     alu = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     peaks_tf = {"tensor": tensor_peak(pk, plan.get("proj_mode")),
                 "alu": (alu, "148 SMs x 128 FP32 lanes x 2 flop/FMA x sm_max_mhz (MEASURED_PEAKS.json; B200_PROFILING "
                              "unit counts)")}
     hbm = pk["hbm_gbs"]
+    # the binding resource of the model: the largest of the HBM time and each arithmetic unit's time at its peak
+    kind, fl = max(work, key=lambda kf: kf[1] / (peaks_tf[kf[0]][0] * 1e12)) if work else (None, 0.0)
     if fl and fl / (peaks_tf[kind][0] * 1e12) > by / (hbm * 1e9):
         r = {"kernel": slot, "bound": kind, "achieved": fl / t / 1e12, "peak": peaks_tf[kind][0], "unit": "TFLOP/s",
              "peak_source": peaks_tf[kind][1], "algorithmic_flops_per_launch": fl}
@@ -127,6 +139,9 @@ def roofline(slot, cfg, P, plan, ms_per_launch, pk, traffic):
         r = {"kernel": slot, "bound": "hbm", "achieved": by / t / 1e9, "peak": hbm, "unit": "GB/s",
              "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else "")}
     r["frac"] = r["achieved"] / r["peak"]
+    # every modelled resource's time at its peak / the launch time (the headline frac is the largest)
+    r["frac_by_resource"] = {"hbm": by / (hbm * 1e9) / t,
+                             **{k: f / (peaks_tf[k][0] * 1e12) / t for k, f in work}}
     r["model"] = "SURVEY.md Sec. 8(d) per-slice-point work x slice-points per launch"
     r["algorithmic_bytes_per_launch"] = by
     r["compulsory_bytes_per_launch"] = comp
