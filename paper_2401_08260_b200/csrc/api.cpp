@@ -165,7 +165,7 @@ constexpr size_t kStatusBytes = 64;
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
   size_t status = 0, s64 = 0, mm = 0, Z = 0, xs3 = 0, part = 0, tot = 0, sp = 0, grid = 0, D = 0, fpar = 0, Q = 0,
-         what = 0, bound = 0, xlo = 0, ylo = 0, dpart = 0, total = 0;
+         what = 0, bound = 0, xh = 0, xl = 0, yh = 0, yl = 0, rsx = 0, rsy = 0, dpart = 0, total = 0;
   int dgroups = 0;   // deterministic mode: TargetAcc groups of the whole call
 };
 
@@ -267,8 +267,14 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, 
     L.what = take(sizeof(double) * 2 * sks::kNdftWidth * static_cast<size_t>(nbat));
     if (fused) {
       L.bound = take(sks::source_bound_bytes(d));
-      L.xlo = take(sizeof(float) * static_cast<size_t>(N) * d);   // the TF32x2 lo pieces of the sources and the
-      L.ylo = take(sizeof(float) * static_cast<size_t>(M) * d);   // targets (written by the bound pass, fused path)
+      // both point sets as FP16x2 operands (hi, lo: fp16 [rows][dp16]) and their per-32-row scales (source prep)
+      const size_t dp16 = static_cast<size_t>(sks::fused_dp16(d));
+      L.xh = take(sizeof(uint16_t) * static_cast<size_t>(N) * dp16);
+      L.xl = take(sizeof(uint16_t) * static_cast<size_t>(N) * dp16);
+      L.yh = take(sizeof(uint16_t) * static_cast<size_t>(M) * dp16);
+      L.yl = take(sizeof(uint16_t) * static_cast<size_t>(M) * dp16);
+      L.rsx = take(sizeof(float) * static_cast<size_t>((N + 127) / 128 * 4));   // per 32-row group (whole tiles)
+      L.rsy = take(sizeof(float) * static_cast<size_t>((M + 127) / 128 * 4));
     }
   }
   if (dgroups) {
@@ -488,9 +494,10 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
   }
   launches += 1;
   const ProjMode pm = pr.with_Z ? proj_mode_call(pr.d, o.proj, x, pr.N, y, pr.M) : PM_AUTO;
-  // fused path: the shape qualifies, the points are TMA-readable, and the projection is TF32x2 (the variant the
-  // fused kernel computes; d <= 128)
-  const bool fused = fshape && pm == PM_TF32X2 && s_out && sks::fused_spread_ok(pr.d, x) && sks::fused_spread_ok(pr.d, y);
+  // fused path: the shape qualifies, the points are 16-byte aligned rows, and the projection variant is the automatic
+  // choice or FP16x2 (the fused kernels compute FP16x2 with per-tile scales; d <= 128)
+  const bool fused = fshape && (o.proj == 0 || o.proj == PM_FP16X2) && s_out && sks::fused_spread_ok(pr.d, x) &&
+                     sks::fused_spread_ok(pr.d, y);
   const bool tc = pr.with_Z && pm == PM_BF16X3;
   const bool tf = pr.with_Z && pm == PM_TF32X2;
   const bool th = pr.with_Z && pm == PM_FP16X2;
@@ -499,11 +506,13 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
     SKS_CUDA(sks::launch_split3(x, pr.N, y, pr.M, pr.d, ws + L.xs3, st));
     ++launches;
   }
-  if (fused) {   // direction-independent: the sources' centre and radius, the targets' radius, both lo pieces
+  if (fused) {   // direction-independent: the sources' centre and radius, the targets' radius, FP16x2 operands
     ProfScope ps(PS_MINMAX, st);
     SKS_CUDA(sks::launch_source_prep(x, pr.N, y, pr.M, pr.d, reinterpret_cast<double*>(ws + L.bound),
                                      reinterpret_cast<unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32),
-                                     reinterpret_cast<float*>(ws + L.xlo), reinterpret_cast<float*>(ws + L.ylo), st));
+                                     reinterpret_cast<uint16_t*>(ws + L.xh), reinterpret_cast<uint16_t*>(ws + L.xl),
+                                     reinterpret_cast<float*>(ws + L.rsx), reinterpret_cast<uint16_t*>(ws + L.yh),
+                                     reinterpret_cast<uint16_t*>(ws + L.yl), reinterpret_cast<float*>(ws + L.rsy), st));
     launches += 4;
   }
   for (int b0 = 0; b0 < pr.nslices; b0 += batch) {
@@ -624,8 +633,11 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
       }
       if (fused) {
         ProfScope ps(PS_SPREAD, st);
-        SKS_CUDA(sks::launch_proj_spread(x, reinterpret_cast<const float*>(ws + L.xlo), pr.N, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
-                                         dirs->inv + b0, nbat, w, fp, plan.pw, kNcap, grid, flag16, st));
+        SKS_CUDA(sks::launch_proj_spread(reinterpret_cast<const uint16_t*>(ws + L.xh),
+                                         reinterpret_cast<const uint16_t*>(ws + L.xl),
+                                         reinterpret_cast<const float*>(ws + L.rsx), pr.N, pr.d,
+                                         static_cast<const uint16_t*>(dirs->g16) + static_cast<int64_t>(b0) * dirs->K3,
+                                         dirs->K3, dirs->inv + b0, nbat, w, fp, plan.pw, kNcap, grid, flag16, st));
       } else {
         ProfScope ps(PS_SPREAD, st);
         SKS_CUDA(sks::launch_spread(zv, w, nbat, fp, kNcap, plan.pw, pr.k.kind == SKS_LAPLACIAN, det, grid, flag16, st));
@@ -655,9 +667,11 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
                                                 : target_acc((nbat + sks::kEvalGroup - 1) / sks::kEvalGroup);
     if (fused) {
       ProfScope ps(PS_EVAL, st);
-      SKS_CUDA(sks::launch_proj_eval(y, pr.M, pr.d, dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32,
-                                     dirs->inv + b0, nbat, ea.fp, ea.Q, kNcap, o.w, s64,
-                                     reinterpret_cast<const float*>(ws + L.ylo), flag16, st));
+      SKS_CUDA(sks::launch_proj_eval(reinterpret_cast<const uint16_t*>(ws + L.yh),
+                                     reinterpret_cast<const uint16_t*>(ws + L.yl),
+                                     reinterpret_cast<const float*>(ws + L.rsy), pr.M, pr.d,
+                                     static_cast<const uint16_t*>(dirs->g16) + static_cast<int64_t>(b0) * dirs->K3,
+                                     dirs->K3, dirs->inv + b0, nbat, ea.fp, ea.Q, kNcap, o.w, s64, flag16, st));
       launches += 1;
     } else if (pt.fourier || pt.moment) {
       ProfScope ps(PS_EVAL, st);
@@ -681,7 +695,7 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
   info.slice_batch = batch;
   info.n_batches = nbatches;
   info.launches = launches;
-  info.proj_mode = !pr.with_Z ? 0 : tc ? 2 : tf ? 3 : 4;
+  info.proj_mode = !pr.with_Z ? 0 : fused ? 4 : tc ? 2 : tf ? 3 : 4;
   info.fused = fused ? 1 : 0;
   *info_out = info;
   return SKS_OK;

@@ -15,6 +15,7 @@
 //                   slice each (TMEM lane = slice) and spread w_n phi(v - l) into the slice's private grid column
 //                   in shared memory ([half][cell][slice]: conflict-free read-modify-writes, no atomics), flushed
 //                   once per CTA with global atomics
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -57,53 +58,97 @@ __global__ void k_sample_mean_fin(int64_t N, int d, const double* __restrict__ p
   if (threadIdx.x < 8) nb[threadIdx.x] = 0u;
 }
 
-__device__ __forceinline__ float tf32_lo(float v) {
-  return tf32_cvt_rn(v - __uint_as_float(__float_as_uint(v) & 0xffffe000u));
-}
-__device__ __forceinline__ float4 tf32_lo4(float4 v) {
-  return make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+// The fused kernels' operands (reading R2, FP16x2 with one scale per 32-row group -- the rows one epilogue warp
+// handles in both fused kernels): for the group's rows
+//   s_g = 2^(14 - e), max |x| over the group = m 2^e (m in [0.5, 1)): s_g max|x| < 2^14 (s_g = 1 for a zero group)
+//   hi = f16_rn(s_g x), lo = f16_rn(s_g x - hi)         (|s_g x - hi - lo| <= 2^-22 |s_g x| + 2^-25)
+// stored as two fp16 arrays [rows][dp16] (dp16 = d rounded up to 8, pad columns zero) and rs[g] = 1 / (2^8 s_g):
+// the tensor cores accumulate (2^8 g) . (s_g x) exactly in fp32 (directions fp16 x 2^8, exact: R1), and the
+// epilogue's rs[g] (a power of two) restores <g, x> without rounding.
+constexpr int PR_U = 8;   // rows per batch (loads in flight per lane)
+
+__device__ __forceinline__ float group_scale(float m) {   // s_g from the group's max |x| (finite, >= 0)
+  if (!(m > 0.f) || !(m < 3.0e38f)) return 1.0f;
+  int e;
+  frexpf(m, &e);
+  e = e < -100 ? -100 : e;
+  return ldexpf(1.0f, 14 - e);
 }
 
-// one warp per row (d <= 128: one float4 per lane), fp32 sums of squares, maxima as float bits (non-negative
-// floats order as unsigned ints); out[0] = max ||x - mu||^2, out[1] = max ||x||^2, out[2] = non-finite seen.
-// The same pass writes the TF32x2 lo piece of every element, lo = rn_tf32(x - trunc_tf32(x)) (reading R2; the
-// fused kernels read the raw tile as the hi piece and this array as the lo piece)
-__global__ void __launch_bounds__(256) k_norm_bound(const float* __restrict__ x, int64_t N, int d,
-                                                    const double* __restrict__ mu, unsigned* __restrict__ out,
-                                                    float* __restrict__ lo) {
+// one warp per 32-row group (grid-stride), lane l dims 4 l .. 4 l + 3 (d <= 128).  Pass 1 streams the rows from
+// HBM: out[0] = max ||x - mu||^2, out[1] = max ||x||^2 (float bits: non-negative floats order as unsigned ints),
+// out[2] = non-finite seen, and the group's max |x|; pass 2 re-reads the group (12.8 KB at d = 100: an L2 hit)
+// and writes its fp16 hi / lo rows
+__global__ void __launch_bounds__(256) k_prep_f16(const float* __restrict__ x, int64_t N, int d, int dp16,
+                                                  const double* __restrict__ mu, unsigned* __restrict__ out,
+                                                  __half* __restrict__ xh, __half* __restrict__ xl,
+                                                  float* __restrict__ rs) {
   __shared__ float smu[128];
   for (int j = threadIdx.x; j < 128; j += blockDim.x) smu[j] = j < d ? static_cast<float>(mu[j]) : 0.f;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const bool on = 4 * lane < d;
+  const bool on = 4 * lane < d, pad = 4 * lane < dp16;
   const float4 m4 = on ? make_float4(smu[4 * lane], smu[4 * lane + 1], smu[4 * lane + 2], smu[4 * lane + 3])
                        : make_float4(0.f, 0.f, 0.f, 0.f);
   float r2max = 0.f, n2max = 0.f;
   bool bad = false;
-  constexpr int U = 4;   // rows per warp and iteration, all loads in flight first
-  for (int64_t i0 = w0 * U; i0 < N; i0 += nw * U) {
-    float4 v[U];
+  const int64_t ngroups = (N + 31) / 32;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t g = w0; g < ngroups; g += nw) {
+    const int64_t r0 = g * 32;
+    float am = 0.f;
+    for (int b = 0; b < 32; b += PR_U) {
+      float4 v[PR_U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (on && i0 + u < N) v[u] = __ldcs(reinterpret_cast<const float4*>(x + (i0 + u) * d) + lane);   // streamed once
+      for (int u = 0; u < PR_U; ++u) {   // all loads in flight first
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (on && r0 + b + u < N) v[u] = __ldcg(reinterpret_cast<const float4*>(x + (r0 + b + u) * d) + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < PR_U; ++u) {
+        am = fmaxf(am, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+        const float a = v[u].x - m4.x, bb = v[u].y - m4.y, c = v[u].z - m4.z, e = v[u].w - m4.w;
+        float r2 = fmaf(a, a, fmaf(bb, bb, fmaf(c, c, e * e)));
+        float n2 = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, v[u].w * v[u].w)));
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+          n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        }
+        bad |= !isfinite(n2);
+        r2max = fmaxf(r2max, r2);
+        n2max = fmaxf(n2max, n2);
+      }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (on && i0 + u < N) __stcg(reinterpret_cast<float4*>(lo + (i0 + u) * d) + lane, tf32_lo4(v[u]));
-      const float a = v[u].x - m4.x, b = v[u].y - m4.y, c = v[u].z - m4.z, e = v[u].w - m4.w;
-      float r2 = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
-      float n2 = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, v[u].w * v[u].w)));
+    for (int o = 16; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+    const float sg = group_scale(am);
+    if (lane == 0) rs[g] = 1.0f / (256.0f * sg);   // (exact: a power of two)
+    if (!pad) continue;
+    for (int b = 0; b < 32; b += PR_U) {
+      float4 v[PR_U];
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+      for (int u = 0; u < PR_U; ++u) {
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (on && r0 + b + u < N) v[u] = __ldcs(reinterpret_cast<const float4*>(x + (r0 + b + u) * d) + lane);
       }
-      bad |= !isfinite(n2);
-      r2max = fmaxf(r2max, r2);
-      n2max = fmaxf(n2max, n2);
+#pragma unroll
+      for (int u = 0; u < PR_U; ++u) {
+        const int64_t r = r0 + b + u;
+        if (r >= N) break;
+        const float a0 = v[u].x * sg, a1 = v[u].y * sg, a2 = v[u].z * sg, a3 = v[u].w * sg;
+        const __half2 h01 = __floats2half2_rn(a0, a1), h23 = __floats2half2_rn(a2, a3);
+        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+        const __half2 l01 = __floats2half2_rn(a0 - f01.x, a1 - f01.y), l23 = __floats2half2_rn(a2 - f23.x, a3 - f23.y);
+        uint2 hv, lv;
+        hv.x = *reinterpret_cast<const uint32_t*>(&h01);
+        hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+        lv.x = *reinterpret_cast<const uint32_t*>(&l01);
+        lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+        __stcs(reinterpret_cast<uint2*>(xh + r * dp16) + lane, hv);
+        __stcs(reinterpret_cast<uint2*>(xl + r * dp16) + lane, lv);
+      }
     }
   }
   if (lane == 0) {
@@ -171,13 +216,17 @@ __global__ void k_bound_ranges(const float* __restrict__ g32, int dp32, int d, c
 constexpr int FS_S = 128;          // slices per tile (UMMA M = TMEM lanes)
 constexpr int FS_P = 128;          // points per tile (UMMA N)
 constexpr int FS_STAGES = 3;
-constexpr int FS_KBMAX = 4;        // k-blocks of 32 dims: d <= 128
+constexpr int FS_KBMAX = 2;        // k-blocks of 64 fp16 dims (128-byte rows): d <= 128
 constexpr int FS_WCAP = 32;        // private grid cells per slice (wider footprints: global atomics)
 constexpr int FS_EPI = 16;         // epilogue warps: 4 per TMEM lane quadrant, 32 points of the tile each
-constexpr int FS_THREADS = 32 * (4 + FS_EPI);   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 -, w4.. epilogue
+// warp roles: w0 .. FS_EPI - 1 epilogue, then TMEM alloc, -, TMA producer, MMA issuer.  The issuers take the highest
+// warp ids: the warp scheduler prefers the highest ready warp id, so the single-thread MMA loop is never starved
+// of issue slots by the busy epilogue warps of its SM sub-partition
+constexpr int FS_WALLOC = FS_EPI, FS_WTMA = FS_EPI + 2, FS_WMMA = FS_EPI + 3;
+constexpr int FS_THREADS = 32 * (4 + FS_EPI);
 constexpr int FS_PIECE = FS_P * 128;                      // one k-block of 128 points: 16 KB
 constexpr int FS_A = FS_S * 128;                          // one k-block of the directions: 16 KB
-constexpr int FS_OFF_STAGE = FS_KBMAX * FS_A;             // 64 KB of resident directions
+constexpr int FS_OFF_STAGE = FS_KBMAX * FS_A;             // 32 KB of resident directions
 constexpr int FS_OFF_GRID = FS_OFF_STAGE + FS_STAGES * 2 * FS_PIECE;
 constexpr int FS_OFF_BAR = FS_OFF_GRID + (FS_EPI / 4) * FS_WCAP * FS_S * 4;
 constexpr int FS_SMEM = FS_OFF_BAR + 256 + 1024;          // + barriers, TMEM slot, alignment slack
@@ -187,7 +236,8 @@ template <int WT>
 __global__ void __launch_bounds__(FS_THREADS, 1)
     k_proj_spread(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXlo, int nk, int klast, int64_t N,
-                  int np, int ranges, const float* __restrict__ inv_norm, const float* __restrict__ w,
+                  int np, int ranges, const float* __restrict__ rs, const float* __restrict__ inv_norm,
+                  const float* __restrict__ w,
                   const FPar* __restrict__ fp, PolyWin pw, int ncap, float* __restrict__ grid,
                   const unsigned* __restrict__ flag16) {
   if (call_failed(flag16)) return;
@@ -221,7 +271,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmXlo)) : "memory");
   }
-  if (warp == 2) {
+  if (warp == FS_WALLOC) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(2 * FS_P));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -231,11 +281,11 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer: the tile's directions once, then the raw fp32 point tiles (the hi piece) and their lo
-    //      pieces (written by the k_norm_bound pass)
+  if (warp == FS_WTMA && lane == 0) {
+    // ---- TMA producer: the tile's directions (fp16 x 2^8) once, then the point tiles' fp16 hi and lo pieces
+    //      (written by the k_prep_f16 pass)
     mbar_expect_tx(afull, nk * FS_A);
-    for (int kb = 0; kb < nk; ++kb) tma_load_2d(&tmA, afull, sm + kb * FS_A, kb * 32, s0);
+    for (int kb = 0; kb < nk; ++kb) tma_load_2d(&tmA, afull, sm + kb * FS_A, kb * 64, s0);
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = t0; t < t1; ++t)
@@ -243,13 +293,13 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         unsigned char* sa = sm + FS_OFF_STAGE + stage * 2 * FS_PIECE;
         mbar_expect_tx(&xfull[stage], 2 * FS_PIECE);
-        tma_load_2d(&tmX, &xfull[stage], sa, kb * 32, static_cast<int>(t * FS_P));
-        tma_load_2d(&tmXlo, &xfull[stage], sa + FS_PIECE, kb * 32, static_cast<int>(t * FS_P));
+        tma_load_2d(&tmX, &xfull[stage], sa, kb * 64, static_cast<int>(t * FS_P));
+        tma_load_2d(&tmXlo, &xfull[stage], sa + FS_PIECE, kb * 64, static_cast<int>(t * FS_P));
         if (++stage == FS_STAGES) { stage = 0; phase ^= 1; }
       }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer: D[slice][point] += A (directions, tf32-exact) . B (hi, then lo)
-    constexpr uint32_t idesc = idesc_tf32(FS_S, FS_P);
+  } else if (warp == FS_WMMA && lane == 0) {
+    // ---- MMA issuer: D[slice][point] += A (2^8 g, fp16-exact) . B (s_t x: hi, then lo), K = 16 per MMA
+    constexpr uint32_t idesc = idesc_f16(FS_S, FS_P);
     mbar_wait(afull, 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -275,7 +325,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
                 "setp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
                 "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
           }
         }
@@ -288,13 +338,13 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
                        smem_u32(&tfull[b]))
                    : "memory");
     }
-  } else if (warp >= 4) {
+  } else if (warp < FS_EPI) {
     // ---- epilogue: warp w owns TMEM lane quadrant q = w % 4 (slices s0 + 32 q + lane) and the 32 points
     //      h = (w - 8) / 4 of the tile; per point: the grid coordinate a = acc (tau_p n_p / ||g_p||) - (cen_p tau_p
     //      n_p + w/2) (one FMA; the planner's footprint has a cell of margin either side and the cell index is
     //      clamped to the private column), WT taps of the window polynomial (centred even / odd form), w_n-weighted
     //      into the slice's private column (cell-major: bank = lane, conflict-free)
-    const int q = warp & 3, h = (warp - 4) >> 2;
+    const int q = warp & 3, h = warp >> 2;
     const int p = s0 + 32 * q + lane;
     const bool live = p < np;
     FPar f{};
@@ -313,7 +363,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     // window coefficients through shared memory into registers (read from the parameter bank, ptxas would
     // re-load them inside the loop)
     float* eos = reinterpret_cast<float*>(sm + FS_OFF_BAR + 128);   // [WT / 2][8]
-    if (warp == 4 && lane < WT / 2 * 8) eos[lane] = pw.eo[lane / 8][lane % 8];
+    if (warp == 0 && lane < WT / 2 * 8) eos[lane] = pw.eo[lane / 8][lane % 8];
     asm volatile("bar.sync 1, %0;" ::"r"(FS_EPI * 32) : "memory");
     float E[WT / 2][4], O[WT / 2][4];
 #pragma unroll
@@ -339,6 +389,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
       const int64_t i0 = t * FS_P + c0;
       const float wv = wnext;
       wnext = wload(t + 1);
+      const float gat = ga * __ldg(rs + 4 * t + h);   // the 32-point group's 1 / (2^8 s_g): exact (a power of two)
       mbar_wait_sleep(&tfull[b], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t taddr = tmem_base + static_cast<uint32_t>(b * FS_P + c0) + (static_cast<uint32_t>(32 * q) << 16);
@@ -364,7 +415,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
 #pragma unroll
           for (int jj = 0; jj < 8; jj += 2) {
             const float2 a = __ffma2_rn(make_float2(__uint_as_float(v[jj]), __uint_as_float(v[jj + 1])),
-                                        make_float2(ga, ga), make_float2(gb, gb));
+                                        make_float2(gat, gat), make_float2(gb, gb));
             const float2 fl = make_float2(floorf(a.x), floorf(a.y));
             const float2 u = __fadd2_rn(__fadd2_rn(a, make_float2(-fl.x, -fl.y)), make_float2(-0.5f, -0.5f));
             const float2 u2 = __fmul2_rn(u, u);
@@ -403,7 +454,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
           for (int jj = 0; jj < 8; ++jj) {
             const float wi = w8[jj];
             if (j0 + jj >= nj) continue;
-            const float a = fmaf(__uint_as_float(v[jj]), ga, gb), fl = floorf(a);
+            const float a = fmaf(__uint_as_float(v[jj]), gat, gb), fl = floorf(a);
             const float u = (a - fl) - 0.5f, u2 = u * u;
             const int cl = min(max(static_cast<int>(fl) + 1 - f.lmin, 0), cmax);
             for (int m = 0; m < WT / 2; ++m) {
@@ -424,7 +475,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp >= 4 && warp < 8) {   // flush: the FS_EPI / 4 private columns of each slice, one atomic per cell
+  if (warp < 4) {   // flush: the FS_EPI / 4 private columns of each slice, one atomic per cell
     const int q = warp & 3, p = s0 + 32 * q + lane;
     if (p < np) {
       const FPar f = fp[p];
@@ -441,7 +492,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
       }
     }
   }
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * FS_P));
+  if (warp == FS_WALLOC) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * FS_P));
 }
 
 // ------------------------------------------------------------------ the fused projection + interpolation
@@ -456,15 +507,18 @@ constexpr int FE_T = 128;          // targets per tile (UMMA M)
 constexpr int FE_S = 64;           // slices per group (UMMA N)
 constexpr int FE_STAGES = 3;
 constexpr int FE_QCAP = 40;        // cells of interpolation polynomials staged per slice (wider: read from global)
-constexpr int FE_EPI = 16;         // epilogue warps: 4 per TMEM lane quadrant, 16 slices each
+constexpr int FE_EPI = 16;         // epilogue warps: FE_H per TMEM lane quadrant, FE_SPW slices each
+constexpr int FE_H = FE_EPI / 4, FE_SPW = FE_S / FE_H;
+static_assert(FE_SPW % 8 == 0, "TMEM loads of 8 columns");
+constexpr int FE_WALLOC = FE_EPI, FE_WTMA = FE_EPI + 2, FE_WMMA = FE_EPI + 3;   // (roles as in k_proj_spread)
 constexpr int FE_THREADS = 32 * (4 + FE_EPI);
 constexpr int FE_PIECE = FE_T * 128;                      // one k-block of 128 targets: 16 KB
 constexpr int FE_B = FE_S * 128;                          // one k-block of the group's directions: 8 KB
 constexpr int FE_OFF_STAGE = FS_KBMAX * FE_B;             // 32 KB of resident directions
 constexpr int FE_OFF_Q = FE_OFF_STAGE + FE_STAGES * 2 * FE_PIECE;
 constexpr int FE_OFF_SP = FE_OFF_Q + FE_S * FE_QCAP * 32;            // per-slice constants float4 [FE_S]
-constexpr int FE_OFF_RED = FE_OFF_SP + FE_S * 16;                    // partial sums [2][4][FE_T] fp32
-constexpr int FE_OFF_BAR = FE_OFF_RED + 2 * 4 * FE_T * 4;
+constexpr int FE_OFF_RED = FE_OFF_SP + FE_S * 16;                    // partial sums [2][FE_H][FE_T] fp32
+constexpr int FE_OFF_BAR = FE_OFF_RED + 2 * FE_H * FE_T * 4;
 constexpr int FE_SMEM = FE_OFF_BAR + 256 + 1024;
 static_assert(FE_SMEM <= 227 * 1024, "k_proj_eval shared memory");
 
@@ -475,7 +529,8 @@ __device__ __forceinline__ int qswz(int c) { return c ^ ((c >> 3) & 7); }
 __global__ void __launch_bounds__(FE_THREADS, 1)
     k_proj_eval(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY,
                 const __grid_constant__ CUtensorMap tmYlo, int nk, int klast, int64_t M,
-                int np, int ranges, const float* __restrict__ inv_norm, const FPar* __restrict__ fp,
+                int np, int ranges, const float* __restrict__ rs, const float* __restrict__ inv_norm,
+                const FPar* __restrict__ fp,
                 const float* __restrict__ Q, int ncap, int w, double* __restrict__ s64,
                 const unsigned* __restrict__ flag16) {
   if (call_failed(flag16)) return;
@@ -484,7 +539,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
   unsigned char* sm = feraw + ((1024u - (smem_u32(feraw) & 1023u)) & 1023u);
   float4* sq = reinterpret_cast<float4*>(sm + FE_OFF_Q);   // [2][FE_S][FE_QCAP]: coefficients 0-3 | 4-7 of a cell
   float4* sp = reinterpret_cast<float4*>(sm + FE_OFF_SP);  // (ga, gb, -, -) per slice; .z = int bits of lminA, .w = WQ
-  float* red = reinterpret_cast<float*>(sm + FE_OFF_RED);  // [2][4][FE_T]
+  float* red = reinterpret_cast<float*>(sm + FE_OFF_RED);  // [2][FE_H][FE_T]
   uint64_t* bfull = reinterpret_cast<uint64_t*>(sm + FE_OFF_BAR);
   uint64_t* xfull = bfull + 1;
   uint64_t* empty = xfull + FE_STAGES;
@@ -531,7 +586,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmYlo)) : "memory");
   }
-  if (warp == 2) {
+  if (warp == FE_WALLOC) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(2 * FE_S));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -541,25 +596,24 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer: the group's directions once, then the raw fp32 target tiles (the hi piece)
+  if (warp == FE_WTMA && lane == 0) {
+    // ---- TMA producer: the group's directions (fp16 x 2^8) once, then the target tiles' fp16 hi and lo pieces
     mbar_expect_tx(bfull, nk * FE_B);
-    for (int kb = 0; kb < nk; ++kb) tma_load_2d(&tmB, bfull, sm + kb * FE_B, kb * 32, s0);
+    for (int kb = 0; kb < nk; ++kb) tma_load_2d(&tmB, bfull, sm + kb * FE_B, kb * 64, s0);
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = t0; t < t1; ++t)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         unsigned char* sa = sm + FE_OFF_STAGE + stage * 2 * FE_PIECE;
-        // the raw fp32 tile (the hi piece) and the pre-split lo piece (k_split_lo): no conversion in the CTA
         mbar_expect_tx(&xfull[stage], 2 * FE_PIECE);
-        tma_load_2d(&tmY, &xfull[stage], sa, kb * 32, static_cast<int>(t * FE_T));
-        tma_load_2d(&tmYlo, &xfull[stage], sa + FE_PIECE, kb * 32, static_cast<int>(t * FE_T));
+        tma_load_2d(&tmY, &xfull[stage], sa, kb * 64, static_cast<int>(t * FE_T));
+        tma_load_2d(&tmYlo, &xfull[stage], sa + FE_PIECE, kb * 64, static_cast<int>(t * FE_T));
         if (++stage == FE_STAGES) { stage = 0; phase ^= 1; }
       }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer: D[target][slice] += A (hi, then lo) . B (directions, tf32-exact)
-    constexpr uint32_t idesc = idesc_tf32(FE_T, FE_S);
+  } else if (warp == FE_WMMA && lane == 0) {
+    // ---- MMA issuer: D[target][slice] += A (s_t y: hi, then lo) . B (2^8 g, fp16-exact), K = 16 per MMA
+    constexpr uint32_t idesc = idesc_f16(FE_T, FE_S);
     mbar_wait(bfull, 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -585,7 +639,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
                 "setp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
                 "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
           }
         }
@@ -598,25 +652,27 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
                        smem_u32(&tfull[b]))
                    : "memory");
     }
-  } else if (warp >= 4) {
-    // ---- epilogue: warp w owns TMEM lane quadrant q = w % 4 (targets 32 q + lane of the tile) and the 16 slices
-    //      h = (w - 4) / 4 of the group
-    const int q = warp & 3, h = (warp - 4) >> 2;
+  } else if (warp < FE_EPI) {
+    // ---- epilogue: warp w owns TMEM lane quadrant q = w % 4 (targets 32 q + lane of the tile) and the FE_SPW
+    //      slices h = w / 4 of the group
+    const int q = warp & 3, h = warp >> 2;
     bool fits = true;   // (warp-uniform) every table of the warp's slices is staged in shared memory
-    for (int j = 0; j < 16; ++j) fits &= __float_as_int(sp[16 * h + j].w) <= FE_QCAP;
+    for (int j = 0; j < FE_SPW; ++j) fits &= __float_as_int(sp[FE_SPW * h + j].w) <= FE_QCAP;
     int it = 0;
     for (int64_t t = t0; t < t1; ++t, ++it) {
       const int b = it & 1;
+      const float rt = __ldg(rs + 4 * t + q);   // the 32-target group's 1 / (2^8 s_g): exact (a power of two)
       mbar_wait_sleep(&tfull[b], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      uint32_t v[16];
-      const uint32_t taddr = tmem_base + static_cast<uint32_t>(b * FE_S + 16 * h) + (static_cast<uint32_t>(32 * q) << 16);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-          "%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
+      uint32_t v[FE_SPW];
+      const uint32_t taddr =
+          tmem_base + static_cast<uint32_t>(b * FE_S + FE_SPW * h) + (static_cast<uint32_t>(32 * q) << 16);
+#pragma unroll
+      for (int j8 = 0; j8 < FE_SPW; j8 += 8)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v[j8]), "=r"(v[j8 + 1]), "=r"(v[j8 + 2]), "=r"(v[j8 + 3]), "=r"(v[j8 + 4]),
+                       "=r"(v[j8 + 5]), "=r"(v[j8 + 6]), "=r"(v[j8 + 7])
+                     : "r"(taddr + j8));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
@@ -627,14 +683,14 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
         // first, then the 4 Horner chains (independent: latency hidden by ILP).  Dead slices (p >= np) have a zero
         // table and WA = 1: they add exactly 0
 #pragma unroll
-        for (int j0 = 0; j0 < 16; j0 += 4) {
+        for (int j0 = 0; j0 < FE_SPW; j0 += 4) {
           float fr[4];
           float4 c0[4], c1[4];
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
-            const int ls = 16 * h + j0 + jj;
+            const int ls = FE_SPW * h + j0 + jj;
             const float4 c = sp[ls];   // broadcast
-            const float a = fmaf(__uint_as_float(v[j0 + jj]), c.x, c.y), fl = floorf(a);
+            const float a = fmaf(__uint_as_float(v[j0 + jj]), c.x * rt, c.y), fl = floorf(a);
             fr[jj] = a - fl;
             // (fl is an integer of magnitude < 2^22: its int value from the 1.5 2^23 shift, no F2I)
             int cl = (__float_as_int(fl + 12582912.f) - 0x4B400000) + 1 - __float_as_int(c.z);
@@ -657,10 +713,10 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
         }
       } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int ls = 16 * h + j;
+      for (int j = 0; j < FE_SPW; ++j) {
+        const int ls = FE_SPW * h + j;
         const float4 c = sp[ls];   // broadcast
-        const float a = fmaf(__uint_as_float(v[j]), c.x, c.y), fl = floorf(a);
+        const float a = fmaf(__uint_as_float(v[j]), c.x * rt, c.y), fl = floorf(a);
         int cl = static_cast<int>(fl) + 1 - __float_as_int(c.z);
         const int wq = __float_as_int(c.w);
         SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < wq));   // the bound holds
@@ -685,13 +741,14 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
         acc += (s0 + ls < np) ? tv : 0.f;
       }
       }
-      float* rb = red + (b * 4) * FE_T;
+      float* rb = red + (b * FE_H) * FE_T;
       rb[h * FE_T + 32 * q + lane] = acc;
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");   // the quadrant's four partial sums of the tile
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * FE_H) : "memory");   // the quadrant's partial sums
       if (h == 0) {
         const int64_t m = t * FE_T + 32 * q + lane;
-        const double sum = static_cast<double>(rb[32 * q + lane]) + rb[FE_T + 32 * q + lane] +
-                           rb[2 * FE_T + 32 * q + lane] + rb[3 * FE_T + 32 * q + lane];
+        double sum = 0.0;
+#pragma unroll
+        for (int hh = 0; hh < FE_H; ++hh) sum += static_cast<double>(rb[hh * FE_T + 32 * q + lane]);
         if (m < M) atomicAdd(s64 + m, sum);
       }
     }
@@ -699,42 +756,49 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * FE_S));
+  if (warp == FE_WALLOC) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * FE_S));
 }
 
-bool encode_f32_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+// 2-byte elements (fp16), 64 per 128-byte swizzled row of the box
+bool encode_h16_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                     uint32_t box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
   const cuuint64_t gdim[2] = {cols, rows};
-  const cuuint64_t gstride[1] = {row_stride_elems * 4};
-  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint64_t gstride[1] = {row_stride_elems * 2};
+  const cuuint32_t box[2] = {64, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
 
+int fused_dp16(int d) { return (d + 7) / 8 * 8; }
+
 size_t source_bound_bytes(int d) { return sizeof(double) * static_cast<size_t>(d) * (1 + MEAN_PARTS) + 32; }
 
 bool fused_spread_ok(int d, const float* x) {
-  return d <= 32 * FS_KBMAX && d % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  return d <= 64 * FS_KBMAX && d % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
 }
 
 cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_t M, int d, double* mu, unsigned* nb,
-                               float* xlo, float* ylo, cudaStream_t st) {
+                               uint16_t* xh, uint16_t* xl, float* rsx, uint16_t* yh, uint16_t* yl, float* rsy,
+                               cudaStream_t st) {
   double* part = mu + d;   // [MEAN_PARTS][d] scratch after mu (source_bound_bytes)
   k_sample_mean_part<<<MEAN_PARTS, 128, 0, st>>>(x, N, d, part);
   k_sample_mean_fin<<<1, 128, 0, st>>>(N, d, part, mu, nb);
-  auto norms = [&](const float* z, int64_t n, unsigned* out, float* lo) {
-    int64_t blocks = (n * 32 / 4 + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    k_norm_bound<<<static_cast<unsigned>(blocks), 256, 0, st>>>(z, n, d, mu, out, lo);
+  const int dp16 = fused_dp16(d);
+  auto prep = [&](const float* z, int64_t n, unsigned* out, uint16_t* h, uint16_t* l, float* rs) {
+    int64_t blocks = ((n + 31) / 32 + 7) / 8;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    k_prep_f16<<<static_cast<unsigned>(blocks), 256, 0, st>>>(z, n, d, dp16, mu, out,
+                                                                       reinterpret_cast<__half*>(h),
+                                                                       reinterpret_cast<__half*>(l), rs);
   };
-  norms(x, N, nb, xlo);
-  norms(y, M, nb + 4, ylo);
+  prep(x, N, nb, xh, xl, rsx);
+  prep(y, M, nb + 4, yh, yl, rsy);
   return cudaGetLastError();
 }
 
@@ -744,15 +808,18 @@ cudaError_t launch_bound_ranges(const float* g32, int dp32, int d, const float* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_proj_spread(const float* x, const float* xlo, int64_t N, int d, const float* g32, int dp32,
-                               const float* inv_norm, int np, const float* w, const FPar* fp, const PolyWin& pw,
-                               int ncap, float* grid, const unsigned* flag16, cudaStream_t st) {
+cudaError_t launch_proj_spread(const uint16_t* xh, const uint16_t* xl, const float* rsx, int64_t N, int d,
+                               const uint16_t* g16, int dpg, const float* inv_norm, int np, const float* w,
+                               const FPar* fp, const PolyWin& pw, int ncap, float* grid, const unsigned* flag16,
+                               cudaStream_t st) {
   CUtensorMap tmA, tmX, tmXlo;
-  const int nk = dp32 / 32;
-  if (!encode_f32_map(&tmA, g32, static_cast<uint64_t>(np), static_cast<uint64_t>(dp32), static_cast<uint64_t>(dp32),
+  const int dp16 = fused_dp16(d), nk = (d + 63) / 64, klast = (d - 64 * (nk - 1) + 15) / 16;
+  if (!encode_h16_map(&tmA, g16, static_cast<uint64_t>(np), static_cast<uint64_t>(dpg), static_cast<uint64_t>(dpg),
                       FS_S) ||
-      !encode_f32_map(&tmX, x, static_cast<uint64_t>(N), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FS_P) ||
-      !encode_f32_map(&tmXlo, xlo, static_cast<uint64_t>(N), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FS_P))
+      !encode_h16_map(&tmX, xh, static_cast<uint64_t>(N), static_cast<uint64_t>(dp16), static_cast<uint64_t>(dp16),
+                      FS_P) ||
+      !encode_h16_map(&tmXlo, xl, static_cast<uint64_t>(N), static_cast<uint64_t>(dp16), static_cast<uint64_t>(dp16),
+                      FS_P))
     return cudaErrorInvalidValue;
   const int ntiles_s = (np + FS_S - 1) / FS_S;
   const int64_t ntp = (N + FS_P - 1) / FS_P;
@@ -761,8 +828,8 @@ cudaError_t launch_proj_spread(const float* x, const float* xlo, int64_t N, int 
   if (ranges > ntp) ranges = static_cast<int>(ntp);
   auto go = [&](auto kern) {
     set_smem_attr_once(reinterpret_cast<const void*>(kern), FS_SMEM);
-    kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, tmXlo, nk, (d - 32 * (nk - 1) + 7) / 8, N, np, ranges, inv_norm, w, fp, pw, ncap, grid,
-                                                         flag16);
+    kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, tmXlo, nk, klast, N, np, ranges, rsx, inv_norm, w,
+                                                         fp, pw, ncap, grid, flag16);
   };
   switch (pw.w) {
     case 4: go(k_proj_spread<4>); break;
@@ -775,21 +842,17 @@ cudaError_t launch_proj_spread(const float* x, const float* xlo, int64_t N, int 
   return cudaGetLastError();
 }
 
-}  // namespace sks
-
-namespace sks {
-
-// the TF32x2 lo piece of every coordinate, once (the eval CTAs of all slice groups load it by TMA instead of each
-// converting the same tile): lo = rn_tf32(y - trunc_tf32(y)), the kind::tf32 operand read of y being the hi piece
-cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32, int dp32, const float* inv_norm, int np,
-                             const FPar* fp, const float* Q, int ncap, int w, double* s64, const float* ylo,
-                             const unsigned* flag16, cudaStream_t st) {
+cudaError_t launch_proj_eval(const uint16_t* yh, const uint16_t* yl, const float* rsy, int64_t M, int d,
+                             const uint16_t* g16, int dpg, const float* inv_norm, int np, const FPar* fp,
+                             const float* Q, int ncap, int w, double* s64, const unsigned* flag16, cudaStream_t st) {
   CUtensorMap tmB, tmY, tmYlo;
-  const int nk = dp32 / 32;
-  if (!encode_f32_map(&tmB, g32, static_cast<uint64_t>(np), static_cast<uint64_t>(dp32), static_cast<uint64_t>(dp32),
+  const int dp16 = fused_dp16(d), nk = (d + 63) / 64, klast = (d - 64 * (nk - 1) + 15) / 16;
+  if (!encode_h16_map(&tmB, g16, static_cast<uint64_t>(np), static_cast<uint64_t>(dpg), static_cast<uint64_t>(dpg),
                       FE_S) ||
-      !encode_f32_map(&tmY, y, static_cast<uint64_t>(M), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FE_T) ||
-      !encode_f32_map(&tmYlo, ylo, static_cast<uint64_t>(M), static_cast<uint64_t>(d), static_cast<uint64_t>(d), FE_T))
+      !encode_h16_map(&tmY, yh, static_cast<uint64_t>(M), static_cast<uint64_t>(dp16), static_cast<uint64_t>(dp16),
+                      FE_T) ||
+      !encode_h16_map(&tmYlo, yl, static_cast<uint64_t>(M), static_cast<uint64_t>(dp16), static_cast<uint64_t>(dp16),
+                      FE_T))
     return cudaErrorInvalidValue;
   const int ngroups = (np + FE_S - 1) / FE_S;
   const int64_t ntt = (M + FE_T - 1) / FE_T;
@@ -797,8 +860,8 @@ cudaError_t launch_proj_eval(const float* y, int64_t M, int d, const float* g32,
   if (ranges < 1) ranges = 1;
   if (ranges > ntt) ranges = static_cast<int>(ntt);
   set_smem_attr_once(reinterpret_cast<const void*>(k_proj_eval), FE_SMEM);
-  k_proj_eval<<<ngroups * ranges, FE_THREADS, FE_SMEM, st>>>(tmB, tmY, tmYlo, nk, (d - 32 * (nk - 1) + 7) / 8, M, np, ranges, inv_norm, fp, Q, ncap, w, s64,
-                                                            flag16);
+  k_proj_eval<<<ngroups * ranges, FE_THREADS, FE_SMEM, st>>>(tmB, tmY, tmYlo, nk, klast, M, np, ranges, rsy, inv_norm,
+                                                            fp, Q, ncap, w, s64, flag16);
   return cudaGetLastError();
 }
 

@@ -290,8 +290,12 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
             const int box = c >> 2, j0 = 2 * (c & 3);   // fp32 box (0: hi slot, 1: lo slot), chunks j0, j0 + 1
             const unsigned char* rb = sa + box * SM::A_BYTES + r * 128;
             if (r < split) {
-              const float4 a4 = *reinterpret_cast<const float4*>(rb + ((j0 ^ (r & 7)) << 4));
-              const float4 b4 = *reinterpret_cast<const float4*>(rb + (((j0 + 1) ^ (r & 7)) << 4));
+              // the two boxes are 16 KB apart (same banks): lanes of box 1 read their two chunks in the other
+              // order, so that the 8 lanes of a quarter-warp hit 8 distinct 16-byte bank groups per load
+              const int jf = j0 + box, js = j0 + 1 - box;
+              const float4 f4 = *reinterpret_cast<const float4*>(rb + ((jf ^ (r & 7)) << 4));
+              const float4 s4 = *reinterpret_cast<const float4*>(rb + ((js ^ (r & 7)) << 4));
+              const float4 a4 = box ? s4 : f4, b4 = box ? f4 : s4;
               v[q][0] = a4.x; v[q][1] = a4.y; v[q][2] = a4.z; v[q][3] = a4.w;
               v[q][4] = b4.x; v[q][5] = b4.y; v[q][6] = b4.z; v[q][7] = b4.w;
             } else {   // straddling tile: y rows from global memory

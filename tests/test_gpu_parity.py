@@ -495,6 +495,24 @@ def test_fused_projection_spread(kind, scale, d, N, M, P):
     assert err <= TOL[kind], err
 
 
+@pytest.mark.gpu
+def test_fused_mixed_row_magnitudes():
+    # the fused kernels' FP16x2 operands carry one power-of-two scale per 32-row group (fused.cu k_prep_f16): rows
+    # whose magnitudes differ by up to 2^8 inside a group keep the projection's fp32 accuracy (reading R2)
+    cfg = I.Config("fused", "gaussian", 100, 300_001, 3000, 40, 33, 133, "mixture10", "pm1", param=200.0)
+    x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
+    rng = np.random.default_rng(7)
+    x = (x * np.exp2(rng.uniform(-4, 4, size=(cfg.N, 1)))).astype(np.float32)
+    y = (y * np.exp2(rng.uniform(-4, 4, size=(cfg.M, 1)))).astype(np.float32)
+    s = S.sks_sum(dev(x), dev(y), dev(w), "gaussian", 200.0, cfg.P, cfg.dir_seed).cpu().numpy()
+    assert S.sks_last_plan()["fused"] == 1
+    tgt = I.target_subset(cfg.M, 48)
+    ref = O.sliced_sum("gaussian", 200.0, x, y, w, cfg.P, cfg.dir_seed, targets=tgt)
+    err = rel_err(s[tgt], ref, w)
+    print(f"fused, mixed row magnitudes: max|ds|/sum|w| = {err:.3e}")
+    assert err <= TOL["gaussian"], err
+
+
 # ---------------------------------------------------------------- opt-in bitwise determinism
 @pytest.mark.parametrize("name,size,kw", [("cfg1", {}, {}), ("cfg1", {}, {"engine": "ndft"}),
                                           ("cfg2", dict(N=30000, M=5000, P=24), {}),
