@@ -165,7 +165,7 @@ constexpr size_t kStatusBytes = 64;
 // workspace layout of one slice batch (offsets in bytes)
 struct Layout {
   size_t status = 0, s64 = 0, mm = 0, Z = 0, xs3 = 0, part = 0, tot = 0, sp = 0, grid = 0, D = 0, fpar = 0, Q = 0,
-         what = 0, bound = 0, xh = 0, xl = 0, yh = 0, yl = 0, rsx = 0, rsy = 0, dpart = 0, total = 0;
+         what = 0, bound = 0, wpad = 0, xh = 0, xl = 0, yh = 0, yl = 0, rsx = 0, rsy = 0, dpart = 0, total = 0;
   int dgroups = 0;   // deterministic mode: TargetAcc groups of the whole call
 };
 
@@ -274,6 +274,7 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, 
       L.yh = take(sizeof(uint16_t) * static_cast<size_t>(M) * dp16);
       L.yl = take(sizeof(uint16_t) * static_cast<size_t>(M) * dp16);
       L.rsx = take(sizeof(float) * static_cast<size_t>((N + 127) / 128 * 4));   // per 32-row group (whole tiles)
+      L.wpad = take(sizeof(float) * static_cast<size_t>((N + 127) / 128 * 128));
       L.rsy = take(sizeof(float) * static_cast<size_t>((M + 127) / 128 * 4));
     }
   }
@@ -512,7 +513,8 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
                                      reinterpret_cast<unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32),
                                      reinterpret_cast<uint16_t*>(ws + L.xh), reinterpret_cast<uint16_t*>(ws + L.xl),
                                      reinterpret_cast<float*>(ws + L.rsx), reinterpret_cast<uint16_t*>(ws + L.yh),
-                                     reinterpret_cast<uint16_t*>(ws + L.yl), reinterpret_cast<float*>(ws + L.rsy), st));
+                                     reinterpret_cast<uint16_t*>(ws + L.yl), reinterpret_cast<float*>(ws + L.rsy), w,
+                                     reinterpret_cast<float*>(ws + L.wpad), st));
     launches += 4;
   }
   for (int b0 = 0; b0 < pr.nslices; b0 += batch) {
@@ -637,7 +639,8 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
                                          reinterpret_cast<const uint16_t*>(ws + L.xl),
                                          reinterpret_cast<const float*>(ws + L.rsx), pr.N, pr.d,
                                          static_cast<const uint16_t*>(dirs->g16) + static_cast<int64_t>(b0) * dirs->K3,
-                                         dirs->K3, dirs->inv + b0, nbat, w, fp, plan.pw, kNcap, grid, flag16, st));
+                                         dirs->K3, dirs->inv + b0, nbat, reinterpret_cast<const float*>(ws + L.wpad), fp,
+                                         plan.pw, kNcap, grid, flag16, st));
       } else {
         ProfScope ps(PS_SPREAD, st);
         SKS_CUDA(sks::launch_spread(zv, w, nbat, fp, kNcap, plan.pw, pr.k.kind == SKS_LAPLACIAN, det, grid, flag16, st));

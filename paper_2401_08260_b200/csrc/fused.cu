@@ -82,7 +82,8 @@ __device__ __forceinline__ float group_scale(float m) {   // s_g from the group'
 __global__ void __launch_bounds__(256) k_prep_f16(const float* __restrict__ x, int64_t N, int d, int dp16,
                                                   const double* __restrict__ mu, unsigned* __restrict__ out,
                                                   __half* __restrict__ xh, __half* __restrict__ xl,
-                                                  float* __restrict__ rs) {
+                                                  float* __restrict__ rs, const float* __restrict__ w,
+                                                  float* __restrict__ wpad) {
   __shared__ float smu[128];
   for (int j = threadIdx.x; j < 128; j += blockDim.x) smu[j] = j < d ? static_cast<float>(mu[j]) : 0.f;
   __syncthreads();
@@ -92,11 +93,12 @@ __global__ void __launch_bounds__(256) k_prep_f16(const float* __restrict__ x, i
                        : make_float4(0.f, 0.f, 0.f, 0.f);
   float r2max = 0.f, n2max = 0.f;
   bool bad = false;
-  const int64_t ngroups = (N + 31) / 32;
+  const int64_t ngroups = (N + 127) / 128 * 4;   // whole 128-row tiles (rs and wpad cover them)
   const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t g = w0; g < ngroups; g += nw) {
     const int64_t r0 = g * 32;
+    if (w) wpad[r0 + lane] = r0 + lane < N ? __ldg(w + r0 + lane) : 0.f;   // (the spread's weights, zero padded)
     float am = 0.f;
     for (int b = 0; b < 32; b += PR_U) {
       float4 v[PR_U];
@@ -228,8 +230,9 @@ constexpr int FS_PIECE = FS_P * 128;                      // one k-block of 128 
 constexpr int FS_A = FS_S * 128;                          // one k-block of the directions: 16 KB
 constexpr int FS_OFF_STAGE = FS_KBMAX * FS_A;             // 32 KB of resident directions
 constexpr int FS_OFF_GRID = FS_OFF_STAGE + FS_STAGES * 2 * FS_PIECE;
-constexpr int FS_OFF_BAR = FS_OFF_GRID + (FS_EPI / 4) * FS_WCAP * FS_S * 4;
-constexpr int FS_SMEM = FS_OFF_BAR + 256 + 1024;          // + barriers, TMEM slot, alignment slack
+constexpr int FS_OFF_W = FS_OFF_GRID + (FS_EPI / 4) * FS_WCAP * FS_S * 4;   // the tiles' weights [2][FS_P]
+constexpr int FS_OFF_BAR = FS_OFF_W + 2 * FS_P * 4;
+constexpr int FS_SMEM = FS_OFF_BAR + 512 + 1024;          // + barriers, TMEM slot, window coefficients, alignment
 static_assert(FS_SMEM <= 227 * 1024, "k_proj_spread shared memory");
 
 template <int WT>
@@ -237,8 +240,8 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     k_proj_spread(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXlo, int nk, int klast, int64_t N,
                   int np, int ranges, const float* __restrict__ rs, const float* __restrict__ inv_norm,
-                  const float* __restrict__ w,
-                  const FPar* __restrict__ fp, PolyWin pw, int ncap, float* __restrict__ grid,
+                  const float* __restrict__ wpad, const FPar* __restrict__ fp, PolyWin pw, int ncap,
+                  float* __restrict__ grid,
                   const unsigned* __restrict__ flag16) {
   if (call_failed(flag16)) return;
   extern __shared__ unsigned char fsraw[];
@@ -251,7 +254,9 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   uint64_t* empty = xfull + FS_STAGES;         // [FS_STAGES] consumed by the MMAs
   uint64_t* tfull = empty + FS_STAGES;         // [2]
   uint64_t* tempty = tfull + 2;                // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* wfull = tempty + 2;                // [2] the tile's weights landed (slot b = the TMEM buffer's)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 2);
+  const float* wsm = reinterpret_cast<const float*>(sm + FS_OFF_W);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int st_idx = blockIdx.x % ((np + FS_S - 1) / FS_S), r = blockIdx.x / ((np + FS_S - 1) / FS_S);
   const int64_t ntp = (N + FS_P - 1) / FS_P;
@@ -265,7 +270,11 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
       mbar_init(&xfull[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], FS_EPI); }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], FS_EPI);
+      mbar_init(&wfull[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
@@ -288,7 +297,8 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     for (int kb = 0; kb < nk; ++kb) tma_load_2d(&tmA, afull, sm + kb * FS_A, kb * 64, s0);
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t t = t0; t < t1; ++t)
+    int it = 0;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         unsigned char* sa = sm + FS_OFF_STAGE + stage * 2 * FS_PIECE;
@@ -297,6 +307,13 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
         tma_load_2d(&tmXlo, &xfull[stage], sa + FS_PIECE, kb * 64, static_cast<int>(t * FS_P));
         if (++stage == FS_STAGES) { stage = 0; phase ^= 1; }
       }
+      // the tile's 128 weights (zero padded beyond N) into slot b, free once the epilogue of tile t - 2 released
+      // TMEM buffer b
+      const int b = it & 1;
+      mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
+      mbar_expect_tx(&wfull[b], FS_P * 4);
+      bulk_load_1d(sm + FS_OFF_W + b * FS_P * 4, wpad + t * FS_P, FS_P * 4, &wfull[b]);
+    }
   } else if (warp == FS_WMMA && lane == 0) {
     // ---- MMA issuer: D[slice][point] += A (2^8 g, fp16-exact) . B (s_t x: hi, then lo), K = 16 per MMA
     constexpr uint32_t idesc = idesc_f16(FS_S, FS_P);
@@ -362,7 +379,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     float* gp = grid + static_cast<int64_t>(live ? p : 0) * ncap;
     // window coefficients through shared memory into registers (read from the parameter bank, ptxas would
     // re-load them inside the loop)
-    float* eos = reinterpret_cast<float*>(sm + FS_OFF_BAR + 128);   // [WT / 2][8]
+    float* eos = reinterpret_cast<float*>(sm + FS_OFF_BAR + 256);   // [WT / 2][8]
     if (warp == 0 && lane < WT / 2 * 8) eos[lane] = pw.eo[lane / 8][lane % 8];
     asm volatile("bar.sync 1, %0;" ::"r"(FS_EPI * 32) : "memory");
     float E[WT / 2][4], O[WT / 2][4];
@@ -375,24 +392,17 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
       }
     const int cmax = W - WT;   // last admissible first-tap cell (relative to lmin)
     const bool fast = live && !wide;   // (dead lanes of the last slice tile and wide footprints: the slow loop)
-    // the weights of the warp's 32 points, one per lane, loaded one tile ahead (software pipelined: a global load's
-    // latency would otherwise stall the epilogue warps at every tile)
-    auto wload = [&](int64_t t) {
-      const int64_t i = t * FS_P + h * 32 + lane;
-      return (t < t1 && i < N) ? __ldg(w + i) : 0.f;
-    };
-    float wnext = wload(t0);
     int it = 0;
     for (int64_t t = t0; t < t1; ++t, ++it) {
       const int b = it & 1;
       const int c0 = h * 32;
       const int64_t i0 = t * FS_P + c0;
-      const float wv = wnext;
-      wnext = wload(t + 1);
       const float gat = ga * __ldg(rs + 4 * t + h);   // the 32-point group's 1 / (2^8 s_g): exact (a power of two)
       mbar_wait_sleep(&tfull[b], (it >> 1) & 1);
+      mbar_wait(&wfull[b], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t taddr = tmem_base + static_cast<uint32_t>(b * FS_P + c0) + (static_cast<uint32_t>(32 * q) << 16);
+      const float4* w4 = reinterpret_cast<const float4*>(wsm + b * FS_P + c0);
       const int nj = (N - i0 < 32) ? static_cast<int>(N - i0) : 32;
 #pragma unroll 1
       for (int j0 = 0; j0 < 32; j0 += 8) {   // 8 columns (points) per TMEM load: few registers held
@@ -401,12 +411,9 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                      : "r"(taddr + j0));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        float w8[8];   // the 8 points' weights (shuffled by the whole warp before any lane-dependent branch)
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const float t = __shfl_sync(0xffffffffu, wv, j0 + jj);
-          w8[jj] = j0 + jj < nj ? t : 0.f;
-        }
+        // the 8 points' weights: two 16-byte broadcast loads (every lane reads the same address; zero beyond N)
+        const float4 wa = w4[j0 / 4], wb = w4[j0 / 4 + 1];
+        const float w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
         if (fast) {
           // branch-free: points beyond N carry weight 0 (their rows are zero-filled by TMA; the clamp keeps their
           // cell in range).  Two points per step: the grid coordinate and the window polynomials of both in packed
@@ -785,20 +792,21 @@ bool fused_spread_ok(int d, const float* x) {
 
 cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_t M, int d, double* mu, unsigned* nb,
                                uint16_t* xh, uint16_t* xl, float* rsx, uint16_t* yh, uint16_t* yl, float* rsy,
-                               cudaStream_t st) {
+                               const float* w, float* wpad, cudaStream_t st) {
   double* part = mu + d;   // [MEAN_PARTS][d] scratch after mu (source_bound_bytes)
   k_sample_mean_part<<<MEAN_PARTS, 128, 0, st>>>(x, N, d, part);
   k_sample_mean_fin<<<1, 128, 0, st>>>(N, d, part, mu, nb);
   const int dp16 = fused_dp16(d);
-  auto prep = [&](const float* z, int64_t n, unsigned* out, uint16_t* h, uint16_t* l, float* rs) {
-    int64_t blocks = ((n + 31) / 32 + 7) / 8;
+  auto prep = [&](const float* z, int64_t n, unsigned* out, uint16_t* h, uint16_t* l, float* rs, const float* w,
+                  float* wp) {
+    int64_t blocks = ((n + 127) / 128 * 4 + 7) / 8;
     if (blocks > 148 * 4) blocks = 148 * 4;
     k_prep_f16<<<static_cast<unsigned>(blocks), 256, 0, st>>>(z, n, d, dp16, mu, out,
                                                                        reinterpret_cast<__half*>(h),
-                                                                       reinterpret_cast<__half*>(l), rs);
+                                                                       reinterpret_cast<__half*>(l), rs, w, wp);
   };
-  prep(x, N, nb, xh, xl, rsx);
-  prep(y, M, nb + 4, yh, yl, rsy);
+  prep(x, N, nb, xh, xl, rsx, w, wpad);
+  prep(y, M, nb + 4, yh, yl, rsy, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -809,7 +817,7 @@ cudaError_t launch_bound_ranges(const float* g32, int dp32, int d, const float* 
 }
 
 cudaError_t launch_proj_spread(const uint16_t* xh, const uint16_t* xl, const float* rsx, int64_t N, int d,
-                               const uint16_t* g16, int dpg, const float* inv_norm, int np, const float* w,
+                               const uint16_t* g16, int dpg, const float* inv_norm, int np, const float* wpad,
                                const FPar* fp, const PolyWin& pw, int ncap, float* grid, const unsigned* flag16,
                                cudaStream_t st) {
   CUtensorMap tmA, tmX, tmXlo;
@@ -828,8 +836,8 @@ cudaError_t launch_proj_spread(const uint16_t* xh, const uint16_t* xl, const flo
   if (ranges > ntp) ranges = static_cast<int>(ntp);
   auto go = [&](auto kern) {
     set_smem_attr_once(reinterpret_cast<const void*>(kern), FS_SMEM);
-    kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, tmXlo, nk, klast, N, np, ranges, rsx, inv_norm, w,
-                                                         fp, pw, ncap, grid, flag16);
+    kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, tmXlo, nk, klast, N, np, ranges, rsx, inv_norm,
+                                                         wpad, fp, pw, ncap, grid, flag16);
   };
   switch (pw.w) {
     case 4: go(k_proj_spread<4>); break;

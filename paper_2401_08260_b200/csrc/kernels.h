@@ -200,17 +200,18 @@ size_t source_bound_bytes(int d);   // scratch of launch_source_prep: mu, partia
 // launch_source_prep (once per call, direction-independent): mu, the norm words nb (max ||z - mu||^2, max ||z||^2,
 // non-finite) of x (nb[0..2]) and y (nb[4..6]), and both point sets as the fused kernels' FP16x2 operands in the
 // same pass: per 32-row group g a scale s_g = 2^(14 - e) (max |z| over the group = m 2^e), hi = f16(s_g z),
-// lo = f16(s_g z - hi) as fp16 arrays [rows][fused_dp16(d)] (pad columns zero), rs[g] = 1 / (2^8 s_g) (reading R2).
+// lo = f16(s_g z - hi) as fp16 arrays [rows][fused_dp16(d)] (pad columns zero), rs[g] = 1 / (2^8 s_g) (reading R2),
+// and the source weights w zero padded to whole 128-point tiles (wpad, read by the spread's bulk copies).
 // launch_bound_ranges (per slice batch): every slice's range bound c_p +- rho' of both sets into mm[p]
 int fused_dp16(int d);   // row length of the fp16 operand arrays: d rounded up to 8
 cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_t M, int d, double* mu, unsigned* nb,
                                uint16_t* xh, uint16_t* xl, float* rsx, uint16_t* yh, uint16_t* yl, float* rsy,
-                               cudaStream_t st);
+                               const float* w, float* wpad, cudaStream_t st);
 cudaError_t launch_bound_ranges(const float* g32, int dp32, int d, const float* inv_norm, int np, const double* mu,
                                 const unsigned* nb, unsigned* mm, unsigned* flag16, cudaStream_t st);
 // g16: the slices' fp16 directions 2^8 g, row stride dpg (a multiple of 64)
 cudaError_t launch_proj_spread(const uint16_t* xh, const uint16_t* xl, const float* rsx, int64_t N, int d,
-                               const uint16_t* g16, int dpg, const float* inv_norm, int np, const float* w,
+                               const uint16_t* g16, int dpg, const float* inv_norm, int np, const float* wpad,
                                const FPar* fp, const PolyWin& pw, int ncap, float* grid, const unsigned* flag16,
                                cudaStream_t st);
 // rows a1 + a7 fused for the targets (fused.cu): projections of y interpolated from the tensor-core accumulators,

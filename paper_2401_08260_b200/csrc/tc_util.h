@@ -52,6 +52,14 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+// 1D bulk copy global -> shared (bytes: a multiple of 16, both addresses 16-byte aligned), completion on bar
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // UMMA shared-memory descriptor, K-major, 128-byte swizzle: SBO = 1024 B (8 rows x 128 B), LBO = 16 B
 // (ignored for swizzled K-major), version 1, layout type 2 (SWIZZLE_128B).
 __device__ __forceinline__ uint64_t umma_desc_sw128(const void* p) {
