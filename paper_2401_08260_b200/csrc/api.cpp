@@ -267,15 +267,15 @@ Layout make_layout(int64_t N, int64_t M, Path pt, int nbat, bool with_Z, int d, 
     L.what = take(sizeof(double) * 2 * sks::kNdftWidth * static_cast<size_t>(nbat));
     if (fused) {
       L.bound = take(sks::source_bound_bytes(d));
-      // both point sets as FP16x2 operands (hi, lo: fp16 [rows][dp16]) and their per-32-row scales (source prep)
+      // both point sets as FP16x2 operands (hi, lo: fp16 [rows][dp16]) and their per-8-row scales (source prep)
       const size_t dp16 = static_cast<size_t>(sks::fused_dp16(d));
       L.xh = take(sizeof(uint16_t) * static_cast<size_t>(N) * dp16);
       L.xl = take(sizeof(uint16_t) * static_cast<size_t>(N) * dp16);
       L.yh = take(sizeof(uint16_t) * static_cast<size_t>(M) * dp16);
       L.yl = take(sizeof(uint16_t) * static_cast<size_t>(M) * dp16);
-      L.rsx = take(sizeof(float) * static_cast<size_t>((N + 127) / 128 * 4));   // per 32-row group (whole tiles)
+      L.rsx = take(sizeof(float) * static_cast<size_t>((N + 127) / 128 * 16));   // per 8-row group (whole tiles)
       L.wpad = take(sizeof(float) * static_cast<size_t>((N + 127) / 128 * 128));
-      L.rsy = take(sizeof(float) * static_cast<size_t>((M + 127) / 128 * 4));
+      L.rsy = take(sizeof(float) * static_cast<size_t>((M + 127) / 128 * 16));
     }
   }
   if (dgroups) {

@@ -58,14 +58,13 @@ __global__ void k_sample_mean_fin(int64_t N, int d, const double* __restrict__ p
   if (threadIdx.x < 8) nb[threadIdx.x] = 0u;
 }
 
-// The fused kernels' operands (reading R2, FP16x2 with one scale per 32-row group -- the rows one epilogue warp
-// handles in both fused kernels): for the group's rows
+// The fused kernels' operands (reading R2, FP16x2 with one scale per 8-row group): for the group's rows
 //   s_g = 2^(14 - e), max |x| over the group = m 2^e (m in [0.5, 1)): s_g max|x| < 2^14 (s_g = 1 for a zero group)
 //   hi = f16_rn(s_g x), lo = f16_rn(s_g x - hi)         (|s_g x - hi - lo| <= 2^-22 |s_g x| + 2^-25)
 // stored as two fp16 arrays [rows][dp16] (dp16 = d rounded up to 8, pad columns zero) and rs[g] = 1 / (2^8 s_g):
 // the tensor cores accumulate (2^8 g) . (s_g x) exactly in fp32 (directions fp16 x 2^8, exact: R1), and the
-// epilogue's rs[g] (a power of two) restores <g, x> without rounding.
-constexpr int PR_U = 8;   // rows per batch (loads in flight per lane)
+// epilogues' rs[g] (a power of two) restores <g, x> without rounding.
+constexpr int PR_G = 8;    // rows per scale group: one warp holds a group in registers (one float4 per lane and row)
 
 __device__ __forceinline__ float group_scale(float m) {   // s_g from the group's max |x| (finite, >= 0)
   if (!(m > 0.f) || !(m < 3.0e38f)) return 1.0f;
@@ -75,11 +74,10 @@ __device__ __forceinline__ float group_scale(float m) {   // s_g from the group'
   return ldexpf(1.0f, 14 - e);
 }
 
-// one warp per 32-row group (grid-stride), lane l dims 4 l .. 4 l + 3 (d <= 128).  Pass 1 streams the rows from
-// HBM: out[0] = max ||x - mu||^2, out[1] = max ||x||^2 (float bits: non-negative floats order as unsigned ints),
-// out[2] = non-finite seen, and the group's max |x|; pass 2 re-reads the group (12.8 KB at d = 100: an L2 hit)
-// and writes its fp16 hi / lo rows
-__global__ void __launch_bounds__(256) k_prep_f16(const float* __restrict__ x, int64_t N, int d, int dp16,
+// one warp per 8-row group (grid-stride), lane l dims 4 l .. 4 l + 3 (d <= 128), one pass over the rows:
+// out[0] = max ||x - mu||^2, out[1] = max ||x||^2 (float bits: non-negative floats order as unsigned ints),
+// out[2] = non-finite seen; the group's fp16 hi / lo rows and rs[g]; with w, the weights zero padded (wpad)
+__global__ void __launch_bounds__(256, 4) k_prep_f16(const float* __restrict__ x, int64_t N, int d, int dp16,
                                                   const double* __restrict__ mu, unsigned* __restrict__ out,
                                                   __half* __restrict__ xh, __half* __restrict__ xl,
                                                   float* __restrict__ rs, const float* __restrict__ w,
@@ -93,64 +91,56 @@ __global__ void __launch_bounds__(256) k_prep_f16(const float* __restrict__ x, i
                        : make_float4(0.f, 0.f, 0.f, 0.f);
   float r2max = 0.f, n2max = 0.f;
   bool bad = false;
-  const int64_t ngroups = (N + 127) / 128 * 4;   // whole 128-row tiles (rs and wpad cover them)
-  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t ngroups = (N + 127) / 128 * (128 / PR_G);   // whole 128-row tiles (rs and wpad cover them)
+  // the warp index as a visibly warp-uniform value (launched with 8 warps): the loop's shuffles then compile without
+  // divergence handling (a threadIdx-derived bound made ptxas wrap each one, at 2.5x the registers)
+  const int64_t w0 = blockIdx.x * 8 + __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * 8;
   for (int64_t g = w0; g < ngroups; g += nw) {
-    const int64_t r0 = g * 32;
-    if (w) wpad[r0 + lane] = r0 + lane < N ? __ldg(w + r0 + lane) : 0.f;   // (the spread's weights, zero padded)
+    const int64_t r0 = g * PR_G;
+    if (w && lane < PR_G) wpad[r0 + lane] = r0 + lane < N ? __ldg(w + r0 + lane) : 0.f;
+    float4 v[PR_G];
+#pragma unroll
+    for (int u = 0; u < PR_G; ++u) {   // all loads in flight first (streamed once)
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (on && r0 + u < N) v[u] = __ldcs(reinterpret_cast<const float4*>(x + (r0 + u) * d) + lane);
+    }
     float am = 0.f;
-    for (int b = 0; b < 32; b += PR_U) {
-      float4 v[PR_U];
 #pragma unroll
-      for (int u = 0; u < PR_U; ++u) {   // all loads in flight first
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (on && r0 + b + u < N) v[u] = __ldcg(reinterpret_cast<const float4*>(x + (r0 + b + u) * d) + lane);
+    for (int u = 0; u < PR_G; ++u) {
+      am = fmaxf(am, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+      const float a = v[u].x - m4.x, b = v[u].y - m4.y, c = v[u].z - m4.z, e = v[u].w - m4.w;
+      float r2 = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
+      float n2 = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, v[u].w * v[u].w)));
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
       }
-#pragma unroll
-      for (int u = 0; u < PR_U; ++u) {
-        am = fmaxf(am, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
-        const float a = v[u].x - m4.x, bb = v[u].y - m4.y, c = v[u].z - m4.z, e = v[u].w - m4.w;
-        float r2 = fmaf(a, a, fmaf(bb, bb, fmaf(c, c, e * e)));
-        float n2 = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, v[u].w * v[u].w)));
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-          r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-          n2 += __shfl_xor_sync(0xffffffffu, n2, o);
-        }
-        bad |= !isfinite(n2);
-        r2max = fmaxf(r2max, r2);
-        n2max = fmaxf(n2max, n2);
-      }
+      bad |= !isfinite(n2);
+      r2max = fmaxf(r2max, r2);
+      n2max = fmaxf(n2max, n2);
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
     const float sg = group_scale(am);
     if (lane == 0) rs[g] = 1.0f / (256.0f * sg);   // (exact: a power of two)
-    if (!pad) continue;
-    for (int b = 0; b < 32; b += PR_U) {
-      float4 v[PR_U];
+    // (no early continue: the shuffles above must stay convergent)
 #pragma unroll
-      for (int u = 0; u < PR_U; ++u) {
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (on && r0 + b + u < N) v[u] = __ldcs(reinterpret_cast<const float4*>(x + (r0 + b + u) * d) + lane);
-      }
-#pragma unroll
-      for (int u = 0; u < PR_U; ++u) {
-        const int64_t r = r0 + b + u;
-        if (r >= N) break;
-        const float a0 = v[u].x * sg, a1 = v[u].y * sg, a2 = v[u].z * sg, a3 = v[u].w * sg;
-        const __half2 h01 = __floats2half2_rn(a0, a1), h23 = __floats2half2_rn(a2, a3);
-        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-        const __half2 l01 = __floats2half2_rn(a0 - f01.x, a1 - f01.y), l23 = __floats2half2_rn(a2 - f23.x, a3 - f23.y);
-        uint2 hv, lv;
-        hv.x = *reinterpret_cast<const uint32_t*>(&h01);
-        hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-        lv.x = *reinterpret_cast<const uint32_t*>(&l01);
-        lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-        __stcs(reinterpret_cast<uint2*>(xh + r * dp16) + lane, hv);
-        __stcs(reinterpret_cast<uint2*>(xl + r * dp16) + lane, lv);
-      }
+    for (int u = 0; u < PR_G; ++u) {
+      const int64_t r = r0 + u;
+      if (!pad || r >= N) continue;
+      const float a0 = v[u].x * sg, a1 = v[u].y * sg, a2 = v[u].z * sg, a3 = v[u].w * sg;
+      const __half2 h01 = __floats2half2_rn(a0, a1), h23 = __floats2half2_rn(a2, a3);
+      const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+      const __half2 l01 = __floats2half2_rn(a0 - f01.x, a1 - f01.y), l23 = __floats2half2_rn(a2 - f23.x, a3 - f23.y);
+      uint2 hv, lv;
+      hv.x = *reinterpret_cast<const uint32_t*>(&h01);
+      hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+      lv.x = *reinterpret_cast<const uint32_t*>(&l01);
+      lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+      __stcs(reinterpret_cast<uint2*>(xh + r * dp16) + lane, hv);
+      __stcs(reinterpret_cast<uint2*>(xl + r * dp16) + lane, lv);
     }
   }
   if (lane == 0) {
@@ -397,7 +387,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
       const int b = it & 1;
       const int c0 = h * 32;
       const int64_t i0 = t * FS_P + c0;
-      const float gat = ga * __ldg(rs + 4 * t + h);   // the 32-point group's 1 / (2^8 s_g): exact (a power of two)
+      const float* rsg = rs + 16 * t + 4 * h;   // the 8-point groups' 1 / (2^8 s_g) (powers of two: exact)
       mbar_wait_sleep(&tfull[b], (it >> 1) & 1);
       mbar_wait(&wfull[b], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -411,6 +401,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                      : "r"(taddr + j0));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const float gat = ga * __ldg(rsg + j0 / 8);   // (the 8 points are one scale group)
         // the 8 points' weights: two 16-byte broadcast loads (every lane reads the same address; zero beyond N)
         const float4 wa = w4[j0 / 4], wb = w4[j0 / 4 + 1];
         const float w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
@@ -668,7 +659,7 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
     int it = 0;
     for (int64_t t = t0; t < t1; ++t, ++it) {
       const int b = it & 1;
-      const float rt = __ldg(rs + 4 * t + q);   // the 32-target group's 1 / (2^8 s_g): exact (a power of two)
+      const float rt = __ldg(rs + 16 * t + 4 * q + (lane >> 3));   // this target's 1 / (2^8 s_g): exact
       mbar_wait_sleep(&tfull[b], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       uint32_t v[FE_SPW];
@@ -799,7 +790,7 @@ cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_
   const int dp16 = fused_dp16(d);
   auto prep = [&](const float* z, int64_t n, unsigned* out, uint16_t* h, uint16_t* l, float* rs, const float* w,
                   float* wp) {
-    int64_t blocks = ((n + 127) / 128 * 4 + 7) / 8;
+    int64_t blocks = ((n + 127) / 128 * (128 / PR_G) + 7) / 8;
     if (blocks > 148 * 4) blocks = 148 * 4;
     k_prep_f16<<<static_cast<unsigned>(blocks), 256, 0, st>>>(z, n, d, dp16, mu, out,
                                                                        reinterpret_cast<__half*>(h),

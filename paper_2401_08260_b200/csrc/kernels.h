@@ -199,7 +199,7 @@ bool fused_spread_ok(int d, const float* x);
 size_t source_bound_bytes(int d);   // scratch of launch_source_prep: mu, partial sums, nb (32 bytes, at the end)
 // launch_source_prep (once per call, direction-independent): mu, the norm words nb (max ||z - mu||^2, max ||z||^2,
 // non-finite) of x (nb[0..2]) and y (nb[4..6]), and both point sets as the fused kernels' FP16x2 operands in the
-// same pass: per 32-row group g a scale s_g = 2^(14 - e) (max |z| over the group = m 2^e), hi = f16(s_g z),
+// same pass: per 8-row group g a scale s_g = 2^(14 - e) (max |z| over the group = m 2^e), hi = f16(s_g z),
 // lo = f16(s_g z - hi) as fp16 arrays [rows][fused_dp16(d)] (pad columns zero), rs[g] = 1 / (2^8 s_g) (reading R2),
 // and the source weights w zero padded to whole 128-point tiles (wpad, read by the spread's bulk copies).
 // launch_bound_ranges (per slice batch): every slice's range bound c_p +- rho' of both sets into mm[p]

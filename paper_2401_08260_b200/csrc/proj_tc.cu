@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
   uint64_t* xfull = tempty + 2;         // [STAGES] TF32x2 with TMA points: the raw fp32 tile (hi piece) landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + STAGES);
   unsigned* rng = reinterpret_cast<unsigned*>(sm + SM::RANGE_OFF);   // [np_pad][4] keys
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // (the warp index through a shuffle: visibly warp-uniform, so the role branches below are uniform and the
+  // epilogue's warp collectives (redux, shuffles) compile without divergence handling)
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int ntn = (np + BN - 1) / BN;
   float* sinv = reinterpret_cast<float*>(rng + 4 * ntn * BN);          // [np_pad] 1/||g_p||
   // FP16x2: D accumulates (2^8 g) . (s x); the epilogue scale takes 1 / (2^8 s) with the 1 / ||g||

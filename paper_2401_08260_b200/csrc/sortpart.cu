@@ -772,7 +772,8 @@ __global__ void __launch_bounds__(S4_T) k_sp_gather(ZView zv, int np, int G, dou
     // warp w: slice p0 + w.  For a target of owner o, the x of owners < o lie below it and those of owners > o
     // above it: sum w |x - z| over them = z (Alo - Ahi) + (Bhi - Blo), from the owners' fp64 totals (fused here:
     // every CTA of the slice group rebuilds the small table; the first target block also writes the slice totals)
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, p = p0 + wid;
+    const int wid = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;   // (uniform)
+    const int p = p0 + wid;
     if (p < p1 && !GDAB) {
       const double* ot = otot + static_cast<int64_t>(p) * G * 4;
       double A = 0.0, B = 0.0, C = 0.0;

@@ -497,7 +497,7 @@ def test_fused_projection_spread(kind, scale, d, N, M, P):
 
 @pytest.mark.gpu
 def test_fused_mixed_row_magnitudes():
-    # the fused kernels' FP16x2 operands carry one power-of-two scale per 32-row group (fused.cu k_prep_f16): rows
+    # the fused kernels' FP16x2 operands carry one power-of-two scale per 8-row group (fused.cu k_prep_f16): rows
     # whose magnitudes differ by up to 2^8 inside a group keep the projection's fp32 accuracy (reading R2)
     cfg = I.Config("fused", "gaussian", 100, 300_001, 3000, 40, 33, 133, "mixture10", "pm1", param=200.0)
     x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
