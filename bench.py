@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg5", choices=sorted(I.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="async", choices=["sync", "async", "graph"],
+                    help="sks_options for the device-resident step: sync (status read per call), async (no host "
+                         "synchronisation; status read after the timed region), graph (async + CUDA-graph replay)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
@@ -309,9 +312,11 @@ def main():
 
     from paper_2401_08260_b200.parallel import distributed_sliced_sum
 
+    mode_kw = {"sync": {}, "async": {"async_": True}, "graph": {"graph": True}}[args.mode]
+
     def step():   # this rank's slice range through the C-ABI, then the one all-reduce (SUM) of the partials
         distributed_sliced_sum(lambda a, b: S.sks_sum(xd, yd, wd, cfg.kind, scale, cfg.P, cfg.dir_seed, a, b,
-                                                      cfg.matern_p, out=s, workspace=ws), cfg.P)
+                                                      cfg.matern_p, out=s, workspace=ws, **mode_kw), cfg.P)
 
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
@@ -338,6 +343,20 @@ def main():
         dist.barrier()
     clocks.wait_rows(r0 + 1, 1.0)
     clk = clocks.stop()
+    if args.mode != "sync":
+        S.sks_sync_status(ws)   # the device status of the timed calls (raises on a failed call)
+    kernels_from = "the timed region (CUDA events around every launch scope, on the launching stream)"
+    if args.mode == "graph":
+        # graph replays carry no per-launch events: the kernel breakdown comes from the same steps without the graph
+        S.sks_profile_read()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()
+            distributed_sliced_sum(lambda a, b: S.sks_sum(xd, yd, wd, cfg.kind, scale, cfg.P, cfg.dir_seed, a, b,
+                                                          cfg.matern_p, out=s, workspace=ws, async_=True), cfg.P)
+        torch.cuda.synchronize()
+        S.sks_sync_status(ws)
+        kernels_from = "an async (non-graph) pass of the same steps right after the timed graph region"
     prof = S.sks_profile_read()
     S.sks_profile_enable(False)
     ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
@@ -403,15 +422,17 @@ def main():
     for k, v in kernels.items():
         if k == "aux":
             continue
-        r = roofline(k, cfg, P_launch, plan, v["ms_per_step"] / max(1e-9, v["launches_per_step"]), pk,
-                     traffic_all.get(k))
+        lps = max(1e-9, v["launches_per_step"])
+        r = roofline(k, cfg, P_launch, plan, v["ms_per_step"] / lps, pk,
+                     traffic_all[k] / lps if isinstance(traffic_all.get(k), (int, float)) else None)
         v["roofline_frac"] = r["frac"]
         v["bound"] = r["bound"]
     # headline: the dominant top-level stage; the sort path's four kernels run on two streams and overlap,
     # so the stage (fork to join on the caller's stream) is the unit, its kernels are itemised in "kernels"
     dom = max((k for k in kernels if k != "aux" and not k.startswith("sp_")), key=lambda k: kernels[k]["ms_per_step"])
-    roof = roofline(dom, cfg, P_launch, plan, kernels[dom]["ms_per_step"] / max(1e-9, kernels[dom]["launches_per_step"]),
-                    pk, traffic_all.get(dom))
+    lps = max(1e-9, kernels[dom]["launches_per_step"])
+    roof = roofline(dom, cfg, P_launch, plan, kernels[dom]["ms_per_step"] / lps, pk,
+                    traffic_all[dom] / lps if isinstance(traffic_all.get(dom), (int, float)) else None)
     roof["share_of_step"] = kernels[dom]["ms_per_step"] / ms
 
     cpu = None
@@ -423,7 +444,7 @@ def main():
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": config_dict(cfg, param, G), "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": int(plan.get("launches", 0)) * args.steps, "clocks": clk,
-            "kernels": kernels, "plan": plan}
+            "mode": args.mode, "kernels_from": kernels_from, "kernels": kernels, "plan": plan}
     print(json.dumps(line), flush=True)
     if G > 1:
         dist.barrier()

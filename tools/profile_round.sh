@@ -16,7 +16,7 @@ timeout 200 python tools/latency.py cfg1 > $out/${tag}_latency_cfg1.json 2>&1
 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 \
   --csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $out/${tag}_launches_cfg5.csv 2> /dev/null
 # full captures: the cfg5 fused kernels on the full problem (tools/run_cfg.py: one call)
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_proj_spread|k_proj_eval|k_norm_bound" \
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_proj_spread|k_proj_eval|k_prep_f16" \
   -c 4 -o $out/${tag}_cfg5_full python tools/run_cfg.py cfg5 0 0 0 1 > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_proj_tc|k_sp_owner|k_sp_part" -c 4 \
   -o $out/${tag}_cfg4_full python tools/run_cfg.py cfg4 0 0 0 1 > /dev/null 2>&1
