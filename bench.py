@@ -91,14 +91,15 @@ def roofline_model(slot, cfg, P, plan):
     if slot == "sortsum":   # the sort stage (fork .. join of its kernels on two streams)
         return SORT_B_PER_SP * L * P, sum(comp.values()), None
     if plan.get("fused"):   # the fused large-N path (fused.cu): projection + spread / projection + interpolation
-        if slot == "minmax":   # source prep: one pass over x and y (norm bounds) writing their TF32x2 lo pieces
-            by = 4 * (N + M) * d * 2
+        dp16 = (d + 7) // 8 * 8
+        if slot == "minmax":   # source prep: one pass over x and y (norm bounds) writing their fp16 hi / lo rows
+            by = 4 * (N + M) * d + 4 * (N + M) * dp16 + 8 * N
             return by, by, None
-        if slot == "spread":   # per x slice-point: 2 d projection flops (tensor) + w taps (FP32); x and its lo piece
-            by = 8 * N * d + 4 * N + 4 * n * P
+        if slot == "spread":   # per x slice-point: 2 d projection flops (tensor) + w taps (FP32); x's fp16 hi / lo
+            by = 4 * N * dp16 + 4 * N + 4 * n * P
             return by, by, ("tensor", 2.0 * N * d * P), ("alu", 2.0 * N * P * w * 5)
         if slot == "eval":     # per y slice-point: 2 d projection flops (tensor) + one degree-7 Horner (FP32)
-            by = 8 * M * d + 8 * M + 4 * n * P
+            by = 4 * M * dp16 + 8 * M + 4 * n * P
             return by, by, ("tensor", 2.0 * M * d * P), ("alu", 2.0 * M * P * 7)
     if slot == "spread":    # per x slice-point: w taps, each a degree-7 window polynomial (even/odd form: 4 FMA
         #                     per tap) and one FMA into the grid

@@ -600,8 +600,8 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
     if (pt.fourier) {
       sks::FPar* fp = reinterpret_cast<sks::FPar*>(ws + L.fpar);
       float* grid = reinterpret_cast<float*>(ws + L.grid);
-      if (fused) {   // both point sets' range bounds in place of their exact ranges (fused.cu)
-        ProfScope ps(PS_MINMAX, st);
+      if (fused) {   // both point sets' range bounds in place of their exact ranges (fused.cu; the planner's input)
+        ProfScope ps(PS_PLAN, st);
         SKS_CUDA(sks::launch_bound_ranges(dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32, pr.d,
                                           dirs->inv + b0, nbat, reinterpret_cast<const double*>(ws + L.bound),
                                           reinterpret_cast<const unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32),
