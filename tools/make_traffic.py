@@ -15,11 +15,14 @@ SLOTS = [("k_split3", "split3"), ("k_proj_tc", "project"), ("k_minmax", "minmax"
          ("k_proj_eval", "eval"), ("k_eval", "eval")]
 rows = list(csv.reader(open(sys.argv[1])))
 hdr, per = None, {}
+# complete calls only: launches up to the last k_finalize (a launch list cut by ncu -c may end inside a call)
+fin = [int(r[0]) for r in rows if len(r) > 4 and r[0].isdigit() and "k_finalize" in r[4]]
+last = max(fin) if fin else 1 << 60
 for r in rows:
     if r and r[0] == "ID":
         hdr = r
         continue
-    if not hdr or len(r) < len(hdr):
+    if not hdr or len(r) < len(hdr) or not r[0].isdigit() or int(r[0]) > last:
         continue
     d = dict(zip(hdr, r))
     slot = next((s for k, s in SLOTS if k in d["Kernel Name"]), None)
