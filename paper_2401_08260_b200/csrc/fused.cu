@@ -207,10 +207,11 @@ __global__ void k_bound_ranges(const float* __restrict__ g32, int dp32, int d, c
 // ------------------------------------------------------------------ the fused projection + spread
 constexpr int FS_S = 128;          // slices per tile (UMMA M = TMEM lanes)
 constexpr int FS_P = 128;          // points per tile (UMMA N)
-constexpr int FS_STAGES = 3;
+constexpr int FS_STAGES = 2;       // (one tile of lookahead: the MMAs are far ahead of the epilogue)
 constexpr int FS_KBMAX = 2;        // k-blocks of 64 fp16 dims (128-byte rows): d <= 128
 constexpr int FS_WCAP = 32;        // private grid cells per slice (wider footprints: global atomics)
 constexpr int FS_EPI = 16;         // epilogue warps: 4 per TMEM lane quadrant, 32 points of the tile each
+constexpr int FS_NCOL = 2 * (FS_EPI / 4);   // private grid copies per slice: one per (point group, point parity)
 // warp roles: w0 .. FS_EPI - 1 epilogue, then TMEM alloc, -, TMA producer, MMA issuer.  The issuers take the highest
 // warp ids: the warp scheduler prefers the highest ready warp id, so the single-thread MMA loop is never starved
 // of issue slots by the busy epilogue warps of its SM sub-partition
@@ -220,7 +221,7 @@ constexpr int FS_PIECE = FS_P * 128;                      // one k-block of 128 
 constexpr int FS_A = FS_S * 128;                          // one k-block of the directions: 16 KB
 constexpr int FS_OFF_STAGE = FS_KBMAX * FS_A;             // 32 KB of resident directions
 constexpr int FS_OFF_GRID = FS_OFF_STAGE + FS_STAGES * 2 * FS_PIECE;
-constexpr int FS_OFF_W = FS_OFF_GRID + (FS_EPI / 4) * FS_WCAP * FS_S * 4;   // the tiles' weights [2][FS_P]
+constexpr int FS_OFF_W = FS_OFF_GRID + FS_NCOL * FS_WCAP * FS_S * 4;   // the tiles' weights [2][FS_P]
 constexpr int FS_OFF_BAR = FS_OFF_W + 2 * FS_P * 4;
 constexpr int FS_SMEM = FS_OFF_BAR + 512 + 1024;          // + barriers, TMEM slot, window coefficients, alignment
 static_assert(FS_SMEM <= 227 * 1024, "k_proj_spread shared memory");
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   // aligned by pointer arithmetic on the __shared__ array: the compiler keeps the shared state space (LDS / STS,
   // not generic LD / ST)
   unsigned char* sm = fsraw + ((1024u - (smem_u32(fsraw) & 1023u)) & 1023u);
-  float* priv = reinterpret_cast<float*>(sm + FS_OFF_GRID);   // [FS_EPI / 4][FS_WCAP][FS_S]
+  float* priv = reinterpret_cast<float*>(sm + FS_OFF_GRID);   // [FS_NCOL][FS_WCAP][FS_S]
   uint64_t* afull = reinterpret_cast<uint64_t*>(sm + FS_OFF_BAR);
   uint64_t* xfull = afull + 1;                 // [FS_STAGES] raw tile (hi) and lo piece landed
   uint64_t* empty = xfull + FS_STAGES;         // [FS_STAGES] consumed by the MMAs
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   const int64_t t0 = r * ntp / ranges, t1 = (r + 1) * ntp / ranges;   // this CTA's point tiles
   const int s0 = st_idx * FS_S;
 
-  for (int e = threadIdx.x; e < (FS_EPI / 4) * FS_WCAP * FS_S; e += FS_THREADS) priv[e] = 0.f;
+  for (int e = threadIdx.x; e < FS_NCOL * FS_WCAP * FS_S; e += FS_THREADS) priv[e] = 0.f;
   if (warp == 0 && lane == 0) {
     mbar_init(afull, 1);
     for (int s = 0; s < FS_STAGES; ++s) {
@@ -365,7 +366,10 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     const float ga = inv * taun, gb = -fmaf(f.cen, taun, 0.5f * pw.w);
     const int W = f.W;
     const bool wide = W > FS_WCAP;   // (footprint beyond the private column: global atomics for this slice)
-    float* col = priv + (h * FS_WCAP) * FS_S + 32 * q + lane;   // cell c at col[c * FS_S]
+    // two private copies of the slice's column per warp, for the even and the odd points of a pair: the pair's
+    // read-modify-writes cannot alias, so both points' loads are issued before either's stores
+    float* col = priv + (2 * h * FS_WCAP) * FS_S + 32 * q + lane;   // cell c at col[c * FS_S] (even points)
+    float* colo = col + FS_WCAP * FS_S;                             // (odd points)
     float* gp = grid + static_cast<int64_t>(live ? p : 0) * ncap;
     // window coefficients through shared memory into registers (read from the parameter bank, ptxas would
     // re-load them inside the loop)
@@ -435,17 +439,20 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
               tl[m] = __ffma2_rn(u, Om, Em);
               th[m] = __ffma2_rn(make_float2(-u.x, -u.y), Om, Em);
             }
-            float* cell = col + cl0 * FS_S;
+            float* c0p = col + cl0 * FS_S;    // even point: copy 0
+            float* c1p = colo + cl1 * FS_S;   // odd point: copy 1
+            float g0[WT], g1[WT];
 #pragma unroll
-            for (int m = 0; m < WT / 2; ++m) {
-              cell[m * FS_S] = fmaf(w8[jj], tl[m].x, cell[m * FS_S]);
-              cell[(WT - 1 - m) * FS_S] = fmaf(w8[jj], th[m].x, cell[(WT - 1 - m) * FS_S]);
+            for (int m = 0; m < WT; ++m) {   // all 2 WT loads first (disjoint copies: no ordering needed)
+              g0[m] = c0p[m * FS_S];
+              g1[m] = c1p[m * FS_S];
             }
-            cell = col + cl1 * FS_S;
 #pragma unroll
             for (int m = 0; m < WT / 2; ++m) {
-              cell[m * FS_S] = fmaf(w8[jj + 1], tl[m].y, cell[m * FS_S]);
-              cell[(WT - 1 - m) * FS_S] = fmaf(w8[jj + 1], th[m].y, cell[(WT - 1 - m) * FS_S]);
+              c0p[m * FS_S] = fmaf(w8[jj], tl[m].x, g0[m]);
+              c0p[(WT - 1 - m) * FS_S] = fmaf(w8[jj], th[m].x, g0[WT - 1 - m]);
+              c1p[m * FS_S] = fmaf(w8[jj + 1], tl[m].y, g1[m]);
+              c1p[(WT - 1 - m) * FS_S] = fmaf(w8[jj + 1], th[m].y, g1[WT - 1 - m]);
             }
           }
         } else if (live) {   // footprint wider than the private column: global atomics for this slice
@@ -473,7 +480,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp < 4) {   // flush: the FS_EPI / 4 private columns of each slice, one atomic per cell
+  if (warp < 4) {   // flush: the FS_NCOL private columns of each slice, one atomic per cell
     const int q = warp & 3, p = s0 + 32 * q + lane;
     if (p < np) {
       const FPar f = fp[p];
@@ -484,7 +491,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
         for (int c = 0; c < f.W; ++c) {
           float s = 0.f;
 #pragma unroll
-          for (int g = 0; g < FS_EPI / 4; ++g) s += c0[(g * FS_WCAP + c) * FS_S];
+          for (int g = 0; g < FS_NCOL; ++g) s += c0[(g * FS_WCAP + c) * FS_S];
           if (s != 0.f) atomicAdd(&gp[(f.lmin + c) & (n - 1)], s);
         }
       }
