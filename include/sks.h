@@ -81,7 +81,10 @@ typedef struct {
                             2 = NDFT on the kept band (the paper's Gaussian engine; at most 32
                             coefficients, else SKS_ERR_UNSUPPORTED); auto = NFFT (measured faster on B200)  */
   int32_t projection;    /* [0 = auto] row a1 arithmetic (R2), all fp32-accurate: 1 = BF16x3, 2 = TF32x2,
-                            3 = FP16x2 (falls back to TF32x2 where it cannot run); auto picks by d and alignment   */
+                            3 = FP16x2 (falls back to TF32x2 where it cannot run); auto picks by d and alignment.
+                            The fused large-N path (Fourier kernels, N >= 2^18, d <= 128, d % 4 == 0, 16-byte
+                            aligned rows) runs with auto or FP16x2 and computes FP16x2 with one power-of-two scale
+                            per 8 points; 1 / 2 force the unfused path                                             */
   int32_t async;         /* [0] 1: return right after enqueueing (no synchronisation); the device status is read by
                             sks_sync_status(workspace, stream)                                                     */
   int32_t deterministic; /* [0] 1: bitwise run-to-run deterministic results: no floating-point atomics --
@@ -112,8 +115,9 @@ typedef struct {
   int32_t proj_mode;     /* projection arithmetic: 0 none (given projections), 2 BF16x3 (three bf16
                             MMAs per product), 3 TF32x2 (two tf32 MMAs per product), 4 FP16x2 (two fp16 MMAs per
                             product on 2^e-scaled points); reading R2                                             */
-  int32_t fused;         /* 1: the sources' projections were spread from the tensor-core accumulators (rows a1 + a5
-                            fused, never stored), 0: projections stored and re-read            */
+  int32_t fused;         /* 1: the sources' projections were spread and the targets' interpolated straight from the
+                            tensor-core accumulators (rows a1 + a5 and a1 + a7 fused, never stored; SURVEY Sec. 8(f)
+                            f2; proj_mode 4), 0: projections stored and re-read                                    */
 } sks_plan_info;
 
 /* Bytes of DEVICE workspace sks_sum needs for this problem (slice range [p_begin, p_end) of P).
