@@ -651,7 +651,7 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
         // BJ / paper workloads), the Gaussian / Matern narrow ones (n_p ~ 64-1024)
         SKS_CUDA(sks::launch_fft_filter(grid, reinterpret_cast<const float*>(ws + L.D), nbat, kNcap, fp, plan.pw,
                                         reinterpret_cast<float*>(ws + L.Q), pr.k.kind == SKS_LAPLACIAN ? 4096 : 2048,
-                                        flag16, st));
+                                        fused, flag16, st));
       }
       launches += nbat <= 148 ? 2 : 3;
       ea.fourier = true;

@@ -501,35 +501,39 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
 }
 
 // ------------------------------------------------------------------ the fused projection + interpolation
-// Rows a1 + a7 for the TARGETS: persistent, one CTA per (slice group of 64, range of 128-point target tiles);
-// A = the target tile (TMA, TF32x2 as above), B = the group's directions (resident), tcgen05.mma M = 128 targets x
-// N = 64 slices into double-buffered TMEM (TMEM lane = target).  The group's interpolation polynomials Q (written by
-// k_fft_filter) are staged in shared memory once; an epilogue thread owns one target and 16 of the group's slices:
-// per slice one FMA for the grid coordinate, one 32-byte polynomial lookup (the lanes of a warp read the same
-// slice's table: broadcasts), one degree-7 Horner.  The four partial sums of a target (16 slices each) are added
-// in shared memory and the group's sum goes to the target's fp64 accumulator with one atomic.
+// Rows a1 + a7 for the TARGETS: persistent, one CTA per (slice group of 128, range of 128-point target tiles);
+// A = the target tile (TMA, FP16x2 as above), B = the group's directions (resident), tcgen05.mma M = 128 targets x
+// N = 128 slices into double-buffered TMEM (TMEM lane = target).  The group's interpolation polynomials Q (written by
+// k_fft_filter, economised to degree 5) are staged in shared memory once; an epilogue thread owns one target and 32
+// of the group's slices: per slice one FMA for the grid coordinate, one 24-byte polynomial lookup (the lanes of a
+// warp read the same slice's table), one degree-5 Horner.  The four partial sums of a target (32 slices each) are
+// added in shared memory and the group's sum goes to the target's fp64 accumulator with one atomic.
 constexpr int FE_T = 128;          // targets per tile (UMMA M)
-constexpr int FE_S = 64;           // slices per group (UMMA N)
-constexpr int FE_STAGES = 3;
+constexpr int FE_S = 128;          // slices per group (UMMA N): each target tile is loaded once per 128 slices
+constexpr int FE_STAGES = 2;
 constexpr int FE_QCAP = 40;        // cells of interpolation polynomials staged per slice (wider: read from global)
 constexpr int FE_EPI = 16;         // epilogue warps: FE_H per TMEM lane quadrant, FE_SPW slices each
 constexpr int FE_H = FE_EPI / 4, FE_SPW = FE_S / FE_H;
-static_assert(FE_SPW % 8 == 0, "TMEM loads of 8 columns");
+constexpr int FE_HALF = 16;        // TMEM columns (slices) loaded per round of an epilogue warp
+static_assert(FE_SPW % FE_HALF == 0 && FE_HALF % 8 == 0, "TMEM loads of 8 columns");
 constexpr int FE_WALLOC = FE_EPI, FE_WTMA = FE_EPI + 2, FE_WMMA = FE_EPI + 3;   // (roles as in k_proj_spread)
 constexpr int FE_THREADS = 32 * (4 + FE_EPI);
 constexpr int FE_PIECE = FE_T * 128;                      // one k-block of 128 targets: 16 KB
-constexpr int FE_B = FE_S * 128;                          // one k-block of the group's directions: 8 KB
+constexpr int FE_B = FE_S * 128;                          // one k-block of the group's directions: 16 KB
 constexpr int FE_OFF_STAGE = FS_KBMAX * FE_B;             // 32 KB of resident directions
-constexpr int FE_OFF_Q = FE_OFF_STAGE + FE_STAGES * 2 * FE_PIECE;
-constexpr int FE_OFF_SP = FE_OFF_Q + FE_S * FE_QCAP * 32;            // per-slice constants float4 [FE_S]
+constexpr int FE_OFF_Q = FE_OFF_STAGE + FE_STAGES * 2 * FE_PIECE;    // coefficients 0-3 float4 [FE_S][FE_QCAP]
+constexpr int FE_OFF_Q1 = FE_OFF_Q + FE_S * FE_QCAP * 16;            // coefficients 4-5 float2 [FE_S][FE_QCAP]
+constexpr int FE_OFF_SP = FE_OFF_Q1 + FE_S * FE_QCAP * 8;            // per-slice constants float4 [FE_S]
 constexpr int FE_OFF_RED = FE_OFF_SP + FE_S * 16;                    // partial sums [2][FE_H][FE_T] fp32
 constexpr int FE_OFF_BAR = FE_OFF_RED + 2 * FE_H * FE_T * 4;
 constexpr int FE_SMEM = FE_OFF_BAR + 256 + 1024;
 static_assert(FE_SMEM <= 227 * 1024, "k_proj_eval shared memory");
 
 // position of cell c in a slice's staged table: 16-byte entries, cells 8a + b stored at 8a + (b ^ (a & 7)), so that
-// the cells of a contiguous range fall into different 4-bank groups (a plain layout puts c and c + 8 in the same one)
+// the cells of a contiguous range fall into different 4-bank groups (a plain layout puts c and c + 8 in the same one);
+// 8-byte entries (the second plane): cells 16a + b at 16a + (b ^ (a & 15))
 __device__ __forceinline__ int qswz(int c) { return c ^ ((c >> 3) & 7); }
+__device__ __forceinline__ int qswz2(int c) { return c ^ ((c >> 4) & 15); }
 
 __global__ void __launch_bounds__(FE_THREADS, 1)
     k_proj_eval(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY,
@@ -542,7 +546,8 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
   extern __shared__ unsigned char feraw[];
   // aligned by pointer arithmetic on the __shared__ array (shared state space kept: LDS / STS)
   unsigned char* sm = feraw + ((1024u - (smem_u32(feraw) & 1023u)) & 1023u);
-  float4* sq = reinterpret_cast<float4*>(sm + FE_OFF_Q);   // [2][FE_S][FE_QCAP]: coefficients 0-3 | 4-7 of a cell
+  float4* sq = reinterpret_cast<float4*>(sm + FE_OFF_Q);   // [FE_S][FE_QCAP]: coefficients 0-3 of a cell
+  float2* sq1 = reinterpret_cast<float2*>(sm + FE_OFF_Q1); // [FE_S][FE_QCAP]: coefficients 4-5 (6, 7: economised)
   float4* sp = reinterpret_cast<float4*>(sm + FE_OFF_SP);  // (ga, gb, -, -) per slice; .z = int bits of lminA, .w = WQ
   float* red = reinterpret_cast<float*>(sm + FE_OFF_RED);  // [2][FE_H][FE_T]
   uint64_t* bfull = reinterpret_cast<uint64_t*>(sm + FE_OFF_BAR);
@@ -570,14 +575,20 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
     }
     sp[ls] = c;
   }
-  // (two planes: the lanes of a warp read one slice's table at ~16 distinct cells, 16-byte cell stride per plane:
-  // at most two lanes' cells share a bank group, half the wavefronts of the 32-byte interleaved layout)
-  for (int e = threadIdx.x; e < FE_S * FE_QCAP * 2; e += FE_THREADS) {
-    const int ls = e / (FE_QCAP * 2), rem = e - ls * FE_QCAP * 2, cell = rem >> 1, half = rem & 1;
+  // (two planes: the lanes of a warp read one slice's table at ~16 distinct cells; 16- and 8-byte cell strides)
+  for (int e = threadIdx.x; e < FE_S * FE_QCAP; e += FE_THREADS) {
+    const int ls = e / FE_QCAP, cell = e - ls * FE_QCAP;
     const int p = s0 + ls;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (p < np && cell < fp[p].WA) v = __ldg(reinterpret_cast<const float4*>(Q + p * qs + cell * 8) + half);
-    sq[(half * FE_S + ls) * FE_QCAP + qswz(cell)] = v;
+    float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float2 v1 = make_float2(0.f, 0.f);
+    if (p < np && cell < fp[p].WA) {
+      const float4* qc = reinterpret_cast<const float4*>(Q + p * qs + cell * 8);
+      v0 = __ldg(qc);
+      const float4 hi = __ldg(qc + 1);
+      v1 = make_float2(hi.x, hi.y);
+    }
+    sq[ls * FE_QCAP + qswz(cell)] = v0;
+    sq1[ls * FE_QCAP + qswz2(cell)] = v1;
   }
   if (warp == 0 && lane == 0) {
     mbar_init(bfull, 1);
@@ -669,82 +680,86 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
       const float rt = __ldg(rs + 16 * t + 4 * q + (lane >> 3));   // this target's 1 / (2^8 s_g): exact
       mbar_wait_sleep(&tfull[b], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      uint32_t v[FE_SPW];
       const uint32_t taddr =
           tmem_base + static_cast<uint32_t>(b * FE_S + FE_SPW * h) + (static_cast<uint32_t>(32 * q) << 16);
-#pragma unroll
-      for (int j8 = 0; j8 < FE_SPW; j8 += 8)
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                     : "=r"(v[j8]), "=r"(v[j8 + 1]), "=r"(v[j8 + 2]), "=r"(v[j8 + 3]), "=r"(v[j8 + 4]),
-                       "=r"(v[j8 + 5]), "=r"(v[j8 + 6]), "=r"(v[j8 + 7])
-                     : "r"(taddr + j8));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
       float acc = 0.f;
-      if (fits) {
-        // every table of the warp's 16 slices is staged: 4 slices at a time, their cells and both table loads
-        // first, then the 4 Horner chains (independent: latency hidden by ILP).  Dead slices (p >= np) have a zero
-        // table and WA = 1: they add exactly 0
+#pragma unroll 1
+      for (int hf = 0; hf < FE_SPW; hf += FE_HALF) {   // FE_HALF columns per TMEM load round: few registers held
+        uint32_t v[FE_HALF];
 #pragma unroll
-        for (int j0 = 0; j0 < FE_SPW; j0 += 4) {
-          float fr[4];
-          float4 c0[4], c1[4];
+        for (int j8 = 0; j8 < FE_HALF; j8 += 8)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                       : "=r"(v[j8]), "=r"(v[j8 + 1]), "=r"(v[j8 + 2]), "=r"(v[j8 + 3]), "=r"(v[j8 + 4]),
+                         "=r"(v[j8 + 5]), "=r"(v[j8 + 6]), "=r"(v[j8 + 7])
+                       : "r"(taddr + hf + j8));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (hf + FE_HALF == FE_SPW) {   // the accumulator is read: release it to the MMAs of tile t + 2
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[b]);
+        }
+        if (fits) {
+          // every table of the warp's slices is staged: 4 slices at a time, their cells and both table loads first,
+          // then the 4 Horner chains (independent: latency hidden by ILP).  Dead slices (p >= np) have a zero table
+          // and WA = 1: they add exactly 0
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int ls = FE_SPW * h + j0 + jj;
+          for (int j0 = 0; j0 < FE_HALF; j0 += 4) {
+            float fr[4];
+            float4 c0[4];
+            float2 c1[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int ls = FE_SPW * h + hf + j0 + jj;
+              const float4 c = sp[ls];   // broadcast
+              const float a = fmaf(__uint_as_float(v[j0 + jj]), c.x * rt, c.y), fl = floorf(a);
+              fr[jj] = a - fl;
+              // (fl is an integer of magnitude < 2^22: its int value from the 1.5 2^23 shift, no F2I)
+              int cl = (__float_as_int(fl + 12582912.f) - 0x4B400000) + 1 - __float_as_int(c.z);
+              const int wq = __float_as_int(c.w);
+              SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < wq));
+              cl = cl < 0 ? 0 : (cl >= wq ? wq - 1 : cl);   // (memory safety only)
+              c0[jj] = sq[ls * FE_QCAP + qswz(cl)];
+              c1[jj] = sq1[ls * FE_QCAP + qswz2(cl)];
+            }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              float tv = fmaf(c1[jj].y, fr[jj], c1[jj].x);
+              tv = fmaf(tv, fr[jj], c0[jj].w);
+              tv = fmaf(tv, fr[jj], c0[jj].z);
+              tv = fmaf(tv, fr[jj], c0[jj].y);
+              acc += fmaf(tv, fr[jj], c0[jj].x);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < FE_HALF; ++j) {
+            const int ls = FE_SPW * h + hf + j;
             const float4 c = sp[ls];   // broadcast
-            const float a = fmaf(__uint_as_float(v[j0 + jj]), c.x * rt, c.y), fl = floorf(a);
-            fr[jj] = a - fl;
-            // (fl is an integer of magnitude < 2^22: its int value from the 1.5 2^23 shift, no F2I)
-            int cl = (__float_as_int(fl + 12582912.f) - 0x4B400000) + 1 - __float_as_int(c.z);
+            const float a = fmaf(__uint_as_float(v[j]), c.x * rt, c.y), fl = floorf(a);
+            int cl = static_cast<int>(fl) + 1 - __float_as_int(c.z);
             const int wq = __float_as_int(c.w);
-            SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < wq));
-            cl = cl < 0 ? 0 : (cl >= wq ? wq - 1 : cl);   // (memory safety only)
-            c0[jj] = sq[ls * FE_QCAP + qswz(cl)];
-            c1[jj] = sq[(FE_S + ls) * FE_QCAP + qswz(cl)];
-          }
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            float tv = fmaf(c1[jj].w, fr[jj], c1[jj].z);
-            tv = fmaf(tv, fr[jj], c1[jj].y);
-            tv = fmaf(tv, fr[jj], c1[jj].x);
-            tv = fmaf(tv, fr[jj], c0[jj].w);
-            tv = fmaf(tv, fr[jj], c0[jj].z);
-            tv = fmaf(tv, fr[jj], c0[jj].y);
-            acc += fmaf(tv, fr[jj], c0[jj].x);
+            SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < wq));   // the bound holds
+            cl = cl < 0 ? 0 : (cl >= wq ? wq - 1 : cl);   // (a valid bound never clamps; memory safety only)
+            float4 c0;
+            float2 c1;
+            if (wq <= FE_QCAP) {
+              c0 = sq[ls * FE_QCAP + qswz(cl)];
+              c1 = sq1[ls * FE_QCAP + qswz2(cl)];
+            } else {   // footprint wider than the staged table: the polynomial from global memory
+              const float4* qp = reinterpret_cast<const float4*>(Q + (s0 + ls) * qs + cl * 8);
+              c0 = __ldg(qp);
+              const float4 hi = __ldg(qp + 1);
+              c1 = make_float2(hi.x, hi.y);
+            }
+            const float fr = a - fl;
+            float tv = fmaf(c1.y, fr, c1.x);
+            tv = fmaf(tv, fr, c0.w);
+            tv = fmaf(tv, fr, c0.z);
+            tv = fmaf(tv, fr, c0.y);
+            tv = fmaf(tv, fr, c0.x);
+            acc += (s0 + ls < np) ? tv : 0.f;
           }
         }
-      } else {
-#pragma unroll
-      for (int j = 0; j < FE_SPW; ++j) {
-        const int ls = FE_SPW * h + j;
-        const float4 c = sp[ls];   // broadcast
-        const float a = fmaf(__uint_as_float(v[j]), c.x * rt, c.y), fl = floorf(a);
-        int cl = static_cast<int>(fl) + 1 - __float_as_int(c.z);
-        const int wq = __float_as_int(c.w);
-        SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < wq));   // the bound holds
-        cl = cl < 0 ? 0 : (cl >= wq ? wq - 1 : cl);   // (a valid bound never clamps; memory safety only)
-        float4 c0, c1;
-        if (wq <= FE_QCAP) {
-          c0 = sq[ls * FE_QCAP + qswz(cl)];
-          c1 = sq[(FE_S + ls) * FE_QCAP + qswz(cl)];
-        } else {   // footprint wider than the staged table: the polynomial from global memory
-          const float4* qp = reinterpret_cast<const float4*>(Q + (s0 + ls) * qs + cl * 8);
-          c0 = __ldg(qp);
-          c1 = __ldg(qp + 1);
-        }
-        const float fr = a - fl;
-        float tv = fmaf(c1.w, fr, c1.z);
-        tv = fmaf(tv, fr, c1.y);
-        tv = fmaf(tv, fr, c1.x);
-        tv = fmaf(tv, fr, c0.w);
-        tv = fmaf(tv, fr, c0.z);
-        tv = fmaf(tv, fr, c0.y);
-        tv = fmaf(tv, fr, c0.x);
-        acc += (s0 + ls < np) ? tv : 0.f;
-      }
       }
       float* rb = red + (b * FE_H) * FE_T;
       rb[h * FE_T + 32 * q + lane] = acc;

@@ -403,7 +403,7 @@ __device__ __forceinline__ void fft_stages(float2* buf, const float2* tw, int n,
 // cap complex cells and their twiddles), the others exit at once
 __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restrict__ grid, const float* __restrict__ D,
                                                            int ncap, const FPar* __restrict__ fp, PolyWin pw,
-                                                           float* __restrict__ Q, int nlo, int cap,
+                                                           float* __restrict__ Q, int nlo, int cap, int econ,
                                                            const unsigned* __restrict__ flag16) {
   extern __shared__ float2 sm[];
   if (call_failed(flag16)) return;
@@ -450,16 +450,44 @@ __global__ void __launch_bounds__(FF_THREADS) k_fft_filter(const float* __restri
   // interpolation polynomials of the footprint cells: Q[c][k] = sum_j h[lminA + c + j] coef_j[k]
   const int l00 = f.lminA, WA = f.WA;
   float* qp = Q + static_cast<int64_t>(p) * q_stride(ncap);
-  for (int e = threadIdx.x; e < WA * (PW_D + 1); e += FF_THREADS) {
-    const int c = e / (PW_D + 1), k = e - c * (PW_D + 1);
-    float acc = 0.f;
-    for (int j = 0; j < pw.w; ++j) acc = fmaf(buf[(l00 + c + j) & (n - 1)].x, pw.c[j * (PW_D + 1) + k], acc);
-    qp[e] = acc;
+  if (!econ) {
+    for (int e = threadIdx.x; e < WA * (PW_D + 1); e += FF_THREADS) {
+      const int c = e / (PW_D + 1), k = e - c * (PW_D + 1);
+      float acc = 0.f;
+      for (int j = 0; j < pw.w; ++j) acc = fmaf(buf[(l00 + c + j) & (n - 1)].x, pw.c[j * (PW_D + 1) + k], acc);
+      qp[e] = acc;
+    }
+    return;
+  }
+  // economised to degree 5 (the fused interpolation reads 6 coefficients per cell): one thread per cell forms the
+  // degree-7 polynomial in fp64, then subtracts (a_7 / 2^13) T*_7 and (a_6 / 2^11) T*_6 (shifted Chebyshev
+  // polynomials T*_n(f) = T_n(2 f - 1), leading coefficient 2^(2n-1)): the change is at most |a_7| / 2^13 + |a_6'| /
+  // 2^11 on f in [0, 1] (|T*_n| <= 1) -- 0.5-2e-6 of the cell's amplitude for a band within n_p / 4 (R6b)
+  static_assert(PW_D == 7, "economisation of degree-7 polynomials");
+  for (int c = threadIdx.x; c < WA; c += FF_THREADS) {
+    double a[PW_D + 1];
+#pragma unroll
+    for (int k = 0; k <= PW_D; ++k) a[k] = 0.0;
+    for (int j = 0; j < pw.w; ++j) {
+      const double hv = buf[(l00 + c + j) & (n - 1)].x;
+#pragma unroll
+      for (int k = 0; k <= PW_D; ++k) a[k] = fma(hv, static_cast<double>(pw.c[j * (PW_D + 1) + k]), a[k]);
+    }
+    const double t7[8] = {-1.0, 98.0, -1568.0, 9408.0, -26880.0, 39424.0, -28672.0, 8192.0};
+    const double t6[7] = {1.0, -72.0, 840.0, -3584.0, 6912.0, -6144.0, 2048.0};
+    const double r7 = a[7] / 8192.0;
+#pragma unroll
+    for (int k = 0; k <= 7; ++k) a[k] -= r7 * t7[k];
+    const double r6 = a[6] / 2048.0;
+#pragma unroll
+    for (int k = 0; k <= 6; ++k) a[k] -= r6 * t6[k];
+#pragma unroll
+    for (int k = 0; k <= PW_D; ++k) qp[c * (PW_D + 1) + k] = k <= 5 ? static_cast<float>(a[k]) : 0.f;
   }
 }
 
 cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int ncap, const FPar* fp, const PolyWin& pw,
-                              float* Q, int cap_hint, const unsigned* flag16, cudaStream_t st) {
+                              float* Q, int cap_hint, bool econ, const unsigned* flag16, cudaStream_t st) {
   // two capacity tiers: the common grids (n_p <= cap_hint) with the shared memory they need -- several CTAs per SM
   // -- and, predicated on the device plan, any larger grid up to n_cap in a second launch whose CTAs otherwise exit
   auto smem_for = [](int cap) {
@@ -468,8 +496,9 @@ cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int nca
   set_smem_attr_once(reinterpret_cast<const void*>(k_fft_filter), static_cast<int>(smem_for(ncap)));
   // (at most one CTA per SM anyway -- np <= 148 -- one launch at full capacity saves the second launch's latency)
   const int cap = np <= 148 ? ncap : std::min(cap_hint, ncap);
-  k_fft_filter<<<np, FF_THREADS, smem_for(cap), st>>>(grid, D, ncap, fp, pw, Q, 0, cap, flag16);
-  if (cap < ncap) k_fft_filter<<<np, FF_THREADS, smem_for(ncap), st>>>(grid, D, ncap, fp, pw, Q, cap, ncap, flag16);
+  k_fft_filter<<<np, FF_THREADS, smem_for(cap), st>>>(grid, D, ncap, fp, pw, Q, 0, cap, econ ? 1 : 0, flag16);
+  if (cap < ncap)
+    k_fft_filter<<<np, FF_THREADS, smem_for(ncap), st>>>(grid, D, ncap, fp, pw, Q, cap, ncap, econ ? 1 : 0, flag16);
   return cudaGetLastError();
 }
 

@@ -227,9 +227,10 @@ cudaError_t launch_spread(ZView zv, const float* w, int np, const FPar* fp, int 
 // also writes the per-cell interpolation polynomials Q[p][c][k] = sum_j h[lminA + c + j] coef[j][k] for the
 // WA cells of the all-points footprint (Q stride kQStride(n_cap) floats per slice)
 __host__ __device__ inline int64_t q_stride(int ncap) { return static_cast<int64_t>(ncap + 16) * (PW_D + 1); }
-// (cap_hint: the grid size up to which the first of two launches handles a slice: sizes its shared memory)
+// (cap_hint: the grid size up to which the first of two launches handles a slice: sizes its shared memory;
+// econ: the polynomials economised to degree 5, coefficients 6 and 7 zero -- the fused interpolation's tables)
 cudaError_t launch_fft_filter(const float* grid, const float* D, int np, int ncap, const FPar* fp, const PolyWin& pw,
-                              float* Q, int cap_hint, const unsigned* flag16, cudaStream_t st);
+                              float* Q, int cap_hint, bool econ, const unsigned* flag16, cudaStream_t st);
 
 // rows a5 + a7 by the NDFT on the kept band (ndft.cu; the paper's Gaussian engine): KW = padded band
 // width (8, 16 or 32; ndft_width(K) = 0: too wide), what [np][2 KW] fp64 (zeroed by the caller)
