@@ -181,6 +181,25 @@ int det_groups(int64_t N, int64_t M, Path pt, int nslices, int batch) {
   return g;
 }
 
+// The Laplacian's Fourier part (plan, spread, FFT: rows a2, a5, a6) does not read the sort stage's results (rows a3,
+// a4), so it runs beside it on a side stream (forked after the projection, joined before the interpolation, which
+// needs the sort stage's slice totals for the moment term).  One stream and two events per (thread, device), as the
+// sort stage's helper streams (sortpart.cu): concurrent calls on different threads never share them.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool ok = false;
+};
+SideStream* side_stream(int dev) {
+  thread_local std::map<int, SideStream> pools;
+  SideStream& p = pools[dev];
+  if (!p.ok)
+    p.ok = cudaStreamCreateWithFlags(&p.s, cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p.join, cudaEventDisableTiming) == cudaSuccess;
+  return p.ok ? &p : nullptr;
+}
+
 // rows a1 + a5 and a1 + a7 fused (fused.cu) for the Fourier-only kernels when the points are many: the sources'
 // projections are spread and the targets' interpolated straight from the tensor-core accumulators; no projection
 // is stored.  The decision depends on the problem's shape only (never on data), so the workspace size is known up
@@ -578,6 +597,19 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
     ea.zv = zv;
     ea.np = nbat;
     ea.flag16 = flag16;
+    // the Laplacian's Fourier part beside the sort stage (SideStream above)
+    cudaStream_t fst = st;
+    SideStream* side = nullptr;
+    if (pt.sort && pt.fourier && !ndft) {
+      int dev = 0;
+      SKS_CUDA(cudaGetDevice(&dev));
+      side = side_stream(dev);
+      if (side) {
+        SKS_CUDA(cudaEventRecord(side->fork, st));
+        SKS_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+        fst = side->s;
+      }
+    }
     if (pt.sort) {
       // negdist: f = -c_d r; Laplacian sort part K2 = -alpha ||.||  -> -alpha c_d r (R7)
       sks::SortPartArgs sa{};
@@ -601,59 +633,63 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
       sks::FPar* fp = reinterpret_cast<sks::FPar*>(ws + L.fpar);
       float* grid = reinterpret_cast<float*>(ws + L.grid);
       if (fused) {   // both point sets' range bounds in place of their exact ranges (fused.cu; the planner's input)
-        ProfScope ps(PS_PLAN, st);
+        ProfScope ps(PS_PLAN, fst);
         SKS_CUDA(sks::launch_bound_ranges(dirs->g32 + static_cast<int64_t>(b0) * dirs->K32, dirs->K32, pr.d,
                                           dirs->inv + b0, nbat, reinterpret_cast<const double*>(ws + L.bound),
                                           reinterpret_cast<const unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32),
-                                          mm, flag16, st));
+                                          mm, flag16, fst));
         launches += 1;
       }
       {
-        ProfScope ps(PS_PLAN, st);
+        ProfScope ps(PS_PLAN, fst);
         SKS_CUDA(sks::launch_plan(mm, nbat, plan.pc, plan.phi2inv, fp, reinterpret_cast<float*>(ws + L.D), grid, flag16,
-                                  summary, st));
+                                  summary, fst));
         launches += 1;
       }
       if (ndft) {
         double* what = reinterpret_cast<double*>(ws + L.what);
         {
-          ProfScope ps(PS_AUX, st);
-          SKS_CUDA(sks::launch_zero(what, al(sizeof(double) * 2 * sks::kNdftWidth * static_cast<size_t>(nbat)), st));
+          ProfScope ps(PS_AUX, fst);
+          SKS_CUDA(sks::launch_zero(what, al(sizeof(double) * 2 * sks::kNdftWidth * static_cast<size_t>(nbat)), fst));
         }
         {
-          ProfScope ps(PS_NDFT_SPREAD, st);
-          SKS_CUDA(sks::launch_ndft_spread(zv, w, nbat, fp, what, det, flag16, st));
+          ProfScope ps(PS_NDFT_SPREAD, fst);
+          SKS_CUDA(sks::launch_ndft_spread(zv, w, nbat, fp, what, det, flag16, fst));
         }
         {
-          ProfScope ps(PS_NDFT_EVAL, st);
+          ProfScope ps(PS_NDFT_EVAL, fst);
           SKS_CUDA(sks::launch_ndft_eval(zv, nbat, fp, reinterpret_cast<const float*>(ws + L.D), kNcap / 2 + 1, what,
                                          target_acc((nbat + sks::kNdftEvalGroup - 1) / sks::kNdftEvalGroup), tps,
-                                         pt.sort, flag16, st));
+                                         pt.sort, flag16, fst));
         }
         launches += nbat <= 148 ? 2 : 3;
         continue;
       }
       if (fused) {
-        ProfScope ps(PS_SPREAD, st);
+        ProfScope ps(PS_SPREAD, fst);
         SKS_CUDA(sks::launch_proj_spread(reinterpret_cast<const uint16_t*>(ws + L.xh),
                                          reinterpret_cast<const uint16_t*>(ws + L.xl),
                                          reinterpret_cast<const float*>(ws + L.rsx), pr.N, pr.d,
                                          static_cast<const uint16_t*>(dirs->g16) + static_cast<int64_t>(b0) * dirs->K3,
                                          dirs->K3, dirs->inv + b0, nbat, reinterpret_cast<const float*>(ws + L.wpad), fp,
-                                         plan.pw, kNcap, grid, flag16, st));
+                                         plan.pw, kNcap, grid, flag16, fst));
       } else {
-        ProfScope ps(PS_SPREAD, st);
-        SKS_CUDA(sks::launch_spread(zv, w, nbat, fp, kNcap, plan.pw, pr.k.kind == SKS_LAPLACIAN, det, grid, flag16, st));
+        ProfScope ps(PS_SPREAD, fst);
+        SKS_CUDA(sks::launch_spread(zv, w, nbat, fp, kNcap, plan.pw, pr.k.kind == SKS_LAPLACIAN, det, grid, flag16, fst));
       }
       {
-        ProfScope ps(PS_FFT, st);
+        ProfScope ps(PS_FFT, fst);
         // the first tier's grid capacity: the Laplacian's smooth part needs wide bands (n_p ~ 2048-4096 on the
         // BJ / paper workloads), the Gaussian / Matern narrow ones (n_p ~ 64-1024)
         SKS_CUDA(sks::launch_fft_filter(grid, reinterpret_cast<const float*>(ws + L.D), nbat, kNcap, fp, plan.pw,
                                         reinterpret_cast<float*>(ws + L.Q), pr.k.kind == SKS_LAPLACIAN ? 4096 : 2048,
-                                        fused, flag16, st));
+                                        fused, flag16, fst));
       }
       launches += nbat <= 148 ? 2 : 3;
+      if (side) {   // join: the interpolation (on st, after the sort stage) waits for the Fourier part
+        SKS_CUDA(cudaEventRecord(side->join, fst));
+        SKS_CUDA(cudaStreamWaitEvent(st, side->join, 0));
+      }
       ea.fourier = true;
       ea.fp = fp;
       ea.Q = reinterpret_cast<const float*>(ws + L.Q);
