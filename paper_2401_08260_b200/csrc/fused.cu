@@ -521,8 +521,10 @@ constexpr int FE_THREADS = 32 * (4 + FE_EPI);
 constexpr int FE_PIECE = FE_T * 128;                      // one k-block of 128 targets: 16 KB
 constexpr int FE_B = FE_S * 128;                          // one k-block of the group's directions: 16 KB
 constexpr int FE_OFF_STAGE = FS_KBMAX * FE_B;             // 32 KB of resident directions
-constexpr int FE_OFF_Q = FE_OFF_STAGE + FE_STAGES * 2 * FE_PIECE;    // coefficients 0-3 float4 [FE_S][FE_QCAP]
-constexpr int FE_OFF_Q1 = FE_OFF_Q + FE_S * FE_QCAP * 16;            // coefficients 4-5 float2 [FE_S][FE_QCAP]
+// the cells' degree-5 polynomials in three planes of coefficient pairs (0-1, 2-3, 4-5), float2 [FE_S][FE_QCAP] each:
+// an 8-byte lookup per plane is served in 2 wavefronts (ncu: a 16-byte lookup of the same cells took 5)
+constexpr int FE_OFF_Q = FE_OFF_STAGE + FE_STAGES * 2 * FE_PIECE;    // coefficients 0-1 | 2-3 (two planes)
+constexpr int FE_OFF_Q1 = FE_OFF_Q + FE_S * FE_QCAP * 16;            // coefficients 4-5
 constexpr int FE_OFF_SP = FE_OFF_Q1 + FE_S * FE_QCAP * 8;            // per-slice constants float4 [FE_S]
 constexpr int FE_OFF_RED = FE_OFF_SP + FE_S * 16;                    // partial sums [2][FE_H][FE_T] fp32
 constexpr int FE_OFF_BAR = FE_OFF_RED + 2 * FE_H * FE_T * 4;
@@ -546,7 +548,8 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
   extern __shared__ unsigned char feraw[];
   // aligned by pointer arithmetic on the __shared__ array (shared state space kept: LDS / STS)
   unsigned char* sm = feraw + ((1024u - (smem_u32(feraw) & 1023u)) & 1023u);
-  float4* sq = reinterpret_cast<float4*>(sm + FE_OFF_Q);   // [FE_S][FE_QCAP]: coefficients 0-3 of a cell
+  float2* sqa = reinterpret_cast<float2*>(sm + FE_OFF_Q);                     // [FE_S][FE_QCAP]: coefficients 0-1
+  float2* sqb = reinterpret_cast<float2*>(sm + FE_OFF_Q + FE_S * FE_QCAP * 8);  // 2-3
   float2* sq1 = reinterpret_cast<float2*>(sm + FE_OFF_Q1); // [FE_S][FE_QCAP]: coefficients 4-5 (6, 7: economised)
   float4* sp = reinterpret_cast<float4*>(sm + FE_OFF_SP);  // (ga, gb, -, -) per slice; .z = int bits of lminA, .w = WQ
   float* red = reinterpret_cast<float*>(sm + FE_OFF_RED);  // [2][FE_H][FE_T]
@@ -587,7 +590,8 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
       const float4 hi = __ldg(qc + 1);
       v1 = make_float2(hi.x, hi.y);
     }
-    sq[ls * FE_QCAP + qswz(cell)] = v0;
+    sqa[ls * FE_QCAP + qswz2(cell)] = make_float2(v0.x, v0.y);
+    sqb[ls * FE_QCAP + qswz2(cell)] = make_float2(v0.z, v0.w);
     sq1[ls * FE_QCAP + qswz2(cell)] = v1;
   }
   if (warp == 0 && lane == 0) {
@@ -718,7 +722,8 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
               const int wq = __float_as_int(c.w);
               SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < wq));
               cl = cl < 0 ? 0 : (cl >= wq ? wq - 1 : cl);   // (memory safety only)
-              c0[jj] = sq[ls * FE_QCAP + qswz(cl)];
+              const float2 qa = sqa[ls * FE_QCAP + qswz2(cl)], qb = sqb[ls * FE_QCAP + qswz2(cl)];
+              c0[jj] = make_float4(qa.x, qa.y, qb.x, qb.y);
               c1[jj] = sq1[ls * FE_QCAP + qswz2(cl)];
             }
 #pragma unroll
@@ -743,7 +748,8 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
             float4 c0;
             float2 c1;
             if (wq <= FE_QCAP) {
-              c0 = sq[ls * FE_QCAP + qswz(cl)];
+              const float2 qa = sqa[ls * FE_QCAP + qswz2(cl)], qb = sqb[ls * FE_QCAP + qswz2(cl)];
+              c0 = make_float4(qa.x, qa.y, qb.x, qb.y);
               c1 = sq1[ls * FE_QCAP + qswz2(cl)];
             } else {   // footprint wider than the staged table: the polynomial from global memory
               const float4* qp = reinterpret_cast<const float4*>(Q + (s0 + ls) * qs + cl * 8);
