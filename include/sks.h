@@ -188,6 +188,14 @@ sks_status sks_profile_read(double* ms, int64_t* launches, int32_t n_slots);
 /* Comma-separated slot names: "project,minmax,sortsum,plan_D,spread,fft_filter,eval,aux". */
 const char* sks_profile_names(void);
 
+/* Frees the library's device caches: the cached directions of every (device, seed, P, d, slice range) seen so far
+ * (P_local x d x 8 bytes each), the planner's window tables and the CUDA graphs of sks_options.graph.  The caches
+ * otherwise live until the process exits (calls with new (seed, P, d, range) keys add entries; each entry's first
+ * call uploads it synchronously).  Waits for all work on the devices that hold entries; must not run while other
+ * sks calls are in flight on any thread (their cached pointers would be freed).  The next call rebuilds what it
+ * needs.  Returns SKS_OK or SKS_ERR_CUDA. */
+sks_status sks_release_caches(void);
+
 /* Thread-local message for the last non-OK status ("" if none). */
 const char* sks_last_error(void);
 

@@ -16,7 +16,7 @@ from ._lib import SKSError, check, kernel, options  # noqa: F401
 
 __all__ = ["sks_workspace_size", "sks_sum", "sks_sum_host", "sks_workspace_size_host", "sks_directions",
            "sks_project", "sks_sum_1d", "sks_workspace_size_1d", "sks_fourier_coeffs", "sks_last_plan", "sks_sync_status",
-           "sks_version", "sks_profile_enable", "sks_profile_read", "SKSError"]
+           "sks_version", "sks_release_caches", "sks_profile_enable", "sks_profile_read", "SKSError"]
 
 
 def _torch():
@@ -51,6 +51,11 @@ def _alloc_workspace(nbytes: int, device):
 
 def sks_version() -> str:
     return _lib.load().sks_version().decode()
+
+
+def sks_release_caches() -> None:
+    """Free the library's device caches (directions, planner tables, CUDA graphs); include/sks.h."""
+    check(_lib.load().sks_release_caches())
 
 
 def sks_workspace_size(N: int, M: int, d: int, kind: str, scale: float, P: int, p_begin: int = 0,

@@ -56,6 +56,7 @@ SIGNATURES = {
     "sks_profile_enable": (_i32, [_i32]),
     "sks_profile_read": (_i32, [_vp, _vp, _i32]),
     "sks_profile_names": (ctypes.c_char_p, []),
+    "sks_release_caches": (_i32, []),
     "sks_last_error": (ctypes.c_char_p, []),
     "sks_version": (ctypes.c_char_p, []),
 }

@@ -794,6 +794,39 @@ extern "C" {
 
 const char* sks_version(void) { return "sks 0.2 (sm_100a)"; }
 
+sks_status sks_release_caches(void) {
+  int cur = 0;
+  SKS_CUDA(cudaGetDevice(&cur));
+  cudaError_t first = cudaSuccess;
+  auto keep = [&](cudaError_t e) {
+    if (first == cudaSuccess && e != cudaSuccess) first = e;
+  };
+  std::lock_guard<std::mutex> lg(g_graph_mu);   // (lock order: graphs, directions, plans -- as the calls take them)
+  for (auto& kv : g_graphs) keep(cudaGraphExecDestroy(kv.second.exec));
+  g_graphs.clear();
+  std::lock_guard<std::mutex> ld(g_dir_mu);
+  for (auto& kv : g_dirs) {
+    keep(cudaSetDevice(std::get<0>(kv.first)));
+    keep(cudaDeviceSynchronize());
+    DirEntry& e = kv.second;
+    keep(cudaFree(e.inv));
+    keep(cudaFree(e.g3));
+    keep(cudaFree(e.g32));
+    keep(cudaFree(e.g16));
+  }
+  g_dirs.clear();
+  std::lock_guard<std::mutex> lp(g_plan_mu);
+  for (auto& kv : g_plans) {
+    keep(cudaSetDevice(std::get<0>(kv.first)));
+    keep(cudaDeviceSynchronize());
+    keep(cudaFree(kv.second.phi2inv));
+  }
+  g_plans.clear();
+  keep(cudaSetDevice(cur));
+  if (first != cudaSuccess) return fail(SKS_ERR_CUDA, std::string("sks_release_caches: ") + cudaGetErrorString(first));
+  return SKS_OK;
+}
+
 const char* sks_last_error(void) { return g_err.c_str(); }
 
 sks_status sks_profile_enable(int32_t enable) {

@@ -537,3 +537,18 @@ def test_deterministic_mode_bitwise(name, size, kw):
     ref = O.sliced_sum(cfg.kind, par if cfg.kind != "negdist" else 0.0, x, y, w, cfg.P, cfg.dir_seed, targets=tgt,
                        matern_p=cfg.matern_p)
     assert rel_err(runs[0][tgt], ref, w) <= TOL[cfg.kind]
+
+
+def test_release_caches_then_rebuild():
+    # sks_release_caches frees the cached directions, planner tables and CUDA graphs; the next calls rebuild them
+    # and return the same sums (eager and graph-replayed calls)
+    cfg = I.CONFIGS["cfg1"]
+    x, y, w = (dev(v) for v in (I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)))
+    s1 = S.sks_sum(x, y, w, "gaussian", 1.0, cfg.P, cfg.dir_seed).cpu()
+    g1 = S.sks_sum(x, y, w, "gaussian", 1.0, cfg.P, cfg.dir_seed, graph=True).cpu()
+    S.sks_release_caches()
+    s2 = S.sks_sum(x, y, w, "gaussian", 1.0, cfg.P, cfg.dir_seed).cpu()
+    g2 = S.sks_sum(x, y, w, "gaussian", 1.0, cfg.P, cfg.dir_seed, graph=True).cpu()
+    S.sks_release_caches()
+    assert torch.equal(s1, s2) and torch.equal(g1, g2)
+    assert float((s1 - g1).abs().max()) <= 1e-6 * float(w.abs().sum())
