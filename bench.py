@@ -122,6 +122,20 @@ def tensor_peak(pk, pmode):
     return pk["bf16_tflops"] / div, src.get(pmode, "MEASURED_PEAKS.json bf16_tflops / 3 (BF16x3)")
 
 
+def alu_peak(pk):
+    """FP32 FMA peak (TFLOP/s, source): the measured packed-FMA (FFMA2, the fused spread's form) throughput of a B200
+    at its maximum clock (tools/fp32_peak.cu -> profiles/r02/fp32_peak.json: 74.3 TF/s, scalar 3-register FFMA 72.5),
+    else the unit counts (148 SMs x 128 FP32 lanes x 2 flop x sm_max_mhz, B200_PROFILING.md)"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "fp32_peak.json")) as f:
+            m = json.load(f)
+        return (float(m["ffma2_tflops"]), "measured FFMA2 throughput at %d MHz (tools/fp32_peak.cu, "
+                "profiles/r02/fp32_peak.json)" % m["max_clock_mhz"])
+    except (OSError, KeyError, ValueError):
+        return (148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12,
+                "148 SMs x 128 FP32 lanes x 2 flop/FMA x sm_max_mhz (B200_PROFILING unit counts)")
+
+
 def roofline(slot, cfg, P, plan, ms_per_launch, pk, traffic):
     """achieved / peak of one kernel, Sec. 8(d) units: the bound is the larger of the HBM time of its Sec. 8(d)
     bytes and the time of its algorithmic arithmetic at peak (tensor for the projection, FP32 FMA for the
@@ -129,10 +143,7 @@ def roofline(slot, cfg, P, plan, ms_per_launch, pk, traffic):
     by, comp, *work = roofline_model(slot, cfg, P, plan)
     work = [x for x in work if x]
     t = ms_per_launch * 1e-3
-    alu = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    peaks_tf = {"tensor": tensor_peak(pk, plan.get("proj_mode")),
-                "alu": (alu, "148 SMs x 128 FP32 lanes x 2 flop/FMA x sm_max_mhz (MEASURED_PEAKS.json; B200_PROFILING "
-                             "unit counts)")}
+    peaks_tf = {"tensor": tensor_peak(pk, plan.get("proj_mode")), "alu": alu_peak(pk)}
     hbm = pk["hbm_gbs"]
     # the binding resource of the model: the largest of the HBM time and each arithmetic unit's time at its peak
     kind, fl = max(work, key=lambda kf: kf[1] / (peaks_tf[kf[0]][0] * 1e12)) if work else (None, 0.0)
