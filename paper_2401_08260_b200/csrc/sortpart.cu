@@ -49,6 +49,7 @@ constexpr int S0_T = 512;      // histogram threads
 // {4096,1024,2,512} 401; finer buckets {4096,2048,3,512} 418.  At d = 100, P = 1000, N = 1e6 / 1e7 (ms): kept
 // 34.5 / 489, the others 35.5-40.2 / 485-588.
 constexpr int SP_CAP = 4096, SP_NBF = 1024, SP_MINB = 3, SP_NT = 512;
+static_assert(SP_CAP < 65536, "bucket bounds packed as 16-bit pairs (OwnerShared::se)");
 constexpr int S4_T = 256, S4_PER = 4, S4_CH = S4_T * S4_PER;    // gather
 constexpr int S4_SG = 8;   // slices per gather thread (measured 4 / 8 / 16 / 32: 8 best; also on the global-table
                            // path at N = 1e7, P = 1000: 8 / 16 / 32 -> 489 / 494 / 507 ms, scratch/gsg.sh)
@@ -481,7 +482,8 @@ struct __align__(16) OwnerShared {
   float2 xs[SP_CAP];          // the pass's x (z, w) in fine-bucket order
   double2 rec[SP_NBF + 1];    // exclusive prefix (sum w, sum w x) over the pass's buckets; [NBF] = pass totals
   int start[SP_NBF + 1];      // bucket b holds xs[start[b], start[b+1])
-  int2 se[SP_NBF];            // (start[b], start[b+1]) in one 8-byte word for the lookups
+  unsigned se[SP_NBF];        // start[b] | start[b+1] << 16 in one 4-byte word for the lookups (SP_CAP <= 8192):
+                              // a random 4-byte lookup costs fewer shared-memory wavefronts than an 8-byte one
   int wbuf[NT / 32 + 1];
   double2 dbuf[NT / 32 + 1];
 };
@@ -522,6 +524,8 @@ __device__ __forceinline__ double2 block_excl_scan_d2(double2 v, double2* wbuf, 
   __syncthreads();
   return r;
 }
+
+__device__ __forceinline__ int2 se_unpack(unsigned v) { return make_int2(static_cast<int>(v & 0xffffu), static_cast<int>(v >> 16)); }
 
 template <int SP_CAP, int SP_NBF, int MINB, int S3_T>
 __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restrict__ own, double* __restrict__ otot,
@@ -580,7 +584,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
 #pragma unroll
       for (int j = 0; j < PB; ++j) {
         S.start[tid * PB + j] = run;
-        S.se[tid * PB + j] = make_int2(run, run + c[j]);
+        S.se[tid * PB + j] = static_cast<unsigned>(run) | (static_cast<unsigned>(run + c[j]) << 16);
         run += c[j];
       }
       if (tid == 0) S.start[SP_NBF] = total;
@@ -597,7 +601,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
                  // shared atomics' timing; the bucket sums below are then taken in a fixed order); a bucket holds a
                  // handful of points, one thread sorts it by insertion
       for (int b = tid; b < SP_NBF; b += S3_T) {
-        const int2 br = S.se[b];
+        const int2 br = se_unpack(S.se[b]);
         for (int i = br.x + 1; i < br.y; ++i) {
           const float2 v = S.xs[i];
           int j = i - 1;
@@ -617,7 +621,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
     for (int c0 = 0; c0 < SP_NBF; c0 += S3_T) {
       const int b = c0 + tid;
       double2 v = make_double2(0.0, 0.0);
-      const int2 br = S.se[b];
+      const int2 br = se_unpack(S.se[b]);
       for (int i = br.x, e = br.y; i < e; ++i) {
         const float2 q = S.xs[i];
         const double wz = static_cast<double>(q.y) * q.x;
@@ -676,7 +680,7 @@ __global__ void __launch_bounds__(S3_T, MINB) k_sp_owner(const SpOwner* __restri
         const float zf = zy[k];
         const int b = fine_of<SP_NBF>(ucoord(zf, uoff, hscale), r.blo, r.fmul);
         const double2 rb = S.rec[b];
-        const int2 jr = S.se[b];
+        const int2 jr = se_unpack(S.se[b]);
         const int j0 = jr.x, j1 = jr.y;
         float s0 = 0.f, s1 = 0.f;
         int j = j0;
