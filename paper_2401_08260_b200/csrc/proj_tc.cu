@@ -571,6 +571,373 @@ __global__ void __launch_bounds__(MODE != 0 ? TC_THREADS_TF32 : TC_THREADS, 1)
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
 }
 
+// ------------------------------------------------------------------ FP16x2 on CTA pairs (cta_group::2)
+// The FP16x2 projection is bound by the SM's shared-memory pipe (TMA writes, converters, MMA operand reads: 224 KB
+// per 64-dim k-block against 1024 tensor cycles).  A CTA pair (cluster of 2 on one TPC) computes a 256-point x
+// 256-slice tile with tcgen05.mma.cta_group::2 (M = 256, N = 256): each CTA converts its own 128 points and
+// loads only its half of the direction tile; the pair's tensor cores share the B halves, so each SM's shared
+// memory serves half the direction bytes (176 KB per k-block).  Each CTA's TMEM holds its 128 points x 256 slices
+// (double-buffered); the epilogue is the single-CTA one.  Barriers: per CTA xfull (raw tile landed), ready
+// (converters done + own direction half landed), empty (MMA done, multicast commit to both CTAs), tfull (multicast);
+// in the leader (rank 0) only: peer[stage] (the peer's ready, forwarded by its otherwise idle MMA warp with a
+// cluster-scope arrive) and tempty (both CTAs' epilogue warps, count 2 NEPI).
+constexpr int PR_STAGES = 4;
+constexpr int PR_BN = 256;
+constexpr int PR_A = TC_M * 128;          // one fp16 piece of 128 points x 64 dims (or a raw fp32 box of 32 dims)
+constexpr int PR_BH = 128 * 128;          // this CTA's half of the direction tile: 128 slices x 64 dims
+constexpr int PR_STAGE = 2 * PR_A + PR_BH;
+constexpr int PR_BAR_OFF = PR_STAGES * PR_STAGE;
+constexpr int PR_RANGE_OFF = (PR_BAR_OFF + 8 * (5 * PR_STAGES + 4) + 16 + 63) / 64 * 64;
+constexpr int PR_FIXED = PR_RANGE_OFF + 1024;
+constexpr int PR_NEPI = 4, PR_CW0 = 8, PR_NCONV = 8, PR_RPW = TC_M / PR_NCONV;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_TF32, 1)
+    k_proj_pair(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ CUtensorMap tmY, int nk, int64_t L, int64_t Nx, int np,
+                const float* __restrict__ inv_norm, float* __restrict__ Z, int64_t ldz, unsigned* __restrict__ mm,
+                int* __restrict__ flag, const float* __restrict__ py, int d, const unsigned* __restrict__ f16max) {
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(sm + PR_BAR_OFF);
+  uint64_t* ready = xfull + PR_STAGES;
+  uint64_t* peer = ready + PR_STAGES;
+  uint64_t* empty = peer + PR_STAGES;
+  uint64_t* tfull = empty + PR_STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  unsigned* rng = reinterpret_cast<unsigned*>(sm + PR_RANGE_OFF);
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int ntn = (np + PR_BN - 1) / PR_BN;
+  float* sinv = reinterpret_cast<float*>(rng + 4 * ntn * PR_BN);
+  const float zs = 1.0f / (256.0f * f16_scale(__ldg(f16max)));
+  for (int c = threadIdx.x; c < ntn * PR_BN; c += blockDim.x) sinv[c] = (c < np) ? inv_norm[c] * zs : 0.f;
+  const int64_t ntm = (L + 2 * TC_M - 1) / (2 * TC_M);
+  const int64_t ntiles = ntm * ntn;
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  for (int c = threadIdx.x; c < ntn * PR_BN; c += blockDim.x) {
+    rng[4 * c + 0] = 0xffffffffu; rng[4 * c + 1] = 0u; rng[4 * c + 2] = 0xffffffffu; rng[4 * c + 3] = 0u;
+  }
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < PR_STAGES; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&ready[s], PR_NCONV + 1);
+      mbar_init(&peer[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2 * PR_NEPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * PR_BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();   // both CTAs' barriers initialised before any cross-CTA arrive
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer: this CTA's 128 raw fp32 points (two boxes of 32 dims) and its half of the direction tile
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = pair; t < ntiles; t += npairs) {
+      const int64_t m0 = (t / ntn) * (2 * TC_M) + TC_M * rank;
+      const int nb = static_cast<int>(t % ntn) * PR_BN + 128 * static_cast<int>(rank);
+      const bool hasx = m0 < Nx;
+      const CUtensorMap* mp = hasx ? &tmX : &tmY;
+      const int row = hasx ? static_cast<int>(m0) : static_cast<int>(m0 - Nx);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char* sa = sm + stage * PR_STAGE;
+        mbar_expect_tx(&xfull[stage], 2 * PR_A);
+        tma_load_2d(mp, &xfull[stage], sa, kb * 64, row);
+        tma_load_2d(mp, &xfull[stage], sa + PR_A, kb * 64 + 32, row);
+        mbar_expect_tx(&ready[stage], PR_BH);
+        tma_load_2d(&tmB, &ready[stage], sa + 2 * PR_A, kb * TC_BK, nb);
+        if (++stage == PR_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    if (leader) {
+      // ---- MMA issuer (leader): D[256 points][256 slices] across the pair, K = 16 per MMA
+      constexpr uint32_t idesc = idesc_f16(2 * TC_M, PR_BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int64_t t = pair; t < ntiles; t += npairs, ++it) {
+        const int b = it & 1;
+        mbar_wait_cluster(&tempty[b], ((it >> 1) & 1) ^ 1);   // both CTAs' epilogues drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(b * PR_BN);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&ready[stage], phase);
+          mbar_wait_cluster(&peer[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const unsigned char* sa = sm + stage * PR_STAGE;
+          const uint64_t db = umma_desc_sw128(sa + 2 * PR_A);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint64_t da = umma_desc_sw128(sa + q * PR_A);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t acc = (kb > 0 || q > 0 || k > 0) ? 1u : 0u;
+              const uint64_t adv = static_cast<uint64_t>((k * 32) >> 4);
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\t"
+                  "setp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                  "l"(da + adv), "l"(db + adv), "r"(idesc), "r"(acc));
+            }
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_u32(&empty[stage])),
+              "h"(static_cast<uint16_t>(3))
+              : "memory");
+          if (++stage == PR_STAGES) { stage = 0; phase ^= 1; }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(&tfull[b])),
+            "h"(static_cast<uint16_t>(3))
+            : "memory");
+      }
+    } else {
+      // ---- forwarder (peer): this CTA's stage is ready (its points converted, its direction half landed)
+      const uint32_t rpeer = mapa_rank(&peer[0], 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = pair; t < ntiles; t += npairs)
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&ready[stage], phase);
+          mbar_arrive_remote(rpeer + 8u * static_cast<uint32_t>(stage));
+          if (++stage == PR_STAGES) { stage = 0; phase ^= 1; }
+        }
+    }
+  } else if (warp >= PR_CW0) {
+    // ---- converters (as k_proj_tc MODE 3): the raw fp32 rows of a k-block -> fp16 hi / lo of the scaled points
+    const int cw = warp - PR_CW0;
+    const int c = lane & 7, rsub = lane >> 3;
+    const float xs = f16_scale(__ldg(f16max));
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = pair; t < ntiles; t += npairs) {
+      const int64_t m0 = (t / ntn) * (2 * TC_M) + TC_M * rank;
+      const int split = (m0 < Nx && m0 + TC_M > Nx) ? static_cast<int>(Nx - m0) : TC_M;   // y rows >= split
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&xfull[stage], phase);
+        unsigned char* sa = sm + stage * PR_STAGE;
+        float v[4][8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = PR_RPW * cw + 4 * q + rsub;
+          const int box = c >> 2, j0 = 2 * (c & 3);
+          const unsigned char* rb = sa + box * PR_A + r * 128;
+          if (r < split) {
+            const int jf = j0 + box, js = j0 + 1 - box;
+            const float4 f4 = *reinterpret_cast<const float4*>(rb + ((jf ^ (r & 7)) << 4));
+            const float4 s4 = *reinterpret_cast<const float4*>(rb + ((js ^ (r & 7)) << 4));
+            const float4 a4 = box ? s4 : f4, b4 = box ? f4 : s4;
+            v[q][0] = a4.x; v[q][1] = a4.y; v[q][2] = a4.z; v[q][3] = a4.w;
+            v[q][4] = b4.x; v[q][5] = b4.y; v[q][6] = b4.z; v[q][7] = b4.w;
+          } else {   // straddling tile: y rows from global memory
+            const int64_t i = m0 + r;
+            const int col = kb * 64 + 8 * c;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[q][u] = 0.f;
+            if (i < L) {
+              const float* rowp = py + (i - Nx) * static_cast<int64_t>(d);
+              if (col < d) {
+                const float4 a4 = __ldg(reinterpret_cast<const float4*>(rowp + col));
+                v[q][0] = a4.x; v[q][1] = a4.y; v[q][2] = a4.z; v[q][3] = a4.w;
+              }
+              if (col + 4 < d) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(rowp + col + 4));
+                v[q][4] = b4.x; v[q][5] = b4.y; v[q][6] = b4.z; v[q][7] = b4.w;
+              }
+            }
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = PR_RPW * cw + 4 * q + rsub;
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float a = v[q][2 * k] * xs, b = v[q][2 * k + 1] * xs;
+            const __half2 h = __floats2half2_rn(a, b);
+            const float2 hf = __half22float2(h);
+            const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+            hi[k] = *reinterpret_cast<const uint32_t*>(&h);
+            lo[k] = *reinterpret_cast<const uint32_t*>(&l);
+          }
+          const int off = r * 128 + ((c ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(sa + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(sa + PR_A + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ready[stage]);
+        if (++stage == PR_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + PR_NEPI) {
+    // ---- epilogue (as k_proj_tc): warp w, TMEM lane quadrant q = w % 4 of this CTA's 128 points, all 256 slices
+    const int q = warp & 3;
+    const uint32_t rtempty = mapa_rank(&tempty[0], 0);
+    float trap = 0.f;
+    int it = 0;
+    for (int64_t t = pair; t < ntiles; t += npairs, ++it) {
+      const int b = it & 1;
+      const uint32_t tph = (it >> 1) & 1;
+      const int64_t m0 = (t / ntn) * (2 * TC_M) + TC_M * rank;
+      const int n0 = static_cast<int>(t % ntn) * PR_BN;
+      const int64_t w0 = m0 + 32 * q;
+      const int64_t i = w0 + lane;
+      const bool valid = i < L, isx = i < Nx;
+      const bool warp_any_x = (w0 < Nx), mixed = warp_any_x && (w0 + 32 > Nx), warp_full = (w0 + 32 <= L);
+      const int ncols = min(PR_BN, np - n0);
+      mbar_wait(&tfull[b], tph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tbase = tmem_base + static_cast<uint32_t>(b * PR_BN) + (static_cast<uint32_t>(32 * q) << 16);
+      uint32_t v[16];
+      if (ncols > 0)
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(tbase));
+      float* zrow = Z + static_cast<int64_t>(n0) * ldz + i;
+#pragma unroll 1
+      for (int c0 = 0; c0 < ncols; c0 += 16) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t cur[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cur[j] = v[j];
+        if (c0 + 16 < ncols)
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+              "%14, %15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(tbase + static_cast<uint32_t>(c0 + 16)));
+        const int nc = min(16, ncols - c0);
+        const float4* sv = reinterpret_cast<const float4*>(sinv + n0 + c0);
+        float sc[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 f = sv[k];
+          sc[4 * k] = f.x; sc[4 * k + 1] = f.y; sc[4 * k + 2] = f.z; sc[4 * k + 3] = f.w;
+        }
+        float fmn[16], fmx[16];
+        float* zp = zrow + static_cast<int64_t>(c0) * ldz;
+        if (warp_full && nc == 16) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float z = __uint_as_float(cur[j]) * sc[j];
+            *zp = z;
+            zp += ldz;
+            trap = fmaf(z, 0.f, trap);
+            fmn[j] = z;
+            fmx[j] = z;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float z = __uint_as_float(cur[j]) * sc[j];
+            const bool ok = valid && j < nc;
+            if (ok) {
+              *zp = z;
+              trap = fmaf(z, 0.f, trap);
+            }
+            zp += ldz;
+            fmn[j] = ok ? z : CUDART_INF_F;
+            fmx[j] = ok ? z : -CUDART_INF_F;
+          }
+        }
+        float amn, amx;
+        colrange16r(fmn, fmx, lane, &amn, &amx);
+        float xmn = amn, xmx = amx;
+        if (mixed) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float z = __uint_as_float(cur[j]) * sc[j];
+            const bool ok = valid && isx && j < nc;
+            fmn[j] = ok ? z : CUDART_INF_F;
+            fmx[j] = ok ? z : -CUDART_INF_F;
+          }
+          colrange16r(fmn, fmx, lane, &xmn, &xmx);
+        }
+        if (lane < nc) {
+          const int s = n0 + c0 + lane;
+          if (amn <= amx) { atomicMin(&rng[4 * s + 2], f2key_tc(amn)); atomicMax(&rng[4 * s + 3], f2key_tc(amx)); }
+          if (warp_any_x && xmn <= xmx) {
+            atomicMin(&rng[4 * s + 0], f2key_tc(xmn));
+            atomicMax(&rng[4 * s + 1], f2key_tc(xmx));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) {   // release the accumulator to the leader's MMA of tile t + 2 (both CTAs' epilogues)
+        if (leader) mbar_arrive(&tempty[b]);
+        else mbar_arrive_remote(rtempty + 8u * static_cast<uint32_t>(b));
+      }
+    }
+    if (__any_sync(0xffffffffu, trap != 0.f) && lane == 0) atomicOr(flag, 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();   // the peer's remote arrives and both CTAs' TMEM reads are done before the pair deallocates
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int ne = 4 * np, e0 = static_cast<int>((static_cast<int64_t>(blockIdx.x) * 4 * 61) % ne);
+  for (int k = threadIdx.x; k < ne; k += blockDim.x) {
+    const int e = (e0 + k) % ne;
+    const unsigned v = rng[e];
+    if ((e & 1) == 0) {
+      if (v != 0xffffffffu) atomicMin(mm + e, v);
+    } else if (v != 0u) {
+      atomicMax(mm + e, v);
+    }
+  }
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * PR_BN));
+}
+
 // fp32 -> three bf16 pieces, K-concatenated:  Xs[i][j] = hi, Xs[i][dp+j] = mid, Xs[i][2dp+j] = lo.
 // One thread per 8 consecutive coordinates of a row: vector loads when the row is 16-byte aligned,
 // three 16-byte stores (dp is a multiple of 64, so every 8-group is aligned in Xs).
@@ -760,7 +1127,18 @@ cudaError_t launch_project_f16(const float* x, int64_t N, const float* y, int64_
     unsigned* mmc = mm + 4 * s0;
     const float* ic = inv_norm + s0;
     cudaError_t e;
-    if (BN == 256) e = launch_tc<256, 3, 3>(tb, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, &tx, &ty, f16max);
+    if (BN == 256 && L >= 2 * TC_M) {   // CTA pairs (cta_group::2): half the direction bytes per SM
+      CUtensorMap th;
+      if (!make_map(&th, g, static_cast<uint64_t>(ns), static_cast<uint64_t>(dp), 128u)) return cudaErrorInvalidValue;
+      const int ntn = (ns + PR_BN - 1) / PR_BN;
+      const size_t smem = PR_FIXED + static_cast<size_t>(20) * ntn * PR_BN;
+      set_smem_attr_once(reinterpret_cast<const void*>(k_proj_pair), 227 * 1024);
+      const int64_t ntiles = ((L + 2 * TC_M - 1) / (2 * TC_M)) * ntn;
+      const int pairs = static_cast<int>(ntiles < kProjMaxCtas / 2 ? ntiles : kProjMaxCtas / 2);
+      k_proj_pair<<<2 * pairs, TC_THREADS_TF32, smem, st>>>(th, tx, ty, nk, L, N, ns, ic, Zc, ldz, mmc, flag, y, d,
+                                                            f16max);
+      e = cudaGetLastError();
+    } else if (BN == 256) e = launch_tc<256, 3, 3>(tb, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, &tx, &ty, f16max);
     else if (BN == 128) e = launch_tc<128, 4, 3>(tb, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, &tx, &ty, f16max);
     else e = launch_tc<64, 4, 3>(tb, tb, nk, L, N, ns, ic, Zc, ldz, mmc, flag, nullptr, st, x, y, d, &tx, &ty, f16max);
     if (e != cudaSuccess) return e;

@@ -63,7 +63,10 @@ def rel_err(got, ref, w):
 
 
 # ---------------------------------------------------------------- a1: projection
-@pytest.mark.parametrize("n,d,P", [(1, 3, 1), (300, 3, 64), (1000, 50, 70), (257, 784, 33), (129, 3072, 17)])
+@pytest.mark.parametrize("n,d,P", [(1, 3, 1), (300, 3, 64), (1000, 50, 70), (257, 784, 33), (129, 3072, 17),
+                                   # > 128 slices at d >= 256: FP16x2 on CTA pairs (k_proj_pair), ragged slice and
+                                   # point tiles, a pair tile whose second CTA holds no points
+                                   (3001, 784, 300), (1000, 3072, 257), (300, 256, 512)])
 def test_projection_parity(n, d, P):
     rng = np.random.default_rng(n + d)
     pts = rng.uniform(-1, 1, (n, d)).astype(np.float32)
