@@ -591,32 +591,6 @@ constexpr int PR_RANGE_OFF = (PR_BAR_OFF + 8 * (5 * PR_STAGES + 4) + 16 + 63) / 
 constexpr int PR_FIXED = PR_RANGE_OFF + 1024;
 constexpr int PR_NEPI = 4, PR_CW0 = 8, PR_NCONV = 8, PR_RPW = TC_M / PR_NCONV;
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_TF32, 1)
     k_proj_pair(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ CUtensorMap tmY, int nk, int64_t L, int64_t Nx, int np,
