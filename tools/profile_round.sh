@@ -25,9 +25,9 @@ if [ "${FULL:-1}" = "1" ]; then
   # full captures (tools/run_cfg.py: one call on the full problem)
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_proj_spread|k_proj_eval|k_prep_f16" \
     -c 4 -o $out/${tag}_cfg5_full python tools/run_cfg.py cfg5 0 0 0 1 > /dev/null 2>&1
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_proj_tc|k_sp_owner|k_sp_part" -c 4 \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_proj_pair|k_proj_tc|k_sp_owner|k_sp_part" -c 4 \
     -o $out/${tag}_cfg4_full python tools/run_cfg.py cfg4 0 0 0 1 > /dev/null 2>&1
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_proj_tc|k_spread|k_eval" -c 3 \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_proj_pair|k_proj_tc|k_spread|k_eval" -c 3 \
     -o $out/${tag}_cfg3_full python tools/run_cfg.py cfg3 0 0 0 1 > /dev/null 2>&1
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_sp_(owner|part|hist|gather)" -c 8 \
     -o $out/${tag}_cfg2_full python tools/run_cfg.py cfg2 0 0 0 1 > /dev/null 2>&1
