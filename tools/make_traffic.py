@@ -8,7 +8,7 @@ import csv
 import json
 import sys
 
-SLOTS = [("k_split3", "split3"), ("k_proj_tc", "project"), ("k_minmax", "minmax"), ("k_prep_f16", "minmax"),
+SLOTS = [("k_split3", "split3"), ("k_proj_tc", "project"), ("k_proj_pair", "project"), ("k_minmax", "minmax"), ("k_prep_f16", "minmax"),
          ("k_sample_mean", "minmax"), ("k_bound_ranges", "minmax"),
          ("k_sp_hist", "sp_hist"), ("k_sp_part", "sp_part"), ("k_sp_owner", "sp_owner"), ("k_sp_gather", "sp_gather"),
          ("k_plan", "plan"), ("k_proj_spread", "spread"), ("k_spread", "spread"), ("k_fft_filter", "fft_filter"),
