@@ -136,6 +136,35 @@ def alu_peak(pk):
                 "148 SMs x 128 FP32 lanes x 2 flop/FMA x sm_max_mhz (B200_PROFILING unit counts)")
 
 
+# the kernels of a bench slot as they appear in the committed ncu summaries (tools/ncu_summary.py)
+NCU_KERNELS = {"spread": ("k_proj_spread", "k_spread"), "eval": ("k_proj_eval", "k_eval"),
+               "project": ("k_proj_pair", "k_proj_tc"), "minmax": ("k_prep_f16",)}
+
+
+def ncu_context(cfg_name, slot):
+    """Context for the roofline record, not a measurement of this run: the pipe utilisations of the slot's kernel
+    in the committed ncu --set full summary of this configuration (profiles/r02/ncu_<cfg>*.csv), where one exists
+    -- the shared-memory data pipe (LSU + tensor-core operand wavefronts), tensor pipe, issue slots."""
+    import csv
+    import glob
+    names = NCU_KERNELS.get(slot, ())
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r02", f"ncu_{cfg_name}*.csv"))):
+        try:
+            rows = list(csv.DictReader(open(path)))
+        except OSError:
+            continue
+        for n in names:
+            for r in rows:
+                if n in r.get("kernel", ""):
+                    f = lambda k: float(r[k]) if r.get(k) not in (None, "") else None
+                    lsu, tc = f("smem_lsu_wavefronts_pct"), f("smem_tc_wavefronts_pct")
+                    return {"source": os.path.relpath(path, ROOT), "kernel": r["kernel"],
+                            "smem_pipe_pct": (lsu or 0.0) + (tc or 0.0) if lsu is not None else None,
+                            "tensor_pipe_active_pct": f("tensor_pipe_active_pct"),
+                            "issue_active_pct": f("issue_active_pct"), "fma_pipe_pct": f("fma_pipe_pct")}
+    return None
+
+
 def roofline(slot, cfg, P, plan, ms_per_launch, pk, traffic):
     """achieved / peak of one kernel, Sec. 8(d) units: the bound is the larger of the HBM time of its Sec. 8(d)
     bytes and the time of its algorithmic arithmetic at peak (tensor for the projection, FP32 FMA for the
@@ -446,6 +475,7 @@ def main():
     roof = roofline(dom, cfg, P_launch, plan, kernels[dom]["ms_per_step"] / lps, pk,
                     traffic_all[dom] / lps if isinstance(traffic_all.get(dom), (int, float)) else None)
     roof["share_of_step"] = kernels[dom]["ms_per_step"] / ms
+    roof["ncu"] = ncu_context(cfg.name, dom)
 
     cpu = None
     if not args.no_cpu_baseline and G == 1:
