@@ -80,3 +80,17 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference" and line["value"] > 0 and line["config"]["workload"] == "cfg1"
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_alu_peak_is_the_measured_fma_throughput():
+    # bench's ALU roofline peak: the committed B200 measurement (tools/fp32_peak.cu), within 5% of the unit-count
+    # figure 148 SMs x 128 lanes x 2 flop x 1965 MHz = 74.4 TF/s
+    peak, src = bench.alu_peak(PK)
+    assert "fp32_peak" in src and abs(peak - 74.45) / 74.45 < 0.05
+
+
+def test_ncu_context_reads_the_committed_summaries():
+    ctx = bench.ncu_context("cfg5", "spread")
+    assert ctx is not None and "k_proj_spread" in ctx["kernel"]
+    assert 0.0 < ctx["smem_pipe_pct"] <= 100.0 and 0.0 <= ctx["issue_active_pct"] <= 100.0
+    assert bench.ncu_context("cfg5", "no_such_slot") is None
