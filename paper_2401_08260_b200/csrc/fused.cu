@@ -526,7 +526,9 @@ constexpr int FE_OFF_STAGE = FS_KBMAX * FE_B;             // 32 KB of resident d
 constexpr int FE_OFF_Q = FE_OFF_STAGE + FE_STAGES * 2 * FE_PIECE;    // coefficients 0-1 | 2-3 (two planes)
 constexpr int FE_OFF_Q1 = FE_OFF_Q + FE_S * FE_QCAP * 16;            // coefficients 4-5
 constexpr int FE_OFF_SP = FE_OFF_Q1 + FE_S * FE_QCAP * 8;            // per-slice constants float4 [FE_S]
-constexpr int FE_OFF_RED = FE_OFF_SP + FE_S * 16;                    // partial sums [2][FE_H][FE_T] fp32
+constexpr int FE_OFF_SPQ = FE_OFF_SP + FE_S * 16;                    // (ga, gb) per slice float2 [FE_S]
+constexpr int FE_OFF_SPK = FE_OFF_SPQ + FE_S * 8;                    // 0x4B400000 - 1 + lminA per slice int [FE_S]
+constexpr int FE_OFF_RED = FE_OFF_SPK + FE_S * 4;                    // partial sums [2][FE_H][FE_T] fp32
 constexpr int FE_OFF_BAR = FE_OFF_RED + 2 * FE_H * FE_T * 4;
 constexpr int FE_SMEM = FE_OFF_BAR + 256 + 1024;
 static_assert(FE_SMEM <= 227 * 1024, "k_proj_eval shared memory");
@@ -553,6 +555,10 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
   float2* sq1 = reinterpret_cast<float2*>(sm + FE_OFF_Q1); // [FE_S][FE_QCAP]: coefficients 4-5 (6, 7: economised)
   float4* sp = reinterpret_cast<float4*>(sm + FE_OFF_SP);  // (ga, gb, -, -) per slice; .z = int bits of lminA, .w = WQ
   float* red = reinterpret_cast<float*>(sm + FE_OFF_RED);  // [2][FE_H][FE_T]
+  // the staged-table path reads the slice constants of 4 slices with two 16-byte and one 16-byte broadcast
+  // (3 wavefronts) instead of four (one per slice)
+  float2* spq = reinterpret_cast<float2*>(sm + FE_OFF_SPQ);
+  int* spk = reinterpret_cast<int*>(sm + FE_OFF_SPK);
   uint64_t* bfull = reinterpret_cast<uint64_t*>(sm + FE_OFF_BAR);
   uint64_t* xfull = bfull + 1;
   uint64_t* empty = xfull + FE_STAGES;
@@ -577,6 +583,8 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
       c = make_float4(inv_norm[p] * taun, -fmaf(f.cen, taun, 0.5f * w), __int_as_float(f.lminA), __int_as_float(f.WA));
     }
     sp[ls] = c;
+    spq[ls] = make_float2(c.x, c.y);
+    spk[ls] = 0x4B400000 - 1 + __float_as_int(c.z);   // cell of a = (bits of floor(a) + 1.5 2^23) - spk
   }
   // (two planes: the lanes of a warp read one slice's table at ~16 distinct cells; 16- and 8-byte cell strides)
   for (int e = threadIdx.x; e < FE_S * FE_QCAP; e += FE_THREADS) {
@@ -711,17 +719,22 @@ __global__ void __launch_bounds__(FE_THREADS, 1)
             float fr[4];
             float4 c0[4];
             float2 c1[4];
+            const int lq = FE_SPW * h + hf + j0;   // (a multiple of 4)
+            const float4 g01 = reinterpret_cast<const float4*>(spq)[lq / 2];       // broadcasts
+            const float4 g23 = reinterpret_cast<const float4*>(spq)[lq / 2 + 1];
+            const int4 kq = reinterpret_cast<const int4*>(spk)[lq / 4];
+            const float gav[4] = {g01.x, g01.z, g23.x, g23.z}, gbv[4] = {g01.y, g01.w, g23.y, g23.w};
+            const int kv[4] = {kq.x, kq.y, kq.z, kq.w};
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-              const int ls = FE_SPW * h + hf + j0 + jj;
-              const float4 c = sp[ls];   // broadcast
-              const float a = fmaf(__uint_as_float(v[j0 + jj]), c.x * rt, c.y), fl = floorf(a);
+              const int ls = lq + jj;
+              const float a = fmaf(__uint_as_float(v[j0 + jj]), gav[jj] * rt, gbv[jj]), fl = floorf(a);
               fr[jj] = a - fl;
               // (fl is an integer of magnitude < 2^22: its int value from the 1.5 2^23 shift, no F2I)
-              int cl = (__float_as_int(fl + 12582912.f) - 0x4B400000) + 1 - __float_as_int(c.z);
-              const int wq = __float_as_int(c.w);
-              SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < wq));
-              cl = cl < 0 ? 0 : (cl >= wq ? wq - 1 : cl);   // (memory safety only)
+              int cl = __float_as_int(fl + 12582912.f) - kv[jj];
+              SKS_CHECK(t * FE_T + 32 * q + lane >= M || s0 + ls >= np || (cl >= 0 && cl < __float_as_int(sp[ls].w)));
+              // (memory safety only: every staged table is zero beyond its WA <= FE_QCAP cells)
+              cl = cl < 0 ? 0 : (cl >= FE_QCAP ? FE_QCAP - 1 : cl);
               const float2 qa = sqa[ls * FE_QCAP + qswz2(cl)], qb = sqb[ls * FE_QCAP + qswz2(cl)];
               c0[jj] = make_float4(qa.x, qa.y, qb.x, qb.y);
               c1[jj] = sq1[ls * FE_QCAP + qswz2(cl)];
