@@ -533,11 +533,9 @@ constexpr int FE_OFF_BAR = FE_OFF_RED + 2 * FE_H * FE_T * 4;
 constexpr int FE_SMEM = FE_OFF_BAR + 256 + 1024;
 static_assert(FE_SMEM <= 227 * 1024, "k_proj_eval shared memory");
 
-// position of cell c in a slice's staged table: 16-byte entries, cells 8a + b stored at 8a + (b ^ (a & 7)), so that
-// the cells of a contiguous range fall into different 4-bank groups (a plain layout puts c and c + 8 in the same one)
-__device__ __forceinline__ int qswz(int c) { return c ^ ((c >> 3) & 7); }
-// 8-byte entries (the planes of coefficient pairs): plain layout -- ncu counts the ideal 2 wavefronts per warp
-// lookup without a swizzle (measured: the swizzle c ^ ((c >> 4) & 15) only cost its instructions)
+// position of cell c in a slice's staged table.  8-byte entries (the planes of coefficient pairs): plain layout --
+// ncu counts the ideal 2 wavefronts per warp lookup without a swizzle (measured: the swizzle c ^ ((c >> 4) & 15)
+// only cost its instructions)
 __device__ __forceinline__ int qswz2(int c) { return c; }
 
 __global__ void __launch_bounds__(FE_THREADS, 1)
