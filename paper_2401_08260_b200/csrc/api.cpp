@@ -207,7 +207,7 @@ SideStream* side_stream(int dev) {
 // workspace the layout then also holds).
 constexpr int64_t kFusedMinN = 1 << 18;
 bool fused_shape(int64_t N, int d, Path pt, bool with_Z, int w) {
-  return with_Z && pt.fourier && !pt.sort && N >= kFusedMinN && d <= 128 && d % 4 == 0 && (w % 2) == 0 && w >= 4;
+  return with_Z && pt.fourier && !pt.sort && N >= kFusedMinN && d <= 128 && d % 4 == 0 && w >= 4 && w != 9 && w != 11;
 }
 
 // fp32 -> IEEE binary16, round to nearest even (host; |v| < 65504 here)
@@ -685,7 +685,7 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
                                         reinterpret_cast<float*>(ws + L.Q), pr.k.kind == SKS_LAPLACIAN ? 4096 : 2048,
                                         fused, flag16, fst));
       }
-      launches += nbat <= 148 ? 2 : 3;
+      launches += (nbat <= 148 ? 2 : 3) + (fused ? 1 : 0);   // (fused spread: two variants, one per footprint class)
       if (side) {   // join: the interpolation (on st, after the sort stage) waits for the Fourier part
         SKS_CUDA(cudaEventRecord(side->join, fst));
         SKS_CUDA(cudaStreamWaitEvent(st, side->join, 0));

@@ -226,7 +226,12 @@ constexpr int FS_OFF_BAR = FS_OFF_W + 2 * FS_P * 4;
 constexpr int FS_SMEM = FS_OFF_BAR + 512 + 1024;          // + barriers, TMEM slot, window coefficients, alignment
 static_assert(FS_SMEM <= 227 * 1024, "k_proj_spread shared memory");
 
-template <int WT>
+// NC private copies of WCAP = 256 / NC cells per slice: 8 x 32 (a copy per point group and point parity), or 4 x 64
+// (a copy per point group) for wider footprints.  The footprints are known on the device only (the planner's
+// FPar.W), so both variants are launched and each slice tile is taken by exactly one of them: the 8-copy kernel
+// when every slice of the tile fits 32 cells, the 4-copy kernel otherwise (slices beyond 64 cells fall back to
+// global atomics there); the other kernel's CTAs of that tile exit at once
+template <int WT, int NC>
 __global__ void __launch_bounds__(FS_THREADS, 1)
     k_proj_spread(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXlo, int nk, int klast, int64_t N,
@@ -235,11 +240,19 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
                   float* __restrict__ grid,
                   const unsigned* __restrict__ flag16) {
   if (call_failed(flag16)) return;
+  {
+    const int ps = (blockIdx.x % ((np + FS_S - 1) / FS_S)) * FS_S + static_cast<int>(threadIdx.x);
+    const int beyond = __syncthreads_or(threadIdx.x < FS_S && ps < np && fp[ps].W > FS_WCAP);
+    if ((beyond != 0) != (NC != FS_NCOL)) return;   // (block-uniform) the other variant's tile
+  }
   extern __shared__ unsigned char fsraw[];
   // aligned by pointer arithmetic on the __shared__ array: the compiler keeps the shared state space (LDS / STS,
   // not generic LD / ST)
   unsigned char* sm = fsraw + ((1024u - (smem_u32(fsraw) & 1023u)) & 1023u);
-  float* priv = reinterpret_cast<float*>(sm + FS_OFF_GRID);   // [FS_NCOL][FS_WCAP][FS_S]
+  constexpr int WCAP = FS_NCOL * FS_WCAP / NC;   // private cells per slice and copy
+  constexpr int WH = (WT + 1) / 2;               // mirror pairs (+ the middle tap of an odd window)
+  static_assert(NC == FS_NCOL || NC == FS_EPI / 4, "one copy per point group, or per point group and parity");
+  float* priv = reinterpret_cast<float*>(sm + FS_OFF_GRID);   // [NC][WCAP][FS_S]
   uint64_t* afull = reinterpret_cast<uint64_t*>(sm + FS_OFF_BAR);
   uint64_t* xfull = afull + 1;                 // [FS_STAGES] raw tile (hi) and lo piece landed
   uint64_t* empty = xfull + FS_STAGES;         // [FS_STAGES] consumed by the MMAs
@@ -365,20 +378,22 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     const float taun = f.tau * static_cast<float>(n);
     const float ga = inv * taun, gb = -fmaf(f.cen, taun, 0.5f * pw.w);
     const int W = f.W;
-    const bool wide = W > FS_WCAP;   // (footprint beyond the private column: global atomics for this slice)
-    // two private copies of the slice's column per warp, for the even and the odd points of a pair: the pair's
-    // read-modify-writes cannot alias, so both points' loads are issued before either's stores
-    float* col = priv + (2 * h * FS_WCAP) * FS_S + 32 * q + lane;   // cell c at col[c * FS_S] (even points)
-    float* colo = col + FS_WCAP * FS_S;                             // (odd points)
+    const bool wide = W > WCAP;   // (footprint beyond the private column: global atomics for this slice)
+    // NC = 8: two private copies of the slice's column per warp, for the even and the odd points of a pair: the
+    // pair's read-modify-writes cannot alias, so both points' loads are issued before either's stores.  NC = 4: one
+    // copy per warp, the two points' read-modify-writes in order
+    constexpr int CPW = NC / (FS_EPI / 4);                           // copies per warp
+    float* col = priv + (CPW * h * WCAP) * FS_S + 32 * q + lane;     // cell c at col[c * FS_S] (even points)
+    float* colo = col + (CPW - 1) * WCAP * FS_S;                     // (odd points)
     float* gp = grid + static_cast<int64_t>(live ? p : 0) * ncap;
     // window coefficients through shared memory into registers (read from the parameter bank, ptxas would
     // re-load them inside the loop)
-    float* eos = reinterpret_cast<float*>(sm + FS_OFF_BAR + 256);   // [WT / 2][8]
-    if (warp == 0 && lane < WT / 2 * 8) eos[lane] = pw.eo[lane / 8][lane % 8];
+    float* eos = reinterpret_cast<float*>(sm + FS_OFF_BAR + 256);   // [WH][8]
+    if (threadIdx.x < WH * 8) eos[threadIdx.x] = pw.eo[threadIdx.x / 8][threadIdx.x % 8];   // (warps 0, 1: epilogue)
     asm volatile("bar.sync 1, %0;" ::"r"(FS_EPI * 32) : "memory");
-    float E[WT / 2][4], O[WT / 2][4];
+    float E[WH][4], O[WH][4];
 #pragma unroll
-    for (int j = 0; j < WT / 2; ++j)
+    for (int j = 0; j < WH; ++j)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         E[j][k] = eos[8 * j + k];
@@ -425,9 +440,9 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
             const int cl1 = min(max(static_cast<int>(fl.y) + 1 - f.lmin, 0), cmax);
             SKS_CHECK(w8[jj] == 0.f || cl0 == static_cast<int>(fl.x) + 1 - f.lmin);   // the bound holds: no clamping
             SKS_CHECK(w8[jj + 1] == 0.f || cl1 == static_cast<int>(fl.y) + 1 - f.lmin);
-            float2 tl[WT / 2], th[WT / 2];   // taps m and WT - 1 - m of both points
+            float2 tl[WH], th[WH];   // taps m and WT - 1 - m of both points (odd WT: tl[WT / 2] the middle tap)
 #pragma unroll
-            for (int m = 0; m < WT / 2; ++m) {
+            for (int m = 0; m < WH; ++m) {
               const float2 Em = __ffma2_rn(
                   __ffma2_rn(__ffma2_rn(make_float2(E[m][3], E[m][3]), u2, make_float2(E[m][2], E[m][2])), u2,
                              make_float2(E[m][1], E[m][1])),
@@ -442,17 +457,40 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
             float* c0p = col + cl0 * FS_S;    // even point: copy 0
             float* c1p = colo + cl1 * FS_S;   // odd point: copy 1
             float g0[WT], g1[WT];
+            if constexpr (CPW == 2) {
 #pragma unroll
-            for (int m = 0; m < WT; ++m) {   // all 2 WT loads first (disjoint copies: no ordering needed)
-              g0[m] = c0p[m * FS_S];
-              g1[m] = c1p[m * FS_S];
-            }
+              for (int m = 0; m < WT; ++m) {   // all 2 WT loads first (disjoint copies: no ordering needed)
+                g0[m] = c0p[m * FS_S];
+                g1[m] = c1p[m * FS_S];
+              }
 #pragma unroll
-            for (int m = 0; m < WT / 2; ++m) {
-              c0p[m * FS_S] = fmaf(w8[jj], tl[m].x, g0[m]);
-              c0p[(WT - 1 - m) * FS_S] = fmaf(w8[jj], th[m].x, g0[WT - 1 - m]);
-              c1p[m * FS_S] = fmaf(w8[jj + 1], tl[m].y, g1[m]);
-              c1p[(WT - 1 - m) * FS_S] = fmaf(w8[jj + 1], th[m].y, g1[WT - 1 - m]);
+              for (int m = 0; m < WT / 2; ++m) {
+                c0p[m * FS_S] = fmaf(w8[jj], tl[m].x, g0[m]);
+                c0p[(WT - 1 - m) * FS_S] = fmaf(w8[jj], th[m].x, g0[WT - 1 - m]);
+                c1p[m * FS_S] = fmaf(w8[jj + 1], tl[m].y, g1[m]);
+                c1p[(WT - 1 - m) * FS_S] = fmaf(w8[jj + 1], th[m].y, g1[WT - 1 - m]);
+              }
+              if constexpr (WT & 1) {
+                c0p[(WT / 2) * FS_S] = fmaf(w8[jj], tl[WT / 2].x, g0[WT / 2]);
+                c1p[(WT / 2) * FS_S] = fmaf(w8[jj + 1], tl[WT / 2].y, g1[WT / 2]);
+              }
+            } else {   // one copy: the even point's stores before the odd point's loads (their cells may coincide)
+#pragma unroll
+              for (int m = 0; m < WT; ++m) g0[m] = c0p[m * FS_S];
+#pragma unroll
+              for (int m = 0; m < WT / 2; ++m) {
+                c0p[m * FS_S] = fmaf(w8[jj], tl[m].x, g0[m]);
+                c0p[(WT - 1 - m) * FS_S] = fmaf(w8[jj], th[m].x, g0[WT - 1 - m]);
+              }
+              if constexpr (WT & 1) c0p[(WT / 2) * FS_S] = fmaf(w8[jj], tl[WT / 2].x, g0[WT / 2]);
+#pragma unroll
+              for (int m = 0; m < WT; ++m) g1[m] = c1p[m * FS_S];
+#pragma unroll
+              for (int m = 0; m < WT / 2; ++m) {
+                c1p[m * FS_S] = fmaf(w8[jj + 1], tl[m].y, g1[m]);
+                c1p[(WT - 1 - m) * FS_S] = fmaf(w8[jj + 1], th[m].y, g1[WT - 1 - m]);
+              }
+              if constexpr (WT & 1) c1p[(WT / 2) * FS_S] = fmaf(w8[jj + 1], tl[WT / 2].y, g1[WT / 2]);
             }
           }
         } else if (live) {   // footprint wider than the private column: global atomics for this slice
@@ -468,6 +506,12 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
               atomicAdd(&gp[(f.lmin + cl + m) & (n - 1)], wi * fmaf(u, Om, Em));
               atomicAdd(&gp[(f.lmin + cl + WT - 1 - m) & (n - 1)], wi * fmaf(-u, Om, Em));
             }
+            if (WT & 1) {
+              constexpr int m = WT / 2;
+              const float Em = fmaf(fmaf(fmaf(E[m][3], u2, E[m][2]), u2, E[m][1]), u2, E[m][0]);
+              const float Om = fmaf(fmaf(fmaf(O[m][3], u2, O[m][2]), u2, O[m][1]), u2, O[m][0]);
+              atomicAdd(&gp[(f.lmin + cl + m) & (n - 1)], wi * fmaf(u, Om, Em));
+            }
           }
         }
       }
@@ -480,18 +524,18 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp < 4) {   // flush: the FS_NCOL private columns of each slice, one atomic per cell
+  if (warp < 4) {   // flush: the NC private columns of each slice, one atomic per cell
     const int q = warp & 3, p = s0 + 32 * q + lane;
     if (p < np) {
       const FPar f = fp[p];
       const int n = 1 << f.logn;
-      if (f.W <= FS_WCAP) {
+      if (f.W <= WCAP) {
         float* gp = grid + static_cast<int64_t>(p) * ncap;
         const float* c0 = priv + 32 * q + lane;
         for (int c = 0; c < f.W; ++c) {
           float s = 0.f;
 #pragma unroll
-          for (int g = 0; g < FS_NCOL; ++g) s += c0[(g * FS_WCAP + c) * FS_S];
+          for (int g = 0; g < NC; ++g) s += c0[(g * WCAP + c) * FS_S];
           if (s != 0.f) atomicAdd(&gp[(f.lmin + c) & (n - 1)], s);
         }
       }
@@ -870,13 +914,17 @@ cudaError_t launch_proj_spread(const uint16_t* xh, const uint16_t* xl, const flo
     kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, tmXlo, nk, klast, N, np, ranges, rsx, inv_norm,
                                                          wpad, fp, pw, ncap, grid, flag16);
   };
+  // both variants (see k_proj_spread): each slice tile runs in the one its footprints select
+  constexpr int NA = FS_NCOL, NB = FS_EPI / 4;
   switch (pw.w) {
-    case 4: go(k_proj_spread<4>); break;
-    case 6: go(k_proj_spread<6>); break;
-    case 8: go(k_proj_spread<8>); break;
-    case 10: go(k_proj_spread<10>); break;
-    case 12: go(k_proj_spread<12>); break;
-    default: return cudaErrorInvalidValue;   // (odd widths: the unfused path)
+    case 4: go(k_proj_spread<4, NA>); go(k_proj_spread<4, NB>); break;
+    case 5: go(k_proj_spread<5, NA>); go(k_proj_spread<5, NB>); break;
+    case 6: go(k_proj_spread<6, NA>); go(k_proj_spread<6, NB>); break;
+    case 7: go(k_proj_spread<7, NA>); go(k_proj_spread<7, NB>); break;
+    case 8: go(k_proj_spread<8, NA>); go(k_proj_spread<8, NB>); break;
+    case 10: go(k_proj_spread<10, NA>); go(k_proj_spread<10, NB>); break;
+    case 12: go(k_proj_spread<12, NA>); go(k_proj_spread<12, NB>); break;
+    default: return cudaErrorInvalidValue;   // (widths 9, 11: the unfused path)
   }
   return cudaGetLastError();
 }

@@ -498,6 +498,32 @@ def test_fused_projection_spread(kind, scale, d, N, M, P):
     assert err <= TOL[kind], err
 
 
+_WINDOW_CASE = {}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("w,os_,tol", [(5, 2, 1e-6), (5, 4, 1e-6), (4, 4, 1e-5), (7, 2, 1e-6), (10, 2, 1e-6),
+                                        (6, 4, 1e-6), (4, 2, 1e-5)])
+def test_fused_window_variants(w, os_, tol):
+    # the fused spread's window variants: odd widths (a middle tap beside the mirror pairs), footprints beyond 32
+    # cells (w = 7, 10 and oversampling 4: the kernel variant with 4 private copies of 64 cells instead of 8 of 32
+    # takes the tile), more than 4 mirror pairs (coefficients staged by 2 warps).  Bounds: 10x the measured errors
+    cfg = I.Config("fused", "gaussian", 100, 300_001, 2000, 40, 35, 135, "mixture10", "pm1", param=30.0)
+    if "case" not in _WINDOW_CASE:   # (one oracle run serves all variants)
+        x, y, wt = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
+        tgt = I.target_subset(cfg.M, 32)
+        _WINDOW_CASE["case"] = (x, y, wt, tgt, O.sliced_sum("gaussian", 30.0, x, y, wt, cfg.P, cfg.dir_seed,
+                                                            targets=tgt))
+    x, y, wt, tgt, ref = _WINDOW_CASE["case"]
+    s = S.sks_sum(dev(x), dev(y), dev(wt), "gaussian", 30.0, cfg.P, cfg.dir_seed, window_w=w,
+                  oversample=os_).cpu().numpy()
+    info = S.sks_last_plan()
+    assert info["fused"] == 1 and info["window_w"] == w, info
+    err = rel_err(s[tgt], ref, wt)
+    print(f"fused window w={w} os={os_}: max|ds|/sum|w| = {err:.3e}  plan={info}")
+    assert err <= tol, err
+
+
 @pytest.mark.gpu
 def test_fused_mixed_row_magnitudes():
     # the fused kernels' FP16x2 operands carry one power-of-two scale per 8-row group (fused.cu k_prep_f16): rows
