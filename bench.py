@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--mode", default="async", choices=["sync", "async", "graph"],
                     help="sks_options for the device-resident step: sync (status read per call), async (no host "
                          "synchronisation; status read after the timed region), graph (async + CUDA-graph replay)")
+    ap.add_argument("--shard", default="auto", choices=["auto", "slices", "points"],
+                    help="N > 1: slice ranges + one all-reduce of the sums, or point rows + the in-call exchanges of "
+                         "the large-N Fourier path (parallel.point_sharded_sum); auto = points where that path runs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
@@ -301,10 +304,20 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(cfg, param, G):
+def config_dict(cfg, param, G, points=False):
     return {"workload": cfg.name, "kernel": cfg.kind, "kernel_param": param, "d": cfg.d, "N": cfg.N, "M": cfg.M,
-            "P": cfg.P, "slices_per_gpu": cfg.P // G, "parallelism": f"slices{G}",
+            "P": cfg.P, "slices_per_gpu": cfg.P if points else cfg.P // G,
+            "parallelism": f"points{G}" if points else f"slices{G}",
             "l2": "flushed before every step (256 MiB write, outside the timed events)"}
+
+
+def shard_by_points(shard, cfg, G):
+    """the point-sharded large-N Fourier path (include/sks.h sks_exchange_fn) applies: every rank's share of the
+    sources takes the fused path (api.cpp fused_shape)"""
+    ok = cfg.kind in ("gaussian", "matern") and cfg.N // G >= (1 << 18) and cfg.d <= 128 and cfg.d % 4 == 0
+    if shard == "points" and not ok:
+        raise SystemExit(f"--shard points: {cfg.name} on {G} GPUs does not take the fused large-N Fourier path")
+    return G > 1 and ok and shard != "slices"
 
 
 # ------------------------------------------------------------------ our arm
@@ -342,12 +355,26 @@ def main():
     x, y, w = I.points(cfg, "x"), I.points(cfg, "y"), I.weights(cfg)
     param = I.kernel_param(cfg)
     scale = param if cfg.kind != "negdist" else 1.0
-    from paper_2401_08260_b200.parallel import slice_range
-    p0, p1 = slice_range(rank, G, cfg.P)
+    from paper_2401_08260_b200.parallel import make_exchange, point_range, slice_range
+    points = shard_by_points(args.shard, cfg, G)
+    if points and args.mode == "graph":
+        raise SystemExit("--mode graph cannot replay the point-sharded call's exchanges")
+    full = cfg
+    if points:   # this rank's rows of x, w and y, all slices
+        (n0, n1), (m0, m1) = point_range(rank, G, cfg.N), point_range(rank, G, cfg.M)
+        x, y, w = (np.ascontiguousarray(a) for a in (x[n0:n1], y[m0:m1], w[n0:n1]))
+        cfg = I.scaled(cfg, N=n1 - n0, M=m1 - m0)
+        p0, p1 = 0, cfg.P
+    else:
+        p0, p1 = slice_range(rank, G, cfg.P)
     xd, yd, wd = (torch.from_numpy(a).to(dev) for a in (x, y, w))
     ws = torch.empty(S.sks_workspace_size(cfg.N, cfg.M, cfg.d, cfg.kind, scale, cfg.P, p0, p1, cfg.matern_p),
                      dtype=torch.uint8, device=dev)
     s = torch.empty(cfg.M, dtype=torch.float32, device=dev)
+    if points:
+        xfn, xerr = make_exchange(ws)
+        counts = [point_range(r, G, full.M) for r in range(G)]
+        s_parts = [torch.empty(b - a, dtype=torch.float32, device=dev) for a, b in counts]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -355,9 +382,18 @@ def main():
 
     mode_kw = {"sync": {}, "async": {"async_": True}, "graph": {"graph": True}}[args.mode]
 
-    def step():   # this rank's slice range through the C-ABI, then the one all-reduce (SUM) of the partials
+    def step_slices(kw):   # this rank's slice range through the C-ABI, then the one all-reduce (SUM) of the partials
         distributed_sliced_sum(lambda a, b: S.sks_sum(xd, yd, wd, cfg.kind, scale, cfg.P, cfg.dir_seed, a, b,
-                                                      cfg.matern_p, out=s, workspace=ws, **mode_kw), cfg.P)
+                                                      cfg.matern_p, out=s, workspace=ws, **kw), cfg.P)
+
+    def step_points(kw):   # this rank's point rows, all slices (three small exchanges inside the call), then the
+        #                    all-gather that leaves the full result on every rank, as the slice mode does
+        S.sks_sum(xd, yd, wd, cfg.kind, scale, cfg.P, cfg.dir_seed, 0, cfg.P, cfg.matern_p, out=s, workspace=ws,
+                  exchange=xfn, **kw)
+        dist.all_gather(s_parts, s)
+
+    def step():
+        (step_points if points else step_slices)(mode_kw)
 
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
@@ -393,8 +429,7 @@ def main():
         torch.cuda.synchronize()
         for _ in range(args.steps):
             flush.zero_()
-            distributed_sliced_sum(lambda a, b: S.sks_sum(xd, yd, wd, cfg.kind, scale, cfg.P, cfg.dir_seed, a, b,
-                                                          cfg.matern_p, out=s, workspace=ws, async_=True), cfg.P)
+            step_slices({"async_": True})
         torch.cuda.synchronize()
         S.sks_sync_status(ws)
         kernels_from = "an async (non-graph) pass of the same steps right after the timed graph region"
@@ -405,7 +440,7 @@ def main():
     if G > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    value = (cfg.N + cfg.M) * cfg.P / (ms * 1e-3)
+    value = (full.N + full.M) * full.P / (ms * 1e-3)
 
     # ---- end to end through the public host-buffer API (H2D inputs + D2H result inside the timed region)
     e2e = None
@@ -415,10 +450,11 @@ def main():
         wsh = torch.empty(S.sks_workspace_size_host(cfg.N, cfg.M, cfg.d, cfg.kind, scale, cfg.P, p0, p1, cfg.matern_p),
                           dtype=torch.uint8, device=dev)
         del ws
+        xkw = {"exchange": make_exchange(wsh)[0]} if points else {}
         def e2e_step():
             S.sks_sum_host(xh.numpy(), yh.numpy(), wh.numpy(), cfg.kind, scale, cfg.P, cfg.dir_seed, p0, p1,
-                           cfg.matern_p, out=sh.numpy(), workspace=wsh)
-            if G > 1:
+                           cfg.matern_p, out=sh.numpy(), workspace=wsh, **xkw)
+            if G > 1 and not points:   # (points: every rank holds its own targets' sums)
                 sd = sh.to(dev, non_blocking=True)
                 dist.all_reduce(sd)
                 sh.copy_(sd)
@@ -440,9 +476,10 @@ def main():
         if G > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         me = float(te.item())
-        e2e = {"value": (cfg.N + cfg.M) * cfg.P / (me * 1e-3), "unit": UNIT, "ms_per_step": me,
+        e2e = {"value": (full.N + full.M) * full.P / (me * 1e-3), "unit": UNIT, "ms_per_step": me,
                "h2d_bytes_per_step": 4 * (cfg.N * cfg.d + cfg.M * cfg.d + cfg.N),
-               "d2h_bytes_per_step": 4 * cfg.M, "api": "sks_sum_host (pinned host buffers)"}
+               "d2h_bytes_per_step": 4 * cfg.M, "api": "sks_sum_host (pinned host buffers)",
+               "bytes": "per rank"}
 
     if rank != 0:
         if G > 1:
@@ -484,7 +521,7 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": config_dict(cfg, param, G), "roofline": roof, "cpu_baseline": cpu,
+            "data": "synthetic", "config": config_dict(full, param, G, points), "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": int(plan.get("launches", 0)) * args.steps, "clocks": clk,
             "mode": args.mode, "kernels_from": kernels_from, "kernels": kernels, "plan": plan}
     print(json.dumps(line), flush=True)

@@ -70,6 +70,23 @@ typedef struct {
   double scale;       /* sigma | unused | ell | beta  (must be > 0 unless NEGDIST)  */
 } sks_kernel;
 
+/* Point sharding across GPUs (one process per GPU) for the large-N Fourier path.  The 1D fast Fourier summation
+ * is linear in the sources up to the grids of Fourier data and pointwise in the targets after them, so
+ * ranks may split the POINTS instead of the slices: every rank calls sks_sum with its own rows of x, w and y and the
+ * full slice range, and the call invokes `exchange` (on the host, in enqueue order, for work on `stream`) where the
+ * ranks' data must meet:
+ *   SKS_XCHG_BCAST_F64  count doubles at dev_ptr: overwrite with rank 0's (the common centre mu of the range bound)
+ *   SKS_XCHG_MAX_I32    count int32 at dev_ptr: element-wise maximum over the ranks (the 8 norm words; bit patterns
+ *                       of non-negative floats, which order as integers)
+ *   SKS_XCHG_SUM_F32    count floats at dev_ptr: element-wise sum over the ranks (a slice batch's NFFT grids)
+ * dev_ptr points into the call's workspace.  The callback enqueues the collective after the work already enqueued on
+ * `stream` (e.g. ncclAllReduce on that stream, or torch.distributed on the current stream) and returns 0, non-zero
+ * on failure (the call then returns SKS_ERR_CUDA).  s receives the sums of the rank's own targets, equal to the
+ * unsharded call's up to fp32 summation order of the grids.  Only the fused large-N path takes part (otherwise
+ * SKS_ERR_UNSUPPORTED); not combinable with `graph` or `deterministic`. */
+typedef enum { SKS_XCHG_BCAST_F64 = 0, SKS_XCHG_MAX_I32 = 1, SKS_XCHG_SUM_F32 = 2 } sks_exchange_op;
+typedef int (*sks_exchange_fn)(void* user, int32_t op, void* dev_ptr, size_t count, void* stream);
+
 /* Optional tuning knobs.  Pass NULL for the defaults (given in brackets). */
 typedef struct {
   double eps;            /* [1e-6] absolute tail mass (f(0)-relative) of dropped Fourier coefficients and aliasing level
@@ -95,6 +112,8 @@ typedef struct {
                             of arguments (pointers, sizes, kernel, P, seed, range, options, stream) runs eagerly and
                             captures its launches; later identical calls launch the instantiated graph (one
                             cudaGraphLaunch): for launch-latency-bound problems (hard part 9)        */
+  sks_exchange_fn exchange; /* [NULL] point sharding: the collective callback described above                      */
+  void* exchange_user;      /* passed back to `exchange`                                                            */
 } sks_options;
 
 /* Diagnostic description of the last plan built on this thread (for reports and tests). */

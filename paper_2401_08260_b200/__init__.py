@@ -29,13 +29,14 @@ PROJECTIONS = {"auto": 0, "bf16x3": 1, "tf32x2": 2, "fp16x2": 3}
 
 
 def _opts(eps=0.0, window_w=0, oversample=0, slice_batch=0, engine="auto", projection="auto", async_=False,
-          graph=False, deterministic=False):
+          graph=False, deterministic=False, exchange=None):
     e = ENGINES[engine] if isinstance(engine, str) else int(engine)
     pj = PROJECTIONS[projection] if isinstance(projection, str) else int(projection)
-    if not (eps or window_w or oversample or slice_batch or e or pj or async_ or graph or deterministic):
+    if not (eps or window_w or oversample or slice_batch or e or pj or async_ or graph or deterministic
+            or exchange is not None):
         return None
     return options(eps, window_w, oversample, slice_batch, e, pj, int(bool(async_)), int(bool(graph)),
-                   int(bool(deterministic)))
+                   int(bool(deterministic)), exchange)
 
 
 def _stream_ptr(stream) -> Optional[int]:

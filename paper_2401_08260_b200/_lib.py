@@ -23,7 +23,14 @@ class sks_kernel(ctypes.Structure):
 class sks_options(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("window_w", ctypes.c_int32), ("oversample", ctypes.c_int32),
                 ("slice_batch", ctypes.c_int32), ("engine", ctypes.c_int32), ("projection", ctypes.c_int32),
-                ("async_", ctypes.c_int32), ("deterministic", ctypes.c_int32), ("graph", ctypes.c_int32)]
+                ("async_", ctypes.c_int32), ("deterministic", ctypes.c_int32), ("graph", ctypes.c_int32),
+                ("exchange", ctypes.c_void_p), ("exchange_user", ctypes.c_void_p)]
+
+
+# int (*sks_exchange_fn)(void* user, int32_t op, void* dev_ptr, size_t count, void* stream)   (include/sks.h)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
+                               ctypes.c_void_p)
+XCHG_BCAST_F64, XCHG_MAX_I32, XCHG_SUM_F32 = 0, 1, 2
 
 
 class sks_plan_info(ctypes.Structure):
@@ -95,6 +102,8 @@ def kernel(kind: str, scale: float = 1.0, matern_p: int = 1) -> sks_kernel:
 
 
 def options(eps: float = 0.0, window_w: int = 0, oversample: int = 0, slice_batch: int = 0, engine: int = 0,
-            projection: int = 0, async_: int = 0, graph: int = 0, deterministic: int = 0):
+            projection: int = 0, async_: int = 0, graph: int = 0, deterministic: int = 0, exchange=None):
+    """exchange: an EXCHANGE_FN instance (kept alive by the caller for the duration of the call) or None"""
+    fn = ctypes.cast(exchange, ctypes.c_void_p) if exchange is not None else None
     return ctypes.pointer(sks_options(float(eps), int(window_w), int(oversample), int(slice_batch), int(engine),
-                                      int(projection), int(async_), int(deterministic), int(graph)))
+                                      int(projection), int(async_), int(deterministic), int(graph), fn, None))

@@ -113,6 +113,8 @@ struct Opts {
   int async = 0;    // 1: enqueue only (status through sks_sync_status)
   int graph = 0;    // 1: replay a captured CUDA graph of the call (implies async)
   int det = 0;      // 1: bitwise run-to-run deterministic (no float atomics; fixed-order reductions)
+  sks_exchange_fn xchg = nullptr;   // point sharding: the ranks' collective callback (sks.h)
+  void* xuser = nullptr;
 };
 
 sks_status resolve_opts(const sks_options* o, Opts* r) {
@@ -133,6 +135,10 @@ sks_status resolve_opts(const sks_options* o, Opts* r) {
     d.graph = o->graph ? 1 : 0;
     d.async = (o->async || d.graph) ? 1 : 0;
     d.det = o->deterministic ? 1 : 0;
+    d.xchg = o->exchange;
+    d.xuser = o->exchange_user;
+    if (d.xchg && (d.graph || d.det))
+      return fail(SKS_ERR_INVALID, "exchange (point sharding) cannot be combined with graph or deterministic");
   }
   *r = d;
   return SKS_OK;
@@ -518,6 +524,14 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
   // choice or FP16x2 (the fused kernels compute FP16x2 with per-tile scales; d <= 128)
   const bool fused = fshape && (o.proj == 0 || o.proj == PM_FP16X2) && s_out && sks::fused_spread_ok(pr.d, x) &&
                      sks::fused_spread_ok(pr.d, y);
+  if (o.xchg && !fused)
+    return fail(SKS_ERR_UNSUPPORTED,
+                "exchange (point sharding): the fused large-N Fourier path only (Gaussian / Matern, local N >= 2^18, "
+                "d <= 128, d % 4 == 0, 16-byte aligned rows)");
+  auto exchange = [&](int op, void* ptr, size_t count, cudaStream_t s) -> sks_status {
+    if (o.xchg && o.xchg(o.xuser, op, ptr, count, s) != 0) return fail(SKS_ERR_CUDA, "exchange callback failed");
+    return SKS_OK;
+  };
   const bool tc = pr.with_Z && pm == PM_BF16X3;
   const bool tf = pr.with_Z && pm == PM_TF32X2;
   const bool th = pr.with_Z && pm == PM_FP16X2;
@@ -528,12 +542,16 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
   }
   if (fused) {   // direction-independent: the sources' centre and radius, the targets' radius, FP16x2 operands
     ProfScope ps(PS_MINMAX, st);
-    SKS_CUDA(sks::launch_source_prep(x, pr.N, y, pr.M, pr.d, reinterpret_cast<double*>(ws + L.bound),
-                                     reinterpret_cast<unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32),
-                                     reinterpret_cast<uint16_t*>(ws + L.xh), reinterpret_cast<uint16_t*>(ws + L.xl),
-                                     reinterpret_cast<float*>(ws + L.rsx), reinterpret_cast<uint16_t*>(ws + L.yh),
-                                     reinterpret_cast<uint16_t*>(ws + L.yl), reinterpret_cast<float*>(ws + L.rsy), w,
-                                     reinterpret_cast<float*>(ws + L.wpad), st));
+    double* mu = reinterpret_cast<double*>(ws + L.bound);
+    unsigned* nb = reinterpret_cast<unsigned*>(ws + L.bound + sks::source_bound_bytes(pr.d) - 32);
+    // (point sharding: every rank bounds its points about rank 0's centre, the bounds' maxima cover all points)
+    SKS_CUDA(sks::launch_source_mean(x, pr.N, pr.d, mu, nb, st));
+    if (exchange(SKS_XCHG_BCAST_F64, mu, static_cast<size_t>(pr.d), st) != SKS_OK) return SKS_ERR_CUDA;
+    SKS_CUDA(sks::launch_source_prep(x, pr.N, y, pr.M, pr.d, mu, nb, reinterpret_cast<uint16_t*>(ws + L.xh),
+                                     reinterpret_cast<uint16_t*>(ws + L.xl), reinterpret_cast<float*>(ws + L.rsx),
+                                     reinterpret_cast<uint16_t*>(ws + L.yh), reinterpret_cast<uint16_t*>(ws + L.yl),
+                                     reinterpret_cast<float*>(ws + L.rsy), w, reinterpret_cast<float*>(ws + L.wpad), st));
+    if (exchange(SKS_XCHG_MAX_I32, nb, 8, st) != SKS_OK) return SKS_ERR_CUDA;
     launches += 4;
   }
   for (int b0 = 0; b0 < pr.nslices; b0 += batch) {
@@ -673,6 +691,8 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
                                          static_cast<const uint16_t*>(dirs->g16) + static_cast<int64_t>(b0) * dirs->K3,
                                          dirs->K3, dirs->inv + b0, nbat, reinterpret_cast<const float*>(ws + L.wpad), fp,
                                          plan.pw, kNcap, grid, flag16, fst));
+        // (point sharding: the grids of all ranks' sources)
+        if (exchange(SKS_XCHG_SUM_F32, grid, static_cast<size_t>(nbat) * kNcap, fst) != SKS_OK) return SKS_ERR_CUDA;
       } else {
         ProfScope ps(PS_SPREAD, fst);
         SKS_CUDA(sks::launch_spread(zv, w, nbat, fp, kNcap, plan.pw, pr.k.kind == SKS_LAPLACIAN, det, grid, flag16, fst));

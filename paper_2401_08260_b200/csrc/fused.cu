@@ -865,12 +865,16 @@ bool fused_spread_ok(int d, const float* x) {
   return d <= 64 * FS_KBMAX && d % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
 }
 
-cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_t M, int d, double* mu, unsigned* nb,
-                               uint16_t* xh, uint16_t* xl, float* rsx, uint16_t* yh, uint16_t* yl, float* rsy,
-                               const float* w, float* wpad, cudaStream_t st) {
+cudaError_t launch_source_mean(const float* x, int64_t N, int d, double* mu, unsigned* nb, cudaStream_t st) {
   double* part = mu + d;   // [MEAN_PARTS][d] scratch after mu (source_bound_bytes)
   k_sample_mean_part<<<MEAN_PARTS, 128, 0, st>>>(x, N, d, part);
   k_sample_mean_fin<<<1, 128, 0, st>>>(N, d, part, mu, nb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_t M, int d, const double* mu,
+                               unsigned* nb, uint16_t* xh, uint16_t* xl, float* rsx, uint16_t* yh, uint16_t* yl,
+                               float* rsy, const float* w, float* wpad, cudaStream_t st) {
   const int dp16 = fused_dp16(d);
   auto prep = [&](const float* z, int64_t n, unsigned* out, uint16_t* h, uint16_t* l, float* rs, const float* w,
                   float* wp) {

@@ -204,9 +204,12 @@ size_t source_bound_bytes(int d);   // scratch of launch_source_prep: mu, partia
 // and the source weights w zero padded to whole 128-point tiles (wpad, read by the spread's bulk copies).
 // launch_bound_ranges (per slice batch): every slice's range bound c_p +- rho' of both sets into mm[p]
 int fused_dp16(int d);   // row length of the fp16 operand arrays: d rounded up to 8
-cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_t M, int d, double* mu, unsigned* nb,
-                               uint16_t* xh, uint16_t* xl, float* rsx, uint16_t* yh, uint16_t* yl, float* rsy,
-                               const float* w, float* wpad, cudaStream_t st);
+// launch_source_mean: mu (and nb zeroed), before launch_source_prep (between them a point-sharded call makes every
+// rank adopt rank 0's mu; after it the ranks take the maxima of nb: sks.h sks_exchange_fn)
+cudaError_t launch_source_mean(const float* x, int64_t N, int d, double* mu, unsigned* nb, cudaStream_t st);
+cudaError_t launch_source_prep(const float* x, int64_t N, const float* y, int64_t M, int d, const double* mu,
+                               unsigned* nb, uint16_t* xh, uint16_t* xl, float* rsx, uint16_t* yh, uint16_t* yl,
+                               float* rsy, const float* w, float* wpad, cudaStream_t st);
 cudaError_t launch_bound_ranges(const float* g32, int dp32, int d, const float* inv_norm, int np, const double* mu,
                                 const unsigned* nb, unsigned* mm, unsigned* flag16, cudaStream_t st);
 // g16: the slices' fp16 directions 2^8 g, row stride dpg (a multiple of 64)

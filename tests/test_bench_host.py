@@ -94,3 +94,18 @@ def test_ncu_context_reads_the_committed_summaries():
     assert ctx is not None and "k_proj_spread" in ctx["kernel"]
     assert 0.0 < ctx["smem_pipe_pct"] <= 100.0 and 0.0 <= ctx["issue_active_pct"] <= 100.0
     assert bench.ncu_context("cfg5", "no_such_slot") is None
+
+
+def test_shard_choice_and_config():
+    # N > 1: cfg5 (Gaussian, d = 100, 1.25e6 sources per rank at 8 GPUs) shards by points, the sort-path and
+    # small-N configs by slices; one GPU never shards; --shard points refuses configs without the fused path
+    assert bench.shard_by_points("auto", I.CONFIGS["cfg5"], 8) and bench.shard_by_points("auto", I.CONFIGS["cfg5"], 2)
+    assert not bench.shard_by_points("auto", I.CONFIGS["cfg5"], 1)
+    assert not bench.shard_by_points("slices", I.CONFIGS["cfg5"], 8)
+    for name in ("cfg1", "cfg2", "cfg3", "cfg4"):
+        assert not bench.shard_by_points("auto", I.CONFIGS[name], 8), name
+    with pytest.raises(SystemExit):
+        bench.shard_by_points("points", I.CONFIGS["cfg2"], 8)
+    c = bench.config_dict(I.CONFIGS["cfg5"], 30.0, 8, True)
+    assert c["parallelism"] == "points8" and c["slices_per_gpu"] == 512 and c["N"] == 10_000_000
+    assert bench.config_dict(I.CONFIGS["cfg5"], 30.0, 8)["parallelism"] == "slices8"
