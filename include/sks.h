@@ -91,7 +91,10 @@ typedef int (*sks_exchange_fn)(void* user, int32_t op, void* dev_ptr, size_t cou
 typedef struct {
   double eps;            /* [1e-6] absolute tail mass (f(0)-relative) of dropped Fourier coefficients and aliasing level
                             of the torus scaling (readings R3/R5 of P:339-349)             */
-  int32_t window_w;      /* [6]  NFFT window width in grid cells (taps per point), 2..12              */
+  int32_t window_w;      /* [6]  NFFT window width in grid cells (taps per point), 2..12 (the fused large-N path:
+                            4..8, 10, 12; others take the stored-projection path).  6 is the narrowest width whose
+                            worst-case aliasing bound meets the Fourier paths' 1e-4 tolerance with margin; measured
+                            errors and times per width: DESIGN.md Sec. 7                                          */
   int32_t oversample;    /* [2]  NFFT oversampling factor n >= oversample * 2 * (k_max + 1)           */
   int32_t slice_batch;   /* [0 = auto] slices processed per batch (memory bound, Remark P:973-979)   */
   int32_t engine;        /* [0 = auto] Fourier engine for the Gaussian / Matern: 1 = NFFT (Remark P:519-525),

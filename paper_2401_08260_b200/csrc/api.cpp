@@ -705,7 +705,7 @@ sks_status enqueue_call(const Problem& pr, const Opts& o, const float* x, const 
                                         reinterpret_cast<float*>(ws + L.Q), pr.k.kind == SKS_LAPLACIAN ? 4096 : 2048,
                                         fused, flag16, fst));
       }
-      launches += (nbat <= 148 ? 2 : 3) + (fused ? 1 : 0);   // (fused spread: two variants, one per footprint class)
+      launches += (nbat <= 148 ? 2 : 3) + (fused ? 2 : 0);   // (fused spread: three variants, one per footprint class)
       if (side) {   // join: the interpolation (on st, after the sort stage) waits for the Fourier part
         SKS_CUDA(cudaEventRecord(side->join, fst));
         SKS_CUDA(cudaStreamWaitEvent(st, side->join, 0));

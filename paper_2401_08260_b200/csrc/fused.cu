@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(128) k_sample_mean_part(const float* __restric
   const int S = static_cast<int>(N < MEAN_ROWS ? N : MEAN_ROWS);
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     double s = 0.0;
-    for (int k = blockIdx.x; k < S; k += MEAN_PARTS)
+#pragma unroll 8
+    for (int k = blockIdx.x; k < S; k += MEAN_PARTS)   // (unrolled: the rows' loads in flight together, same order of adds)
       s += static_cast<double>(__ldg(x + (static_cast<int64_t>(k) * N / S) * d + j));
     part[static_cast<int64_t>(blockIdx.x) * d + j] = s;
   }
@@ -226,11 +227,12 @@ constexpr int FS_OFF_BAR = FS_OFF_W + 2 * FS_P * 4;
 constexpr int FS_SMEM = FS_OFF_BAR + 512 + 1024;          // + barriers, TMEM slot, window coefficients, alignment
 static_assert(FS_SMEM <= 227 * 1024, "k_proj_spread shared memory");
 
-// NC private copies of WCAP = 256 / NC cells per slice: 8 x 32 (a copy per point group and point parity), or 4 x 64
-// (a copy per point group) for wider footprints.  The footprints are known on the device only (the planner's
-// FPar.W), so both variants are launched and each slice tile is taken by exactly one of them: the 8-copy kernel
-// when every slice of the tile fits 32 cells, the 4-copy kernel otherwise (slices beyond 64 cells fall back to
-// global atomics there); the other kernel's CTAs of that tile exit at once
+// NC private copies of WCAP = 256 / NC cells per slice: 8 x 32 (a copy per point group and point parity), 4 x 64
+// (a copy per point group), or one shared column of 256 cells updated with shared-memory atomics (fp32 atomicAdd on
+// shared memory is a CAS loop on sm_100a, ~3x the cost of a private read-modify-write, against ~35x for the global
+// atomics a slice beyond 256 cells falls back to).  The footprints are known on the device only (the planner's
+// FPar.W), so all three variants are launched and each slice tile is taken by exactly one of them, by the widest
+// footprint among its slices (<= 32, <= 64, wider); the other variants' CTAs of that tile exit at once
 template <int WT, int NC>
 __global__ void __launch_bounds__(FS_THREADS, 1)
     k_proj_spread(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
@@ -242,8 +244,10 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   if (call_failed(flag16)) return;
   {
     const int ps = (blockIdx.x % ((np + FS_S - 1) / FS_S)) * FS_S + static_cast<int>(threadIdx.x);
-    const int beyond = __syncthreads_or(threadIdx.x < FS_S && ps < np && fp[ps].W > FS_WCAP);
-    if ((beyond != 0) != (NC != FS_NCOL)) return;   // (block-uniform) the other variant's tile
+    const int wps = (threadIdx.x < FS_S && ps < np) ? fp[ps].W : 0;
+    const int b32 = __syncthreads_or(wps > FS_WCAP), b64 = __syncthreads_or(wps > 2 * FS_WCAP);
+    const int cls = b64 ? 2 : (b32 ? 1 : 0);
+    if (cls != (NC == FS_NCOL ? 0 : (NC == 1 ? 2 : 1))) return;   // (block-uniform) another variant's tile
   }
   extern __shared__ unsigned char fsraw[];
   // aligned by pointer arithmetic on the __shared__ array: the compiler keeps the shared state space (LDS / STS,
@@ -251,7 +255,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
   unsigned char* sm = fsraw + ((1024u - (smem_u32(fsraw) & 1023u)) & 1023u);
   constexpr int WCAP = FS_NCOL * FS_WCAP / NC;   // private cells per slice and copy
   constexpr int WH = (WT + 1) / 2;               // mirror pairs (+ the middle tap of an odd window)
-  static_assert(NC == FS_NCOL || NC == FS_EPI / 4, "one copy per point group, or per point group and parity");
+  static_assert(NC == FS_NCOL || NC == FS_EPI / 4 || NC == 1, "copies: per point group and parity, per group, one");
   float* priv = reinterpret_cast<float*>(sm + FS_OFF_GRID);   // [NC][WCAP][FS_S]
   uint64_t* afull = reinterpret_cast<uint64_t*>(sm + FS_OFF_BAR);
   uint64_t* xfull = afull + 1;                 // [FS_STAGES] raw tile (hi) and lo piece landed
@@ -382,9 +386,9 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
     // NC = 8: two private copies of the slice's column per warp, for the even and the odd points of a pair: the
     // pair's read-modify-writes cannot alias, so both points' loads are issued before either's stores.  NC = 4: one
     // copy per warp, the two points' read-modify-writes in order
-    constexpr int CPW = NC / (FS_EPI / 4);                           // copies per warp
+    constexpr int CPW = NC / (FS_EPI / 4);                           // copies per warp (0: one copy for all warps)
     float* col = priv + (CPW * h * WCAP) * FS_S + 32 * q + lane;     // cell c at col[c * FS_S] (even points)
-    float* colo = col + (CPW - 1) * WCAP * FS_S;                     // (odd points)
+    float* colo = col + (CPW == 2 ? WCAP * FS_S : 0);                // (odd points)
     float* gp = grid + static_cast<int64_t>(live ? p : 0) * ncap;
     // window coefficients through shared memory into registers (read from the parameter bank, ptxas would
     // re-load them inside the loop)
@@ -473,6 +477,18 @@ __global__ void __launch_bounds__(FS_THREADS, 1)
               if constexpr (WT & 1) {
                 c0p[(WT / 2) * FS_S] = fmaf(w8[jj], tl[WT / 2].x, g0[WT / 2]);
                 c1p[(WT / 2) * FS_S] = fmaf(w8[jj + 1], tl[WT / 2].y, g1[WT / 2]);
+              }
+            } else if constexpr (CPW == 0) {   // one column shared by the CTA's warps: shared-memory atomics
+#pragma unroll
+              for (int m = 0; m < WT / 2; ++m) {
+                atomicAdd(c0p + m * FS_S, w8[jj] * tl[m].x);
+                atomicAdd(c0p + (WT - 1 - m) * FS_S, w8[jj] * th[m].x);
+                atomicAdd(c1p + m * FS_S, w8[jj + 1] * tl[m].y);
+                atomicAdd(c1p + (WT - 1 - m) * FS_S, w8[jj + 1] * th[m].y);
+              }
+              if constexpr (WT & 1) {
+                atomicAdd(c0p + (WT / 2) * FS_S, w8[jj] * tl[WT / 2].x);
+                atomicAdd(c1p + (WT / 2) * FS_S, w8[jj + 1] * tl[WT / 2].y);
               }
             } else {   // one copy: the even point's stores before the odd point's loads (their cells may coincide)
 #pragma unroll
@@ -918,16 +934,16 @@ cudaError_t launch_proj_spread(const uint16_t* xh, const uint16_t* xl, const flo
     kern<<<ntiles_s * ranges, FS_THREADS, FS_SMEM, st>>>(tmA, tmX, tmXlo, nk, klast, N, np, ranges, rsx, inv_norm,
                                                          wpad, fp, pw, ncap, grid, flag16);
   };
-  // both variants (see k_proj_spread): each slice tile runs in the one its footprints select
+  // all variants (see k_proj_spread): each slice tile runs in the one its footprints select
   constexpr int NA = FS_NCOL, NB = FS_EPI / 4;
   switch (pw.w) {
-    case 4: go(k_proj_spread<4, NA>); go(k_proj_spread<4, NB>); break;
-    case 5: go(k_proj_spread<5, NA>); go(k_proj_spread<5, NB>); break;
-    case 6: go(k_proj_spread<6, NA>); go(k_proj_spread<6, NB>); break;
-    case 7: go(k_proj_spread<7, NA>); go(k_proj_spread<7, NB>); break;
-    case 8: go(k_proj_spread<8, NA>); go(k_proj_spread<8, NB>); break;
-    case 10: go(k_proj_spread<10, NA>); go(k_proj_spread<10, NB>); break;
-    case 12: go(k_proj_spread<12, NA>); go(k_proj_spread<12, NB>); break;
+    case 4: go(k_proj_spread<4, NA>); go(k_proj_spread<4, NB>); go(k_proj_spread<4, 1>); break;
+    case 5: go(k_proj_spread<5, NA>); go(k_proj_spread<5, NB>); go(k_proj_spread<5, 1>); break;
+    case 6: go(k_proj_spread<6, NA>); go(k_proj_spread<6, NB>); go(k_proj_spread<6, 1>); break;
+    case 7: go(k_proj_spread<7, NA>); go(k_proj_spread<7, NB>); go(k_proj_spread<7, 1>); break;
+    case 8: go(k_proj_spread<8, NA>); go(k_proj_spread<8, NB>); go(k_proj_spread<8, 1>); break;
+    case 10: go(k_proj_spread<10, NA>); go(k_proj_spread<10, NB>); go(k_proj_spread<10, 1>); break;
+    case 12: go(k_proj_spread<12, NA>); go(k_proj_spread<12, NB>); go(k_proj_spread<12, 1>); break;
     default: return cudaErrorInvalidValue;   // (widths 9, 11: the unfused path)
   }
   return cudaGetLastError();

@@ -54,6 +54,12 @@ def main(big=True):
         x = rng.normal(size=(N, 100)).astype(np.float32)
         S.sks_sum(dev(x), dev(rng.normal(size=(2000, 100))), dev(rng.uniform(-1, 1, N)), "gaussian", 15.0, 20, 5)
         assert S.sks_last_plan()["fused"] == 1
+        # the fused spread's other footprint classes (<= 64 cells: 4 private copies; wider: one shared column with
+        # shared-memory atomics) and an odd window width
+        for kw in (dict(window_w=7), dict(oversample=4), dict(oversample=8), dict(window_w=5, oversample=8)):
+            S.sks_sum(dev(x), dev(rng.normal(size=(2000, 100))), dev(rng.uniform(-1, 1, N)), "gaussian", 15.0, 20, 5,
+                      **kw)
+            assert S.sks_last_plan()["fused"] == 1
     torch.cuda.synchronize()
     print("sanitize run OK", runs)
 
